@@ -1,0 +1,229 @@
+/*
+ * nysgpu.h -- C ABI of libnysgpu.so, the B200 (sm_100a) kernels behind the
+ * inexact-ADMM x-subproblem hot path of GeNIOS (arXiv 2310.08333).
+ *
+ * The reference (`/root/reference/pkg/src/nysopt`, Python/NumPy) has no FFI:
+ * its numeric call sites are NumPy `@` and LAPACK calls.  Each entry point
+ * below replaces one of those call sites (file:line cited per function) and is
+ * what a reference-side binding (ctypes / cffi) would bind.
+ *
+ * Conventions
+ *   - all matrix/vector pointers are DEVICE pointers to FP64 data;
+ *   - matrices are row-major (NumPy C order) with an explicit leading dim;
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on that stream unless stated otherwise;
+ *   - `ws` is caller-allocated device workspace of at least the size the
+ *     matching *_workspace() query returns, ZERO-FILLED once at allocation
+ *     (kernels keep an atomic ticket in it and reset it themselves);
+ *   - scalar outputs (`sc`, `out`) are device arrays of doubles;
+ *   - return value: NYS_OK or an error code (mapped to the reference's
+ *     exception classes by the host layer, errors.py:4-29).
+ *
+ * Reductions are deterministic (fixed-order, no floating-point atomics).
+ */
+#ifndef NYSGPU_H
+#define NYSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NYS_ABI_VERSION 1
+
+enum nys_status {
+  NYS_OK = 0,
+  NYS_ERR_ARG = 1,          /* DimensionMismatchError / DataError            */
+  NYS_ERR_CUDA = 2,         /* CUDA launch/runtime failure                   */
+  NYS_ERR_NOT_SPD = 3,      /* NotSPDError: nonpositive curvature (krylov.py:76-77) */
+  NYS_ERR_NONFINITE = 4,    /* NumericalError (krylov.py:74-75, 85-86)       */
+  NYS_ERR_NOT_PSD = 5,      /* DataError: indefinite sketch core (sketch.py:117-120) */
+  NYS_ERR_UNSUPPORTED = 6,  /* CapabilityError                               */
+  NYS_ERR_WORKSPACE = 7,    /* workspace too small                           */
+  NYS_ERR_NO_DEVICE = 8     /* no sm_100 device visible                      */
+};
+
+/* loss kinds (problems.py:53-111) */
+enum nys_loss { NYS_LOSS_SQUARE = 0, NYS_LOSS_LOGISTIC = 1, NYS_LOSS_HUBER = 2 };
+/* prox kinds (prox.py:38-48) */
+enum nys_prox { NYS_PROX_SOFT = 0, NYS_PROX_BOX = 1 };
+
+/* CG scalar block layout (device doubles), see krylov.py:58-93 */
+enum nys_cg_slot {
+  NYS_CG_RZ = 0,     /* r.z of the current direction             */
+  NYS_CG_PAP = 1,    /* p.Ap                                      */
+  NYS_CG_ALPHA = 2,  /* rz / pAp                                  */
+  NYS_CG_RES2 = 3,   /* ||r||^2                                   */
+  NYS_CG_RZNEW = 4,  /* r.z of the freshly preconditioned residual */
+  NYS_CG_B2 = 5,     /* ||b||^2                                   */
+  NYS_CG_FLAG = 6,   /* 0 ok, 1 non-finite pAp, 2 pAp <= 0        */
+  NYS_CG_NSLOTS = 8
+};
+
+/* ---------------------------------------------------------------- misc -- */
+int nys_abi_version(void);
+const char* nys_status_string(int status);
+/* NYS_OK when a compute-capability-10.x device is current */
+int nys_device_check(void);
+/* bytes of the generic reduction workspace used by the vector kernels */
+size_t nys_reduce_workspace(void);
+
+/* ------------------------------------------------ K1/K2 dense products -- */
+/* K1 (operators.py:114-115 `a @ v`, k right-hand sides, k <= 4):
+ *   Y[j*ldy + i] = sum_c A[i*lda + c] * X[j*ldx + c]      0 <= i < rows, j < k */
+size_t nys_gemv_workspace(int64_t rows, int64_t n, int k);
+int nys_gemv_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X,
+                 int64_t ldx, int k, double* Y, int64_t ldy, void* ws, size_t ws_bytes,
+                 void* stream);
+
+/* K2 (operators.py:117-118 `a.T @ u`, k <= 4):
+ *   Y[j*ldy + c] = sum_i A[i*lda + c] * T[j*ldt + i]      0 <= c < n, j < k
+ * Split over rows with a deterministic fixed-order reduction of the splits. */
+size_t nys_gemvT_workspace(int64_t rows, int64_t n, int k);
+int nys_gemvT_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T,
+                  int64_t ldt, int k, double* Y, int64_t ldy, void* ws, size_t ws_bytes,
+                  void* stream);
+
+/* ---------------------------------------------- K3 Hessian-vector product -- */
+/* K3 (problems.py:263-264 MLHessian._apply + admm.py:262-263 shift):
+ *   y = A^T (d o (A v)) + shift * v,   and *pAp = v . y  when pAp != NULL.
+ * d == NULL means d == 1 (square loss, problems.py:59).
+ * finish == 0: write only the local partial A^T(d o Av) (row shard), to be
+ * all-reduced across GPUs and completed by nys_shift_dot_f64. */
+size_t nys_hvp_workspace(int64_t rows, int64_t n);
+int nys_hvp_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
+                const double* v, double shift, double* y, double* pAp, int finish, void* ws,
+                size_t ws_bytes, void* stream);
+/* y += shift * v; *dot = v . y when dot != NULL (device scalar). */
+int nys_shift_dot_f64(int64_t n, const double* v, double shift, double* y, double* dot,
+                      void* ws, void* stream);
+/* *out = a . b (device scalar, deterministic) */
+int nys_dot_f64(int64_t n, const double* a, const double* b, double* out, void* ws,
+                void* stream);
+
+/* ----------------------------------------------------- K6 preconditioner -- */
+/* K6 (sketch.py:143-151, Eq. (11)):
+ *   z = U((lam[r-1] + nu) * (U^T v)/(lam + nu) - U^T v) + v
+ * U is n x r row-major (ldu), lam has r entries (device).  r == 0 -> z = v.
+ * If rz != NULL, *rz = rdot . z (device scalar). */
+size_t nys_precond_workspace(int64_t n, int r);
+int nys_precond_apply_f64(const double* U, int64_t n, int r, int64_t ldu, const double* lam,
+                          double nu, const double* v, double* z, const double* rdot,
+                          double* rz, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------- K7 CG vectors -- */
+/* krylov.py:58-62: r = b - Ax0; sc[B2] = ||b||^2; sc[RES2] = ||r||^2 */
+int nys_cg_start_f64(int64_t n, const double* b, const double* Ax0, double* r, double* sc,
+                     void* ws, void* stream);
+/* krylov.py:72-84: alpha = rz/pAp (sc[FLAG] set on non-finite / <= 0 pAp);
+ * x += alpha p; unless refresh: r -= alpha Ap and sc[RES2] = ||r||^2 */
+int nys_cg_step_xr_f64(int64_t n, double* x, double* r, const double* p, const double* Ap,
+                       int refresh, double* sc, void* ws, void* stream);
+/* krylov.py:89-93: first: p = z, rz = rz_new;  else beta = rz_new/rz,
+ * rz = rz_new, p = z + beta p.   (rz_new = sc[RZNEW]) */
+int nys_cg_dir_f64(int64_t n, const double* z, double* p, int first, double* sc,
+                   void* stream);
+
+/* ---------------------------------------------- K8/K9 ADMM elementwise -- */
+/* x-update right-hand side and initial CG residual, M = I, c = 0
+ * (admm.py:270-272, krylov.py:61):
+ *   hx = hxA + lambda2 x;  g = gA + lambda2 x (+ q);
+ *   rhs = hx + sigma x - g + rho (z - u);   r = rhs - (hx + shift x)
+ *   sc[B2] = ||rhs||^2, sc[RES2] = ||r||^2.   q may be NULL. */
+int nys_admm_rhs_f64(int64_t n, const double* hxA, const double* gA, const double* q,
+                     double lambda2, double sigma, double rho, double shift, const double* x,
+                     const double* z, const double* u, double* rhs, double* r, double* sc,
+                     void* ws, void* stream);
+/* over-relaxation, prox and dual update (admm.py:278-300, prox.py:38-48):
+ *   w = alpha x + (1-alpha) z;  z = prox(w + u);  u = u + w - z;
+ *   if accum: xbar += x, zbar += z   (admm.py:580-583) */
+int nys_admm_zu_f64(int64_t n, const double* x, double* z, double* u, double alpha,
+                    int prox_kind, double kappa, const double* lo, const double* hi,
+                    double* xbar, double* zbar, int accum, void* stream);
+/* residual norms and objective pieces (admm.py:215-224, problems.py:227-351):
+ * out[ 0..1] = sum/max of (x-z)^2/|x-z|      out[ 2..3] rd = gA+lambda2 x(+q)+rho u
+ * out[ 4..5] x                               out[ 6..7] z
+ * out[ 8..9] rho u                           out[10] sum|z|
+ * out[11] x.gA       out[12] q.x             out[13] max|atnu|
+ * out[14] sum (|atnu|-lambda1)_+^2           out[15] max(lo-z, z-hi)
+ * (sum slots are sums of squares; max slots are max-abs).  q/atnu/lo/hi may be NULL. */
+#define NYS_NORMS_NOUT 16
+int nys_admm_norms_f64(int64_t n, const double* x, const double* z, const double* u,
+                       const double* gA, const double* q, double lambda2, double rho,
+                       const double* atnu, double lambda1, const double* lo,
+                       const double* hi, double* out, void* ws, void* stream);
+
+/* row-space (sample) elementwise pass for ML problems (problems.py:219-351):
+ *   r1 = Ax - b:  tg = l'(r1), w = l''(r1), thx = w o Ax
+ *   r2 = Az - b (if Az):  tnu = l'(r2)
+ * out[0] = sum l(r1), out[1] = sum l(r2), out[2] = sum l*(tnu) (finite part),
+ * out[3] = count of infinite l*(tnu), out[4] = b . tnu.   (row-shard partials) */
+#define NYS_ROWS_NOUT 5
+int nys_ml_rowwise_f64(int64_t rows, int loss, const double* Ax, const double* Az,
+                       const double* b, double* tg, double* w, double* thx, double* tnu,
+                       double* out, void* ws, void* stream);
+/* dual value at the scaled point c*nu (problems.py:313-328):
+ * out[0] = sum l*(c nu) (finite part), out[1] = #inf, out[2] = b.(c nu) */
+int nys_ml_conj_scaled_f64(int64_t rows, int loss, const double* nu, double c,
+                           const double* b, double* out, void* ws, void* stream);
+
+/* ------------------------------------------------- K13/K14 loop support -- */
+/* cycle guard / windows (admm.py:643-675): ring[slot*ld + i];
+ * out[0] = ||x_cur||^2, out[1+j] = ||x_cur - x_others[j]||^2 (j < nothers <= 16).
+ * `others` is a HOST array copied into the launch. */
+int nys_window_norms_f64(int64_t n, const double* ring, int64_t ld, int cur,
+                         const int* others, int nothers, double* out, void* ws, void* stream);
+/* penalty change (admm.py:303-319): y_old = rho_old u; u *= rho_old/rho_new;
+ * out[0] = ||y_old||^2, out[1] = ||rho_new u - y_old||^2 */
+int nys_scale_dual_f64(int64_t n, double* u, double rho_old, double rho_new, double* out,
+                       void* ws, void* stream);
+/* QP infeasibility pieces (admm.py:361-415, prox.py:96-135), M = I:
+ *   dx = (xa - xb)/width, du = (ua - ub)/width  (dx written out for the P.dx GEMV)
+ * out[0] = ||du||^2, out[1] = box support S(du) (finite part), out[2] = #inf terms,
+ * out[3] = ||dx||^2, out[4] = dist(dx, recession cone)^2, out[5] = q . dx */
+int nys_qp_infeas_f64(int64_t n, const double* xa, const double* xb, const double* ua,
+                      const double* ub, double width, const double* lo, const double* hi,
+                      const double* q, double* dx, double* out, void* ws, void* stream);
+/* elementwise helpers used by the operator API */
+int nys_axpby_f64(int64_t n, double a, const double* x, double b, double* y, void* stream);
+int nys_soft_threshold_f64(int64_t n, const double* v, double kappa, double* out, void* stream);
+int nys_box_project_f64(int64_t n, const double* v, const double* lo, const double* hi,
+                        double* out, void* stream);
+int nys_row_scale_f64(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d,
+                      void* stream);
+
+/* ------------------------------------------------------ K5 Nystrom sketch -- */
+/* C = alpha op(A) op(B) + beta C (row-major; trans = 1 means op(X) = X^T),
+ * FP64 DMMA (mma.sync m8n8k4) tiles; split-K with a deterministic reduction
+ * when M*N is small.  Used for Y = A Omega and A^T (D A Omega) (sketch.py:100). */
+size_t nys_gemm_workspace(int64_t M, int64_t N, int64_t K);
+int nys_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                 double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+/* Orthonormalise the raw Gaussian test matrix (sketch.py:97-99) by CholeskyQR2:
+ * Q (n x s, row-major) spans the same range as Omega.  Synchronises `stream`. */
+size_t nys_orthonormalize_workspace(int64_t n, int s);
+int nys_orthonormalize_f64(int64_t n, int s, const double* Omega, double* Q, void* ws,
+                           size_t ws_bytes, void* stream);
+/* Everything of nystrom_sketch after Y = A Q (sketch.py:102-128): trace-shift,
+ * core = Q^T Y_s, Cholesky (eigh fallback), B = Y_s L^-T, thin SVD of B via a
+ * Jacobi eigensolver of B^T B, lam = max(sv^2 - shift, 0), truncation to r.
+ * Y is destroyed.  Writes U (n x r_out, row-major, ld = r) and lam (r_out) and
+ * the HOST int *r_out (may be < r on the eigh path, 0 for an empty sketch).
+ * Returns NYS_ERR_NOT_PSD for a clearly indefinite core.  Synchronises `stream`. */
+size_t nys_nystrom_workspace(int64_t n, int s, int r);
+int nys_nystrom_core_f64(int64_t n, int s, int r, const double* Q, double* Y, double* U,
+                         double* lam, int* r_out, void* ws, size_t ws_bytes, void* stream);
+/* small symmetric eigensolver (one-sided Jacobi, cooperative grid): on exit the
+ * columns of V (s x s row-major) are eigenvectors, w the eigenvalues sorted in
+ * DESCENDING order.  A is destroyed.  Synchronises `stream`. */
+size_t nys_syevj_workspace(int s);
+int nys_syevj_f64(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NYSGPU_H */

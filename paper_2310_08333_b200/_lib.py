@@ -1,0 +1,139 @@
+"""ctypes binding of libnysgpu.so (the C ABI declared in include/nysgpu.h).
+
+The product path has NO CPU fallback: ``lib()`` raises ``CapabilityError`` when
+the library is missing or no sm_100 device is visible, and every kernel
+status code is turned into the reference's exception classes
+(``/root/reference/pkg/src/nysopt/errors.py:4-29``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import CapabilityError, DataError, DimensionMismatchError, NotSPDError, NumericalError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnysgpu.so")
+
+NYS_OK = 0
+NYS_ERR_ARG = 1
+NYS_ERR_CUDA = 2
+NYS_ERR_NOT_SPD = 3
+NYS_ERR_NONFINITE = 4
+NYS_ERR_NOT_PSD = 5
+NYS_ERR_UNSUPPORTED = 6
+NYS_ERR_WORKSPACE = 7
+NYS_ERR_NO_DEVICE = 8
+
+LOSS = {"square": 0, "logistic": 1, "huber": 2}
+PROX_SOFT, PROX_BOX = 0, 1
+
+# CG scalar slots (nys_cg_slot)
+CG_RZ, CG_PAP, CG_ALPHA, CG_RES2, CG_RZNEW, CG_B2, CG_FLAG, CG_NSLOTS = 0, 1, 2, 3, 4, 5, 6, 8
+NORMS_NOUT = 16
+ROWS_NOUT = 5
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int
+F64 = C.c_double
+SZ = C.c_size_t
+
+# name: (restype, argtypes)
+SIGNATURES = {
+    "nys_abi_version": (I32, []),
+    "nys_status_string": (C.c_char_p, [I32]),
+    "nys_device_check": (I32, []),
+    "nys_reduce_workspace": (SZ, []),
+    "nys_gemv_workspace": (SZ, [I64, I64, I32]),
+    "nys_gemv_f64": (I32, [P, I64, I64, I64, P, I64, I32, P, I64, P, SZ, P]),
+    "nys_gemvT_workspace": (SZ, [I64, I64, I32]),
+    "nys_gemvT_f64": (I32, [P, I64, I64, I64, P, I64, I32, P, I64, P, SZ, P]),
+    "nys_hvp_workspace": (SZ, [I64, I64]),
+    "nys_hvp_f64": (I32, [P, I64, I64, I64, P, P, F64, P, P, I32, P, SZ, P]),
+    "nys_shift_dot_f64": (I32, [I64, P, F64, P, P, P, P]),
+    "nys_dot_f64": (I32, [I64, P, P, P, P, P]),
+    "nys_precond_workspace": (SZ, [I64, I32]),
+    "nys_precond_apply_f64": (I32, [P, I64, I32, I64, P, F64, P, P, P, P, P, SZ, P]),
+    "nys_cg_start_f64": (I32, [I64, P, P, P, P, P, P]),
+    "nys_cg_step_xr_f64": (I32, [I64, P, P, P, P, I32, P, P, P]),
+    "nys_cg_dir_f64": (I32, [I64, P, P, I32, P, P]),
+    "nys_admm_rhs_f64": (I32, [I64, P, P, P, F64, F64, F64, F64, P, P, P, P, P, P, P, P]),
+    "nys_admm_zu_f64": (I32, [I64, P, P, P, F64, I32, F64, P, P, P, P, I32, P]),
+    "nys_admm_norms_f64": (I32, [I64, P, P, P, P, P, F64, F64, P, F64, P, P, P, P, P]),
+    "nys_ml_rowwise_f64": (I32, [I64, I32, P, P, P, P, P, P, P, P, P, P]),
+    "nys_ml_conj_scaled_f64": (I32, [I64, I32, P, F64, P, P, P, P]),
+    "nys_window_norms_f64": (I32, [I64, P, I64, I32, C.POINTER(C.c_int), I32, P, P, P]),
+    "nys_scale_dual_f64": (I32, [I64, P, F64, F64, P, P, P]),
+    "nys_qp_infeas_f64": (I32, [I64, P, P, P, P, F64, P, P, P, P, P, P, P]),
+    "nys_axpby_f64": (I32, [I64, F64, P, F64, P, P]),
+    "nys_soft_threshold_f64": (I32, [I64, P, F64, P, P]),
+    "nys_box_project_f64": (I32, [I64, P, P, P, P, P]),
+    "nys_row_scale_f64": (I32, [I64, I64, P, I64, P, P]),
+    "nys_gemm_workspace": (SZ, [I64, I64, I64]),
+    "nys_gemm_f64": (I32, [I32, I32, I64, I64, I64, F64, P, I64, P, I64, F64, P, I64, P, SZ, P]),
+    "nys_orthonormalize_workspace": (SZ, [I64, I32]),
+    "nys_orthonormalize_f64": (I32, [I64, I32, P, P, P, SZ, P]),
+    "nys_nystrom_workspace": (SZ, [I64, I32, I32]),
+    "nys_nystrom_core_f64": (I32, [I64, I32, I32, P, P, P, P, C.POINTER(C.c_int), P, SZ, P]),
+    "nys_syevj_workspace": (SZ, [I32]),
+    "nys_syevj_f64": (I32, [I32, P, P, P, P, SZ, P]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """dlopen the library and bind every declared symbol (no device needed)."""
+    if not os.path.exists(path):
+        raise CapabilityError(
+            f"libnysgpu.so not found at {path}; build it with `python -m paper_2310_08333_b200.build` "
+            "(there is no CPU fallback)"
+        )
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def lib() -> C.CDLL:
+    """The loaded library, after checking that an sm_100 GPU is present."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                import torch
+
+                if not torch.cuda.is_available():
+                    raise CapabilityError("no CUDA device: the B200 path has no CPU fallback")
+                l = load_library()
+                if l.nys_abi_version() != 1:
+                    raise CapabilityError("libnysgpu ABI version mismatch")
+                torch.cuda.init()
+                if l.nys_device_check() != NYS_OK:
+                    raise CapabilityError("libnysgpu requires an sm_100 (B200) device")
+                _lib = l
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a C-ABI status to the reference exception hierarchy."""
+    if rc == NYS_OK:
+        return
+    msg = f"{what}: {lib().nys_status_string(rc).decode()}" if _lib is not None else what
+    if rc == NYS_ERR_ARG:
+        raise DimensionMismatchError(msg)
+    if rc == NYS_ERR_NOT_SPD:
+        raise NotSPDError(msg)
+    if rc == NYS_ERR_NONFINITE:
+        raise NumericalError(msg)
+    if rc == NYS_ERR_NOT_PSD:
+        raise DataError("operator is not positive semidefinite (negative pivot in sketch core)")
+    if rc in (NYS_ERR_UNSUPPORTED, NYS_ERR_NO_DEVICE):
+        raise CapabilityError(msg)
+    raise NumericalError(f"CUDA failure in {what} (status {rc})")

@@ -1,0 +1,769 @@
+"""Inexact ADMM engine on the B200 (``/root/reference/pkg/src/nysopt/admm.py``).
+
+Same public surface as the reference -- ``solve``, ``SolverOptions``,
+``SolveResult``, ``IterationRecord``, ``PenaltyEvent``, ``Status``, ... --
+and the same control flow line for line (CG tolerance schedule, gap / residual
+termination, over-relaxation, windows, cycle guard, penalty adaptation, QP
+infeasibility tests), so iteration counts follow the reference.  What changes
+is where the arithmetic runs: all vectors live in HBM and every numeric step
+is a sm_100a kernel behind the C ABI:
+
+  per ADMM iteration (dense ML problem, M = I, c = 0)
+    x-update   rhs + initial residual (fused K8) -> device PCG (K3 HVP, K6, K7)
+    z/u        one fused over-relaxation/prox/dual kernel (K8)
+    A-pass     one 2-RHS GEMV  A{x, z}                       (K1)
+    epilogue   l'(Ax-b), w, w o Ax, nu = l'(Az-b) + sums       (K12)
+    A^T-pass   one 3-RHS GEMV^T A^T{l', w o Ax, nu}            (K2)
+    norms      residual norms / objective / gap pieces (K9)  -> one D2H
+
+The reference spends 7 A-passes and 5 A^T-passes per iteration outside CG
+(SURVEY.md §3.1); caching Ax, A^T l' and A^T(w o Ax) across iterations
+brings that to one 2-RHS A-pass and one 3-RHS A^T-pass with identical
+arithmetic meaning (differences are at the roundoff floor).
+
+Row sharding (``torch.distributed`` initialised): each rank holds a row block
+of A and b; the A^T-pass output and the row sums are all-reduced in one packed
+buffer, HVP partials are all-reduced inside CG, the sketch Y is all-reduced.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from collections import deque
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .dist import Shard, current_shard
+from .errors import CapabilityError, DataError
+from .krylov import CgReport, CgWork, cg_tolerance, pcg_device
+from .operators import DenseOperator, IdentityOperator, to_device
+from .problems import GenericProblem, lower
+from .sketch import NystromPreconditioner, NystromSketch, default_sketch_rank, raw_test_matrix, sketch_device, sketch_width
+
+PENALTY_ADAPT_CUTOFF = 1000  # admm.py:29
+DELTA_WINDOW = 25  # admm.py:33
+
+
+class Status(str, Enum):
+    OPTIMAL = "optimal"
+    PRIMAL_INFEASIBLE = "primal_infeasible"
+    DUAL_INFEASIBLE = "dual_infeasible"
+    PRIMAL_AND_DUAL_INFEASIBLE = "primal_and_dual_infeasible"
+    ITERATION_LIMIT = "iteration_limit"
+    TIME_LIMIT = "time_limit"
+
+
+@dataclass
+class SolverOptions:
+    """Tunable parameters (admm.py:45-99); same names, defaults and validation."""
+
+    sigma: float = 1e-6
+    gamma: float = 1.2
+    sketch_rank: Optional[int] = None
+    resketch_every: int = 20
+    norm_kind: str = "l2"
+    eps_abs: float = 1e-4
+    eps_rel: float = 1e-4
+    eps_inf: float = 1e-8
+    alpha: float = 1.6
+    tau: float = 2.0
+    mu: float = 10.0
+    rho0: float = 1.0
+    penalty_update_every: int = 25
+    penalty_warmup: int = 100
+    max_iter: int = 10000
+    time_limit: Optional[float] = None
+    use_preconditioner: bool = True
+    exact_x_solve: bool = False
+    use_dual_gap: Optional[bool] = None
+    eps_dual_gap: float = 1e-4
+    rng_seed: int = 0
+    assume_full_rank: bool = False
+    check_rank: bool = False
+    custom_stop: Optional[Callable] = None
+    record_iterates: bool = False
+    track_averaged_objective: bool = False
+    prox_tol0: float = 1e-8
+
+    def __post_init__(self):
+        if self.sigma < 0:
+            raise DataError("sigma must be nonnegative")
+        if self.gamma <= 1:
+            raise DataError("gamma must exceed 1")
+        if not 0 < self.alpha < 2:
+            raise DataError("over-relaxation alpha must lie in (0, 2)")
+        if self.tau <= 1 or self.mu <= 1:
+            raise DataError("penalty factors tau and mu must exceed 1")
+        if self.rho0 <= 0:
+            raise DataError("initial penalty must be positive")
+        if self.norm_kind not in ("l2", "linf"):
+            raise DataError("norm_kind must be 'l2' or 'linf'")
+
+
+@dataclass
+class SolverState:
+    """Host snapshot of the iterate state (admm.py:101-127); filled for
+    ``custom_stop`` callbacks and at the end of a solve."""
+
+    x: np.ndarray
+    z: np.ndarray
+    u: np.ndarray
+    rho: float
+    k: int = 0
+    x_prev: Optional[np.ndarray] = None
+    u_prev: Optional[np.ndarray] = None
+    Mx: Optional[np.ndarray] = None
+    x_bar_sum: Optional[np.ndarray] = None
+    z_bar_sum: Optional[np.ndarray] = None
+    bar_count: int = 0
+
+    @property
+    def x_bar(self):
+        return None if self.bar_count == 0 else self.x_bar_sum / self.bar_count
+
+    @property
+    def z_bar(self):
+        return None if self.bar_count == 0 else self.z_bar_sum / self.bar_count
+
+
+@dataclass
+class Residuals:
+    rp_norm: float
+    rd_norm: float
+    primal_scale: float
+    dual_scale: float
+    size: int = 0
+
+
+@dataclass
+class IterationRecord:
+    k: int
+    rp_norm: float
+    rd_norm: float
+    objective: float
+    rho: float
+    cg_iters: int
+    cg_tol: float
+    linsys_s: float
+    prox_s: float
+    gap: Optional[float] = None
+    avg_objective: Optional[float] = None
+
+
+@dataclass
+class PenaltyEvent:
+    k: int
+    rho_old: float
+    rho_new: float
+    dual_jump_rel: float
+
+
+@dataclass
+class Timings:
+    setup_s: float = 0.0
+    precond_s: float = 0.0
+    linsys_total_s: float = 0.0
+    prox_total_s: float = 0.0
+    total_s: float = 0.0
+
+
+@dataclass
+class SolveResult:
+    status: Status
+    x: np.ndarray
+    z: np.ndarray
+    u: np.ndarray
+    objective: float
+    iterations: int
+    rp_norm: float
+    rd_norm: float
+    history: list
+    timings: Timings
+    x_bar: Optional[np.ndarray] = None
+    z_bar: Optional[np.ndarray] = None
+    certificate_primal: Optional[np.ndarray] = None
+    certificate_dual: Optional[np.ndarray] = None
+    penalty_events: list = field(default_factory=list)
+    iterates: Optional[list] = None
+    gap: Optional[float] = None
+    device_stats: dict = field(default_factory=dict)
+
+    @property
+    def certificate(self):
+        if self.status in (Status.PRIMAL_INFEASIBLE, Status.PRIMAL_AND_DUAL_INFEASIBLE):
+            return self.certificate_primal
+        if self.status == Status.DUAL_INFEASIBLE:
+            return self.certificate_dual
+        return None
+
+
+# stats buffer layout (doubles)
+_S_NORMS = 0  # 16 (nys_admm_norms_f64)
+_S_WIN = 16  # 17 (window norms)
+_S_INF = 33  # 6 (QP infeasibility pieces)
+_S_PDX = 39  # 1 (||P dx||^2)
+_S_CONJ = 40  # 3 (scaled conjugate sums)
+_S_DUAL = 44  # 2 (penalty change)
+_S_LEN = 48
+
+
+class _Engine:
+    """Device-resident state and per-iteration kernel schedule of one solve."""
+
+    def __init__(self, gp: GenericProblem, opts: SolverOptions, kx, shard: Optional[Shard]):
+        self.kx = kx
+        self.opts = opts
+        self.gp = gp
+        n = self.n = gp.n
+        self.is_ml = gp.ml is not None
+        self.t_events = None  # optional per-kernel CUDA-event timing (bench)
+        if self.is_ml:
+            p = gp.ml
+            if not isinstance(p.A, DenseOperator):
+                raise CapabilityError("the B200 path supports dense data matrices (DenseOperator) only")
+            if p.loss.kind not in _lib.LOSS:
+                raise CapabilityError(f"loss {p.loss.kind!r} is not implemented on the B200 path")
+            self.shard = shard or current_shard(p.N)
+            self.A = p.A.device_rows(self.shard)
+            rows = self.rows = self.A.shape[0]
+            self.b = to_device(p.b[self.shard.row_start:self.shard.row_stop])
+            self.loss = p.loss.kind
+            self.l1, self.l2 = float(p.lambda1), float(p.lambda2)
+            self.const_hess = p.loss.deriv2_constant
+            self.diag_shift = self.l2
+            # row-space buffers
+            self.AXZ = kx.empty(2, rows)
+            self.T = kx.empty(3, rows)  # l'(Ax-b), w o Ax, nu
+            self.w = kx.empty(rows)
+            # packed all-reduce buffer: A^T outputs (3 n) + row sums (8)
+            self.red = kx.zeros(3 * n + 8)
+            self.AT = self.red[:3 * n].view(3, n)  # gA, hxA, atnu
+            self.rowsums = self.red[3 * n:3 * n + 8]
+        else:
+            qp = gp.qp
+            if not isinstance(qp.P, DenseOperator):
+                raise CapabilityError("the B200 path supports a dense QP matrix P only")
+            if not isinstance(qp.M, IdentityOperator):
+                raise CapabilityError("the B200 path supports QPs with M = I only")
+            self.shard = Shard(0, 1, 0, n, n)  # P is replicated
+            self.P = qp.P.device_rows()
+            self.q = to_device(qp.q)
+            self.lo = to_device(qp.box.l)
+            self.hi = to_device(qp.box.u)
+            self.const_hess = True
+            self.diag_shift = 0.0
+            self.Px = kx.empty(1, n)
+            self.dx = kx.empty(1, n)
+            self.Pdx = kx.empty(1, n)
+        self.XZ = kx.zeros(2, n)  # x, z rows (one 2-RHS GEMV operand)
+        self.x, self.z = self.XZ[0], self.XZ[1]
+        self.u = kx.zeros(n)
+        self.xbar = kx.zeros(n)
+        self.zbar = kx.zeros(n)
+        self.rhs = kx.empty(n)
+        self.cg = CgWork(kx, n)
+        self.stats = kx.zeros(_S_LEN)
+        self.stats_h = torch.zeros(_S_LEN + 8, dtype=torch.float64).pin_memory()
+        self.ring = kx.empty(DELTA_WINDOW + 2, n)
+        self.uring = kx.empty(DELTA_WINDOW + 2, n) if not self.is_ml else None
+        self.U = None
+        self.lam = None
+        self.pc_nu = 1.0
+
+    # ----------------------------------------------------------- passes --
+    def evaluate(self, with_z: bool) -> None:
+        """Data passes at the current (x, z): ML -> A{x,z}, loss epilogue,
+        A^T{l', w o Ax, nu} (+ all-reduce); QP -> P x."""
+        kx = self.kx
+        if self.is_ml:
+            k = 2 if with_z else 1
+            kx.gemv(self.A, self.XZ[:k], self.AXZ[:k])
+            kx.ml_rowwise(self.loss, self.AXZ[0], self.AXZ[1] if with_z else None, self.b,
+                          self.T[0], self.w, self.T[1], self.T[2] if with_z else None, self.rowsums)
+            kT = 3 if with_z else 2
+            kx.gemvT(self.A, self.T[:kT], self.AT[:kT])
+            if self.shard.sharded:
+                self.shard.allreduce(self.red)
+        else:
+            kx.gemv(self.P, self.XZ[:1], self.Px)
+
+    def norms(self, with_nu: bool) -> None:
+        kx = self.kx
+        if self.is_ml:
+            kx.admm_norms(self.x, self.z, self.u, self.AT[0], None, self.l2, self.rho,
+                          self.AT[2] if with_nu else None, self.l1, None, None, self.stats[_S_NORMS:_S_NORMS + 16])
+        else:
+            kx.admm_norms(self.x, self.z, self.u, self.Px[0], self.q, 0.0, self.rho, None, 0.0,
+                          self.lo, self.hi, self.stats[_S_NORMS:_S_NORMS + 16])
+
+    def read_stats(self) -> np.ndarray:
+        h = self.stats_h
+        h[:_S_LEN].copy_(self.stats, non_blocking=True)
+        if self.is_ml:
+            h[_S_LEN:_S_LEN + 5].copy_(self.rowsums[:5], non_blocking=True)
+        self.kx.sync()
+        return h.numpy().copy()
+
+    # ----------------------------------------------------------- matvec --
+    def matvec(self, shift: float):
+        kx = self.kx
+        if self.is_ml:
+            d = None if self.loss == "square" else self.w
+            tot = self.diag_shift + shift
+            if not self.shard.sharded:
+                def mv(v, out, dot):
+                    kx.hvp(self.A, d, v, tot, out, dot, True)
+            else:
+                def mv(v, out, dot):
+                    kx.hvp(self.A, d, v, 0.0, out, None, False)
+                    self.shard.allreduce(out)
+                    kx.shift_dot(v, tot, out, dot)
+        else:
+            def mv(v, out, dot):
+                kx.gemv(self.P, v.view(1, -1), out.view(1, -1))
+                kx.shift_dot(v, shift, out, dot)
+        return mv
+
+    def precond(self):
+        if self.U is None:
+            return None
+        kx = self.kx
+        return lambda v, out, rdot, rz: kx.precond_apply(self.U, self.lam, self.pc_nu, v, out, rdot, rz)
+
+    # ----------------------------------------------------------- sketch --
+    def sketch(self, seed: int, omega: Optional[np.ndarray] = None) -> None:
+        kx = self.kx
+        n = self.n
+        if self.is_ml:
+            A, w = self.A, (None if self.loss == "square" else self.w)
+
+            def cols(Q):
+                rows = A.shape[0]
+                s = Q.shape[1]
+                Z = kx.empty(rows, s)
+                kx.gemm(0, 0, rows, s, n, 1.0, A, A.stride(0), Q, s, 0.0, Z, s)
+                if w is not None:
+                    kx.row_scale(Z, w)
+                Y = kx.empty(n, s)
+                kx.gemm(1, 0, n, s, rows, 1.0, A, A.stride(0), Z, s, 0.0, Y, s)
+                return Y
+
+            reduce = self.shard.allreduce if self.shard.sharded else None
+        else:
+            P = self.P
+
+            def cols(Q):
+                s = Q.shape[1]
+                Y = kx.empty(n, s)
+                kx.gemm(0, 0, n, s, n, 1.0, P, P.stride(0), Q, s, 0.0, Y, s)
+                return Y
+
+            reduce = None
+        U, lam = sketch_device(kx, cols, n, self.r_sk, seed, omega=omega, reduce=reduce)
+        if U.shape[1] == 0:
+            self.U, self.lam = None, None
+        else:
+            self.U, self.lam = U, lam
+        self.n_sketches += 1
+
+    # ------------------------------------------------------------- run ---
+    def run(self, x0, z0, u0, callback, t_start) -> SolveResult:
+        opts, kx, n = self.opts, self.kx, self.n
+
+        def warm(v, name, dst):
+            if v is None:
+                return
+            vt = to_device(v)
+            if vt.shape != (n,):
+                raise DataError(f"warm start {name} must have length {n}, got shape {tuple(vt.shape)}")
+            dst.copy_(vt)
+
+        warm(x0, "x0", self.x)
+        warm(z0, "z0", self.z)
+        warm(u0, "u0", self.u)
+        self.rho = float(opts.rho0)
+        self.n_sketches = 0
+
+        # offset policy (admm.py:462-474): both in-scope lowerings are full rank
+        sigma_eff = 0.0 if (self.gp.full_rank or opts.assume_full_rank) else opts.sigma
+        use_gap = opts.use_dual_gap
+        if use_gap is None:
+            use_gap = self.is_ml and self.gp.ml.loss.has_conj
+        if use_gap and not self.is_ml:
+            raise DataError("the duality-gap criterion requires an ML problem")
+        self.use_gap = use_gap
+
+        timings = Timings()
+        r_sk = opts.sketch_rank or default_sketch_rank(n)
+        self.r_sk = max(1, min(r_sk, n))
+        nu_identity = lambda rho: rho + sigma_eff + self.diag_shift  # admm.py:490-491
+
+        # hess.update(x0) and the data passes at x0
+        self.evaluate(with_z=False)
+        last_sketch = 0
+        have_pc = False
+        if opts.use_preconditioner:
+            t0 = time.perf_counter()
+            self.sketch(opts.rng_seed)
+            timings.precond_s += time.perf_counter() - t0
+            self.pc_nu = nu_identity(self.rho)
+            have_pc = True
+        self.norms(with_nu=False)
+        st = self.read_stats()
+        res = self._residuals(st)
+        last_obj = self._objective(st)
+        timings.setup_s = time.perf_counter() - t_start
+
+        history: list[IterationRecord] = []
+        events: list[PenaltyEvent] = []
+        iterates = [] if opts.record_iterates else None
+        win: deque = deque(maxlen=DELTA_WINDOW + 1)  # slots of (x, u) copies in the device rings
+        self._win_append(win)
+        status = Status.ITERATION_LIMIT
+        cert_p = cert_d = None
+        gap = None
+        rho_frozen = False
+        cycle_hits = 0
+        best_res = np.inf
+        trend: deque = deque(maxlen=DELTA_WINDOW + 1)
+        bar_count = 0
+        k_done = 0
+        omega_next = None
+
+        for k in range(1, opts.max_iter + 1):
+            if opts.time_limit is not None and time.perf_counter() - t_start > opts.time_limit:
+                status = Status.TIME_LIMIT
+                break
+            k_done = k
+            # resketch on the cadence for iterate-dependent Hessians (admm.py:545-551)
+            if have_pc and not self.const_hess and k - last_sketch >= opts.resketch_every:
+                t0 = time.perf_counter()
+                self.sketch(opts.rng_seed + k)
+                timings.precond_s += time.perf_counter() - t0
+                self.pc_nu = nu_identity(self.rho)
+                last_sketch = k
+            tol = 1e-12 if opts.exact_x_solve else cg_tolerance(k, res.rp_norm, res.rd_norm, opts.gamma)
+
+            # x-update (admm.py:243-275)
+            t0 = time.perf_counter()
+            shift = self.rho + sigma_eff
+            if self.is_ml:
+                kx.admm_rhs(self.AT[1], self.AT[0], None, self.l2, sigma_eff, self.rho, shift,
+                            self.x, self.z, self.u, self.rhs, self.cg.r, self.cg.sc)
+            else:
+                kx.admm_rhs(self.Px[0], self.Px[0], self.q, 0.0, sigma_eff, self.rho, shift,
+                            self.x, self.z, self.u, self.rhs, self.cg.r, self.cg.sc)
+            rep = pcg_device(self.cg, self.matvec(shift), self.rhs, self.x, self.precond(), tol, 10 * n,
+                             started=True)
+            linsys_s = time.perf_counter() - t0
+            timings.linsys_total_s += linsys_s
+
+            # z/u update (admm.py:562-576) + averaged sums (admm.py:580-583)
+            t0 = time.perf_counter()
+            if self.is_ml:
+                kx.admm_zu(self.x, self.z, self.u, opts.alpha, _lib.PROX_SOFT, self.l1 / self.rho, None, None,
+                           self.xbar, self.zbar, k >= 2)
+            else:
+                kx.admm_zu(self.x, self.z, self.u, opts.alpha, _lib.PROX_BOX, 0.0, self.lo, self.hi,
+                           self.xbar, self.zbar, k >= 2)
+            prox_s = time.perf_counter() - t0
+            timings.prox_total_s += prox_s
+            if k >= 2:
+                bar_count += 1
+
+            # data passes, norms, and (speculatively) the window reductions
+            self.evaluate(with_z=use_gap)
+            self.norms(with_nu=use_gap)
+            spec = self._win_speculate(win)
+            st = self.read_stats()
+            res = self._residuals(st)
+            objective = self._objective(st)
+            last_obj = objective
+            gap = self._gap(st) if use_gap else None
+
+            avg_obj = None
+            if opts.track_averaged_objective and bar_count > 0:
+                avg_obj = self._averaged_objective(bar_count)
+
+            history.append(IterationRecord(k, res.rp_norm, res.rd_norm, objective, self.rho, rep.iterations,
+                                           tol, linsys_s, prox_s, gap, avg_obj))
+            if iterates is not None:
+                iterates.append((self.x.cpu().numpy(), self.z.cpu().numpy(), self.u.cpu().numpy()))
+            if callback is not None:
+                callback(k, res.rp_norm, res.rd_norm, objective, self.rho, rep.iterations)
+
+            if opts.custom_stop is not None:
+                if opts.custom_stop(self.gp, self._snapshot(k, bar_count)):
+                    status = Status.OPTIMAL
+                    break
+            elif self._terminated(res, gap):
+                status = Status.OPTIMAL
+                break
+
+            # windows (admm.py:621-634): commit the speculative append
+            self._win_commit(win, spec)
+            if not self.is_ml and len(win) == DELTA_WINDOW + 1:
+                st_inf, near, cp, cd = self._infeasibility(st, win)
+                if near:
+                    rho_frozen = True
+                if st_inf is not None:
+                    status, cert_p, cert_d = st_inf, cp, cd
+                    break
+
+            # cycle guard (admm.py:643-675)
+            best_res = min(best_res, max(res.rp_norm, res.rd_norm))
+            trend.append(best_res)
+            if len(win) >= 4 and not rho_frozen and k <= PENALTY_ADAPT_CUTOFF:
+                step = math.sqrt(max(st[_S_WIN + 1], 0.0))
+                xk_norm = math.sqrt(max(st[_S_WIN], 0.0))
+                locked = False
+                if step > 1e-8 * max(1.0, xk_norm):
+                    nper = min(len(win) - 1, 10) - 1
+                    rg = min(math.sqrt(max(st[_S_WIN + 2 + j], 0.0)) for j in range(nper))
+                    locked = rg <= 1e-3 * step
+                cycle_hits = cycle_hits + 1 if locked else 0
+                stagnant = len(trend) == trend.maxlen and trend[-1] >= 0.99 * trend[0]
+                if cycle_hits >= 5 and stagnant:
+                    cycle_hits = 0
+                    trend.clear()
+                    events.append(self._change_penalty(k, self.rho * opts.tau, have_pc, nu_identity))
+                    win.clear()
+                    self._win_append(win)
+
+            # balanced-residual penalty rule (admm.py:677-698)
+            if (not rho_frozen and opts.penalty_update_every > 0 and k >= opts.penalty_warmup
+                    and k % opts.penalty_update_every == 0 and k <= PENALTY_ADAPT_CUTOFF):
+                t_p = math.sqrt(n) * opts.eps_abs + opts.eps_rel * res.primal_scale
+                t_d = math.sqrt(n) * opts.eps_abs + opts.eps_rel * res.dual_scale
+                if t_p > 0 and t_d > 0:
+                    pm, dm = res.rp_norm / t_p, res.rd_norm / t_d
+                else:
+                    pm, dm = res.rp_norm, res.rd_norm
+                new = None
+                if pm > opts.mu * dm:
+                    new = self.rho * opts.tau
+                elif dm > opts.mu * pm:
+                    new = self.rho / opts.tau
+                if new is not None:
+                    events.append(self._change_penalty(k, new, have_pc, nu_identity))
+                    win.clear()
+                    self._win_append(win)
+
+        timings.total_s = time.perf_counter() - t_start
+        x = self.x.cpu().numpy()
+        z = self.z.cpu().numpy()
+        u = self.u.cpu().numpy()
+        x_bar = z_bar = None
+        if bar_count > 0:
+            x_bar = self.xbar.cpu().numpy() / bar_count
+            z_bar = self.zbar.cpu().numpy() / bar_count
+        return SolveResult(
+            status=status, x=x, z=z, u=u, objective=last_obj, iterations=k_done,
+            rp_norm=res.rp_norm, rd_norm=res.rd_norm, history=history, timings=timings,
+            x_bar=x_bar, z_bar=z_bar, certificate_primal=cert_p, certificate_dual=cert_d,
+            penalty_events=events, iterates=iterates, gap=gap,
+            device_stats={"kernel_launches": kx.launches, "sketches": self.n_sketches,
+                          "world": self.shard.world},
+        )
+
+    # ------------------------------------------------------ host maths ----
+    def _residuals(self, st) -> Residuals:
+        """admm.py:215-224 from the fused norms (M = I, c = 0)."""
+        s = st[_S_NORMS:]
+        if self.opts.norm_kind == "linf":
+            rp, rd, nx, nz, nru = s[1], s[3], s[5], s[7], s[9]
+        else:
+            rp, rd, nx, nz, nru = (math.sqrt(max(s[i], 0.0)) for i in (0, 2, 4, 6, 8))
+        return Residuals(rp, rd, max(nx, nz, 0.0), nru, self.n)
+
+    def _objective(self, st) -> float:
+        s = st[_S_NORMS:]
+        if self.is_ml:
+            f = float(st[_S_LEN + 0]) + 0.5 * self.l2 * s[4]  # problems.py:227-230
+            return f + self.l1 * s[10]  # g(z) = lambda1 ||z||_1
+        f = 0.5 * s[11] + s[12]  # problems.py:396-397
+        scale = 1.0 + s[7]
+        g = 0.0 if s[15] <= 1e-9 * scale else np.inf  # prox.py:138-144
+        return f + g
+
+    def _gap(self, st) -> float:
+        """ml_dual_gap at z (problems.py:306-351) from the fused sums."""
+        s = st[_S_NORMS:]
+        rs = st[_S_LEN:]
+        primal = float(rs[1]) + 0.5 * self.l2 * s[6] + self.l1 * s[10]
+        conj_sum, n_inf, b_nu = float(rs[2]), float(rs[3]), float(rs[4])
+        if self.l2 == 0.0:
+            denom = s[13]  # ||A' nu||_inf
+            if denom > self.l1:
+                c = self.l1 / denom
+                if self.loss in ("square", "huber"):
+                    # degree-2 homogeneous conjugates inside their domain
+                    conj_sum, b_nu = conj_sum * c * c, b_nu * c
+                else:
+                    out = self.stats[_S_CONJ:_S_CONJ + 3]
+                    self.kx.ml_conj_scaled(self.loss, self.T[2], c, self.b, out)
+                    if self.shard.sharded:
+                        self.shard.allreduce(out)
+                    o = out.cpu().numpy()
+                    conj_sum, n_inf, b_nu = float(o[0]), float(o[1]), float(o[2])
+        if n_inf > 0:
+            return np.inf
+        dual = -conj_sum - b_nu
+        if self.l2 > 0.0:
+            dual -= float(s[14]) / (2.0 * self.l2)
+        if not np.isfinite(dual):
+            return np.inf
+        num = primal - dual
+        denom = min(primal, abs(dual))
+        if denom <= 1e-16:
+            return 0.0 if abs(num) <= 1e-12 else np.inf
+        return num / denom
+
+    def _terminated(self, res: Residuals, gap) -> bool:
+        """admm.py:227-240."""
+        if gap is not None:
+            return gap <= self.opts.eps_dual_gap
+        o = self.opts
+        p_ok = res.rp_norm <= math.sqrt(self.n) * o.eps_abs + o.eps_rel * res.primal_scale
+        d_ok = res.rd_norm <= math.sqrt(self.n) * o.eps_abs + o.eps_rel * res.dual_scale
+        return bool(p_ok and d_ok)
+
+    def _change_penalty(self, k, rho_new, have_pc, nu_identity) -> PenaltyEvent:
+        """admm.py:303-319: rescale u so rho u is unchanged; shift the preconditioner."""
+        rho_old = self.rho
+        out = self.stats[_S_DUAL:_S_DUAL + 2]
+        self.kx.scale_dual(self.u, rho_old, rho_new, out)
+        o = out.cpu().numpy()
+        self.rho = rho_new
+        denom = max(math.sqrt(max(o[0], 0.0)), 1e-30)
+        jump = math.sqrt(max(o[1], 0.0)) / denom
+        if have_pc:
+            self.pc_nu = nu_identity(rho_new)
+        return PenaltyEvent(k, rho_old, rho_new, jump)
+
+    # ---------------------------------------------------------- windows --
+    def _free_slot(self, win) -> int:
+        used = set(win)
+        return next(i for i in range(self.ring.shape[0]) if i not in used)
+
+    def _win_append(self, win) -> None:
+        slot = self._free_slot(win)
+        self.ring[slot].copy_(self.x)
+        if self.uring is not None:
+            self.uring[slot].copy_(self.u)
+        win.append(slot)
+
+    def _win_speculate(self, win):
+        """Copy the new (x, u) into a free ring slot and launch the window
+        reductions for the deque state after the append, so that one readback
+        serves the stats, the cycle guard and the QP infeasibility test."""
+        slot = self._free_slot(win)
+        self.ring[slot].copy_(self.x)
+        if self.uring is not None:
+            self.uring[slot].copy_(self.u)
+        after = list(win) + [slot]
+        if len(after) > DELTA_WINDOW + 1:
+            after = after[1:]
+        if len(after) >= 4:
+            nper = min(len(after) - 1, 10) - 1
+            others = [after[-2]] + [after[-1 - p] for p in range(2, 2 + nper)]
+            self.kx.window_norms(self.ring, slot, others, self.stats[_S_WIN:_S_WIN + 17])
+        if not self.is_ml and len(after) == DELTA_WINDOW + 1:
+            first, last = after[0], after[-1]
+            self.kx.qp_infeas(self.ring[last], self.ring[first], self.uring[last], self.uring[first],
+                              float(DELTA_WINDOW), self.lo, self.hi, self.q, self.dx[0],
+                              self.stats[_S_INF:_S_INF + 6])
+            self.kx.gemv(self.P, self.dx, self.Pdx)
+            self.kx.dot(self.Pdx[0], self.Pdx[0], self.stats[_S_PDX:_S_PDX + 1])
+        return slot
+
+    def _win_commit(self, win, slot) -> None:
+        win.append(slot)
+
+    def _infeasibility(self, st, win):
+        """admm.py:361-415 with M = I from the speculative reductions."""
+        eps = self.opts.eps_inf
+        s = st[_S_INF:]
+        primal = dual = near_p = near_d = False
+        cp = cd = None
+        du = math.sqrt(max(s[0], 0.0))
+        if du > 1e-14:
+            t_map = du
+            t_sup = np.inf if s[2] > 0 else float(s[1])
+            primal = t_map < eps * du and t_sup < eps * du
+            near_p = t_map < 10 * eps * du and t_sup < 10 * eps * du
+            if primal:
+                last, first = win[-1], win[0]
+                cp =self.rho * ((self.uring[last] - self.uring[first]) / DELTA_WINDOW).cpu().numpy()
+        dxn = math.sqrt(max(s[3], 0.0))
+        if dxn > 1e-14:
+            s_obj = math.sqrt(max(st[_S_PDX], 0.0))
+            s_cone = math.sqrt(max(s[4], 0.0))
+            s_lin = float(s[5])
+            dual = s_obj < eps * dxn and s_cone < eps * dxn and s_lin < eps * dxn
+            near_d = s_obj < 10 * eps * dxn and s_cone < 10 * eps * dxn and s_lin < 10 * eps * dxn
+            if dual:
+                cd = self.dx[0].cpu().numpy().copy()
+        if primal and dual:
+            status = Status.PRIMAL_AND_DUAL_INFEASIBLE
+        elif primal:
+            status = Status.PRIMAL_INFEASIBLE
+        elif dual:
+            status = Status.DUAL_INFEASIBLE
+        else:
+            status = None
+        return status, near_p or near_d, cp, cd
+
+    # ------------------------------------------------------------ misc ----
+    def _snapshot(self, k, bar_count) -> SolverState:
+        x = self.x.cpu().numpy()
+        return SolverState(x=x, z=self.z.cpu().numpy(), u=self.u.cpu().numpy(), rho=self.rho, k=k, Mx=x,
+                           x_bar_sum=self.xbar.cpu().numpy(), z_bar_sum=self.zbar.cpu().numpy(),
+                           bar_count=bar_count)
+
+    def _averaged_objective(self, bar_count) -> float:
+        """f(x_bar) + g(z_bar) (admm.py:589-591): extra data pass, only when asked."""
+        kx = self.kx
+        xb = self.xbar / bar_count
+        zb = self.zbar / bar_count
+        if self.is_ml:
+            XB = xb.view(1, -1).contiguous()
+            ab = kx.empty(1, self.rows)
+            kx.gemv(self.A, XB, ab)
+            out = kx.zeros(8)
+            kx.ml_rowwise(self.loss, ab[0], None, self.b, None, None, None, None, out)
+            if self.shard.sharded:
+                self.shard.allreduce(out)
+            f = float(out[0]) + 0.5 * self.l2 * float(torch.dot(xb, xb))
+            return f + self.l1 * float(zb.abs().sum())
+        pxb = kx.empty(1, self.n)
+        kx.gemv(self.P, xb.view(1, -1).contiguous(), pxb)
+        f = 0.5 * float(torch.dot(xb, pxb[0])) + float(torch.dot(self.q, xb))
+        scale = 1.0 + float(zb.abs().max())
+        ok = bool(torch.all(zb >= self.lo - 1e-9 * scale)) and bool(torch.all(zb <= self.hi + 1e-9 * scale))
+        return f + (0.0 if ok else np.inf)
+
+
+def solve(problem, options: Optional[SolverOptions] = None, x0=None, z0=None, u0=None,
+          callback: Optional[Callable] = None, kernels=None, shard: Optional[Shard] = None) -> SolveResult:
+    """Run the splitting method on a QP or ML problem (admm.py:422-719).
+
+    Drop-in for ``nysopt.solve``; the extra keyword arguments are for the
+    harness (an explicit kernel backend / shard, used by the multi-rank tests)."""
+    t_start = time.perf_counter()
+    options = options or SolverOptions()
+    gp = lower(problem)
+    if gp.ml is None and gp.qp is None:
+        raise CapabilityError("generic problems (user f/prox callables) are outside the dense B200 path")
+    if kernels is None:
+        from .kernels import get_kernels
+
+        kernels = get_kernels()
+    eng = _Engine(gp, options, kernels, shard)
+    return eng.run(x0, z0, u0, callback, t_start)

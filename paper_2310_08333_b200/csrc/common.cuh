@@ -1,0 +1,124 @@
+// Shared helpers for the libnysgpu kernels (sm_100a, FP64 throughout).
+//
+// Reductions are deterministic: every kernel that reduces writes one partial
+// per CTA and the last CTA to finish (atomic ticket) sums the partials in a
+// fixed order, so results are bitwise reproducible run to run (the reference
+// pins bitwise trajectory determinism, tests/test_admm.py:476-484).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/nysgpu.h"
+
+#define NYS_CHECK_LAUNCH()                                   \
+  do {                                                       \
+    cudaError_t _e = cudaGetLastError();                     \
+    if (_e != cudaSuccess) return NYS_ERR_CUDA;              \
+  } while (0)
+
+namespace nys {
+
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;  // B200
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum of NV values per thread; result valid in thread 0.
+// `sh` must hold NV * (blockDim/32) doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) sh[j * nw + wid] = v[j];
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double t = lane < nw ? sh[j * nw + lane] : 0.0;
+      v[j] = warp_sum(t);
+    }
+  }
+  __syncthreads();
+}
+
+template <int NV>
+__device__ __forceinline__ void block_max(double (&v)[NV], double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_max(v[j]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) sh[j * nw + wid] = v[j];
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double t = lane < nw ? sh[j * nw + lane] : 0.0;
+      v[j] = warp_max(t);
+    }
+  }
+  __syncthreads();
+}
+
+// Last-block-done ticket.  Returns true in exactly one CTA (all threads of
+// it), after every CTA has published its partials.  The counter is reset by
+// the winner so the same workspace can be reused by the next launch.
+__device__ __forceinline__ bool last_block(unsigned int* counter) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    am_last = (t == gridDim.x * gridDim.y * gridDim.z - 1);
+  }
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+  return am_last;
+}
+
+// Fixed-order sum of `cnt` partials laid out with stride `stride`, by one CTA.
+// Each thread sums a strided subset in order, then a block tree; the result is
+// deterministic for fixed (cnt, blockDim).
+__device__ __forceinline__ double block_sum_partials(const double* p, int cnt, int stride,
+                                                     double* sh) {
+  double v[1] = {0.0};
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) v[0] += p[(size_t)i * stride];
+  block_sum<1>(v, sh);
+  return v[0];
+}
+
+__device__ __forceinline__ double block_max_partials(const double* p, int cnt, int stride,
+                                                     double* sh) {
+  double v[1] = {0.0};
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) v[0] = fmax(v[0], p[(size_t)i * stride]);
+  block_max<1>(v, sh);
+  return v[0];
+}
+
+template <class T>
+__host__ __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+template <class T>
+__host__ __device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace nys

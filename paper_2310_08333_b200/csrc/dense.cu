@@ -1,0 +1,798 @@
+// K5: Nystrom sketch construction on the GPU (sketch.py:74-128).
+//
+//   * nys_gemm_f64: FP64 GEMM on the DMMA tensor-core path (mma.sync m8n8k4
+//     f64 -> SASS DMMA.8x8x4).  tcgen05 has no FP64 kind, so DMMA is the
+//     FP64 tensor path on sm_100a.  128x64x16 CTA tiles, 8 warps of 32x32,
+//     3-stage cp.async pipeline, split-K with a fixed-order reduction when the
+//     output has too few tiles to fill 148 SMs (the s x s Gram products).
+//   * CholeskyQR2 orthonormalisation of the raw Gaussian Omega (replaces the
+//     Householder QR of sketch.py:99; the sketch depends only on range(Omega)).
+//   * single-CTA Cholesky (LAPACK potf2 failure rule), triangular inverse,
+//   * one-sided Jacobi symmetric eigensolver on a cooperative grid (replaces
+//     the thin SVD of sketch.py:126 via B^T B, and eigh of sketch.py:115).
+#include <cooperative_groups.h>
+#include <math.h>
+#include <vector>
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace nys {
+
+// ------------------------------------------------------------- GEMM -------
+constexpr int GBM = 128, GBN = 64, GBK = 16, GSTAGES = 3, GTHREADS = 256;
+// shared-memory row strides (doubles) chosen so DMMA fragment loads are
+// 2-wavefront (conflict-free for 256 B per warp request)
+constexpr int kStrideKmaj(int mn) { return mn + 8; }  // tile stored [k][m]
+constexpr int kStrideMmaj = GBK + 4;                   // tile stored [m][k]
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// TA: op(A) = A^T (A stored K x M). TB: op(B) = B^T (B stored N x K).
+template <bool TA, bool TB>
+struct GemmSmem {
+  static constexpr int A_ELEMS = TA ? GBK * kStrideKmaj(GBM) : GBM * kStrideMmaj;
+  static constexpr int B_ELEMS = TB ? GBN * kStrideMmaj : GBK * kStrideKmaj(GBN);
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr size_t BYTES = (size_t)STAGE * GSTAGES * sizeof(double);
+};
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GTHREADS)
+dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A,
+             int64_t lda, const double* __restrict__ B, int64_t ldb, double beta,
+             double* __restrict__ C, int64_t ldc, int64_t k_per_split, double* __restrict__ P) {
+  extern __shared__ __align__(16) double smem[];
+  using S = GemmSmem<TA, TB>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps, 32 x 32 each
+  const int64_t n0 = (int64_t)blockIdx.x * GBN, m0 = (int64_t)blockIdx.y * GBM;
+  const int64_t kb = (int64_t)blockIdx.z * k_per_split;
+  const int64_t ke = min(K, kb + k_per_split);
+  const int ktiles = (int)cdiv(tmax<int64_t>(ke - kb, 0), GBK);
+
+  auto load_tile = [&](int stage, int64_t k0) {
+    double* As = smem + stage * S::STAGE;
+    double* Bs = As + S::A_ELEMS;
+    // A tile: GBM x GBK elements of op(A)
+#pragma unroll
+    for (int e = tid; e < GBM * GBK; e += GTHREADS) {
+      if (TA) {  // consecutive threads along m (contiguous in memory)
+        const int kk = e / GBM, mm = e - kk * GBM;
+        const int64_t gm = m0 + mm, gk = k0 + kk;
+        const bool v = gm < M && gk < ke;
+        cp_async8(As + kk * kStrideKmaj(GBM) + mm, v ? A + gk * lda + gm : A, v);
+      } else {  // consecutive threads along k
+        const int mm = e / GBK, kk = e - mm * GBK;
+        const int64_t gm = m0 + mm, gk = k0 + kk;
+        const bool v = gm < M && gk < ke;
+        cp_async8(As + mm * kStrideMmaj + kk, v ? A + gm * lda + gk : A, v);
+      }
+    }
+#pragma unroll
+    for (int e = tid; e < GBN * GBK; e += GTHREADS) {
+      if (TB) {
+        const int nn = e / GBK, kk = e - nn * GBK;
+        const int64_t gn = n0 + nn, gk = k0 + kk;
+        const bool v = gn < N && gk < ke;
+        cp_async8(Bs + nn * kStrideMmaj + kk, v ? B + gn * ldb + gk : B, v);
+      } else {
+        const int kk = e / GBN, nn = e - kk * GBN;
+        const int64_t gn = n0 + nn, gk = k0 + kk;
+        const bool v = gn < N && gk < ke;
+        cp_async8(Bs + kk * kStrideKmaj(GBN) + nn, v ? B + gk * ldb + gn : B, v);
+      }
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < GSTAGES - 1; ++s) {
+    if (s < ktiles) load_tile(s, kb + (int64_t)s * GBK);
+    cp_async_commit();
+  }
+  const int fr = lane >> 2, fc = lane & 3;
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    {  // prefetch tile kt + STAGES - 1
+      const int nk = kt + GSTAGES - 1;
+      if (nk < ktiles) load_tile(nk % GSTAGES, kb + (int64_t)nk * GBK);
+      cp_async_commit();
+    }
+    const double* As = smem + (kt % GSTAGES) * S::STAGE;
+    const double* Bs = As + S::A_ELEMS;
+#pragma unroll
+    for (int k4 = 0; k4 < GBK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int mm = wm * 32 + i * 8 + fr, kk = k4 + fc;
+        af[i] = TA ? As[kk * kStrideKmaj(GBM) + mm] : As[mm * kStrideMmaj + kk];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int nn = wn * 32 + j * 8 + fr, kk = k4 + fc;
+        bf[j] = TB ? Bs[nn * kStrideMmaj + kk] : Bs[kk * kStrideKmaj(GBN) + nn];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: fragment (row = lane/4, cols = 2*(lane%4) + {0,1})
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gm = m0 + wm * 32 + i * 8 + fr;
+        const int64_t gn = n0 + wn * 32 + j * 8 + fc * 2 + h;
+        if (gm < M && gn < N) {
+          if (P) {
+            P[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j][h];
+          } else {
+            double v = alpha * acc[i][j][h];
+            if (beta != 0.0) v = fma(beta, C[gm * ldc + gn], v);
+            C[gm * ldc + gn] = v;
+          }
+        }
+      }
+}
+
+__global__ void splitk_reduce(const double* __restrict__ P, int64_t M, int64_t N, int splits,
+                              double alpha, double beta, double* __restrict__ C, int64_t ldc) {
+  const int64_t total = M * N;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int z = 0; z < splits; ++z) acc += P[(int64_t)z * total + t];
+    const int64_t m = t / N, nn = t - m * N;
+    double v = alpha * acc;
+    if (beta != 0.0) v = fma(beta, C[m * ldc + nn], v);
+    C[m * ldc + nn] = v;
+  }
+}
+
+static int gemm_splits(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = cdiv(M, GBM) * cdiv(N, GBN);
+  const int64_t target = kNumSMs * 2;
+  if (tiles >= target || K < 4 * GBK) return 1;
+  int64_t sp = cdiv(target, tiles);
+  sp = tmin<int64_t>(sp, cdiv(K, 4 * GBK));
+  // keep partials under 32 M doubles
+  sp = tmin<int64_t>(sp, tmax<int64_t>(1, (32ll << 20) / tmax<int64_t>(1, M * N)));
+  return (int)tmax<int64_t>(1, sp);
+}
+
+size_t gemm_ws(int64_t M, int64_t N, int64_t K) {
+  const int sp = gemm_splits(M, N, K);
+  return sp > 1 ? (size_t)sp * M * N * sizeof(double) : 0;
+}
+
+template <bool TA, bool TB>
+static int gemm_launch(int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                       int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                       int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  using S = GemmSmem<TA, TB>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::BYTES);
+    attr_set = true;
+  }
+  int sp = gemm_splits(M, N, K);
+  if (sp > 1 && ws_bytes < (size_t)sp * M * N * sizeof(double)) sp = 1;
+  const int64_t kps = sp > 1 ? cdiv(cdiv(K, sp), GBK) * GBK : K;
+  sp = (int)cdiv(K, kps);
+  dim3 grid((unsigned)cdiv(N, GBN), (unsigned)cdiv(M, GBM), (unsigned)sp);
+  double* P = sp > 1 ? reinterpret_cast<double*>(ws) : nullptr;
+  dgemm_kernel<TA, TB><<<grid, GTHREADS, S::BYTES, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C,
+                                                         ldc, kps, P);
+  NYS_CHECK_LAUNCH();
+  if (sp > 1) {
+    const int64_t blocks = tmin<int64_t>(cdiv(M * N, 256), kNumSMs * 8);
+    splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(P, M, N, sp, alpha, beta, C, ldc);
+    NYS_CHECK_LAUNCH();
+  }
+  return NYS_OK;
+}
+
+int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+         int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws,
+         size_t ws_bytes, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return NYS_ERR_ARG;
+  if (ta && tb) return gemm_launch<true, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes, st);
+  if (ta) return gemm_launch<true, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes, st);
+  if (tb) return gemm_launch<false, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes, st);
+  return gemm_launch<false, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes, st);
+}
+
+// ------------------------------------------------- small dense kernels ----
+// In-place lower Cholesky of the s x s matrix C (row-major), one CTA.
+// info = 0 on success, j+1 if the j-th pivot is not positive (LAPACK potf2).
+__global__ void __launch_bounds__(1024) cholesky_kernel(int s, double* C, int64_t ldc, int* info) {
+  __shared__ int fail;
+  __shared__ double piv;
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < s; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = C[(int64_t)j * ldc + j];
+      if (!(d > 0.0) || isnan(d)) {
+        fail = j + 1;
+      } else {
+        piv = sqrt(d);
+        C[(int64_t)j * ldc + j] = piv;
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    const double pj = piv;
+    for (int i = j + 1 + threadIdx.x; i < s; i += blockDim.x) C[(int64_t)i * ldc + j] /= pj;
+    __syncthreads();
+    // trailing update of the lower triangle: C[i][k] -= C[i][j] C[k][j], j < k <= i
+    const int m = s - j - 1;
+    const int64_t tot = (int64_t)m * (m + 1) / 2;
+    for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
+      // map t -> (a, b) with 0 <= b <= a < m
+      int a = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while ((int64_t)a * (a + 1) / 2 > t) --a;
+      while ((int64_t)(a + 1) * (a + 2) / 2 <= t) ++a;
+      const int b = (int)(t - (int64_t)a * (a + 1) / 2);
+      const int i = j + 1 + a, k = j + 1 + b;
+      C[(int64_t)i * ldc + k] -= C[(int64_t)i * ldc + j] * C[(int64_t)k * ldc + j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *info = fail;
+  __syncthreads();
+  if (!fail) {  // zero the strict upper triangle
+    for (int64_t t = threadIdx.x; t < (int64_t)s * s; t += blockDim.x) {
+      const int i = (int)(t / s), k = (int)(t % s);
+      if (k > i) C[(int64_t)i * ldc + k] = 0.0;
+    }
+  }
+}
+
+// Linv = L^{-1} (lower), one warp per column.
+__global__ void __launch_bounds__(256) trinv_lower_kernel(int s, const double* __restrict__ L,
+                                                          int64_t ldl, double* __restrict__ X,
+                                                          int64_t ldx) {
+  extern __shared__ double xs[];  // 8 warps x s
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.x * 8 + warp;
+  if (j >= s) return;
+  double* x = xs + (int64_t)warp * s;
+  for (int i = lane; i < s; i += 32) x[i] = 0.0;
+  __syncwarp();
+  if (lane == 0) x[j] = 1.0 / L[(int64_t)j * ldl + j];
+  __syncwarp();
+  for (int i = j + 1; i < s; ++i) {
+    double acc = 0.0;
+    for (int k = j + lane; k < i; k += 32) acc = fma(L[(int64_t)i * ldl + k], x[k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) x[i] = -acc / L[(int64_t)i * ldl + i];
+    __syncwarp();
+  }
+  for (int i = lane; i < s; i += 32) X[(int64_t)i * ldx + j] = x[i];
+}
+
+__global__ void symmetrize_kernel(int s, double* C, int64_t ldc) {
+  const int64_t tot = (int64_t)s * s;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / s), k = (int)(t % s);
+    if (k < i) {
+      const double v = 0.5 * (C[(int64_t)i * ldc + k] + C[(int64_t)k * ldc + i]);
+      C[(int64_t)i * ldc + k] = v;
+      C[(int64_t)k * ldc + i] = v;
+    }
+  }
+}
+
+// trace-shift of sketch.py:103-107: trace = (n/s) sum(Q o Y); shift = eps*max(trace,0)
+// (eps if 0); Y += shift Q.  Two passes in one kernel via a ticket.
+__global__ void sketch_shift_kernel(int64_t n, int s, const double* __restrict__ Q,
+                                    double* __restrict__ Y, double* part, unsigned int* counter,
+                                    double* shift_out, unsigned int* gate) {
+  __shared__ double sh[32];
+  const int64_t tot = n * s;
+  double acc[1] = {0.0};
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x)
+    acc[0] = fma(Q[t], Y[t], acc[0]);
+  block_sum<1>(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(counter)) {
+    const double sum = block_sum_partials(part, gridDim.x, 1, sh);
+    if (threadIdx.x == 0) {
+      const double trace = ((double)n / (double)s) * sum;
+      double sft = 2.220446049250313e-16 * fmax(trace, 0.0);
+      if (sft == 0.0) sft = 2.220446049250313e-16;
+      *shift_out = sft;
+    }
+  }
+}
+
+__global__ void add_scaled_kernel(int64_t tot, const double* __restrict__ Q, double* __restrict__ Y,
+                                  const double* shift) {
+  const double sft = *shift;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x)
+    Y[t] = __dadd_rn(Y[t], __dmul_rn(sft, Q[t]));
+}
+
+// ------------------------------------------------------- Jacobi eigen -----
+// One-sided Jacobi on the s x s symmetric matrix held as ROWS of Xt (row p =
+// column p of X), accumulating V^T in Vt.  Round-robin (circle) pairing: all
+// m/2 pairs of a round are disjoint and processed in parallel, one warp per
+// pair, with a grid-wide barrier between rounds (cooperative launch).
+__global__ void __launch_bounds__(256) jacobi_kernel(int s, double* __restrict__ Xt,
+                                                     double* __restrict__ Vt, int max_sweeps,
+                                                     double tol, unsigned int* rot_count,
+                                                     int* sweeps_out) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int m = s + (s & 1);  // padded to even; index s is a dummy when s is odd
+  const int npairs = m / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) rot_count[sweep & 1] = 0u;
+    // make sure the other parity slot was consumed before it is reset next sweep
+    grid.sync();
+    unsigned int local_rot = 0;
+    for (int round = 0; round < m - 1; ++round) {
+      for (int k = gw; k < npairs; k += nwarps) {
+        int a, b;
+        if (k == 0) {
+          a = round;
+          b = m - 1;
+        } else {
+          a = (round + k) % (m - 1);
+          b = (round - k + (m - 1)) % (m - 1);
+        }
+        if (a >= s || b >= s) continue;
+        const int p = min(a, b), q = max(a, b);
+        double* xp = Xt + (int64_t)p * s;
+        double* xq = Xt + (int64_t)q * s;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < s; i += 32) {
+          const double u = xp[i], v = xq[i];
+          al = fma(u, u, al);
+          be = fma(v, v, be);
+          ga = fma(u, v, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t);
+          const double sn = c * t;
+          double* vp = Vt + (int64_t)p * s;
+          double* vq = Vt + (int64_t)q * s;
+          for (int i = lane; i < s; i += 32) {
+            const double u = xp[i], v = xq[i];
+            xp[i] = c * u - sn * v;
+            xq[i] = sn * u + c * v;
+            const double vu = vp[i], vv = vq[i];
+            vp[i] = c * vu - sn * vv;
+            vq[i] = sn * vu + c * vv;
+          }
+          ++local_rot;
+        }
+      }
+      grid.sync();
+    }
+    if (lane == 0 && local_rot) atomicAdd(&rot_count[sweep & 1], local_rot);
+    grid.sync();
+    const unsigned int total = *((volatile unsigned int*)&rot_count[sweep & 1]);
+    grid.sync();
+    if (total == 0) {
+      ++sweep;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
+// eigenvalue of column p: w_p = sign(v_p . x_p) ||x_p||; then rank-sort
+// descending and scatter V columns: V[i][rank_p] = Vt[p][i].
+__global__ void jacobi_finish_kernel(int s, const double* __restrict__ Xt,
+                                     const double* __restrict__ Vt, double* __restrict__ wtmp,
+                                     double* __restrict__ V, double* __restrict__ w) {
+  extern __shared__ double ws_[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int p = warp; p < s; p += nw) {
+    double nx = 0.0, d = 0.0;
+    for (int i = lane; i < s; i += 32) {
+      const double x = Xt[(int64_t)p * s + i];
+      nx = fma(x, x, nx);
+      d = fma(Vt[(int64_t)p * s + i], x, d);
+    }
+    nx = warp_sum(nx);
+    d = warp_sum(d);
+    if (lane == 0) ws_[p] = (d >= 0.0 ? 1.0 : -1.0) * sqrt(nx);
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < s; p += blockDim.x) {
+    const double wp = ws_[p];
+    int rank = 0;
+    for (int q = 0; q < s; ++q) {
+      const double wq = ws_[q];
+      rank += (wq > wp) || (wq == wp && q < p);
+    }
+    wtmp[p] = (double)rank;
+    w[rank] = wp;
+  }
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < (int64_t)s * s; t += blockDim.x) {
+    const int p = (int)(t / s), i = (int)(t % s);
+    V[(int64_t)i * s + (int)wtmp[p]] = Vt[(int64_t)p * s + i];
+  }
+}
+
+__global__ void eye_kernel(int s, double* V) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)s * s;
+       t += (int64_t)gridDim.x * blockDim.x)
+    V[t] = (t / s == t % s) ? 1.0 : 0.0;
+}
+
+// Cmat[i][j] = V[i][j] * scale[j]  (s x cols, ldc = cols)
+__global__ void scale_cols_kernel(int s, int cols, const double* __restrict__ V, int64_t ldv,
+                                  const double* __restrict__ scale, double* __restrict__ Cm,
+                                  int64_t ldc) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)s * cols;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / cols), j = (int)(t % cols);
+    Cm[(int64_t)i * ldc + j] = V[(int64_t)i * ldv + j] * scale[j];
+  }
+}
+
+// ----------------------------------------------------- host orchestration --
+struct Arena {
+  char* base;
+  size_t cap, off = 0;
+  bool ok = true;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    if (off > cap) ok = false;
+    return p;
+  }
+};
+
+constexpr size_t kRedBytesD = (4096 * 16 + 64) * sizeof(double);
+
+size_t syevj_ws(int s) {
+  return 2 * (size_t)s * s * sizeof(double) + 4 * (size_t)s * sizeof(double) + 4096;
+}
+
+// Eigen-decomposition of the symmetric s x s matrix A (destroyed): V columns
+// are eigenvectors, w descending.
+static int syevj(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes,
+                 cudaStream_t st) {
+  Arena ar{reinterpret_cast<char*>(ws), ws_bytes};
+  double* Vt = ar.take<double>((size_t)s * s);
+  double* wtmp = ar.take<double>(s);
+  unsigned int* rot = ar.take<unsigned int>(4);
+  int* sweeps = ar.take<int>(2);
+  if (!ar.ok) return NYS_ERR_WORKSPACE;
+  // A is symmetric, so its rows are its columns: Xt = A.
+  eye_kernel<<<(unsigned)tmin<int64_t>(cdiv((int64_t)s * s, 256), 1024), 256, 0, st>>>(s, Vt);
+  NYS_CHECK_LAUNCH();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int bps = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, jacobi_kernel, 256, 0);
+  int nsm = kNumSMs;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int npairs = (s + (s & 1)) / 2;
+  int blocks = (int)tmin<int64_t>(cdiv(npairs, 8), (int64_t)max(1, bps) * nsm);
+  blocks = max(1, blocks);
+  int max_sweeps = 40;
+  double tol = 1e-15;
+  void* args[] = {(void*)&s, (void*)&A, (void*)&Vt, (void*)&max_sweeps, (void*)&tol,
+                  (void*)&rot, (void*)&sweeps};
+  if (cudaLaunchCooperativeKernel((void*)jacobi_kernel, blocks, 256, args, 0, st) != cudaSuccess)
+    return NYS_ERR_CUDA;
+  jacobi_finish_kernel<<<1, 1024, s * sizeof(double), st>>>(s, A, Vt, wtmp, V, w);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+static int cholesky(int s, double* C, int* info_dev, int* info_host, cudaStream_t st) {
+  cholesky_kernel<<<1, 1024, 0, st>>>(s, C, s, info_dev);
+  NYS_CHECK_LAUNCH();
+  if (cudaMemcpyAsync(info_host, info_dev, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return NYS_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+  return NYS_OK;
+}
+
+static int trinv(int s, const double* L, double* X, cudaStream_t st) {
+  trinv_lower_kernel<<<(unsigned)cdiv(s, 8), 256, 8 * s * sizeof(double), st>>>(s, L, s, X, s);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+size_t ortho_ws(int64_t n, int s) {
+  const size_t ss = (size_t)s * s * sizeof(double);
+  return kRedBytesD + 3 * ss + (size_t)n * s * sizeof(double) + gemm_ws(s, s, n) + syevj_ws(s) +
+         8 * s * sizeof(double) + 8192;
+}
+
+// CholeskyQR2: Q = Omega R^{-1}, twice.  Falls back to an eigen-based
+// orthonormalisation if a Gram matrix is numerically singular.
+static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* ws,
+                          size_t ws_bytes, cudaStream_t st) {
+  Arena ar{reinterpret_cast<char*>(ws), ws_bytes};
+  ar.take<char>(kRedBytesD);
+  double* G = ar.take<double>((size_t)s * s);
+  double* Li = ar.take<double>((size_t)s * s);
+  double* Vm = ar.take<double>((size_t)s * s);
+  double* tmp = ar.take<double>((size_t)n * s);
+  double* wv = ar.take<double>(s);
+  double* sc = ar.take<double>(s);
+  int* info = ar.take<int>(2);
+  const size_t gws_b = gemm_ws(s, s, n);
+  void* gws = ar.take<char>(gws_b);
+  const size_t jws_b = syevj_ws(s);
+  void* jws = ar.take<char>(jws_b);
+  if (!ar.ok) return NYS_ERR_WORKSPACE;
+  const double* src = Om;
+  int rc;
+  for (int pass = 0; pass < 2; ++pass) {
+    rc = gemm(1, 0, s, s, n, 1.0, src, s, src, s, 0.0, G, s, gws, gws_b, st);
+    if (rc) return rc;
+    int info_h = 0;
+    rc = cholesky(s, G, info, &info_h, st);
+    if (rc) return rc;
+    if (info_h == 0) {
+      rc = trinv(s, G, Li, st);
+      if (rc) return rc;
+      // tmp = src L^{-T}
+      rc = gemm(0, 1, n, s, s, 1.0, src, s, Li, s, 0.0, tmp, s, nullptr, 0, st);
+    } else {
+      // eigen fallback: src V diag(1/sqrt(w))  (full-rank Gaussian input expected)
+      rc = gemm(1, 0, s, s, n, 1.0, src, s, src, s, 0.0, G, s, gws, gws_b, st);
+      if (rc) return rc;
+      rc = syevj(s, G, Vm, wv, jws, jws_b, st);
+      if (rc) return rc;
+      std::vector<double> wh(s);
+      cudaMemcpyAsync(wh.data(), wv, s * sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+      for (int j = 0; j < s; ++j) wh[j] = wh[j] > 0.0 ? 1.0 / sqrt(wh[j]) : 0.0;
+      cudaMemcpyAsync(sc, wh.data(), s * sizeof(double), cudaMemcpyHostToDevice, st);
+      scale_cols_kernel<<<(unsigned)cdiv((int64_t)s * s, 256), 256, 0, st>>>(s, s, Vm, s, sc, Li, s);
+      NYS_CHECK_LAUNCH();
+      rc = gemm(0, 0, n, s, s, 1.0, src, s, Li, s, 0.0, tmp, s, nullptr, 0, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+    }
+    if (rc) return rc;
+    if (cudaMemcpyAsync(Q, tmp, (size_t)n * s * sizeof(double), cudaMemcpyDeviceToDevice, st) !=
+        cudaSuccess)
+      return NYS_ERR_CUDA;
+    src = Q;
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+  return NYS_OK;
+}
+
+size_t nystrom_ws(int64_t n, int s, int r) {
+  const size_t ss = (size_t)s * s * sizeof(double);
+  return kRedBytesD + 6 * ss + (size_t)n * s * sizeof(double) + gemm_ws(s, s, n) + syevj_ws(s) +
+         16 * (size_t)s * sizeof(double) + 16384;
+}
+
+static int nystrom_core(int64_t n, int s, int r, const double* Q, double* Y, double* U,
+                        double* lam, int* r_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  Arena ar{reinterpret_cast<char*>(ws), ws_bytes};
+  char* red = ar.take<char>(kRedBytesD);
+  double* shift_d = ar.take<double>(4);
+  double* core = ar.take<double>((size_t)s * s);
+  double* Lm = ar.take<double>((size_t)s * s);
+  double* Li = ar.take<double>((size_t)s * s);
+  double* G = ar.take<double>((size_t)s * s);
+  double* V = ar.take<double>((size_t)s * s);
+  double* Cm = ar.take<double>((size_t)s * s);
+  double* wv = ar.take<double>(s);
+  double* scl = ar.take<double>(s);
+  double* B = ar.take<double>((size_t)n * s);
+  int* info = ar.take<int>(4);
+  const size_t gws_b = gemm_ws(s, s, n);
+  void* gws = ar.take<char>(gws_b);
+  const size_t jws_b = syevj_ws(s);
+  void* jws = ar.take<char>(jws_b);
+  if (!ar.ok) return NYS_ERR_WORKSPACE;
+  const double eps = 2.220446049250313e-16;
+  cudaMemsetAsync(shift_d, 0, 4 * sizeof(double), st);
+
+  // 1. trace shift and Y_s = Y + shift Q   (sketch.py:102-106)
+  const int64_t tot = n * (int64_t)s;
+  const unsigned sb = (unsigned)tmax<int64_t>(1, tmin<int64_t>(cdiv(tot, 256), kNumSMs * 4));
+  sketch_shift_kernel<<<sb, 256, 0, st>>>(n, s, Q, Y, reinterpret_cast<double*>(red),
+                                          reinterpret_cast<unsigned int*>(
+                                              reinterpret_cast<double*>(red) + 4096 * 16),
+                                          shift_d, nullptr);
+  NYS_CHECK_LAUNCH();
+  add_scaled_kernel<<<sb, 256, 0, st>>>(tot, Q, Y, shift_d);
+  NYS_CHECK_LAUNCH();
+  // 2. core = Q^T Y_s, symmetrised  (sketch.py:107-108)
+  int rc = gemm(1, 0, s, s, n, 1.0, Q, s, Y, s, 0.0, core, s, gws, gws_b, st);
+  if (rc) return rc;
+  symmetrize_kernel<<<(unsigned)cdiv((int64_t)s * s, 256), 256, 0, st>>>(s, core, s);
+  NYS_CHECK_LAUNCH();
+  double shift_h = 0.0;
+  cudaMemcpyAsync(&shift_h, shift_d, sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(Lm, core, (size_t)s * s * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  // 3. Cholesky, B = Y_s L^{-T}   (sketch.py:110-113)
+  int info_h = 0;
+  rc = cholesky(s, Lm, info, &info_h, st);
+  if (rc) return rc;
+  int s_eff = s;
+  if (info_h == 0) {
+    rc = trinv(s, Lm, Li, st);
+    if (rc) return rc;
+    rc = gemm(0, 1, n, s, s, 1.0, Y, s, Li, s, 0.0, B, s, nullptr, 0, st);
+    if (rc) return rc;
+  } else {
+    // eigh fallback (sketch.py:114-124)
+    rc = syevj(s, core, V, wv, jws, jws_b, st);
+    if (rc) return rc;
+    std::vector<double> wh(s);
+    cudaMemcpyAsync(wh.data(), wv, s * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+    // wh is descending: wh[0] largest, wh[s-1] smallest
+    const double scale = fmax(fabs(wh[0]), shift_h);
+    if (wh[s - 1] < -1e-8 * scale) return NYS_ERR_NOT_PSD;
+    int keep = 0;
+    std::vector<double> sc(s, 0.0);
+    for (int j = 0; j < s; ++j)
+      if (wh[j] > eps * scale) {
+        sc[j] = 1.0 / sqrt(wh[j]);
+        ++keep;
+      }
+    if (keep == 0) {
+      *r_out = 0;
+      return NYS_OK;
+    }
+    // kept eigenvalues are the leading `keep` columns (descending order)
+    cudaMemcpyAsync(scl, sc.data(), s * sizeof(double), cudaMemcpyHostToDevice, st);
+    scale_cols_kernel<<<(unsigned)cdiv((int64_t)s * keep, 256), 256, 0, st>>>(s, keep, V, s, scl,
+                                                                             Cm, keep);
+    NYS_CHECK_LAUNCH();
+    rc = gemm(0, 0, n, keep, s, 1.0, Y, s, Cm, keep, 0.0, B, keep, nullptr, 0, st);
+    if (rc) return rc;
+    s_eff = keep;
+  }
+  // 4. thin SVD of B through the eigenpairs of B^T B   (sketch.py:126-128)
+  rc = gemm(1, 0, s_eff, s_eff, n, 1.0, B, s_eff, B, s_eff, 0.0, G, s_eff, gws, gws_b, st);
+  if (rc) return rc;
+  symmetrize_kernel<<<(unsigned)cdiv((int64_t)s_eff * s_eff, 256), 256, 0, st>>>(s_eff, G, s_eff);
+  NYS_CHECK_LAUNCH();
+  rc = syevj(s_eff, G, V, wv, jws, jws_b, st);
+  if (rc) return rc;
+  std::vector<double> wh(s_eff);
+  cudaMemcpyAsync(wh.data(), wv, s_eff * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+  const int rr = r < s_eff ? r : s_eff;
+  std::vector<double> lam_h(rr), inv_sv(rr);
+  for (int j = 0; j < rr; ++j) {
+    const double sv2 = fmax(wh[j], 0.0);
+    lam_h[j] = fmax(sv2 - shift_h, 0.0);
+    inv_sv[j] = sv2 > 0.0 ? 1.0 / sqrt(sv2) : 0.0;
+  }
+  cudaMemcpyAsync(lam, lam_h.data(), rr * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(scl, inv_sv.data(), rr * sizeof(double), cudaMemcpyHostToDevice, st);
+  scale_cols_kernel<<<(unsigned)cdiv((int64_t)s_eff * rr, 256), 256, 0, st>>>(s_eff, rr, V, s_eff,
+                                                                             scl, Cm, rr);
+  NYS_CHECK_LAUNCH();
+  rc = gemm(0, 0, n, rr, s_eff, 1.0, B, s_eff, Cm, rr, 0.0, U, r, nullptr, 0, st);
+  if (rc) return rc;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+  *r_out = rr;
+  return NYS_OK;
+}
+
+}  // namespace nys
+
+// ------------------------------------------------------------- C ABI ------
+using namespace nys;
+
+extern "C" size_t nys_gemm_workspace(int64_t M, int64_t N, int64_t K) { return gemm_ws(M, N, K); }
+
+extern "C" int nys_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
+                            const double* A, int64_t lda, const double* B, int64_t ldb,
+                            double beta, double* C, int64_t ldc, void* ws, size_t ws_bytes,
+                            void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || ldc < N) return NYS_ERR_ARG;
+  if ((transA ? lda < M : lda < K) || (transB ? ldb < K : ldb < N)) return NYS_ERR_ARG;
+  return gemm(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_bytes,
+              as_stream(stream));
+}
+
+extern "C" size_t nys_orthonormalize_workspace(int64_t n, int s) { return ortho_ws(n, s); }
+
+extern "C" int nys_orthonormalize_f64(int64_t n, int s, const double* Omega, double* Q, void* ws,
+                                      size_t ws_bytes, void* stream) {
+  if (n <= 0 || s <= 0 || s > n) return NYS_ERR_ARG;
+  return orthonormalize(n, s, Omega, Q, ws, ws_bytes, as_stream(stream));
+}
+
+extern "C" size_t nys_nystrom_workspace(int64_t n, int s, int r) { return nystrom_ws(n, s, r); }
+
+extern "C" int nys_nystrom_core_f64(int64_t n, int s, int r, const double* Q, double* Y, double* U,
+                                    double* lam, int* r_out, void* ws, size_t ws_bytes,
+                                    void* stream) {
+  if (n <= 0 || s <= 0 || s > n || r < 1 || r > s || !r_out) return NYS_ERR_ARG;
+  return nystrom_core(n, s, r, Q, Y, U, lam, r_out, ws, ws_bytes, as_stream(stream));
+}
+
+extern "C" size_t nys_syevj_workspace(int s) { return syevj_ws(s); }
+
+extern "C" int nys_syevj_f64(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes,
+                             void* stream) {
+  if (s <= 0) return NYS_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  int rc = syevj(s, A, V, w, ws, ws_bytes, st);
+  if (rc) return rc;
+  return cudaStreamSynchronize(st) == cudaSuccess ? NYS_OK : NYS_ERR_CUDA;
+}
+
+// ------------------------------------------------------------- misc -------
+extern "C" int nys_abi_version(void) { return NYS_ABI_VERSION; }
+
+extern "C" const char* nys_status_string(int status) {
+  switch (status) {
+    case NYS_OK: return "ok";
+    case NYS_ERR_ARG: return "invalid argument";
+    case NYS_ERR_CUDA: return "CUDA error";
+    case NYS_ERR_NOT_SPD: return "operator is not SPD";
+    case NYS_ERR_NONFINITE: return "non-finite value";
+    case NYS_ERR_NOT_PSD: return "operator is not positive semidefinite";
+    case NYS_ERR_UNSUPPORTED: return "unsupported";
+    case NYS_ERR_WORKSPACE: return "workspace too small";
+    case NYS_ERR_NO_DEVICE: return "no sm_100 device";
+    default: return "unknown";
+  }
+}
+
+extern "C" int nys_device_check(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return NYS_ERR_NO_DEVICE;
+  int major = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+    return NYS_ERR_NO_DEVICE;
+  return major == 10 ? NYS_OK : NYS_ERR_NO_DEVICE;
+}

@@ -1,0 +1,493 @@
+// K1 / K2 / K3: FP64 dense products on row-major A.
+//
+//   K1  Y = A X        (operators.py:114-115), k <= 4 right-hand sides
+//   K2  Y = A^T T      (operators.py:117-118), k <= 4 right-hand sides
+//   K3  y = A^T(d o Av) + shift v, pAp = v.y   (problems.py:263-264, admm.py:262-263)
+//
+// All three are HBM-bound streams of A (8 bytes per element, 1/4 flop per
+// byte per RHS).  Design for B200:
+//   * 128-bit (double2) coalesced loads of A rows; a warp covers 512 B per load;
+//   * K1: one warp owns RW=4 rows so every load of X is reused 4x from
+//     registers (X traffic from L1/L2 = k/4 of the A traffic); columns are
+//     split when there are too few row groups to fill 148 SMs;
+//   * K2: a CTA owns a 512-column strip and a contiguous row range; the
+//     per-row coefficients T are staged in shared memory; splits over rows are
+//     summed in a fixed order by a second kernel (deterministic, no atomics);
+//   * grids are sized in multiples of the 148 SMs.
+#include "common.cuh"
+
+namespace nys {
+
+// ------------------------------------------------------------------ K1 ----
+constexpr int kGemvThreads = 256;
+constexpr int kGemvRW = 4;
+
+template <int K, int RW, bool VEC>
+__global__ void __launch_bounds__(kGemvThreads)
+gemv_n_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
+              const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
+              const double* __restrict__ dscale, int splits, int64_t chunk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t ngroups = cdiv(rows, RW);
+  if (warp >= ngroups * splits) return;
+  const int64_t g = warp % ngroups;
+  const int s = (int)(warp / ngroups);
+  const int64_t r0 = g * RW;
+  const int64_t c0 = (int64_t)s * chunk;
+  const int64_t c1 = min(n, c0 + chunk);
+
+  const double* arow[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) arow[r] = A + min(r0 + r, rows - 1) * lda;
+
+  double acc[RW][K];
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[r][j] = 0.0;
+
+  if (VEC) {
+    constexpr int U = 2;
+    int64_t c = c0 + 2 * lane;
+    for (; c + 64 * (U - 1) + 1 < c1; c += 64 * U) {
+      double2 a[U][RW], x[U][K];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+          a[u][r] = __ldg(reinterpret_cast<const double2*>(arow[r] + c + 64 * u));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          x[u][j] = __ldg(reinterpret_cast<const double2*>(X + j * ldx + c + 64 * u));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            acc[r][j] = fma(a[u][r].x, x[u][j].x, acc[r][j]);
+            acc[r][j] = fma(a[u][r].y, x[u][j].y, acc[r][j]);
+          }
+    }
+    for (; c + 1 < c1; c += 64) {
+      double2 a[RW], x[K];
+#pragma unroll
+      for (int r = 0; r < RW; ++r) a[r] = __ldg(reinterpret_cast<const double2*>(arow[r] + c));
+#pragma unroll
+      for (int j = 0; j < K; ++j) x[j] = __ldg(reinterpret_cast<const double2*>(X + j * ldx + c));
+#pragma unroll
+      for (int r = 0; r < RW; ++r)
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          acc[r][j] = fma(a[r].x, x[j].x, acc[r][j]);
+          acc[r][j] = fma(a[r].y, x[j].y, acc[r][j]);
+        }
+    }
+    // odd tail element of this column range
+    if (((c1 - c0) & 1) && lane == 0) {
+      const int64_t ct = c1 - 1;
+#pragma unroll
+      for (int r = 0; r < RW; ++r)
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[r][j] = fma(arow[r][ct], X[j * ldx + ct], acc[r][j]);
+    }
+  } else {
+    for (int64_t c = c0 + lane; c < c1; c += 32) {
+      double x[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) x[j] = __ldg(X + j * ldx + c);
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        const double a = __ldg(arow[r] + c);
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[r][j] = fma(a, x[j], acc[r][j]);
+      }
+    }
+  }
+
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[r][j] = warp_sum(acc[r][j]);
+
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (lane == r * K + j && r0 + r < rows) {
+        if (splits == 1) {
+          double v = acc[r][j];
+          if (dscale) v *= dscale[r0 + r];
+          Y[j * ldy + r0 + r] = v;
+        } else {
+          Y[((int64_t)s * K + j) * rows + r0 + r] = acc[r][j];
+        }
+      }
+    }
+}
+
+// Y[j*ldy + i] = (sum_s P[(s*K + j)*rows + i]) * (dscale ? dscale[i] : 1)
+__global__ void gemv_n_reduce(const double* __restrict__ P, int64_t rows, int K, int splits,
+                              double* __restrict__ Y, int64_t ldy,
+                              const double* __restrict__ dscale) {
+  const int64_t total = rows * K;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(t / rows);
+    const int64_t i = t - (int64_t)j * rows;
+    double v = 0.0;
+    for (int s = 0; s < splits; ++s) v += P[((int64_t)s * K + j) * rows + i];
+    if (dscale) v *= dscale[i];
+    Y[j * ldy + i] = v;
+  }
+}
+
+static void gemv_n_plan(int64_t rows, int64_t n, int& splits, int64_t& chunk) {
+  const int64_t ngroups = cdiv(rows, kGemvRW);
+  const int64_t target_warps = (int64_t)kNumSMs * 16;
+  int64_t sp = ngroups >= target_warps ? 1 : cdiv(target_warps, ngroups);
+  // keep at least 512 columns per split
+  sp = tmax<int64_t>(1, tmin<int64_t>(sp, n / 512));
+  chunk = cdiv(cdiv(n, sp), 64) * 64;
+  sp = cdiv(n, chunk);
+  splits = (int)sp;
+}
+
+template <int K>
+static int gemv_n_launch(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X,
+                         int64_t ldx, double* Y, int64_t ldy, const double* dscale, double* ws,
+                         size_t ws_bytes, cudaStream_t st) {
+  int splits;
+  int64_t chunk;
+  gemv_n_plan(rows, n, splits, chunk);
+  if (splits > 1 && ws_bytes < (size_t)splits * K * rows * sizeof(double)) {
+    splits = 1;
+    chunk = n;
+  }
+  const bool vec = ((lda & 1) == 0) && ((ldx & 1) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  const int64_t warps = cdiv(rows, kGemvRW) * splits;
+  const int64_t blocks = cdiv(warps * 32, kGemvThreads);
+  double* out = splits == 1 ? Y : ws;
+  if (vec)
+    gemv_n_kernel<K, kGemvRW, true><<<(unsigned)blocks, kGemvThreads, 0, st>>>(
+        A, rows, n, lda, X, ldx, out, ldy, dscale, splits, chunk);
+  else
+    gemv_n_kernel<K, kGemvRW, false><<<(unsigned)blocks, kGemvThreads, 0, st>>>(
+        A, rows, n, lda, X, ldx, out, ldy, dscale, splits, chunk);
+  NYS_CHECK_LAUNCH();
+  if (splits > 1) {
+    const int64_t total = rows * K;
+    const int64_t rb = tmin<int64_t>(cdiv(total, 256), kNumSMs * 8);
+    gemv_n_reduce<<<(unsigned)rb, 256, 0, st>>>(ws, rows, K, splits, Y, ldy, dscale);
+    NYS_CHECK_LAUNCH();
+  }
+  return NYS_OK;
+}
+
+int gemv_n(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X, int64_t ldx,
+           int k, double* Y, int64_t ldy, const double* dscale, void* ws, size_t ws_bytes,
+           cudaStream_t st) {
+  double* w = reinterpret_cast<double*>(ws);
+  switch (k) {
+    case 1: return gemv_n_launch<1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st);
+    case 2: return gemv_n_launch<2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st);
+    case 3: return gemv_n_launch<3>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st);
+    case 4: return gemv_n_launch<4>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st);
+    default: return NYS_ERR_ARG;
+  }
+}
+
+size_t gemv_n_ws(int64_t rows, int64_t n, int k) {
+  int splits;
+  int64_t chunk;
+  gemv_n_plan(rows, n, splits, chunk);
+  return splits > 1 ? (size_t)splits * k * rows * sizeof(double) : 0;
+}
+
+// ------------------------------------------------------------------ K2 ----
+constexpr int kGemvTThreads = 256;
+constexpr int kGemvTTile = 256;  // rows of T staged per smem tile
+constexpr int kGemvTUnroll = 8;
+
+template <int K, bool VEC>
+__global__ void __launch_bounds__(kGemvTThreads)
+gemv_t_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
+              const double* __restrict__ T, int64_t ldt, double* __restrict__ out, int64_t ldo,
+              int64_t rows_per_split, int direct) {
+  __shared__ double tsh[K][kGemvTTile];
+  constexpr int CPT = VEC ? 2 : 1;  // columns per thread
+  const int64_t c = ((int64_t)blockIdx.x * kGemvTThreads + threadIdx.x) * CPT;
+  const int64_t i0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t i1 = min(rows, i0 + rows_per_split);
+  double acc[K][CPT];
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) acc[j][q] = 0.0;
+
+  for (int64_t ib = i0; ib < i1; ib += kGemvTTile) {
+    const int cnt = (int)tmin<int64_t>(kGemvTTile, i1 - ib);
+    __syncthreads();
+    for (int t = threadIdx.x; t < K * kGemvTTile; t += kGemvTThreads) {
+      const int j = t / kGemvTTile, ii = t - j * kGemvTTile;
+      tsh[j][ii] = ii < cnt ? T[j * ldt + ib + ii] : 0.0;
+    }
+    __syncthreads();
+    if (VEC && c + 1 < n) {
+      const double* ap = A + ib * lda + c;
+      int t = 0;
+      for (; t + kGemvTUnroll <= cnt; t += kGemvTUnroll) {
+        double2 a[kGemvTUnroll];
+#pragma unroll
+        for (int u = 0; u < kGemvTUnroll; ++u)
+          a[u] = __ldg(reinterpret_cast<const double2*>(ap + (int64_t)(t + u) * lda));
+#pragma unroll
+        for (int u = 0; u < kGemvTUnroll; ++u)
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            const double tv = tsh[j][t + u];
+            acc[j][0] = fma(a[u].x, tv, acc[j][0]);
+            acc[j][CPT - 1] = fma(a[u].y, tv, acc[j][CPT - 1]);
+          }
+      }
+      for (; t < cnt; ++t) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(ap + (int64_t)t * lda));
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const double tv = tsh[j][t];
+          acc[j][0] = fma(a.x, tv, acc[j][0]);
+          acc[j][CPT - 1] = fma(a.y, tv, acc[j][CPT - 1]);
+        }
+      }
+    } else if (c < n) {
+      // scalar path: misaligned data or the odd last column
+      const double* ap = A + ib * lda + c;
+      for (int t = 0; t < cnt; ++t) {
+        const double a = __ldg(ap + (int64_t)t * lda);
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j][0] = fma(a, tsh[j][t], acc[j][0]);
+      }
+    }
+  }
+  if (c >= n) return;
+  const bool two = VEC && (c + 1 < n);
+  double* o = direct ? out : out + (int64_t)blockIdx.y * K * ldo;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (two) {
+      *reinterpret_cast<double2*>(o + j * ldo + c) = make_double2(acc[j][0], acc[j][CPT - 1]);
+    } else {
+      o[j * ldo + c] = acc[j][0];
+    }
+  }
+}
+
+// Y[j*ldy + c] = sum_s P[(s*K + j)*n + c]  (fixed order);
+// optional epilogue for K = 1: Y += shift * v, dot = v.Y  (last-block reduction)
+__global__ void gemv_t_reduce(const double* __restrict__ P, int64_t n, int K, int splits,
+                              double* __restrict__ Y, int64_t ldy, const double* __restrict__ v,
+                              double shift, double* __restrict__ dot, double* __restrict__ part,
+                              unsigned int* counter) {
+  __shared__ double sh[32];
+  double d[1] = {0.0};
+  const int64_t total = n * K;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(t / n);
+    const int64_t c = t - (int64_t)j * n;
+    double acc = 0.0;
+    for (int s = 0; s < splits; ++s) acc += P[((int64_t)s * K + j) * n + c];
+    if (v) {
+      acc += shift * v[c];
+      if (dot) d[0] = fma(v[c], acc, d[0]);
+    }
+    Y[j * ldy + c] = acc;
+  }
+  if (!dot) return;
+  block_sum<1>(d, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = d[0];
+  if (last_block(counter)) {
+    const double tot = block_sum_partials(part, gridDim.x, 1, sh);
+    if (threadIdx.x == 0) *dot = tot;
+  }
+}
+
+static void gemv_t_plan(int64_t rows, int64_t n, bool vec, int& splits, int64_t& rps) {
+  const int64_t strips = cdiv(n, (int64_t)kGemvTThreads * (vec ? 2 : 1));
+  const int64_t target = (int64_t)kNumSMs * 6;
+  int64_t sp = strips >= target ? 1 : cdiv(target, strips);
+  sp = tmax<int64_t>(1, tmin<int64_t>(sp, cdiv(rows, 64)));
+  rps = cdiv(cdiv(rows, sp), kGemvTUnroll) * kGemvTUnroll;
+  splits = (int)cdiv(rows, rps);
+}
+
+// reduction workspace layout (doubles): [0, kRedPartials) partials, then the ticket
+constexpr int kRedPartials = 4096;
+constexpr size_t kRedBytes = (kRedPartials * 16 + 64) * sizeof(double);
+
+inline double* red_part(void* ws) { return reinterpret_cast<double*>(ws); }
+inline unsigned int* red_counter(void* ws) {
+  return reinterpret_cast<unsigned int*>(reinterpret_cast<double*>(ws) + kRedPartials * 16);
+}
+
+template <int K>
+static int gemv_t_launch(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T,
+                         int64_t ldt, double* Y, int64_t ldy, const double* v, double shift,
+                         double* dot, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const bool vec = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                   ((ldy & 1) == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+  int splits;
+  int64_t rps;
+  gemv_t_plan(rows, n, vec, splits, rps);
+  const bool epi = (v != nullptr);
+  // the split partials live after the reduction scratch
+  const size_t need = kRedBytes + (size_t)splits * K * n * sizeof(double);
+  if (ws_bytes < need) {
+    if (ws_bytes < kRedBytes + (size_t)K * n * sizeof(double)) return NYS_ERR_WORKSPACE;
+    splits = 1;
+    rps = rows;
+  }
+  double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
+  const bool direct = (splits == 1) && !epi;
+  const int64_t strips = cdiv(n, (int64_t)kGemvTThreads * (vec ? 2 : 1));
+  dim3 grid((unsigned)strips, (unsigned)splits);
+  if (vec)
+    gemv_t_kernel<K, true><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt,
+                                                           direct ? Y : P, direct ? ldy : n,
+                                                           rps, direct ? 1 : 0);
+  else
+    gemv_t_kernel<K, false><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt,
+                                                            direct ? Y : P, direct ? ldy : n,
+                                                            rps, direct ? 1 : 0);
+  NYS_CHECK_LAUNCH();
+  if (!direct) {
+    const int64_t rb = tmin<int64_t>(cdiv(n * K, 256), kRedPartials);
+    gemv_t_reduce<<<(unsigned)rb, 256, 0, st>>>(P, n, K, splits, Y, ldy, v, shift, dot,
+                                                red_part(ws), red_counter(ws));
+    NYS_CHECK_LAUNCH();
+  }
+  return NYS_OK;
+}
+
+int gemv_t(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt,
+           int k, double* Y, int64_t ldy, const double* v, double shift, double* dot, void* ws,
+           size_t ws_bytes, cudaStream_t st) {
+  switch (k) {
+    case 1: return gemv_t_launch<1>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st);
+    case 2: return gemv_t_launch<2>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st);
+    case 3: return gemv_t_launch<3>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st);
+    case 4: return gemv_t_launch<4>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st);
+    default: return NYS_ERR_ARG;
+  }
+}
+
+size_t gemv_t_ws(int64_t rows, int64_t n, int k) {
+  int splits;
+  int64_t rps;
+  gemv_t_plan(rows, n, true, splits, rps);
+  int s2;
+  gemv_t_plan(rows, n, false, s2, rps);
+  splits = max(splits, s2);
+  return kRedBytes + (size_t)splits * k * n * sizeof(double);
+}
+
+// --------------------------------------------------------- small vectors ----
+__global__ void shift_dot_kernel(int64_t n, const double* __restrict__ v, double shift,
+                                 double* __restrict__ y, double* __restrict__ dot,
+                                 double* __restrict__ part, unsigned int* counter) {
+  __shared__ double sh[32];
+  double d[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double yi = y[i];
+    if (shift != 0.0) {
+      yi += shift * v[i];
+      y[i] = yi;
+    }
+    d[0] = fma(v[i], yi, d[0]);
+  }
+  if (!dot) return;
+  block_sum<1>(d, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = d[0];
+  if (last_block(counter)) {
+    const double tot = block_sum_partials(part, gridDim.x, 1, sh);
+    if (threadIdx.x == 0) *dot = tot;
+  }
+}
+
+int shift_dot(int64_t n, const double* v, double shift, double* y, double* dot, void* ws,
+              cudaStream_t st) {
+  if (n <= 0) return NYS_ERR_ARG;
+  const int64_t blocks = tmin<int64_t>(cdiv(n, 256), kNumSMs * 4);
+  shift_dot_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, v, shift, y, dot, red_part(ws),
+                                                     red_counter(ws));
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+size_t reduce_ws() { return kRedBytes; }
+
+}  // namespace nys
+
+// ------------------------------------------------------------- C ABI ------
+using namespace nys;
+
+extern "C" size_t nys_reduce_workspace(void) { return kRedBytes; }
+
+extern "C" size_t nys_gemv_workspace(int64_t rows, int64_t n, int k) {
+  return gemv_n_ws(rows, n, k);
+}
+
+extern "C" int nys_gemv_f64(const double* A, int64_t rows, int64_t n, int64_t lda,
+                            const double* X, int64_t ldx, int k, double* Y, int64_t ldy,
+                            void* ws, size_t ws_bytes, void* stream) {
+  if (rows <= 0 || n <= 0 || lda < n || k < 1 || k > 4 || ldx < n || ldy < rows)
+    return NYS_ERR_ARG;
+  return gemv_n(A, rows, n, lda, X, ldx, k, Y, ldy, nullptr, ws, ws_bytes, as_stream(stream));
+}
+
+extern "C" size_t nys_gemvT_workspace(int64_t rows, int64_t n, int k) {
+  return gemv_t_ws(rows, n, k);
+}
+
+extern "C" int nys_gemvT_f64(const double* A, int64_t rows, int64_t n, int64_t lda,
+                             const double* T, int64_t ldt, int k, double* Y, int64_t ldy,
+                             void* ws, size_t ws_bytes, void* stream) {
+  if (rows <= 0 || n <= 0 || lda < n || k < 1 || k > 4 || ldt < rows || ldy < n)
+    return NYS_ERR_ARG;
+  return gemv_t(A, rows, n, lda, T, ldt, k, Y, ldy, nullptr, 0.0, nullptr, ws, ws_bytes,
+                as_stream(stream));
+}
+
+extern "C" size_t nys_hvp_workspace(int64_t rows, int64_t n) {
+  // t = d o (A v) (rows doubles) + the K1 split partials + the K2 workspace
+  return cdiv(rows, 2) * 2 * sizeof(double) + gemv_n_ws(rows, n, 1) + gemv_t_ws(rows, n, 1);
+}
+
+extern "C" int nys_hvp_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
+                           const double* v, double shift, double* y, double* pAp, int finish,
+                           void* ws, size_t ws_bytes, void* stream) {
+  if (rows <= 0 || n <= 0 || lda < n) return NYS_ERR_ARG;
+  if (ws_bytes < nys_hvp_workspace(rows, n)) return NYS_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  char* base = reinterpret_cast<char*>(ws);
+  // layout: [K2 ws (reduction scratch first)] [t] [K1 partials]
+  const size_t wt = gemv_t_ws(rows, n, 1);
+  double* t = reinterpret_cast<double*>(base + wt);
+  void* wn = base + wt + cdiv(rows, 2) * 2 * sizeof(double);
+  int rc = gemv_n(A, rows, n, lda, v, n, 1, t, rows, d, wn, gemv_n_ws(rows, n, 1), st);
+  if (rc) return rc;
+  if (finish)
+    return gemv_t(A, rows, n, lda, t, rows, 1, y, n, v, shift, pAp, base, wt, st);
+  return gemv_t(A, rows, n, lda, t, rows, 1, y, n, nullptr, 0.0, nullptr, base, wt, st);
+}
+
+extern "C" int nys_shift_dot_f64(int64_t n, const double* v, double shift, double* y,
+                                 double* dot, void* ws, void* stream) {
+  return shift_dot(n, v, shift, y, dot, ws, as_stream(stream));
+}

@@ -1,0 +1,237 @@
+"""Tensor-level wrappers of the C ABI (include/nysgpu.h).
+
+``Kernels`` owns the stream and the workspaces of one solve and exposes every
+kernel as a method over torch CUDA tensors (torch is only the device-buffer
+allocator here).  The ADMM engine (``admm.py``) talks to nothing else, which
+keeps the drop-in boundary in one place.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+F64 = torch.float64
+
+
+def _p(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class Kernels:
+    """GPU implementation of the kernel interface used by the engine."""
+
+    name = "cuda"
+
+    def __init__(self, device: Optional[torch.device] = None):
+        self.L = _lib.lib()
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.current_stream(self.device)
+        self.sp = self.stream.cuda_stream
+        self._ws: dict[str, torch.Tensor] = {}
+        self.red = self.workspace("red", self.L.nys_reduce_workspace())
+        self.launches = 0
+
+    # ------------------------------------------------------------ memory --
+    def workspace(self, name: str, nbytes: int) -> torch.Tensor:
+        """Zero-filled device workspace (kernels keep tickets in it)."""
+        nbytes = max(int(nbytes), 256)
+        t = self._ws.get(name)
+        if t is None or t.numel() < nbytes:
+            t = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws[name] = t
+        return t
+
+    def empty(self, *shape) -> torch.Tensor:
+        return torch.empty(*shape, dtype=F64, device=self.device)
+
+    def zeros(self, *shape) -> torch.Tensor:
+        return torch.zeros(*shape, dtype=F64, device=self.device)
+
+    def sync(self) -> None:
+        self.stream.synchronize()
+
+    # ------------------------------------------------------- K1/K2/K3 ----
+    def gemv(self, A: torch.Tensor, X: torch.Tensor, Y: torch.Tensor) -> None:
+        """Y[j] = A X[j] for the k rows of X (k <= 4)."""
+        rows, n = A.shape
+        k = X.shape[0]
+        ws = self.workspace("gemv", self.L.nys_gemv_workspace(rows, n, k))
+        self.launches += 1
+        check(self.L.nys_gemv_f64(A.data_ptr(), rows, n, A.stride(0), X.data_ptr(), X.stride(0), k,
+                                  Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(), self.sp), "gemv")
+
+    def gemvT(self, A: torch.Tensor, T: torch.Tensor, Y: torch.Tensor) -> None:
+        """Y[j] = A^T T[j] for the k rows of T (k <= 4)."""
+        rows, n = A.shape
+        k = T.shape[0]
+        ws = self.workspace("gemvT", self.L.nys_gemvT_workspace(rows, n, k))
+        self.launches += 1
+        check(self.L.nys_gemvT_f64(A.data_ptr(), rows, n, A.stride(0), T.data_ptr(), T.stride(0), k,
+                                   Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(), self.sp), "gemvT")
+
+    def hvp(self, A, d, v, shift, y, pAp=None, finish=True) -> None:
+        rows, n = A.shape
+        ws = self.workspace("hvp", self.L.nys_hvp_workspace(rows, n))
+        self.launches += 1
+        check(self.L.nys_hvp_f64(A.data_ptr(), rows, n, A.stride(0), _p(d), v.data_ptr(), float(shift),
+                                 y.data_ptr(), _p(pAp), 1 if finish else 0, ws.data_ptr(), ws.numel(),
+                                 self.sp), "hvp")
+
+    def shift_dot(self, v, shift, y, dot=None) -> None:
+        self.launches += 1
+        check(self.L.nys_shift_dot_f64(v.numel(), v.data_ptr(), float(shift), y.data_ptr(), _p(dot),
+                                       self.red.data_ptr(), self.sp), "shift_dot")
+
+    def dot(self, a, b, out) -> None:
+        self.launches += 1
+        check(self.L.nys_dot_f64(a.numel(), a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                                 self.red.data_ptr(), self.sp), "dot")
+
+    # -------------------------------------------------------------- K6 ----
+    def precond_apply(self, U, lam, nu, v, z, rdot=None, rz=None) -> None:
+        n = v.numel()
+        r = 0 if U is None else U.shape[1]
+        ws = self.workspace("prec", self.L.nys_precond_workspace(n, r))
+        self.launches += 1
+        check(self.L.nys_precond_apply_f64(_p(U), n, r, U.stride(0) if r else 0, _p(lam), float(nu),
+                                           v.data_ptr(), z.data_ptr(), _p(rdot), _p(rz), ws.data_ptr(),
+                                           ws.numel(), self.sp), "precond")
+
+    # -------------------------------------------------------------- K7 ----
+    def cg_start(self, b, Ax, r, sc) -> None:
+        self.launches += 1
+        check(self.L.nys_cg_start_f64(b.numel(), b.data_ptr(), Ax.data_ptr(), r.data_ptr(), sc.data_ptr(),
+                                      self.red.data_ptr(), self.sp), "cg_start")
+
+    def cg_step_xr(self, x, r, p, Ap, refresh, sc) -> None:
+        self.launches += 1
+        check(self.L.nys_cg_step_xr_f64(x.numel(), x.data_ptr(), r.data_ptr(), p.data_ptr(), Ap.data_ptr(),
+                                        1 if refresh else 0, sc.data_ptr(), self.red.data_ptr(), self.sp),
+              "cg_step")
+
+    def cg_dir(self, z, p, first, sc) -> None:
+        self.launches += 1
+        check(self.L.nys_cg_dir_f64(z.numel(), z.data_ptr(), p.data_ptr(), 1 if first else 0, sc.data_ptr(),
+                                    self.sp), "cg_dir")
+
+    # --------------------------------------------------------- K8/K9 ----
+    def admm_rhs(self, hxA, gA, q, lambda2, sigma, rho, shift, x, z, u, rhs, r, sc) -> None:
+        self.launches += 1
+        check(self.L.nys_admm_rhs_f64(x.numel(), hxA.data_ptr(), gA.data_ptr(), _p(q), float(lambda2),
+                                      float(sigma), float(rho), float(shift), x.data_ptr(), z.data_ptr(),
+                                      u.data_ptr(), rhs.data_ptr(), r.data_ptr(), sc.data_ptr(),
+                                      self.red.data_ptr(), self.sp), "admm_rhs")
+
+    def admm_zu(self, x, z, u, alpha, prox_kind, kappa, lo, hi, xbar, zbar, accum) -> None:
+        self.launches += 1
+        check(self.L.nys_admm_zu_f64(x.numel(), x.data_ptr(), z.data_ptr(), u.data_ptr(), float(alpha),
+                                     int(prox_kind), float(kappa), _p(lo), _p(hi), _p(xbar), _p(zbar),
+                                     1 if accum else 0, self.sp), "admm_zu")
+
+    def admm_norms(self, x, z, u, gA, q, lambda2, rho, atnu, lambda1, lo, hi, out) -> None:
+        self.launches += 1
+        check(self.L.nys_admm_norms_f64(x.numel(), x.data_ptr(), z.data_ptr(), u.data_ptr(), gA.data_ptr(),
+                                        _p(q), float(lambda2), float(rho), _p(atnu), float(lambda1), _p(lo),
+                                        _p(hi), out.data_ptr(), self.red.data_ptr(), self.sp), "admm_norms")
+
+    def ml_rowwise(self, loss, Ax, Az, b, tg, w, thx, tnu, out) -> None:
+        self.launches += 1
+        check(self.L.nys_ml_rowwise_f64(b.numel(), _lib.LOSS[loss], _p(Ax), _p(Az), b.data_ptr(), _p(tg),
+                                        _p(w), _p(thx), _p(tnu), out.data_ptr(), self.red.data_ptr(),
+                                        self.sp), "ml_rowwise")
+
+    def ml_conj_scaled(self, loss, nu, c, b, out) -> None:
+        self.launches += 1
+        check(self.L.nys_ml_conj_scaled_f64(b.numel(), _lib.LOSS[loss], nu.data_ptr(), float(c), b.data_ptr(),
+                                            out.data_ptr(), self.red.data_ptr(), self.sp), "conj_scaled")
+
+    # ------------------------------------------------------ K13/K14 ----
+    def window_norms(self, ring, cur, others, out) -> None:
+        arr = (C.c_int * max(1, len(others)))(*others)
+        self.launches += 1
+        check(self.L.nys_window_norms_f64(ring.shape[1], ring.data_ptr(), ring.stride(0), int(cur), arr,
+                                          len(others), out.data_ptr(), self.red.data_ptr(), self.sp),
+              "window_norms")
+
+    def scale_dual(self, u, rho_old, rho_new, out) -> None:
+        self.launches += 1
+        check(self.L.nys_scale_dual_f64(u.numel(), u.data_ptr(), float(rho_old), float(rho_new),
+                                        out.data_ptr(), self.red.data_ptr(), self.sp), "scale_dual")
+
+    def qp_infeas(self, xa, xb, ua, ub, width, lo, hi, q, dx, out) -> None:
+        self.launches += 1
+        check(self.L.nys_qp_infeas_f64(xa.numel(), xa.data_ptr(), xb.data_ptr(), ua.data_ptr(), ub.data_ptr(),
+                                       float(width), lo.data_ptr(), hi.data_ptr(), _p(q), dx.data_ptr(),
+                                       out.data_ptr(), self.red.data_ptr(), self.sp), "qp_infeas")
+
+    def axpby(self, a, x, b, y) -> None:
+        self.launches += 1
+        check(self.L.nys_axpby_f64(x.numel(), float(a), x.data_ptr(), float(b), y.data_ptr(), self.sp), "axpby")
+
+    def soft_threshold(self, v, kappa, out) -> None:
+        self.launches += 1
+        check(self.L.nys_soft_threshold_f64(v.numel(), v.data_ptr(), float(kappa), out.data_ptr(), self.sp),
+              "soft_threshold")
+
+    def box_project(self, v, lo, hi, out) -> None:
+        self.launches += 1
+        check(self.L.nys_box_project_f64(v.numel(), v.data_ptr(), lo.data_ptr(), hi.data_ptr(), out.data_ptr(),
+                                         self.sp), "box_project")
+
+    def row_scale(self, X, d) -> None:
+        self.launches += 1
+        check(self.L.nys_row_scale_f64(X.shape[0], X.shape[1], X.data_ptr(), X.stride(0), d.data_ptr(),
+                                       self.sp), "row_scale")
+
+    # -------------------------------------------------------------- K5 ----
+    def gemm(self, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, Cm, ldc) -> None:
+        ws = self.workspace("gemm", self.L.nys_gemm_workspace(M, N, K))
+        self.launches += 1
+        check(self.L.nys_gemm_f64(int(ta), int(tb), M, N, K, float(alpha), A.data_ptr(), lda, B.data_ptr(),
+                                  ldb, float(beta), Cm.data_ptr(), ldc, ws.data_ptr(), ws.numel(), self.sp),
+              "gemm")
+
+    def orthonormalize(self, Om, Q) -> None:
+        n, s = Om.shape
+        ws = self.workspace("sketch", self.L.nys_orthonormalize_workspace(n, s))
+        self.launches += 1
+        check(self.L.nys_orthonormalize_f64(n, s, Om.data_ptr(), Q.data_ptr(), ws.data_ptr(), ws.numel(),
+                                            self.sp), "orthonormalize")
+
+    def nystrom_core(self, Q, Y, U, lam, r) -> int:
+        n, s = Q.shape
+        ws = self.workspace("sketch", max(self.L.nys_nystrom_workspace(n, s, r),
+                                          self.L.nys_orthonormalize_workspace(n, s)))
+        rr = C.c_int(0)
+        self.launches += 1
+        check(self.L.nys_nystrom_core_f64(n, s, r, Q.data_ptr(), Y.data_ptr(), U.data_ptr(), lam.data_ptr(),
+                                          C.byref(rr), ws.data_ptr(), ws.numel(), self.sp), "nystrom")
+        return int(rr.value)
+
+    def syevj(self, A, V, w) -> None:
+        s = A.shape[0]
+        ws = self.workspace("syevj", self.L.nys_syevj_workspace(s))
+        self.launches += 1
+        check(self.L.nys_syevj_f64(s, A.data_ptr(), V.data_ptr(), w.data_ptr(), ws.data_ptr(), ws.numel(),
+                                   self.sp), "syevj")
+
+
+_CACHE: dict = {}
+
+
+def get_kernels() -> Kernels:
+    """Kernels bound to the current device and torch stream (cached, so the
+    operator-level API reuses its workspaces)."""
+    dev = torch.cuda.current_device()
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    k = _CACHE.get((dev, sp))
+    if k is None:
+        k = Kernels(torch.device("cuda", dev))
+        _CACHE[(dev, sp)] = k
+    return k

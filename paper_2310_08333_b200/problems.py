@@ -1,0 +1,387 @@
+"""Problem interfaces of the hot path (``/root/reference/pkg/src/nysopt/problems.py``).
+
+Same constructors and fields as the reference: ``MLProblem`` (square /
+logistic / huber loss, l1 + l2 regularisation, problems.py:191-220),
+``QPProblem`` (problems.py:160-188) and the convenience constructors
+(problems.py:468-481).  Losses are identified by ``kind``; their derivatives
+and conjugates are evaluated on the device by the K8-K12 kernels, so ``Loss``
+carries the reference's flags rather than NumPy callables.
+
+The ML oracles (objective, gradient, Hessian, dual point/value/gap) run on the
+GPU through the C ABI; inside ``solve`` they are fused into the per-iteration
+passes (admm.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+
+from .errors import CapabilityError, DataError
+from .operators import (
+    ConstantHessian,
+    DenseOperator,
+    HessianOperator,
+    IdentityOperator,
+    LinearOperator,
+    MatrixFreeOperator,
+    as_operator,
+    like_input,
+    to_device,
+)
+from .prox import Box
+
+
+@dataclass(frozen=True)
+class Loss:
+    """Per-sample convex loss (problems.py:35-50), identified by kind."""
+
+    kind: str
+    deriv2_constant: bool = False
+    has_conj: bool = True
+
+    @property
+    def conj(self):
+        # the reference exposes the conjugate callable; its presence enables the
+        # duality-gap stopping rule (admm.py:476-478)
+        return True if self.has_conj else None
+
+
+def square_loss() -> Loss:
+    """l(w) = w^2/2, conjugate y^2/2 (problems.py:53-62)."""
+    return Loss("square", deriv2_constant=True)
+
+
+def logistic_loss() -> Loss:
+    """l(w) = log(1 + e^w), conjugate the binary entropy (problems.py:76-86)."""
+    return Loss("logistic")
+
+
+def huber_loss() -> Loss:
+    """w^2 on [-1, 1], 2|w| - 1 outside; conjugate y^2/4 on |y| <= 2 (problems.py:89-111)."""
+    return Loss("huber")
+
+
+def builtin_loss(kind: str) -> Loss:
+    factories = {"square": square_loss, "logistic": logistic_loss, "huber": huber_loss}
+    if kind not in factories:
+        raise DataError(f"unknown loss kind {kind!r}; expected one of {sorted(factories)}")
+    return factories[kind]()
+
+
+@dataclass
+class QPProblem:
+    """minimize (1/2) x'Px + q'x subject to l <= Mx <= u (problems.py:160-188)."""
+
+    P: LinearOperator
+    q: np.ndarray
+    M: LinearOperator
+    box: Box
+
+    def __post_init__(self):
+        self.P = as_operator(self.P)
+        self.M = as_operator(self.M)
+        self.q = np.asarray(self.q, dtype=float)
+        if self.P.input_dim != self.P.output_dim:
+            raise DataError("P must be square")
+        if self.q.shape != (self.P.input_dim,):
+            raise DataError("q must have length n")
+        if self.M.input_dim != self.P.input_dim:
+            raise DataError("M must map from dimension n")
+        if self.box.dim != self.M.output_dim:
+            raise DataError("box dimension must equal the number of constraint rows")
+
+    @property
+    def n(self) -> int:
+        return self.P.input_dim
+
+    @property
+    def m(self) -> int:
+        return self.M.output_dim
+
+
+@dataclass
+class MLProblem:
+    """minimize sum_i l(a_i'x - b_i) + lambda1 ||x||_1 + (lambda2/2)||x||_2^2
+    (problems.py:191-220)."""
+
+    loss: Loss
+    A: LinearOperator
+    b: np.ndarray
+    lambda1: float = 0.0
+    lambda2: float = 0.0
+
+    def __post_init__(self):
+        self.A = as_operator(self.A)
+        if isinstance(self.b, torch.Tensor):
+            self.b = self.b.detach().cpu().numpy()
+        self.b = np.asarray(self.b, dtype=float)
+        if self.b.shape != (self.A.output_dim,):
+            raise DataError("response vector length must equal the number of samples")
+        if self.lambda1 < 0 or self.lambda2 < 0:
+            raise DataError("regularization parameters must be nonnegative")
+        if self.lambda1 == 0 and self.lambda2 == 0:
+            raise DataError("at least one regularization parameter must be positive")
+
+    @property
+    def n(self) -> int:
+        return self.A.input_dim
+
+    @property
+    def N(self) -> int:
+        return self.A.output_dim
+
+    def residuals(self, x):
+        return like_input(self.A._apply_dev(to_device(x)) - to_device(self.b), x)
+
+
+@dataclass
+class GenericProblem:
+    """Lowered form minimize f(x) + g(z) s.t. Mx - z = c (problems.py:125-157).
+
+    On the B200 path the lowering keeps a back reference to the structured
+    problem; arbitrary user callables (f, prox_g on NumPy) are outside the
+    device hot path and are rejected by ``solve``."""
+
+    n: int
+    m: int
+    M: LinearOperator
+    c: np.ndarray
+    hess: Optional[HessianOperator] = None
+    is_quadratic: bool = False
+    full_rank: bool = False
+    qp: Optional[QPProblem] = None
+    ml: Optional[MLProblem] = None
+
+
+def lasso_problem(A, b, lambda1: float) -> MLProblem:
+    return MLProblem(square_loss(), A, b, lambda1=lambda1, lambda2=0.0)
+
+
+def elastic_net_problem(A, b, lambda1: float, lambda2: float) -> MLProblem:
+    return MLProblem(square_loss(), A, b, lambda1=lambda1, lambda2=lambda2)
+
+
+def logistic_problem(A, b, lambda1: float, lambda2: float = 0.0) -> MLProblem:
+    return MLProblem(logistic_loss(), A, b, lambda1=lambda1, lambda2=lambda2)
+
+
+def huber_problem(A, b, lambda1: float) -> MLProblem:
+    return MLProblem(huber_loss(), A, b, lambda1=lambda1, lambda2=0.0)
+
+
+def qp_lower(qp: QPProblem) -> GenericProblem:
+    """problems.py:387-421 (full_rank iff M is the identity)."""
+    return GenericProblem(n=qp.n, m=qp.m, M=qp.M, c=np.zeros(qp.m), hess=ConstantHessian(qp.P),
+                          is_quadratic=True, full_rank=isinstance(qp.M, IdentityOperator), qp=qp)
+
+
+def ml_lower(p: MLProblem) -> GenericProblem:
+    """problems.py:424-450: M = I, c = 0, full rank."""
+    return GenericProblem(n=p.n, m=p.n, M=IdentityOperator(p.n), c=np.zeros(p.n), hess=None,
+                          is_quadratic=p.loss.deriv2_constant, full_rank=True, ml=p)
+
+
+def lower(problem) -> GenericProblem:
+    if isinstance(problem, GenericProblem):
+        return problem
+    if isinstance(problem, QPProblem):
+        return qp_lower(problem)
+    if isinstance(problem, MLProblem):
+        return ml_lower(problem)
+    raise DataError(f"cannot solve object of type {type(problem).__name__}")
+
+
+# ---------------------------------------------------------------------------
+# ML oracles on the device (problems.py:227-351).  Single-GPU helpers; the
+# solver uses fused, sharded versions of the same kernels.
+
+
+def _dense_A(p: MLProblem) -> torch.Tensor:
+    if not isinstance(p.A, DenseOperator):
+        raise CapabilityError("the B200 path supports dense data matrices only")
+    return p.A.device_rows()
+
+
+class _MLEval:
+    """One pass A{x[,z]} -> row-wise loss epilogue -> A^T{...} on the device."""
+
+    def __init__(self, p: MLProblem):
+        from .kernels import get_kernels
+
+        self.p = p
+        self.kx = get_kernels()
+        self.A = _dense_A(p)
+        self.b = to_device(p.b)
+        self.N, self.n = self.A.shape
+
+    def at(self, x, z=None):
+        kx = self.kx
+        X = torch.stack([to_device(x)] + ([to_device(z)] if z is not None else [])).contiguous()
+        AX = kx.empty(X.shape[0], self.N)
+        kx.gemv(self.A, X, AX)
+        tg, w, thx, tnu = (kx.empty(self.N) for _ in range(4))
+        out = kx.zeros(8)
+        kx.ml_rowwise(self.p.loss.kind, AX[0], AX[1] if z is not None else None, self.b, tg, w, thx,
+                      tnu if z is not None else None, out)
+        return AX, tg, w, thx, tnu, out
+
+
+def ml_smooth_value(p: MLProblem, x) -> float:
+    """sum_i l(a_i'x - b_i) + (lambda2/2)||x||^2 (problems.py:227-230)."""
+    ev = _MLEval(p)
+    _, _, _, _, _, out = ev.at(x)
+    xt = to_device(x)
+    return float(out[0]) + 0.5 * p.lambda2 * float(torch.dot(xt, xt))
+
+
+def ml_objective(p: MLProblem, x) -> float:
+    return ml_smooth_value(p, x) + p.lambda1 * float(to_device(x).abs().sum())
+
+
+def ml_gradient(p: MLProblem, x):
+    """A' l'(Ax - b) + lambda2 x (problems.py:238-242)."""
+    ev = _MLEval(p)
+    _, tg, _, _, _, _ = ev.at(x)
+    g = ev.kx.empty(1, ev.n)
+    ev.kx.gemvT(ev.A, tg.view(1, -1), g)
+    g = g.view(-1)
+    ev.kx.axpby(p.lambda2, to_device(x), 1.0, g)
+    return like_input(g, x)
+
+
+class MLHessian(HessianOperator):
+    """A' diag(l''(Ax - b)) A + lambda2 I kept matrix-free (problems.py:245-273);
+    the product is the fused HVP kernel K3."""
+
+    def __init__(self, p: MLProblem, x=None):
+        super().__init__(p.n)
+        self.p = p
+        self.diag_shift = p.lambda2
+        self.is_constant = p.loss.deriv2_constant
+        self._A = _dense_A(p)
+        self._w = None
+        self.update(np.zeros(p.n) if x is None else x)
+
+    def update(self, x) -> None:
+        if self.p.loss.kind == "square":
+            self._w = None  # l'' == 1
+            return
+        ev = _MLEval(self.p)
+        _, _, w, _, _, _ = ev.at(x)
+        self._w = w
+
+    @property
+    def _weights(self):
+        if self._w is None:
+            return np.ones(self.p.N)
+        return self._w.cpu().numpy()
+
+    def _apply_dev(self, v):
+        from .kernels import get_kernels
+
+        kx = get_kernels()
+        y = kx.empty(self.input_dim)
+        kx.hvp(self._A, self._w, v, self.diag_shift, y, None, True)
+        return y
+
+    def _smooth_cols(self, V):
+        from .kernels import get_kernels
+
+        kx = get_kernels()
+        A = self._A
+        N, n = A.shape
+        s = V.shape[1]
+        Z = kx.empty(N, s)
+        kx.gemm(0, 0, N, s, n, 1.0, A, A.stride(0), V, V.stride(0), 0.0, Z, s)
+        if self._w is not None:
+            kx.row_scale(Z, self._w)
+        Y = kx.empty(n, s)
+        kx.gemm(1, 0, n, s, N, 1.0, A, A.stride(0), Z, s, 0.0, Y, s)
+        return Y
+
+    def smooth_part(self) -> LinearOperator:
+        """A' diag(w) A, the sketching target (problems.py:266-273)."""
+        from .kernels import get_kernels
+
+        def mv(v):
+            kx = get_kernels()
+            y = kx.empty(self.input_dim)
+            kx.hvp(self._A, self._w, to_device(v), 0.0, y, None, True)
+            return y
+
+        op = MatrixFreeOperator(self.input_dim, self.output_dim, mv, mv)
+        op.apply_columns_dev = self._smooth_cols
+        return op
+
+
+def ml_hessian_operator(p: MLProblem, x) -> MLHessian:
+    return MLHessian(p, x)
+
+
+def ml_x_system(p: MLProblem, x, z, u, rho: float, hess: Optional[MLHessian] = None):
+    """Matvec and right-hand side of the ML x-update (problems.py:280-303)."""
+    if hess is None:
+        hess = MLHessian(p, x)
+
+    def matvec(v):
+        vt = to_device(v)
+        return like_input(hess._apply_dev(vt) + rho * vt, v)
+
+    xt = to_device(x)
+    rhs = hess._apply_dev(xt) - to_device(ml_gradient(p, xt)) + rho * (to_device(z) - to_device(u))
+    return matvec, like_input(rhs, x)
+
+
+def ml_dual_point(p: MLProblem, x):
+    """nu = l'(Ax - b), scaled into ||A'nu||_inf <= lambda1 when lambda2 == 0
+    (problems.py:306-318)."""
+    ev = _MLEval(p)
+    AX, tg, _, _, _, _ = ev.at(x)
+    nu = tg
+    if p.lambda2 == 0.0:
+        at = ev.kx.empty(1, ev.n)
+        ev.kx.gemvT(ev.A, nu.view(1, -1), at)
+        denom = float(at.abs().max()) if at.numel() else 0.0
+        if denom > p.lambda1:
+            nu = nu * (p.lambda1 / denom)
+    return like_input(nu, x)
+
+
+def ml_dual_value(p: MLProblem, nu) -> float:
+    """Dual objective at nu; -inf outside the conjugate's domain (problems.py:321-332)."""
+    from .kernels import get_kernels
+
+    kx = get_kernels()
+    nut = to_device(nu)
+    b = to_device(p.b)
+    out = kx.zeros(4)
+    kx.ml_conj_scaled(p.loss.kind, nut, 1.0, b, out)
+    o = out.cpu().numpy()
+    if o[1] > 0:
+        return -np.inf
+    val = -float(o[0]) - float(o[2])
+    if p.lambda2 > 0.0:
+        A = _dense_A(p)
+        at = kx.empty(1, A.shape[1])
+        kx.gemvT(A, nut.view(1, -1), at)
+        excess = torch.clamp(at.abs() - p.lambda1, min=0.0)
+        val -= float(torch.sum(excess * excess)) / (2.0 * p.lambda2)
+    return val
+
+
+def ml_dual_gap(p: MLProblem, x) -> float:
+    """(primal - dual) / min(primal, |dual|) (problems.py:335-351)."""
+    nu = ml_dual_point(p, x)
+    primal = ml_objective(p, x)
+    dual = ml_dual_value(p, nu)
+    if not np.isfinite(dual):
+        return np.inf
+    num = primal - dual
+    denom = min(primal, abs(dual))
+    if denom <= 1e-16:
+        return 0.0 if abs(num) <= 1e-12 else np.inf
+    return num / denom

@@ -1,0 +1,118 @@
+"""Seeded inputs for the golden parity cases.
+
+Inputs are regenerated from seeds (NumPy PCG64 is bit-reproducible across
+machines with the same NumPy), so the committed fixtures hold only the
+reference's OUTPUTS.  ``make_golden.py`` feeds these inputs to the reference
+package; the tests feed the same inputs to the oracle and to the GPU path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2310_08333_b200 import datagen
+
+
+def random_psd(n, rng, rank=None, decay=None):
+    """Symmetric PSD matrix with a controlled spectrum (same construction as the
+    reference test oracle ``tests/_oracles.py:152-161``)."""
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    if decay is not None:
+        lam = np.asarray(decay, dtype=float)
+    elif rank is not None:
+        lam = np.concatenate([rng.uniform(0.5, 2.0, size=rank), np.zeros(n - rank)])
+    else:
+        lam = rng.uniform(0.1, 2.0, size=n)
+    return (Q * lam) @ Q.T
+
+
+# ---- solve cases: name -> dict(kind, builder) --------------------------------
+
+
+def _ml_small(kind, N, n, seed, lam2=0.0, lam_frac=0.1):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((N, n)) / np.sqrt(N)
+    xt = np.zeros(n)
+    sup = rng.choice(n, size=max(1, n // 10), replace=False)
+    xt[sup] = rng.standard_normal(sup.size)
+    if kind == "logistic":
+        y = np.where(rng.random(N) < 1.0 / (1.0 + np.exp(-(A @ xt) * 3.0)), 1.0, -1.0)
+        A = -y[:, None] * A
+        b = np.zeros(N)
+        lam1 = lam_frac * float(np.max(np.abs(A.T @ np.ones(N)))) / 2.0
+    else:
+        b = A @ xt + 0.05 * rng.standard_normal(N)
+        if kind == "huber":
+            idx = rng.choice(N, size=max(1, N // 20), replace=False)
+            b[idx] += 5.0
+        lam1 = lam_frac * float(np.max(np.abs(A.T @ b)))
+    return dict(loss=kind, A=A, b=b, lambda1=lam1, lambda2=lam2)
+
+
+def _qp_small(N, n, seed):
+    A, b, P, q = datagen.boxqp_data(N, n, seed)
+    return dict(P=P, q=q, lo=np.zeros(n), hi=np.ones(n))
+
+
+def _cfg(c):
+    d = datagen.make_config(c)
+    if d.kind == "boxqp":
+        return dict(P=d.P, q=d.q, lo=d.lo, hi=d.hi)
+    return dict(loss=d.loss, A=d.A, b=d.b, lambda1=d.lambda1, lambda2=d.lambda2)
+
+
+# name: (problem builder, options dict)
+SOLVE_CASES = {
+    "lasso_small": (lambda: _ml_small("square", 120, 200, 11), dict(sketch_rank=10, rng_seed=11)),
+    "lasso_tall": (lambda: _ml_small("square", 300, 80, 12), dict(sketch_rank=8, rng_seed=12)),
+    "enet_small": (lambda: _ml_small("square", 150, 120, 13, lam2=0.05), dict(sketch_rank=12, rng_seed=13)),
+    "logistic_small": (lambda: _ml_small("logistic", 300, 150, 14, lam2=1e-3, lam_frac=0.1), dict(sketch_rank=10, rng_seed=14)),
+    "logistic_l1only": (lambda: _ml_small("logistic", 200, 100, 15, lam2=0.0, lam_frac=0.2), dict(sketch_rank=8, rng_seed=15)),
+    "huber_small": (lambda: _ml_small("huber", 200, 100, 16), dict(sketch_rank=8, rng_seed=16)),
+    "lasso_noprec": (lambda: _ml_small("square", 120, 200, 17), dict(use_preconditioner=False, rng_seed=17)),
+    "lasso_linf": (lambda: _ml_small("square", 120, 200, 18), dict(sketch_rank=10, rng_seed=18, norm_kind="linf", use_dual_gap=False)),
+    "lasso_exact": (lambda: _ml_small("square", 100, 150, 19), dict(sketch_rank=10, rng_seed=19, exact_x_solve=True)),
+    "boxqp_small": (lambda: _qp_small(400, 200, 20), dict(sketch_rank=20, rng_seed=20)),
+    "cfg1": (lambda: _cfg(1), dict(sketch_rank=50, rng_seed=0)),
+    "cfg3": (lambda: _cfg(3), dict(sketch_rank=100, rng_seed=2)),
+    "cfg2": (lambda: _cfg(2), dict(sketch_rank=100, rng_seed=1)),
+    "cfg4": (lambda: _cfg(4), dict(sketch_rank=200, rng_seed=3)),
+}
+
+# tolerances of the configs: eps_abs = eps_rel = eps_dual_gap = 1e-4 (BASELINE.json)
+BASE_OPTIONS = dict(eps_abs=1e-4, eps_rel=1e-4, eps_dual_gap=1e-4)
+
+# cases the default generator run produces (cfg4 needs ~10 min of CPU: --big)
+DEFAULT_SOLVES = [k for k in SOLVE_CASES if k != "cfg4"]
+
+
+def options_for(name):
+    opts = dict(BASE_OPTIONS)
+    opts.update(SOLVE_CASES[name][1])
+    return opts
+
+
+# ---- kernel-level cases -------------------------------------------------------
+
+
+def hvp_case(seed=101, N=70, n=45):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((N, n))
+    b = rng.standard_normal(N)
+    x = rng.standard_normal(n) * 0.3
+    v = rng.standard_normal(n)
+    return A, b, x, v
+
+
+def sketch_case(seed=202, n=40, r=8):
+    rng = np.random.default_rng(seed)
+    return random_psd(n, rng, decay=np.logspace(1, -3, n)), r, 7
+
+
+def pcg_case(seed=303, n=30):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((2 * n, n))
+    H = A.T @ A + 0.7 * np.eye(n)
+    b = rng.standard_normal(n)
+    x0 = rng.standard_normal(n) * 0.1
+    return H, b, x0

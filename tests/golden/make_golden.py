@@ -1,0 +1,145 @@
+"""Generate the golden fixtures by running the REFERENCE package itself.
+
+Run in the development container (the only place ``/root/reference`` exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py          # default cases
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py --big    # + config 4 (~10 min)
+
+It imports ``nysopt`` from ``/root/reference/pkg/src`` (read-only, no install),
+feeds it the seeded inputs of ``tests/golden/cases.py`` and stores only the
+outputs as compressed ``.npz`` files next to this script.  Nothing on the GPU
+box reads ``/root/reference``: the tests there use these committed fixtures.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import nysopt  # noqa: E402  (the reference)
+from nysopt import (  # noqa: E402
+    Box,
+    DenseOperator,
+    IdentityOperator,
+    MLProblem,
+    NystromPreconditioner,
+    QPProblem,
+    SolverOptions,
+    builtin_loss,
+    nystrom_sketch,
+    pcg,
+)
+from nysopt.problems import MLHessian, ml_dual_gap, ml_gradient, ml_objective  # noqa: E402
+
+import cases  # noqa: E402
+
+
+def ref_problem(spec):
+    if "P" in spec:
+        n = spec["P"].shape[0]
+        return QPProblem(DenseOperator(spec["P"]), spec["q"], IdentityOperator(n), Box(spec["lo"], spec["hi"]))
+    return MLProblem(builtin_loss(spec["loss"]), spec["A"], spec["b"], spec["lambda1"], spec["lambda2"])
+
+
+def run_solve(name):
+    spec = cases.SOLVE_CASES[name][0]()
+    opts = SolverOptions(**cases.options_for(name))
+    t0 = time.perf_counter()
+    res = nysopt.solve(ref_problem(spec), opts)
+    dt = time.perf_counter() - t0
+    hist = res.history
+    out = dict(
+        x=res.x,
+        z=res.z,
+        u=res.u,
+        objective=np.float64(res.objective),
+        iterations=np.int64(res.iterations),
+        status=np.array(res.status.value),
+        rp_norm=np.float64(res.rp_norm),
+        rd_norm=np.float64(res.rd_norm),
+        gap=np.float64(np.nan if res.gap is None else res.gap),
+        cg_iters=np.array([h.cg_iters for h in hist], dtype=np.int64),
+        cg_tol=np.array([h.cg_tol for h in hist]),
+        rho=np.array([h.rho for h in hist]),
+        obj_hist=np.array([h.objective for h in hist]),
+        rp_hist=np.array([h.rp_norm for h in hist]),
+        rd_hist=np.array([h.rd_norm for h in hist]),
+        gap_hist=np.array([np.nan if h.gap is None else h.gap for h in hist]),
+        penalty_events=np.array([[e.k, e.rho_old, e.rho_new, e.dual_jump_rel] for e in res.penalty_events]).reshape(-1, 4),
+        x_bar=res.x_bar if res.x_bar is not None else np.zeros(0),
+        z_bar=res.z_bar if res.z_bar is not None else np.zeros(0),
+        ref_total_s=np.float64(dt),
+        ref_setup_s=np.float64(res.timings.setup_s),
+        ref_precond_s=np.float64(res.timings.precond_s),
+        ref_linsys_s=np.float64(res.timings.linsys_total_s),
+    )
+    if "A" in spec:
+        p = ref_problem(spec)
+        out["ml_objective_z"] = np.float64(ml_objective(p, res.z))
+    np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), **out)
+    print(f"{name}: iters={res.iterations} status={res.status.value} obj={res.objective:.12e} "
+          f"cg={int(out['cg_iters'].sum())} t={dt:.2f}s", flush=True)
+
+
+def run_kernels():
+    # fused HVP / gradient / gap at a logistic point (problems.py:238-351)
+    A, b, x, v = cases.hvp_case()
+    out = {}
+    for loss in ("square", "logistic", "huber"):
+        for lam2 in (0.0, 0.3):
+            p = MLProblem(builtin_loss(loss), A, b, 0.7, lam2)
+            H = MLHessian(p, x)
+            key = f"{loss}_{lam2}"
+            out[f"hvp_{key}"] = H.apply(v)
+            out[f"w_{key}"] = H._weights
+            out[f"grad_{key}"] = ml_gradient(p, x)
+            out[f"obj_{key}"] = np.float64(ml_objective(p, x))
+            out[f"gap_{key}"] = np.float64(ml_dual_gap(p, x))
+    np.savez_compressed(os.path.join(HERE, "kernels_ml.npz"), **out)
+
+    # Nystrom sketch + preconditioner (sketch.py:74-151)
+    M, r, seed = cases.sketch_case()
+    S = nystrom_sketch(DenseOperator(M), r, rng_seed=seed)
+    pc = NystromPreconditioner(S, nu=0.5)
+    rng = np.random.default_rng(9)
+    V = rng.standard_normal((M.shape[0], 5))
+    PV = np.column_stack([pc.apply(V[:, j]) for j in range(5)])
+    np.savez_compressed(os.path.join(HERE, "kernels_sketch.npz"), U=S.U, lam=S.lambda_hat, V=V, PV=PV)
+
+    # PCG with and without the preconditioner (krylov.py:35-95)
+    H, bb, x0 = cases.pcg_case()
+    S2 = nystrom_sketch(DenseOperator(H - 0.7 * np.eye(H.shape[0])), 6, rng_seed=4)
+    pc2 = NystromPreconditioner(S2, nu=0.7)
+    x1, rep1 = pcg(DenseOperator(H), bb, x0=x0, tol_rel=1e-10)
+    x2, rep2 = pcg(DenseOperator(H), bb, x0=x0, Minv=pc2.apply, tol_rel=1e-10)
+    np.savez_compressed(
+        os.path.join(HERE, "kernels_pcg.npz"),
+        x_plain=x1, it_plain=np.int64(rep1.iterations), x_prec=x2, it_prec=np.int64(rep2.iterations),
+    )
+    print("kernel fixtures written", flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true", help="also run config 4 (~10 min)")
+    ap.add_argument("--only", nargs="*", default=None)
+    args = ap.parse_args()
+    names = args.only if args.only else list(cases.DEFAULT_SOLVES) + (["cfg4"] if args.big else [])
+    if not args.only:
+        run_kernels()
+    for name in names:
+        run_solve(name)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+"""Kernel-level parity of the C-ABI kernels against NumPy / the oracle.
+
+Integer-free FP64 work: tolerances are stated per test (relative ~1e-12 for
+single products, looser where the reference test uses looser ones)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from conftest import load_golden  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def kx():
+    from paper_2310_08333_b200.kernels import get_kernels
+
+    return get_kernels()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+SHAPES = [(1, 1), (3, 5), (7, 129), (64, 64), (1000, 2000), (37, 1001), (5000, 333), (130, 10000)]
+
+
+@pytest.mark.parametrize("rows,n", SHAPES)
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_gemv_multi_rhs(kx, rows, n, k):
+    g = np.random.default_rng(rows * 7 + n + k)
+    A = g.standard_normal((rows, n))
+    X = g.standard_normal((k, n))
+    Y = kx.empty(k, rows)
+    kx.gemv(dev(A), dev(X), Y)
+    ref = X @ A.T
+    np.testing.assert_allclose(Y.cpu().numpy(), ref, rtol=1e-12, atol=1e-12 * np.abs(A).sum(1).max())
+
+
+@pytest.mark.parametrize("rows,n", SHAPES)
+@pytest.mark.parametrize("k", [1, 3])
+def test_gemvT_multi_rhs(kx, rows, n, k):
+    g = np.random.default_rng(rows * 3 + n + k)
+    A = g.standard_normal((rows, n))
+    T = g.standard_normal((k, rows))
+    Y = kx.empty(k, n)
+    kx.gemvT(dev(A), dev(T), Y)
+    ref = T @ A
+    np.testing.assert_allclose(Y.cpu().numpy(), ref, rtol=1e-12, atol=1e-12 * np.abs(A).sum(0).max())
+
+
+def test_gemv_odd_leading_dim(kx):
+    g = np.random.default_rng(5)
+    big = g.standard_normal((50, 77))
+    At = dev(big)[:, :75]  # lda = 77 (odd), misaligned rows
+    A = big[:, :75]
+    x = g.standard_normal((2, 75))
+    Y = kx.empty(2, 50)
+    kx.gemv(At, dev(x), Y)
+    np.testing.assert_allclose(Y.cpu().numpy(), x @ A.T, rtol=1e-12, atol=1e-12)
+    t = g.standard_normal((1, 50))
+    Z = kx.empty(1, 75)
+    kx.gemvT(At, dev(t), Z)
+    np.testing.assert_allclose(Z.cpu().numpy(), t @ A, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("rows,n", [(70, 45), (1000, 2000), (5000, 3000), (33, 7)])
+def test_hvp_fused(kx, rows, n):
+    g = np.random.default_rng(n)
+    A = g.standard_normal((rows, n))
+    d = g.uniform(0.1, 1.0, rows)
+    v = g.standard_normal(n)
+    y = kx.empty(n)
+    pAp = kx.zeros(1)
+    kx.hvp(dev(A), dev(d), dev(v), 0.7, y, pAp, True)
+    ref = A.T @ (d * (A @ v)) + 0.7 * v
+    np.testing.assert_allclose(y.cpu().numpy(), ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
+    assert abs(float(pAp) - v @ ref) <= 1e-11 * abs(v @ ref)
+    # partial form (row shard) + finish
+    y2 = kx.empty(n)
+    kx.hvp(dev(A), None, dev(v), 0.0, y2, None, False)
+    kx.shift_dot(dev(v), 0.3, y2, pAp)
+    ref2 = A.T @ (A @ v) + 0.3 * v
+    np.testing.assert_allclose(y2.cpu().numpy(), ref2, rtol=1e-11, atol=1e-11 * np.abs(ref2).max())
+
+
+def test_hvp_matches_reference_golden(kx):
+    """MLHessian.apply of the reference (problems.py:263-264) at a fixed point."""
+    from cases import hvp_case
+    from paper_2310_08333_b200 import MLProblem, builtin_loss
+    from paper_2310_08333_b200.problems import MLHessian, ml_dual_gap, ml_gradient, ml_objective
+
+    gold = load_golden("kernels_ml.npz")
+    A, b, x, v = hvp_case()
+    for loss in ("square", "logistic", "huber"):
+        for lam2 in (0.0, 0.3):
+            key = f"{loss}_{lam2}"
+            p = MLProblem(builtin_loss(loss), A, b, 0.7, lam2)
+            H = MLHessian(p, x)
+            np.testing.assert_allclose(H.apply(v), gold[f"hvp_{key}"], rtol=1e-11, atol=1e-11)
+            np.testing.assert_allclose(ml_gradient(p, x), gold[f"grad_{key}"], rtol=1e-11, atol=1e-11)
+            assert abs(ml_objective(p, x) - gold[f"obj_{key}"]) <= 1e-12 * abs(gold[f"obj_{key}"])
+            gg = float(gold[f"gap_{key}"])
+            got = ml_dual_gap(p, x)
+            if np.isfinite(gg):
+                assert abs(got - gg) <= 1e-9 * max(1.0, abs(gg)), (key, got, gg)
+            else:
+                assert not np.isfinite(got)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(5, 3, 7), (130, 70, 257), (1000, 133, 2000), (133, 133, 10000), (64, 64, 16)])
+def test_dgemm_dmma(kx, ta, tb, M, N, K):
+    g = np.random.default_rng(M + N + K + 10 * ta + tb)
+    A = g.standard_normal((K, M) if ta else (M, K))
+    B = g.standard_normal((N, K) if tb else (K, N))
+    C0 = g.standard_normal((M, N))
+    Cd = dev(C0)
+    kx.gemm(ta, tb, M, N, K, 1.5, dev(A), A.shape[1], dev(B), B.shape[1], 0.5, Cd, N)
+    ref = 1.5 * (A.T if ta else A) @ (B.T if tb else B) + 0.5 * C0
+    np.testing.assert_allclose(Cd.cpu().numpy(), ref, rtol=1e-11, atol=1e-12 * np.sqrt(K) * 10)
+
+
+@pytest.mark.parametrize("s", [1, 2, 5, 33, 133, 258])
+def test_syevj(kx, s):
+    g = np.random.default_rng(s)
+    Q, _ = np.linalg.qr(g.standard_normal((s, s)))
+    lam = np.concatenate([g.uniform(0.1, 10.0, s - s // 4), -g.uniform(0.1, 1.0, s // 4)])
+    M = (Q * lam) @ Q.T
+    M = 0.5 * (M + M.T)
+    V = kx.empty(s, s)
+    w = kx.empty(s)
+    kx.syevj(dev(M), V, w)
+    wn = w.cpu().numpy()
+    Vn = V.cpu().numpy()
+    np.testing.assert_allclose(wn, np.sort(lam)[::-1], rtol=1e-11, atol=1e-12 * 10)
+    np.testing.assert_allclose(Vn.T @ Vn, np.eye(s), atol=1e-12 * s)
+    np.testing.assert_allclose(M @ Vn, Vn * wn, atol=1e-11 * 10)
+
+
+def test_orthonormalize_spans_omega(kx):
+    g = np.random.default_rng(1)
+    Om = g.standard_normal((2000, 70))
+    Q = kx.empty(2000, 70)
+    kx.orthonormalize(dev(Om), Q)
+    Qn = Q.cpu().numpy()
+    np.testing.assert_allclose(Qn.T @ Qn, np.eye(70), atol=1e-13)
+    Qh, _ = np.linalg.qr(Om)
+    # same range: projector equality
+    np.testing.assert_allclose(Qn @ (Qn.T @ Om), Om, atol=1e-11)
+    np.testing.assert_allclose(np.abs(Qh.T @ Qn).sum(0).min() >= 0.0, True)
+
+
+def test_sketch_matches_reference_golden():
+    """nystrom_sketch on the reference's fixture: eigenvalues to 1e-10 and the
+    preconditioner apply (Eq. 11) to 1e-10 (test_sketch.py:113-120 tolerance)."""
+    from cases import sketch_case
+    from paper_2310_08333_b200 import DenseOperator, NystromPreconditioner, nystrom_sketch
+
+    gold = load_golden("kernels_sketch.npz")
+    M, r, seed = sketch_case()
+    S = nystrom_sketch(DenseOperator(M), r, rng_seed=seed)
+    np.testing.assert_allclose(S.lambda_hat, gold["lam"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(np.abs(S.U.T @ gold["U"]), np.eye(r), atol=1e-8)
+    pc = NystromPreconditioner(S, nu=0.5)
+    PV = np.column_stack([pc.apply(gold["V"][:, j]) for j in range(gold["V"].shape[1])])
+    np.testing.assert_allclose(PV, gold["PV"], rtol=1e-10, atol=1e-10)
+
+
+def test_pcg_matches_reference_golden():
+    from cases import pcg_case
+    from paper_2310_08333_b200 import DenseOperator, NystromPreconditioner, nystrom_sketch, pcg
+
+    gold = load_golden("kernels_pcg.npz")
+    H, b, x0 = pcg_case()
+    S2 = nystrom_sketch(DenseOperator(H - 0.7 * np.eye(H.shape[0])), 6, rng_seed=4)
+    pc2 = NystromPreconditioner(S2, nu=0.7)
+    x1, rep1 = pcg(DenseOperator(H), b, x0=x0, tol_rel=1e-10)
+    x2, rep2 = pcg(DenseOperator(H), b, x0=x0, Minv=pc2.apply, tol_rel=1e-10)
+    assert rep1.iterations == int(gold["it_plain"])
+    assert abs(rep2.iterations - int(gold["it_prec"])) <= 1
+    np.testing.assert_allclose(x1, gold["x_plain"], rtol=1e-8, atol=1e-10)
+    np.testing.assert_allclose(x2, gold["x_prec"], rtol=1e-8, atol=1e-10)
+
+
+def test_precond_kat():
+    """precond diag(2,1), nu = 1 applied to (1,1) -> (2/3, 1) (test_sketch.py:100-104)."""
+    from paper_2310_08333_b200 import DenseOperator, NystromPreconditioner, nystrom_sketch, precond_apply
+
+    S = nystrom_sketch(DenseOperator(np.diag([2.0, 1.0])), 2, rng_seed=0)
+    P = NystromPreconditioner(S, nu=1.0)
+    np.testing.assert_allclose(precond_apply(P, np.array([1.0, 1.0])), [2.0 / 3.0, 1.0], atol=1e-7)
+
+
+def test_non_psd_sketch_rejected():
+    from paper_2310_08333_b200 import DataError, DenseOperator, nystrom_sketch
+
+    with pytest.raises(DataError):
+        nystrom_sketch(DenseOperator(np.diag([1.0, -1.0, 0.5])), 3, rng_seed=0)
+
+
+def test_exact_rank_recovery():
+    from paper_2310_08333_b200 import DenseOperator, nystrom_sketch
+
+    A = np.diag([3.0, 2.0, 0.0, 0.0])
+    S = nystrom_sketch(DenseOperator(A), 2, rng_seed=0)
+    assert np.allclose(sorted(S.lambda_hat, reverse=True), [3.0, 2.0], atol=1e-7)
+    assert np.allclose(S.to_dense(), A, atol=1e-7)
+
+
+def test_pcg_kats():
+    from paper_2310_08333_b200 import DenseOperator, NotSPDError, pcg
+
+    x, rep = pcg(DenseOperator(np.eye(3)), np.array([1.0, 2.0, 3.0]), tol_rel=1e-12)
+    assert rep.iterations == 1 and rep.converged
+    np.testing.assert_allclose(x, [1, 2, 3], atol=1e-12)
+    x, rep = pcg(DenseOperator(np.diag([1.0, 100.0])), np.ones(2), tol_rel=1e-10)
+    assert rep.iterations <= 2
+    np.testing.assert_allclose(x, [1.0, 0.01], atol=1e-9)
+    x, rep = pcg(DenseOperator(np.eye(4)), np.zeros(4))
+    assert np.array_equal(x, np.zeros(4)) and rep.iterations == 0
+    with pytest.raises(NotSPDError):
+        pcg(DenseOperator(np.diag([1.0, -1.0])), np.ones(2), tol_rel=1e-12)
