@@ -1,0 +1,323 @@
+"""Benchmark of the B200 inexact-ADMM hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+Workload (N=1): BASELINE.json configs[1] = config 2, dense elastic-net
+logistic regression, A 5000 x 10000 FP64 (400 MB, larger than the 126 MB L2,
+so no L2 flush is needed between steps), Nystrom rank 100, tolerances 1e-4.
+A step is one complete ``solve`` to tolerance (358 ADMM iterations, 18
+Nystrom sketches).  ``value`` = ADMM iterations/s over the timed steps with A
+already resident in HBM; ``e2e`` = the same metric through the public API with
+A in pinned host memory, uploaded inside every step, results read back.
+N > 1 (torchrun): A is row-sharded over the ranks with NCCL all-reduces of the
+A^T partials (strong scaling: total work fixed).
+
+``--impl reference`` times the reference algorithm on the host CPU (the
+pinned NumPy oracle, oracle/port.py -- the Python reference cannot travel to
+the GPU box) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CPU_SAMPLE_ITERS = 60  # 3 sketches per 60 iterations, the full solve's sketch density
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 8:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def build_problem(cfg: int, A_op=None):
+    import paper_2310_08333_b200 as nys
+    from paper_2310_08333_b200 import datagen
+
+    d = datagen.make_config(cfg)
+    opts = nys.SolverOptions(sketch_rank=d.rank, rng_seed=d.seed, eps_abs=1e-4, eps_rel=1e-4, eps_dual_gap=1e-4)
+    return d, opts
+
+
+def make_gpu_problem(d, A):
+    import paper_2310_08333_b200 as nys
+
+    if d.kind == "boxqp":
+        n = d.P.shape[0]
+        return nys.QPProblem(nys.DenseOperator(A), d.q, nys.IdentityOperator(n), nys.Box(d.lo, d.hi))
+    return nys.MLProblem(nys.builtin_loss(d.loss), nys.DenseOperator(A), d.b, d.lambda1, d.lambda2)
+
+
+def cpu_reference_rate(d, opts_gpu, max_iter, reps=1):
+    """The reference algorithm on the host (oracle port) over a bounded sample."""
+    from oracle import port
+
+    if d.kind == "boxqp":
+        prob = port.QPSpec(d.P, d.q, d.lo, d.hi)
+    else:
+        prob = port.MLSpec(d.loss, d.A, d.b, d.lambda1, d.lambda2)
+    o = port.Options(sketch_rank=opts_gpu.sketch_rank, rng_seed=opts_gpu.rng_seed, eps_abs=1e-4, eps_rel=1e-4,
+                     eps_dual_gap=1e-4, max_iter=max_iter)
+    times, iters = [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = port.solve(prob, o)
+        times.append(time.perf_counter() - t0)
+        iters.append(r.iterations)
+    return times, iters
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        return max((i.get("num_threads", 1) for i in info if i.get("user_api") == "blas"), default=os.cpu_count())
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    d, opts = build_problem(args.config)
+    sample = min(CPU_SAMPLE_ITERS, 10**9)
+    cpu_reference_rate(d, opts, sample, reps=max(0, min(args.warmup, 1)))  # warm caches / BLAS threads
+    times, iters = cpu_reference_rate(d, opts, sample, reps=args.steps)
+    tot_t, tot_i = sum(times), sum(iters)
+    value = tot_i / tot_t
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": "ADMM iters/s", "value": value, "unit": "iters/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(args, d, world),
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
+                         "sample": f"first {sample} ADMM iterations of config {args.config} per step "
+                                   f"(3 Nystrom sketches, same density as the full solve), NumPy/OpenBLAS"},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, d, world):
+    n = d.P.shape[0] if d.kind == "boxqp" else d.A.shape[1]
+    N = d.A.shape[0]
+    return {"workload": f"config {args.config}: {d.kind} {N}x{n} FP64, rank {d.rank}, tol 1e-4, solve to tolerance",
+            "config_index": args.config, "rows": N, "features": n, "sketch_rank": d.rank,
+            "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+            "l2_policy": "A (%.0f MB) larger than the 126 MB L2; no flush" % (8 * N * n / 1e6)}
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = _env_rank()
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    import paper_2310_08333_b200 as nys
+    from paper_2310_08333_b200.kernels import get_kernels
+
+    d, opts = build_problem(args.config)
+    host_A = d.P if d.kind == "boxqp" else d.A
+    kx = get_kernels()
+    # A resident in HBM for the kernel-side metric (each rank: its row shard inside solve)
+    A_dev = torch.from_numpy(host_A).cuda()
+    prob = make_gpu_problem(d, A_dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def maxred(x):
+        if world > 1:
+            t = torch.tensor([x], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            return float(t)
+        return x
+
+    for _ in range(args.warmup):
+        res = nys.solve(prob, opts)
+    # timed region
+    kx.timed_name = args.profile_kernel
+    kx.events = []
+    launches0 = kx.kernel_launches()
+    iters = 0
+    barrier()
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            res = nys.solve(prob, opts)
+            iters += res.iterations
+        e1.record(st)
+        barrier()
+    el_ms = maxred(e0.elapsed_time(e1))
+    launches = kx.kernel_launches() - launches0
+    ktimes = kx.event_times_ms()
+    kx.timed_name = None
+    value = iters / (el_ms / 1e3)
+    tts = el_ms / 1e3 / args.steps
+
+    # roofline of the dominant kernel (HVP, K3): algorithmic bytes per launch
+    N_loc = A_dev.shape[0] if d.kind == "boxqp" else res.device_stats.get("rows", d.A.shape[0] // world)
+    n = host_A.shape[1]
+    peak, peak_kind = _peaks()
+    roof = None
+    if ktimes:
+        avg_ms = sum(ktimes) / len(ktimes)
+        rows_loc = d.A.shape[0] // world if d.kind != "boxqp" else n
+        alg_bytes = 8 * rows_loc * n + 8 * (2 * n + rows_loc)
+        achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get(f"cfg{args.config}_{args.profile_kernel}")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": args.profile_kernel, "achieved": achieved, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "launches_timed": len(ktimes),
+                "share_of_step": sum(ktimes) / el_ms}
+
+    # e2e: public API with host buffers (pinned), upload + readback inside each step
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(host_A).pin_memory()
+        host_view = pinned.numpy()
+        kx.h2d = kx.d2h = 0
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        e_iters = 0
+        t0.record(st)
+        for _ in range(max(1, args.steps)):
+            p2 = make_gpu_problem(d, host_view)
+            r2 = nys.solve(p2, opts)
+            e_iters += r2.iterations
+        t1.record(st)
+        barrier()
+        e_ms = maxred(t0.elapsed_time(t1))
+        steps_e = max(1, args.steps)
+        a_bytes = host_A.nbytes // world
+        b_bytes = 0 if d.kind == "boxqp" else d.b.nbytes // world
+        e2e = {"value": e_iters / (e_ms / 1e3), "unit": "iters/s",
+               "h2d_bytes_per_step": int(a_bytes + b_bytes + kx.h2d / steps_e),
+               "d2h_bytes_per_step": int(kx.d2h / steps_e), "time_to_tolerance_s": e_ms / 1e3 / steps_e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        times, its = cpu_reference_rate(d, opts, CPU_SAMPLE_ITERS, reps=1)
+        cpu = {"value": its[0] / times[0], "unit": "iters/s", "cores": blas_threads(), "kind": "port",
+               "sample": f"first {CPU_SAMPLE_ITERS} ADMM iterations of config {args.config} (oracle port, "
+                         f"NumPy/OpenBLAS, {times[0]:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "ADMM iters/s", "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(config_block(args, d, world), time_to_tolerance_s=tts, iterations=res.iterations,
+                           status=res.status.value, objective=res.objective, sketches=res.device_stats.get("sketches")),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--profile-kernel", default="hvp", choices=["hvp", "gemv", "gemvT"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

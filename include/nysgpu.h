@@ -67,6 +67,8 @@ int nys_abi_version(void);
 const char* nys_status_string(int status);
 /* NYS_OK when a compute-capability-10.x device is current */
 int nys_device_check(void);
+/* number of kernels launched by this library since load (instrumentation) */
+unsigned long long nys_launch_count(void);
 /* bytes of the generic reduction workspace used by the vector kernels */
 size_t nys_reduce_workspace(void);
 
@@ -202,6 +204,15 @@ size_t nys_gemm_workspace(int64_t M, int64_t N, int64_t K);
 int nys_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
                  const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                  double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+/* The raw Gaussian test matrix itself (sketch.py:97-98): fills out[0..count)
+ * with exactly np.random.Generator(PCG64).standard_normal(count) continued
+ * from the given 128-bit PCG64 (state, inc) -- for default_rng(seed) that is
+ * np.random.PCG64(seed).state.  PCG64 jump-ahead + NumPy's ziggurat with a
+ * parallel resolution of the variable draw consumption.  Synchronises `stream`;
+ * returns NYS_ERR_NONFINITE if the draw buffer was exhausted (never expected). */
+size_t nys_gaussian_workspace(int64_t count);
+int nys_gaussian_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                     int64_t count, double* out, void* ws, size_t ws_bytes, void* stream);
 /* Orthonormalise the raw Gaussian test matrix (sketch.py:97-99) by CholeskyQR2:
  * Q (n x s, row-major) spans the same range as Omega.  Synchronises `stream`. */
 size_t nys_orthonormalize_workspace(int64_t n, int s);

@@ -46,6 +46,7 @@ SIGNATURES = {
     "nys_abi_version": (I32, []),
     "nys_status_string": (C.c_char_p, [I32]),
     "nys_device_check": (I32, []),
+    "nys_launch_count": (C.c_ulonglong, []),
     "nys_reduce_workspace": (SZ, []),
     "nys_gemv_workspace": (SZ, [I64, I64, I32]),
     "nys_gemv_f64": (I32, [P, I64, I64, I64, P, I64, I32, P, I64, P, SZ, P]),
@@ -74,6 +75,8 @@ SIGNATURES = {
     "nys_row_scale_f64": (I32, [I64, I64, P, I64, P, P]),
     "nys_gemm_workspace": (SZ, [I64, I64, I64]),
     "nys_gemm_f64": (I32, [I32, I32, I64, I64, I64, F64, P, I64, P, I64, F64, P, I64, P, SZ, P]),
+    "nys_gaussian_workspace": (SZ, [I64]),
+    "nys_gaussian_f64": (I32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, I64, P, P, SZ, P]),
     "nys_orthonormalize_workspace": (SZ, [I64, I32]),
     "nys_orthonormalize_f64": (I32, [I64, I32, P, P, P, SZ, P]),
     "nys_nystrom_workspace": (SZ, [I64, I32, I32]),

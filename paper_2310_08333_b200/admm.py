@@ -307,6 +307,7 @@ class _Engine:
         h[:_S_LEN].copy_(self.stats, non_blocking=True)
         if self.is_ml:
             h[_S_LEN:_S_LEN + 5].copy_(self.rowsums[:5], non_blocking=True)
+        self.kx.d2h += (_S_LEN + 5) * 8
         self.kx.sync()
         return h.numpy().copy()
 
@@ -555,7 +556,6 @@ class _Engine:
                     win.clear()
                     self._win_append(win)
 
-        timings.total_s = time.perf_counter() - t_start
         x = self.x.cpu().numpy()
         z = self.z.cpu().numpy()
         u = self.u.cpu().numpy()
@@ -563,6 +563,8 @@ class _Engine:
         if bar_count > 0:
             x_bar = self.xbar.cpu().numpy() / bar_count
             z_bar = self.zbar.cpu().numpy() / bar_count
+        kx.d2h += 5 * n * 8
+        timings.total_s = time.perf_counter() - t_start
         return SolveResult(
             status=status, x=x, z=z, u=u, objective=last_obj, iterations=k_done,
             rp_norm=res.rp_norm, rd_norm=res.rd_norm, history=history, timings=timings,

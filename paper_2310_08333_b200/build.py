@@ -50,8 +50,17 @@ def _needs(obj, src):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+GEN = os.path.join(OBJ, "gen")
+NVCC_FLAGS += ["-I", GEN]
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    tables = os.path.join(GEN, "zig_tables.h")
+    if force or not os.path.exists(tables):
+        from .gen_tables import write_header
+
+        write_header(tables)
     cc = nvcc()
     jobs = []
     objs = []

@@ -9,8 +9,14 @@
 #include <stdint.h>
 #include "../../include/nysgpu.h"
 
+namespace nys {
+// Number of kernels this library has launched (reported as gpu_launches).
+extern unsigned long long g_launches;
+}
+
 #define NYS_CHECK_LAUNCH()                                   \
   do {                                                       \
+    __atomic_fetch_add(&nys::g_launches, 1ull, __ATOMIC_RELAXED); \
     cudaError_t _e = cudaGetLastError();                     \
     if (_e != cudaSuccess) return NYS_ERR_CUDA;              \
   } while (0)

@@ -526,6 +526,7 @@ static int syevj(int s, double* A, double* V, double* w, void* ws, size_t ws_byt
                   (void*)&rot, (void*)&sweeps};
   if (cudaLaunchCooperativeKernel((void*)jacobi_kernel, blocks, 256, args, 0, st) != cudaSuccess)
     return NYS_ERR_CUDA;
+  __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
   jacobi_finish_kernel<<<1, 1024, s * sizeof(double), st>>>(s, A, Vt, wtmp, V, w);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
@@ -771,7 +772,13 @@ extern "C" int nys_syevj_f64(int s, double* A, double* V, double* w, void* ws, s
 }
 
 // ------------------------------------------------------------- misc -------
+unsigned long long nys::g_launches = 0ull;
+
 extern "C" int nys_abi_version(void) { return NYS_ABI_VERSION; }
+
+extern "C" unsigned long long nys_launch_count(void) {
+  return __atomic_load_n(&nys::g_launches, __ATOMIC_RELAXED);
+}
 
 extern "C" const char* nys_status_string(int status) {
   switch (status) {

@@ -35,7 +35,33 @@ class Kernels:
         self.sp = self.stream.cuda_stream
         self._ws: dict[str, torch.Tensor] = {}
         self.red = self.workspace("red", self.L.nys_reduce_workspace())
-        self.launches = 0
+        self.launches = 0  # C-ABI calls (each launches >= 1 kernel)
+        # instrumentation: CUDA-event timing of one kernel family, host<->device bytes
+        self.timed_name: Optional[str] = None
+        self.events: list = []
+        self.h2d = 0
+        self.d2h = 0
+
+    def kernel_launches(self) -> int:
+        """Kernels launched by libnysgpu so far (all instances in this process)."""
+        return int(self.L.nys_launch_count())
+
+    def _t0(self, name):
+        if self.timed_name != name:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def _t1(self, e) -> None:
+        if e is not None:
+            e2 = torch.cuda.Event(enable_timing=True)
+            e2.record(self.stream)
+            self.events.append((e, e2))
+
+    def event_times_ms(self) -> list:
+        self.sync()
+        return [a.elapsed_time(b) for a, b in self.events]
 
     # ------------------------------------------------------------ memory --
     def workspace(self, name: str, nbytes: int) -> torch.Tensor:
@@ -63,8 +89,10 @@ class Kernels:
         k = X.shape[0]
         ws = self.workspace("gemv", self.L.nys_gemv_workspace(rows, n, k))
         self.launches += 1
+        e = self._t0("gemv")
         check(self.L.nys_gemv_f64(A.data_ptr(), rows, n, A.stride(0), X.data_ptr(), X.stride(0), k,
                                   Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(), self.sp), "gemv")
+        self._t1(e)
 
     def gemvT(self, A: torch.Tensor, T: torch.Tensor, Y: torch.Tensor) -> None:
         """Y[j] = A^T T[j] for the k rows of T (k <= 4)."""
@@ -72,16 +100,20 @@ class Kernels:
         k = T.shape[0]
         ws = self.workspace("gemvT", self.L.nys_gemvT_workspace(rows, n, k))
         self.launches += 1
+        e = self._t0("gemvT")
         check(self.L.nys_gemvT_f64(A.data_ptr(), rows, n, A.stride(0), T.data_ptr(), T.stride(0), k,
                                    Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(), self.sp), "gemvT")
+        self._t1(e)
 
     def hvp(self, A, d, v, shift, y, pAp=None, finish=True) -> None:
         rows, n = A.shape
         ws = self.workspace("hvp", self.L.nys_hvp_workspace(rows, n))
         self.launches += 1
+        e = self._t0("hvp")
         check(self.L.nys_hvp_f64(A.data_ptr(), rows, n, A.stride(0), _p(d), v.data_ptr(), float(shift),
                                  y.data_ptr(), _p(pAp), 1 if finish else 0, ws.data_ptr(), ws.numel(),
                                  self.sp), "hvp")
+        self._t1(e)
 
     def shift_dot(self, v, shift, y, dot=None) -> None:
         self.launches += 1
@@ -196,6 +228,19 @@ class Kernels:
         check(self.L.nys_gemm_f64(int(ta), int(tb), M, N, K, float(alpha), A.data_ptr(), lda, B.data_ptr(),
                                   ldb, float(beta), Cm.data_ptr(), ldc, ws.data_ptr(), ws.numel(), self.sp),
               "gemm")
+
+    def gaussian(self, seed: int, out: torch.Tensor) -> None:
+        """out <- np.random.default_rng(seed).standard_normal(out.shape), generated on the GPU."""
+        import numpy as np
+
+        st = np.random.PCG64(seed).state["state"]
+        s, inc = int(st["state"]), int(st["inc"])
+        m64 = (1 << 64) - 1
+        count = out.numel()
+        ws = self.workspace("gauss", self.L.nys_gaussian_workspace(count))
+        self.launches += 1
+        check(self.L.nys_gaussian_f64(s >> 64, s & m64, inc >> 64, inc & m64, count, out.data_ptr(),
+                                      ws.data_ptr(), ws.numel(), self.sp), "gaussian")
 
     def orthonormalize(self, Om, Q) -> None:
         n, s = Om.shape

@@ -63,6 +63,7 @@ class CgWork:
 
     def read(self) -> np.ndarray:
         self.host.copy_(self.sc, non_blocking=True)
+        self.kx.d2h += self.host.numel() * 8
         self.kx.sync()
         return self.host.numpy()
 

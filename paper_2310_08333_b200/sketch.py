@@ -59,8 +59,12 @@ def sketch_device(kx, apply_cols: Callable[[torch.Tensor], torch.Tensor], n: int
         raise DataError(f"sketch rank must satisfy 1 <= r <= {n}, got {r}")
     s = sketch_width(n, r, oversample)
     if omega is None:
-        omega = raw_test_matrix(n, s, seed)
-    Om = upload_pinned(omega, kx.device)
+        # the reference's default_rng(seed).standard_normal((n, s)), drawn on the GPU
+        Om = kx.empty(n, s)
+        kx.gaussian(seed, Om)
+    else:
+        Om = upload_pinned(omega, kx.device)
+        kx.h2d += omega.nbytes
     Q = kx.empty(n, s)
     kx.orthonormalize(Om, Q)
     Y = apply_cols(Q).contiguous()

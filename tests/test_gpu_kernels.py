@@ -222,3 +222,17 @@ def test_pcg_kats():
     assert np.array_equal(x, np.zeros(4)) and rep.iterations == 0
     with pytest.raises(NotSPDError):
         pcg(DenseOperator(np.diag([1.0, -1.0])), np.ones(2), tol_rel=1e-12)
+
+
+@pytest.mark.parametrize("seed,count", [(0, 1), (1, 70 * 2000), (7, 133 * 10000), (123456789, 5_000_003)])
+def test_gaussian_matches_numpy_stream(kx, seed, count):
+    """Omega drawn on the GPU equals np.random.default_rng(seed).standard_normal
+    (sketch.py:97-98).  Bitwise except where CUDA's exp/log1p may differ from
+    glibc by one ulp on the rare ziggurat rejection paths."""
+    out = kx.empty(count)
+    kx.gaussian(seed, out)
+    got = out.cpu().numpy()
+    ref = np.random.default_rng(seed).standard_normal(count)
+    diff = got != ref
+    assert diff.sum() <= max(1, count // 100000), diff.sum()
+    np.testing.assert_allclose(got, ref, rtol=1e-15, atol=0)
