@@ -347,119 +347,6 @@ __global__ void add_scaled_kernel(int64_t tot, const double* __restrict__ Q, dou
     Y[t] = __dadd_rn(Y[t], __dmul_rn(sft, Q[t]));
 }
 
-// ------------------------------------------------------- Jacobi eigen -----
-// One-sided Jacobi on the s x s symmetric matrix held as ROWS of Xt (row p =
-// column p of X), accumulating V^T in Vt.  Round-robin (circle) pairing: all
-// m/2 pairs of a round are disjoint and processed in parallel, one warp per
-// pair, with a grid-wide barrier between rounds (cooperative launch).
-__global__ void __launch_bounds__(256) jacobi_kernel(int s, double* __restrict__ Xt,
-                                                     double* __restrict__ Vt, int max_sweeps,
-                                                     double tol, unsigned int* rot_count,
-                                                     int* sweeps_out) {
-  cg::grid_group grid = cg::this_grid();
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int m = s + (s & 1);  // padded to even; index s is a dummy when s is odd
-  const int npairs = m / 2;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) rot_count[sweep & 1] = 0u;
-    // make sure the other parity slot was consumed before it is reset next sweep
-    grid.sync();
-    unsigned int local_rot = 0;
-    for (int round = 0; round < m - 1; ++round) {
-      for (int k = gw; k < npairs; k += nwarps) {
-        int a, b;
-        if (k == 0) {
-          a = round;
-          b = m - 1;
-        } else {
-          a = (round + k) % (m - 1);
-          b = (round - k + (m - 1)) % (m - 1);
-        }
-        if (a >= s || b >= s) continue;
-        const int p = min(a, b), q = max(a, b);
-        double* xp = Xt + (int64_t)p * s;
-        double* xq = Xt + (int64_t)q * s;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < s; i += 32) {
-          const double u = xp[i], v = xq[i];
-          al = fma(u, u, al);
-          be = fma(v, v, be);
-          ga = fma(u, v, ga);
-        }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t);
-          const double sn = c * t;
-          double* vp = Vt + (int64_t)p * s;
-          double* vq = Vt + (int64_t)q * s;
-          for (int i = lane; i < s; i += 32) {
-            const double u = xp[i], v = xq[i];
-            xp[i] = c * u - sn * v;
-            xq[i] = sn * u + c * v;
-            const double vu = vp[i], vv = vq[i];
-            vp[i] = c * vu - sn * vv;
-            vq[i] = sn * vu + c * vv;
-          }
-          ++local_rot;
-        }
-      }
-      grid.sync();
-    }
-    if (lane == 0 && local_rot) atomicAdd(&rot_count[sweep & 1], local_rot);
-    grid.sync();
-    const unsigned int total = *((volatile unsigned int*)&rot_count[sweep & 1]);
-    grid.sync();
-    if (total == 0) {
-      ++sweep;
-      break;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
-}
-
-// eigenvalue of column p: w_p = sign(v_p . x_p) ||x_p||; then rank-sort
-// descending and scatter V columns: V[i][rank_p] = Vt[p][i].
-__global__ void jacobi_finish_kernel(int s, const double* __restrict__ Xt,
-                                     const double* __restrict__ Vt, double* __restrict__ wtmp,
-                                     double* __restrict__ V, double* __restrict__ w) {
-  extern __shared__ double ws_[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int p = warp; p < s; p += nw) {
-    double nx = 0.0, d = 0.0;
-    for (int i = lane; i < s; i += 32) {
-      const double x = Xt[(int64_t)p * s + i];
-      nx = fma(x, x, nx);
-      d = fma(Vt[(int64_t)p * s + i], x, d);
-    }
-    nx = warp_sum(nx);
-    d = warp_sum(d);
-    if (lane == 0) ws_[p] = (d >= 0.0 ? 1.0 : -1.0) * sqrt(nx);
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < s; p += blockDim.x) {
-    const double wp = ws_[p];
-    int rank = 0;
-    for (int q = 0; q < s; ++q) {
-      const double wq = ws_[q];
-      rank += (wq > wp) || (wq == wp && q < p);
-    }
-    wtmp[p] = (double)rank;
-    w[rank] = wp;
-  }
-  __syncthreads();
-  for (int64_t t = threadIdx.x; t < (int64_t)s * s; t += blockDim.x) {
-    const int p = (int)(t / s), i = (int)(t % s);
-    V[(int64_t)i * s + (int)wtmp[p]] = Vt[(int64_t)p * s + i];
-  }
-}
-
 __global__ void eye_kernel(int s, double* V) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)s * s;
        t += (int64_t)gridDim.x * blockDim.x)
@@ -494,43 +381,9 @@ struct Arena {
 
 constexpr size_t kRedBytesD = (4096 * 16 + 64) * sizeof(double);
 
-size_t syevj_ws(int s) {
-  return 2 * (size_t)s * s * sizeof(double) + 4 * (size_t)s * sizeof(double) + 4096;
-}
-
-// Eigen-decomposition of the symmetric s x s matrix A (destroyed): V columns
-// are eigenvectors, w descending.
-static int syevj(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes,
-                 cudaStream_t st) {
-  Arena ar{reinterpret_cast<char*>(ws), ws_bytes};
-  double* Vt = ar.take<double>((size_t)s * s);
-  double* wtmp = ar.take<double>(s);
-  unsigned int* rot = ar.take<unsigned int>(4);
-  int* sweeps = ar.take<int>(2);
-  if (!ar.ok) return NYS_ERR_WORKSPACE;
-  // A is symmetric, so its rows are its columns: Xt = A.
-  eye_kernel<<<(unsigned)tmin<int64_t>(cdiv((int64_t)s * s, 256), 1024), 256, 0, st>>>(s, Vt);
-  NYS_CHECK_LAUNCH();
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int bps = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, jacobi_kernel, 256, 0);
-  int nsm = kNumSMs;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int npairs = (s + (s & 1)) / 2;
-  int blocks = (int)tmin<int64_t>(cdiv(npairs, 8), (int64_t)max(1, bps) * nsm);
-  blocks = max(1, blocks);
-  int max_sweeps = 40;
-  double tol = 1e-15;
-  void* args[] = {(void*)&s, (void*)&A, (void*)&Vt, (void*)&max_sweeps, (void*)&tol,
-                  (void*)&rot, (void*)&sweeps};
-  if (cudaLaunchCooperativeKernel((void*)jacobi_kernel, blocks, 256, args, 0, st) != cudaSuccess)
-    return NYS_ERR_CUDA;
-  __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
-  jacobi_finish_kernel<<<1, 1024, s * sizeof(double), st>>>(s, A, Vt, wtmp, V, w);
-  NYS_CHECK_LAUNCH();
-  return NYS_OK;
-}
+// eig.cu: one-sided Jacobi on a thread-block cluster (A preserved)
+size_t syevj_ws(int s);
+int syevj(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes, cudaStream_t st);
 
 static int cholesky(int s, double* C, int* info_dev, int* info_host, cudaStream_t st) {
   cholesky_kernel<<<1, 1024, 0, st>>>(s, C, s, info_dev);

@@ -15,6 +15,7 @@ Pipeline of ``sketch_device`` (K5):
 from __future__ import annotations
 
 import math
+import time
 from typing import Callable, Optional
 
 import numpy as np
@@ -58,6 +59,14 @@ def sketch_device(kx, apply_cols: Callable[[torch.Tensor], torch.Tensor], n: int
     if not 1 <= r <= n:
         raise DataError(f"sketch rank must satisfy 1 <= r <= {n}, got {r}")
     s = sketch_width(n, r, oversample)
+    trace = _TRACE is not None
+    t = [time.perf_counter()] if trace else None
+
+    def mark():
+        if trace:
+            kx.sync()
+            t.append(time.perf_counter())
+
     if omega is None:
         # the reference's default_rng(seed).standard_normal((n, s)), drawn on the GPU
         Om = kx.empty(n, s)
@@ -65,15 +74,26 @@ def sketch_device(kx, apply_cols: Callable[[torch.Tensor], torch.Tensor], n: int
     else:
         Om = upload_pinned(omega, kx.device)
         kx.h2d += omega.nbytes
+    mark()
     Q = kx.empty(n, s)
     kx.orthonormalize(Om, Q)
+    mark()
     Y = apply_cols(Q).contiguous()
     if reduce is not None:
         reduce(Y)
+    mark()
     U = kx.empty(n, r)
     lam = kx.empty(r)
     rr = kx.nystrom_core(Q, Y, U, lam, r)
+    mark()
+    if trace:
+        d = np.diff(t) * 1e3
+        _TRACE.append({"gauss_ms": d[0], "ortho_ms": d[1], "target_ms": d[2], "core_ms": d[3]})
     return U[:, :rr], lam[:rr]
+
+
+# development instrumentation: set to a list to collect per-stage sketch times
+_TRACE: Optional[list] = None
 
 
 class NystromSketch:
