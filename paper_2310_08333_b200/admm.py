@@ -213,6 +213,11 @@ _S_DUAL = 44  # 2 (penalty change)
 _S_LEN = 48
 
 
+def _host_buffer(n, device):
+    t = torch.zeros(n, dtype=torch.float64)
+    return t.pin_memory() if device.type == "cuda" else t
+
+
 class _Engine:
     """Device-resident state and per-iteration kernel schedule of one solve."""
 
@@ -230,9 +235,9 @@ class _Engine:
             if p.loss.kind not in _lib.LOSS:
                 raise CapabilityError(f"loss {p.loss.kind!r} is not implemented on the B200 path")
             self.shard = shard or current_shard(p.N)
-            self.A = p.A.device_rows(self.shard)
+            self.A = p.A.device_rows(self.shard, kx.device)
             rows = self.rows = self.A.shape[0]
-            self.b = to_device(p.b[self.shard.row_start:self.shard.row_stop])
+            self.b = to_device(p.b[self.shard.row_start:self.shard.row_stop], kx.device)
             self.loss = p.loss.kind
             self.l1, self.l2 = float(p.lambda1), float(p.lambda2)
             self.const_hess = p.loss.deriv2_constant
@@ -252,10 +257,10 @@ class _Engine:
             if not isinstance(qp.M, IdentityOperator):
                 raise CapabilityError("the B200 path supports QPs with M = I only")
             self.shard = Shard(0, 1, 0, n, n)  # P is replicated
-            self.P = qp.P.device_rows()
-            self.q = to_device(qp.q)
-            self.lo = to_device(qp.box.l)
-            self.hi = to_device(qp.box.u)
+            self.P = qp.P.device_rows(None, kx.device)
+            self.q = to_device(qp.q, kx.device)
+            self.lo = to_device(qp.box.l, kx.device)
+            self.hi = to_device(qp.box.u, kx.device)
             self.const_hess = True
             self.diag_shift = 0.0
             self.Px = kx.empty(1, n)
@@ -269,7 +274,7 @@ class _Engine:
         self.rhs = kx.empty(n)
         self.cg = CgWork(kx, n)
         self.stats = kx.zeros(_S_LEN)
-        self.stats_h = torch.zeros(_S_LEN + 8, dtype=torch.float64).pin_memory()
+        self.stats_h = _host_buffer(_S_LEN + 8, kx.device)
         self.ring = kx.empty(DELTA_WINDOW + 2, n)
         self.uring = kx.empty(DELTA_WINDOW + 2, n) if not self.is_ml else None
         self.U = None
@@ -380,7 +385,7 @@ class _Engine:
         def warm(v, name, dst):
             if v is None:
                 return
-            vt = to_device(v)
+            vt = to_device(v, kx.device)
             if vt.shape != (n,):
                 raise DataError(f"warm start {name} must have length {n}, got shape {tuple(vt.shape)}")
             dst.copy_(vt)

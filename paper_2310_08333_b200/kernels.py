@@ -273,6 +273,7 @@ _CACHE: dict = {}
 def get_kernels() -> Kernels:
     """Kernels bound to the current device and torch stream (cached, so the
     operator-level API reuses its workspaces)."""
+    _lib.lib()  # CapabilityError without the library or an sm_100 GPU (no CPU fallback)
     dev = torch.cuda.current_device()
     sp = torch.cuda.current_stream(dev).cuda_stream
     k = _CACHE.get((dev, sp))

@@ -56,7 +56,9 @@ class CgWork:
         self.z = kx.empty(n)
         self.Ap = kx.empty(n)
         self.sc = kx.zeros(_lib.CG_NSLOTS)  # slot 7 holds a kernel ticket: keep zero
-        self.host = torch.zeros(_lib.CG_NSLOTS, dtype=torch.float64).pin_memory()
+        self.host = torch.zeros(_lib.CG_NSLOTS, dtype=torch.float64)
+        if kx.device.type == "cuda":
+            self.host = self.host.pin_memory()
 
     def slot(self, i: int) -> torch.Tensor:
         return self.sc[i:i + 1]

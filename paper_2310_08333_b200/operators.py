@@ -33,13 +33,12 @@ def _kx():
 
 def to_device(v, device=None) -> torch.Tensor:
     """Contiguous FP64 CUDA tensor view/copy of ``v``."""
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
     if isinstance(v, torch.Tensor):
-        t = v.to(dtype=F64)
-        if not t.is_cuda:
-            t = t.cuda(device)
-        return t.contiguous()
+        return v.to(device=device, dtype=F64).contiguous()
     a = np.ascontiguousarray(np.asarray(v, dtype=float))
-    return torch.from_numpy(a).to(device or torch.device("cuda", torch.cuda.current_device()))
+    return torch.from_numpy(a).to(device)
 
 
 def like_input(t: torch.Tensor, ref):
@@ -154,18 +153,20 @@ class DenseOperator(LinearOperator):
         self._shards: dict = {}
 
     # -- device data ---------------------------------------------------------
-    def device_rows(self, shard: Optional[Shard] = None) -> torch.Tensor:
+    def device_rows(self, shard: Optional[Shard] = None, device=None) -> torch.Tensor:
         """The (row-shard of the) matrix in HBM, uploaded once."""
         if shard is None:
             shard = Shard(0, 1, 0, self.output_dim, self.output_dim)
-        key = (shard.row_start, shard.row_stop, torch.cuda.current_device())
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        key = (shard.row_start, shard.row_stop, str(device))
         t = self._shards.get(key)
         if t is None:
             if self._dev_full is not None:
-                t = self._dev_full[shard.row_start:shard.row_stop]
+                t = self._dev_full[shard.row_start:shard.row_stop].to(device)
             else:
                 blk = np.ascontiguousarray(self.a[shard.row_start:shard.row_stop])
-                t = torch.from_numpy(blk).cuda()
+                t = torch.from_numpy(blk).to(device)
             self._shards[key] = t
         return t
 
