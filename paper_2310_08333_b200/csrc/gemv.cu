@@ -14,6 +14,7 @@
 //     per-row coefficients T are staged in shared memory; splits over rows are
 //     summed in a fixed order by a second kernel (deterministic, no atomics);
 //   * grids are sized in multiples of the 148 SMs.
+#include <stdlib.h>
 #include "common.cuh"
 
 namespace nys {
@@ -22,8 +23,8 @@ namespace nys {
 constexpr int kGemvThreads = 256;
 constexpr int kGemvRW = 4;
 
-template <int K, int RW, bool VEC>
-__global__ void __launch_bounds__(kGemvThreads)
+template <int K, int RW, int U, bool VEC>
+__global__ void __launch_bounds__(kGemvThreads, 2)
 gemv_n_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
               const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
               const double* __restrict__ dscale, int splits, int64_t chunk) {
@@ -48,7 +49,6 @@ gemv_n_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda
     for (int j = 0; j < K; ++j) acc[r][j] = 0.0;
 
   if (VEC) {
-    constexpr int U = 2;
     int64_t c = c0 + 2 * lane;
     for (; c + 64 * (U - 1) + 1 < c1; c += 64 * U) {
       double2 a[U][RW], x[U][K];
@@ -145,8 +145,8 @@ __global__ void gemv_n_reduce(const double* __restrict__ P, int64_t rows, int K,
   }
 }
 
-static void gemv_n_plan(int64_t rows, int64_t n, int& splits, int64_t& chunk) {
-  const int64_t ngroups = cdiv(rows, kGemvRW);
+static void gemv_n_plan(int64_t rows, int64_t n, int rw, int& splits, int64_t& chunk) {
+  const int64_t ngroups = cdiv(rows, rw);
   const int64_t target_warps = (int64_t)kNumSMs * 16;
   int64_t sp = ngroups >= target_warps ? 1 : cdiv(target_warps, ngroups);
   // keep at least 512 columns per split
@@ -156,13 +156,23 @@ static void gemv_n_plan(int64_t rows, int64_t n, int& splits, int64_t& chunk) {
   splits = (int)sp;
 }
 
-template <int K>
-static int gemv_n_launch(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X,
-                         int64_t ldx, double* Y, int64_t ldy, const double* dscale, double* ws,
-                         size_t ws_bytes, cudaStream_t st) {
+// register blocking per number of right-hand sides: rows per warp (RW) and
+// 128-bit loads in flight per row (U); overridable for tuning (NYS_GEMV_VARIANT)
+static int gemv_variant(int K) {
+  static const int forced = getenv("NYS_GEMV_VARIANT") ? atoi(getenv("NYS_GEMV_VARIANT")) : -1;
+  if (forced >= 0) return forced;
+  // measured on B200 (tools/micro.py): k<=2 one row per warp with 4 loads in
+  // flight per lane; k=3 two rows x 2 loads; k=4 two rows x 1 load
+  return K <= 2 ? 4 : (K == 3 ? 2 : 3);
+}
+
+template <int K, int RW, int U>
+static int gemv_n_launch_v(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X,
+                           int64_t ldx, double* Y, int64_t ldy, const double* dscale, double* ws,
+                           size_t ws_bytes, cudaStream_t st) {
   int splits;
   int64_t chunk;
-  gemv_n_plan(rows, n, splits, chunk);
+  gemv_n_plan(rows, n, RW, splits, chunk);
   if (splits > 1 && ws_bytes < (size_t)splits * K * rows * sizeof(double)) {
     splits = 1;
     chunk = n;
@@ -170,14 +180,14 @@ static int gemv_n_launch(const double* A, int64_t rows, int64_t n, int64_t lda, 
   const bool vec = ((lda & 1) == 0) && ((ldx & 1) == 0) &&
                    ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-  const int64_t warps = cdiv(rows, kGemvRW) * splits;
+  const int64_t warps = cdiv(rows, RW) * splits;
   const int64_t blocks = cdiv(warps * 32, kGemvThreads);
   double* out = splits == 1 ? Y : ws;
   if (vec)
-    gemv_n_kernel<K, kGemvRW, true><<<(unsigned)blocks, kGemvThreads, 0, st>>>(
+    gemv_n_kernel<K, RW, U, true><<<(unsigned)blocks, kGemvThreads, 0, st>>>(
         A, rows, n, lda, X, ldx, out, ldy, dscale, splits, chunk);
   else
-    gemv_n_kernel<K, kGemvRW, false><<<(unsigned)blocks, kGemvThreads, 0, st>>>(
+    gemv_n_kernel<K, RW, 1, false><<<(unsigned)blocks, kGemvThreads, 0, st>>>(
         A, rows, n, lda, X, ldx, out, ldy, dscale, splits, chunk);
   NYS_CHECK_LAUNCH();
   if (splits > 1) {
@@ -187,6 +197,19 @@ static int gemv_n_launch(const double* A, int64_t rows, int64_t n, int64_t lda, 
     NYS_CHECK_LAUNCH();
   }
   return NYS_OK;
+}
+
+template <int K>
+static int gemv_n_launch(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X,
+                         int64_t ldx, double* Y, int64_t ldy, const double* dscale, double* ws,
+                         size_t ws_bytes, cudaStream_t st) {
+  switch (gemv_variant(K)) {
+    case 0: return gemv_n_launch_v<K, 4, 2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
+    case 1: return gemv_n_launch_v<K, 4, 1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
+    case 2: return gemv_n_launch_v<K, 2, 2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
+    case 3: return gemv_n_launch_v<K, 2, 1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
+    default: return gemv_n_launch_v<K, 1, 4>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
+  }
 }
 
 int gemv_n(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X, int64_t ldx,
@@ -205,7 +228,7 @@ int gemv_n(const double* A, int64_t rows, int64_t n, int64_t lda, const double* 
 size_t gemv_n_ws(int64_t rows, int64_t n, int k) {
   int splits;
   int64_t chunk;
-  gemv_n_plan(rows, n, splits, chunk);
+  gemv_n_plan(rows, n, 4, splits, chunk);  // RW = 4 needs the most splits
   return splits > 1 ? (size_t)splits * k * rows * sizeof(double) : 0;
 }
 
@@ -464,9 +487,23 @@ extern "C" int nys_gemvT_f64(const double* A, int64_t rows, int64_t n, int64_t l
                 as_stream(stream));
 }
 
+namespace nys {
+struct HvpPlan {
+  int C, W, K, S, nclusters;
+  size_t smem;
+  bool ok;
+};
+HvpPlan hvp_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
+int hvp_fused(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
+              const double* v, double* ypart, cudaStream_t st);
+}  // namespace nys
+
 extern "C" size_t nys_hvp_workspace(int64_t rows, int64_t n) {
-  // t = d o (A v) (rows doubles) + the K1 split partials + the K2 workspace
-  return cdiv(rows, 2) * 2 * sizeof(double) + gemv_n_ws(rows, n, 1) + gemv_t_ws(rows, n, 1);
+  // two-pass: t = d o (A v) (rows doubles) + the K1 split partials + the K2 workspace
+  const size_t two = cdiv(rows, 2) * 2 * sizeof(double) + gemv_n_ws(rows, n, 1) + gemv_t_ws(rows, n, 1);
+  // single pass: reduction scratch + one y partial per cluster (<= 148)
+  const size_t one = kRedBytes + (size_t)kNumSMs * n * sizeof(double);
+  return tmax(two, one);
 }
 
 extern "C" int nys_hvp_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
@@ -475,6 +512,19 @@ extern "C" int nys_hvp_f64(const double* A, int64_t rows, int64_t n, int64_t lda
   if (rows <= 0 || n <= 0 || lda < n) return NYS_ERR_ARG;
   if (ws_bytes < nys_hvp_workspace(rows, n)) return NYS_ERR_WORKSPACE;
   cudaStream_t st = as_stream(stream);
+  static const bool two_pass_only = getenv("NYS_HVP_TWOPASS") != nullptr;
+  const HvpPlan plan = hvp_plan(rows, n, lda, A, v);
+  if (plan.ok && !two_pass_only) {
+    // single pass over A (csrc/hvp.cu), then a fixed-order sum of the cluster partials
+    double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
+    int rc = hvp_fused(plan, A, rows, n, lda, d, v, P, st);
+    if (rc) return rc;
+    const int64_t rb = tmin<int64_t>(cdiv(n, 256), kRedPartials);
+    gemv_t_reduce<<<(unsigned)rb, 256, 0, st>>>(P, n, 1, plan.nclusters, y, n, finish ? v : nullptr,
+                                                 shift, finish ? pAp : nullptr, red_part(ws), red_counter(ws));
+    NYS_CHECK_LAUNCH();
+    return NYS_OK;
+  }
   char* base = reinterpret_cast<char*>(ws);
   // layout: [K2 ws (reduction scratch first)] [t] [K1 partials]
   const size_t wt = gemv_t_ws(rows, n, 1);
