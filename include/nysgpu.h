@@ -59,8 +59,42 @@ enum nys_cg_slot {
   NYS_CG_RZNEW = 4,  /* r.z of the freshly preconditioned residual */
   NYS_CG_B2 = 5,     /* ||b||^2                                   */
   NYS_CG_FLAG = 6,   /* 0 ok, 1 non-finite pAp, 2 pAp <= 0        */
-  NYS_CG_NSLOTS = 8
+  NYS_CG_TICKET = 7, /* kernel ticket (keep zero)                 */
+  NYS_CG_DONE = 8,   /* batched CG: 0 running, 1 converged, 2 non-finite, 3 not SPD, 4 cap */
+  NYS_CG_ITERS = 9,  /* batched CG: iterations taken              */
+  NYS_CG_RESREL = 10,/* batched CG: final ||r|| / ||b||           */
+  NYS_CG_RUNNING = 11,/* batched CG: 1 while iterating, 0 once DONE is set */
+  NYS_CG_NSLOTS = 16
 };
+
+/* One PCG solve for nys_cg_iterate_f64 (krylov.py:35-95).  All pointers are
+ * device pointers; `sc` is the NYS_CG_NSLOTS scalar block with B2 and RES2
+ * already set for r = b - A x0 (e.g. by nys_admm_rhs_f64 or nys_cg_start_f64). */
+typedef struct nys_cg_problem {
+  int op_kind;          /* 0: y = A^T (d o A v) + shift v (ML Hessian, A rows x n)
+                           1: y = A v + shift v (dense symmetric A, n x n)          */
+  const double* A;
+  int64_t rows, n, lda;
+  const double* d;      /* row weights (op 0) or NULL (== 1)                        */
+  double shift;
+  const double* U;      /* preconditioner factors (sketch.py:143-151); r = 0: none  */
+  int r;
+  int64_t ldu;
+  const double* lam;
+  double nu;
+  const double* b;
+  double* x;            /* in: x0, out: solution                                    */
+  double* res;          /* residual r                                               */
+  double* p;
+  double* z;
+  double* Ap;
+  double* sc;
+  double tol;           /* relative tolerance (krylov.py:87)                        */
+  int64_t max_iter;
+  void* ws_op;  size_t ws_op_bytes;   /* operator workspace (zero-filled once)     */
+  void* ws_pc;  size_t ws_pc_bytes;   /* preconditioner workspace                  */
+  void* ws_red;                        /* reduction scratch (returned size)         */
+} nys_cg_problem;
 
 /* ---------------------------------------------------------------- misc -- */
 int nys_abi_version(void);
@@ -127,6 +161,46 @@ int nys_cg_step_xr_f64(int64_t n, double* x, double* r, const double* p, const d
  * rz = rz_new, p = z + beta p.   (rz_new = sc[RZNEW]) */
 int nys_cg_dir_f64(int64_t n, const double* z, double* p, int first, double* sc,
                    void* stream);
+
+/* Batched, device-predicated PCG: launches iterations k_first .. k_first+count-1
+ * (k_first == 1 also runs the initial test and first preconditioning).  The
+ * stop test of krylov.py:80-93 runs on the device and sets sc[NYS_CG_DONE];
+ * every later launch is a no-op, so the host may run ahead and read sc once.
+ * Workspace sizes: returns the reduction scratch bytes, *ws_op / *ws_pc. */
+size_t nys_cg_workspace(int op_kind, int64_t rows, int64_t n, int r, size_t* ws_op, size_t* ws_pc);
+int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int count, void* stream);
+
+/* Everything of one ADMM iteration after the x-update (admm.py:562-611 and
+ * 621-675), launched as one predicated sequence: relax/prox/dual update (+
+ * averages), window copy, data passes (ML: A{x,z}, loss epilogue,
+ * A^T{l', w o Ax, nu}; QP: P x), residual/objective/gap norms, window norms,
+ * QP infeasibility pieces.  Every launch is skipped while *pred != 0 (pass
+ * &sc[NYS_CG_RUNNING] to chain it behind a batched CG solve). */
+typedef struct nys_admm_tail {
+  int kind;                   /* 0: ML (M = I), 1: box QP (M = I)                     */
+  int loss;                   /* nys_loss (ML)                                        */
+  int64_t n, rows;
+  const double* A; int64_t lda;     /* ML data (rows x n) or P (n x n)                */
+  const double* b;                  /* ML responses (rows)                            */
+  double* XZ;                 /* 2 x n: x (row 0), z (row 1)                          */
+  double* u; double* xbar; double* zbar; int accum;
+  double alpha; double kappa; const double* lo; const double* hi; const double* q;
+  double lambda1, lambda2, rho;
+  int with_z;                 /* ML: also A z, the dual point and A^T nu              */
+  double* AXZ;                /* 2 x rows                                             */
+  double* T;                  /* 3 x rows: l'(Ax-b), w o Ax, nu                       */
+  double* w;                  /* rows                                                 */
+  double* AT;                 /* ML: 3 x n (gA, hxA, atnu) ; QP: 1 x n (P x)          */
+  double* rowsums;            /* NYS_ROWS_NOUT                                        */
+  double* norms;              /* NYS_NORMS_NOUT                                       */
+  double* ring; double* uring; int64_t ring_ld; int slot;
+  int nothers; int others[16]; double* wnorms;   /* window norms (17)             */
+  int qp_infeas; int inf_first; int inf_last; double width; double* dx; double* Pdx;
+  double* infeas; double* pdx2;                   /* 6 pieces, ||P dx||^2          */
+  void* ws_gemv; size_t ws_gemv_bytes; void* ws_gemvT; size_t ws_gemvT_bytes; void* ws_red;
+  const double* pred;
+} nys_admm_tail;
+int nys_admm_tail_f64(const nys_admm_tail* t, void* stream);
 
 /* ---------------------------------------------- K8/K9 ADMM elementwise -- */
 /* x-update right-hand side and initial CG residual, M = I, c = 0

@@ -31,7 +31,8 @@ LOSS = {"square": 0, "logistic": 1, "huber": 2}
 PROX_SOFT, PROX_BOX = 0, 1
 
 # CG scalar slots (nys_cg_slot)
-CG_RZ, CG_PAP, CG_ALPHA, CG_RES2, CG_RZNEW, CG_B2, CG_FLAG, CG_NSLOTS = 0, 1, 2, 3, 4, 5, 6, 8
+CG_RZ, CG_PAP, CG_ALPHA, CG_RES2, CG_RZNEW, CG_B2, CG_FLAG = 0, 1, 2, 3, 4, 5, 6
+CG_TICKET, CG_DONE, CG_ITERS, CG_RESREL, CG_RUNNING, CG_NSLOTS = 7, 8, 9, 10, 11, 16
 NORMS_NOUT = 16
 ROWS_NOUT = 5
 
@@ -41,8 +42,39 @@ I32 = C.c_int
 F64 = C.c_double
 SZ = C.c_size_t
 
+
+class CgProblem(C.Structure):
+    """Mirror of ``nys_cg_problem`` (include/nysgpu.h)."""
+
+    _fields_ = [
+        ("op_kind", C.c_int), ("A", P), ("rows", I64), ("n", I64), ("lda", I64), ("d", P),
+        ("shift", F64), ("U", P), ("r", C.c_int), ("ldu", I64), ("lam", P), ("nu", F64),
+        ("b", P), ("x", P), ("res", P), ("p", P), ("z", P), ("Ap", P), ("sc", P),
+        ("tol", F64), ("max_iter", I64), ("ws_op", P), ("ws_op_bytes", SZ), ("ws_pc", P),
+        ("ws_pc_bytes", SZ), ("ws_red", P),
+    ]
+
+class AdmmTail(C.Structure):
+    """Mirror of ``nys_admm_tail`` (include/nysgpu.h)."""
+
+    _fields_ = [
+        ("kind", C.c_int), ("loss", C.c_int), ("n", I64), ("rows", I64), ("A", P), ("lda", I64), ("b", P),
+        ("XZ", P), ("u", P), ("xbar", P), ("zbar", P), ("accum", C.c_int),
+        ("alpha", F64), ("kappa", F64), ("lo", P), ("hi", P), ("q", P),
+        ("lambda1", F64), ("lambda2", F64), ("rho", F64), ("with_z", C.c_int),
+        ("AXZ", P), ("T", P), ("w", P), ("AT", P), ("rowsums", P), ("norms", P),
+        ("ring", P), ("uring", P), ("ring_ld", I64), ("slot", C.c_int),
+        ("nothers", C.c_int), ("others", C.c_int * 16), ("wnorms", P),
+        ("qp_infeas", C.c_int), ("inf_first", C.c_int), ("inf_last", C.c_int), ("width", F64),
+        ("dx", P), ("Pdx", P), ("infeas", P), ("pdx2", P),
+        ("ws_gemv", P), ("ws_gemv_bytes", SZ), ("ws_gemvT", P), ("ws_gemvT_bytes", SZ), ("ws_red", P),
+        ("pred", P),
+    ]
+
+
 # name: (restype, argtypes)
 SIGNATURES = {
+    "nys_admm_tail_f64": (I32, [C.POINTER(AdmmTail), P]),
     "nys_abi_version": (I32, []),
     "nys_status_string": (C.c_char_p, [I32]),
     "nys_device_check": (I32, []),
@@ -61,6 +93,8 @@ SIGNATURES = {
     "nys_cg_start_f64": (I32, [I64, P, P, P, P, P, P]),
     "nys_cg_step_xr_f64": (I32, [I64, P, P, P, P, I32, P, P, P]),
     "nys_cg_dir_f64": (I32, [I64, P, P, I32, P, P]),
+    "nys_cg_workspace": (SZ, [I32, I64, I64, I32, C.POINTER(SZ), C.POINTER(SZ)]),
+    "nys_cg_iterate_f64": (I32, [C.POINTER(CgProblem), I64, I32, P]),
     "nys_admm_rhs_f64": (I32, [I64, P, P, P, F64, F64, F64, F64, P, P, P, P, P, P, P, P]),
     "nys_admm_zu_f64": (I32, [I64, P, P, P, F64, I32, F64, P, P, P, P, I32, P]),
     "nys_admm_norms_f64": (I32, [I64, P, P, P, P, P, F64, F64, P, F64, P, P, P, P, P]),

@@ -40,8 +40,8 @@ import torch
 
 from . import _lib
 from .dist import Shard, current_shard
-from .errors import CapabilityError, DataError
-from .krylov import CgReport, CgWork, cg_tolerance, pcg_device
+from .errors import CapabilityError, DataError, NotSPDError, NumericalError
+from .krylov import CgReport, CgWork, cg_tolerance, pcg_batched, pcg_device
 from .operators import DenseOperator, IdentityOperator, to_device
 from .problems import GenericProblem, lower
 from .sketch import NystromPreconditioner, NystromSketch, default_sketch_rank, raw_test_matrix, sketch_device, sketch_width
@@ -280,6 +280,7 @@ class _Engine:
         self.U = None
         self.lam = None
         self.pc_nu = 1.0
+        self._last_cg = 8  # first x-update runs to the 1e-12 floor: start with a larger batch
 
     # ----------------------------------------------------------- passes --
     def evaluate(self, with_z: bool) -> None:
@@ -404,6 +405,12 @@ class _Engine:
         if use_gap and not self.is_ml:
             raise DataError("the duality-gap criterion requires an ML problem")
         self.use_gap = use_gap
+        # single-process CUDA path: batched CG + predicated iteration tail (one
+        # host round trip per ADMM iteration); sharded runs keep the per-step path
+        # because their all-reduces sit between the kernels
+        self.fast = hasattr(kx, "admm_tail") and not self.shard.sharded
+        if self.fast:
+            self._make_tail()
 
         timings = Timings()
         r_sk = opts.sketch_rank or default_sketch_rank(n)
@@ -456,7 +463,7 @@ class _Engine:
                 last_sketch = k
             tol = 1e-12 if opts.exact_x_solve else cg_tolerance(k, res.rp_norm, res.rd_norm, opts.gamma)
 
-            # x-update (admm.py:243-275)
+            # x-update (admm.py:243-275): rhs and the initial residual r = b - A x0
             t0 = time.perf_counter()
             shift = self.rho + sigma_eff
             if self.is_ml:
@@ -465,29 +472,33 @@ class _Engine:
             else:
                 kx.admm_rhs(self.Px[0], self.Px[0], self.q, 0.0, sigma_eff, self.rho, shift,
                             self.x, self.z, self.u, self.rhs, self.cg.r, self.cg.sc)
-            rep = pcg_device(self.cg, self.matvec(shift), self.rhs, self.x, self.precond(), tol, 10 * n,
-                             started=True)
-            linsys_s = time.perf_counter() - t0
-            timings.linsys_total_s += linsys_s
-
-            # z/u update (admm.py:562-576) + averaged sums (admm.py:580-583)
-            t0 = time.perf_counter()
-            if self.is_ml:
-                kx.admm_zu(self.x, self.z, self.u, opts.alpha, _lib.PROX_SOFT, self.l1 / self.rho, None, None,
-                           self.xbar, self.zbar, k >= 2)
+            if self.fast:
+                # CG batches with the device stop test, then the predicated rest of
+                # the iteration (z/u, data passes, norms, windows): one round trip
+                rep, st, linsys_s, prox_s, spec = self._fused_iteration(k, tol, shift, win, k >= 2)
             else:
-                kx.admm_zu(self.x, self.z, self.u, opts.alpha, _lib.PROX_BOX, 0.0, self.lo, self.hi,
-                           self.xbar, self.zbar, k >= 2)
-            prox_s = time.perf_counter() - t0
+                rep = pcg_device(self.cg, self.matvec(shift), self.rhs, self.x, self.precond(), tol, 10 * n,
+                                 started=True)
+                linsys_s = time.perf_counter() - t0
+                # z/u update (admm.py:562-576) + averaged sums (admm.py:580-583)
+                t0 = time.perf_counter()
+                if self.is_ml:
+                    kx.admm_zu(self.x, self.z, self.u, opts.alpha, _lib.PROX_SOFT, self.l1 / self.rho, None, None,
+                               self.xbar, self.zbar, k >= 2)
+                else:
+                    kx.admm_zu(self.x, self.z, self.u, opts.alpha, _lib.PROX_BOX, 0.0, self.lo, self.hi,
+                               self.xbar, self.zbar, k >= 2)
+                prox_s = time.perf_counter() - t0
+                # data passes, norms, and (speculatively) the window reductions
+                self.evaluate(with_z=use_gap)
+                self.norms(with_nu=use_gap)
+                spec = self._win_speculate(win)
+                st = self.read_stats()
+            self._last_cg = rep.iterations
+            timings.linsys_total_s += linsys_s
             timings.prox_total_s += prox_s
             if k >= 2:
                 bar_count += 1
-
-            # data passes, norms, and (speculatively) the window reductions
-            self.evaluate(with_z=use_gap)
-            self.norms(with_nu=use_gap)
-            spec = self._win_speculate(win)
-            st = self.read_stats()
             res = self._residuals(st)
             objective = self._objective(st)
             last_obj = objective
@@ -692,6 +703,119 @@ class _Engine:
 
     def _win_commit(self, win, slot) -> None:
         win.append(slot)
+
+    # ------------------------------------------------ fused iteration ----
+    def _make_tail(self):
+        """Static part of the nys_admm_tail descriptor (pointers into this
+        solve's buffers; the workspaces have their own keys so they are never
+        reallocated under the descriptor)."""
+        kx, L, n = self.kx, self.kx.L, self.n
+        t = _lib.AdmmTail()
+        st = self.stats
+        ptr = lambda x: x.data_ptr() if x is not None else None
+        t.n = n
+        t.XZ = self.XZ.data_ptr()
+        t.u, t.xbar, t.zbar = self.u.data_ptr(), self.xbar.data_ptr(), self.zbar.data_ptr()
+        t.alpha = float(self.opts.alpha)
+        t.norms = st.data_ptr()
+        t.ring, t.ring_ld = self.ring.data_ptr(), self.ring.stride(0)
+        t.uring = ptr(self.uring)
+        t.wnorms = st[_S_WIN:].data_ptr()
+        t.infeas = st[_S_INF:].data_ptr()
+        t.pdx2 = st[_S_PDX:].data_ptr()
+        t.width = float(DELTA_WINDOW)
+        t.pred = self.cg.sc[_lib.CG_RUNNING:].data_ptr()
+        if self.is_ml:
+            rows = self.rows
+            t.kind, t.loss, t.rows = 0, _lib.LOSS[self.loss], rows
+            t.A, t.lda, t.b = self.A.data_ptr(), self.A.stride(0), self.b.data_ptr()
+            t.lambda1, t.lambda2 = self.l1, self.l2
+            t.with_z = 1 if self.use_gap else 0
+            t.AXZ, t.T, t.w, t.AT = self.AXZ.data_ptr(), self.T.data_ptr(), self.w.data_ptr(), self.AT.data_ptr()
+            t.rowsums = self.rowsums.data_ptr()
+            wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(rows, n, 2))
+            wt = kx.workspace("tail_gemvT", L.nys_gemvT_workspace(rows, n, 3))
+        else:
+            t.kind, t.rows = 1, n
+            t.A, t.lda = self.P.data_ptr(), self.P.stride(0)
+            t.lo, t.hi, t.q = self.lo.data_ptr(), self.hi.data_ptr(), self.q.data_ptr()
+            t.AT = self.Px.data_ptr()
+            t.dx, t.Pdx = self.dx.data_ptr(), self.Pdx.data_ptr()
+            wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(n, n, 1))
+            wt = kx.workspace("tail_gemvT", 256)
+        wr = kx.workspace("tail_red", L.nys_reduce_workspace())
+        t.ws_gemv, t.ws_gemv_bytes = wg.data_ptr(), wg.numel()
+        t.ws_gemvT, t.ws_gemvT_bytes = wt.data_ptr(), wt.numel()
+        t.ws_red = wr.data_ptr()
+        self._tail = t
+        self._rb = _host_buffer(_lib.CG_NSLOTS + _S_LEN + 8, kx.device)
+        self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+    def _read_fused(self):
+        """sc + stats (+ row sums) in one readback; returns (sc, st)."""
+        rb, C = self._rb, _lib.CG_NSLOTS
+        rb[:C].copy_(self.cg.sc, non_blocking=True)
+        rb[C:C + _S_LEN].copy_(self.stats, non_blocking=True)
+        if self.is_ml:
+            rb[C + _S_LEN:C + _S_LEN + 5].copy_(self.rowsums[:5], non_blocking=True)
+        self.kx.d2h += (C + _S_LEN + 5) * 8
+        self.kx.sync()
+        h = rb.numpy().copy()
+        return h[:C], h[C:]
+
+    def _fused_iteration(self, k, tol, shift, win, accum):
+        kx, n, t = self.kx, self.n, self._tail
+        if self.is_ml:
+            pb = kx.cg_problem(0, self.A, None if self.loss == "square" else self.w, self.diag_shift + shift,
+                               self.U, self.lam, self.pc_nu, self.rhs, self.x, self.cg, tol, 10 * n)
+        else:
+            pb = kx.cg_problem(1, self.P, None, shift, self.U, self.lam, self.pc_nu, self.rhs, self.x, self.cg,
+                               tol, 10 * n)
+        # the window after the speculative append (committed by the host later)
+        slot = self._free_slot(win)
+        after = list(win) + [slot]
+        if len(after) > DELTA_WINDOW + 1:
+            after = after[1:]
+        t.accum = 1 if accum else 0
+        t.rho = float(self.rho)
+        t.kappa = float(self.l1 / self.rho) if self.is_ml else 0.0
+        t.slot = slot
+        if len(after) >= 4:
+            nper = min(len(after) - 1, 10) - 1
+            others = [after[-2]] + [after[-1 - p] for p in range(2, 2 + nper)]
+        else:
+            others = []
+        t.nothers = len(others)
+        for j, o in enumerate(others):
+            t.others[j] = o
+        t.qp_infeas = 1 if (not self.is_ml and len(after) == DELTA_WINDOW + 1) else 0
+        if t.qp_infeas:
+            t.inf_first, t.inf_last = after[0], after[-1]
+        ev = self._ev
+        k_first, batch = 1, min(16, max(2, self._last_cg + 1))
+        lin_ms = tail_ms = 0.0
+        max_iter = 10 * n
+        while True:
+            ev[0].record(kx.stream)
+            kx.cg_iterate(pb, k_first, batch)
+            ev[1].record(kx.stream)
+            kx.admm_tail(t)
+            ev[2].record(kx.stream)
+            sc, st = self._read_fused()
+            lin_ms += ev[0].elapsed_time(ev[1])
+            tail_ms += ev[1].elapsed_time(ev[2])
+            done = int(sc[_lib.CG_DONE])
+            if done or k_first + batch > max_iter:
+                break
+            k_first += batch
+            batch = min(16, 2 * batch)
+        if done == 2:
+            raise NumericalError("non-finite value in conjugate gradient")
+        if done == 3:
+            raise NotSPDError(f"nonpositive curvature p'Ap = {sc[_lib.CG_PAP]:.3e}; operator is not SPD")
+        iters = int(sc[_lib.CG_ITERS])
+        rep = CgReport(iters, float(sc[_lib.CG_RESREL]), done == 1)
+        return rep, st, lin_ms / 1e3, tail_ms / 1e3, slot
 
     def _infeasibility(self, st, win):
         """admm.py:361-415 with M = I from the speculative reductions."""

@@ -1,0 +1,208 @@
+// Device-predicated PCG (krylov.py:35-95) -- several iterations per host sync.
+//
+// The reference takes its stopping decision on the host after every CG
+// iteration.  Here the same decision (recurrence residual ||r|| <= tol ||b||,
+// true-residual refresh every 50 iterations, non-finite / non-positive
+// curvature errors, max_iter) is taken ON THE DEVICE by the last CTA of the
+// update kernel, which raises sc[NYS_CG_DONE]; every kernel of the iteration
+// (HVP, preconditioner, vector updates) is predicated on that flag and exits
+// immediately once it is set.  The host launches `count` iterations back to
+// back and reads the scalar block once, so a CG solve of c iterations costs
+// ceil(c / count) syncs instead of c, with the identical iteration sequence.
+#include <math.h>
+#include "common.cuh"
+
+namespace nys {
+
+// defined in gemv.cu / vec.cu
+int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const double* d, const double* v,
+              double shift, double* y, double* pAp, int finish, void* ws, size_t ws_bytes, cudaStream_t st,
+              const double* pred);
+int dense_mv_apply(const double* P, int64_t n, int64_t ldp, const double* v, double shift, double* y, double* pAp,
+                   void* ws, size_t ws_bytes, cudaStream_t st, const double* pred);
+size_t hvp_ws(int64_t rows, int64_t n);
+size_t dense_mv_ws(int64_t n);
+int precond_apply(const double* U, int64_t n, int r, int64_t ldu, const double* lam, double nu,
+                  const double* v, double* z, const double* rdot, double* rz, void* ws, size_t ws_bytes,
+                  cudaStream_t st, const double* pred);
+
+constexpr int kCgThreads = 256;
+constexpr int kCgMaxBlocks = kNumSMs * 4;
+constexpr int kCgRedPartials = 4096;
+inline double* cg_part(void* ws) { return reinterpret_cast<double*>(ws); }
+inline unsigned int* cg_counter(void* ws) {
+  return reinterpret_cast<unsigned int*>(reinterpret_cast<double*>(ws) + kCgRedPartials * 16);
+}
+inline unsigned cg_blocks(int64_t n) {
+  return (unsigned)tmax<int64_t>(1, tmin<int64_t>(cdiv(n, kCgThreads), kCgMaxBlocks));
+}
+
+// the reference's stop test on ||r||^2 (krylov.py:84-88); k = iteration index
+__device__ __forceinline__ void stop_test(double* sc, double res2, double tol, int64_t k, int64_t max_iter) {
+  const double b2 = sc[NYS_CG_B2];
+  const double denom = b2 > 0.0 ? sqrt(b2) : 1.0;
+  const double res = sqrt(res2);
+  sc[NYS_CG_RES2] = res2;
+  if (!isfinite(res)) {
+    sc[NYS_CG_DONE] = 2.0;  // non-finite residual
+    sc[NYS_CG_ITERS] = (double)k;
+  } else if (res <= tol * denom) {
+    sc[NYS_CG_DONE] = 1.0;
+    sc[NYS_CG_ITERS] = (double)k;
+  } else if (k >= max_iter) {
+    sc[NYS_CG_DONE] = 4.0;  // iteration cap, not converged
+    sc[NYS_CG_ITERS] = (double)k;
+  }
+  sc[NYS_CG_RESREL] = res / denom;
+  if (sc[NYS_CG_DONE] != 0.0) sc[NYS_CG_RUNNING] = 0.0;
+}
+
+__global__ void cgp_begin_kernel(double* sc, double tol, int64_t max_iter) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  sc[NYS_CG_DONE] = 0.0;
+  sc[NYS_CG_ITERS] = 0.0;
+  sc[NYS_CG_RUNNING] = 1.0;
+  stop_test(sc, sc[NYS_CG_RES2], tol, 0, max_iter > 0 ? max_iter : 1);
+  if (sc[NYS_CG_DONE] == 4.0) {  // only the k >= 1 updates may hit the cap
+    sc[NYS_CG_DONE] = 0.0;
+    sc[NYS_CG_RUNNING] = 1.0;
+  }
+}
+
+__device__ __forceinline__ void block_total(double& v, double* sh) {
+  double a[1] = {v};
+  block_sum<1>(a, sh);
+  v = a[0];
+}
+
+__global__ void cgp_step_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                const double* __restrict__ p, const double* __restrict__ Ap, int refresh,
+                                double* sc, double tol, int64_t k, int64_t max_iter, double* part,
+                                unsigned int* counter) {
+  if (sc[NYS_CG_DONE] != 0.0) return;
+  __shared__ double sh[32];
+  const double pAp = sc[NYS_CG_PAP];
+  const double rz = sc[NYS_CG_RZ];
+  const bool bad = !isfinite(pAp) || pAp <= 0.0;
+  if (bad) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc[NYS_CG_FLAG] = !isfinite(pAp) ? 1.0 : 2.0;
+      sc[NYS_CG_DONE] = !isfinite(pAp) ? 2.0 : 3.0;  // krylov.py:74-77
+      sc[NYS_CG_ITERS] = (double)k;
+      sc[NYS_CG_RUNNING] = 0.0;
+    }
+    return;
+  }
+  const double alpha = rz / pAp;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    if (!refresh) {
+      const double ri = __dadd_rn(r[i], -__dmul_rn(alpha, Ap[i]));
+      r[i] = ri;
+      s = fma(ri, ri, s);
+    }
+  }
+  if (refresh) return;  // the residual is recomputed by cgp_restart_kernel
+  block_total(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (last_block(counter)) {
+    const double tot = block_sum_partials(part, gridDim.x, 1, sh);
+    if (threadIdx.x == 0) {
+      sc[NYS_CG_ALPHA] = alpha;
+      stop_test(sc, tot, tol, k, max_iter);
+    }
+  }
+}
+
+// true residual refresh (krylov.py:80-81): r = b - A x, then the stop test
+__global__ void cgp_restart_kernel(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
+                                   double* __restrict__ r, double* sc, double tol, int64_t k, int64_t max_iter,
+                                   double* part, unsigned int* counter) {
+  if (sc[NYS_CG_DONE] != 0.0) return;
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = __dadd_rn(b[i], -Ax[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  block_total(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (last_block(counter)) {
+    const double tot = block_sum_partials(part, gridDim.x, 1, sh);
+    if (threadIdx.x == 0) stop_test(sc, tot, tol, k, max_iter);
+  }
+}
+
+// p = z (first) or z + beta p, beta = rz_new / rz (krylov.py:89-93)
+__global__ void cgp_dir_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ p, int first,
+                               double* sc, unsigned int* counter) {
+  if (sc[NYS_CG_DONE] != 0.0) return;
+  const double rz_new = sc[NYS_CG_RZNEW];
+  const double beta = first ? 0.0 : rz_new / sc[NYS_CG_RZ];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = first ? z[i] : __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+  if (last_block(counter)) {
+    if (threadIdx.x == 0) sc[NYS_CG_RZ] = rz_new;
+  }
+}
+
+static int matvec(const nys_cg_problem* pb, const double* v, double* y, double* pAp, cudaStream_t st,
+                  const double* pred) {
+  if (pb->op_kind == 0)
+    return hvp_apply(pb->A, pb->rows, pb->n, pb->lda, pb->d, v, pb->shift, y, pAp, 1, pb->ws_op, pb->ws_op_bytes,
+                     st, pred);
+  return dense_mv_apply(pb->A, pb->n, pb->lda, v, pb->shift, y, pAp, pb->ws_op, pb->ws_op_bytes, st, pred);
+}
+
+static int precondition(const nys_cg_problem* pb, cudaStream_t st, const double* pred) {
+  return precond_apply(pb->r > 0 ? pb->U : nullptr, pb->n, pb->r, pb->ldu, pb->lam, pb->nu, pb->res, pb->z,
+                       pb->res, pb->sc + NYS_CG_RZNEW, pb->ws_pc, pb->ws_pc_bytes, st, pred);
+}
+
+}  // namespace nys
+
+using namespace nys;
+
+extern "C" size_t nys_cg_workspace(int op_kind, int64_t rows, int64_t n, int r, size_t* ws_op, size_t* ws_pc) {
+  *ws_op = op_kind == 0 ? hvp_ws(rows, n) : dense_mv_ws(n);
+  *ws_pc = nys_precond_workspace(n, r);
+  return (kCgRedPartials * 16 + 64) * sizeof(double);
+}
+
+extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int count, void* stream) {
+  if (!pb || pb->n <= 0 || count < 0 || k_first < 1 || (pb->op_kind != 0 && pb->op_kind != 1)) return NYS_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = pb->n;
+  double* sc = pb->sc;
+  const double* pred = sc + NYS_CG_DONE;
+  // the cg_dir ticket lives in the spare slot of the scalar block
+  unsigned int* dir_counter = reinterpret_cast<unsigned int*>(sc + NYS_CG_TICKET);
+  int rc;
+  if (k_first == 1) {
+    cgp_begin_kernel<<<1, 32, 0, st>>>(sc, pb->tol, pb->max_iter);
+    NYS_CHECK_LAUNCH();
+    if ((rc = precondition(pb, st, pred))) return rc;
+    cgp_dir_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->z, pb->p, 1, sc, dir_counter);
+    NYS_CHECK_LAUNCH();
+  }
+  for (int64_t k = k_first; k < k_first + count && k <= pb->max_iter; ++k) {
+    const int refresh = (k % 50) == 0;  // krylov.py:16
+    if ((rc = matvec(pb, pb->p, pb->Ap, sc + NYS_CG_PAP, st, pred))) return rc;
+    cgp_step_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->x, pb->res, pb->p, pb->Ap, refresh, sc, pb->tol,
+                                                         k, pb->max_iter, cg_part(pb->ws_red), cg_counter(pb->ws_red));
+    NYS_CHECK_LAUNCH();
+    if (refresh) {
+      if ((rc = matvec(pb, pb->x, pb->Ap, nullptr, st, pred))) return rc;
+      cgp_restart_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->b, pb->Ap, pb->res, sc, pb->tol, k,
+                                                              pb->max_iter, cg_part(pb->ws_red),
+                                                              cg_counter(pb->ws_red));
+      NYS_CHECK_LAUNCH();
+    }
+    if ((rc = precondition(pb, st, pred))) return rc;
+    cgp_dir_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->z, pb->p, 0, sc, dir_counter);
+    NYS_CHECK_LAUNCH();
+  }
+  return NYS_OK;
+}

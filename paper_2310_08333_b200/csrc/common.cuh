@@ -14,11 +14,21 @@ namespace nys {
 extern unsigned long long g_launches;
 }
 
+namespace nys {
+// NYS_SYNC_DEBUG=1: synchronise after every launch and report the failing site
+int debug_sync_check(const char* file, int line);
+void debug_report(cudaError_t e, const char* file, int line);
+}
+
 #define NYS_CHECK_LAUNCH()                                   \
   do {                                                       \
     __atomic_fetch_add(&nys::g_launches, 1ull, __ATOMIC_RELAXED); \
     cudaError_t _e = cudaGetLastError();                     \
-    if (_e != cudaSuccess) return NYS_ERR_CUDA;              \
+    if (_e != cudaSuccess) {                                 \
+      nys::debug_report(_e, __FILE__, __LINE__);             \
+      return NYS_ERR_CUDA;                                   \
+    }                                                        \
+    if (nys::debug_sync_check(__FILE__, __LINE__)) return NYS_ERR_CUDA; \
   } while (0)
 
 namespace nys {

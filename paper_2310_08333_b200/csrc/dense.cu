@@ -12,6 +12,8 @@
 //     the thin SVD of sketch.py:126 via B^T B, and eigh of sketch.py:115).
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <vector>
 #include "common.cuh"
 
@@ -235,46 +237,52 @@ int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const do
 // ------------------------------------------------- small dense kernels ----
 // In-place lower Cholesky of the s x s matrix C (row-major), one CTA.
 // info = 0 on success, j+1 if the j-th pivot is not positive (LAPACK potf2).
+// Right-looking, column by column.  SMEM = true keeps the whole matrix in
+// shared memory (s <= 160); warps take trailing rows, lanes columns.
+template <bool SMEM>
 __global__ void __launch_bounds__(1024) cholesky_kernel(int s, double* C, int64_t ldc, int* info) {
+  extern __shared__ double csm[];
   __shared__ int fail;
   __shared__ double piv;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ld = SMEM ? (s | 1) : (int)ldc;
+  double* M = SMEM ? csm : C;
+  if (SMEM)
+    for (int t = threadIdx.x; t < s * s; t += blockDim.x) {
+      const int i = t / s, k = t - i * s;
+      if (k <= i) M[i * ld + k] = C[(int64_t)i * ldc + k];
+    }
   if (threadIdx.x == 0) fail = 0;
   __syncthreads();
   for (int j = 0; j < s; ++j) {
     if (threadIdx.x == 0) {
-      const double d = C[(int64_t)j * ldc + j];
-      if (!(d > 0.0) || isnan(d)) {
+      const double d = M[(int64_t)j * ld + j];
+      if (!(d > 0.0) || isnan(d)) {  // LAPACK potf2 failure rule
         fail = j + 1;
       } else {
         piv = sqrt(d);
-        C[(int64_t)j * ldc + j] = piv;
+        M[(int64_t)j * ld + j] = piv;
       }
     }
     __syncthreads();
     if (fail) break;
     const double pj = piv;
-    for (int i = j + 1 + threadIdx.x; i < s; i += blockDim.x) C[(int64_t)i * ldc + j] /= pj;
+    for (int i = j + 1 + threadIdx.x; i < s; i += blockDim.x) M[(int64_t)i * ld + j] /= pj;
     __syncthreads();
-    // trailing update of the lower triangle: C[i][k] -= C[i][j] C[k][j], j < k <= i
-    const int m = s - j - 1;
-    const int64_t tot = (int64_t)m * (m + 1) / 2;
-    for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
-      // map t -> (a, b) with 0 <= b <= a < m
-      int a = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-      while ((int64_t)a * (a + 1) / 2 > t) --a;
-      while ((int64_t)(a + 1) * (a + 2) / 2 <= t) ++a;
-      const int b = (int)(t - (int64_t)a * (a + 1) / 2);
-      const int i = j + 1 + a, k = j + 1 + b;
-      C[(int64_t)i * ldc + k] -= C[(int64_t)i * ldc + j] * C[(int64_t)k * ldc + j];
+    // trailing update of the lower triangle: M[i][k] -= M[i][j] M[k][j], j < k <= i
+    for (int i = j + 1 + warp; i < s; i += nw) {
+      const double lij = M[(int64_t)i * ld + j];
+      for (int k = j + 1 + lane; k <= i; k += 32) M[(int64_t)i * ld + k] -= lij * M[(int64_t)k * ld + j];
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) *info = fail;
   __syncthreads();
-  if (!fail) {  // zero the strict upper triangle
+  if (!fail) {  // write back the lower factor, zero the strict upper triangle
     for (int64_t t = threadIdx.x; t < (int64_t)s * s; t += blockDim.x) {
       const int i = (int)(t / s), k = (int)(t % s);
       if (k > i) C[(int64_t)i * ldc + k] = 0.0;
+      else if (SMEM) C[(int64_t)i * ldc + k] = M[(int64_t)i * ld + k];
     }
   }
 }
@@ -386,7 +394,17 @@ size_t syevj_ws(int s);
 int syevj(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes, cudaStream_t st);
 
 static int cholesky(int s, double* C, int* info_dev, int* info_host, cudaStream_t st) {
-  cholesky_kernel<<<1, 1024, 0, st>>>(s, C, s, info_dev);
+  const size_t smem = (size_t)s * (s | 1) * sizeof(double);
+  if (smem <= 210 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(cholesky_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+      attr = true;
+    }
+    cholesky_kernel<true><<<1, 1024, smem, st>>>(s, C, s, info_dev);
+  } else {
+    cholesky_kernel<false><<<1, 1024, 0, st>>>(s, C, s, info_dev);
+  }
   NYS_CHECK_LAUNCH();
   if (cudaMemcpyAsync(info_host, info_dev, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return NYS_ERR_CUDA;
@@ -626,6 +644,22 @@ extern "C" int nys_syevj_f64(int s, double* A, double* V, double* w, void* ws, s
 
 // ------------------------------------------------------------- misc -------
 unsigned long long nys::g_launches = 0ull;
+
+void nys::debug_report(cudaError_t e, const char* file, int line) {
+  static const bool on = getenv("NYS_SYNC_DEBUG") != nullptr;
+  if (on) fprintf(stderr, "[nys] launch error at %s:%d: %s\n", file, line, cudaGetErrorString(e));
+}
+
+int nys::debug_sync_check(const char* file, int line) {
+  static const bool on = getenv("NYS_SYNC_DEBUG") != nullptr;
+  if (!on) return 0;
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[nys] CUDA error after launch at %s:%d: %s\n", file, line, cudaGetErrorString(e));
+    return 1;
+  }
+  return 0;
+}
 
 extern "C" int nys_abi_version(void) { return NYS_ABI_VERSION; }
 

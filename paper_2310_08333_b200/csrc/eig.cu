@@ -440,8 +440,17 @@ __global__ void jacobi_finish_kernel(int s, const double* __restrict__ Xc, const
   }
 }
 
+size_t eig_tri_ws(int s);
+int eig_tri(int s, const double* A, double* V, double* w, void* ws, cudaStream_t st);
+// s <= 160: tridiagonal path (eig_tri.cu) unless NYS_EIG=jacobi selects the
+// single-CTA two-sided Jacobi (kept for cross-checking)
+static bool use_jacobi_small() {
+  static const bool j = getenv("NYS_EIG") && getenv("NYS_EIG")[0] == 'j';
+  return j;
+}
+
 size_t syevj_ws(int s) {
-  if (s <= kJ2MaxM) return jacobi2_ws(s);
+  if (s <= kJ2MaxM) return tmax(jacobi2_ws(s), eig_tri_ws(s));
   const EigGeom g = eig_geom(s);
   return 2 * (size_t)g.nb * g.b * s * sizeof(double) + 2 * (size_t)s * sizeof(double) + 4096;
 }
@@ -450,7 +459,7 @@ size_t syevj_ws(int s) {
 // V columns are eigenvectors, w descending.
 int syevj(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (ws_bytes < syevj_ws(s)) return NYS_ERR_WORKSPACE;
-  if (s <= kJ2MaxM) return jacobi2(s, A, V, w, ws, st);
+  if (s <= kJ2MaxM) return use_jacobi_small() ? jacobi2(s, A, V, w, ws, st) : eig_tri(s, A, V, w, ws, st);
   const EigGeom g = eig_geom(s);
   if (g.smem > 210 * 1024) return NYS_ERR_UNSUPPORTED;
   const int ncols = g.nb * g.b;

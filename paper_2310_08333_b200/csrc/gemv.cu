@@ -27,7 +27,9 @@ template <int K, int RW, int U, bool VEC>
 __global__ void __launch_bounds__(kGemvThreads, 2)
 gemv_n_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
               const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
-              const double* __restrict__ dscale, int splits, int64_t chunk) {
+              const double* __restrict__ dscale, int splits, int64_t chunk,
+              const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;  // device-predicated launch (CG batches)
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t ngroups = cdiv(rows, RW);
@@ -132,7 +134,8 @@ gemv_n_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda
 // Y[j*ldy + i] = (sum_s P[(s*K + j)*rows + i]) * (dscale ? dscale[i] : 1)
 __global__ void gemv_n_reduce(const double* __restrict__ P, int64_t rows, int K, int splits,
                               double* __restrict__ Y, int64_t ldy,
-                              const double* __restrict__ dscale) {
+                              const double* __restrict__ dscale, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
   const int64_t total = rows * K;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -169,7 +172,7 @@ static int gemv_variant(int K) {
 template <int K, int RW, int U>
 static int gemv_n_launch_v(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X,
                            int64_t ldx, double* Y, int64_t ldy, const double* dscale, double* ws,
-                           size_t ws_bytes, cudaStream_t st) {
+                           size_t ws_bytes, cudaStream_t st, const double* pred) {
   int splits;
   int64_t chunk;
   gemv_n_plan(rows, n, RW, splits, chunk);
@@ -185,15 +188,15 @@ static int gemv_n_launch_v(const double* A, int64_t rows, int64_t n, int64_t lda
   double* out = splits == 1 ? Y : ws;
   if (vec)
     gemv_n_kernel<K, RW, U, true><<<(unsigned)blocks, kGemvThreads, 0, st>>>(
-        A, rows, n, lda, X, ldx, out, ldy, dscale, splits, chunk);
+        A, rows, n, lda, X, ldx, out, ldy, dscale, splits, chunk, pred);
   else
     gemv_n_kernel<K, RW, 1, false><<<(unsigned)blocks, kGemvThreads, 0, st>>>(
-        A, rows, n, lda, X, ldx, out, ldy, dscale, splits, chunk);
+        A, rows, n, lda, X, ldx, out, ldy, dscale, splits, chunk, pred);
   NYS_CHECK_LAUNCH();
   if (splits > 1) {
     const int64_t total = rows * K;
     const int64_t rb = tmin<int64_t>(cdiv(total, 256), kNumSMs * 8);
-    gemv_n_reduce<<<(unsigned)rb, 256, 0, st>>>(ws, rows, K, splits, Y, ldy, dscale);
+    gemv_n_reduce<<<(unsigned)rb, 256, 0, st>>>(ws, rows, K, splits, Y, ldy, dscale, pred);
     NYS_CHECK_LAUNCH();
   }
   return NYS_OK;
@@ -202,25 +205,25 @@ static int gemv_n_launch_v(const double* A, int64_t rows, int64_t n, int64_t lda
 template <int K>
 static int gemv_n_launch(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X,
                          int64_t ldx, double* Y, int64_t ldy, const double* dscale, double* ws,
-                         size_t ws_bytes, cudaStream_t st) {
+                         size_t ws_bytes, cudaStream_t st, const double* pred) {
   switch (gemv_variant(K)) {
-    case 0: return gemv_n_launch_v<K, 4, 2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
-    case 1: return gemv_n_launch_v<K, 4, 1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
-    case 2: return gemv_n_launch_v<K, 2, 2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
-    case 3: return gemv_n_launch_v<K, 2, 1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
-    default: return gemv_n_launch_v<K, 1, 4>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st);
+    case 0: return gemv_n_launch_v<K, 4, 2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st, pred);
+    case 1: return gemv_n_launch_v<K, 4, 1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st, pred);
+    case 2: return gemv_n_launch_v<K, 2, 2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st, pred);
+    case 3: return gemv_n_launch_v<K, 2, 1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st, pred);
+    default: return gemv_n_launch_v<K, 1, 4>(A, rows, n, lda, X, ldx, Y, ldy, dscale, ws, ws_bytes, st, pred);
   }
 }
 
 int gemv_n(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X, int64_t ldx,
            int k, double* Y, int64_t ldy, const double* dscale, void* ws, size_t ws_bytes,
-           cudaStream_t st) {
+           cudaStream_t st, const double* pred = nullptr) {
   double* w = reinterpret_cast<double*>(ws);
   switch (k) {
-    case 1: return gemv_n_launch<1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st);
-    case 2: return gemv_n_launch<2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st);
-    case 3: return gemv_n_launch<3>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st);
-    case 4: return gemv_n_launch<4>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st);
+    case 1: return gemv_n_launch<1>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st, pred);
+    case 2: return gemv_n_launch<2>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st, pred);
+    case 3: return gemv_n_launch<3>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st, pred);
+    case 4: return gemv_n_launch<4>(A, rows, n, lda, X, ldx, Y, ldy, dscale, w, ws_bytes, st, pred);
     default: return NYS_ERR_ARG;
   }
 }
@@ -241,7 +244,8 @@ template <int K, bool VEC>
 __global__ void __launch_bounds__(kGemvTThreads)
 gemv_t_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
               const double* __restrict__ T, int64_t ldt, double* __restrict__ out, int64_t ldo,
-              int64_t rows_per_split, int direct) {
+              int64_t rows_per_split, int direct, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
   __shared__ double tsh[K][kGemvTTile];
   constexpr int CPT = VEC ? 2 : 1;  // columns per thread
   const int64_t c = ((int64_t)blockIdx.x * kGemvTThreads + threadIdx.x) * CPT;
@@ -315,21 +319,38 @@ gemv_t_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda
 __global__ void gemv_t_reduce(const double* __restrict__ P, int64_t n, int K, int splits,
                               double* __restrict__ Y, int64_t ldy, const double* __restrict__ v,
                               double shift, double* __restrict__ dot, double* __restrict__ part,
-                              unsigned int* counter) {
+                              unsigned int* counter, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  // 256 threads = 32 consecutive outputs x 8 split-chunks (split s goes to chunk
+  // s % 8); chunk sums are combined in a fixed order -> deterministic
   __shared__ double sh[32];
+  __shared__ double cs[8][33];
   double d[1] = {0.0};
+  const int cx = threadIdx.x & 31, q = threadIdx.x >> 5;
   const int64_t total = n * K;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(t / n);
-    const int64_t c = t - (int64_t)j * n;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < total; base += (int64_t)gridDim.x * 32) {
+    const int64_t t = base + cx;
+    int j = 0;
+    int64_t c = 0;
     double acc = 0.0;
-    for (int s = 0; s < splits; ++s) acc += P[((int64_t)s * K + j) * n + c];
-    if (v) {
-      acc += shift * v[c];
-      if (dot) d[0] = fma(v[c], acc, d[0]);
+    if (t < total) {
+      j = (int)(t / n);
+      c = t - (int64_t)j * n;
+      for (int s = q; s < splits; s += 8) acc += P[((int64_t)s * K + j) * n + c];
     }
-    Y[j * ldy + c] = acc;
+    cs[q][cx] = acc;
+    __syncthreads();
+    if (q == 0 && t < total) {
+      double a = cs[0][cx];
+#pragma unroll
+      for (int qq = 1; qq < 8; ++qq) a += cs[qq][cx];
+      if (v) {
+        a += shift * v[c];
+        if (dot) d[0] = fma(v[c], a, d[0]);
+      }
+      Y[j * ldy + c] = a;
+    }
+    __syncthreads();
   }
   if (!dot) return;
   block_sum<1>(d, sh);
@@ -361,7 +382,8 @@ inline unsigned int* red_counter(void* ws) {
 template <int K>
 static int gemv_t_launch(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T,
                          int64_t ldt, double* Y, int64_t ldy, const double* v, double shift,
-                         double* dot, void* ws, size_t ws_bytes, cudaStream_t st) {
+                         double* dot, void* ws, size_t ws_bytes, cudaStream_t st,
+                         const double* pred) {
   const bool vec = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
                    ((ldy & 1) == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
   int splits;
@@ -382,16 +404,16 @@ static int gemv_t_launch(const double* A, int64_t rows, int64_t n, int64_t lda, 
   if (vec)
     gemv_t_kernel<K, true><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt,
                                                            direct ? Y : P, direct ? ldy : n,
-                                                           rps, direct ? 1 : 0);
+                                                           rps, direct ? 1 : 0, pred);
   else
     gemv_t_kernel<K, false><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt,
                                                             direct ? Y : P, direct ? ldy : n,
-                                                            rps, direct ? 1 : 0);
+                                                            rps, direct ? 1 : 0, pred);
   NYS_CHECK_LAUNCH();
   if (!direct) {
-    const int64_t rb = tmin<int64_t>(cdiv(n * K, 256), kRedPartials);
+    const int64_t rb = tmin<int64_t>(cdiv(n * K, 32), kRedPartials);
     gemv_t_reduce<<<(unsigned)rb, 256, 0, st>>>(P, n, K, splits, Y, ldy, v, shift, dot,
-                                                red_part(ws), red_counter(ws));
+                                                red_part(ws), red_counter(ws), pred);
     NYS_CHECK_LAUNCH();
   }
   return NYS_OK;
@@ -399,12 +421,12 @@ static int gemv_t_launch(const double* A, int64_t rows, int64_t n, int64_t lda, 
 
 int gemv_t(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt,
            int k, double* Y, int64_t ldy, const double* v, double shift, double* dot, void* ws,
-           size_t ws_bytes, cudaStream_t st) {
+           size_t ws_bytes, cudaStream_t st, const double* pred = nullptr) {
   switch (k) {
-    case 1: return gemv_t_launch<1>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st);
-    case 2: return gemv_t_launch<2>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st);
-    case 3: return gemv_t_launch<3>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st);
-    case 4: return gemv_t_launch<4>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st);
+    case 1: return gemv_t_launch<1>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st, pred);
+    case 2: return gemv_t_launch<2>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st, pred);
+    case 3: return gemv_t_launch<3>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st, pred);
+    case 4: return gemv_t_launch<4>(A, rows, n, lda, T, ldt, Y, ldy, v, shift, dot, ws, ws_bytes, st, pred);
     default: return NYS_ERR_ARG;
   }
 }
@@ -422,7 +444,9 @@ size_t gemv_t_ws(int64_t rows, int64_t n, int k) {
 // --------------------------------------------------------- small vectors ----
 __global__ void shift_dot_kernel(int64_t n, const double* __restrict__ v, double shift,
                                  double* __restrict__ y, double* __restrict__ dot,
-                                 double* __restrict__ part, unsigned int* counter) {
+                                 double* __restrict__ part, unsigned int* counter,
+                                 const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
   __shared__ double sh[32];
   double d[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -448,7 +472,68 @@ int shift_dot(int64_t n, const double* v, double shift, double* y, double* dot, 
   if (n <= 0) return NYS_ERR_ARG;
   const int64_t blocks = tmin<int64_t>(cdiv(n, 256), kNumSMs * 4);
   shift_dot_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, v, shift, y, dot, red_part(ws),
-                                                     red_counter(ws));
+                                                     red_counter(ws), nullptr);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+struct HvpPlan {
+  int C, W, K, S, nclusters;
+  size_t smem;
+  bool ok;
+};
+HvpPlan hvp_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
+int hvp_fused(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
+              const double* v, double* ypart, cudaStream_t st, const double* pred);
+
+size_t hvp_ws(int64_t rows, int64_t n) {
+  // two-pass: t = d o (A v) (rows doubles) + the K1 split partials + the K2 workspace
+  const size_t two = cdiv(rows, 2) * 2 * sizeof(double) + gemv_n_ws(rows, n, 1) + gemv_t_ws(rows, n, 1);
+  // single pass: reduction scratch + one y partial per cluster (<= 148)
+  const size_t one = kRedBytes + (size_t)kNumSMs * n * sizeof(double);
+  return tmax(two, one);
+}
+
+// y = A^T(d o Av) (+ shift v, pAp = v.y when finish); every launch predicated on *pred == 0
+int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const double* d, const double* v,
+              double shift, double* y, double* pAp, int finish, void* ws, size_t ws_bytes, cudaStream_t st,
+              const double* pred) {
+  if (ws_bytes < hvp_ws(rows, n)) return NYS_ERR_WORKSPACE;
+  static const bool two_pass_only = getenv("NYS_HVP_TWOPASS") != nullptr;
+  const HvpPlan plan = hvp_plan(rows, n, lda, A, v);
+  if (plan.ok && !two_pass_only) {
+    // single pass over A (csrc/hvp.cu), then a fixed-order sum of the cluster partials
+    double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
+    int rc = hvp_fused(plan, A, rows, n, lda, d, v, P, st, pred);
+    if (rc) return rc;
+    const int64_t rb = tmin<int64_t>(cdiv(n, 32), kRedPartials);
+    gemv_t_reduce<<<(unsigned)rb, 256, 0, st>>>(P, n, 1, plan.nclusters, y, n, finish ? v : nullptr, shift,
+                                                 finish ? pAp : nullptr, red_part(ws), red_counter(ws), pred);
+    NYS_CHECK_LAUNCH();
+    return NYS_OK;
+  }
+  char* base = reinterpret_cast<char*>(ws);
+  // layout: [K2 ws (reduction scratch first)] [t] [K1 partials]
+  const size_t wt = gemv_t_ws(rows, n, 1);
+  double* t = reinterpret_cast<double*>(base + wt);
+  void* wn = base + wt + cdiv(rows, 2) * 2 * sizeof(double);
+  int rc = gemv_n(A, rows, n, lda, v, n, 1, t, rows, d, wn, gemv_n_ws(rows, n, 1), st, pred);
+  if (rc) return rc;
+  if (finish) return gemv_t(A, rows, n, lda, t, rows, 1, y, n, v, shift, pAp, base, wt, st, pred);
+  return gemv_t(A, rows, n, lda, t, rows, 1, y, n, nullptr, 0.0, nullptr, base, wt, st, pred);
+}
+
+size_t dense_mv_ws(int64_t n) { return kRedBytes + gemv_n_ws(n, n, 1) + 256; }
+
+// y = P v + shift v, pAp = v.y  (QP operator of admm.py:262-263 with P dense)
+int dense_mv_apply(const double* P, int64_t n, int64_t ldp, const double* v, double shift, double* y, double* pAp,
+                   void* ws, size_t ws_bytes, cudaStream_t st, const double* pred) {
+  if (ws_bytes < dense_mv_ws(n)) return NYS_ERR_WORKSPACE;
+  char* base = reinterpret_cast<char*>(ws);
+  int rc = gemv_n(P, n, n, ldp, v, n, 1, y, n, nullptr, base + kRedBytes, gemv_n_ws(n, n, 1), st, pred);
+  if (rc) return rc;
+  const int64_t blocks = tmin<int64_t>(cdiv(n, 256), kNumSMs * 4);
+  shift_dot_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, v, shift, y, pAp, red_part(ws), red_counter(ws), pred);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -487,54 +572,13 @@ extern "C" int nys_gemvT_f64(const double* A, int64_t rows, int64_t n, int64_t l
                 as_stream(stream));
 }
 
-namespace nys {
-struct HvpPlan {
-  int C, W, K, S, nclusters;
-  size_t smem;
-  bool ok;
-};
-HvpPlan hvp_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
-int hvp_fused(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
-              const double* v, double* ypart, cudaStream_t st);
-}  // namespace nys
-
-extern "C" size_t nys_hvp_workspace(int64_t rows, int64_t n) {
-  // two-pass: t = d o (A v) (rows doubles) + the K1 split partials + the K2 workspace
-  const size_t two = cdiv(rows, 2) * 2 * sizeof(double) + gemv_n_ws(rows, n, 1) + gemv_t_ws(rows, n, 1);
-  // single pass: reduction scratch + one y partial per cluster (<= 148)
-  const size_t one = kRedBytes + (size_t)kNumSMs * n * sizeof(double);
-  return tmax(two, one);
-}
+extern "C" size_t nys_hvp_workspace(int64_t rows, int64_t n) { return hvp_ws(rows, n); }
 
 extern "C" int nys_hvp_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
                            const double* v, double shift, double* y, double* pAp, int finish,
                            void* ws, size_t ws_bytes, void* stream) {
   if (rows <= 0 || n <= 0 || lda < n) return NYS_ERR_ARG;
-  if (ws_bytes < nys_hvp_workspace(rows, n)) return NYS_ERR_WORKSPACE;
-  cudaStream_t st = as_stream(stream);
-  static const bool two_pass_only = getenv("NYS_HVP_TWOPASS") != nullptr;
-  const HvpPlan plan = hvp_plan(rows, n, lda, A, v);
-  if (plan.ok && !two_pass_only) {
-    // single pass over A (csrc/hvp.cu), then a fixed-order sum of the cluster partials
-    double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
-    int rc = hvp_fused(plan, A, rows, n, lda, d, v, P, st);
-    if (rc) return rc;
-    const int64_t rb = tmin<int64_t>(cdiv(n, 256), kRedPartials);
-    gemv_t_reduce<<<(unsigned)rb, 256, 0, st>>>(P, n, 1, plan.nclusters, y, n, finish ? v : nullptr,
-                                                 shift, finish ? pAp : nullptr, red_part(ws), red_counter(ws));
-    NYS_CHECK_LAUNCH();
-    return NYS_OK;
-  }
-  char* base = reinterpret_cast<char*>(ws);
-  // layout: [K2 ws (reduction scratch first)] [t] [K1 partials]
-  const size_t wt = gemv_t_ws(rows, n, 1);
-  double* t = reinterpret_cast<double*>(base + wt);
-  void* wn = base + wt + cdiv(rows, 2) * 2 * sizeof(double);
-  int rc = gemv_n(A, rows, n, lda, v, n, 1, t, rows, d, wn, gemv_n_ws(rows, n, 1), st);
-  if (rc) return rc;
-  if (finish)
-    return gemv_t(A, rows, n, lda, t, rows, 1, y, n, v, shift, pAp, base, wt, st);
-  return gemv_t(A, rows, n, lda, t, rows, 1, y, n, nullptr, 0.0, nullptr, base, wt, st);
+  return hvp_apply(A, rows, n, lda, d, v, shift, y, pAp, finish, ws, ws_bytes, as_stream(stream), nullptr);
 }
 
 extern "C" int nys_shift_dot_f64(int64_t n, const double* v, double shift, double* y,

@@ -124,22 +124,38 @@ __global__ void __launch_bounds__(kPcThreads)
 precond_utv_kernel(const double* __restrict__ U, int64_t n, int r, int64_t ldu,
                    const double* __restrict__ v, int64_t rows_per_block, double* part,
                    unsigned int* counter, const double* __restrict__ lam, double nu,
-                   double* __restrict__ coef) {
+                   double* __restrict__ coef, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  // each warp streams whole rows of U (r contiguous doubles, coalesced); lane
+  // l accumulates columns l, l+32, ... ; warps are combined in a fixed order
+  extern __shared__ double wsum[];  // (kPcThreads/32) x r
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kPcThreads / 32;
+  constexpr int MAXC = 16;  // r <= 512
+  double acc[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
   const int64_t i0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t i1 = min(n, i0 + rows_per_block);
-  for (int j = threadIdx.x; j < r; j += kPcThreads) {
-    double acc = 0.0;
-    int64_t i = i0;
-    for (; i + 4 <= i1; i += 4) {
-      const double u0 = U[i * ldu + j], u1 = U[(i + 1) * ldu + j];
-      const double u2 = U[(i + 2) * ldu + j], u3 = U[(i + 3) * ldu + j];
-      acc = fma(u0, v[i], acc);
-      acc = fma(u1, v[i + 1], acc);
-      acc = fma(u2, v[i + 2], acc);
-      acc = fma(u3, v[i + 3], acc);
+  for (int64_t i = i0 + warp; i < i1; i += NW) {
+    const double vi = v[i];
+    const double* ui = U + i * ldu;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int j = lane + 32 * c;
+      if (j < r) acc[c] = fma(ui[j], vi, acc[c]);
     }
-    for (; i < i1; ++i) acc = fma(U[i * ldu + j], v[i], acc);
-    part[(int64_t)blockIdx.x * r + j] = acc;
+  }
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    const int j = lane + 32 * c;
+    if (j < r) wsum[warp * r + j] = acc[c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < r; j += kPcThreads) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += wsum[w * r + j];
+    part[(int64_t)blockIdx.x * r + j] = s;
   }
   if (last_block(counter)) {
     const double lr = lam[r - 1] + nu;
@@ -157,7 +173,8 @@ __global__ void __launch_bounds__(256)
 precond_apply_kernel(const double* __restrict__ U, int64_t n, int r, int64_t ldu,
                      const double* __restrict__ coef, const double* __restrict__ v,
                      double* __restrict__ z, const double* __restrict__ rdot, double* rz,
-                     double* part, unsigned int* counter) {
+                     double* part, unsigned int* counter, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
   extern __shared__ double csh[];
   for (int j = threadIdx.x; j < r; j += blockDim.x) csh[j] = coef[j];
   __syncthreads();
@@ -183,7 +200,8 @@ precond_apply_kernel(const double* __restrict__ U, int64_t n, int r, int64_t ldu
 
 __global__ void copy_dot_kernel(int64_t n, const double* __restrict__ v, double* __restrict__ z,
                                 const double* __restrict__ rdot, double* rz, double* part,
-                                unsigned int* counter) {
+                                unsigned int* counter, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
   double s[1] = {0.0}, m[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -232,7 +250,9 @@ __device__ __forceinline__ double soft1(double v, double kappa) {
 __global__ void admm_zu_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ z,
                                double* __restrict__ u, double alpha, int prox_kind, double kappa,
                                const double* __restrict__ lo, const double* __restrict__ hi,
-                               double* __restrict__ xbar, double* __restrict__ zbar, int accum) {
+                               double* __restrict__ xbar, double* __restrict__ zbar, int accum,
+                               const double* __restrict__ pred = nullptr) {
+  if (pred && *pred != 0.0) return;
   const double beta = 1.0 - alpha;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -261,7 +281,8 @@ __global__ void admm_norms_kernel(int64_t n, const double* __restrict__ x,
                                   double lambda2, double rho, const double* __restrict__ atnu,
                                   double lambda1, const double* __restrict__ lo,
                                   const double* __restrict__ hi, double* out, double* part,
-                                  unsigned int* counter) {
+                                  unsigned int* counter, const double* __restrict__ pred = nullptr) {
+  if (pred && *pred != 0.0) return;
   // sums: (x-z)^2, rd^2, x^2, z^2, (rho u)^2, |z|, x.gA, q.x, (|atnu|-l1)_+^2
   // maxes: |x-z|, |rd|, |x|, |z|, |rho u|, |atnu|, box violation (shifted by +inf guard)
   double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -347,7 +368,9 @@ __global__ void ml_rowwise_kernel(int64_t rows, int loss, const double* __restri
                                   const double* __restrict__ Az, const double* __restrict__ b,
                                   double* __restrict__ tg, double* __restrict__ w,
                                   double* __restrict__ thx, double* __restrict__ tnu, double* out,
-                                  double* part, unsigned int* counter) {
+                                  double* part, unsigned int* counter,
+                                  const double* __restrict__ pred = nullptr) {
+  if (pred && *pred != 0.0) return;
   double s[5] = {0, 0, 0, 0, 0}, m[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -397,7 +420,9 @@ struct SlotList {
 
 __global__ void window_norms_kernel(int64_t n, const double* __restrict__ ring, int64_t ld,
                                     int cur, SlotList others, int nothers, double* out,
-                                    double* part, unsigned int* counter) {
+                                    double* part, unsigned int* counter,
+                                    const double* __restrict__ pred = nullptr) {
+  if (pred && *pred != 0.0) return;
   double s[17], m[1] = {0.0};
 #pragma unroll
   for (int j = 0; j < 17; ++j) s[j] = 0.0;
@@ -441,7 +466,9 @@ __global__ void qp_infeas_kernel(int64_t n, const double* __restrict__ xa,
                                  const double* __restrict__ ub, double width,
                                  const double* __restrict__ lo, const double* __restrict__ hi,
                                  const double* __restrict__ q, double* __restrict__ dx,
-                                 double* out, double* part, unsigned int* counter) {
+                                 double* out, double* part, unsigned int* counter,
+                                 const double* __restrict__ pred = nullptr) {
+  if (pred && *pred != 0.0) return;
   double s[6] = {0, 0, 0, 0, 0, 0}, m[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -468,6 +495,27 @@ __global__ void qp_infeas_kernel(int64_t n, const double* __restrict__ xa,
   }
   const int os[6] = {0, 1, 2, 3, 4, 5}, om[1] = {0};
   grid_reduce<6, 0>(s, m, part, counter, out, os, om);
+}
+
+// ring[slot] = x (and uring[slot] = u): window copies, predicated
+__global__ void ring_copy_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ dx,
+                                 const double* __restrict__ u, double* __restrict__ du,
+                                 const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    dx[i] = x[i];
+    if (du) du[i] = u[i];
+  }
+}
+
+__global__ void dot_pred_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* out,
+                                double* part, unsigned int* counter, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  double s[1] = {0.0}, m[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s[0] = fma(a[i], b[i], s[0]);
+  const int os[1] = {0}, om[1] = {0};
+  grid_reduce<1, 0>(s, m, part, counter, out, os, om);
 }
 
 __global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, double b,
@@ -551,32 +599,41 @@ extern "C" size_t nys_precond_workspace(int64_t n, int r) {
          (size_t)kVecMaxBlocks * (r + 1) * sizeof(double);
 }
 
-extern "C" int nys_precond_apply_f64(const double* U, int64_t n, int r, int64_t ldu,
-                                     const double* lam, double nu, const double* v, double* z,
-                                     const double* rdot, double* rz, void* ws, size_t ws_bytes,
-                                     void* stream) {
-  cudaStream_t st = as_stream(stream);
+namespace nys {
+// Eq. (11) apply, every launch predicated on *pred == 0 (nullptr: always run)
+int precond_apply(const double* U, int64_t n, int r, int64_t ldu, const double* lam, double nu,
+                  const double* v, double* z, const double* rdot, double* rz, void* ws, size_t ws_bytes,
+                  cudaStream_t st, const double* pred) {
   if (n <= 0 || r < 0 || (r > 0 && ldu < r)) return NYS_ERR_ARG;
   if (ws_bytes < nys_precond_workspace(n, r)) return NYS_ERR_WORKSPACE;
   if (r == 0) {
-    copy_dot_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, v, z, rdot, rz, RED_ARGS(ws));
+    copy_dot_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, v, z, rdot, rz, RED_ARGS(ws), pred);
     NYS_CHECK_LAUNCH();
     return NYS_OK;
   }
   double* coef = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) +
                                            (kRedPartials * 16 + 64) * sizeof(double));
   double* hpart = coef + (r + 1);
-  const int64_t blocks = tmin<int64_t>(kVecMaxBlocks, tmax<int64_t>(1, cdiv(n, 16)));
+  if (r > 512) return NYS_ERR_UNSUPPORTED;
+  const int64_t blocks = tmin<int64_t>(kNumSMs * 2, tmax<int64_t>(1, cdiv(n, 32)));
   const int64_t rpb = cdiv(n, blocks);
   const int64_t nb = cdiv(n, rpb);
-  precond_utv_kernel<<<(unsigned)nb, kPcThreads, 0, st>>>(U, n, r, ldu, v, rpb, hpart,
-                                                          red_counter(ws), lam, nu, coef);
+  precond_utv_kernel<<<(unsigned)nb, kPcThreads, (kPcThreads / 32) * r * sizeof(double), st>>>(
+      U, n, r, ldu, v, rpb, hpart, red_counter(ws), lam, nu, coef, pred);
   NYS_CHECK_LAUNCH();
   const int64_t ab = tmin<int64_t>(kVecMaxBlocks, cdiv(n * 32, 256));
   precond_apply_kernel<<<(unsigned)ab, 256, r * sizeof(double), st>>>(U, n, r, ldu, coef, v, z,
-                                                                      rdot, rz, RED_ARGS(ws));
+                                                                      rdot, rz, RED_ARGS(ws), pred);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
+}
+}  // namespace nys
+
+extern "C" int nys_precond_apply_f64(const double* U, int64_t n, int r, int64_t ldu,
+                                     const double* lam, double nu, const double* v, double* z,
+                                     const double* rdot, double* rz, void* ws, size_t ws_bytes,
+                                     void* stream) {
+  return precond_apply(U, n, r, ldu, lam, nu, v, z, rdot, rz, ws, ws_bytes, as_stream(stream), nullptr);
 }
 
 extern "C" int nys_admm_rhs_f64(int64_t n, const double* hxA, const double* gA, const double* q,
@@ -693,5 +750,86 @@ extern "C" int nys_row_scale_f64(int64_t rows, int64_t cols, double* X, int64_t 
   row_scale_kernel<<<vec_blocks(rows * cols), kVecThreads, 0, as_stream(stream)>>>(rows, cols, X,
                                                                                    ldx, d);
   NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+// ------------------------------------------------------ ADMM tail ---------
+namespace nys {
+int gemv_n(const double* A, int64_t rows, int64_t n, int64_t lda, const double* X, int64_t ldx, int k, double* Y,
+           int64_t ldy, const double* dscale, void* ws, size_t ws_bytes, cudaStream_t st, const double* pred);
+int gemv_t(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt, int k, double* Y,
+           int64_t ldy, const double* v, double shift, double* dot, void* ws, size_t ws_bytes, cudaStream_t st,
+           const double* pred);
+}  // namespace nys
+
+extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
+  if (!t || t->n <= 0 || (t->kind != 0 && t->kind != 1)) return NYS_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = t->n;
+  const double* pred = t->pred;
+  double* x = t->XZ;
+  double* z = t->XZ + n;
+  int rc;
+  // relax / prox / dual update + averages (admm.py:562-583)
+  admm_zu_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, z, t->u, t->alpha, t->kind == 0 ? NYS_PROX_SOFT
+                                                                                               : NYS_PROX_BOX,
+                                                        t->kappa, t->lo, t->hi, t->xbar, t->zbar, t->accum, pred);
+  NYS_CHECK_LAUNCH();
+  // window append (admm.py:622-623), speculative: the host commits it
+  if (t->ring) {
+    ring_copy_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, t->ring + (int64_t)t->slot * t->ring_ld, t->u,
+                                                            t->uring ? t->uring + (int64_t)t->slot * t->ring_ld
+                                                                     : nullptr,
+                                                            pred);
+    NYS_CHECK_LAUNCH();
+  }
+  // data passes at (x, z) (admm.py:585-587)
+  if (t->kind == 0) {
+    const int k = t->with_z ? 2 : 1;
+    if ((rc = gemv_n(t->A, t->rows, n, t->lda, t->XZ, n, k, t->AXZ, t->rows, nullptr, t->ws_gemv, t->ws_gemv_bytes,
+                     st, pred)))
+      return rc;
+    ml_rowwise_kernel<<<vec_blocks(t->rows), kVecThreads, 0, st>>>(
+        t->rows, t->loss, t->AXZ, t->with_z ? t->AXZ + t->rows : nullptr, t->b, t->T, t->w, t->T + t->rows,
+        t->with_z ? t->T + 2 * t->rows : nullptr, t->rowsums, red_part(t->ws_red), red_counter(t->ws_red), pred);
+    NYS_CHECK_LAUNCH();
+    if ((rc = gemv_t(t->A, t->rows, n, t->lda, t->T, t->rows, t->with_z ? 3 : 2, t->AT, n, nullptr, 0.0, nullptr,
+                     t->ws_gemvT, t->ws_gemvT_bytes, st, pred)))
+      return rc;
+    admm_norms_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, z, t->u, t->AT, nullptr, t->lambda2, t->rho,
+                                                             t->with_z ? t->AT + 2 * n : nullptr, t->lambda1,
+                                                             nullptr, nullptr, t->norms, red_part(t->ws_red),
+                                                             red_counter(t->ws_red), pred);
+    NYS_CHECK_LAUNCH();
+  } else {
+    if ((rc = gemv_n(t->A, n, n, t->lda, x, n, 1, t->AT, n, nullptr, t->ws_gemv, t->ws_gemv_bytes, st, pred)))
+      return rc;
+    admm_norms_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, z, t->u, t->AT, t->q, 0.0, t->rho, nullptr, 0.0,
+                                                             t->lo, t->hi, t->norms, red_part(t->ws_red),
+                                                             red_counter(t->ws_red), pred);
+    NYS_CHECK_LAUNCH();
+  }
+  // cycle-guard norms for the window after the append (admm.py:645-655)
+  if (t->ring && t->nothers > 0) {
+    SlotList sl;
+    for (int j = 0; j < 16; ++j) sl.idx[j] = j < t->nothers ? t->others[j] : 0;
+    window_norms_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, t->ring, t->ring_ld, t->slot, sl, t->nothers,
+                                                               t->wnorms, red_part(t->ws_red), red_counter(t->ws_red),
+                                                               pred);
+    NYS_CHECK_LAUNCH();
+  }
+  // QP infeasibility pieces over the 25-step window (admm.py:624-634, 361-415)
+  if (t->kind == 1 && t->qp_infeas) {
+    qp_infeas_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(
+        n, t->ring + (int64_t)t->inf_last * t->ring_ld, t->ring + (int64_t)t->inf_first * t->ring_ld,
+        t->uring + (int64_t)t->inf_last * t->ring_ld, t->uring + (int64_t)t->inf_first * t->ring_ld, t->width, t->lo,
+        t->hi, t->q, t->dx, t->infeas, red_part(t->ws_red), red_counter(t->ws_red), pred);
+    NYS_CHECK_LAUNCH();
+    if ((rc = gemv_n(t->A, n, n, t->lda, t->dx, n, 1, t->Pdx, n, nullptr, t->ws_gemv, t->ws_gemv_bytes, st, pred)))
+      return rc;
+    dot_pred_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, t->Pdx, t->Pdx, t->pdx2, red_part(t->ws_red),
+                                                           red_counter(t->ws_red), pred);
+    NYS_CHECK_LAUNCH();
+  }
   return NYS_OK;
 }

@@ -147,6 +147,34 @@ class Kernels:
                                         1 if refresh else 0, sc.data_ptr(), self.red.data_ptr(), self.sp),
               "cg_step")
 
+    def cg_problem(self, op_kind, A, d, shift, U, lam, nu, b, x, work, tol, max_iter):
+        """Fill a ``nys_cg_problem`` for the batched CG driver (workspaces cached)."""
+        rows, n = (A.shape[0], A.shape[1])
+        r = 0 if U is None else U.shape[1]
+        s_op, s_pc = C.c_size_t(0), C.c_size_t(0)
+        red_b = self.L.nys_cg_workspace(op_kind, rows, n, r, C.byref(s_op), C.byref(s_pc))
+        w_op = self.workspace("hvp" if op_kind == 0 else "densemv", s_op.value)
+        w_pc = self.workspace("prec", s_pc.value)
+        w_red = self.workspace("cgred", red_b)
+        pb = _lib.CgProblem(
+            op_kind=op_kind, A=A.data_ptr(), rows=rows, n=n, lda=A.stride(0), d=_p(d), shift=float(shift),
+            U=_p(U), r=r, ldu=(U.stride(0) if r else 0), lam=_p(lam), nu=float(nu), b=b.data_ptr(),
+            x=x.data_ptr(), res=work.r.data_ptr(), p=work.p.data_ptr(), z=work.z.data_ptr(),
+            Ap=work.Ap.data_ptr(), sc=work.sc.data_ptr(), tol=float(tol), max_iter=int(max_iter),
+            ws_op=w_op.data_ptr(), ws_op_bytes=w_op.numel(), ws_pc=w_pc.data_ptr(), ws_pc_bytes=w_pc.numel(),
+            ws_red=w_red.data_ptr())
+        return pb
+
+    def admm_tail(self, t) -> None:
+        self.launches += 1
+        check(self.L.nys_admm_tail_f64(C.byref(t), self.sp), "admm_tail")
+
+    def cg_iterate(self, pb, k_first: int, count: int) -> None:
+        self.launches += 1
+        e = self._t0("cg")
+        check(self.L.nys_cg_iterate_f64(C.byref(pb), int(k_first), int(count), self.sp), "cg_iterate")
+        self._t1(e)
+
     def cg_dir(self, z, p, first, sc) -> None:
         self.launches += 1
         check(self.L.nys_cg_dir_f64(z.numel(), z.data_ptr(), p.data_ptr(), 1 if first else 0, sc.data_ptr(),

@@ -127,6 +127,35 @@ def pcg_device(work: CgWork, matvec: MatvecInto, b: torch.Tensor, x: torch.Tenso
     return CgReport(k, res / denom, False)
 
 
+def pcg_batched(work: CgWork, pb, max_iter: int, first_batch: int = 2, max_batch: int = 16) -> CgReport:
+    """krylov.py:35-95 with the stop test on the device (nys_cg_iterate_f64).
+
+    Launches batches of predicated iterations and reads the scalar block once
+    per batch; the iteration sequence and the stopping decision are the
+    reference's, only the number of host round trips changes.  The caller has
+    set B2 / RES2 for r = b - A x0 (``started`` form of ``pcg_device``)."""
+    kx = work.kx
+    k = 1
+    batch = max(1, first_batch)
+    while True:
+        kx.cg_iterate(pb, k, batch)
+        h = work.read()
+        done = int(h[_lib.CG_DONE])
+        if done or k + batch > max_iter:
+            break
+        k += batch
+        batch = min(max_batch, batch * 2)
+    iters = int(h[_lib.CG_ITERS])
+    resrel = float(h[_lib.CG_RESREL])
+    if done == 2:
+        raise NumericalError("non-finite value in conjugate gradient")
+    if done == 3:
+        raise NotSPDError(f"nonpositive curvature p'Ap = {h[_lib.CG_PAP]:.3e}; operator is not SPD")
+    if done == 1:
+        return CgReport(iters, resrel, True)
+    return CgReport(iters if done == 4 else max_iter, resrel, False)
+
+
 def _matvec_for(A) -> MatvecInto:
     from .kernels import get_kernels
 

@@ -139,6 +139,35 @@ def test_syevj(kx, s):
     np.testing.assert_allclose(M @ Vn, Vn * wn, atol=1e-11 * 10)
 
 
+@pytest.mark.parametrize("kind", ["identity", "repeated", "diagonal", "rank1", "graded"])
+@pytest.mark.parametrize("s", [3, 40, 133])
+def test_syevj_degenerate_spectra(kx, kind, s):
+    g = np.random.default_rng(7 * s)
+    Q, _ = np.linalg.qr(g.standard_normal((s, s)))
+    if kind == "identity":
+        M = 2.5 * np.eye(s)
+    elif kind == "repeated":
+        lam = np.repeat([3.0, 1.0, 0.5], (s + 2) // 3)[:s]
+        M = (Q * lam) @ Q.T
+    elif kind == "diagonal":
+        M = np.diag(np.linspace(5.0, 1.0, s))
+    elif kind == "rank1":
+        q = g.standard_normal(s)
+        M = np.outer(q, q)
+    else:
+        M = (Q * np.logspace(0, -12, s)) @ Q.T
+    M = 0.5 * (M + M.T)
+    V = kx.empty(s, s)
+    w = kx.empty(s)
+    kx.syevj(dev(M), V, w)
+    wn, Vn = w.cpu().numpy(), V.cpu().numpy()
+    ref = np.sort(np.linalg.eigvalsh(M))[::-1]
+    scale = np.abs(ref).max()
+    np.testing.assert_allclose(wn, ref, atol=1e-12 * scale * s)
+    np.testing.assert_allclose(Vn.T @ Vn, np.eye(s), atol=1e-10)
+    np.testing.assert_allclose(M @ Vn, Vn * wn, atol=1e-11 * scale * s)
+
+
 def test_orthonormalize_spans_omega(kx):
     g = np.random.default_rng(1)
     Om = g.standard_normal((2000, 70))
