@@ -169,6 +169,13 @@ int nys_cg_dir_f64(int64_t n, const double* z, double* p, int first, double* sc,
  * Workspace sizes: returns the reduction scratch bytes, *ws_op / *ws_pc. */
 size_t nys_cg_workspace(int op_kind, int64_t rows, int64_t n, int r, size_t* ws_op, size_t* ws_pc);
 int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int count, void* stream);
+/* Instrumentation (bench roofline): with timing enabled, nys_cg_iterate_f64
+ * brackets every operator launch with CUDA events tagged by its CG iteration;
+ * nys_timing_commit(k) keeps those of iterations <= k (the ones that ran --
+ * later launches of a batch were predicated no-ops) and drops the rest. */
+int nys_timing_enable(int on);
+int nys_timing_commit(int64_t last_real_k);
+int nys_timing_read(double* total_ms, int64_t* launches);
 
 /* Everything of one ADMM iteration after the x-update (admm.py:562-611 and
  * 621-675), launched as one predicated sequence: relax/prox/dual update (+

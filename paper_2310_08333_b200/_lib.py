@@ -95,6 +95,9 @@ SIGNATURES = {
     "nys_cg_dir_f64": (I32, [I64, P, P, I32, P, P]),
     "nys_cg_workspace": (SZ, [I32, I64, I64, I32, C.POINTER(SZ), C.POINTER(SZ)]),
     "nys_cg_iterate_f64": (I32, [C.POINTER(CgProblem), I64, I32, P]),
+    "nys_timing_enable": (I32, [I32]),
+    "nys_timing_commit": (I32, [I64]),
+    "nys_timing_read": (I32, [C.POINTER(F64), C.POINTER(I64)]),
     "nys_admm_rhs_f64": (I32, [I64, P, P, P, F64, F64, F64, F64, P, P, P, P, P, P, P, P]),
     "nys_admm_zu_f64": (I32, [I64, P, P, P, F64, I32, F64, P, P, P, P, I32, P]),
     "nys_admm_norms_f64": (I32, [I64, P, P, P, P, P, F64, F64, P, F64, P, P, P, P, P]),

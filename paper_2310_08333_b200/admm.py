@@ -805,6 +805,8 @@ class _Engine:
             lin_ms += ev[0].elapsed_time(ev[1])
             tail_ms += ev[1].elapsed_time(ev[2])
             done = int(sc[_lib.CG_DONE])
+            if hasattr(kx, "timing_commit"):
+                kx.timing_commit(int(sc[_lib.CG_ITERS]) if done else k_first + batch - 1)
             if done or k_first + batch > max_iter:
                 break
             k_first += batch

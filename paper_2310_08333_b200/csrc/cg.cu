@@ -10,6 +10,7 @@
 // back and reads the scalar block once, so a CG solve of c iterations costs
 // ceil(c / count) syncs instead of c, with the identical iteration sequence.
 #include <math.h>
+#include <vector>
 #include "common.cuh"
 
 namespace nys {
@@ -161,9 +162,65 @@ static int precondition(const nys_cg_problem* pb, cudaStream_t st, const double*
                        pb->res, pb->sc + NYS_CG_RZNEW, pb->ws_pc, pb->ws_pc_bytes, st, pred);
 }
 
+// ---- optional CUDA-event timing of the HVP launches (bench roofline) -------
+struct TimedLaunch {
+  int64_t k;
+  cudaEvent_t a, b;
+};
+static bool g_timing = false;
+static std::vector<TimedLaunch> g_pending;
+static std::vector<cudaEvent_t> g_pool;
+static double g_total_ms = 0.0;
+static int64_t g_count = 0;
+
+static cudaEvent_t pool_get() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
 }  // namespace nys
 
 using namespace nys;
+
+extern "C" int nys_timing_enable(int on) {
+  g_timing = on != 0;
+  g_total_ms = 0.0;
+  g_count = 0;
+  for (auto& t : g_pending) {
+    g_pool.push_back(t.a);
+    g_pool.push_back(t.b);
+  }
+  g_pending.clear();
+  return NYS_OK;
+}
+
+extern "C" int nys_timing_commit(int64_t last_real_k) {
+  for (auto& t : g_pending) {
+    if (t.k <= last_real_k) {
+      float ms = 0.f;
+      if (cudaEventSynchronize(t.b) != cudaSuccess) return NYS_ERR_CUDA;
+      cudaEventElapsedTime(&ms, t.a, t.b);
+      g_total_ms += ms;
+      ++g_count;
+    }
+    g_pool.push_back(t.a);
+    g_pool.push_back(t.b);
+  }
+  g_pending.clear();
+  return NYS_OK;
+}
+
+extern "C" int nys_timing_read(double* total_ms, int64_t* launches) {
+  *total_ms = g_total_ms;
+  *launches = g_count;
+  return NYS_OK;
+}
 
 extern "C" size_t nys_cg_workspace(int op_kind, int64_t rows, int64_t n, int r, size_t* ws_op, size_t* ws_pc) {
   *ws_op = op_kind == 0 ? hvp_ws(rows, n) : dense_mv_ws(n);
@@ -189,7 +246,17 @@ extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int
   }
   for (int64_t k = k_first; k < k_first + count && k <= pb->max_iter; ++k) {
     const int refresh = (k % 50) == 0;  // krylov.py:16
+    TimedLaunch tl{k, nullptr, nullptr};
+    if (g_timing) {
+      tl.a = pool_get();
+      tl.b = pool_get();
+      cudaEventRecord(tl.a, st);
+    }
     if ((rc = matvec(pb, pb->p, pb->Ap, sc + NYS_CG_PAP, st, pred))) return rc;
+    if (g_timing) {
+      cudaEventRecord(tl.b, st);
+      g_pending.push_back(tl);
+    }
     cgp_step_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->x, pb->res, pb->p, pb->Ap, refresh, sc, pb->tol,
                                                          k, pb->max_iter, cg_part(pb->ws_red), cg_counter(pb->ws_red));
     NYS_CHECK_LAUNCH();

@@ -165,6 +165,20 @@ class Kernels:
             ws_red=w_red.data_ptr())
         return pb
 
+    # CUDA-event timing of the operator launches inside the batched CG driver
+    def timing_enable(self, on: bool) -> None:
+        self.L.nys_timing_enable(1 if on else 0)
+        self._lib_timing = bool(on)
+
+    def timing_commit(self, last_real_k: int) -> None:
+        if getattr(self, "_lib_timing", False):
+            check(self.L.nys_timing_commit(int(last_real_k)), "timing_commit")
+
+    def timing_read(self):
+        tot, cnt = C.c_double(0.0), C.c_int64(0)
+        self.L.nys_timing_read(C.byref(tot), C.byref(cnt))
+        return float(tot.value), int(cnt.value)
+
     def admm_tail(self, t) -> None:
         self.launches += 1
         check(self.L.nys_admm_tail_f64(C.byref(t), self.sp), "admm_tail")
