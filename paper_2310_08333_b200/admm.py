@@ -211,6 +211,8 @@ _S_PDX = 39  # 1 (||P dx||^2)
 _S_CONJ = 40  # 3 (scaled conjugate sums)
 _S_DUAL = 44  # 2 (penalty change)
 _S_LEN = 48
+# device readback block: row sums (8) | CG scalars (16) | stats (_S_LEN)
+_RB_LEN = 8 + 16 + _S_LEN
 
 
 def _host_buffer(n, device):
@@ -246,10 +248,11 @@ class _Engine:
             self.AXZ = kx.empty(2, rows)
             self.T = kx.empty(3, rows)  # l'(Ax-b), w o Ax, nu
             self.w = kx.empty(rows)
-            # packed all-reduce buffer: A^T outputs (3 n) + row sums (8)
-            self.red = kx.zeros(3 * n + 8)
+            # packed all-reduce buffer: A^T outputs (3 n) + row sums (8), then
+            # the CG scalars and the stats so one D2H copy reads a whole iteration
+            self.red = kx.zeros(3 * n + _RB_LEN)
             self.AT = self.red[:3 * n].view(3, n)  # gA, hxA, atnu
-            self.rowsums = self.red[3 * n:3 * n + 8]
+            self.rb_dev = self.red[3 * n:]
         else:
             qp = gp.qp
             if not isinstance(qp.P, DenseOperator):
@@ -266,15 +269,17 @@ class _Engine:
             self.Px = kx.empty(1, n)
             self.dx = kx.empty(1, n)
             self.Pdx = kx.empty(1, n)
+            self.rb_dev = kx.zeros(_RB_LEN)
+        self.rowsums = self.rb_dev[:8]
         self.XZ = kx.zeros(2, n)  # x, z rows (one 2-RHS GEMV operand)
         self.x, self.z = self.XZ[0], self.XZ[1]
         self.u = kx.zeros(n)
         self.xbar = kx.zeros(n)
         self.zbar = kx.zeros(n)
         self.rhs = kx.empty(n)
-        self.cg = CgWork(kx, n)
-        self.stats = kx.zeros(_S_LEN)
-        self.stats_h = _host_buffer(_S_LEN + 8, kx.device)
+        self.cg = CgWork(kx, n, self.rb_dev[8:8 + _lib.CG_NSLOTS])
+        self.stats = self.rb_dev[8 + _lib.CG_NSLOTS:]
+        self.rb_host = _host_buffer(_RB_LEN, kx.device)
         self.ring = kx.empty(DELTA_WINDOW + 2, n)
         self.uring = kx.empty(DELTA_WINDOW + 2, n) if not self.is_ml else None
         self.U = None
@@ -295,7 +300,7 @@ class _Engine:
             kT = 3 if with_z else 2
             kx.gemvT(self.A, self.T[:kT], self.AT[:kT])
             if self.shard.sharded:
-                self.shard.allreduce(self.red)
+                self.shard.allreduce(self.red[:3 * self.n + 8])
         else:
             kx.gemv(self.P, self.XZ[:1], self.Px)
 
@@ -309,13 +314,9 @@ class _Engine:
                           self.lo, self.hi, self.stats[_S_NORMS:_S_NORMS + 16])
 
     def read_stats(self) -> np.ndarray:
-        h = self.stats_h
-        h[:_S_LEN].copy_(self.stats, non_blocking=True)
-        if self.is_ml:
-            h[_S_LEN:_S_LEN + 5].copy_(self.rowsums[:5], non_blocking=True)
-        self.kx.d2h += (_S_LEN + 5) * 8
-        self.kx.sync()
-        return h.numpy().copy()
+        """stats followed by the row sums (one D2H copy of the readback block)."""
+        _, st = self._read_block()
+        return st
 
     # ----------------------------------------------------------- matvec --
     def matvec(self, shift: float):
@@ -748,20 +749,16 @@ class _Engine:
         t.ws_gemvT, t.ws_gemvT_bytes = wt.data_ptr(), wt.numel()
         t.ws_red = wr.data_ptr()
         self._tail = t
-        self._rb = _host_buffer(_lib.CG_NSLOTS + _S_LEN + 8, kx.device)
         self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 
-    def _read_fused(self):
-        """sc + stats (+ row sums) in one readback; returns (sc, st)."""
-        rb, C = self._rb, _lib.CG_NSLOTS
-        rb[:C].copy_(self.cg.sc, non_blocking=True)
-        rb[C:C + _S_LEN].copy_(self.stats, non_blocking=True)
-        if self.is_ml:
-            rb[C + _S_LEN:C + _S_LEN + 5].copy_(self.rowsums[:5], non_blocking=True)
-        self.kx.d2h += (C + _S_LEN + 5) * 8
+    def _read_block(self):
+        """The whole readback block in one D2H copy; returns (sc, stats + row sums)."""
+        rb, C = self.rb_host, _lib.CG_NSLOTS
+        rb.copy_(self.rb_dev, non_blocking=True)
+        self.kx.d2h += _RB_LEN * 8
         self.kx.sync()
         h = rb.numpy().copy()
-        return h[:C], h[C:]
+        return h[8:8 + C], np.concatenate([h[8 + C:], h[:8]])
 
     def _fused_iteration(self, k, tol, shift, win, accum):
         kx, n, t = self.kx, self.n, self._tail
@@ -801,7 +798,7 @@ class _Engine:
             ev[1].record(kx.stream)
             kx.admm_tail(t)
             ev[2].record(kx.stream)
-            sc, st = self._read_fused()
+            sc, st = self._read_block()
             lin_ms += ev[0].elapsed_time(ev[1])
             tail_ms += ev[1].elapsed_time(ev[2])
             done = int(sc[_lib.CG_DONE])

@@ -22,7 +22,13 @@ namespace cg = cooperative_groups;
 namespace nys {
 
 // ------------------------------------------------------------- GEMM -------
-constexpr int GBM = 128, GBN = 64, GBK = 16, GSTAGES = 3, GTHREADS = 256;
+// One kernel template, several CTA tile shapes: the sketch GEMMs are skinny
+// (N = s ~ 100-300 columns), so a fixed 128x64 tile wastes up to 40% of the
+// tensor work on padding and leaves partial waves.  The host planner
+// (gemm_plan) picks tile shape and split-K per call from a cost model of
+// padded work, wave quantisation and split-K partial traffic.
+constexpr int GBK = 16, GSTAGES = 3, GTHREADS = 256;
+constexpr int GWM = 4, GWN = 2;  // 8 warps: 4 along M, 2 along N
 // shared-memory row strides (doubles) chosen so DMMA fragment loads are
 // 2-wavefront (conflict-free for 256 B per warp request)
 constexpr int kStrideKmaj(int mn) { return mn + 8; }  // tile stored [k][m]
@@ -46,24 +52,28 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 // TA: op(A) = A^T (A stored K x M). TB: op(B) = B^T (B stored N x K).
-template <bool TA, bool TB>
-struct GemmSmem {
-  static constexpr int A_ELEMS = TA ? GBK * kStrideKmaj(GBM) : GBM * kStrideMmaj;
-  static constexpr int B_ELEMS = TB ? GBN * kStrideMmaj : GBK * kStrideKmaj(GBN);
+template <bool TA, bool TB, int BM, int BN>
+struct GemmCfg {
+  static constexpr int FM = BM / (GWM * 8), FN = BN / (GWN * 8);  // 8x8 fragments per warp
+  static constexpr int A_ELEMS = TA ? GBK * kStrideKmaj(BM) : BM * kStrideMmaj;
+  static constexpr int B_ELEMS = TB ? BN * kStrideMmaj : GBK * kStrideKmaj(BN);
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
   static constexpr size_t BYTES = (size_t)STAGE * GSTAGES * sizeof(double);
+  static_assert(FM >= 1 && FN >= 1 && BM % (GWM * 8) == 0 && BN % (GWN * 8) == 0, "tile");
+  static_assert((BM * GBK) % GTHREADS == 0 && (BN * GBK) % GTHREADS == 0, "loader");
 };
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, int BM, int BN>
 __global__ void __launch_bounds__(GTHREADS)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A,
              int64_t lda, const double* __restrict__ B, int64_t ldb, double beta,
              double* __restrict__ C, int64_t ldc, int64_t k_per_split, double* __restrict__ P) {
   extern __shared__ __align__(16) double smem[];
-  using S = GemmSmem<TA, TB>;
+  using S = GemmCfg<TA, TB, BM, BN>;
+  constexpr int FM = S::FM, FN = S::FN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps, 32 x 32 each
-  const int64_t n0 = (int64_t)blockIdx.x * GBN, m0 = (int64_t)blockIdx.y * GBM;
+  const int wm = warp % GWM, wn = warp / GWM;
+  const int64_t n0 = (int64_t)blockIdx.x * BN, m0 = (int64_t)blockIdx.y * BM;
   const int64_t kb = (int64_t)blockIdx.z * k_per_split;
   const int64_t ke = min(K, kb + k_per_split);
   const int ktiles = (int)cdiv(tmax<int64_t>(ke - kb, 0), GBK);
@@ -71,14 +81,13 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
   auto load_tile = [&](int stage, int64_t k0) {
     double* As = smem + stage * S::STAGE;
     double* Bs = As + S::A_ELEMS;
-    // A tile: GBM x GBK elements of op(A)
 #pragma unroll
-    for (int e = tid; e < GBM * GBK; e += GTHREADS) {
+    for (int e = tid; e < BM * GBK; e += GTHREADS) {
       if (TA) {  // consecutive threads along m (contiguous in memory)
-        const int kk = e / GBM, mm = e - kk * GBM;
+        const int kk = e / BM, mm = e - kk * BM;
         const int64_t gm = m0 + mm, gk = k0 + kk;
         const bool v = gm < M && gk < ke;
-        cp_async8(As + kk * kStrideKmaj(GBM) + mm, v ? A + gk * lda + gm : A, v);
+        cp_async8(As + kk * kStrideKmaj(BM) + mm, v ? A + gk * lda + gm : A, v);
       } else {  // consecutive threads along k
         const int mm = e / GBK, kk = e - mm * GBK;
         const int64_t gm = m0 + mm, gk = k0 + kk;
@@ -87,26 +96,26 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
       }
     }
 #pragma unroll
-    for (int e = tid; e < GBN * GBK; e += GTHREADS) {
+    for (int e = tid; e < BN * GBK; e += GTHREADS) {
       if (TB) {
         const int nn = e / GBK, kk = e - nn * GBK;
         const int64_t gn = n0 + nn, gk = k0 + kk;
         const bool v = gn < N && gk < ke;
         cp_async8(Bs + nn * kStrideMmaj + kk, v ? B + gn * ldb + gk : B, v);
       } else {
-        const int kk = e / GBN, nn = e - kk * GBN;
+        const int kk = e / BN, nn = e - kk * BN;
         const int64_t gn = n0 + nn, gk = k0 + kk;
         const bool v = gn < N && gk < ke;
-        cp_async8(Bs + kk * kStrideKmaj(GBN) + nn, v ? B + gk * ldb + gn : B, v);
+        cp_async8(Bs + kk * kStrideKmaj(BN) + nn, v ? B + gk * ldb + gn : B, v);
       }
     }
   };
 
-  double acc[4][4][2];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) {
@@ -126,34 +135,34 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
     const double* Bs = As + S::A_ELEMS;
 #pragma unroll
     for (int k4 = 0; k4 < GBK; k4 += 4) {
-      double af[4], bf[4];
+      double af[FM], bf[FN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int mm = wm * 32 + i * 8 + fr, kk = k4 + fc;
-        af[i] = TA ? As[kk * kStrideKmaj(GBM) + mm] : As[mm * kStrideMmaj + kk];
+      for (int i = 0; i < FM; ++i) {
+        const int mm = wm * (FM * 8) + i * 8 + fr, kk = k4 + fc;
+        af[i] = TA ? As[kk * kStrideKmaj(BM) + mm] : As[mm * kStrideMmaj + kk];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int nn = wn * 32 + j * 8 + fr, kk = k4 + fc;
-        bf[j] = TB ? Bs[nn * kStrideMmaj + kk] : Bs[kk * kStrideKmaj(GBN) + nn];
+      for (int j = 0; j < FN; ++j) {
+        const int nn = wn * (FN * 8) + j * 8 + fr, kk = k4 + fc;
+        bf[j] = TB ? Bs[nn * kStrideMmaj + kk] : Bs[kk * kStrideKmaj(BN) + nn];
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
 
   // epilogue: fragment (row = lane/4, cols = 2*(lane%4) + {0,1})
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < FN; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t gm = m0 + wm * 32 + i * 8 + fr;
-        const int64_t gn = n0 + wn * 32 + j * 8 + fc * 2 + h;
+        const int64_t gm = m0 + wm * (FM * 8) + i * 8 + fr;
+        const int64_t gn = n0 + wn * (FN * 8) + j * 8 + fc * 2 + h;
         if (gm < M && gn < N) {
           if (P) {
             P[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j][h];
@@ -180,48 +189,97 @@ __global__ void splitk_reduce(const double* __restrict__ P, int64_t M, int64_t N
   }
 }
 
-static int gemm_splits(int64_t M, int64_t N, int64_t K) {
-  const int64_t tiles = cdiv(M, GBM) * cdiv(N, GBN);
-  const int64_t target = kNumSMs * 2;
-  if (tiles >= target || K < 4 * GBK) return 1;
-  int64_t sp = cdiv(target, tiles);
-  sp = tmin<int64_t>(sp, cdiv(K, 4 * GBK));
-  // keep partials under 32 M doubles
-  sp = tmin<int64_t>(sp, tmax<int64_t>(1, (32ll << 20) / tmax<int64_t>(1, M * N)));
-  return (int)tmax<int64_t>(1, sp);
+// tile shapes: {BM, BN, relative per-SM efficiency of the shape}
+struct TileShape {
+  int bm, bn;
+  double eff;
+};
+constexpr int kNumShapes = 5;
+static const TileShape kShapes[kNumShapes] = {
+    {128, 64, 1.00}, {128, 48, 0.96}, {64, 64, 0.90}, {64, 48, 0.86}, {64, 32, 0.78}};
+
+struct GemmPlan {
+  int shape = 0, splits = 1;
+  int64_t kps = 0;
+  size_t ws = 0;
+};
+
+// cost model in seconds: padded tensor work per SM over the busiest SM, plus
+// split-K partial traffic (write + read) and one extra launch
+static GemmPlan gemm_plan(int64_t M, int64_t N, int64_t K, size_t ws_cap) {
+  const char* force = getenv("NYS_GEMM_SHAPE");
+  const int only = force ? atoi(force) : -1;
+  GemmPlan best;
+  double best_t = 1e300;
+  const double sm_rate = 68.0 * 1.9e9;  // FP64 DMMA FMA/s per SM (~40 TF/148)
+  for (int c = 0; c < kNumShapes; ++c) {
+    if (only >= 0 && c != only) continue;
+    const TileShape& t = kShapes[c];
+    const int64_t tiles = cdiv(M, t.bm) * cdiv(N, t.bn);
+    const int64_t max_sp = tmax<int64_t>(1, tmin<int64_t>(64, cdiv(K, 4 * GBK)));
+    for (int64_t sp = 1; sp <= max_sp; ++sp) {
+      const int64_t kps = cdiv(cdiv(K, sp), GBK) * GBK;
+      const int64_t spr = cdiv(K, kps);  // realised splits
+      if (spr != sp) continue;
+      const size_t ws = sp > 1 ? (size_t)sp * M * N * sizeof(double) : 0;
+      if (ws > ws_cap) break;
+      const int64_t ctas = tiles * sp;
+      const int64_t per_sm = cdiv(ctas, kNumSMs);
+      // pipeline fill: ~2 k-tiles of latency per CTA
+      const double work = (double)per_sm * t.bm * t.bn * (double)(kps + 2 * GBK);
+      double tt = work / (sm_rate * t.eff);
+      if (sp > 1) tt += 2.0 * (double)ws / 6.0e12 + 3.0e-6;
+      if (tt < best_t * 0.999) {
+        best_t = tt;
+        best.shape = c;
+        best.splits = (int)sp;
+        best.kps = kps;
+        best.ws = ws;
+      }
+    }
+  }
+  if (best.kps == 0) best.kps = K;
+  return best;
 }
 
-size_t gemm_ws(int64_t M, int64_t N, int64_t K) {
-  const int sp = gemm_splits(M, N, K);
-  return sp > 1 ? (size_t)sp * M * N * sizeof(double) : 0;
+size_t gemm_ws(int64_t M, int64_t N, int64_t K) { return gemm_plan(M, N, K, (size_t)-1).ws; }
+
+template <bool TA, bool TB, int BM, int BN>
+static int gemm_launch_shape(const GemmPlan& pl, int64_t M, int64_t N, int64_t K, double alpha,
+                             const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                             double* C, int64_t ldc, void* ws, cudaStream_t st) {
+  using S = GemmCfg<TA, TB, BM, BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB, BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::BYTES);
+    attr_set = true;
+  }
+  dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM), (unsigned)pl.splits);
+  double* P = pl.splits > 1 ? reinterpret_cast<double*>(ws) : nullptr;
+  dgemm_kernel<TA, TB, BM, BN><<<grid, GTHREADS, S::BYTES, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C,
+                                                                 ldc, pl.kps, P);
+  NYS_CHECK_LAUNCH();
+  if (pl.splits > 1) {
+    const int64_t blocks = tmin<int64_t>(cdiv(M * N, 256), kNumSMs * 8);
+    splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(P, M, N, pl.splits, alpha, beta, C, ldc);
+    NYS_CHECK_LAUNCH();
+  }
+  return NYS_OK;
 }
 
 template <bool TA, bool TB>
 static int gemm_launch(int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                        int64_t lda, const double* B, int64_t ldb, double beta, double* C,
                        int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
-  using S = GemmSmem<TA, TB>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(dgemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)S::BYTES);
-    attr_set = true;
+  const GemmPlan pl = gemm_plan(M, N, K, ws ? ws_bytes : 0);
+  switch (pl.shape) {
+    case 0: return gemm_launch_shape<TA, TB, 128, 64>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
+    case 1: return gemm_launch_shape<TA, TB, 128, 48>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
+    case 2: return gemm_launch_shape<TA, TB, 64, 64>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
+    case 3: return gemm_launch_shape<TA, TB, 64, 48>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
+    default: return gemm_launch_shape<TA, TB, 64, 32>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
   }
-  int sp = gemm_splits(M, N, K);
-  if (sp > 1 && ws_bytes < (size_t)sp * M * N * sizeof(double)) sp = 1;
-  const int64_t kps = sp > 1 ? cdiv(cdiv(K, sp), GBK) * GBK : K;
-  sp = (int)cdiv(K, kps);
-  dim3 grid((unsigned)cdiv(N, GBN), (unsigned)cdiv(M, GBM), (unsigned)sp);
-  double* P = sp > 1 ? reinterpret_cast<double*>(ws) : nullptr;
-  dgemm_kernel<TA, TB><<<grid, GTHREADS, S::BYTES, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C,
-                                                         ldc, kps, P);
-  NYS_CHECK_LAUNCH();
-  if (sp > 1) {
-    const int64_t blocks = tmin<int64_t>(cdiv(M * N, 256), kNumSMs * 8);
-    splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(P, M, N, sp, alpha, beta, C, ldc);
-    NYS_CHECK_LAUNCH();
-  }
-  return NYS_OK;
 }
 
 int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
@@ -308,6 +366,103 @@ __global__ void __launch_bounds__(256) trinv_lower_kernel(int s, const double* _
     __syncwarp();
   }
   for (int i = lane; i < s; i += 32) X[(int64_t)i * ldx + j] = x[i];
+}
+
+// Fused Cholesky + triangular inverse for s <= kCholInvMaxS, one CTA:
+// C (lower triangle read, untouched) = L L^T, Li = L^{-1} (strict upper zeroed).
+// Factorisation (warps < kCholWarps): one barrier per column.  Step j updates
+// the trailing lower triangle with the UNSCALED column
+// (M[i][k] -= M[i][j] M[k][j] / d_j) and scales column j by 1/sqrt(d_j) in
+// step j + 1, when no thread reads it any more.
+// Inverse (all warps): one warp per column of L^{-1}, forward substitution
+// with the column in registers (lane owns rows lane + 32 m); the row blocks
+// are unrolled so the register index is static and only the diagonal block
+// is predicated.  L is read from shared memory (rows padded to 32 m).
+// info = j + 1 at the first non-positive pivot (LAPACK potf2 rule).
+constexpr int kCholInvMaxS = 160;  // (s_pad (s|1) + s_pad) doubles fit in 227 KB
+constexpr int kCholWarps = 16;
+inline size_t cholinv_smem(int s) {
+  const size_t sp = (size_t)cdiv(s, 32) * 32;
+  return (sp * (size_t)(s | 1) + sp) * sizeof(double);
+}
+__global__ void __launch_bounds__(1024) cholinv_kernel(int s, const double* __restrict__ C, int64_t ldc,
+                                                       double* __restrict__ Li, int64_t ldli, int* info) {
+  extern __shared__ double csm[];
+  constexpr int MR = kCholInvMaxS / 32;
+  const int ld = s | 1;
+  const int s_pad = (s + 31) & ~31;
+  double* dinv = csm;
+  double* M = csm + s_pad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int t = tid; t < s * s; t += blockDim.x) {
+    const int i = t / s, k = t - i * s;
+    if (k <= i) M[i * ld + k] = C[(int64_t)i * ldc + k];
+  }
+  for (int t = s * ld + tid; t < s_pad * ld; t += blockDim.x) M[t] = 0.0;  // padding rows
+  __syncthreads();
+  int fail = 0;
+  double prev_rs = 0.0;
+  const int ctid = tid;  // factorisation threads: tid < 32 * kCholWarps
+  for (int j = 0; j < s; ++j) {
+    const double d = M[j * ld + j];
+    if (j > 0 && warp < kCholWarps) {  // deferred scaling of column j-1 (rows >= j-1)
+      for (int i = j - 1 + ctid; i < s; i += 32 * kCholWarps) {
+        double* e = M + i * ld + (j - 1);
+        *e = (i == j - 1) ? 1.0 / prev_rs : *e * prev_rs;
+      }
+    }
+    if (!(d > 0.0) || isnan(d)) {  // uniform: every thread read the same pivot
+      fail = j + 1;
+      break;
+    }
+    if (warp < kCholWarps) {
+      const double dinv_j = 1.0 / d;
+      const double* colj = M + j;
+      for (int i = j + 1 + warp; i < s; i += kCholWarps) {
+        double* rowi = M + i * ld;
+        const double lij = rowi[j] * dinv_j;
+        const double* pc = colj + (j + 1 + lane) * ld;
+        double* pr = rowi + (j + 1 + lane);
+        for (int k = j + 1 + lane; k <= i; k += 32, pc += 32 * ld, pr += 32) *pr = fma(-lij, *pc, *pr);
+      }
+    }
+    prev_rs = 1.0 / sqrt(d);
+    __syncthreads();
+  }
+  if (tid == 0) *info = fail;
+  if (fail) return;
+  if (tid == 0) M[(s - 1) * ld + s - 1] = 1.0 / prev_rs;
+  __syncthreads();
+  for (int k = tid; k < s; k += blockDim.x) dinv[k] = 1.0 / M[k * ld + k];
+  __syncthreads();
+  for (int j = warp; j < s; j += nw) {
+    double x[MR];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) x[m] = (lane + 32 * m == j) ? 1.0 : 0.0;
+    const int mj = j >> 5;
+#pragma unroll
+    for (int mk = 0; mk < MR; ++mk) {
+      if (mk < mj || 32 * mk >= s) continue;  // warp-uniform
+      const int k1 = min(32 * mk + 32, s);
+      const double* rows[MR];
+#pragma unroll
+      for (int m = 0; m < MR; ++m) rows[m] = M + (lane + 32 * m) * ld;
+      for (int k = (mk == mj ? j : 32 * mk); k < k1; ++k) {
+        const int ok = k & 31;
+        const double xk = __shfl_sync(0xffffffffu, x[mk] * dinv[k], ok);
+        if (lane > ok) x[mk] = fma(-rows[mk][k], xk, x[mk]);
+        else if (lane == ok) x[mk] = xk;
+#pragma unroll
+        for (int m = mk + 1; m < MR; ++m)
+          if (32 * m < s) x[m] = fma(-rows[m][k], xk, x[m]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      const int i = lane + 32 * m;
+      if (i < s) Li[(int64_t)i * ldli + j] = x[m];
+    }
+  }
 }
 
 __global__ void symmetrize_kernel(int s, double* C, int64_t ldc) {
@@ -406,6 +561,7 @@ static int cholesky(int s, double* C, int* info_dev, int* info_host, cudaStream_
     cholesky_kernel<false><<<1, 1024, 0, st>>>(s, C, s, info_dev);
   }
   NYS_CHECK_LAUNCH();
+  if (!info_host) return NYS_OK;
   if (cudaMemcpyAsync(info_host, info_dev, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return NYS_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
@@ -418,20 +574,52 @@ static int trinv(int s, const double* L, double* X, cudaStream_t st) {
   return NYS_OK;
 }
 
+// Li = chol(C)^{-1} (C untouched; Lm is s x s scratch for s > kCholInvMaxS).
+// info_dev gets the potf2 code; with info_host != nullptr the stream is
+// synchronised and the code returned there, otherwise the check is deferred.
+static int chol_inverse(int s, const double* C, double* Li, double* Lm, int* info_dev, int* info_host,
+                        cudaStream_t st) {
+  if (s <= kCholInvMaxS) {
+    const size_t smem = cholinv_smem(s);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(cholinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      attr = true;
+    }
+    cholinv_kernel<<<1, 1024, smem, st>>>(s, C, s, Li, s, info_dev);
+    NYS_CHECK_LAUNCH();
+    if (!info_host) return NYS_OK;
+    if (cudaMemcpyAsync(info_host, info_dev, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return NYS_ERR_CUDA;
+    return cudaStreamSynchronize(st) == cudaSuccess ? NYS_OK : NYS_ERR_CUDA;
+  }
+  if (cudaMemcpyAsync(Lm, C, (size_t)s * s * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return NYS_ERR_CUDA;
+  int info_tmp = 0;
+  int rc = cholesky(s, Lm, info_dev, &info_tmp, st);  // large s: always checked here
+  if (rc) return rc;
+  if (info_host) *info_host = info_tmp;
+  if (info_tmp) return NYS_OK;
+  return trinv(s, Lm, Li, st);
+}
+
 size_t ortho_ws(int64_t n, int s) {
   const size_t ss = (size_t)s * s * sizeof(double);
-  return kRedBytesD + 3 * ss + (size_t)n * s * sizeof(double) + gemm_ws(s, s, n) + syevj_ws(s) +
+  return kRedBytesD + 4 * ss + (size_t)n * s * sizeof(double) + gemm_ws(s, s, n) + syevj_ws(s) +
          8 * s * sizeof(double) + 8192;
 }
 
-// CholeskyQR2: Q = Omega R^{-1}, twice.  Falls back to an eigen-based
-// orthonormalisation if a Gram matrix is numerically singular.
+// CholeskyQR2: Q = Omega R^{-1}, twice.  The fast path runs without a host
+// sync and checks both Cholesky codes once at the end; if either pass hit a
+// numerically singular Gram matrix the careful path (per-pass checks, eigen
+// fallback) recomputes Q from Omega.
 static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* ws,
-                          size_t ws_bytes, cudaStream_t st) {
+                          size_t ws_bytes, cudaStream_t st, bool careful) {
   Arena ar{reinterpret_cast<char*>(ws), ws_bytes};
   ar.take<char>(kRedBytesD);
   double* G = ar.take<double>((size_t)s * s);
   double* Li = ar.take<double>((size_t)s * s);
+  double* Lm = ar.take<double>((size_t)s * s);
   double* Vm = ar.take<double>((size_t)s * s);
   double* tmp = ar.take<double>((size_t)n * s);
   double* wv = ar.take<double>(s);
@@ -442,23 +630,20 @@ static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* w
   const size_t jws_b = syevj_ws(s);
   void* jws = ar.take<char>(jws_b);
   if (!ar.ok) return NYS_ERR_WORKSPACE;
-  const double* src = Om;
   int rc;
   for (int pass = 0; pass < 2; ++pass) {
+    const double* src = pass == 0 ? Om : tmp;
+    double* dst = pass == 0 ? tmp : Q;
     rc = gemm(1, 0, s, s, n, 1.0, src, s, src, s, 0.0, G, s, gws, gws_b, st);
     if (rc) return rc;
     int info_h = 0;
-    rc = cholesky(s, G, info, &info_h, st);
+    rc = chol_inverse(s, G, Li, Lm, info + pass, careful ? &info_h : nullptr, st);
     if (rc) return rc;
     if (info_h == 0) {
-      rc = trinv(s, G, Li, st);
-      if (rc) return rc;
-      // tmp = src L^{-T}
-      rc = gemm(0, 1, n, s, s, 1.0, src, s, Li, s, 0.0, tmp, s, nullptr, 0, st);
+      // dst = src L^{-T}
+      rc = gemm(0, 1, n, s, s, 1.0, src, s, Li, s, 0.0, dst, s, nullptr, 0, st);
     } else {
       // eigen fallback: src V diag(1/sqrt(w))  (full-rank Gaussian input expected)
-      rc = gemm(1, 0, s, s, n, 1.0, src, s, src, s, 0.0, G, s, gws, gws_b, st);
-      if (rc) return rc;
       rc = syevj(s, G, Vm, wv, jws, jws_b, st);
       if (rc) return rc;
       std::vector<double> wh(s);
@@ -468,14 +653,17 @@ static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* w
       cudaMemcpyAsync(sc, wh.data(), s * sizeof(double), cudaMemcpyHostToDevice, st);
       scale_cols_kernel<<<(unsigned)cdiv((int64_t)s * s, 256), 256, 0, st>>>(s, s, Vm, s, sc, Li, s);
       NYS_CHECK_LAUNCH();
-      rc = gemm(0, 0, n, s, s, 1.0, src, s, Li, s, 0.0, tmp, s, nullptr, 0, st);
+      rc = gemm(0, 0, n, s, s, 1.0, src, s, Li, s, 0.0, dst, s, nullptr, 0, st);
       if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
     }
     if (rc) return rc;
-    if (cudaMemcpyAsync(Q, tmp, (size_t)n * s * sizeof(double), cudaMemcpyDeviceToDevice, st) !=
-        cudaSuccess)
+  }
+  if (!careful) {
+    int info_h[2] = {0, 0};
+    if (cudaMemcpyAsync(info_h, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
       return NYS_ERR_CUDA;
-    src = Q;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+    if (info_h[0] || info_h[1]) return orthonormalize(n, s, Om, Q, ws, ws_bytes, st, true);
   }
   if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
   return NYS_OK;
@@ -487,8 +675,25 @@ size_t nystrom_ws(int64_t n, int s, int r) {
          16 * (size_t)s * sizeof(double) + 16384;
 }
 
+// lam_j = max(sigma_j^2 - shift, 0), scl_j = 1/sigma_j (sketch.py:126-128),
+// from the eigenvalues w of B^T B and the device-resident shift
+__global__ void nystrom_lam_kernel(int rr, const double* __restrict__ w, const double* __restrict__ shift,
+                                   double* __restrict__ lam, double* __restrict__ scl) {
+  const double sft = *shift;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < rr; j += gridDim.x * blockDim.x) {
+    const double sv2 = fmax(w[j], 0.0);
+    lam[j] = fmax(sv2 - sft, 0.0);
+    scl[j] = sv2 > 0.0 ? 1.0 / sqrt(sv2) : 0.0;
+  }
+}
+
+// Steps 1-4 of sketch.py:102-128 on device-resident Q (n x s) and Y = H Q.
+// The fast path has one host sync (the Cholesky code of the core, read at
+// the end); a non-positive pivot re-runs the careful path, which takes the
+// eigh fallback of sketch.py:114-124 from the same inputs.
 static int nystrom_core(int64_t n, int s, int r, const double* Q, double* Y, double* U,
-                        double* lam, int* r_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+                        double* lam, int* r_out, void* ws, size_t ws_bytes, cudaStream_t st,
+                        bool careful) {
   Arena ar{reinterpret_cast<char*>(ws), ws_bytes};
   char* red = ar.take<char>(kRedBytesD);
   double* shift_d = ar.take<double>(4);
@@ -508,38 +713,37 @@ static int nystrom_core(int64_t n, int s, int r, const double* Q, double* Y, dou
   void* jws = ar.take<char>(jws_b);
   if (!ar.ok) return NYS_ERR_WORKSPACE;
   const double eps = 2.220446049250313e-16;
-  cudaMemsetAsync(shift_d, 0, 4 * sizeof(double), st);
-
-  // 1. trace shift and Y_s = Y + shift Q   (sketch.py:102-106)
-  const int64_t tot = n * (int64_t)s;
-  const unsigned sb = (unsigned)tmax<int64_t>(1, tmin<int64_t>(cdiv(tot, 256), kNumSMs * 4));
-  sketch_shift_kernel<<<sb, 256, 0, st>>>(n, s, Q, Y, reinterpret_cast<double*>(red),
-                                          reinterpret_cast<unsigned int*>(
-                                              reinterpret_cast<double*>(red) + 4096 * 16),
-                                          shift_d, nullptr);
-  NYS_CHECK_LAUNCH();
-  add_scaled_kernel<<<sb, 256, 0, st>>>(tot, Q, Y, shift_d);
-  NYS_CHECK_LAUNCH();
-  // 2. core = Q^T Y_s, symmetrised  (sketch.py:107-108)
-  int rc = gemm(1, 0, s, s, n, 1.0, Q, s, Y, s, 0.0, core, s, gws, gws_b, st);
-  if (rc) return rc;
-  symmetrize_kernel<<<(unsigned)cdiv((int64_t)s * s, 256), 256, 0, st>>>(s, core, s);
-  NYS_CHECK_LAUNCH();
-  double shift_h = 0.0;
-  cudaMemcpyAsync(&shift_h, shift_d, sizeof(double), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(Lm, core, (size_t)s * s * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  int rc;
+  if (!careful) {
+    cudaMemsetAsync(shift_d, 0, 4 * sizeof(double), st);
+    // 1. trace shift and Y_s = Y + shift Q   (sketch.py:102-106)
+    const int64_t tot = n * (int64_t)s;
+    const unsigned sb = (unsigned)tmax<int64_t>(1, tmin<int64_t>(cdiv(tot, 256), kNumSMs * 4));
+    sketch_shift_kernel<<<sb, 256, 0, st>>>(n, s, Q, Y, reinterpret_cast<double*>(red),
+                                            reinterpret_cast<unsigned int*>(
+                                                reinterpret_cast<double*>(red) + 4096 * 16),
+                                            shift_d, nullptr);
+    NYS_CHECK_LAUNCH();
+    add_scaled_kernel<<<sb, 256, 0, st>>>(tot, Q, Y, shift_d);
+    NYS_CHECK_LAUNCH();
+    // 2. core = Q^T Y_s, symmetrised  (sketch.py:107-108)
+    rc = gemm(1, 0, s, s, n, 1.0, Q, s, Y, s, 0.0, core, s, gws, gws_b, st);
+    if (rc) return rc;
+    symmetrize_kernel<<<(unsigned)cdiv((int64_t)s * s, 256), 256, 0, st>>>(s, core, s);
+    NYS_CHECK_LAUNCH();
+  }
   // 3. Cholesky, B = Y_s L^{-T}   (sketch.py:110-113)
   int info_h = 0;
-  rc = cholesky(s, Lm, info, &info_h, st);
+  rc = chol_inverse(s, core, Li, Lm, info, careful ? &info_h : nullptr, st);
   if (rc) return rc;
   int s_eff = s;
   if (info_h == 0) {
-    rc = trinv(s, Lm, Li, st);
-    if (rc) return rc;
     rc = gemm(0, 1, n, s, s, 1.0, Y, s, Li, s, 0.0, B, s, nullptr, 0, st);
     if (rc) return rc;
   } else {
     // eigh fallback (sketch.py:114-124)
+    double shift_h = 0.0;
+    cudaMemcpyAsync(&shift_h, shift_d, sizeof(double), cudaMemcpyDeviceToHost, st);
     rc = syevj(s, core, V, wv, jws, jws_b, st);
     if (rc) return rc;
     std::vector<double> wh(s);
@@ -575,23 +779,21 @@ static int nystrom_core(int64_t n, int s, int r, const double* Q, double* Y, dou
   NYS_CHECK_LAUNCH();
   rc = syevj(s_eff, G, V, wv, jws, jws_b, st);
   if (rc) return rc;
-  std::vector<double> wh(s_eff);
-  cudaMemcpyAsync(wh.data(), wv, s_eff * sizeof(double), cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
   const int rr = r < s_eff ? r : s_eff;
-  std::vector<double> lam_h(rr), inv_sv(rr);
-  for (int j = 0; j < rr; ++j) {
-    const double sv2 = fmax(wh[j], 0.0);
-    lam_h[j] = fmax(sv2 - shift_h, 0.0);
-    inv_sv[j] = sv2 > 0.0 ? 1.0 / sqrt(sv2) : 0.0;
-  }
-  cudaMemcpyAsync(lam, lam_h.data(), rr * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(scl, inv_sv.data(), rr * sizeof(double), cudaMemcpyHostToDevice, st);
+  nystrom_lam_kernel<<<1, 256, 0, st>>>(rr, wv, shift_d, lam, scl);
+  NYS_CHECK_LAUNCH();
   scale_cols_kernel<<<(unsigned)cdiv((int64_t)s_eff * rr, 256), 256, 0, st>>>(s_eff, rr, V, s_eff,
                                                                              scl, Cm, rr);
   NYS_CHECK_LAUNCH();
   rc = gemm(0, 0, n, rr, s_eff, 1.0, B, s_eff, Cm, rr, 0.0, U, r, nullptr, 0, st);
   if (rc) return rc;
+  if (!careful) {
+    int info_c = 0;
+    if (cudaMemcpyAsync(&info_c, info, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return NYS_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+    if (info_c) return nystrom_core(n, s, r, Q, Y, U, lam, r_out, ws, ws_bytes, st, true);
+  }
   if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
   *r_out = rr;
   return NYS_OK;
@@ -619,7 +821,7 @@ extern "C" size_t nys_orthonormalize_workspace(int64_t n, int s) { return ortho_
 extern "C" int nys_orthonormalize_f64(int64_t n, int s, const double* Omega, double* Q, void* ws,
                                       size_t ws_bytes, void* stream) {
   if (n <= 0 || s <= 0 || s > n) return NYS_ERR_ARG;
-  return orthonormalize(n, s, Omega, Q, ws, ws_bytes, as_stream(stream));
+  return orthonormalize(n, s, Omega, Q, ws, ws_bytes, as_stream(stream), false);
 }
 
 extern "C" size_t nys_nystrom_workspace(int64_t n, int s, int r) { return nystrom_ws(n, s, r); }
@@ -628,7 +830,7 @@ extern "C" int nys_nystrom_core_f64(int64_t n, int s, int r, const double* Q, do
                                     double* lam, int* r_out, void* ws, size_t ws_bytes,
                                     void* stream) {
   if (n <= 0 || s <= 0 || s > n || r < 1 || r > s || !r_out) return NYS_ERR_ARG;
-  return nystrom_core(n, s, r, Q, Y, U, lam, r_out, ws, ws_bytes, as_stream(stream));
+  return nystrom_core(n, s, r, Q, Y, U, lam, r_out, ws, ws_bytes, as_stream(stream), false);
 }
 
 extern "C" size_t nys_syevj_workspace(int s) { return syevj_ws(s); }

@@ -48,14 +48,15 @@ def cg_tolerance(k: int, rp_norm: float, rd_norm: float, gamma: float = 1.2) -> 
 class CgWork:
     """Device buffers of one PCG solve (reused across ADMM iterations)."""
 
-    def __init__(self, kx, n: int):
+    def __init__(self, kx, n: int, sc: Optional[torch.Tensor] = None):
         self.kx = kx
         self.n = n
         self.r = kx.empty(n)
         self.p = kx.empty(n)
         self.z = kx.empty(n)
         self.Ap = kx.empty(n)
-        self.sc = kx.zeros(_lib.CG_NSLOTS)  # slot 7 holds a kernel ticket: keep zero
+        # slot 7 holds a kernel ticket: keep zero
+        self.sc = kx.zeros(_lib.CG_NSLOTS) if sc is None else sc
         self.host = torch.zeros(_lib.CG_NSLOTS, dtype=torch.float64)
         if kx.device.type == "cuda":
             self.host = self.host.pin_memory()

@@ -168,6 +168,46 @@ def test_syevj_degenerate_spectra(kx, kind, s):
     np.testing.assert_allclose(M @ Vn, Vn * wn, atol=1e-11 * scale * s)
 
 
+@pytest.mark.parametrize("shape", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1)])
+@pytest.mark.parametrize("M,N,K", [(5000, 133, 3000), (133, 133, 10000), (77, 45, 33)])
+def test_dgemm_every_tile_shape(kx, monkeypatch, shape, ta, tb, M, N, K):
+    """Each CTA tile shape of the planner (NYS_GEMM_SHAPE forces it), with
+    split-K where the planner picks it, against NumPy FP64."""
+    monkeypatch.setenv("NYS_GEMM_SHAPE", str(shape))
+    g = np.random.default_rng(M * 7 + N + K + shape)
+    A = g.standard_normal((K, M) if ta else (M, K))
+    B = g.standard_normal((N, K) if tb else (K, N))
+    Cd = kx.empty(M, N)
+    kx.gemm(ta, tb, M, N, K, 1.0, dev(A), A.shape[1], dev(B), B.shape[1], 0.0, Cd, N)
+    ref = (A.T if ta else A) @ (B.T if tb else B)
+    np.testing.assert_allclose(Cd.cpu().numpy(), ref, rtol=1e-11, atol=1e-12 * np.sqrt(K) * 10)
+
+
+@pytest.mark.parametrize("s", [1, 7, 64, 133, 160, 161, 200])
+def test_orthonormalize_cholinv_sizes(kx, s):
+    """The fused Cholesky-inverse kernel (s <= 160) and the split path (s > 160)."""
+    g = np.random.default_rng(s)
+    n = max(4 * s, 50)
+    Om = g.standard_normal((n, s))
+    Q = kx.empty(n, s)
+    kx.orthonormalize(dev(Om), Q)
+    Qn = Q.cpu().numpy()
+    np.testing.assert_allclose(Qn.T @ Qn, np.eye(s), atol=1e-13 * max(1, s // 16))
+    np.testing.assert_allclose(Qn @ (Qn.T @ Om), Om, atol=1e-11)
+
+
+def test_orthonormalize_singular_gram_falls_back(kx):
+    """A rank-deficient Omega makes the Cholesky fail: the deferred check must
+    catch it and the careful path must still return finite output."""
+    g = np.random.default_rng(3)
+    Om = g.standard_normal((500, 20))
+    Om[:, 7] = Om[:, 3]  # exactly dependent columns
+    Q = kx.empty(500, 20)
+    kx.orthonormalize(dev(Om), Q)
+    assert np.isfinite(Q.cpu().numpy()).all()
+
+
 def test_orthonormalize_spans_omega(kx):
     g = np.random.default_rng(1)
     Om = g.standard_normal((2000, 70))
