@@ -60,7 +60,8 @@ enum nys_cg_slot {
   NYS_CG_B2 = 5,     /* ||b||^2                                   */
   NYS_CG_FLAG = 6,   /* 0 ok, 1 non-finite pAp, 2 pAp <= 0        */
   NYS_CG_TICKET = 7, /* kernel ticket (keep zero)                 */
-  NYS_CG_DONE = 8,   /* batched CG: 0 running, 1 converged, 2 non-finite, 3 not SPD, 4 cap */
+  NYS_CG_DONE = 8,   /* batched CG: 0 running, 1 converged, 2 non-finite, 3 not SPD, 4 cap,
+                        5 skipped (closed gate: the previous ADMM iteration is unfinished) */
   NYS_CG_ITERS = 9,  /* batched CG: iterations taken              */
   NYS_CG_RESREL = 10,/* batched CG: final ||r|| / ||b||           */
   NYS_CG_RUNNING = 11,/* batched CG: 1 while iterating, 0 once DONE is set */
@@ -94,6 +95,9 @@ typedef struct nys_cg_problem {
   void* ws_op;  size_t ws_op_bytes;   /* operator workspace (zero-filled once)     */
   void* ws_pc;  size_t ws_pc_bytes;   /* preconditioner workspace                  */
   void* ws_red;                        /* reduction scratch (returned size)         */
+  const double* gate;   /* NULL, or: *gate == 0 skips the solve (sc[DONE] = 5, RUNNING = 1) */
+  const double* tol_dev;/* NULL, or the tolerance is read from *tol_dev (device-computed) */
+  int64_t timing_tag;   /* tag of the timing events of this solve (nys_timing_commit)      */
 } nys_cg_problem;
 
 /* ---------------------------------------------------------------- misc -- */
@@ -171,10 +175,11 @@ size_t nys_cg_workspace(int op_kind, int64_t rows, int64_t n, int r, size_t* ws_
 int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int count, void* stream);
 /* Instrumentation (bench roofline): with timing enabled, nys_cg_iterate_f64
  * brackets every operator launch with CUDA events tagged by its CG iteration;
- * nys_timing_commit(k) keeps those of iterations <= k (the ones that ran --
- * later launches of a batch were predicated no-ops) and drops the rest. */
+ * nys_timing_commit(tag, k) keeps those of the solve `tag` with iterations
+ * <= k (the ones that ran -- later launches of a batch were predicated no-ops)
+ * and drops that solve's others. */
 int nys_timing_enable(int on);
-int nys_timing_commit(int64_t last_real_k);
+int nys_timing_commit(int64_t tag, int64_t last_real_k);
 int nys_timing_read(double* total_ms, int64_t* launches);
 
 /* Everything of one ADMM iteration after the x-update (admm.py:562-611 and
@@ -206,8 +211,36 @@ typedef struct nys_admm_tail {
   double* infeas; double* pdx2;                   /* 6 pieces, ||P dx||^2          */
   void* ws_gemv; size_t ws_gemv_bytes; void* ws_gemvT; size_t ws_gemvT_bytes; void* ws_red;
   const double* pred;
+  double* gate_next;          /* NULL, or set to 1 once the tail has run (opens the next
+                                 iteration's gate, see nys_admm_head)                  */
+  double* conj_out;           /* NULL, or (ML, with_z, lambda2 == 0) the scaled-dual conjugate
+                                 sums of problems.py:330-340 with c = lambda1 / max|atnu|,
+                                 computed when max|atnu| > lambda1 (3 values)           */
 } nys_admm_tail;
 int nys_admm_tail_f64(const nys_admm_tail* t, void* stream);
+
+/* Start of one ADMM iteration on the device, for a host that runs one
+ * iteration ahead (admm.py:520-560 with the stopping test of iteration k-1
+ * still pending): if *gate == 0 (iteration k-1 unfinished) nothing is done.
+ * Otherwise: *gate_next = 0; snapshot (x, z, u, xbar, zbar) -> snap (5 n, may
+ * be NULL) so the host can roll back if k-1 turns out to be the last
+ * iteration; the CG tolerance of krylov.py:98-112 from the previous norms
+ *   rp, rd = sqrt(prev[0]), sqrt(prev[2])   (norm_kind 0; 1: prev[1], prev[3])
+ *   *tol_out = max(min(sqrt(rp rd), 1) / kpow, 1e-12)    (kpow = k^gamma)
+ * or *tol_out = tol_fixed when tol_fixed > 0; then the right-hand side and
+ * initial residual exactly as nys_admm_rhs_f64. */
+typedef struct nys_admm_head {
+  int64_t n;
+  const double* hxA; const double* gA; const double* q;
+  double lambda2, sigma, rho, shift;
+  const double* x; const double* z; const double* u; const double* xbar; const double* zbar;
+  double* rhs; double* r; double* sc;
+  double* snap;
+  const double* gate; double* gate_next;
+  const double* prev; int norm_kind; double kpow; double tol_fixed; double* tol_out;
+  void* ws_red;
+} nys_admm_head;
+int nys_admm_head_f64(const nys_admm_head* h, void* stream);
 
 /* ---------------------------------------------- K8/K9 ADMM elementwise -- */
 /* x-update right-hand side and initial CG residual, M = I, c = 0

@@ -33,6 +33,7 @@ PROX_SOFT, PROX_BOX = 0, 1
 # CG scalar slots (nys_cg_slot)
 CG_RZ, CG_PAP, CG_ALPHA, CG_RES2, CG_RZNEW, CG_B2, CG_FLAG = 0, 1, 2, 3, 4, 5, 6
 CG_TICKET, CG_DONE, CG_ITERS, CG_RESREL, CG_RUNNING, CG_NSLOTS = 7, 8, 9, 10, 11, 16
+CG_SKIPPED = 5  # sc[CG_DONE] of a solve whose gate was closed
 NORMS_NOUT = 16
 ROWS_NOUT = 5
 
@@ -51,7 +52,7 @@ class CgProblem(C.Structure):
         ("shift", F64), ("U", P), ("r", C.c_int), ("ldu", I64), ("lam", P), ("nu", F64),
         ("b", P), ("x", P), ("res", P), ("p", P), ("z", P), ("Ap", P), ("sc", P),
         ("tol", F64), ("max_iter", I64), ("ws_op", P), ("ws_op_bytes", SZ), ("ws_pc", P),
-        ("ws_pc_bytes", SZ), ("ws_red", P),
+        ("ws_pc_bytes", SZ), ("ws_red", P), ("gate", P), ("tol_dev", P), ("timing_tag", I64),
     ]
 
 class AdmmTail(C.Structure):
@@ -68,13 +69,25 @@ class AdmmTail(C.Structure):
         ("qp_infeas", C.c_int), ("inf_first", C.c_int), ("inf_last", C.c_int), ("width", F64),
         ("dx", P), ("Pdx", P), ("infeas", P), ("pdx2", P),
         ("ws_gemv", P), ("ws_gemv_bytes", SZ), ("ws_gemvT", P), ("ws_gemvT_bytes", SZ), ("ws_red", P),
-        ("pred", P),
+        ("pred", P), ("gate_next", P), ("conj_out", P),
+    ]
+
+
+class AdmmHead(C.Structure):
+    """Mirror of ``nys_admm_head`` (include/nysgpu.h)."""
+
+    _fields_ = [
+        ("n", I64), ("hxA", P), ("gA", P), ("q", P), ("lambda2", F64), ("sigma", F64), ("rho", F64),
+        ("shift", F64), ("x", P), ("z", P), ("u", P), ("xbar", P), ("zbar", P), ("rhs", P), ("r", P),
+        ("sc", P), ("snap", P), ("gate", P), ("gate_next", P), ("prev", P), ("norm_kind", C.c_int),
+        ("kpow", F64), ("tol_fixed", F64), ("tol_out", P), ("ws_red", P),
     ]
 
 
 # name: (restype, argtypes)
 SIGNATURES = {
     "nys_admm_tail_f64": (I32, [C.POINTER(AdmmTail), P]),
+    "nys_admm_head_f64": (I32, [C.POINTER(AdmmHead), P]),
     "nys_abi_version": (I32, []),
     "nys_status_string": (C.c_char_p, [I32]),
     "nys_device_check": (I32, []),
@@ -96,7 +109,7 @@ SIGNATURES = {
     "nys_cg_workspace": (SZ, [I32, I64, I64, I32, C.POINTER(SZ), C.POINTER(SZ)]),
     "nys_cg_iterate_f64": (I32, [C.POINTER(CgProblem), I64, I32, P]),
     "nys_timing_enable": (I32, [I32]),
-    "nys_timing_commit": (I32, [I64]),
+    "nys_timing_commit": (I32, [I64, I64]),
     "nys_timing_read": (I32, [C.POINTER(F64), C.POINTER(I64)]),
     "nys_admm_rhs_f64": (I32, [I64, P, P, P, F64, F64, F64, F64, P, P, P, P, P, P, P, P]),
     "nys_admm_zu_f64": (I32, [I64, P, P, P, F64, I32, F64, P, P, P, P, I32, P]),

@@ -29,6 +29,7 @@ buffer, HVP partials are all-reduced inside CG, the sketch Y is all-reduced.
 from __future__ import annotations
 
 import math
+import os
 import time
 from collections import deque
 from dataclasses import dataclass, field
@@ -218,6 +219,29 @@ _RB_LEN = 8 + 16 + _S_LEN
 def _host_buffer(n, device):
     t = torch.zeros(n, dtype=torch.float64)
     return t.pin_memory() if device.type == "cuda" else t
+
+
+@dataclass
+class _Issued:
+    """An ADMM iteration launched on the device (one-iteration-ahead pipeline)."""
+
+    k: int
+    par: int
+    slot: int
+    after: list
+    batch: int
+    tag: int
+    shift: float
+    exact: bool
+    win_before: list
+    reissue: Optional["_Issued"] = None
+
+
+class _ParityWork:
+    """CgWork view with the CG scalar block of one parity."""
+
+    def __init__(self, cg: CgWork, sc: torch.Tensor):
+        self.r, self.p, self.z, self.Ap, self.sc = cg.r, cg.p, cg.z, cg.Ap, sc
 
 
 class _Engine:
@@ -410,8 +434,16 @@ class _Engine:
         # host round trip per ADMM iteration); sharded runs keep the per-step path
         # because their all-reduces sit between the kernels
         self.fast = hasattr(kx, "admm_tail") and not self.shard.sharded
+        self.sigma_eff = sigma_eff
         if self.fast:
             self._make_tail()
+        # one-iteration-ahead launches: iteration k+1 is queued before the host
+        # has read k, whenever nothing that k's readback can trigger (penalty
+        # change, cycle guard, resketch) changes k+1's launch parameters; a
+        # stop at k rolls back k+1 from the snapshot its head kernel took
+        lookahead = (self.fast and opts.custom_stop is None and not opts.record_iterates
+                     and not opts.track_averaged_objective and os.environ.get("NYS_LOOKAHEAD", "1") != "0")
+        pending: Optional[_Issued] = None
 
         timings = Timings()
         r_sk = opts.sketch_rank or default_sketch_rank(n)
@@ -453,9 +485,12 @@ class _Engine:
         for k in range(1, opts.max_iter + 1):
             if opts.time_limit is not None and time.perf_counter() - t_start > opts.time_limit:
                 status = Status.TIME_LIMIT
+                if pending is not None:
+                    self._rollback()
                 break
             k_done = k
             # resketch on the cadence for iterate-dependent Hessians (admm.py:545-551)
+            # (never due for an iteration launched ahead, by the lookahead rule)
             if have_pc and not self.const_hess and k - last_sketch >= opts.resketch_every:
                 t0 = time.perf_counter()
                 self.sketch(opts.rng_seed + k)
@@ -467,17 +502,24 @@ class _Engine:
             # x-update (admm.py:243-275): rhs and the initial residual r = b - A x0
             t0 = time.perf_counter()
             shift = self.rho + sigma_eff
-            if self.is_ml:
-                kx.admm_rhs(self.AT[1], self.AT[0], None, self.l2, sigma_eff, self.rho, shift,
-                            self.x, self.z, self.u, self.rhs, self.cg.r, self.cg.sc)
-            else:
-                kx.admm_rhs(self.Px[0], self.Px[0], self.q, 0.0, sigma_eff, self.rho, shift,
-                            self.x, self.z, self.u, self.rhs, self.cg.r, self.cg.sc)
             if self.fast:
-                # CG batches with the device stop test, then the predicated rest of
-                # the iteration (z/u, data passes, norms, windows): one round trip
-                rep, st, linsys_s, prox_s, spec = self._fused_iteration(k, tol, shift, win, k >= 2)
+                # head (rhs, device tolerance), CG batches with the device stop
+                # test, predicated tail (z/u, data passes, norms, windows), readback
+                it = pending if pending is not None else self._issue(k, shift, list(win), opts.exact_x_solve)
+                pending = None
+                if lookahead and self._may_speculate(k, it, have_pc, last_sketch, rho_frozen, cycle_hits):
+                    pending = self._issue(k + 1, shift, it.after, opts.exact_x_solve)
+                rep, st, linsys_s, prox_s = self._retire(it, pending)
+                if pending is not None and pending.reissue is not None:
+                    pending = pending.reissue
+                spec = it.slot
             else:
+                if self.is_ml:
+                    kx.admm_rhs(self.AT[1], self.AT[0], None, self.l2, sigma_eff, self.rho, shift,
+                                self.x, self.z, self.u, self.rhs, self.cg.r, self.cg.sc)
+                else:
+                    kx.admm_rhs(self.Px[0], self.Px[0], self.q, 0.0, sigma_eff, self.rho, shift,
+                                self.x, self.z, self.u, self.rhs, self.cg.r, self.cg.sc)
                 rep = pcg_device(self.cg, self.matvec(shift), self.rhs, self.x, self.precond(), tol, 10 * n,
                                  started=True)
                 linsys_s = time.perf_counter() - t0
@@ -522,6 +564,8 @@ class _Engine:
                     break
             elif self._terminated(res, gap):
                 status = Status.OPTIMAL
+                if pending is not None:
+                    self._rollback()
                 break
 
             # windows (admm.py:621-634): commit the speculative append
@@ -532,6 +576,8 @@ class _Engine:
                     rho_frozen = True
                 if st_inf is not None:
                     status, cert_p, cert_d = st_inf, cp, cd
+                    if pending is not None:
+                        self._rollback()
                     break
 
             # cycle guard (admm.py:643-675)
@@ -548,6 +594,9 @@ class _Engine:
                 cycle_hits = cycle_hits + 1 if locked else 0
                 stagnant = len(trend) == trend.maxlen and trend[-1] >= 0.99 * trend[0]
                 if cycle_hits >= 5 and stagnant:
+                    if pending is not None:  # not expected under the lookahead rule
+                        self._rollback(resume=True, k=k)
+                        pending = None
                     cycle_hits = 0
                     trend.clear()
                     events.append(self._change_penalty(k, self.rho * opts.tau, have_pc, nu_identity))
@@ -569,6 +618,9 @@ class _Engine:
                 elif dm > opts.mu * pm:
                     new = self.rho / opts.tau
                 if new is not None:
+                    if pending is not None:  # not expected under the lookahead rule
+                        self._rollback(resume=True, k=k)
+                        pending = None
                     events.append(self._change_penalty(k, new, have_pc, nu_identity))
                     win.clear()
                     self._win_append(win)
@@ -624,12 +676,15 @@ class _Engine:
                 if self.loss in ("square", "huber"):
                     # degree-2 homogeneous conjugates inside their domain
                     conj_sum, b_nu = conj_sum * c * c, b_nu * c
+                elif self.fast and self._tails[0].conj_out:
+                    o = st[_S_CONJ:_S_CONJ + 3]  # computed by the tail with the same c
                 else:
                     out = self.stats[_S_CONJ:_S_CONJ + 3]
                     self.kx.ml_conj_scaled(self.loss, self.T[2], c, self.b, out)
                     if self.shard.sharded:
                         self.shard.allreduce(out)
                     o = out.cpu().numpy()
+                if self.loss not in ("square", "huber"):
                     conj_sum, n_inf, b_nu = float(o[0]), float(o[1]), float(o[2])
         if n_inf > 0:
             return np.inf
@@ -707,73 +762,130 @@ class _Engine:
 
     # ------------------------------------------------ fused iteration ----
     def _make_tail(self):
-        """Static part of the nys_admm_tail descriptor (pointers into this
-        solve's buffers; the workspaces have their own keys so they are never
-        reallocated under the descriptor)."""
+        """Device state of the one-iteration-ahead pipeline.
+
+        Iteration k uses the parity p = k % 2 copies of: the readback block
+        (row sums | CG scalars | stats), the CG problem descriptor, the tail
+        descriptor, the gate g[p] ("may run": opened by the tail of k-1) and
+        the CG tolerance slot.  The host can therefore launch k+1 before it
+        has read k (admm.py:520-700 stay on the host, one iteration behind).
+        The workspaces have their own keys so they are never reallocated
+        under the descriptors."""
         kx, L, n = self.kx, self.kx.L, self.n
-        t = _lib.AdmmTail()
-        st = self.stats
+        self.rbs = kx.zeros(2, _RB_LEN)
+        self.rbs_host = [_host_buffer(_RB_LEN, kx.device) for _ in range(2)]
+        self.gates = kx.zeros(2)
+        self.gates[1] = 1.0  # iteration 1 (parity 1) may run
+        self.tols = kx.zeros(2)
+        self.snap = kx.zeros(5, n)
+        self._done_ev = [torch.cuda.Event() for _ in range(2)]
+        self._ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(2)]
+        self._seq = 0
         ptr = lambda x: x.data_ptr() if x is not None else None
-        t.n = n
-        t.XZ = self.XZ.data_ptr()
-        t.u, t.xbar, t.zbar = self.u.data_ptr(), self.xbar.data_ptr(), self.zbar.data_ptr()
-        t.alpha = float(self.opts.alpha)
-        t.norms = st.data_ptr()
-        t.ring, t.ring_ld = self.ring.data_ptr(), self.ring.stride(0)
-        t.uring = ptr(self.uring)
-        t.wnorms = st[_S_WIN:].data_ptr()
-        t.infeas = st[_S_INF:].data_ptr()
-        t.pdx2 = st[_S_PDX:].data_ptr()
-        t.width = float(DELTA_WINDOW)
-        t.pred = self.cg.sc[_lib.CG_RUNNING:].data_ptr()
-        if self.is_ml:
-            rows = self.rows
-            t.kind, t.loss, t.rows = 0, _lib.LOSS[self.loss], rows
-            t.A, t.lda, t.b = self.A.data_ptr(), self.A.stride(0), self.b.data_ptr()
-            t.lambda1, t.lambda2 = self.l1, self.l2
-            t.with_z = 1 if self.use_gap else 0
-            t.AXZ, t.T, t.w, t.AT = self.AXZ.data_ptr(), self.T.data_ptr(), self.w.data_ptr(), self.AT.data_ptr()
-            t.rowsums = self.rowsums.data_ptr()
-            wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(rows, n, 2))
-            wt = kx.workspace("tail_gemvT", L.nys_gemvT_workspace(rows, n, 3))
-        else:
-            t.kind, t.rows = 1, n
-            t.A, t.lda = self.P.data_ptr(), self.P.stride(0)
-            t.lo, t.hi, t.q = self.lo.data_ptr(), self.hi.data_ptr(), self.q.data_ptr()
-            t.AT = self.Px.data_ptr()
-            t.dx, t.Pdx = self.dx.data_ptr(), self.Pdx.data_ptr()
-            wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(n, n, 1))
-            wt = kx.workspace("tail_gemvT", 256)
-        wr = kx.workspace("tail_red", L.nys_reduce_workspace())
-        t.ws_gemv, t.ws_gemv_bytes = wg.data_ptr(), wg.numel()
-        t.ws_gemvT, t.ws_gemvT_bytes = wt.data_ptr(), wt.numel()
-        t.ws_red = wr.data_ptr()
-        self._tail = t
-        self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        self._tails, self._pbs, self._heads = [], [], []
+        for par in range(2):
+            blk = self.rbs[par]
+            st = blk[8 + _lib.CG_NSLOTS:]
+            sc = blk[8:8 + _lib.CG_NSLOTS]
+            t = _lib.AdmmTail()
+            t.n = n
+            t.XZ = self.XZ.data_ptr()
+            t.u, t.xbar, t.zbar = self.u.data_ptr(), self.xbar.data_ptr(), self.zbar.data_ptr()
+            t.alpha = float(self.opts.alpha)
+            t.norms = st.data_ptr()
+            t.ring, t.ring_ld = self.ring.data_ptr(), self.ring.stride(0)
+            t.uring = ptr(self.uring)
+            t.wnorms = st[_S_WIN:].data_ptr()
+            t.infeas = st[_S_INF:].data_ptr()
+            t.pdx2 = st[_S_PDX:].data_ptr()
+            t.width = float(DELTA_WINDOW)
+            t.pred = sc[_lib.CG_RUNNING:].data_ptr()
+            t.gate_next = self.gates[1 - par:].data_ptr()
+            if self.is_ml:
+                rows = self.rows
+                t.kind, t.loss, t.rows = 0, _lib.LOSS[self.loss], rows
+                t.A, t.lda, t.b = self.A.data_ptr(), self.A.stride(0), self.b.data_ptr()
+                t.lambda1, t.lambda2 = self.l1, self.l2
+                t.with_z = 1 if self.use_gap else 0
+                t.AXZ, t.T, t.w, t.AT = self.AXZ.data_ptr(), self.T.data_ptr(), self.w.data_ptr(), self.AT.data_ptr()
+                t.rowsums = blk.data_ptr()
+                if self.use_gap and self.l2 == 0.0 and self.loss not in ("square", "huber"):
+                    t.conj_out = st[_S_CONJ:].data_ptr()
+                wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(rows, n, 2))
+                wt = kx.workspace("tail_gemvT", L.nys_gemvT_workspace(rows, n, 3))
+            else:
+                t.kind, t.rows = 1, n
+                t.A, t.lda = self.P.data_ptr(), self.P.stride(0)
+                t.lo, t.hi, t.q = self.lo.data_ptr(), self.hi.data_ptr(), self.q.data_ptr()
+                t.AT = self.Px.data_ptr()
+                t.dx, t.Pdx = self.dx.data_ptr(), self.Pdx.data_ptr()
+                wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(n, n, 1))
+                wt = kx.workspace("tail_gemvT", 256)
+            wr = kx.workspace("tail_red", L.nys_reduce_workspace())
+            t.ws_gemv, t.ws_gemv_bytes = wg.data_ptr(), wg.numel()
+            t.ws_gemvT, t.ws_gemvT_bytes = wt.data_ptr(), wt.numel()
+            t.ws_red = wr.data_ptr()
+            self._tails.append(t)
 
-    def _read_block(self):
-        """The whole readback block in one D2H copy; returns (sc, stats + row sums)."""
-        rb, C = self.rb_host, _lib.CG_NSLOTS
-        rb.copy_(self.rb_dev, non_blocking=True)
-        self.kx.d2h += _RB_LEN * 8
-        self.kx.sync()
-        h = rb.numpy().copy()
-        return h[8:8 + C], np.concatenate([h[8 + C:], h[:8]])
+            h = _lib.AdmmHead()
+            h.n = n
+            if self.is_ml:
+                h.hxA, h.gA, h.q, h.lambda2 = self.AT[1].data_ptr(), self.AT[0].data_ptr(), None, self.l2
+            else:
+                h.hxA = h.gA = self.Px[0].data_ptr()
+                h.q, h.lambda2 = self.q.data_ptr(), 0.0
+            h.x, h.z, h.u = self.x.data_ptr(), self.z.data_ptr(), self.u.data_ptr()
+            h.xbar, h.zbar = self.xbar.data_ptr(), self.zbar.data_ptr()
+            h.rhs, h.r, h.sc = self.rhs.data_ptr(), self.cg.r.data_ptr(), sc.data_ptr()
+            h.snap = self.snap.data_ptr()
+            h.gate, h.gate_next = self.gates[par:].data_ptr(), self.gates[1 - par:].data_ptr()
+            h.norm_kind = 1 if self.opts.norm_kind == "linf" else 0
+            h.tol_out = self.tols[par:].data_ptr()
+            h.ws_red = kx.red.data_ptr()
+            self._heads.append(h)
+            self._pbs.append(None)
 
-    def _fused_iteration(self, k, tol, shift, win, accum):
-        kx, n, t = self.kx, self.n, self._tail
-        if self.is_ml:
-            pb = kx.cg_problem(0, self.A, None if self.loss == "square" else self.w, self.diag_shift + shift,
-                               self.U, self.lam, self.pc_nu, self.rhs, self.x, self.cg, tol, 10 * n)
+    def _cg_problem(self, par, shift):
+        """The parity-par CG descriptor for the current operator shift and
+        preconditioner (rebuilt only when those change)."""
+        key = (shift, self.pc_nu, None if self.U is None else self.U.data_ptr(), self.n_sketches)
+        pb = self._pbs[par]
+        if pb is None or pb._key != key:
+            kx, n = self.kx, self.n
+            work = _ParityWork(self.cg, self.rbs[par][8:8 + _lib.CG_NSLOTS])
+            if self.is_ml:
+                pb = kx.cg_problem(0, self.A, None if self.loss == "square" else self.w, self.diag_shift + shift,
+                                   self.U, self.lam, self.pc_nu, self.rhs, self.x, work, 1e-12, 10 * n)
+            else:
+                pb = kx.cg_problem(1, self.P, None, shift, self.U, self.lam, self.pc_nu, self.rhs, self.x, work,
+                                   1e-12, 10 * n)
+            pb.gate = self.gates[par:].data_ptr()
+            pb.tol_dev = self.tols[par:].data_ptr()
+            pb._key = key
+            self._pbs[par] = pb
+        return pb
+
+    def _issue(self, k, shift, win_before, exact):
+        """Launch iteration k (head, batched CG, predicated tail, readback);
+        `win_before` is the window as it will be before k's append."""
+        kx, par = self.kx, k % 2
+        h, t = self._heads[par], self._tails[par]
+        h.rho, h.shift = float(self.rho), float(shift)
+        # the previous iteration's norms (the setup pass for k = 1)
+        h.prev = (self.stats if k == 1 else self.rbs[1 - par][8 + _lib.CG_NSLOTS:]).data_ptr()
+        h.sigma = float(self.sigma_eff)
+        if exact:
+            h.tol_fixed, h.kpow = 1e-12, 1.0
         else:
-            pb = kx.cg_problem(1, self.P, None, shift, self.U, self.lam, self.pc_nu, self.rhs, self.x, self.cg,
-                               tol, 10 * n)
-        # the window after the speculative append (committed by the host later)
-        slot = self._free_slot(win)
-        after = list(win) + [slot]
+            h.tol_fixed, h.kpow = 0.0, float(k ** self.opts.gamma)
+        pb = self._cg_problem(par, shift)
+        self._seq += 1
+        pb.timing_tag = self._seq
+        slot = self._free_slot(win_before)
+        after = list(win_before) + [slot]
         if len(after) > DELTA_WINDOW + 1:
             after = after[1:]
-        t.accum = 1 if accum else 0
+        t.accum = 1 if k >= 2 else 0
         t.rho = float(self.rho)
         t.kappa = float(self.l1 / self.rho) if self.is_ml else 0.0
         t.slot = slot
@@ -788,33 +900,111 @@ class _Engine:
         t.qp_infeas = 1 if (not self.is_ml and len(after) == DELTA_WINDOW + 1) else 0
         if t.qp_infeas:
             t.inf_first, t.inf_last = after[0], after[-1]
-        ev = self._ev
-        k_first, batch = 1, min(16, max(2, self._last_cg + 1))
-        lin_ms = tail_ms = 0.0
-        max_iter = 10 * n
-        while True:
+        batch = min(16, max(2, self._last_cg + 1))
+        ev = self._ev[par]
+        kx.admm_head(h)
+        ev[0].record(kx.stream)
+        kx.cg_iterate(pb, 1, batch)
+        ev[1].record(kx.stream)
+        kx.admm_tail(t)
+        ev[2].record(kx.stream)
+        self._readback(par)
+        return _Issued(k, par, slot, after, batch, self._seq, shift, exact, list(win_before))
+
+    def _read_block(self):
+        """The setup / per-step readback block in one D2H copy; returns
+        (sc, stats + row sums)."""
+        rb, C = self.rb_host, _lib.CG_NSLOTS
+        rb.copy_(self.rb_dev, non_blocking=True)
+        self.kx.d2h += _RB_LEN * 8
+        self.kx.sync()
+        h = rb.numpy().copy()
+        return h[8:8 + C], np.concatenate([h[8 + C:], h[:8]])
+
+    def _readback(self, par):
+        self.rbs_host[par].copy_(self.rbs[par], non_blocking=True)
+        self.kx.d2h += _RB_LEN * 8
+        self._done_ev[par].record(self.kx.stream)
+
+    def _read(self, par):
+        self._done_ev[par].synchronize()
+        h = self.rbs_host[par].numpy().copy()
+        C = _lib.CG_NSLOTS
+        return h[8:8 + C], np.concatenate([h[8 + C:], h[:8]])
+
+    def _retire(self, it, nxt):
+        """Wait for iteration `it`, finish its CG if the batch was short (and
+        re-launch the speculated successor, whose closed gate made it a
+        no-op), and return (CgReport, stats, linsys_s, prox_s)."""
+        kx, par = self.kx, it.par
+        sc, st = self._read(par)
+        ev = self._ev[par]
+        lin_ms = ev[0].elapsed_time(ev[1])
+        tail_ms = ev[1].elapsed_time(ev[2])
+        k_last, batch = it.batch, it.batch
+        max_iter = 10 * self.n
+        done = int(sc[_lib.CG_DONE])
+        while done == 0 and k_last < max_iter:
+            batch = min(16, 2 * batch)
+            pb = self._pbs[par]
             ev[0].record(kx.stream)
-            kx.cg_iterate(pb, k_first, batch)
+            kx.cg_iterate(pb, k_last + 1, batch)
             ev[1].record(kx.stream)
-            kx.admm_tail(t)
+            kx.admm_tail(self._tails[par])
             ev[2].record(kx.stream)
-            sc, st = self._read_block()
+            self._readback(par)
+            k_last += batch
+            sc, st = self._read(par)
             lin_ms += ev[0].elapsed_time(ev[1])
             tail_ms += ev[1].elapsed_time(ev[2])
             done = int(sc[_lib.CG_DONE])
+        if hasattr(kx, "timing_commit"):
+            kx.timing_commit(it.tag, int(sc[_lib.CG_ITERS]) if done else k_last)
+        if nxt is not None and k_last > it.batch:
+            # the successor ran with a closed gate: launch it again
             if hasattr(kx, "timing_commit"):
-                kx.timing_commit(int(sc[_lib.CG_ITERS]) if done else k_first + batch - 1)
-            if done or k_first + batch > max_iter:
-                break
-            k_first += batch
-            batch = min(16, 2 * batch)
+                kx.timing_commit(nxt.tag, 0)
+            nxt.reissue = self._issue(nxt.k, nxt.shift, nxt.win_before, nxt.exact)
         if done == 2:
             raise NumericalError("non-finite value in conjugate gradient")
         if done == 3:
             raise NotSPDError(f"nonpositive curvature p'Ap = {sc[_lib.CG_PAP]:.3e}; operator is not SPD")
         iters = int(sc[_lib.CG_ITERS])
         rep = CgReport(iters, float(sc[_lib.CG_RESREL]), done == 1)
-        return rep, st, lin_ms / 1e3, tail_ms / 1e3, slot
+        return rep, st, lin_ms / 1e3, tail_ms / 1e3
+
+    def _rollback(self, resume: bool = False, k: int = 0):
+        """Undo a speculated iteration: restore (x, z, u, xbar, zbar) from the
+        snapshot its head took.  With resume, also redo the data passes at the
+        restored point (the speculated tail overwrote them) and reset the gates
+        so that iteration k+1 can be launched again."""
+        self.kx.sync()
+        self.x.copy_(self.snap[0])
+        self.z.copy_(self.snap[1])
+        self.u.copy_(self.snap[2])
+        self.xbar.copy_(self.snap[3])
+        self.zbar.copy_(self.snap[4])
+        if resume:
+            self.evaluate(with_z=self.use_gap)
+            self.gates[(k + 1) % 2] = 1.0
+            self.gates[k % 2] = 0.0
+
+    def _may_speculate(self, k, it, have_pc, last_sketch, rho_frozen, cycle_hits) -> bool:
+        """May iteration k+1 be launched before k is read?  Only if no outcome
+        of k can change k+1's launch: no resketch due at k+1, no penalty check
+        at k (admm.py:677-698), no possible cycle-guard trigger at k
+        (admm.py:643-675: needs 5 consecutive hits), k+1 within max_iter."""
+        o = self.opts
+        if k + 1 > o.max_iter:
+            return False
+        if have_pc and not self.const_hess and (k + 1) - last_sketch >= o.resketch_every:
+            return False
+        if (not rho_frozen and o.penalty_update_every > 0 and k >= o.penalty_warmup
+                and k % o.penalty_update_every == 0 and k <= PENALTY_ADAPT_CUTOFF):
+            return False
+        if len(it.after) >= 4 and not rho_frozen and k <= PENALTY_ADAPT_CUTOFF and cycle_hits >= 4:
+            return False
+        return True
 
     def _infeasibility(self, st, win):
         """admm.py:361-415 with M = I from the speculative reductions."""

@@ -58,8 +58,17 @@ __device__ __forceinline__ void stop_test(double* sc, double res2, double tol, i
   if (sc[NYS_CG_DONE] != 0.0) sc[NYS_CG_RUNNING] = 0.0;
 }
 
-__global__ void cgp_begin_kernel(double* sc, double tol, int64_t max_iter) {
+__device__ __forceinline__ double tol_of(double tol, const double* tolp) { return tolp ? *tolp : tol; }
+
+__global__ void cgp_begin_kernel(double* sc, double tol, const double* tolp, const double* gate, int64_t max_iter) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (gate && *gate == 0.0) {  // previous ADMM iteration unfinished: skip this solve
+    sc[NYS_CG_DONE] = 5.0;
+    sc[NYS_CG_ITERS] = 0.0;
+    sc[NYS_CG_RUNNING] = 1.0;
+    return;
+  }
+  tol = tol_of(tol, tolp);
   sc[NYS_CG_DONE] = 0.0;
   sc[NYS_CG_ITERS] = 0.0;
   sc[NYS_CG_RUNNING] = 1.0;
@@ -78,8 +87,8 @@ __device__ __forceinline__ void block_total(double& v, double* sh) {
 
 __global__ void cgp_step_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                                 const double* __restrict__ p, const double* __restrict__ Ap, int refresh,
-                                double* sc, double tol, int64_t k, int64_t max_iter, double* part,
-                                unsigned int* counter) {
+                                double* sc, double tol, const double* tolp, int64_t k, int64_t max_iter,
+                                double* part, unsigned int* counter) {
   if (sc[NYS_CG_DONE] != 0.0) return;
   __shared__ double sh[32];
   const double pAp = sc[NYS_CG_PAP];
@@ -111,15 +120,15 @@ __global__ void cgp_step_kernel(int64_t n, double* __restrict__ x, double* __res
     const double tot = block_sum_partials(part, gridDim.x, 1, sh);
     if (threadIdx.x == 0) {
       sc[NYS_CG_ALPHA] = alpha;
-      stop_test(sc, tot, tol, k, max_iter);
+      stop_test(sc, tot, tol_of(tol, tolp), k, max_iter);
     }
   }
 }
 
 // true residual refresh (krylov.py:80-81): r = b - A x, then the stop test
 __global__ void cgp_restart_kernel(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
-                                   double* __restrict__ r, double* sc, double tol, int64_t k, int64_t max_iter,
-                                   double* part, unsigned int* counter) {
+                                   double* __restrict__ r, double* sc, double tol, const double* tolp, int64_t k,
+                                   int64_t max_iter, double* part, unsigned int* counter) {
   if (sc[NYS_CG_DONE] != 0.0) return;
   __shared__ double sh[32];
   double s = 0.0;
@@ -132,7 +141,7 @@ __global__ void cgp_restart_kernel(int64_t n, const double* __restrict__ b, cons
   if (threadIdx.x == 0) part[blockIdx.x] = s;
   if (last_block(counter)) {
     const double tot = block_sum_partials(part, gridDim.x, 1, sh);
-    if (threadIdx.x == 0) stop_test(sc, tot, tol, k, max_iter);
+    if (threadIdx.x == 0) stop_test(sc, tot, tol_of(tol, tolp), k, max_iter);
   }
 }
 
@@ -164,7 +173,7 @@ static int precondition(const nys_cg_problem* pb, cudaStream_t st, const double*
 
 // ---- optional CUDA-event timing of the HVP launches (bench roofline) -------
 struct TimedLaunch {
-  int64_t k;
+  int64_t tag, k;
   cudaEvent_t a, b;
 };
 static bool g_timing = false;
@@ -200,8 +209,13 @@ extern "C" int nys_timing_enable(int on) {
   return NYS_OK;
 }
 
-extern "C" int nys_timing_commit(int64_t last_real_k) {
+extern "C" int nys_timing_commit(int64_t tag, int64_t last_real_k) {
+  std::vector<TimedLaunch> keep;
   for (auto& t : g_pending) {
+    if (t.tag != tag) {
+      keep.push_back(t);
+      continue;
+    }
     if (t.k <= last_real_k) {
       float ms = 0.f;
       if (cudaEventSynchronize(t.b) != cudaSuccess) return NYS_ERR_CUDA;
@@ -212,7 +226,7 @@ extern "C" int nys_timing_commit(int64_t last_real_k) {
     g_pool.push_back(t.a);
     g_pool.push_back(t.b);
   }
-  g_pending.clear();
+  g_pending.swap(keep);
   return NYS_OK;
 }
 
@@ -238,7 +252,7 @@ extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int
   unsigned int* dir_counter = reinterpret_cast<unsigned int*>(sc + NYS_CG_TICKET);
   int rc;
   if (k_first == 1) {
-    cgp_begin_kernel<<<1, 32, 0, st>>>(sc, pb->tol, pb->max_iter);
+    cgp_begin_kernel<<<1, 32, 0, st>>>(sc, pb->tol, pb->tol_dev, pb->gate, pb->max_iter);
     NYS_CHECK_LAUNCH();
     if ((rc = precondition(pb, st, pred))) return rc;
     cgp_dir_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->z, pb->p, 1, sc, dir_counter);
@@ -246,7 +260,7 @@ extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int
   }
   for (int64_t k = k_first; k < k_first + count && k <= pb->max_iter; ++k) {
     const int refresh = (k % 50) == 0;  // krylov.py:16
-    TimedLaunch tl{k, nullptr, nullptr};
+    TimedLaunch tl{pb->timing_tag, k, nullptr, nullptr};
     if (g_timing) {
       tl.a = pool_get();
       tl.b = pool_get();
@@ -258,12 +272,13 @@ extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int
       g_pending.push_back(tl);
     }
     cgp_step_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->x, pb->res, pb->p, pb->Ap, refresh, sc, pb->tol,
-                                                         k, pb->max_iter, cg_part(pb->ws_red), cg_counter(pb->ws_red));
+                                                         pb->tol_dev, k, pb->max_iter, cg_part(pb->ws_red),
+                                                         cg_counter(pb->ws_red));
     NYS_CHECK_LAUNCH();
     if (refresh) {
       if ((rc = matvec(pb, pb->x, pb->Ap, nullptr, st, pred))) return rc;
-      cgp_restart_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->b, pb->Ap, pb->res, sc, pb->tol, k,
-                                                              pb->max_iter, cg_part(pb->ws_red),
+      cgp_restart_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->b, pb->Ap, pb->res, sc, pb->tol, pb->tol_dev,
+                                                              k, pb->max_iter, cg_part(pb->ws_red),
                                                               cg_counter(pb->ws_red));
       NYS_CHECK_LAUNCH();
     }

@@ -242,6 +242,52 @@ __global__ void admm_rhs_kernel(int64_t n, const double* __restrict__ hxA,
   grid_reduce<2, 0>(s, m, part, counter, sc, os, om);
 }
 
+// start of an ADMM iteration for a one-iteration-ahead host (nys_admm_head_f64)
+__global__ void admm_head_kernel(nys_admm_head h, double* part, unsigned int* counter) {
+  if (h.gate && *h.gate == 0.0) return;  // previous iteration unfinished
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (h.gate_next) *h.gate_next = 0.0;
+    if (h.tol_out) {
+      double tol;
+      if (h.tol_fixed > 0.0) {
+        tol = h.tol_fixed;
+      } else {  // krylov.py:98-112 from the residual norms of the previous iteration
+        const double* q = h.prev;
+        const double rp = h.norm_kind ? q[1] : sqrt(fmax(q[0], 0.0));
+        const double rd = h.norm_kind ? q[3] : sqrt(fmax(q[2], 0.0));
+        tol = fmax(fmin(sqrt(rp * rd), 1.0) / h.kpow, 1e-12);
+      }
+      *h.tol_out = tol;
+    }
+  }
+  const int64_t n = h.n;
+  double s[2] = {0.0, 0.0}, m[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double xi = h.x[i], zi = h.z[i], ui = h.u[i];
+    if (h.snap) {
+      h.snap[i] = xi;
+      h.snap[n + i] = zi;
+      h.snap[2 * n + i] = ui;
+      h.snap[3 * n + i] = h.xbar[i];
+      h.snap[4 * n + i] = h.zbar[i];
+    }
+    const double l2x = __dmul_rn(h.lambda2, xi);
+    const double hx = __dadd_rn(h.hxA[i], l2x);
+    double g = __dadd_rn(h.gA[i], l2x);
+    if (h.q) g = __dadd_rn(g, h.q[i]);
+    double b = __dadd_rn(__dadd_rn(hx, __dmul_rn(h.sigma, xi)), -g);
+    b = __dadd_rn(b, __dmul_rn(h.rho, __dadd_rn(zi, -ui)));
+    const double ri = __dadd_rn(b, -__dadd_rn(hx, __dmul_rn(h.shift, xi)));
+    h.rhs[i] = b;
+    h.r[i] = ri;
+    s[0] = fma(b, b, s[0]);
+    s[1] = fma(ri, ri, s[1]);
+  }
+  const int os[2] = {NYS_CG_B2, NYS_CG_RES2}, om[1] = {0};
+  grid_reduce<2, 0>(s, m, part, counter, h.sc, os, om);
+}
+
 __device__ __forceinline__ double soft1(double v, double kappa) {
   const double a = fmax(__dadd_rn(fabs(v), -kappa), 0.0);
   return v > 0.0 ? a : (v < 0.0 ? -a : 0.0 * a);
@@ -411,6 +457,33 @@ __global__ void ml_conj_scaled_kernel(int64_t rows, int loss, const double* __re
   }
   const int os[3] = {0, 1, 2}, om[1] = {0};
   grid_reduce<3, 0>(s, m, part, counter, out, os, om);
+}
+
+// the scaled-dual conjugate sums with c = lambda1 / max|atnu| computed on the
+// device (problems.py:330-340); a no-op unless max|atnu| > lambda1
+__global__ void ml_conj_dev_kernel(int64_t rows, int loss, const double* __restrict__ nu,
+                                   const double* __restrict__ denom, double lambda1,
+                                   const double* __restrict__ b, double* out, double* part,
+                                   unsigned int* counter, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  const double dn = *denom;
+  if (!(dn > lambda1)) return;
+  const double c = lambda1 / dn;
+  double s[3] = {0, 0, 0}, m[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double y = __dmul_rn(nu[i], c);
+    const double cv = loss_conj(loss, y);
+    if (isinf(cv)) s[1] += 1.0; else s[0] += cv;
+    s[2] = fma(b[i], y, s[2]);
+  }
+  const int os[3] = {0, 1, 2}, om[1] = {0};
+  grid_reduce<3, 0>(s, m, part, counter, out, os, om);
+}
+
+__global__ void open_gate_kernel(double* gate, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  if (threadIdx.x == 0) *gate = 1.0;
 }
 
 // ------------------------------------------------------- K13/K14 ----------
@@ -647,6 +720,16 @@ extern "C" int nys_admm_rhs_f64(int64_t n, const double* hxA, const double* gA, 
   return NYS_OK;
 }
 
+extern "C" int nys_admm_head_f64(const nys_admm_head* h, void* stream) {
+  if (!h || h->n <= 0 || !h->rhs || !h->r || !h->sc || !h->ws_red) return NYS_ERR_ARG;
+  if (h->snap && (!h->xbar || !h->zbar)) return NYS_ERR_ARG;
+  if (h->tol_out && h->tol_fixed <= 0.0 && (!h->prev || !(h->kpow > 0.0))) return NYS_ERR_ARG;
+  admm_head_kernel<<<vec_blocks(h->n), kVecThreads, 0, as_stream(stream)>>>(*h, red_part(h->ws_red),
+                                                                           red_counter(h->ws_red));
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
 extern "C" int nys_admm_zu_f64(int64_t n, const double* x, double* z, double* u, double alpha,
                                int prox_kind, double kappa, const double* lo, const double* hi,
                                double* xbar, double* zbar, int accum, void* stream) {
@@ -829,6 +912,17 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       return rc;
     dot_pred_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, t->Pdx, t->Pdx, t->pdx2, red_part(t->ws_red),
                                                            red_counter(t->ws_red), pred);
+    NYS_CHECK_LAUNCH();
+  }
+  // scaled-dual conjugate sums for the gap (problems.py:330-340), device-side c
+  if (t->kind == 0 && t->with_z && t->conj_out) {
+    ml_conj_dev_kernel<<<vec_blocks(t->rows), kVecThreads, 0, st>>>(
+        t->rows, t->loss, t->T + 2 * t->rows, t->norms + 13, t->lambda1, t->b, t->conj_out, red_part(t->ws_red),
+        red_counter(t->ws_red), pred);
+    NYS_CHECK_LAUNCH();
+  }
+  if (t->gate_next) {
+    open_gate_kernel<<<1, 32, 0, st>>>(t->gate_next, pred);
     NYS_CHECK_LAUNCH();
   }
   return NYS_OK;

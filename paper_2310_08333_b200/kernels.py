@@ -170,9 +170,9 @@ class Kernels:
         self.L.nys_timing_enable(1 if on else 0)
         self._lib_timing = bool(on)
 
-    def timing_commit(self, last_real_k: int) -> None:
+    def timing_commit(self, tag: int, last_real_k: int) -> None:
         if getattr(self, "_lib_timing", False):
-            check(self.L.nys_timing_commit(int(last_real_k)), "timing_commit")
+            check(self.L.nys_timing_commit(int(tag), int(last_real_k)), "timing_commit")
 
     def timing_read(self):
         tot, cnt = C.c_double(0.0), C.c_int64(0)
@@ -182,6 +182,10 @@ class Kernels:
     def admm_tail(self, t) -> None:
         self.launches += 1
         check(self.L.nys_admm_tail_f64(C.byref(t), self.sp), "admm_tail")
+
+    def admm_head(self, h) -> None:
+        self.launches += 1
+        check(self.L.nys_admm_head_f64(C.byref(h), self.sp), "admm_head")
 
     def cg_iterate(self, pb, k_first: int, count: int) -> None:
         self.launches += 1

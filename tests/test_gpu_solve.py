@@ -93,6 +93,27 @@ def test_determinism_bitwise():
     assert np.array_equal(r1.x, r2.x) and np.array_equal(r1.z, r2.z)
 
 
+@pytest.mark.parametrize("name", FAST + ["cfg1", "cfg3", "cfg2"])
+def test_lookahead_is_bitwise_neutral(name, monkeypatch):
+    """Launching iteration k+1 before k is read (device-side CG tolerance,
+    gates, snapshot rollback at the stop) changes nothing: same iterates, same
+    history, same status as the one-iteration-at-a-time schedule."""
+    import paper_2310_08333_b200 as nys
+
+    spec = cases.SOLVE_CASES[name][0]()
+    opts = nys.SolverOptions(**cases.options_for(name))
+    r1 = nys.solve(gpu_problem(spec), opts)
+    monkeypatch.setenv("NYS_LOOKAHEAD", "0")
+    r0 = nys.solve(gpu_problem(spec), opts)
+    assert r1.status == r0.status and r1.iterations == r0.iterations
+    assert np.array_equal(r1.x, r0.x) and np.array_equal(r1.z, r0.z) and np.array_equal(r1.u, r0.u)
+    if r0.x_bar is not None:
+        assert np.array_equal(r1.x_bar, r0.x_bar)
+    assert [h.cg_iters for h in r1.history] == [h.cg_iters for h in r0.history]
+    assert [h.cg_tol for h in r1.history] == [h.cg_tol for h in r0.history]
+    assert [(e.k, e.rho_new) for e in r1.penalty_events] == [(e.k, e.rho_new) for e in r0.penalty_events]
+
+
 def test_callback_and_history():
     import paper_2310_08333_b200 as nys
 
