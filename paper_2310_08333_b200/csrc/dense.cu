@@ -368,99 +368,209 @@ __global__ void __launch_bounds__(256) trinv_lower_kernel(int s, const double* _
   for (int i = lane; i < s; i += 32) X[(int64_t)i * ldx + j] = x[i];
 }
 
-// Fused Cholesky + triangular inverse for s <= kCholInvMaxS, one CTA:
-// C (lower triangle read, untouched) = L L^T, Li = L^{-1} (strict upper zeroed).
-// Factorisation (warps < kCholWarps): one barrier per column.  Step j updates
-// the trailing lower triangle with the UNSCALED column
-// (M[i][k] -= M[i][j] M[k][j] / d_j) and scales column j by 1/sqrt(d_j) in
-// step j + 1, when no thread reads it any more.
-// Inverse (all warps): one warp per column of L^{-1}, forward substitution
-// with the column in registers (lane owns rows lane + 32 m); the row blocks
-// are unrolled so the register index is static and only the diagonal block
-// is predicated.  L is read from shared memory (rows padded to 32 m).
+// Fused Cholesky + triangular inverse for s <= kCholInvMaxS, one CTA, blocked
+// by 8 with the O(s^3) work on the DMMA tensor cores:
+//   per 8-column panel  (a) warp 0 factors the 8 x 8 diagonal block in
+//                           registers (shuffles, one sqrt per column),
+//                       (b) one thread per row solves its panel row against
+//                           L11 (L21 = A21 L11^{-T}),
+//                       (c) the warps update the lower block triangle of the
+//                           trailing matrix, A22 -= L21 L21^T, one 8 x 8 block
+//                           per DMMA pair;
+//   then the 8 x 8 diagonal blocks are inverted (warp each) and warp J forms
+//   block column J of L^{-1} by block forward substitution,
+//   X_IJ = D_I^{-1} (delta_IJ I - sum_K L_IK X_KJ), the sums on DMMA with the
+//   earlier blocks read back from Li (rows/columns >= s are the identity
+//   padding and never stored).
+// C: lower triangle read, untouched.  Li: s x s, strict upper zeroed.
 // info = j + 1 at the first non-positive pivot (LAPACK potf2 rule).
-constexpr int kCholInvMaxS = 160;  // (s_pad (s|1) + s_pad) doubles fit in 227 KB
-constexpr int kCholWarps = 16;
-inline size_t cholinv_smem(int s) {
-  const size_t sp = (size_t)cdiv(s, 32) * 32;
-  return (sp * (size_t)(s | 1) + sp) * sizeof(double);
+constexpr int kCholInvMaxS = 152;  // smem: s_pad x ld + diag inverses + warp scratch <= 227 KB
+constexpr int kCholThreads = 1024;
+inline int cholinv_ld(int sp) {  // ld = 4 (mod 8): 2-wavefront DMMA fragment loads
+  int ld = sp;
+  while ((ld & 7) != 4) ++ld;
+  return ld;
 }
-__global__ void __launch_bounds__(1024) cholinv_kernel(int s, const double* __restrict__ C, int64_t ldc,
-                                                       double* __restrict__ Li, int64_t ldli, int* info) {
+inline size_t cholinv_smem(int s) {
+  const int sp = (int)cdiv(s, 8) * 8, np = sp / 8;
+  return ((size_t)sp * cholinv_ld(sp) + (size_t)np * 64 + 32 * 64 + 16) * sizeof(double);
+}
+__global__ void __launch_bounds__(kCholThreads) cholinv_kernel(int s, const double* __restrict__ C, int64_t ldc,
+                                                               double* __restrict__ Li, int64_t ldli, int* info) {
   extern __shared__ double csm[];
-  constexpr int MR = kCholInvMaxS / 32;
-  const int ld = s | 1;
-  const int s_pad = (s + 31) & ~31;
-  double* dinv = csm;
-  double* M = csm + s_pad;
+  const int sp = (s + 7) & ~7, np = sp / 8;
+  int ld = sp;
+  while ((ld & 7) != 4) ++ld;
+  double* M = csm;                              // sp x ld
+  double* Dinv = M + (size_t)sp * ld;           // np x 64
+  double* wscr = Dinv + (size_t)np * 64;        // 32 warps x 64
+  double* dinv8 = wscr + 32 * 64;               // 8
+  __shared__ int s_fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int t = tid; t < s * s; t += blockDim.x) {
-    const int i = t / s, k = t - i * s;
-    if (k <= i) M[i * ld + k] = C[(int64_t)i * ldc + k];
+  const int fr = lane >> 2, fc = lane & 3;
+  if (tid == 0) s_fail = 0;
+  for (int t = tid; t < sp * ld; t += blockDim.x) {
+    const int i = t / ld, j = t - i * ld;
+    M[t] = (j > i || j >= sp) ? 0.0 : (i < s ? C[(int64_t)i * ldc + j] : (i == j ? 1.0 : 0.0));
   }
-  for (int t = s * ld + tid; t < s_pad * ld; t += blockDim.x) M[t] = 0.0;  // padding rows
   __syncthreads();
-  int fail = 0;
-  double prev_rs = 0.0;
-  const int ctid = tid;  // factorisation threads: tid < 32 * kCholWarps
-  for (int j = 0; j < s; ++j) {
-    const double d = M[j * ld + j];
-    if (j > 0 && warp < kCholWarps) {  // deferred scaling of column j-1 (rows >= j-1)
-      for (int i = j - 1 + ctid; i < s; i += 32 * kCholWarps) {
-        double* e = M + i * ld + (j - 1);
-        *e = (i == j - 1) ? 1.0 / prev_rs : *e * prev_rs;
+  // (a) 8 x 8 diagonal block at (c, c) by warp 0: lane holds (i, j0), (i, j0 + 4),
+  // i = lane / 4; one Newton-refined reciprocal square root per column
+  auto factor_diag = [&](int c) {
+    const int i = fr, j0 = fc, j1 = fc + 4;
+    double m0 = M[(c + i) * ld + c + j0], m1 = M[(c + i) * ld + c + j1];
+    int fail = 0;
+    for (int q = 0; q < 8; ++q) {
+      const double sel = q < 4 ? m0 : m1;
+      const double dq = __shfl_sync(0xffffffffu, sel, q * 4 + (q & 3));
+      if (!(dq > 0.0) || isnan(dq)) {
+        fail = c + q + 1;
+        break;
+      }
+      double rp = rsqrt(dq);
+      rp = rp * fma(-0.5 * dq * rp, rp, 1.5);  // one Newton step: ~full precision
+      const double pq = dq * rp;
+      const double liq = __shfl_sync(0xffffffffu, sel, i * 4 + (q & 3)) * rp;
+      const double lj0 = __shfl_sync(0xffffffffu, sel, j0 * 4 + (q & 3)) * rp;
+      const double lj1 = __shfl_sync(0xffffffffu, sel, j1 * 4 + (q & 3)) * rp;
+      if (j0 > q && j0 <= i) m0 = fma(-liq, lj0, m0);
+      if (j1 > q && j1 <= i) m1 = fma(-liq, lj1, m1);
+      if (j0 == q) m0 = (i == q) ? pq : (i > q ? m0 * rp : m0);
+      if (j1 == q) m1 = (i == q) ? pq : (i > q ? m1 * rp : m1);
+    }
+    if (fail) {
+      if (lane == 0) s_fail = fail;
+    } else {
+      if (j0 <= i) M[(c + i) * ld + c + j0] = m0;
+      if (j1 <= i) M[(c + i) * ld + c + j1] = m1;
+      const int pb = (c >> 3) & 1;  // double-buffered diagonal reciprocals
+      if (j0 == i) dinv8[pb * 8 + i] = 1.0 / m0;
+      if (j1 == i) dinv8[pb * 8 + i] = 1.0 / m1;
+    }
+  };
+  // one 8 x 8 block of the trailing update, A[I][J] -= L[I][c:c+8] L[J][c:c+8]^T
+  auto update_block = [&](int I, int J, int c) {
+    double acc[2];
+    acc[0] = M[(I + fr) * ld + J + 2 * fc];
+    acc[1] = M[(I + fr) * ld + J + 2 * fc + 1];
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4) {
+      const double av = -M[(I + fr) * ld + c + kk + fc];
+      const double bv = M[(J + fr) * ld + c + kk + fc];
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[0]), "+d"(acc[1])
+                   : "d"(av), "d"(bv));
+    }
+    M[(I + fr) * ld + J + 2 * fc] = acc[0];
+    M[(I + fr) * ld + J + 2 * fc + 1] = acc[1];
+  };
+  if (warp == 0) factor_diag(0);
+  __syncthreads();
+  for (int p = 0; p < np && !s_fail; ++p) {
+    const int c = 8 * p;
+    const double* dv = dinv8 + (p & 1) * 8;
+    // (b) panel rows below the diagonal block: x = a L11^{-T}
+    for (int i = c + 8 + tid; i < sp; i += blockDim.x) {
+      double* row = M + (size_t)i * ld + c;
+      double x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double v = row[q];
+#pragma unroll
+        for (int j = 0; j < q; ++j) v = fma(-x[j], M[(c + q) * ld + c + j], v);
+        x[q] = v * dv[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) row[q] = x[q];
+    }
+    __syncthreads();
+    // (c) trailing lower block triangle (DMMA).  Lookahead: warp 0 updates the
+    // next diagonal block first and factors it while the others finish.
+    const int T = np - p - 1;
+    if (warp == 0) {
+      if (T > 0) {
+        update_block(c + 8, c + 8, c);
+        __syncwarp();
+        factor_diag(c + 8);
+      }
+    } else {
+      const int nblk = T * (T + 1) / 2;
+      for (int b = warp; b < nblk; b += nw - 1) {  // block 0 is the next diagonal block (warp 0)
+        int ir = (int)((sqrtf(8.0f * b + 1.0f) - 1.0f) * 0.5f);
+        while ((ir + 1) * (ir + 2) / 2 <= b) ++ir;
+        while (ir * (ir + 1) / 2 > b) --ir;
+        const int jr = b - ir * (ir + 1) / 2;
+        update_block(c + 8 + 8 * ir, c + 8 + 8 * jr, c);
       }
     }
-    if (!(d > 0.0) || isnan(d)) {  // uniform: every thread read the same pivot
-      fail = j + 1;
-      break;
-    }
-    if (warp < kCholWarps) {
-      const double dinv_j = 1.0 / d;
-      const double* colj = M + j;
-      for (int i = j + 1 + warp; i < s; i += kCholWarps) {
-        double* rowi = M + i * ld;
-        const double lij = rowi[j] * dinv_j;
-        const double* pc = colj + (j + 1 + lane) * ld;
-        double* pr = rowi + (j + 1 + lane);
-        for (int k = j + 1 + lane; k <= i; k += 32, pc += 32 * ld, pr += 32) *pr = fma(-lij, *pc, *pr);
-      }
-    }
-    prev_rs = 1.0 / sqrt(d);
     __syncthreads();
   }
-  if (tid == 0) *info = fail;
-  if (fail) return;
-  if (tid == 0) M[(s - 1) * ld + s - 1] = 1.0 / prev_rs;
+  if (tid == 0) *info = s_fail;
+  if (s_fail) return;
+  // inverses of the diagonal blocks: warp w, lane l < 8 solves column l
+  for (int w = warp; w < np; w += nw) {
+    const double* L = M + (size_t)(8 * w) * ld + 8 * w;
+    double x[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      double v = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < r; ++q) v = fma(-L[r * ld + q], x[q], v);
+      x[r] = v / L[r * ld + r];
+    }
+    if (lane < 8)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) Dinv[w * 64 + r * 8 + lane] = (r >= lane) ? x[r] : 0.0;
+  }
   __syncthreads();
-  for (int k = tid; k < s; k += blockDim.x) dinv[k] = 1.0 / M[k * ld + k];
-  __syncthreads();
-  for (int j = warp; j < s; j += nw) {
-    double x[MR];
+  // block column J of L^{-1} (warp J).  X_KJ (K >= J) is kept transposed in
+  // the block M[8J..][8K..] -- the upper block triangle and the diagonal
+  // blocks of L are no longer read (the diagonal inverses are in Dinv) -- so
+  // the block forward substitution runs out of shared memory.
+  for (int J = warp; J < np; J += nw) {
+    double* scr = wscr + warp * 64;
+    for (int I = 0; I < J; ++I) {  // strict upper block triangle: zeros
 #pragma unroll
-    for (int m = 0; m < MR; ++m) x[m] = (lane + 32 * m == j) ? 1.0 : 0.0;
-    const int mj = j >> 5;
-#pragma unroll
-    for (int mk = 0; mk < MR; ++mk) {
-      if (mk < mj || 32 * mk >= s) continue;  // warp-uniform
-      const int k1 = min(32 * mk + 32, s);
-      const double* rows[MR];
-#pragma unroll
-      for (int m = 0; m < MR; ++m) rows[m] = M + (lane + 32 * m) * ld;
-      for (int k = (mk == mj ? j : 32 * mk); k < k1; ++k) {
-        const int ok = k & 31;
-        const double xk = __shfl_sync(0xffffffffu, x[mk] * dinv[k], ok);
-        if (lane > ok) x[mk] = fma(-rows[mk][k], xk, x[mk]);
-        else if (lane == ok) x[mk] = xk;
-#pragma unroll
-        for (int m = mk + 1; m < MR; ++m)
-          if (32 * m < s) x[m] = fma(-rows[m][k], xk, x[m]);
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * I + fr, cc = 8 * J + 2 * fc + h;
+        if (r < s && cc < s) Li[(int64_t)r * ldli + cc] = 0.0;
       }
     }
+    for (int I = J; I < np; ++I) {
+      double acc[2] = {0.0, 0.0};
+      for (int K = J; K < I; ++K) {
 #pragma unroll
-    for (int m = 0; m < MR; ++m) {
-      const int i = lane + 32 * m;
-      if (i < s) Li[(int64_t)i * ldli + j] = x[m];
+        for (int kk = 0; kk < 8; kk += 4) {
+          const double av = M[(8 * I + fr) * ld + 8 * K + kk + fc];
+          const double bv = M[(8 * J + fr) * ld + 8 * K + kk + fc];  // X_KJ[kk + fc][fr]
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[0]), "+d"(acc[1])
+                       : "d"(av), "d"(bv));
+        }
+      }
+      // rhs = delta_IJ I - acc, staged row-major in the warp scratch
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = 2 * fc + h;
+        scr[fr * 8 + cc] = ((I == J && fr == cc) ? 1.0 : 0.0) - acc[h];
+      }
+      __syncwarp();
+      double x2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 4) {
+        const double av = Dinv[I * 64 + fr * 8 + kk + fc];
+        const double bv = scr[(kk + fc) * 8 + fr];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(x2[0]), "+d"(x2[1])
+                     : "d"(av), "d"(bv));
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * I + fr, cc = 8 * J + 2 * fc + h;
+        M[(8 * J + 2 * fc + h) * ld + 8 * I + fr] = x2[h];  // X_IJ transposed
+        if (r < s && cc < s) Li[(int64_t)r * ldli + cc] = x2[h];
+      }
+      __syncwarp();
     }
   }
 }
@@ -586,7 +696,7 @@ static int chol_inverse(int s, const double* C, double* Li, double* Lm, int* inf
       cudaFuncSetAttribute(cholinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       attr = true;
     }
-    cholinv_kernel<<<1, 1024, smem, st>>>(s, C, s, Li, s, info_dev);
+    cholinv_kernel<<<1, kCholThreads, smem, st>>>(s, C, s, Li, s, info_dev);
     NYS_CHECK_LAUNCH();
     if (!info_host) return NYS_OK;
     if (cudaMemcpyAsync(info_host, info_dev, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)

@@ -18,19 +18,29 @@
 namespace nys {
 
 constexpr int kTriMaxS = 160;
-constexpr int kTriThreads = 1024;
+constexpr int kTriThreads = 512;
 
 // --------------------------------------------------------------- K_a ------
+// Householder reduction with A in shared memory, five barriers per column:
+//   1 ||x(2:)||^2 partials        (every thread then forms beta/tau itself)
+//   2 v (scaled column) -> smem
+//   3 symv partials: thread (g, j) sums rows g, g+RG, ... of column j of A22
+//     (columns are contiguous in smem: no bank conflicts, no warp reductions)
+//   4 p_j = tau sum_g partial(g, j) and the p.v partials
+//   5 rank-2 update A22 -= v w^T + w v^T with w = p - (tau/2)(p.v) v formed on
+//     the fly.  The reflectors are stored row-wise (VhT[k][*]) for the
+//     coalesced back-transformation.
+constexpr int kTriRG = 8;  // max row groups of the symv
 __global__ void __launch_bounds__(kTriThreads)
 tridiag_kernel(int s, const double* __restrict__ A, double* __restrict__ d, double* __restrict__ e,
-               double* __restrict__ Vh, double* __restrict__ tau) {
+               double* __restrict__ VhT, double* __restrict__ tau) {
   extern __shared__ double sm[];
   const int ld = s | 1;
   double* a = sm;                         // s x ld
   double* vs = a + (size_t)s * ld;        // s
-  double* pw = vs + s;                    // s   (p, then w)
-  double* red = pw + s;                   // 32
-  __shared__ double sc_beta, sc_tau, sc_scal, sc_pv;
+  double* pw = vs + s;                    // s
+  double* part = pw + s;                  // kTriRG x s
+  double* red = part + (size_t)kTriRG * s;  // 64
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int t = tid; t < s * s; t += blockDim.x) {
     const int i = t / s, j = t - i * s;
@@ -39,67 +49,76 @@ tridiag_kernel(int s, const double* __restrict__ A, double* __restrict__ d, doub
   __syncthreads();
   for (int k = 0; k + 2 < s; ++k) {
     const int m = s - k - 1;  // size of the trailing block
-    // ||x(2:)||^2 of x = a[k+1:, k]
-    double part = 0.0;
-    for (int i = k + 2 + tid; i < s; i += blockDim.x) part = fma(a[i * ld + k], a[i * ld + k], part);
-    part = warp_sum(part);
-    if (lane == 0) red[warp] = part;
+    // 1. ||x(2:)||^2 of x = a[k+1:, k]
+    double pt = 0.0;
+    for (int i = k + 2 + tid; i < s; i += blockDim.x) pt = fma(a[i * ld + k], a[i * ld + k], pt);
+    pt = warp_sum(pt);
+    if (lane == 0) red[warp] = pt;
     __syncthreads();
-    if (tid == 0) {
-      double xn2 = 0.0;
-      for (int q = 0; q < nw; ++q) xn2 += red[q];
-      const double alpha = a[(k + 1) * ld + k];
-      if (xn2 == 0.0) {
-        sc_tau = 0.0;
-        sc_beta = alpha;
-        sc_scal = 0.0;
-      } else {
-        const double beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
-        sc_tau = (beta - alpha) / beta;
-        sc_scal = 1.0 / (alpha - beta);
-        sc_beta = beta;
-      }
-      tau[k] = sc_tau;
-      e[k] = sc_beta;
+    const double xn2 = warp_sum(lane < nw ? red[lane] : 0.0);
+    const double alpha = a[(k + 1) * ld + k];
+    double tk, beta, scal;
+    if (xn2 == 0.0) {
+      tk = 0.0;
+      beta = alpha;
+      scal = 0.0;
+    } else {
+      beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+      tk = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
     }
-    __syncthreads();
-    const double tk = sc_tau;
+    if (tid == 0) {
+      tau[k] = tk;
+      e[k] = beta;
+    }
+    // 2. reflector v (v_0 = 1)
     for (int i = tid; i < m; i += blockDim.x) {
-      const double vi = (i == 0) ? 1.0 : a[(k + 1 + i) * ld + k] * sc_scal;
+      const double vi = (i == 0) ? 1.0 : a[(k + 1 + i) * ld + k] * scal;
       vs[i] = vi;
-      Vh[(size_t)(k + 1 + i) * s + k] = vi;
+      VhT[(size_t)k * s + (k + 1 + i)] = vi;
     }
     __syncthreads();
-    if (tk == 0.0) continue;  // x(2:) == 0: H = I, nothing to update
-    // p = tau A22 v   (warp per row, lanes over columns)
-    for (int i = warp; i < m; i += nw) {
-      const double* ar = a + (k + 1 + i) * ld + (k + 1);
-      double acc = 0.0;
-      for (int j = lane; j < m; j += 32) acc = fma(ar[j], vs[j], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) pw[i] = tk * acc;
+    if (tk == 0.0) continue;  // x(2:) == 0: H = I, nothing to update (uniform)
+    // 3. symv partials over row groups
+    const int colsP = (m + 31) & ~31;
+    const int RG = min(kTriRG, (int)blockDim.x / colsP);
+    {
+      const int g = tid / colsP, j = tid - g * colsP;
+      if (g < RG && j < m) {
+        const double* col = a + (size_t)(k + 1) * ld + (k + 1) + j;
+        double acc0 = 0.0, acc1 = 0.0;
+        int i = g;
+        for (; i + RG < m; i += 2 * RG) {
+          acc0 = fma(col[(size_t)i * ld], vs[i], acc0);
+          acc1 = fma(col[(size_t)(i + RG) * ld], vs[i + RG], acc1);
+        }
+        if (i < m) acc0 = fma(col[(size_t)i * ld], vs[i], acc0);
+        part[g * s + j] = acc0 + acc1;
+      }
     }
     __syncthreads();
-    // pv = p . v ;  w = p - (tau/2)(p . v) v
-    part = 0.0;
-    for (int i = tid; i < m; i += blockDim.x) part = fma(pw[i], vs[i], part);
-    part = warp_sum(part);
-    if (lane == 0) red[warp] = part;
-    __syncthreads();
-    if (tid == 0) {
-      double pv = 0.0;
-      for (int q = 0; q < nw; ++q) pv += red[q];
-      sc_pv = pv;
+    // 4. p = tau A22 v and the p.v partials
+    pt = 0.0;
+    for (int j = tid; j < m; j += blockDim.x) {
+      double pj = 0.0;
+      for (int g = 0; g < RG; ++g) pj += part[g * s + j];
+      pj *= tk;
+      pw[j] = pj;
+      pt = fma(pj, vs[j], pt);
     }
+    pt = warp_sum(pt);
+    if (lane == 0) red[32 + warp] = pt;
     __syncthreads();
-    const double hpv = 0.5 * tk * sc_pv;
-    for (int i = tid; i < m; i += blockDim.x) pw[i] = fma(-hpv, vs[i], pw[i]);
-    __syncthreads();
-    // A22 -= v w^T + w v^T
+    const double pv = warp_sum(lane < nw ? red[32 + lane] : 0.0);
+    const double hpv = 0.5 * tk * pv;
+    // 5. A22 -= v w^T + w v^T,  w = p - hpv v
     for (int i = warp; i < m; i += nw) {
       double* ar = a + (k + 1 + i) * ld + (k + 1);
-      const double vi = vs[i], wi = pw[i];
-      for (int j = lane; j < m; j += 32) ar[j] -= fma(vi, pw[j], wi * vs[j]);
+      const double vi = vs[i], wi = fma(-hpv, vi, pw[i]);
+      for (int j = lane; j < m; j += 32) {
+        const double vj = vs[j], wj = fma(-hpv, vj, pw[j]);
+        ar[j] -= fma(vi, wj, wi * vj);
+      }
     }
     __syncthreads();
   }
@@ -109,34 +128,65 @@ tridiag_kernel(int s, const double* __restrict__ A, double* __restrict__ d, doub
 }
 
 // --------------------------------------------------------------- K_b ------
-__device__ __forceinline__ int sturm_count(int s, const double* __restrict__ d, const double* __restrict__ e,
-                                           double x, double pivmin) {
-  // number of eigenvalues of T strictly below x (LDL^T inertia)
-  int c = 0;
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  c += (q < 0.0);
-  for (int i = 1; i < s; ++i) {
-    q = d[i] - x - e[i - 1] * e[i - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    c += (q < 0.0);
+// number of eigenvalues of T strictly below x (LDL^T inertia), e2 = e^2;
+// two shifts per call.  1/q by the MUFU reciprocal approximation and two
+// Newton steps (full double precision; only the sign of q is used) keeps the
+// division's slow-path branch out of the recurrence so the chains overlap.
+__device__ __forceinline__ double rcp_nr(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  r = r * fma(-q, r, 2.0);
+  r = r * fma(-q, r, 2.0);
+  return r;
+}
+__device__ __forceinline__ void sturm_count2(int s, const double* __restrict__ d, const double* __restrict__ e2,
+                                             const double (&x)[2], double pivmin, int (&c)[2]) {
+  double q[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    q[u] = d[0] - x[u];
+    if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+    c[u] = (q[u] < 0.0);
   }
-  return c;
+  for (int i = 1; i < s; ++i) {
+    const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      q[u] = fma(-ei, rcp_nr(q[u]), di - x[u]);
+      if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+      c[u] += (q[u] < 0.0);
+    }
+  }
 }
 
-// warp w finds the w-th LARGEST eigenvalue
-__global__ void __launch_bounds__(256) bisect_kernel(int s, const double* __restrict__ d,
-                                                     const double* __restrict__ e, double* __restrict__ w) {
+// CTA (one warp) j finds the j-th LARGEST eigenvalue by 64-way multisection
+// (two shifts per lane).  One warp per SM: the Sturm recurrences are
+// latency-bound, so spreading the eigenvalues over the SMs beats packing them.
+__global__ void __launch_bounds__(32) bisect_kernel(int s, const double* __restrict__ d,
+                                                    const double* __restrict__ e, double* __restrict__ w) {
+  extern __shared__ double bsm[];
+  double* ds = bsm;
+  double* e2s = bsm + s;
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    ds[i] = d[i];
+    e2s[i] = e[i] * e[i];
+  }
+  __syncwarp();
   const int lane = threadIdx.x & 31;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (j >= s) return;
+  const int j = blockIdx.x;
   // Gershgorin interval and pivot guard (LAPACK dstebz conventions)
   double lo = INFINITY, hi = -INFINITY, emax2 = 0.0;
-  for (int i = 0; i < s; ++i) {
+  for (int i = lane; i < s; i += 32) {
     const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < s ? fabs(e[i]) : 0.0);
-    lo = fmin(lo, d[i] - r);
-    hi = fmax(hi, d[i] + r);
-    if (i + 1 < s) emax2 = fmax(emax2, e[i] * e[i]);
+    lo = fmin(lo, ds[i] - r);
+    hi = fmax(hi, ds[i] + r);
+    if (i + 1 < s) emax2 = fmax(emax2, e2s[i]);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, off));
   }
   const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax2);
   const double tnorm = fmax(fabs(lo), fabs(hi));
@@ -144,20 +194,30 @@ __global__ void __launch_bounds__(256) bisect_kernel(int s, const double* __rest
   hi += 2.2e-16 * tnorm * s + pivmin;
   const int t = s - 1 - j;  // ascending index
   double a = lo, b = hi;
-  for (int it = 0; it < 16; ++it) {
-    const double x = a + (b - a) * (double)(lane + 1) / 33.0;
-    const int c = sturm_count(s, d, e, x, pivmin);
-    const unsigned above = __ballot_sync(0xffffffffu, c > t);  // lanes whose point is above lambda_t
-    if (above == 0u) {
-      a = a + (b - a) * 32.0 / 33.0;
+  for (int it = 0; it < 14; ++it) {
+    // 64 interior points a + (b - a) q / 65, q = 1..64; lane owns q = 2 lane + u + 1
+    double x[2];
+    int c[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) x[u] = a + (b - a) * (double)(2 * lane + u + 1) / 65.0;
+    sturm_count2(s, ds, e2s, x, pivmin, c);
+    int first = 64;
+    if (c[1] > t) first = 2 * lane + 1;
+    if (c[0] > t) first = 2 * lane;
+    const unsigned any = __ballot_sync(0xffffffffu, first < 64);
+    if (any == 0u) {
+      a = a + (b - a) * 64.0 / 65.0;
     } else {
-      const int f = __ffs(above) - 1;
-      const double nb = a + (b - a) * (double)(f + 1) / 33.0;
-      const double na = f == 0 ? a : a + (b - a) * (double)f / 33.0;
+      int f = first;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, off));
+      const double nb = a + (b - a) * (double)(f + 1) / 65.0;
+      const double na = f == 0 ? a : a + (b - a) * (double)f / 65.0;
       a = na;
       b = nb;
     }
-    if (b - a <= 2.2e-16 * fmax(fabs(a), fabs(b)) + pivmin) break;
+    // relative precision, floored at the backward error of the reduction
+    if (b - a <= 2.2e-16 * fmax(fabs(a), fabs(b)) + 1e-17 * tnorm + pivmin) break;
   }
   if (lane == 0) w[j] = 0.5 * (a + b);
 }
@@ -223,17 +283,22 @@ __device__ void tri_solve(int s, const double* u0, const double* u1, const doubl
 
 // One WARP per cluster: lane 0 factors T - lam I and runs the (sequential)
 // tridiagonal solves; the Gram-Schmidt against earlier cluster members and the
-// normalisation are warp-parallel.  The vector lives in global scratch.
-__global__ void invit_kernel(int s, const double* __restrict__ d, const double* __restrict__ e,
-                             const double* __restrict__ w, const int* __restrict__ cl_start,
-                             const int* __restrict__ ncl, double* __restrict__ Y, double* __restrict__ scratch) {
-  const int lane = threadIdx.x & 31;
+// normalisation are warp-parallel.  Factor and vector live in shared memory
+// (5 s doubles + s ints per warp); the pivots are stored as reciprocals so the
+// solves' dependency chains carry no division.
+__global__ void __launch_bounds__(256) invit_kernel(int s, const double* __restrict__ d, const double* __restrict__ e,
+                                                    const double* __restrict__ w, const int* __restrict__ cl_start,
+                                                    const int* __restrict__ ncl, double* __restrict__ Y,
+                                                    double* __restrict__ scratch) {
+  extern __shared__ double ism[];
+  (void)scratch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= *ncl) return;
   double tn = 0.0;
   for (int i = 0; i < s; ++i) tn = fmax(tn, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < s ? fabs(e[i]) : 0.0));
   const double eps_t = fmax(2.2e-16 * tn, 1e-300);
-  double* u0 = scratch + (size_t)c * 6 * s;
+  double* u0 = ism + (size_t)warp * (5 * s + (s + 1) / 2 + 1);
   double* u1 = u0 + s;
   double* u2 = u1 + s;
   double* l = u2 + s;
@@ -241,7 +306,10 @@ __global__ void invit_kernel(int s, const double* __restrict__ d, const double* 
   int* piv = reinterpret_cast<int*>(y + s);
   const int j0 = cl_start[c], j1 = cl_start[c + 1];
   for (int j = j0; j < j1; ++j) {
-    if (lane == 0) tri_factor(s, d, e, w[j], eps_t, u0, u1, u2, l, piv);
+    if (lane == 0) {
+      tri_factor(s, d, e, w[j], eps_t, u0, u1, u2, l, piv);
+      for (int i = 0; i < s; ++i) u0[i] = 1.0 / u0[i];
+    }
     // deterministic pseudo-random start (LAPACK uses a random vector too)
     for (int i = lane; i < s; i += 32) {
       unsigned long long hsh = 0x9E3779B97F4A7C15ull * (unsigned long long)(j + 1) + 0xD1B54A32D192ED03ull * (i + 1);
@@ -252,7 +320,35 @@ __global__ void invit_kernel(int s, const double* __restrict__ d, const double* 
     }
     __syncwarp();
     for (int it = 0; it < 3; ++it) {
-      if (lane == 0) tri_solve(s, u0, u1, u2, l, piv, y);
+      if (lane == 0) {
+        // forward: row interchanges and multipliers
+        double yi = y[0];
+        for (int i = 0; i < s - 1; ++i) {
+          const double yn = y[i + 1];
+          if (piv[i]) {
+            y[i] = yn;
+            yi = fma(-l[i], yn, yi);
+          } else {
+            y[i] = yi;
+            yi = fma(-l[i], yi, yn);
+          }
+        }
+        y[s - 1] = yi;
+        // back substitution with the 3-diagonal upper factor (u0 holds 1/u0)
+        double y2 = y[s - 1] * u0[s - 1];
+        y[s - 1] = y2;
+        double y1 = y2;
+        if (s >= 2) {
+          y1 = (y[s - 2] - u1[s - 2] * y2) * u0[s - 2];
+          y[s - 2] = y1;
+        }
+        for (int i = s - 3; i >= 0; --i) {
+          const double yi0 = (y[i] - u1[i] * y1 - u2[i] * y2) * u0[i];
+          y[i] = yi0;
+          y2 = y1;
+          y1 = yi0;
+        }
+      }
       __syncwarp();
       // orthogonalise against the earlier members of the cluster (MGS)
       for (int q = j0; q < j; ++q) {
@@ -295,27 +391,52 @@ __global__ void cluster_kernel(int s, const double* __restrict__ d, const double
 }
 
 // --------------------------------------------------------------- K_d ------
-// z = H_0 H_1 ... H_{s-3} y  (one warp per vector), written as column j of V
-__global__ void __launch_bounds__(256) backtransform_kernel(int s, const double* __restrict__ Vh,
+// z = H_0 H_1 ... H_{s-3} y  (one warp per vector, the vector in registers:
+// lane owns rows lane + 32 m), written as column j of V; the reflectors are
+// read row-wise (coalesced) from VhT
+constexpr int kBtMR = kTriMaxS / 32;
+__global__ void __launch_bounds__(256) backtransform_kernel(int s, const double* __restrict__ VhT,
                                                             const double* __restrict__ tau,
                                                             const double* __restrict__ Y, double* __restrict__ V) {
-  extern __shared__ double ys[];  // 8 warps x s
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * 8 + warp;
   if (j >= s) return;
-  double* y = ys + (size_t)warp * s;
-  for (int i = lane; i < s; i += 32) y[i] = Y[(size_t)j * s + i];
-  __syncwarp();
-  for (int k = s - 3; k >= 0; --k) {
-    const double tk = tau[k];
-    if (tk == 0.0) continue;
-    double dot = 0.0;
-    for (int i = k + 1 + lane; i < s; i += 32) dot = fma(Vh[(size_t)i * s + k], y[i], dot);
-    dot = warp_sum(dot) * tk;
-    for (int i = k + 1 + lane; i < s; i += 32) y[i] = fma(-dot, Vh[(size_t)i * s + k], y[i]);
-    __syncwarp();
+  double y[kBtMR];
+#pragma unroll
+  for (int m = 0; m < kBtMR; ++m) {
+    const int i = lane + 32 * m;
+    y[m] = i < s ? Y[(size_t)j * s + i] : 0.0;
   }
-  for (int i = lane; i < s; i += 32) V[(size_t)i * s + j] = y[i];
+  // software pipeline: the next reflector's entries are loaded while the
+  // current one is applied
+  double vn[kBtMR];
+  auto load = [&](int k, double (&v)[kBtMR]) {
+    const double* vk = VhT + (size_t)k * s;
+#pragma unroll
+    for (int m = 0; m < kBtMR; ++m) {
+      const int i = lane + 32 * m;
+      v[m] = (i > k && i < s) ? vk[i] : 0.0;
+    }
+  };
+  if (s >= 3) load(s - 3, vn);
+  for (int k = s - 3; k >= 0; --k) {
+    double vr[kBtMR];
+#pragma unroll
+    for (int m = 0; m < kBtMR; ++m) vr[m] = vn[m];
+    if (k > 0) load(k - 1, vn);
+    const double tk = tau[k];
+    double dot = 0.0;
+#pragma unroll
+    for (int m = 0; m < kBtMR; ++m) dot = fma(vr[m], y[m], dot);
+    dot = warp_sum(dot) * tk;
+#pragma unroll
+    for (int m = 0; m < kBtMR; ++m) y[m] = fma(-dot, vr[m], y[m]);
+  }
+#pragma unroll
+  for (int m = 0; m < kBtMR; ++m) {
+    const int i = lane + 32 * m;
+    if (i < s) V[(size_t)i * s + j] = y[m];
+  }
 }
 
 int gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
@@ -341,7 +462,7 @@ int eig_tri(int s, const double* A, double* V, double* w, void* ws, cudaStream_t
   int* cl = reinterpret_cast<int*>(tau + s + 1);
   int* ncl = cl + s + 2;
   void* gws = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(ncl + 4) + 511) & ~uintptr_t(255));
-  const size_t smem = ((size_t)s * (s | 1) + 2 * (size_t)s + 32) * sizeof(double);
+  const size_t smem = ((size_t)s * (s | 1) + (2 + kTriRG) * (size_t)s + 64) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -349,12 +470,20 @@ int eig_tri(int s, const double* A, double* V, double* w, void* ws, cudaStream_t
   }
   tridiag_kernel<<<1, kTriThreads, smem, st>>>(s, A, d, e, Vh, tau);
   NYS_CHECK_LAUNCH();
-  bisect_kernel<<<(unsigned)cdiv(s, 8), 256, 0, st>>>(s, d, e, w);
+  bisect_kernel<<<(unsigned)s, 32, 2 * s * sizeof(double), st>>>(s, d, e, w);
   NYS_CHECK_LAUNCH();
   cluster_kernel<<<1, 32, 0, st>>>(s, d, e, w, cl, ncl);
   NYS_CHECK_LAUNCH();
   // one warp per potential cluster (at most s); idle warps exit
-  invit_kernel<<<(unsigned)cdiv(s, 8), 256, 0, st>>>(s, d, e, w, cl, ncl, Y, scratch);
+  {
+    const size_t ism = 8 * (5 * (size_t)s + (s + 1) / 2 + 1) * sizeof(double);
+    static bool iattr = false;
+    if (!iattr) {
+      cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (5 * kTriMaxS + 82) * 8);
+      iattr = true;
+    }
+    invit_kernel<<<(unsigned)cdiv(s, 8), 256, ism, st>>>(s, d, e, w, cl, ncl, Y, scratch);
+  }
   NYS_CHECK_LAUNCH();
   // one Newton-Schulz step Y <- 1.5 Y - 0.5 (Y Y^T) Y (rows of Y are the vectors)
   int rc = gemm(0, 1, s, s, s, 1.0, Y, s, Y, s, 0.0, G, s, gws, gemm_ws(s, s, s), st);
@@ -363,7 +492,7 @@ int eig_tri(int s, const double* A, double* V, double* w, void* ws, cudaStream_t
     return NYS_ERR_CUDA;
   rc = gemm(0, 0, s, s, s, -0.5, G, s, Y, s, 1.5, Y2, s, gws, gemm_ws(s, s, s), st);
   if (rc) return rc;
-  backtransform_kernel<<<(unsigned)cdiv(s, 8), 256, 8 * s * sizeof(double), st>>>(s, Vh, tau, Y2, V);
+  backtransform_kernel<<<(unsigned)cdiv(s, 8), 256, 0, st>>>(s, Vh, tau, Y2, V);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -184,9 +184,9 @@ def test_dgemm_every_tile_shape(kx, monkeypatch, shape, ta, tb, M, N, K):
     np.testing.assert_allclose(Cd.cpu().numpy(), ref, rtol=1e-11, atol=1e-12 * np.sqrt(K) * 10)
 
 
-@pytest.mark.parametrize("s", [1, 7, 64, 133, 160, 161, 200])
+@pytest.mark.parametrize("s", [1, 7, 8, 9, 64, 133, 152, 153, 200])
 def test_orthonormalize_cholinv_sizes(kx, s):
-    """The fused Cholesky-inverse kernel (s <= 160) and the split path (s > 160)."""
+    """The fused Cholesky-inverse kernel (s <= 152) and the split path (s > 152)."""
     g = np.random.default_rng(s)
     n = max(4 * s, 50)
     Om = g.standard_normal((n, s))

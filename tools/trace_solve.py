@@ -42,16 +42,22 @@ def main():
         by[nm][0] += 1
         by[nm][1] += t - s
     busy = 0.0
-    cur_s, cur_t = None, None
+    cur_s, cur_t, cur_nm = None, None, None
     gaps = []
-    for s, t, _ in ivs:
+    ctx = collections.defaultdict(lambda: [0, 0.0])  # (before -> after) gap context
+    for s, t, nm in ivs:
         if cur_t is None or s > cur_t:
             if cur_t is not None:
                 busy += cur_t - cur_s
                 gaps.append(s - cur_t)
+                if s - cur_t > 5:
+                    key = cur_nm.split("(")[0][-40:] + " -> " + nm.split("(")[0][-40:]
+                    ctx[key][0] += 1
+                    ctx[key][1] += s - cur_t
             cur_s, cur_t = s, t
         else:
             cur_t = max(cur_t, t)
+        cur_nm = nm
     if cur_t is not None:
         busy += cur_t - cur_s
     span = ivs[-1][1] - ivs[0][0] if ivs else 0.0
@@ -61,6 +67,8 @@ def main():
         "gpu_busy_frac": busy / span if span else 0.0, "kernels": len(ivs),
         "idle_gaps_ms_total": sum(gaps) / 1e3, "gaps_over_20us": sum(1 for g in gaps if g > 20),
         "top": [{"name": nm[:90], "count": c, "total_ms": tot / 1e3, "avg_us": tot / c} for nm, (c, tot) in top],
+        "gap_contexts": [{"between": k, "count": c, "total_ms": tot / 1e3}
+                         for k, (c, tot) in sorted(ctx.items(), key=lambda kv: -kv[1][1])[:20]],
     }
     print(json.dumps(out, indent=1))
     if args.json:
