@@ -481,10 +481,14 @@ struct HvpPlan {
   int C, W, K, S, nclusters;
   size_t smem;
   bool ok;
+  int P;
 };
 HvpPlan hvp_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
 int hvp_fused(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
               const double* v, double* ypart, cudaStream_t st, const double* pred);
+int hvp_row(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
+            const double* v, double* ypart, double* y, double shift, double* dot, double* part,
+            unsigned int* counter, cudaStream_t st, const double* pred);
 
 size_t hvp_ws(int64_t rows, int64_t n) {
   // two-pass: t = d o (A v) (rows doubles) + the K1 split partials + the K2 workspace
@@ -504,6 +508,10 @@ int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const doubl
   if (plan.ok && !two_pass_only) {
     // single pass over A (csrc/hvp.cu), then a fixed-order sum of the cluster partials
     double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
+    static const bool legacy = getenv("NYS_HVP_LEGACY") != nullptr;
+    if (plan.C == 1 && !legacy)
+      return hvp_row(plan, A, rows, n, lda, d, v, P, y, finish ? shift : 0.0, finish ? pAp : nullptr, red_part(ws),
+                     red_counter(ws), st, pred);
     int rc = hvp_fused(plan, A, rows, n, lda, d, v, P, st, pred);
     if (rc) return rc;
     const int64_t rb = tmin<int64_t>(cdiv(n, 32), kRedPartials);

@@ -245,10 +245,151 @@ hvp_fused_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t 
   if (CLUSTER) cg::this_cluster().sync();  // no CTA may exit while others write its smem
 }
 
+// Single-CTA-per-row-slice variant (C = 1, n <= 12800) with the CG finish
+// fused in.  Per row: partial dot -> barrier -> every warp forms the row scale
+// t from the 16 warp partials itself (fixed order, no serial thread-0 sum and
+// no second broadcast barrier) -> axpy -> barrier -> refill of the stage with
+// row + S, so each load has a full row of work to hide behind.  After the rows,
+// the CTAs (one per SM, cooperative launch) meet at a grid barrier and CTA b
+// sums the 148 y partials of its column slice in a fixed order, adds shift v
+// and the v.y partial; the last CTA sums the partials in a fixed order (p.Ap).
+template <int K, int P>
+__global__ void __launch_bounds__(kHvpThreads, 1)
+hvp_row_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
+               const double* __restrict__ d, const double* __restrict__ v, int W, int S,
+               double* __restrict__ ypart, double* __restrict__ y, double shift, double* __restrict__ dot,
+               double* __restrict__ part, unsigned int* counter, const double* __restrict__ pred) {
+  // P pieces per row (P = 2: half rows, so 2.5 rows fit the ring and ~1.5 rows
+  // of loads stay in flight while a row is processed); S = number of pieces
+  if (pred && *pred != 0.0) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int Wp = W / P;                                                  // piece width (doubles)
+  double* ring = reinterpret_cast<double*>(smem_raw);                   // S x Wp
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * Wp);  // S mbarriers
+  double* red = reinterpret_cast<double*>(full + S);                    // 2 x 16 warp partials
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nctas = gridDim.x, cta = blockIdx.x;
+  const int w_here = (int)n;
+  double2 vr[K], yr[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int j = 2 * (tid + k * kHvpThreads);
+    vr[k] = (j < w_here) ? *reinterpret_cast<const double2*>(v + j) : make_double2(0.0, 0.0);
+    yr[k] = make_double2(0.0, 0.0);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nrows_mine = rows > cta ? (rows - cta + nctas - 1) / nctas : 0;
+  const int64_t npieces = nrows_mine * P;
+  const unsigned pbytes = (unsigned)Wp * 8u;
+  auto issue = [&](int64_t g) {  // piece g = row g / P, part g % P, into stage g % S
+    const int q = (int)(g % S);
+    const int64_t i = cta + (g / P) * nctas;
+    mbar_expect_tx(&full[q], pbytes);
+    tma_load_1d(ring + (size_t)q * Wp, A + i * lda + (g % P) * Wp, pbytes, &full[q]);
+  };
+  if (tid == 0)
+    for (int64_t g = 0; g < S && g < npieces; ++g) issue(g);
+  for (int64_t it = 0; it < nrows_mine; ++it) {
+    // the row weight is fetched before the dot so its latency hides behind it
+    const int64_t i = cta + it * nctas;
+    const double di = d ? __ldg(d + i) : 1.0;
+    const double* pc[P];
+#pragma unroll
+    for (int h = 0; h < P; ++h) {
+      const int64_t g = it * P + h;
+      const int q = (int)(g % S);
+      pc[h] = ring + (size_t)q * Wp;
+      mbar_wait(&full[q], (unsigned)((g / S) & 1));
+    }
+    const double* pc0 = pc[0];
+    const double* pc1 = pc[P - 1] - Wp;  // P == 2: pc1 + j addresses the second half
+    auto elem = [&](int j) -> const double* { return (P == 1 || j < Wp) ? pc0 + j : pc1 + j; };
+    double pt = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = 2 * (tid + k * kHvpThreads);
+      if (j < w_here) {
+        const double2 a = *reinterpret_cast<const double2*>(elem(j));
+        pt = fma(a.x, vr[k].x, pt);
+        pt = fma(a.y, vr[k].y, pt);
+      }
+    }
+    pt = warp_sum(pt);
+    if (lane == 0) red[(it & 1) * 16 + warp] = pt;
+    __syncthreads();
+    // every warp forms t of row it (same fixed-order sum in every warp)
+    const double tot = warp_sum(lane < kHvpThreads / 32 ? red[(it & 1) * 16 + lane] : 0.0);
+    const double t = d ? di * tot : tot;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = 2 * (tid + k * kHvpThreads);
+      if (j < w_here) {
+        const double2 a = *reinterpret_cast<const double2*>(elem(j));
+        yr[k].x = fma(t, a.x, yr[k].x);
+        yr[k].y = fma(t, a.y, yr[k].y);
+      }
+    }
+    __syncthreads();  // the row's stages are free
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+      for (int h = 0; h < P; ++h) {
+        const int64_t g = it * P + h + S;
+        if (g < npieces) issue(g);
+      }
+    }
+  }
+  double* yp = ypart + (int64_t)cta * n;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int j = 2 * (tid + k * kHvpThreads);
+    if (j < w_here) *reinterpret_cast<double2*>(yp + j) = yr[k];
+  }
+  cg::this_grid().sync();
+  // column slice of this CTA: fixed-order sum over the nctas partials
+  __shared__ double cs_acc[8][65];
+  __shared__ double dsh[32];
+  const int64_t slice = ((n + nctas - 1) / nctas + 1) & ~1ll;
+  const int64_t c_begin = (int64_t)cta * slice, c_end = tmin<int64_t>(n, c_begin + slice);
+  double dacc[1] = {0.0};
+  for (int64_t cb = c_begin; cb < c_end; cb += 64) {
+    const int cx = tid & 63, ch = tid >> 6;  // 64 columns x 8 chunks
+    const int64_t c = cb + cx;
+    double acc = 0.0;
+    if (c < c_end)
+      for (int q = ch; q < nctas; q += 8) acc += ypart[(int64_t)q * n + c];
+    cs_acc[ch][cx] = acc;
+    __syncthreads();
+    if (ch == 0 && c < c_end) {
+      double a = cs_acc[0][cx];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) a += cs_acc[q][cx];
+      if (dot) {
+        a += shift * v[c];
+        dacc[0] = fma(v[c], a, dacc[0]);
+      }
+      y[c] = a;
+    }
+    __syncthreads();
+  }
+  if (!dot) return;
+  block_sum<1>(dacc, dsh);
+  if (tid == 0) part[cta] = dacc[0];
+  if (last_block(counter)) {
+    const double tot = block_sum_partials(part, nctas, 1, dsh);
+    if (tid == 0) *dot = tot;
+  }
+}
+
 struct HvpPlan {
   int C, W, K, S, nclusters;
   size_t smem;
   bool ok;
+  int P;  // C = 1 row kernel: pieces per row (S then counts pieces)
 };
 
 HvpPlan hvp_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v) {
@@ -270,6 +411,9 @@ HvpPlan hvp_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const do
   p.S = (int)tmin<int64_t>(8, (kHvpSmemBudget - 1024) / row_bytes);
   if (p.S < (p.C > 1 ? 3 : 2)) return p;
   p.smem = (size_t)p.S * row_bytes + (size_t)p.S * 8 + 1024;
+  // (half-row TMA pieces, P = 2, were measured slower on B200: the kernel is
+  // bound by the shared-memory passes over each row, not by loads in flight)
+  p.P = 1;
   p.nclusters = kNumSMs / p.C;
   p.nclusters = (int)tmax<int64_t>(1, tmin<int64_t>(p.nclusters, rows));
   p.ok = true;
@@ -313,6 +457,43 @@ static int hvp_fused_launch_k(const HvpPlan& p, const double* A, int64_t rows, i
     return NYS_ERR_CUDA;
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
   return NYS_OK;
+}
+
+template <int K, int P>
+static int hvp_row_launch_k(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda,
+                            const double* d, const double* v, double* ypart, double* y, double shift, double* dot,
+                            double* part, unsigned int* counter, cudaStream_t st, const double* pred) {
+  static bool attr = false;
+  auto fn = hvp_row_kernel<K, P>;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kHvpSmemBudget);
+    attr = true;
+  }
+  int S = p.S;  // pieces in the ring
+  int W = p.W;
+  void* args[] = {(void*)&A, (void*)&rows, (void*)&n, (void*)&lda, (void*)&d, (void*)&v, (void*)&W, (void*)&S,
+                  (void*)&ypart, (void*)&y, (void*)&shift, (void*)&dot, (void*)&part, (void*)&counter,
+                  (void*)&pred};
+  if (cudaLaunchCooperativeKernel((const void*)fn, dim3(p.nclusters), dim3(kHvpThreads), args, p.smem, st) !=
+      cudaSuccess)
+    return NYS_ERR_CUDA;
+  __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
+  return debug_sync_check(__FILE__, __LINE__) ? NYS_ERR_CUDA : NYS_OK;
+}
+
+// C = 1 plans: rows pipeline + fused finish (y = sum of partials [+ shift v],
+// dot = v.y when dot != nullptr) in one cooperative launch
+int hvp_row(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
+            const double* v, double* ypart, double* y, double shift, double* dot, double* part,
+            unsigned int* counter, cudaStream_t st, const double* pred) {
+  switch (p.K) {
+#define NYS_K(k) \
+  case k: return hvp_row_launch_k<k, 1>(p, A, rows, n, lda, d, v, ypart, y, shift, dot, part, counter, st, pred);
+    NYS_K(1) NYS_K(2) NYS_K(3) NYS_K(4) NYS_K(5) NYS_K(6) NYS_K(7) NYS_K(8) NYS_K(9) NYS_K(10) NYS_K(11)
+    NYS_K(12) NYS_K(13)
+#undef NYS_K
+    default: return NYS_ERR_UNSUPPORTED;
+  }
 }
 
 int hvp_fused(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
