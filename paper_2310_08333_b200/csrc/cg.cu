@@ -27,6 +27,11 @@ int precond_apply(const double* U, int64_t n, int r, int64_t ldu, const double* 
                   const double* v, double* z, const double* rdot, double* rz, void* ws, size_t ws_bytes,
                   cudaStream_t st, const double* pred);
 
+int precond_apply_z(const double* U, int64_t n, int r, int64_t ldu, const double* v, double* z, const double* rdot,
+                    double* rz, void* ws, cudaStream_t st, const double* pred);
+double* precond_coef(void* ws);
+double* precond_hpart(void* ws, int r);
+
 constexpr int kCgThreads = 256;
 constexpr int kCgMaxBlocks = kNumSMs * 4;
 constexpr int kCgRedPartials = 4096;
@@ -125,6 +130,130 @@ __global__ void cgp_step_kernel(int64_t n, double* __restrict__ x, double* __res
   }
 }
 
+// CG update fused with the first preconditioner pass (non-refresh
+// iterations, r > 0): x += alpha p, r -= alpha Ap, ||r||^2, and the block's
+// share of h = U^T r from the r values it just produced (staged in shared
+// memory).  The last CTA runs the stop test and forms
+// coef_j = (lam_{r-1} + nu)(h_j / (lam_j + nu)) - h_j, both from partials
+// summed in a fixed order.  Block b owns rows [64 b, 64 b + 64): each warp
+// streams 8 rows of U, four rows' loads in flight at a time.
+constexpr int kStepUtvMaxC = 16;  // rank <= 512
+constexpr int kStepUtvRows = 64;
+// STEP = false: only h = U^T v of a given v (the first preconditioner pass
+// of a solve and after a residual refresh); the predicate is then *pred.
+template <int MC, bool STEP>  // column chunks of 32: rank <= 32 MC
+__global__ void __launch_bounds__(kCgThreads)
+cgp_step_utv_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                    const double* __restrict__ Ap, double* sc, double tol, const double* tolp, int64_t k,
+                    int64_t max_iter, const double* __restrict__ U, int rk, int64_t ldu,
+                    const double* __restrict__ lam, double nu, double* __restrict__ coef,
+                    double* __restrict__ hpart, double* part, unsigned int* counter) {
+  if (sc[NYS_CG_DONE] != 0.0) return;
+  extern __shared__ double sm[];
+  double* rs = sm;                   // kStepUtvRows (the r or v values of the block's rows)
+  double* wsum = sm + kStepUtvRows;  // (kCgThreads / 32) x rk
+  __shared__ double sh[32];
+  double alpha = 0.0;
+  if (STEP) {
+    const double pAp = sc[NYS_CG_PAP];
+    const double rz = sc[NYS_CG_RZ];
+    if (!isfinite(pAp) || pAp <= 0.0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc[NYS_CG_FLAG] = !isfinite(pAp) ? 1.0 : 2.0;
+        sc[NYS_CG_DONE] = !isfinite(pAp) ? 2.0 : 3.0;  // krylov.py:74-77
+        sc[NYS_CG_ITERS] = (double)k;
+        sc[NYS_CG_RUNNING] = 0.0;
+      }
+      return;
+    }
+    alpha = rz / pAp;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * kStepUtvRows;
+  double s = 0.0;
+  if (tid < kStepUtvRows) {
+    const int64_t i = i0 + tid;
+    double ri = 0.0;
+    if (i < n) {
+      if (STEP) {
+        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+        ri = __dadd_rn(r[i], -__dmul_rn(alpha, Ap[i]));
+        r[i] = ri;
+        s = ri * ri;
+      } else {
+        ri = r[i];
+      }
+    }
+    rs[tid] = ri;
+  }
+  __syncthreads();
+  double acc[MC];
+#pragma unroll
+  for (int c = 0; c < MC; ++c) acc[c] = 0.0;
+  constexpr int RPW = kStepUtvRows / (kCgThreads / 32);  // rows per warp (8)
+#pragma unroll
+  for (int q = 0; q < RPW; q += 4) {
+    double uv[4][MC];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int ii = warp * RPW + q + h;
+      const bool ok = i0 + ii < n;
+      const double* ui = U + (i0 + ii) * ldu;
+#pragma unroll
+      for (int c = 0; c < MC; ++c) {
+        const int j = lane + 32 * c;
+        uv[h][c] = (ok && j < rk) ? ui[j] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const double ri = rs[warp * RPW + q + h];
+#pragma unroll
+      for (int c = 0; c < MC; ++c) acc[c] = fma(uv[h][c], ri, acc[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < MC; ++c) {
+    const int j = lane + 32 * c;
+    if (j < rk) wsum[warp * rk + j] = acc[c];
+  }
+  if (STEP) {
+    block_total(s, sh);
+    if (tid == 0) part[blockIdx.x] = s;
+  }
+  __syncthreads();
+  for (int j = tid; j < rk; j += kCgThreads) {
+    double h = 0.0;
+#pragma unroll
+    for (int w = 0; w < kCgThreads / 32; ++w) h += wsum[w * rk + j];
+    hpart[(int64_t)blockIdx.x * rk + j] = h;
+  }
+  if (last_block(counter)) {
+    if (STEP) {
+      const double tot = block_sum_partials(part, gridDim.x, 1, sh);
+      if (tid == 0) {
+        sc[NYS_CG_ALPHA] = alpha;
+        stop_test(sc, tot, tol_of(tol, tolp), k, max_iter);
+      }
+    }
+    const double lr = lam[rk - 1] + nu;
+    for (int j = tid; j < rk; j += kCgThreads) {
+      double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;
+      unsigned b = 0;
+      for (; b + 4 <= gridDim.x; b += 4) {
+        h0 += hpart[(int64_t)b * rk + j];
+        h1 += hpart[(int64_t)(b + 1) * rk + j];
+        h2 += hpart[(int64_t)(b + 2) * rk + j];
+        h3 += hpart[(int64_t)(b + 3) * rk + j];
+      }
+      for (; b < gridDim.x; ++b) h0 += hpart[(int64_t)b * rk + j];
+      const double h = (h0 + h1) + (h2 + h3);
+      const double head = __dmul_rn(lr, h / __dadd_rn(lam[j], nu));
+      coef[j] = __dadd_rn(head, -h);
+    }
+  }
+}
+
 // true residual refresh (krylov.py:80-81): r = b - A x, then the stop test
 __global__ void cgp_restart_kernel(int64_t n, const double* __restrict__ b, const double* __restrict__ Ax,
                                    double* __restrict__ r, double* sc, double tol, const double* tolp, int64_t k,
@@ -158,6 +287,29 @@ __global__ void cgp_dir_kernel(int64_t n, const double* __restrict__ z, double* 
   }
 }
 
+// z = P^{-1} r (Eq. 11) and rz = r.z; predicated on sc[DONE] (pred).  The
+// first pass uses the 64-row-block h = U^T r kernel when the rank allows.
+static int precondition(const nys_cg_problem* pb, cudaStream_t st, const double* pred) {
+  const int64_t n = pb->n;
+  if (pb->r > 0 && pb->r <= 32 * kStepUtvMaxC && cdiv(n, (int64_t)kStepUtvRows) <= kNumSMs * 4 &&
+      pred == pb->sc + NYS_CG_DONE) {
+    const int64_t nb = cdiv(n, (int64_t)kStepUtvRows);
+    const size_t smem = (size_t)(kStepUtvRows + (kCgThreads / 32) * pb->r) * sizeof(double);
+    auto fn = pb->r <= 128 ? cgp_step_utv_kernel<4, false>
+              : pb->r <= 256 ? cgp_step_utv_kernel<8, false>
+                             : cgp_step_utv_kernel<16, false>;
+    fn<<<(unsigned)nb, kCgThreads, smem, st>>>(n, nullptr, pb->res, nullptr, nullptr, pb->sc, 0.0, nullptr, 0, 0,
+                                               pb->U, pb->r, pb->ldu, pb->lam, pb->nu, precond_coef(pb->ws_pc),
+                                               precond_hpart(pb->ws_pc, pb->r), cg_part(pb->ws_red),
+                                               cg_counter(pb->ws_red));
+    NYS_CHECK_LAUNCH();
+    return precond_apply_z(pb->U, n, pb->r, pb->ldu, pb->res, pb->z, pb->res, pb->sc + NYS_CG_RZNEW, pb->ws_pc,
+                           st, pred);
+  }
+  return precond_apply(pb->r > 0 ? pb->U : nullptr, pb->n, pb->r, pb->ldu, pb->lam, pb->nu, pb->res, pb->z,
+                       pb->res, pb->sc + NYS_CG_RZNEW, pb->ws_pc, pb->ws_pc_bytes, st, pred);
+}
+
 static int matvec(const nys_cg_problem* pb, const double* v, double* y, double* pAp, cudaStream_t st,
                   const double* pred) {
   if (pb->op_kind == 0)
@@ -166,10 +318,7 @@ static int matvec(const nys_cg_problem* pb, const double* v, double* y, double* 
   return dense_mv_apply(pb->A, pb->n, pb->lda, v, pb->shift, y, pAp, pb->ws_op, pb->ws_op_bytes, st, pred);
 }
 
-static int precondition(const nys_cg_problem* pb, cudaStream_t st, const double* pred) {
-  return precond_apply(pb->r > 0 ? pb->U : nullptr, pb->n, pb->r, pb->ldu, pb->lam, pb->nu, pb->res, pb->z,
-                       pb->res, pb->sc + NYS_CG_RZNEW, pb->ws_pc, pb->ws_pc_bytes, st, pred);
-}
+static int precondition(const nys_cg_problem* pb, cudaStream_t st, const double* pred);
 
 // ---- optional CUDA-event timing of the HVP launches (bench roofline) -------
 struct TimedLaunch {
@@ -270,6 +419,27 @@ extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int
     if (g_timing) {
       cudaEventRecord(tl.b, st);
       g_pending.push_back(tl);
+    }
+    // (the per-block h partials live in the preconditioner workspace, sized
+    // for kNumSMs * 4 blocks: larger n keep the separate passes)
+    if (!refresh && pb->r > 0 && pb->r <= 32 * kStepUtvMaxC && cdiv(n, (int64_t)kStepUtvRows) <= kNumSMs * 4) {
+      // fused x/r update + U^T r, then the second preconditioner pass
+      const int64_t nb = cdiv(n, (int64_t)kStepUtvRows);
+      const size_t smem = (size_t)(kStepUtvRows + (kCgThreads / 32) * pb->r) * sizeof(double);
+      auto fn = pb->r <= 128 ? cgp_step_utv_kernel<4, true>
+                : pb->r <= 256 ? cgp_step_utv_kernel<8, true>
+                               : cgp_step_utv_kernel<16, true>;
+      fn<<<(unsigned)nb, kCgThreads, smem, st>>>(n, pb->x, pb->res, pb->p, pb->Ap, sc, pb->tol, pb->tol_dev, k,
+                                                 pb->max_iter, pb->U, pb->r, pb->ldu, pb->lam, pb->nu,
+                                                 precond_coef(pb->ws_pc), precond_hpart(pb->ws_pc, pb->r),
+                                                 cg_part(pb->ws_red), cg_counter(pb->ws_red));
+      NYS_CHECK_LAUNCH();
+      if ((rc = precond_apply_z(pb->U, n, pb->r, pb->ldu, pb->res, pb->z, pb->res, sc + NYS_CG_RZNEW, pb->ws_pc, st,
+                                pred)))
+        return rc;
+      cgp_dir_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->z, pb->p, 0, sc, dir_counter);
+      NYS_CHECK_LAUNCH();
+      continue;
     }
     cgp_step_kernel<<<cg_blocks(n), kCgThreads, 0, st>>>(n, pb->x, pb->res, pb->p, pb->Ap, refresh, sc, pb->tol,
                                                          pb->tol_dev, k, pb->max_iter, cg_part(pb->ws_red),

@@ -419,6 +419,40 @@ static int gemv_t_launch(const double* A, int64_t rows, int64_t n, int64_t lda, 
   return NYS_OK;
 }
 
+// The split partials of Y = A^T T only (no reduction): P[(s K + j) n + c],
+// s < *splits.  For consumers that fuse the fixed-order split sum into their
+// own epilogue (nys_admm_tail_f64).
+template <int K>
+static int gemv_t_partials_k(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T,
+                             int64_t ldt, void* ws, size_t ws_bytes, cudaStream_t st, const double* pred,
+                             double** Pout, int* splits_out) {
+  const bool vec = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((n & 1) == 0);
+  int splits;
+  int64_t rps;
+  gemv_t_plan(rows, n, vec, splits, rps);
+  if (ws_bytes < kRedBytes + (size_t)splits * K * n * sizeof(double)) return NYS_ERR_WORKSPACE;
+  double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
+  const int64_t strips = cdiv(n, (int64_t)kGemvTThreads * (vec ? 2 : 1));
+  dim3 grid((unsigned)strips, (unsigned)splits);
+  if (vec)
+    gemv_t_kernel<K, true><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt, P, n, rps, 0, pred);
+  else
+    gemv_t_kernel<K, false><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt, P, n, rps, 0, pred);
+  NYS_CHECK_LAUNCH();
+  *Pout = P;
+  *splits_out = splits;
+  return NYS_OK;
+}
+
+int gemv_t_partials(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt, int k,
+                    void* ws, size_t ws_bytes, cudaStream_t st, const double* pred, double** P, int* splits) {
+  switch (k) {
+    case 2: return gemv_t_partials_k<2>(A, rows, n, lda, T, ldt, ws, ws_bytes, st, pred, P, splits);
+    case 3: return gemv_t_partials_k<3>(A, rows, n, lda, T, ldt, ws, ws_bytes, st, pred, P, splits);
+    default: return NYS_ERR_ARG;
+  }
+}
+
 int gemv_t(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt,
            int k, double* Y, int64_t ldy, const double* v, double shift, double* dot, void* ws,
            size_t ws_bytes, cudaStream_t st, const double* pred = nullptr) {

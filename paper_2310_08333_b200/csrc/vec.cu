@@ -37,13 +37,19 @@ __device__ __forceinline__ void grid_reduce(double (&s)[(NS > 0) ? NS : 1],
     for (int j = 0; j < NM; ++j) part[blockIdx.x * NV + NS + j] = m[j];
   }
   if (last_block(counter)) {
-    for (int j = 0; j < NS; ++j) {
-      const double t = block_sum_partials(part + j, gridDim.x, NV, sh);
-      if (threadIdx.x == 0) out[osum[j]] = t;
-    }
-    for (int j = 0; j < NM; ++j) {
-      const double t = block_max_partials(part + NS + j, gridDim.x, NV, sh);
-      if (threadIdx.x == 0) out[omax[j]] = t;
+    // one warp per output (fixed lane-strided order + shuffle tree): the
+    // outputs are finished in parallel instead of one block reduction each
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = wid; j < NV; j += nw) {
+      double acc = 0.0;
+      if (j < NS) {
+        for (unsigned b = lane; b < gridDim.x; b += 32) acc += part[(size_t)b * NV + j];
+        acc = warp_sum(acc);
+      } else {
+        for (unsigned b = lane; b < gridDim.x; b += 32) acc = fmax(acc, part[(size_t)b * NV + j]);
+        acc = warp_max(acc);
+      }
+      if (lane == 0) out[j < NS ? osum[j] : omax[j - NS]] = acc;
     }
   }
 }
@@ -160,8 +166,16 @@ precond_utv_kernel(const double* __restrict__ U, int64_t n, int r, int64_t ldu,
   if (last_block(counter)) {
     const double lr = lam[r - 1] + nu;
     for (int j = threadIdx.x; j < r; j += kPcThreads) {
-      double h = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) h += part[(int64_t)b * r + j];
+      double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0;  // four chains: the loads overlap
+      unsigned b = 0;
+      for (; b + 4 <= gridDim.x; b += 4) {
+        h0 += part[(int64_t)b * r + j];
+        h1 += part[(int64_t)(b + 1) * r + j];
+        h2 += part[(int64_t)(b + 2) * r + j];
+        h3 += part[(int64_t)(b + 3) * r + j];
+      }
+      for (; b < gridDim.x; ++b) h0 += part[(int64_t)b * r + j];
+      const double h = (h0 + h1) + (h2 + h3);
       const double head = __dmul_rn(lr, h / __dadd_rn(lam[j], nu));
       coef[j] = __dadd_rn(head, -h);
     }
@@ -516,6 +530,93 @@ __global__ void window_norms_kernel(int64_t n, const double* __restrict__ ring, 
   grid_reduce<17, 0>(s, m, part, counter, out, os, om);
 }
 
+// ML iteration epilogue in one pass over column slices (nys_admm_tail_f64):
+// the fixed-order sum of the A^T split partials -> AT (K rows: gA, hxA, atnu),
+// then, for the same columns, the residual / objective / gap norms of
+// admm_norms_kernel and the cycle-guard window norms of window_norms_kernel,
+// all reduced in one grid reduction.  Block b owns columns [64 b, 64 b + 64).
+constexpr int kEpiCols = 64;
+template <int K>
+__global__ void __launch_bounds__(256)
+ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* __restrict__ AT,
+                   const double* __restrict__ x, const double* __restrict__ z, const double* __restrict__ u,
+                   double lambda2, double rho, double lambda1, const double* __restrict__ ring, int64_t ld,
+                   int cur, SlotList others, int nothers, double* out, int woff, double* part,
+                   unsigned int* counter, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  __shared__ double cs[4][K][kEpiCols];
+  const int tid = threadIdx.x, cx = tid & (kEpiCols - 1), ch = tid >> 6;
+  const int64_t c = (int64_t)blockIdx.x * kEpiCols + cx;
+  {
+    double acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = 0.0;
+    if (c < n)
+      for (int q = ch; q < splits; q += 4)
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j] += P[((int64_t)q * K + j) * n + c];
+#pragma unroll
+    for (int j = 0; j < K; ++j) cs[ch][j][cx] = acc[j];
+  }
+  __syncthreads();
+  double s[9 + 17], m[7];
+#pragma unroll
+  for (int j = 0; j < 26; ++j) s[j] = 0.0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) m[j] = 0.0;
+  double viol = -INFINITY;
+  if (ch == 0 && c < n) {
+    double at[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      at[j] = ((cs[0][j][cx] + cs[1][j][cx]) + cs[2][j][cx]) + cs[3][j][cx];
+      AT[(int64_t)j * n + c] = at[j];
+    }
+    // admm_norms_kernel, element c (gA = at[0], atnu = at[2])
+    const double xi = x[c], zi = z[c], ui = u[c];
+    const double rp = __dadd_rn(xi, -zi);
+    const double g = __dadd_rn(at[0], __dmul_rn(lambda2, xi));
+    const double ru = __dmul_rn(rho, ui);
+    const double rd = __dadd_rn(g, ru);
+    s[0] = rp * rp;
+    s[1] = rd * rd;
+    s[2] = xi * xi;
+    s[3] = zi * zi;
+    s[4] = ru * ru;
+    s[5] = fabs(zi);
+    s[6] = xi * at[0];
+    m[0] = fabs(rp);
+    m[1] = fabs(rd);
+    m[2] = fabs(xi);
+    m[3] = fabs(zi);
+    m[4] = fabs(ru);
+    if (K == 3) {
+      const double a = fabs(at[K - 1]);
+      m[5] = a;
+      const double e = fmax(a - lambda1, 0.0);
+      s[8] = e * e;
+    }
+    // window_norms_kernel, element c
+    if (nothers > 0) {
+      const double xc = ring[(int64_t)cur * ld + c];
+      s[9] = xc * xc;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < nothers) {
+          const double dd = __dadd_rn(xc, -ring[(int64_t)others.idx[j] * ld + c]);
+          s[10 + j] = dd * dd;
+        }
+      }
+    }
+  }
+  m[6] = viol;
+  const int os[26] = {0, 2, 4, 6, 8, 10, 11, 12, 14, woff, woff + 1, woff + 2, woff + 3, woff + 4, woff + 5,
+                      woff + 6, woff + 7, woff + 8, woff + 9, woff + 10, woff + 11, woff + 12, woff + 13,
+                      woff + 14, woff + 15, woff + 16};
+  const int om[7] = {1, 3, 5, 7, 9, 13, 15};
+  grid_reduce<26, 7>(s, m, part, counter, out, os, om);
+}
+
 __global__ void scale_dual_kernel(int64_t n, double* __restrict__ u, double rho_old,
                                   double rho_new, double* out, double* part,
                                   unsigned int* counter) {
@@ -673,6 +774,9 @@ extern "C" size_t nys_precond_workspace(int64_t n, int r) {
 }
 
 namespace nys {
+int precond_apply_z(const double* U, int64_t n, int r, int64_t ldu, const double* v, double* z, const double* rdot,
+                    double* rz, void* ws, cudaStream_t st, const double* pred);
+double* precond_coef(void* ws);
 // Eq. (11) apply, every launch predicated on *pred == 0 (nullptr: always run)
 int precond_apply(const double* U, int64_t n, int r, int64_t ldu, const double* lam, double nu,
                   const double* v, double* z, const double* rdot, double* rz, void* ws, size_t ws_bytes,
@@ -694,12 +798,24 @@ int precond_apply(const double* U, int64_t n, int r, int64_t ldu, const double* 
   precond_utv_kernel<<<(unsigned)nb, kPcThreads, (kPcThreads / 32) * r * sizeof(double), st>>>(
       U, n, r, ldu, v, rpb, hpart, red_counter(ws), lam, nu, coef, pred);
   NYS_CHECK_LAUNCH();
+  return precond_apply_z(U, n, r, ldu, v, z, rdot, rz, ws, st, pred);
+}
+
+// the second pass alone (coef already in the workspace, e.g. from the fused
+// CG step of cg.cu)
+int precond_apply_z(const double* U, int64_t n, int r, int64_t ldu, const double* v, double* z, const double* rdot,
+                    double* rz, void* ws, cudaStream_t st, const double* pred) {
   const int64_t ab = tmin<int64_t>(kVecMaxBlocks, cdiv(n * 32, 256));
-  precond_apply_kernel<<<(unsigned)ab, 256, r * sizeof(double), st>>>(U, n, r, ldu, coef, v, z,
+  precond_apply_kernel<<<(unsigned)ab, 256, r * sizeof(double), st>>>(U, n, r, ldu, precond_coef(ws), v, z,
                                                                       rdot, rz, RED_ARGS(ws), pred);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
+
+double* precond_coef(void* ws) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + (kRedPartials * 16 + 64) * sizeof(double));
+}
+double* precond_hpart(void* ws, int r) { return precond_coef(ws) + (r + 1); }
 }  // namespace nys
 
 extern "C" int nys_precond_apply_f64(const double* U, int64_t n, int r, int64_t ldu,
@@ -843,6 +959,8 @@ int gemv_n(const double* A, int64_t rows, int64_t n, int64_t lda, const double* 
 int gemv_t(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt, int k, double* Y,
            int64_t ldy, const double* v, double shift, double* dot, void* ws, size_t ws_bytes, cudaStream_t st,
            const double* pred);
+int gemv_t_partials(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt, int k,
+                    void* ws, size_t ws_bytes, cudaStream_t st, const double* pred, double** P, int* splits);
 }  // namespace nys
 
 extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
@@ -876,14 +994,39 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
         t->rows, t->loss, t->AXZ, t->with_z ? t->AXZ + t->rows : nullptr, t->b, t->T, t->w, t->T + t->rows,
         t->with_z ? t->T + 2 * t->rows : nullptr, t->rowsums, red_part(t->ws_red), red_counter(t->ws_red), pred);
     NYS_CHECK_LAUNCH();
-    if ((rc = gemv_t(t->A, t->rows, n, t->lda, t->T, t->rows, t->with_z ? 3 : 2, t->AT, n, nullptr, 0.0, nullptr,
-                     t->ws_gemvT, t->ws_gemvT_bytes, st, pred)))
-      return rc;
-    admm_norms_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, z, t->u, t->AT, nullptr, t->lambda2, t->rho,
-                                                             t->with_z ? t->AT + 2 * n : nullptr, t->lambda1,
-                                                             nullptr, nullptr, t->norms, red_part(t->ws_red),
-                                                             red_counter(t->ws_red), pred);
-    NYS_CHECK_LAUNCH();
+    const int64_t woff = t->wnorms - t->norms;
+    const bool fuse = woff >= 16 && woff <= 64 && cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
+    if (fuse) {
+      // A^T split partials, then one epilogue kernel: split sum -> AT, norms, window norms
+      double* P = nullptr;
+      int splits = 0;
+      const int K = t->with_z ? 3 : 2;
+      if ((rc = gemv_t_partials(t->A, t->rows, n, t->lda, t->T, t->rows, K, t->ws_gemvT, t->ws_gemvT_bytes, st,
+                                pred, &P, &splits)))
+        return rc;
+      SlotList sl;
+      const int no = (t->ring && t->nothers > 0) ? t->nothers : 0;
+      for (int j = 0; j < 16; ++j) sl.idx[j] = j < no ? t->others[j] : 0;
+      const unsigned eb = (unsigned)cdiv(n, (int64_t)kEpiCols);
+      if (K == 3)
+        ml_epilogue_kernel<3><<<eb, 256, 0, st>>>(n, P, splits, t->AT, x, z, t->u, t->lambda2, t->rho, t->lambda1,
+                                                 t->ring, t->ring_ld, t->slot, sl, no, t->norms, (int)woff,
+                                                 red_part(t->ws_red), red_counter(t->ws_red), pred);
+      else
+        ml_epilogue_kernel<2><<<eb, 256, 0, st>>>(n, P, splits, t->AT, x, z, t->u, t->lambda2, t->rho, t->lambda1,
+                                                 t->ring, t->ring_ld, t->slot, sl, no, t->norms, (int)woff,
+                                                 red_part(t->ws_red), red_counter(t->ws_red), pred);
+      NYS_CHECK_LAUNCH();
+    } else {
+      if ((rc = gemv_t(t->A, t->rows, n, t->lda, t->T, t->rows, t->with_z ? 3 : 2, t->AT, n, nullptr, 0.0, nullptr,
+                       t->ws_gemvT, t->ws_gemvT_bytes, st, pred)))
+        return rc;
+      admm_norms_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, z, t->u, t->AT, nullptr, t->lambda2, t->rho,
+                                                               t->with_z ? t->AT + 2 * n : nullptr, t->lambda1,
+                                                               nullptr, nullptr, t->norms, red_part(t->ws_red),
+                                                               red_counter(t->ws_red), pred);
+      NYS_CHECK_LAUNCH();
+    }
   } else {
     if ((rc = gemv_n(t->A, n, n, t->lda, x, n, 1, t->AT, n, nullptr, t->ws_gemv, t->ws_gemv_bytes, st, pred)))
       return rc;
@@ -892,8 +1035,11 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
                                                              red_counter(t->ws_red), pred);
     NYS_CHECK_LAUNCH();
   }
-  // cycle-guard norms for the window after the append (admm.py:645-655)
-  if (t->ring && t->nothers > 0) {
+  // cycle-guard norms for the window after the append (admm.py:645-655);
+  // the ML epilogue kernel already computed them when it ran fused
+  const bool ml_fused = t->kind == 0 && (t->wnorms - t->norms) >= 16 && (t->wnorms - t->norms) <= 64 &&
+                        cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
+  if (t->ring && t->nothers > 0 && !ml_fused) {
     SlotList sl;
     for (int j = 0; j < 16; ++j) sl.idx[j] = j < t->nothers ? t->others[j] : 0;
     window_norms_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, t->ring, t->ring_ld, t->slot, sl, t->nothers,
