@@ -5,6 +5,7 @@
 // deterministically (per-CTA partials + last-CTA fixed-order sum).
 #include <math.h>
 #include "common.cuh"
+#include "loss.cuh"
 
 namespace nys {
 
@@ -383,45 +384,6 @@ __global__ void admm_norms_kernel(int64_t n, const double* __restrict__ x,
   const int os[9] = {0, 2, 4, 6, 8, 10, 11, 12, 14};
   const int om[7] = {1, 3, 5, 7, 9, 13, 15};
   grid_reduce<9, 7>(s, m, part, counter, out, os, om);
-}
-
-// ----------------------------------------------------------- losses -------
-__device__ __forceinline__ double expit_d(double x) { return 1.0 / (1.0 + exp(-x)); }
-
-// numpy npy_logaddexp(0, w)
-__device__ __forceinline__ double logaddexp0(double w) {
-  if (w == 0.0) return 0.6931471805599453;  // log(2)
-  const double tmp = -w;
-  if (tmp > 0.0) return log1p(exp(-tmp));
-  if (tmp <= 0.0) return w + log1p(exp(tmp));
-  return tmp;  // NaN
-}
-
-__device__ __forceinline__ double loss_val(int loss, double w) {
-  if (loss == NYS_LOSS_SQUARE) return 0.5 * (w * w);
-  if (loss == NYS_LOSS_LOGISTIC) return logaddexp0(w);
-  return fabs(w) <= 1.0 ? w * w : 2.0 * fabs(w) - 1.0;
-}
-__device__ __forceinline__ double loss_d1(int loss, double w) {
-  if (loss == NYS_LOSS_SQUARE) return w;
-  if (loss == NYS_LOSS_LOGISTIC) return expit_d(w);
-  return fabs(w) <= 1.0 ? 2.0 * w : (w > 0.0 ? 2.0 : (w < 0.0 ? -2.0 : 0.0));
-}
-__device__ __forceinline__ double loss_d2(int loss, double w) {
-  if (loss == NYS_LOSS_SQUARE) return 1.0;
-  if (loss == NYS_LOSS_LOGISTIC) return expit_d(w) * expit_d(-w);
-  return fabs(w) <= 1.0 ? 2.0 : 0.0;
-}
-// conjugate; returns +inf outside the domain (problems.py:60, 65-73, 107-109)
-__device__ __forceinline__ double loss_conj(int loss, double y) {
-  if (loss == NYS_LOSS_SQUARE) return 0.5 * (y * y);
-  if (loss == NYS_LOSS_LOGISTIC) {
-    if (y == 0.0 || y == 1.0) return 0.0;
-    if (!(y >= 0.0 && y <= 1.0)) return INFINITY;
-    const double yc = fmin(fmax(y, 1e-12), 1.0 - 1e-12);
-    return yc * log(yc) + (1.0 - yc) * log1p(-yc);
-  }
-  return fabs(y) <= 2.0 ? 0.25 * (y * y) : INFINITY;
 }
 
 __global__ void ml_rowwise_kernel(int64_t rows, int loss, const double* __restrict__ Ax,
@@ -961,6 +923,9 @@ int gemv_t(const double* A, int64_t rows, int64_t n, int64_t lda, const double* 
            const double* pred);
 int gemv_t_partials(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt, int k,
                     void* ws, size_t ws_bytes, cudaStream_t st, const double* pred, double** P, int* splits);
+int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
+               const double* b, int loss, double* tg, double* w, double* thx, double* tnu, double* rowsums,
+               double* part, unsigned int* counter, cudaStream_t st, const double* pred);
 }  // namespace nys
 
 extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
@@ -986,14 +951,23 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   }
   // data passes at (x, z) (admm.py:585-587)
   if (t->kind == 0) {
-    const int k = t->with_z ? 2 : 1;
-    if ((rc = gemv_n(t->A, t->rows, n, t->lda, t->XZ, n, k, t->AXZ, t->rows, nullptr, t->ws_gemv, t->ws_gemv_bytes,
-                     st, pred)))
+    // A{x, z} + loss epilogue in one streaming pass (rowpass.cu), else the
+    // 2-RHS GEMV and the row-wise kernel
+    rc = xz_rowpass(t->A, t->rows, n, t->lda, x, t->with_z ? z : nullptr, t->b, t->loss, t->T, t->w, t->T + t->rows,
+                    t->with_z ? t->T + 2 * t->rows : nullptr, t->rowsums, red_part(t->ws_red), red_counter(t->ws_red),
+                    st, pred);
+    if (rc == NYS_ERR_UNSUPPORTED) {
+      const int k = t->with_z ? 2 : 1;
+      if ((rc = gemv_n(t->A, t->rows, n, t->lda, t->XZ, n, k, t->AXZ, t->rows, nullptr, t->ws_gemv,
+                       t->ws_gemv_bytes, st, pred)))
+        return rc;
+      ml_rowwise_kernel<<<vec_blocks(t->rows), kVecThreads, 0, st>>>(
+          t->rows, t->loss, t->AXZ, t->with_z ? t->AXZ + t->rows : nullptr, t->b, t->T, t->w, t->T + t->rows,
+          t->with_z ? t->T + 2 * t->rows : nullptr, t->rowsums, red_part(t->ws_red), red_counter(t->ws_red), pred);
+      NYS_CHECK_LAUNCH();
+    } else if (rc) {
       return rc;
-    ml_rowwise_kernel<<<vec_blocks(t->rows), kVecThreads, 0, st>>>(
-        t->rows, t->loss, t->AXZ, t->with_z ? t->AXZ + t->rows : nullptr, t->b, t->T, t->w, t->T + t->rows,
-        t->with_z ? t->T + 2 * t->rows : nullptr, t->rowsums, red_part(t->ws_red), red_counter(t->ws_red), pred);
-    NYS_CHECK_LAUNCH();
+    }
     const int64_t woff = t->wnorms - t->norms;
     const bool fuse = woff >= 16 && woff <= 64 && cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
     if (fuse) {
