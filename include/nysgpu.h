@@ -65,6 +65,8 @@ enum nys_cg_slot {
   NYS_CG_ITERS = 9,  /* batched CG: iterations taken              */
   NYS_CG_RESREL = 10,/* batched CG: final ||r|| / ||b||           */
   NYS_CG_RUNNING = 11,/* batched CG: 1 while iterating, 0 once DONE is set */
+  NYS_CG_NHVP = 12,  /* persistent CG: operator applications in the last solve */
+  NYS_CG_BETA = 13,  /* persistent CG: beta of the last direction update   */
   NYS_CG_NSLOTS = 16
 };
 
@@ -98,6 +100,9 @@ typedef struct nys_cg_problem {
   const double* gate;   /* NULL, or: *gate == 0 skips the solve (sc[DONE] = 5, RUNNING = 1) */
   const double* tol_dev;/* NULL, or the tolerance is read from *tol_dev (device-computed) */
   int64_t timing_tag;   /* tag of the timing events of this solve (nys_timing_commit)      */
+  void* ws_cp; size_t ws_cp_bytes;     /* NULL, or nys_cg_persist_workspace(n, r) bytes,
+                                          zero-filled once: the whole solve then runs as ONE
+                                          persistent cooperative kernel when the shape allows */
 } nys_cg_problem;
 
 /* ---------------------------------------------------------------- misc -- */
@@ -173,13 +178,16 @@ int nys_cg_dir_f64(int64_t n, const double* z, double* p, int first, double* sc,
  * Workspace sizes: returns the reduction scratch bytes, *ws_op / *ws_pc. */
 size_t nys_cg_workspace(int op_kind, int64_t rows, int64_t n, int r, size_t* ws_op, size_t* ws_pc);
 int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int count, void* stream);
+/* workspace of the persistent single-kernel solve (see nys_cg_problem.ws_cp) */
+size_t nys_cg_persist_workspace(int64_t n, int r);
 /* Instrumentation (bench roofline): with timing enabled, nys_cg_iterate_f64
  * brackets every operator launch with CUDA events tagged by its CG iteration;
- * nys_timing_commit(tag, k) keeps those of the solve `tag` with iterations
- * <= k (the ones that ran -- later launches of a batch were predicated no-ops)
- * and drops that solve's others. */
+ * nys_timing_commit(tag, k, units) keeps those of the solve `tag` with
+ * iterations <= k (the ones that ran -- later launches of a batch were
+ * predicated no-ops) and drops that solve's others; a persistent single-launch
+ * solve is bracketed as a whole and counts `units` operator applications. */
 int nys_timing_enable(int on);
-int nys_timing_commit(int64_t tag, int64_t last_real_k);
+int nys_timing_commit(int64_t tag, int64_t last_real_k, int64_t units);
 int nys_timing_read(double* total_ms, int64_t* launches);
 
 /* Everything of one ADMM iteration after the x-update (admm.py:562-611 and

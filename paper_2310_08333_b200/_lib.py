@@ -33,6 +33,7 @@ PROX_SOFT, PROX_BOX = 0, 1
 # CG scalar slots (nys_cg_slot)
 CG_RZ, CG_PAP, CG_ALPHA, CG_RES2, CG_RZNEW, CG_B2, CG_FLAG = 0, 1, 2, 3, 4, 5, 6
 CG_TICKET, CG_DONE, CG_ITERS, CG_RESREL, CG_RUNNING, CG_NSLOTS = 7, 8, 9, 10, 11, 16
+CG_NHVP = 12
 CG_SKIPPED = 5  # sc[CG_DONE] of a solve whose gate was closed
 NORMS_NOUT = 16
 ROWS_NOUT = 5
@@ -53,6 +54,7 @@ class CgProblem(C.Structure):
         ("b", P), ("x", P), ("res", P), ("p", P), ("z", P), ("Ap", P), ("sc", P),
         ("tol", F64), ("max_iter", I64), ("ws_op", P), ("ws_op_bytes", SZ), ("ws_pc", P),
         ("ws_pc_bytes", SZ), ("ws_red", P), ("gate", P), ("tol_dev", P), ("timing_tag", I64),
+        ("ws_cp", P), ("ws_cp_bytes", SZ),
     ]
 
 class AdmmTail(C.Structure):
@@ -109,7 +111,8 @@ SIGNATURES = {
     "nys_cg_workspace": (SZ, [I32, I64, I64, I32, C.POINTER(SZ), C.POINTER(SZ)]),
     "nys_cg_iterate_f64": (I32, [C.POINTER(CgProblem), I64, I32, P]),
     "nys_timing_enable": (I32, [I32]),
-    "nys_timing_commit": (I32, [I64, I64]),
+    "nys_timing_commit": (I32, [I64, I64, I64]),
+    "nys_cg_persist_workspace": (SZ, [I64, I32]),
     "nys_timing_read": (I32, [C.POINTER(F64), C.POINTER(I64)]),
     "nys_admm_rhs_f64": (I32, [I64, P, P, P, F64, F64, F64, F64, P, P, P, P, P, P, P, P]),
     "nys_admm_zu_f64": (I32, [I64, P, P, P, F64, I32, F64, P, P, P, P, I32, P]),

@@ -959,7 +959,7 @@ class _Engine:
             tail_ms += ev[1].elapsed_time(ev[2])
             done = int(sc[_lib.CG_DONE])
         if hasattr(kx, "timing_commit"):
-            kx.timing_commit(it.tag, int(sc[_lib.CG_ITERS]) if done else k_last)
+            kx.timing_commit(it.tag, int(sc[_lib.CG_ITERS]) if done else k_last, int(sc[_lib.CG_NHVP]))
         if nxt is not None and k_last > it.batch:
             # the successor ran with a closed gate: launch it again
             if hasattr(kx, "timing_commit"):

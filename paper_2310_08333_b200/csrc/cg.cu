@@ -32,6 +32,9 @@ int precond_apply_z(const double* U, int64_t n, int r, int64_t ldu, const double
 double* precond_coef(void* ws);
 double* precond_hpart(void* ws, int r);
 
+size_t cg_persist_ws(int64_t n, int r);
+int cg_persist(const nys_cg_problem* pb, void* ws, size_t ws_bytes, cudaStream_t st);
+
 constexpr int kCgThreads = 256;
 constexpr int kCgMaxBlocks = kNumSMs * 4;
 constexpr int kCgRedPartials = 4096;
@@ -322,7 +325,7 @@ static int precondition(const nys_cg_problem* pb, cudaStream_t st, const double*
 
 // ---- optional CUDA-event timing of the HVP launches (bench roofline) -------
 struct TimedLaunch {
-  int64_t tag, k;
+  int64_t tag, k;  // k = 0: one persistent launch covering a whole solve
   cudaEvent_t a, b;
 };
 static bool g_timing = false;
@@ -358,19 +361,22 @@ extern "C" int nys_timing_enable(int on) {
   return NYS_OK;
 }
 
-extern "C" int nys_timing_commit(int64_t tag, int64_t last_real_k) {
+extern "C" int nys_timing_commit(int64_t tag, int64_t last_real_k, int64_t units) {
+  // per-iteration launches count once each when they ran (k <= last_real_k);
+  // a persistent launch (k = 0) counts `units` operator applications
   std::vector<TimedLaunch> keep;
   for (auto& t : g_pending) {
     if (t.tag != tag) {
       keep.push_back(t);
       continue;
     }
-    if (t.k <= last_real_k) {
+    const int64_t cnt = t.k == 0 ? units : (t.k <= last_real_k ? 1 : 0);
+    if (cnt > 0) {
       float ms = 0.f;
       if (cudaEventSynchronize(t.b) != cudaSuccess) return NYS_ERR_CUDA;
       cudaEventElapsedTime(&ms, t.a, t.b);
       g_total_ms += ms;
-      ++g_count;
+      g_count += cnt;
     }
     g_pool.push_back(t.a);
     g_pool.push_back(t.b);
@@ -384,6 +390,8 @@ extern "C" int nys_timing_read(double* total_ms, int64_t* launches) {
   *launches = g_count;
   return NYS_OK;
 }
+
+extern "C" size_t nys_cg_persist_workspace(int64_t n, int r) { return cg_persist_ws(n, r < 0 ? 0 : r); }
 
 extern "C" size_t nys_cg_workspace(int op_kind, int64_t rows, int64_t n, int r, size_t* ws_op, size_t* ws_pc) {
   *ws_op = op_kind == 0 ? hvp_ws(rows, n) : dense_mv_ws(n);
@@ -400,6 +408,27 @@ extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int
   // the cg_dir ticket lives in the spare slot of the scalar block
   unsigned int* dir_counter = reinterpret_cast<unsigned int*>(sc + NYS_CG_TICKET);
   int rc;
+  if (k_first == 1 && pb->ws_cp) {
+    // the whole solve as one persistent cooperative kernel (cg_persist.cu)
+    TimedLaunch tl{pb->timing_tag, 0, nullptr, nullptr};
+    if (g_timing) {
+      tl.a = pool_get();
+      tl.b = pool_get();
+      cudaEventRecord(tl.a, st);
+    }
+    rc = cg_persist(pb, pb->ws_cp, pb->ws_cp_bytes, st);
+    if (rc != NYS_ERR_UNSUPPORTED) {
+      if (g_timing) {
+        cudaEventRecord(tl.b, st);
+        g_pending.push_back(tl);
+      }
+      return rc;
+    }
+    if (g_timing) {
+      g_pool.push_back(tl.a);
+      g_pool.push_back(tl.b);
+    }
+  }
   if (k_first == 1) {
     cgp_begin_kernel<<<1, 32, 0, st>>>(sc, pb->tol, pb->tol_dev, pb->gate, pb->max_iter);
     NYS_CHECK_LAUNCH();

@@ -1,0 +1,568 @@
+// The whole PCG solve of one ADMM x-update (krylov.py:35-95) as ONE
+// persistent cooperative kernel: one CTA per SM, grid barriers between the
+// phases of an iteration, the stopping decision taken on the device.  No
+// kernel launches, no predicated no-op launches and no launch gaps inside
+// the solve; the host enqueues it once per ADMM iteration.
+//
+// Iteration k, three grid barriers (every CTA; "slice" = its n / 148 entries):
+//   HVP   v = z + beta p (first: v = z) formed in registers (CTA c stores v's
+//         slice as the new p); ||p||^2 from the registers; rows of A streamed
+//         by TMA bulk copies into a 2-stage ring (csrc/hvp.cu), with
+//         sum_i d_i (a_i.p)^2 accumulated on the way   -> barrier
+//   STEP  every CTA forms p.Ap = sum_i d_i (a_i.p)^2 + shift ||p||^2 and alpha
+//         itself (fixed-order sums of the CTA partials); Ap, x, r of the
+//         slice, ||r||^2 and U^T r partials   -> barrier
+//         (k % 50 == 0: x only, an HVP of x, r = b - A x)
+//   APPLY every CTA runs the stop test and forms the Eq. (11) coefficients
+//         itself; z = U coef + r of the slice, r.z partial   -> barrier, beta
+// Scalars are recomputed identically by every CTA instead of broadcast by a
+// last CTA; CTA 0 publishes them in sc.  All sums are fixed-order, so the
+// result is deterministic.
+#include <cooperative_groups.h>
+#include <stdlib.h>
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace nys {
+
+constexpr int kCpThreads = 512;
+constexpr int kCpWarps = kCpThreads / 32;
+constexpr int kCpMaxK = 13;            // n <= 13312
+constexpr int kCpSmemBudget = 200 * 1024;
+
+struct CgPersistArgs {
+  const double* A;
+  int64_t rows, n, lda;
+  const double* d;
+  double shift;
+  const double* U;
+  int r;
+  int64_t ldu;
+  const double* lam;
+  double nu;
+  const double* b;
+  double* x;
+  double* res;
+  double* p[2];
+  double* z;
+  double* Ap;
+  double* sc;
+  double tol;
+  const double* tolp;
+  const double* gate;
+  int64_t max_iter;
+  double* ypart;   // nctas x n
+  double* hpart;   // nctas x r
+  double* part;    // nctas x 8
+  double* coef;    // r
+  unsigned int* counter;
+  int W, S;
+};
+
+__device__ __forceinline__ double cp_tol(const CgPersistArgs& a) { return a.tolp ? *a.tolp : a.tol; }
+
+// the reference's stop test on ||r||^2 (krylov.py:84-88)
+__device__ void cp_stop(double* sc, double res2, double tol, int64_t k, int64_t max_iter) {
+  const double b2 = sc[NYS_CG_B2];
+  const double denom = b2 > 0.0 ? sqrt(b2) : 1.0;
+  const double res = sqrt(res2);
+  sc[NYS_CG_RES2] = res2;
+  if (!isfinite(res)) {
+    sc[NYS_CG_DONE] = 2.0;
+    sc[NYS_CG_ITERS] = (double)k;
+  } else if (res <= tol * denom) {
+    sc[NYS_CG_DONE] = 1.0;
+    sc[NYS_CG_ITERS] = (double)k;
+  } else if (k >= max_iter) {
+    sc[NYS_CG_DONE] = 4.0;
+    sc[NYS_CG_ITERS] = (double)k;
+  }
+  sc[NYS_CG_RESREL] = res / denom;
+  if (sc[NYS_CG_DONE] != 0.0) sc[NYS_CG_RUNNING] = 0.0;
+}
+
+// block sum of v, valid in every thread (sh: 32 doubles; two barriers)
+__device__ __forceinline__ double cp_block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  return warp_sum(lane < kCpWarps ? sh[lane] : 0.0);
+}
+
+template <int K, int MC>
+__global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);                        // S x W
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)a.S * a.W);    // S
+  double* red = reinterpret_cast<double*>(full + a.S);                       // 2 x 16
+  double* sh = red + 32;                                                     // 32
+  double* csh = sh + 32;                                                     // coef (r <= 512)
+  double* ys = csh + 520;                                                    // slice sums
+  __shared__ double s_bcast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nctas = gridDim.x, cta = blockIdx.x;
+  const int64_t n = a.n;
+  double* sc = a.sc;
+  const bool writer = cta == 0 && tid == 0;  // the one thread that publishes sc
+  // ---------------------------------------------------------- begin ----
+  // every CTA evaluates the begin logic itself (same inputs, same result)
+  const double tol = cp_tol(a);
+  {
+    const bool skip = a.gate && *a.gate == 0.0;  // previous ADMM iteration unfinished
+    const double b2 = sc[NYS_CG_B2], res2 = sc[NYS_CG_RES2];
+    const double denom = b2 > 0.0 ? sqrt(b2) : 1.0;
+    const double res = sqrt(res2);
+    const bool done0 = !skip && (!isfinite(res) || res <= tol * denom);
+    __syncthreads();  // every thread has read sc before CTA 0 writes it
+    if (writer) {
+      if (skip) {
+        sc[NYS_CG_DONE] = 5.0;
+        sc[NYS_CG_ITERS] = 0.0;
+        sc[NYS_CG_RUNNING] = 1.0;
+      } else {
+        sc[NYS_CG_DONE] = 0.0;
+        sc[NYS_CG_ITERS] = 0.0;
+        sc[NYS_CG_RUNNING] = 1.0;
+        sc[NYS_CG_NHVP] = 0.0;
+        cp_stop(sc, res2, tol, 0, a.max_iter > 0 ? a.max_iter : 1);
+        if (sc[NYS_CG_DONE] == 4.0) {
+          sc[NYS_CG_DONE] = 0.0;
+          sc[NYS_CG_RUNNING] = 1.0;
+        }
+      }
+    }
+    if (skip || done0) return;
+  }
+  if (tid == 0) {
+    for (int q = 0; q < a.S; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t slice = ((n + nctas - 1) / nctas + 1) & ~1ll;
+  const int64_t c0 = (int64_t)cta * slice, c1 = tmin<int64_t>(n, c0 + slice);
+  const int64_t nrows_mine = a.rows > cta ? (a.rows - cta + nctas - 1) / nctas : 0;
+  const unsigned rbytes = (unsigned)n * 8u;
+  int64_t g0 = 0;  // rows consumed so far by this CTA (mbarrier phase bookkeeping)
+
+  // fixed-order sum over the CTAs of slot q of part (nctas x 8), in every thread
+  auto all_sum = [&](int q) -> double {
+    __syncthreads();
+    if (warp == 0) {
+      double t = 0.0;
+      for (int c = lane; c < nctas; c += 32) t += a.part[c * 8 + q];
+      t = warp_sum(t);
+      if (lane == 0) s_bcast = t;
+    }
+    __syncthreads();
+    return s_bcast;
+  };
+  // y = A^T (d o A v) for this CTA's rows into ypart[cta]; v in registers.
+  // Returns sum_rows d_i (a_i . v)^2 of this CTA's rows (valid in thread 0).
+  auto hvp_rows = [&](double2 (&vr)[K]) -> double {
+    double2 yr[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) yr[k] = make_double2(0.0, 0.0);
+    double vav = 0.0;
+    if (tid == 0)
+      for (int64_t q = 0; q < a.S && q < nrows_mine; ++q) {
+        const int st = (int)((g0 + q) % a.S);
+        const int64_t i = cta + q * nctas;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[st], rbytes);
+        tma_load_1d(ring + (size_t)st * a.W, a.A + i * a.lda, rbytes, &full[st]);
+      }
+    for (int64_t it = 0; it < nrows_mine; ++it) {
+      const int64_t g = g0 + it;
+      const int st = (int)(g % a.S);
+      const int64_t i = cta + it * nctas;
+      const double di = a.d ? __ldg(a.d + i) : 1.0;
+      const double* row = ring + (size_t)st * a.W;
+      mbar_wait(&full[st], (unsigned)((g / a.S) & 1));
+      double pt = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int j = 2 * (tid + k * kCpThreads);
+        if (j < n) {
+          const double2 v2 = *reinterpret_cast<const double2*>(row + j);
+          pt = fma(v2.x, vr[k].x, pt);
+          pt = fma(v2.y, vr[k].y, pt);
+        }
+      }
+      pt = warp_sum(pt);
+      if (lane == 0) red[(it & 1) * 16 + warp] = pt;
+      __syncthreads();
+      const double tot = warp_sum(lane < kCpWarps ? red[(it & 1) * 16 + lane] : 0.0);
+      const double t = a.d ? di * tot : tot;
+      if (tid == 0) vav = fma(t, tot, vav);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int j = 2 * (tid + k * kCpThreads);
+        if (j < n) {
+          const double2 v2 = *reinterpret_cast<const double2*>(row + j);
+          yr[k].x = fma(t, v2.x, yr[k].x);
+          yr[k].y = fma(t, v2.y, yr[k].y);
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && it + a.S < nrows_mine) {
+        const int64_t inext = cta + (it + a.S) * nctas;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[st], rbytes);
+        tma_load_1d(ring + (size_t)st * a.W, a.A + inext * a.lda, rbytes, &full[st]);
+      }
+    }
+    g0 += nrows_mine;
+    double* yp = a.ypart + (int64_t)cta * n;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = 2 * (tid + k * kCpThreads);
+      if (j < n) *reinterpret_cast<double2*>(yp + j) = yr[k];
+    }
+    return vav;
+  };
+  // out[c] = fixed-order sum over q < cnt of P[q * ld + col0 + c], c < ncols, by
+  // all threads: G groups with independent loads in flight, combined in a
+  // fixed order through the (idle) ring.  Valid in every thread after the call.
+  auto colsum = [&](const double* P, int64_t ld, int cnt, int64_t col0, int ncols, double* out) {
+    double* scr = ring;
+    const int G = ncols > 0 ? tmax(1, tmin(16, kCpThreads / ncols)) : 1;
+    __syncthreads();
+    if (tid < G * ncols) {
+      const int col = tid % ncols, g = tid / ncols;
+      const double* pc = P + col0 + col;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int q = g;
+      for (; q + 3 * G < cnt; q += 4 * G) {
+        s0 += pc[(int64_t)q * ld];
+        s1 += pc[(int64_t)(q + G) * ld];
+        s2 += pc[(int64_t)(q + 2 * G) * ld];
+        s3 += pc[(int64_t)(q + 3 * G) * ld];
+      }
+      for (; q < cnt; q += G) s0 += pc[(int64_t)q * ld];
+      scr[g * ncols + col] = (s0 + s1) + (s2 + s3);
+    }
+    __syncthreads();
+    for (int col = tid; col < ncols; col += kCpThreads) {
+      double t = 0.0;
+      for (int g = 0; g < G; ++g) t += scr[g * ncols + col];
+      out[col] = t;
+    }
+    __syncthreads();
+  };
+  // this CTA's share of h = U^T w over its slice -> hpart[cta]
+  auto utw_slice = [&](const double* w) {
+    double acc[MC];
+#pragma unroll
+    for (int cc = 0; cc < MC; ++cc) acc[cc] = 0.0;
+    for (int64_t i = c0 + warp; i < c1; i += kCpWarps) {
+      const double wi = w[i];
+      const double* ui = a.U + i * a.ldu;
+#pragma unroll
+      for (int cc = 0; cc < MC; ++cc) {
+        const int j = lane + 32 * cc;
+        if (j < a.r) acc[cc] = fma(ui[j], wi, acc[cc]);
+      }
+    }
+    double* ws = ring;  // warps in a fixed order (no TMA in flight here)
+    __syncthreads();
+#pragma unroll
+    for (int cc = 0; cc < MC; ++cc) {
+      const int j = lane + 32 * cc;
+      if (j < a.r) ws[warp * a.r + j] = acc[cc];
+    }
+    __syncthreads();
+    for (int j = tid; j < a.r; j += kCpThreads) {
+      double h = 0.0;
+      for (int w2 = 0; w2 < kCpWarps; ++w2) h += ws[w2 * a.r + j];
+      a.hpart[(int64_t)cta * a.r + j] = h;
+    }
+  };
+  // every CTA: coef_j = (lam_{r-1}+nu)(h_j/(lam_j+nu)) - h_j into shared memory
+  auto make_coef = [&]() {
+    const double lr = a.lam[a.r - 1] + a.nu;
+    colsum(a.hpart, a.r, nctas, 0, a.r, csh);
+    for (int j = tid; j < a.r; j += kCpThreads) {
+      const double h = csh[j];
+      const double head = __dmul_rn(lr, h / __dadd_rn(a.lam[j], a.nu));
+      csh[j] = __dadd_rn(head, -h);
+    }
+    __syncthreads();
+  };
+  // z (slice) = U coef + w (Eq. (11) second pass, coef in shared memory);
+  // returns the w.z partial of the slice (every thread)
+  auto apply_slice = [&](const double* w) -> double {
+    double acc = 0.0;
+    if (a.r > 0) {
+      for (int64_t i = c0 + warp; i < c1; i += kCpWarps) {
+        const double* ui = a.U + i * a.ldu;
+        double s2 = 0.0;
+        for (int j = lane; j < a.r; j += 32) s2 = fma(ui[j], csh[j], s2);
+        s2 = warp_sum(s2);
+        if (lane == 0) {
+          const double zi = __dadd_rn(s2, w[i]);
+          a.z[i] = zi;
+          acc = fma(w[i], zi, acc);
+        }
+      }
+    } else {
+      for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
+        a.z[i] = w[i];
+        acc = fma(w[i], w[i], acc);
+      }
+    }
+    return cp_block_sum(acc, sh);
+  };
+
+  // ------------------------------------------- first preconditioning ----
+  if (a.r > 0) {
+    utw_slice(a.res);
+    grid.sync();
+    make_coef();
+  }
+  {
+    const double rz = apply_slice(a.res);
+    if (tid == 0) a.part[cta * 8 + 0] = rz;
+  }
+  grid.sync();
+  double rz = all_sum(0);
+  if (writer) {
+    sc[NYS_CG_RZNEW] = rz;
+    sc[NYS_CG_RZ] = rz;
+  }
+  double beta = 0.0;  // first direction: p = z
+  int pb = 0;         // p buffer holding the current direction
+  for (int64_t k = 1;; ++k) {
+    // ------------------------------------------------------------ HVP ----
+    double vv = 0.0;
+    {
+      double2 vr[K];
+      const double* pold = a.p[pb ^ 1];
+      double* pnew = a.p[pb];
+      double pp = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const int j = 2 * (tid + kk * kCpThreads);
+        if (j < n) {
+          const double2 zz = *reinterpret_cast<const double2*>(a.z + j);
+          double2 v = zz;
+          if (k > 1) {
+            const double2 po = *reinterpret_cast<const double2*>(pold + j);
+            v.x = __dadd_rn(zz.x, __dmul_rn(beta, po.x));
+            v.y = __dadd_rn(zz.y, __dmul_rn(beta, po.y));
+          }
+          vr[kk] = v;
+          pp = fma(v.x, v.x, fma(v.y, v.y, pp));
+          if (j >= c0 && j < c1) *reinterpret_cast<double2*>(pnew + j) = v;
+        } else {
+          vr[kk] = make_double2(0.0, 0.0);
+        }
+      }
+      vv = cp_block_sum(pp, sh);  // ||p||^2, identical in every CTA
+      const double vav = hvp_rows(vr);
+      if (tid == 0) a.part[cta * 8 + 1] = vav;
+    }
+    grid.sync();
+    // --------------------------------------------------- alpha + STEP ----
+    // p.Ap = sum_i d_i (a_i.p)^2 + shift ||p||^2  (fixed order, every CTA)
+    const double pap = fma(a.shift, vv, all_sum(1));
+    if (!isfinite(pap) || pap <= 0.0) {  // krylov.py:74-77
+      if (writer) {
+        sc[NYS_CG_PAP] = pap;
+        sc[NYS_CG_FLAG] = !isfinite(pap) ? 1.0 : 2.0;
+        sc[NYS_CG_DONE] = !isfinite(pap) ? 2.0 : 3.0;
+        sc[NYS_CG_ITERS] = (double)k;
+        sc[NYS_CG_RUNNING] = 0.0;
+      }
+      break;
+    }
+    const double alpha = rz / pap;
+    const bool refresh = (k % 50) == 0;  // krylov.py:16
+    const double* pc = a.p[pb];
+    double rr;
+    if (!refresh) {
+      colsum(a.ypart, n, nctas, c0, (int)(c1 - c0), ys);
+      double acc = 0.0;
+      for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
+        const double api = fma(a.shift, pc[i], ys[i - c0]);
+        a.Ap[i] = api;
+        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, pc[i]));
+        const double ri = __dadd_rn(a.res[i], -__dmul_rn(alpha, api));
+        a.res[i] = ri;
+        acc = fma(ri, ri, acc);
+      }
+      rr = cp_block_sum(acc, sh);
+    } else {
+      // x only, then r = b - A x (true residual refresh, krylov.py:80-81)
+      for (int64_t i = c0 + tid; i < c1; i += kCpThreads) a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, pc[i]));
+      grid.sync();
+      double2 vr[K];
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const int j = 2 * (tid + kk * kCpThreads);
+        vr[kk] = j < n ? *reinterpret_cast<const double2*>(a.x + j) : make_double2(0.0, 0.0);
+      }
+      hvp_rows(vr);
+      grid.sync();
+      colsum(a.ypart, n, nctas, c0, (int)(c1 - c0), ys);
+      double acc = 0.0;
+      for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
+        const double axi = fma(a.shift, a.x[i], ys[i - c0]);
+        a.Ap[i] = axi;
+        const double ri = __dadd_rn(a.b[i], -axi);
+        a.res[i] = ri;
+        acc = fma(ri, ri, acc);
+      }
+      rr = cp_block_sum(acc, sh);
+    }
+    if (a.r > 0) utw_slice(a.res);
+    if (tid == 0) a.part[cta * 8 + 2] = rr;
+    grid.sync();
+    // ------------------------------------------------ stop test + APPLY --
+    {
+      const double rtot = all_sum(2);
+      const double b2 = sc[NYS_CG_B2];
+      const double denom = b2 > 0.0 ? sqrt(b2) : 1.0;
+      const double res = sqrt(rtot);
+      const bool stop = !isfinite(res) || res <= tol * denom || k >= a.max_iter;
+      if (writer) {
+        sc[NYS_CG_PAP] = pap;
+        sc[NYS_CG_ALPHA] = alpha;
+        sc[NYS_CG_NHVP] = (double)(k + k / 50);
+        cp_stop(sc, rtot, tol, k, a.max_iter);
+      }
+      if (stop) break;
+    }
+    if (a.r > 0) make_coef();
+    {
+      const double rzp = apply_slice(a.res);
+      if (tid == 0) a.part[cta * 8 + 3] = rzp;
+    }
+    grid.sync();
+    const double rz_new = all_sum(3);
+    beta = rz_new / rz;  // krylov.py:89-93
+    rz = rz_new;
+    if (writer) {
+      sc[NYS_CG_RZNEW] = rz_new;
+      sc[NYS_CG_RZ] = rz_new;
+      sc[NYS_CG_BETA] = beta;
+    }
+    pb ^= 1;
+  }
+}
+
+struct CpPlan {
+  int K, MC, W, S;
+  size_t smem;
+  bool ok;
+};
+
+static CpPlan cp_plan(const nys_cg_problem* pb) {
+  CpPlan p{};
+  p.ok = false;
+  static const bool off = getenv("NYS_CG_PERSIST_OFF") != nullptr;
+  if (off || pb->op_kind != 0 || pb->rows < kNumSMs || (pb->n & 1) || (pb->lda & 1) ||
+      ((uintptr_t)pb->A & 15) || pb->r > 512)
+    return p;
+  p.W = (int)pb->n;
+  p.K = (int)cdiv(pb->n, (int64_t)2 * kCpThreads);
+  if (p.K > kCpMaxK) return p;
+  p.MC = pb->r <= 128 ? 4 : (pb->r <= 256 ? 8 : 16);
+  const size_t row_bytes = (size_t)p.W * 8;
+  const size_t extra = 64 * 8 + (size_t)(520 + 112) * 8 + 1024;  // red, sh, csh (r <= 512), slice sums
+  p.S = (int)tmin<int64_t>(4, (kCpSmemBudget - extra) / row_bytes);
+  if (p.S < 2) return p;
+  // the U^T r warp partials reuse the ring: 16 x r doubles must fit
+  if ((size_t)kCpWarps * pb->r * 8 > (size_t)p.S * row_bytes) return p;
+  p.smem = (size_t)p.S * row_bytes + (size_t)p.S * 8 + extra;
+  p.ok = true;
+  return p;
+}
+
+template <int K, int MC>
+static int cp_launch(const CpPlan& pl, const CgPersistArgs& args, cudaStream_t st) {
+  static bool attr = false;
+  auto fn = cg_persist_kernel<K, MC>;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kCpSmemBudget);
+    attr = true;
+  }
+  CgPersistArgs a = args;
+  void* kargs[] = {(void*)&a};
+  const unsigned grid = (unsigned)tmin<int64_t>(kNumSMs, a.rows);
+  if (cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kCpThreads), kargs, pl.smem, st) != cudaSuccess)
+    return NYS_ERR_CUDA;
+  __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
+  return debug_sync_check(__FILE__, __LINE__) ? NYS_ERR_CUDA : NYS_OK;
+}
+
+size_t cg_persist_ws(int64_t n, int r) {
+  return (size_t)kNumSMs * n * sizeof(double) + (size_t)kNumSMs * (r + 1) * sizeof(double) +
+         (size_t)kNumSMs * 8 * sizeof(double) + (size_t)(r + 1) * sizeof(double) + 2 * (size_t)n * sizeof(double) +
+         1024;
+}
+
+// The whole solve in one launch when the problem fits the plan; returns
+// NYS_ERR_UNSUPPORTED otherwise (the caller then runs the batched kernels).
+// ws: cg_persist_ws(n, r) bytes, zero-filled once (tickets).
+int cg_persist(const nys_cg_problem* pb, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const CpPlan pl = cp_plan(pb);
+  if (!pl.ok) return NYS_ERR_UNSUPPORTED;
+  if (ws_bytes < cg_persist_ws(pb->n, pb->r)) return NYS_ERR_WORKSPACE;
+  CgPersistArgs a{};
+  a.A = pb->A;
+  a.rows = pb->rows;
+  a.n = pb->n;
+  a.lda = pb->lda;
+  a.d = pb->d;
+  a.shift = pb->shift;
+  a.U = pb->U;
+  a.r = pb->r > 0 ? pb->r : 0;
+  a.ldu = pb->ldu;
+  a.lam = pb->lam;
+  a.nu = pb->nu;
+  a.b = pb->b;
+  a.x = pb->x;
+  a.res = pb->res;
+  a.z = pb->z;
+  a.Ap = pb->Ap;
+  a.sc = pb->sc;
+  a.tol = pb->tol;
+  a.tolp = pb->tol_dev;
+  a.gate = pb->gate;
+  a.max_iter = pb->max_iter;
+  char* base = reinterpret_cast<char*>(ws);
+  a.counter = reinterpret_cast<unsigned int*>(base);
+  size_t off = 256;
+  a.ypart = reinterpret_cast<double*>(base + off);
+  off += (size_t)kNumSMs * pb->n * sizeof(double);
+  a.hpart = reinterpret_cast<double*>(base + off);
+  off += (size_t)kNumSMs * (pb->r + 1) * sizeof(double);
+  a.part = reinterpret_cast<double*>(base + off);
+  off += (size_t)kNumSMs * 8 * sizeof(double);
+  a.coef = reinterpret_cast<double*>(base + off);
+  off += (size_t)(pb->r + 1) * sizeof(double);
+  off = (off + 15) & ~size_t(15);
+  a.p[0] = pb->p;
+  a.p[1] = reinterpret_cast<double*>(base + off);  // second direction buffer
+  a.W = pl.W;
+  a.S = pl.S;
+#define NYS_CP(k)                                                    \
+  case k:                                                            \
+    if (pl.MC == 4) return cp_launch<k, 4>(pl, a, st);               \
+    if (pl.MC == 8) return cp_launch<k, 8>(pl, a, st);               \
+    return cp_launch<k, 16>(pl, a, st);
+  switch (pl.K) {
+    NYS_CP(1) NYS_CP(2) NYS_CP(3) NYS_CP(4) NYS_CP(5) NYS_CP(6) NYS_CP(7) NYS_CP(8) NYS_CP(9) NYS_CP(10)
+    NYS_CP(11) NYS_CP(12) NYS_CP(13)
+    default: return NYS_ERR_UNSUPPORTED;
+  }
+#undef NYS_CP
+}
+
+}  // namespace nys

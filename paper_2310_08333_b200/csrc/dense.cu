@@ -204,9 +204,44 @@ struct GemmPlan {
   size_t ws = 0;
 };
 
-// cost model in seconds: padded tensor work per SM over the busiest SM, plus
-// split-K partial traffic (write + read) and one extra launch
-static GemmPlan gemm_plan(int64_t M, int64_t N, int64_t K, size_t ws_cap) {
+// CTAs per SM of one instantiation (registers and shared memory), cached
+template <bool TA, bool TB, int BM, int BN>
+static int gemm_occ_k() {
+  using S = GemmCfg<TA, TB, BM, BN>;
+  static int occ = 0;
+  if (occ == 0) {
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB, BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dgemm_kernel<TA, TB, BM, BN>, GTHREADS, S::BYTES) !=
+            cudaSuccess ||
+        nb < 1)
+      nb = 1;
+    occ = nb;
+  }
+  return occ;
+}
+template <bool TA, bool TB>
+static int gemm_occ_t(int shape) {
+  switch (shape) {
+    case 0: return gemm_occ_k<TA, TB, 128, 64>();
+    case 1: return gemm_occ_k<TA, TB, 128, 48>();
+    case 2: return gemm_occ_k<TA, TB, 64, 64>();
+    case 3: return gemm_occ_k<TA, TB, 64, 48>();
+    default: return gemm_occ_k<TA, TB, 64, 32>();
+  }
+}
+static int gemm_occ(int ta, int tb, int shape) {
+  if (ta && tb) return gemm_occ_t<true, true>(shape);
+  if (ta) return gemm_occ_t<true, false>(shape);
+  if (tb) return gemm_occ_t<false, true>(shape);
+  return gemm_occ_t<false, false>(shape);
+}
+
+// Cost model in seconds.  An SM runs O = occupancy CTAs at once and shares
+// its tensor throughput among them, so a wave of O CTAs costs O times one
+// CTA's padded work; waves = ceil(CTAs / (148 O)).  Split-K adds the partial
+// traffic (write + read) and one reduction launch.
+static GemmPlan gemm_plan(int ta, int tb, int64_t M, int64_t N, int64_t K, size_t ws_cap) {
   const char* force = getenv("NYS_GEMM_SHAPE");
   const int only = force ? atoi(force) : -1;
   GemmPlan best;
@@ -215,6 +250,7 @@ static GemmPlan gemm_plan(int64_t M, int64_t N, int64_t K, size_t ws_cap) {
   for (int c = 0; c < kNumShapes; ++c) {
     if (only >= 0 && c != only) continue;
     const TileShape& t = kShapes[c];
+    const int occ = gemm_occ(ta, tb, c);
     const int64_t tiles = cdiv(M, t.bm) * cdiv(N, t.bn);
     const int64_t max_sp = tmax<int64_t>(1, tmin<int64_t>(64, cdiv(K, 4 * GBK)));
     for (int64_t sp = 1; sp <= max_sp; ++sp) {
@@ -224,9 +260,11 @@ static GemmPlan gemm_plan(int64_t M, int64_t N, int64_t K, size_t ws_cap) {
       const size_t ws = sp > 1 ? (size_t)sp * M * N * sizeof(double) : 0;
       if (ws > ws_cap) break;
       const int64_t ctas = tiles * sp;
-      const int64_t per_sm = cdiv(ctas, kNumSMs);
+      const int64_t waves = cdiv(ctas, (int64_t)kNumSMs * occ);
+      // concurrent CTAs per SM in a wave (a single partial wave runs fewer)
+      const int64_t conc = waves > 1 ? occ : tmax<int64_t>(1, cdiv(ctas, (int64_t)kNumSMs));
       // pipeline fill: ~2 k-tiles of latency per CTA
-      const double work = (double)per_sm * t.bm * t.bn * (double)(kps + 2 * GBK);
+      const double work = (double)waves * conc * t.bm * t.bn * (double)(kps + 2 * GBK);
       double tt = work / (sm_rate * t.eff);
       if (sp > 1) tt += 2.0 * (double)ws / 6.0e12 + 3.0e-6;
       if (tt < best_t * 0.999) {
@@ -239,10 +277,20 @@ static GemmPlan gemm_plan(int64_t M, int64_t N, int64_t K, size_t ws_cap) {
     }
   }
   if (best.kps == 0) best.kps = K;
+  static const bool dbg = getenv("NYS_GEMM_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr, "[nys] gemm %d%d %lldx%lldx%lld: shape %d (%dx%d, occ %d) splits %d kps %lld est %.1f us\n", ta, tb,
+            (long long)M, (long long)N, (long long)K, best.shape, kShapes[best.shape].bm, kShapes[best.shape].bn,
+            gemm_occ(ta, tb, best.shape), best.splits, (long long)best.kps, best_t * 1e6);
   return best;
 }
 
-size_t gemm_ws(int64_t M, int64_t N, int64_t K) { return gemm_plan(M, N, K, (size_t)-1).ws; }
+size_t gemm_ws(int64_t M, int64_t N, int64_t K) {
+  size_t w = 0;
+  for (int ta = 0; ta < 2; ++ta)
+    for (int tb = 0; tb < 2; ++tb) w = tmax(w, gemm_plan(ta, tb, M, N, K, (size_t)-1).ws);
+  return w;
+}
 
 template <bool TA, bool TB, int BM, int BN>
 static int gemm_launch_shape(const GemmPlan& pl, int64_t M, int64_t N, int64_t K, double alpha,
@@ -272,7 +320,7 @@ template <bool TA, bool TB>
 static int gemm_launch(int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                        int64_t lda, const double* B, int64_t ldb, double beta, double* C,
                        int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const GemmPlan pl = gemm_plan(M, N, K, ws ? ws_bytes : 0);
+  const GemmPlan pl = gemm_plan(TA ? 1 : 0, TB ? 1 : 0, M, N, K, ws ? ws_bytes : 0);
   switch (pl.shape) {
     case 0: return gemm_launch_shape<TA, TB, 128, 64>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
     case 1: return gemm_launch_shape<TA, TB, 128, 48>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);

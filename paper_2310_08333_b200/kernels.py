@@ -9,6 +9,7 @@ keeps the drop-in boundary in one place.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional
 
 import torch
@@ -152,7 +153,9 @@ class Kernels:
         rows, n = (A.shape[0], A.shape[1])
         r = 0 if U is None else U.shape[1]
         s_op, s_pc = C.c_size_t(0), C.c_size_t(0)
-        red_b = self.L.nys_cg_workspace(op_kind, rows, n, r, C.byref(s_op), C.byref(s_pc))
+        # the preconditioner workspaces are sized for the largest supported rank so
+        # that a descriptor built earlier never points at a reallocated buffer
+        red_b = self.L.nys_cg_workspace(op_kind, rows, n, max(r, 512), C.byref(s_op), C.byref(s_pc))
         w_op = self.workspace("hvp" if op_kind == 0 else "densemv", s_op.value)
         w_pc = self.workspace("prec", s_pc.value)
         w_red = self.workspace("cgred", red_b)
@@ -163,6 +166,9 @@ class Kernels:
             Ap=work.Ap.data_ptr(), sc=work.sc.data_ptr(), tol=float(tol), max_iter=int(max_iter),
             ws_op=w_op.data_ptr(), ws_op_bytes=w_op.numel(), ws_pc=w_pc.data_ptr(), ws_pc_bytes=w_pc.numel(),
             ws_red=w_red.data_ptr())
+        if op_kind == 0 and os.environ.get("NYS_CG_PERSIST", "1") != "0":
+            w_cp = self.workspace("cgpersist", self.L.nys_cg_persist_workspace(n, 512))
+            pb.ws_cp, pb.ws_cp_bytes = w_cp.data_ptr(), w_cp.numel()
         return pb
 
     # CUDA-event timing of the operator launches inside the batched CG driver
@@ -170,9 +176,9 @@ class Kernels:
         self.L.nys_timing_enable(1 if on else 0)
         self._lib_timing = bool(on)
 
-    def timing_commit(self, tag: int, last_real_k: int) -> None:
+    def timing_commit(self, tag: int, last_real_k: int, units: int = 0) -> None:
         if getattr(self, "_lib_timing", False):
-            check(self.L.nys_timing_commit(int(tag), int(last_real_k)), "timing_commit")
+            check(self.L.nys_timing_commit(int(tag), int(last_real_k), int(units)), "timing_commit")
 
     def timing_read(self):
         tot, cnt = C.c_double(0.0), C.c_int64(0)
