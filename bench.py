@@ -229,9 +229,11 @@ def run_ours(args):
     value = iters / (el_ms / 1e3)
     tts = el_ms / 1e3 / args.steps
 
-    # one extra, instrumented solve: the HVP launches inside the batched CG
-    # driver are bracketed by CUDA events on the solve's stream (predicated
-    # no-op launches excluded); its own duration gives the kernel's share
+    # one extra, instrumented solve: every x-update PCG launch is bracketed by
+    # CUDA events on the solve's stream.  With the persistent solver
+    # (csrc/cg_persist.cu) one launch is a whole CG solve and counts its
+    # operator applications; otherwise each HVP launch is bracketed alone
+    # (predicated no-op launches excluded).  Its duration gives the share.
     kx.timing_enable(True)
     barrier()
     i0 = torch.cuda.Event(enable_timing=True)
@@ -244,28 +246,54 @@ def run_ours(args):
     k_total_ms, k_count = kx.timing_read()
     kx.timing_enable(False)
 
-    # roofline of the dominant kernel (HVP, K3): algorithmic bytes per launch
+    # roofline of the dominant kernel: algorithmic bytes per operator application
+    # (8 N n + 8 (2n + N)) x applications / measured time
     n = host_A.shape[1]
+    rows_loc = d.A.shape[0] // world if d.kind != "boxqp" else n
+    alg_bytes = 8 * rows_loc * n + 8 * (2 * n + rows_loc)
     peak, peak_kind = _peaks()
+    persistent = os.environ.get("NYS_CG_PERSIST", "1") != "0" and d.kind != "boxqp" and n <= 13312
+    kname = "cg_persist_kernel" if persistent else "hvp"
     roof = None
+    traffic_db = {}
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic_db = json.load(open(tf))
+        except Exception:
+            traffic_db = {}
     if k_count:
         avg_ms = k_total_ms / k_count
-        ktimes = [avg_ms] * k_count
-        rows_loc = d.A.shape[0] // world if d.kind != "boxqp" else n
-        alg_bytes = 8 * rows_loc * n + 8 * (2 * n + rows_loc)
         achieved = alg_bytes / (avg_ms / 1e3) / 1e9
-        traffic = None
-        tf = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tf):
-            try:
-                traffic = json.load(open(tf)).get(f"cfg{args.config}_{args.profile_kernel}")
-            except Exception:
-                traffic = None
-        roof = {"bound": "hbm", "kernel": args.profile_kernel, "achieved": achieved, "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "launches_timed": len(ktimes),
-                "share_of_step": sum(ktimes) / inst_ms,
-                "timing": "CUDA events around each HVP launch of one extra instrumented solve (not the timed steps)"}
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic_db.get(f"cfg{args.config}_{kname}"),
+                "alg_bytes_per_unit": alg_bytes, "unit_of_work": "one Hessian application (HVP) of the PCG, "
+                "incl. the CG vector phases when the persistent solver runs", "ms_per_unit": avg_ms,
+                "units_timed": k_count, "share_of_step": k_total_ms / inst_ms,
+                "timing": "CUDA events around every PCG launch of one extra instrumented solve (not the timed steps)"}
+    # the HVP kernel alone (K3, csrc/hvp.cu), back to back on the same A and row weights
+    hvp_alone = None
+    if d.kind != "boxqp" and world == 1:
+        v = torch.randn(n, dtype=torch.float64, device=A_dev.device)
+        y = torch.empty_like(v)
+        dw = torch.rand(A_dev.shape[0], dtype=torch.float64, device=A_dev.device)
+        pap = torch.zeros(1, dtype=torch.float64, device=A_dev.device)
+        for _ in range(3):
+            kx.hvp(A_dev, dw, v, 1.0, y, pap, True)
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        reps = 20
+        h0.record(st)
+        for _ in range(reps):
+            kx.hvp(A_dev, dw, v, 1.0, y, pap, True)
+        h1.record(st)
+        torch.cuda.synchronize()
+        hms = h0.elapsed_time(h1) / reps
+        ha = alg_bytes / (hms / 1e3) / 1e9
+        hvp_alone = {"kernel": "hvp_row_kernel", "achieved": ha, "peak": peak, "unit": "GB/s", "frac": ha / peak,
+                     "ms_per_launch": hms, "traffic": traffic_db.get(f"cfg{args.config}_hvp"),
+                     "timing": f"CUDA events around {reps} back-to-back launches"}
 
     # e2e: public API with host buffers (pinned), upload + readback inside each step
     e2e = None
@@ -306,7 +334,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(config_block(args, d, world), time_to_tolerance_s=tts, iterations=res.iterations,
                            status=res.status.value, objective=res.objective, sketches=res.device_stats.get("sketches")),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "hvp_alone": hvp_alone, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -321,7 +349,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--profile-kernel", default="hvp", choices=["hvp", "gemv", "gemvT"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
