@@ -106,6 +106,9 @@ typedef struct nys_cg_problem {
 } nys_cg_problem;
 
 /* ---------------------------------------------------------------- misc -- */
+/* dst[i] = src[i] by a kernel; dst may be device-mapped pinned host memory
+ * (the per-iteration readback of the ADMM pipeline) */
+int nys_copy_f64(const double* src, double* dst, int64_t n, void* stream);
 int nys_abi_version(void);
 const char* nys_status_string(int status);
 /* NYS_OK when a compute-capability-10.x device is current */
@@ -249,6 +252,11 @@ typedef struct nys_admm_head {
   void* ws_red;
 } nys_admm_head;
 int nys_admm_head_f64(const nys_admm_head* h, void* stream);
+/* The x-update of admm.py:243-275: head + PCG.  One persistent cooperative
+ * kernel (head fused into its prologue) when pb->ws_cp is set and the dense ML
+ * problem fits its plan; otherwise nys_admm_head_f64 and `count` batched CG
+ * iterations (nys_cg_iterate_f64, k_first = 1). */
+int nys_admm_xupdate_f64(const nys_admm_head* h, const nys_cg_problem* pb, int count, void* stream);
 
 /* ---------------------------------------------- K8/K9 ADMM elementwise -- */
 /* x-update right-hand side and initial CG residual, M = I, c = 0

@@ -90,7 +90,9 @@ class AdmmHead(C.Structure):
 SIGNATURES = {
     "nys_admm_tail_f64": (I32, [C.POINTER(AdmmTail), P]),
     "nys_admm_head_f64": (I32, [C.POINTER(AdmmHead), P]),
+    "nys_admm_xupdate_f64": (I32, [C.POINTER(AdmmHead), C.POINTER(CgProblem), I32, P]),
     "nys_abi_version": (I32, []),
+    "nys_copy_f64": (I32, [P, P, I64, P]),
     "nys_status_string": (C.c_char_p, [I32]),
     "nys_device_check": (I32, []),
     "nys_launch_count": (C.c_ulonglong, []),

@@ -774,6 +774,10 @@ class _Engine:
         kx, L, n = self.kx, self.kx.L, self.n
         self.rbs = kx.zeros(2, _RB_LEN)
         self.rbs_host = [_host_buffer(_RB_LEN, kx.device) for _ in range(2)]
+        # pinned host memory is device-addressable under UVA: a kernel writes the
+        # readback block straight into it (no copy engine in the pipeline)
+        self._kernel_readback = (hasattr(kx, "copy_to_pinned") and kx.device.type == "cuda"
+                                 and os.environ.get("NYS_KERNEL_READBACK", "1") != "0")
         self.gates = kx.zeros(2)
         self.gates[1] = 1.0  # iteration 1 (parity 1) may run
         self.tols = kx.zeros(2)
@@ -902,9 +906,8 @@ class _Engine:
             t.inf_first, t.inf_last = after[0], after[-1]
         batch = min(16, max(2, self._last_cg + 1))
         ev = self._ev[par]
-        kx.admm_head(h)
         ev[0].record(kx.stream)
-        kx.cg_iterate(pb, 1, batch)
+        kx.admm_xupdate(h, pb, batch)  # head + PCG (one persistent kernel when it fits)
         ev[1].record(kx.stream)
         kx.admm_tail(t)
         ev[2].record(kx.stream)
@@ -922,7 +925,10 @@ class _Engine:
         return h[8:8 + C], np.concatenate([h[8 + C:], h[:8]])
 
     def _readback(self, par):
-        self.rbs_host[par].copy_(self.rbs[par], non_blocking=True)
+        if self._kernel_readback:
+            self.kx.copy_to_pinned(self.rbs[par], self.rbs_host[par])
+        else:
+            self.rbs_host[par].copy_(self.rbs[par], non_blocking=True)
         self.kx.d2h += _RB_LEN * 8
         self._done_ev[par].record(self.kx.stream)
 

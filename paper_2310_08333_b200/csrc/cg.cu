@@ -33,7 +33,7 @@ double* precond_coef(void* ws);
 double* precond_hpart(void* ws, int r);
 
 size_t cg_persist_ws(int64_t n, int r);
-int cg_persist(const nys_cg_problem* pb, void* ws, size_t ws_bytes, cudaStream_t st);
+int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, size_t ws_bytes, cudaStream_t st);
 
 constexpr int kCgThreads = 256;
 constexpr int kCgMaxBlocks = kNumSMs * 4;
@@ -393,6 +393,38 @@ extern "C" int nys_timing_read(double* total_ms, int64_t* launches) {
 
 extern "C" size_t nys_cg_persist_workspace(int64_t n, int r) { return cg_persist_ws(n, r < 0 ? 0 : r); }
 
+extern "C" int nys_admm_head_f64(const nys_admm_head* h, void* stream);
+
+// head + PCG of one ADMM x-update: one persistent kernel when the problem fits
+// its plan, else nys_admm_head_f64 followed by `count` batched CG iterations
+extern "C" int nys_admm_xupdate_f64(const nys_admm_head* h, const nys_cg_problem* pb, int count, void* stream) {
+  if (!h || !pb) return NYS_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  if (pb->ws_cp && pb->op_kind == 0) {
+    TimedLaunch tl{pb->timing_tag, 0, nullptr, nullptr};
+    if (g_timing) {
+      tl.a = pool_get();
+      tl.b = pool_get();
+      cudaEventRecord(tl.a, st);
+    }
+    const int rc = cg_persist(pb, h, pb->ws_cp, pb->ws_cp_bytes, st);
+    if (rc != NYS_ERR_UNSUPPORTED) {
+      if (g_timing) {
+        cudaEventRecord(tl.b, st);
+        g_pending.push_back(tl);
+      }
+      return rc;
+    }
+    if (g_timing) {
+      g_pool.push_back(tl.a);
+      g_pool.push_back(tl.b);
+    }
+  }
+  int rc = nys_admm_head_f64(h, stream);
+  if (rc) return rc;
+  return nys_cg_iterate_f64(pb, 1, count, stream);
+}
+
 extern "C" size_t nys_cg_workspace(int op_kind, int64_t rows, int64_t n, int r, size_t* ws_op, size_t* ws_pc) {
   *ws_op = op_kind == 0 ? hvp_ws(rows, n) : dense_mv_ws(n);
   *ws_pc = nys_precond_workspace(n, r);
@@ -416,7 +448,7 @@ extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int
       tl.b = pool_get();
       cudaEventRecord(tl.a, st);
     }
-    rc = cg_persist(pb, pb->ws_cp, pb->ws_cp_bytes, st);
+    rc = cg_persist(pb, nullptr, pb->ws_cp, pb->ws_cp_bytes, st);
     if (rc != NYS_ERR_UNSUPPORTED) {
       if (g_timing) {
         cudaEventRecord(tl.b, st);

@@ -59,6 +59,8 @@ struct CgPersistArgs {
   double* coef;    // r
   unsigned int* counter;
   int W, S;
+  int has_head;       // run the ADMM head (nys_admm_head) as the prologue
+  nys_admm_head h;
 };
 
 __device__ __forceinline__ double cp_tol(const CgPersistArgs& a) { return a.tolp ? *a.tolp : a.tol; }
@@ -109,34 +111,75 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   const int64_t n = a.n;
   double* sc = a.sc;
   const bool writer = cta == 0 && tid == 0;  // the one thread that publishes sc
+  const int64_t slice = ((n + nctas - 1) / nctas + 1) & ~1ll;
+  const int64_t c0 = (int64_t)cta * slice, c1 = tmin<int64_t>(n, c0 + slice);
   // ---------------------------------------------------------- begin ----
   // every CTA evaluates the begin logic itself (same inputs, same result)
-  const double tol = cp_tol(a);
-  {
-    const bool skip = a.gate && *a.gate == 0.0;  // previous ADMM iteration unfinished
-    const double b2 = sc[NYS_CG_B2], res2 = sc[NYS_CG_RES2];
-    const double denom = b2 > 0.0 ? sqrt(b2) : 1.0;
-    const double res = sqrt(res2);
-    const bool done0 = !skip && (!isfinite(res) || res <= tol * denom);
-    __syncthreads();  // every thread has read sc before CTA 0 writes it
-    if (writer) {
-      if (skip) {
+  double tol, b2, res2;
+  if (a.has_head) {
+    // ADMM head (nys_admm_head_f64) on this CTA's slice: gate, device CG
+    // tolerance, snapshot, rhs and r0 = rhs - H x0, ||rhs||^2, ||r0||^2
+    const nys_admm_head& h = a.h;
+    if (h.gate && *h.gate == 0.0) {  // previous ADMM iteration unfinished
+      if (writer) {
         sc[NYS_CG_DONE] = 5.0;
         sc[NYS_CG_ITERS] = 0.0;
         sc[NYS_CG_RUNNING] = 1.0;
-      } else {
-        sc[NYS_CG_DONE] = 0.0;
+      }
+      return;
+    }
+    if (h.tol_fixed > 0.0) {
+      tol = h.tol_fixed;
+    } else {  // krylov.py:98-112 from the residual norms of the previous iteration
+      const double* q = h.prev;
+      const double rp = h.norm_kind ? q[1] : sqrt(fmax(q[0], 0.0));
+      const double rd = h.norm_kind ? q[3] : sqrt(fmax(q[2], 0.0));
+      tol = fmax(fmin(sqrt(rp * rd), 1.0) / h.kpow, 1e-12);
+    }
+    if (writer) {
+      if (h.gate_next) *h.gate_next = 0.0;
+      if (h.tol_out) *h.tol_out = tol;
+    }
+    double sb = 0.0, sr = 0.0;
+    for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
+      const double xi = h.x[i], zi = h.z[i], ui = h.u[i];
+      if (h.snap) {
+        h.snap[i] = xi;
+        h.snap[n + i] = zi;
+        h.snap[2 * n + i] = ui;
+        h.snap[3 * n + i] = h.xbar[i];
+        h.snap[4 * n + i] = h.zbar[i];
+      }
+      const double l2x = __dmul_rn(h.lambda2, xi);
+      const double hx = __dadd_rn(h.hxA[i], l2x);
+      double g = __dadd_rn(h.gA[i], l2x);
+      if (h.q) g = __dadd_rn(g, h.q[i]);
+      double bb = __dadd_rn(__dadd_rn(hx, __dmul_rn(h.sigma, xi)), -g);
+      bb = __dadd_rn(bb, __dmul_rn(h.rho, __dadd_rn(zi, -ui)));
+      const double ri = __dadd_rn(bb, -__dadd_rn(hx, __dmul_rn(h.shift, xi)));
+      h.rhs[i] = bb;
+      h.r[i] = ri;
+      sb = fma(bb, bb, sb);
+      sr = fma(ri, ri, sr);
+    }
+    sb = cp_block_sum(sb, sh);
+    sr = cp_block_sum(sr, sh);
+    if (tid == 0) {
+      a.part[cta * 8 + 4] = sb;
+      a.part[cta * 8 + 5] = sr;
+    }
+  } else {
+    if (a.gate && *a.gate == 0.0) {
+      if (writer) {
+        sc[NYS_CG_DONE] = 5.0;
         sc[NYS_CG_ITERS] = 0.0;
         sc[NYS_CG_RUNNING] = 1.0;
-        sc[NYS_CG_NHVP] = 0.0;
-        cp_stop(sc, res2, tol, 0, a.max_iter > 0 ? a.max_iter : 1);
-        if (sc[NYS_CG_DONE] == 4.0) {
-          sc[NYS_CG_DONE] = 0.0;
-          sc[NYS_CG_RUNNING] = 1.0;
-        }
       }
+      return;
     }
-    if (skip || done0) return;
+    tol = cp_tol(a);
+    b2 = sc[NYS_CG_B2];
+    res2 = sc[NYS_CG_RES2];
   }
   if (tid == 0) {
     for (int q = 0; q < a.S; ++q) mbar_init(&full[q], 1);
@@ -144,8 +187,6 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   }
   __syncthreads();
 
-  const int64_t slice = ((n + nctas - 1) / nctas + 1) & ~1ll;
-  const int64_t c0 = (int64_t)cta * slice, c1 = tmin<int64_t>(n, c0 + slice);
   const int64_t nrows_mine = a.rows > cta ? (a.rows - cta + nctas - 1) / nctas : 0;
   const unsigned rbytes = (unsigned)n * 8u;
   int64_t g0 = 0;  // rows consumed so far by this CTA (mbarrier phase bookkeeping)
@@ -319,12 +360,39 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     return cp_block_sum(acc, sh);
   };
 
-  // ------------------------------------------- first preconditioning ----
+  // ------------------------------- begin + first preconditioning ----
+  // (the head's r0 slice and the U^T r0 partials come from the same phase)
   if (a.r > 0) {
+    __syncthreads();
     utw_slice(a.res);
-    grid.sync();
-    make_coef();
   }
+  if (a.has_head || a.r > 0) grid.sync();
+  if (a.has_head) {
+    b2 = all_sum(4);
+    res2 = all_sum(5);
+  }
+  {
+    const double denom = b2 > 0.0 ? sqrt(b2) : 1.0;
+    const double res = sqrt(res2);
+    const bool done0 = !isfinite(res) || res <= tol * denom;
+    if (writer) {
+      if (a.has_head) {
+        sc[NYS_CG_B2] = b2;
+        sc[NYS_CG_RES2] = res2;
+      }
+      sc[NYS_CG_DONE] = 0.0;
+      sc[NYS_CG_ITERS] = 0.0;
+      sc[NYS_CG_RUNNING] = 1.0;
+      sc[NYS_CG_NHVP] = 0.0;
+      cp_stop(sc, res2, tol, 0, a.max_iter > 0 ? a.max_iter : 1);
+      if (sc[NYS_CG_DONE] == 4.0) {
+        sc[NYS_CG_DONE] = 0.0;
+        sc[NYS_CG_RUNNING] = 1.0;
+      }
+    }
+    if (done0) return;
+  }
+  if (a.r > 0) make_coef();
   {
     const double rz = apply_slice(a.res);
     if (tid == 0) a.part[cta * 8 + 0] = rz;
@@ -426,7 +494,6 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     // ------------------------------------------------ stop test + APPLY --
     {
       const double rtot = all_sum(2);
-      const double b2 = sc[NYS_CG_B2];
       const double denom = b2 > 0.0 ? sqrt(b2) : 1.0;
       const double res = sqrt(rtot);
       const bool stop = !isfinite(res) || res <= tol * denom || k >= a.max_iter;
@@ -510,7 +577,7 @@ size_t cg_persist_ws(int64_t n, int r) {
 // The whole solve in one launch when the problem fits the plan; returns
 // NYS_ERR_UNSUPPORTED otherwise (the caller then runs the batched kernels).
 // ws: cg_persist_ws(n, r) bytes, zero-filled once (tickets).
-int cg_persist(const nys_cg_problem* pb, void* ws, size_t ws_bytes, cudaStream_t st) {
+int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, size_t ws_bytes, cudaStream_t st) {
   const CpPlan pl = cp_plan(pb);
   if (!pl.ok) return NYS_ERR_UNSUPPORTED;
   if (ws_bytes < cg_persist_ws(pb->n, pb->r)) return NYS_ERR_WORKSPACE;
@@ -552,6 +619,8 @@ int cg_persist(const nys_cg_problem* pb, void* ws, size_t ws_bytes, cudaStream_t
   a.p[1] = reinterpret_cast<double*>(base + off);  // second direction buffer
   a.W = pl.W;
   a.S = pl.S;
+  a.has_head = head != nullptr;
+  if (head) a.h = *head;
 #define NYS_CP(k)                                                    \
   case k:                                                            \
     if (pl.MC == 4) return cp_launch<k, 4>(pl, a, st);               \

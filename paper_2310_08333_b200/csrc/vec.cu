@@ -798,6 +798,23 @@ extern "C" int nys_admm_rhs_f64(int64_t n, const double* hxA, const double* gA, 
   return NYS_OK;
 }
 
+// small copy by a kernel (dst may be mapped pinned host memory): the per-
+// iteration readback goes out with the stream's kernels instead of through a
+// copy engine (no copy-engine round trip between two kernels of the pipeline)
+__global__ void copy_small_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  __threadfence_system();
+}
+
+extern "C" int nys_copy_f64(const double* src, double* dst, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return NYS_ERR_ARG;
+  if (n == 0) return NYS_OK;
+  copy_small_kernel<<<(unsigned)tmin<int64_t>(cdiv(n, 256), 64), 256, 0, as_stream(stream)>>>(src, dst, n);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
 extern "C" int nys_admm_head_f64(const nys_admm_head* h, void* stream) {
   if (!h || h->n <= 0 || !h->rhs || !h->r || !h->sc || !h->ws_red) return NYS_ERR_ARG;
   if (h->snap && (!h->xbar || !h->zbar)) return NYS_ERR_ARG;

@@ -189,9 +189,18 @@ class Kernels:
         self.launches += 1
         check(self.L.nys_admm_tail_f64(C.byref(t), self.sp), "admm_tail")
 
+    def copy_to_pinned(self, src: torch.Tensor, dst: torch.Tensor) -> None:
+        """Kernel copy of a small device vector into pinned host memory."""
+        self.launches += 1
+        check(self.L.nys_copy_f64(src.data_ptr(), dst.data_ptr(), src.numel(), self.sp), "copy")
+
     def admm_head(self, h) -> None:
         self.launches += 1
         check(self.L.nys_admm_head_f64(C.byref(h), self.sp), "admm_head")
+
+    def admm_xupdate(self, h, pb, count: int) -> None:
+        self.launches += 1
+        check(self.L.nys_admm_xupdate_f64(C.byref(h), C.byref(pb), int(count), self.sp), "admm_xupdate")
 
     def cg_iterate(self, pb, k_first: int, count: int) -> None:
         self.launches += 1
