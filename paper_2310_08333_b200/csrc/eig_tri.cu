@@ -21,16 +21,18 @@ constexpr int kTriMaxS = 160;
 constexpr int kTriThreads = 512;
 
 // --------------------------------------------------------------- K_a ------
-// Householder reduction with A in shared memory, five barriers per column:
-//   1 ||x(2:)||^2 partials        (every thread then forms beta/tau itself)
-//   2 v (scaled column) -> smem
-//   3 symv partials: thread (g, j) sums rows g, g+RG, ... of column j of A22
+// Householder reduction with A in shared memory, four barriers per column:
+//   1 v (scaled column) -> smem (||x(2:)||^2 comes from the previous update)
+//   2 symv partials: thread (g, j) sums rows g, g+RG, ... of column j of A22
 //     (columns are contiguous in smem: no bank conflicts, no warp reductions)
-//   4 p_j = tau sum_g partial(g, j) and the p.v partials
-//   5 rank-2 update A22 -= v w^T + w v^T with w = p - (tau/2)(p.v) v formed on
-//     the fly.  The reflectors are stored row-wise (VhT[k][*]) for the
-//     coalesced back-transformation.
+//   3 p_j = tau sum_g partial(g, j) and the p.v partials
+//   4 rank-2 update A22 -= v w^T + w v^T with w = p - (tau/2)(p.v) v: each
+//     thread keeps v_j, w_j of its columns in registers and walks its rows;
+//     the updated column k+1 squares feed the next column's norm.
+// The reflectors are stored row-wise (VhT[k][*]) for the coalesced
+// back-transformation.
 constexpr int kTriRG = 8;  // max row groups of the symv
+constexpr int kTriCols = (kTriMaxS + 31) / 32;
 __global__ void __launch_bounds__(kTriThreads)
 tridiag_kernel(int s, const double* __restrict__ A, double* __restrict__ d, double* __restrict__ e,
                double* __restrict__ VhT, double* __restrict__ tau) {
@@ -40,22 +42,25 @@ tridiag_kernel(int s, const double* __restrict__ A, double* __restrict__ d, doub
   double* vs = a + (size_t)s * ld;        // s
   double* pw = vs + s;                    // s
   double* part = pw + s;                  // kTriRG x s
-  double* red = part + (size_t)kTriRG * s;  // 64
+  double* red = part + (size_t)kTriRG * s;  // 2 x 64
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int t = tid; t < s * s; t += blockDim.x) {
     const int i = t / s, j = t - i * s;
     a[i * ld + j] = A[t];
   }
   __syncthreads();
-  for (int k = 0; k + 2 < s; ++k) {
-    const int m = s - k - 1;  // size of the trailing block
-    // 1. ||x(2:)||^2 of x = a[k+1:, k]
+  {  // ||x(2:)||^2 of column 0
     double pt = 0.0;
-    for (int i = k + 2 + tid; i < s; i += blockDim.x) pt = fma(a[i * ld + k], a[i * ld + k], pt);
+    for (int i = 2 + tid; i < s; i += blockDim.x) pt = fma(a[i * ld], a[i * ld], pt);
     pt = warp_sum(pt);
     if (lane == 0) red[warp] = pt;
-    __syncthreads();
-    const double xn2 = warp_sum(lane < nw ? red[lane] : 0.0);
+    for (int q = nw + tid; q < 32; q += blockDim.x) red[q] = 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k + 2 < s; ++k) {
+    const int m = s - k - 1;  // size of the trailing block
+    double* rn = red + (k & 1) * 64;  // norm partials of this column (written by the previous update)
+    const double xn2 = warp_sum(rn[lane]);
     const double alpha = a[(k + 1) * ld + k];
     double tk, beta, scal;
     if (xn2 == 0.0) {
@@ -71,34 +76,45 @@ tridiag_kernel(int s, const double* __restrict__ A, double* __restrict__ d, doub
       tau[k] = tk;
       e[k] = beta;
     }
-    // 2. reflector v (v_0 = 1)
+    // 1. reflector v (v_0 = 1)
     for (int i = tid; i < m; i += blockDim.x) {
       const double vi = (i == 0) ? 1.0 : a[(k + 1 + i) * ld + k] * scal;
       vs[i] = vi;
       VhT[(size_t)k * s + (k + 1 + i)] = vi;
     }
+    double* rnext = red + ((k + 1) & 1) * 64;
+    if (tk == 0.0) {  // H = I: no update; the next column's norm directly (uniform branch)
+      double pt = 0.0;
+      for (int i = k + 3 + tid; i < s; i += blockDim.x) pt = fma(a[i * ld + k + 1], a[i * ld + k + 1], pt);
+      pt = warp_sum(pt);
+      if (lane == 0) rnext[warp] = pt;
+      for (int q = nw + tid; q < 32; q += blockDim.x) rnext[q] = 0.0;
+      __syncthreads();
+      continue;
+    }
     __syncthreads();
-    if (tk == 0.0) continue;  // x(2:) == 0: H = I, nothing to update (uniform)
-    // 3. symv partials over row groups
+    // 2. symv partials over row groups
     const int colsP = (m + 31) & ~31;
     const int RG = min(kTriRG, (int)blockDim.x / colsP);
     {
       const int g = tid / colsP, j = tid - g * colsP;
       if (g < RG && j < m) {
         const double* col = a + (size_t)(k + 1) * ld + (k + 1) + j;
-        double acc0 = 0.0, acc1 = 0.0;
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
         int i = g;
-        for (; i + RG < m; i += 2 * RG) {
+        for (; i + 3 * RG < m; i += 4 * RG) {
           acc0 = fma(col[(size_t)i * ld], vs[i], acc0);
           acc1 = fma(col[(size_t)(i + RG) * ld], vs[i + RG], acc1);
+          acc2 = fma(col[(size_t)(i + 2 * RG) * ld], vs[i + 2 * RG], acc2);
+          acc3 = fma(col[(size_t)(i + 3 * RG) * ld], vs[i + 3 * RG], acc3);
         }
-        if (i < m) acc0 = fma(col[(size_t)i * ld], vs[i], acc0);
-        part[g * s + j] = acc0 + acc1;
+        for (; i < m; i += RG) acc0 = fma(col[(size_t)i * ld], vs[i], acc0);
+        part[g * s + j] = (acc0 + acc1) + (acc2 + acc3);
       }
     }
     __syncthreads();
-    // 4. p = tau A22 v and the p.v partials
-    pt = 0.0;
+    // 3. p = tau A22 v and the p.v partials
+    double pt = 0.0;
     for (int j = tid; j < m; j += blockDim.x) {
       double pj = 0.0;
       for (int g = 0; g < RG; ++g) pj += part[g * s + j];
@@ -107,19 +123,35 @@ tridiag_kernel(int s, const double* __restrict__ A, double* __restrict__ d, doub
       pt = fma(pj, vs[j], pt);
     }
     pt = warp_sum(pt);
-    if (lane == 0) red[32 + warp] = pt;
+    if (lane == 0) red[128 + warp] = pt;
     __syncthreads();
-    const double pv = warp_sum(lane < nw ? red[32 + lane] : 0.0);
+    const double pv = warp_sum(lane < nw ? red[128 + lane] : 0.0);
     const double hpv = 0.5 * tk * pv;
-    // 5. A22 -= v w^T + w v^T,  w = p - hpv v
+    // 4. A22 -= v w^T + w v^T,  w = p - hpv v (v_j, w_j of this lane in registers)
+    double vj[kTriCols], wj[kTriCols];
+#pragma unroll
+    for (int c = 0; c < kTriCols; ++c) {
+      const int j = lane + 32 * c;
+      vj[c] = j < m ? vs[j] : 0.0;
+      wj[c] = j < m ? fma(-hpv, vj[c], pw[j]) : 0.0;
+    }
+    double nrm = 0.0;  // squares of the updated column k+1 below row k+2
     for (int i = warp; i < m; i += nw) {
       double* ar = a + (k + 1 + i) * ld + (k + 1);
       const double vi = vs[i], wi = fma(-hpv, vi, pw[i]);
-      for (int j = lane; j < m; j += 32) {
-        const double vj = vs[j], wj = fma(-hpv, vj, pw[j]);
-        ar[j] -= fma(vi, wj, wi * vj);
+#pragma unroll
+      for (int c = 0; c < kTriCols; ++c) {
+        const int j = lane + 32 * c;
+        if (j < m) {
+          const double t = ar[j] - fma(vi, wj[c], wi * vj[c]);
+          ar[j] = t;
+          if (c == 0 && lane == 0 && i >= 2) nrm = fma(t, t, nrm);
+        }
       }
     }
+    // lane 0 of each warp holds its rows' partial; other lanes hold 0
+    if (lane == 0) rnext[warp] = nrm;
+    for (int q = nw + tid; q < 32; q += blockDim.x) rnext[q] = 0.0;
     __syncthreads();
   }
   for (int i = tid; i < s; i += blockDim.x) d[i] = a[i * ld + i];
@@ -462,7 +494,7 @@ int eig_tri(int s, const double* A, double* V, double* w, void* ws, cudaStream_t
   int* cl = reinterpret_cast<int*>(tau + s + 1);
   int* ncl = cl + s + 2;
   void* gws = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(ncl + 4) + 511) & ~uintptr_t(255));
-  const size_t smem = ((size_t)s * (s | 1) + (2 + kTriRG) * (size_t)s + 64) * sizeof(double);
+  const size_t smem = ((size_t)s * (s | 1) + (2 + kTriRG) * (size_t)s + 192) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
