@@ -39,6 +39,11 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz));
 }
+// 16-byte copy of a pair of doubles; nvalid in {0, 1, 2} (the rest zero-filled)
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int nvalid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(nvalid * 8));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -63,7 +68,8 @@ struct GemmCfg {
   static_assert((BM * GBK) % GTHREADS == 0 && (BN * GBK) % GTHREADS == 0, "loader");
 };
 
-template <bool TA, bool TB, int BM, int BN>
+// VA: op(A) tiles loaded as 16-byte pairs (lda even, A 16-byte aligned)
+template <bool TA, bool TB, int BM, int BN, bool VA>
 __global__ void __launch_bounds__(GTHREADS)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A,
              int64_t lda, const double* __restrict__ B, int64_t ldb, double beta,
@@ -81,6 +87,22 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
   auto load_tile = [&](int stage, int64_t k0) {
     double* As = smem + stage * S::STAGE;
     double* Bs = As + S::A_ELEMS;
+    if (VA) {
+#pragma unroll
+      for (int e2 = tid; e2 < BM * GBK / 2; e2 += GTHREADS) {
+        if (TA) {  // pairs along m
+          const int kk = e2 / (BM / 2), mm = (e2 - kk * (BM / 2)) * 2;
+          const int64_t gm = m0 + mm, gk = k0 + kk;
+          const int nv = gk < ke ? (gm + 1 < M ? 2 : (gm < M ? 1 : 0)) : 0;
+          cp_async16(As + kk * kStrideKmaj(BM) + mm, nv ? A + gk * lda + gm : A, nv);
+        } else {  // pairs along k
+          const int mm = e2 / (GBK / 2), kk = (e2 - mm * (GBK / 2)) * 2;
+          const int64_t gm = m0 + mm, gk = k0 + kk;
+          const int nv = gm < M ? (gk + 1 < ke ? 2 : (gk < ke ? 1 : 0)) : 0;
+          cp_async16(As + mm * kStrideMmaj + kk, nv ? A + gm * lda + gk : A, nv);
+        }
+      }
+    } else
 #pragma unroll
     for (int e = tid; e < BM * GBK; e += GTHREADS) {
       if (TA) {  // consecutive threads along m (contiguous in memory)
@@ -210,9 +232,10 @@ static int gemm_occ_k() {
   using S = GemmCfg<TA, TB, BM, BN>;
   static int occ = 0;
   if (occ == 0) {
-    cudaFuncSetAttribute(dgemm_kernel<TA, TB, BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB, BM, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::BYTES);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dgemm_kernel<TA, TB, BM, BN>, GTHREADS, S::BYTES) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dgemm_kernel<TA, TB, BM, BN, false>, GTHREADS, S::BYTES) !=
             cudaSuccess ||
         nb < 1)
       nb = 1;
@@ -297,16 +320,16 @@ static int gemm_launch_shape(const GemmPlan& pl, int64_t M, int64_t N, int64_t K
                              const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                              double* C, int64_t ldc, void* ws, cudaStream_t st) {
   using S = GemmCfg<TA, TB, BM, BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(dgemm_kernel<TA, TB, BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)S::BYTES);
-    attr_set = true;
+  const bool va = (lda % 2) == 0 && ((uintptr_t)A & 15) == 0;
+  static bool attr_set[2] = {false, false};
+  auto fn = va ? dgemm_kernel<TA, TB, BM, BN, true> : dgemm_kernel<TA, TB, BM, BN, false>;
+  if (!attr_set[va]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    attr_set[va] = true;
   }
   dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM), (unsigned)pl.splits);
   double* P = pl.splits > 1 ? reinterpret_cast<double*>(ws) : nullptr;
-  dgemm_kernel<TA, TB, BM, BN><<<grid, GTHREADS, S::BYTES, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C,
-                                                                 ldc, pl.kps, P);
+  fn<<<grid, GTHREADS, S::BYTES, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pl.kps, P);
   NYS_CHECK_LAUNCH();
   if (pl.splits > 1) {
     const int64_t blocks = tmin<int64_t>(cdiv(M * N, 256), kNumSMs * 8);
