@@ -340,6 +340,17 @@ int nys_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double
  * np.random.PCG64(seed).state.  PCG64 jump-ahead + NumPy's ziggurat with a
  * parallel resolution of the variable draw consumption.  Synchronises `stream`;
  * returns NYS_ERR_NONFINITE if the draw buffer was exhausted (never expected). */
+/* Asynchronous variants for a pipelined sketch: no host synchronisation; a
+ * failure is reported in a device status word instead (nonzero = re-run the
+ * synchronous function): the draw buffer ran short / a Cholesky pivot of a
+ * CholeskyQR pass (2 words) / of the core (1 word).  The sketch's rank is
+ * then min(r, s). */
+int nys_gaussian_async_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                           double* out, int* flag_dev, void* ws, size_t ws_bytes, void* stream);
+int nys_orthonormalize_async_f64(int64_t n, int s, const double* Omega, double* Q, int* info_dev, void* ws,
+                                 size_t ws_bytes, void* stream);
+int nys_nystrom_core_async_f64(int64_t n, int s, int r, const double* Q, double* Y, double* U, double* lam,
+                               int* info_dev, void* ws, size_t ws_bytes, void* stream);
 size_t nys_gaussian_workspace(int64_t count);
 int nys_gaussian_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                      int64_t count, double* out, void* ws, size_t ws_bytes, void* stream);

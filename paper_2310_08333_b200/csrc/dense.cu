@@ -795,7 +795,7 @@ size_t ortho_ws(int64_t n, int s) {
 // numerically singular Gram matrix the careful path (per-pass checks, eigen
 // fallback) recomputes Q from Omega.
 static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* ws,
-                          size_t ws_bytes, cudaStream_t st, bool careful) {
+                          size_t ws_bytes, cudaStream_t st, bool careful, int* info_ext = nullptr) {
   Arena ar{reinterpret_cast<char*>(ws), ws_bytes};
   ar.take<char>(kRedBytesD);
   double* G = ar.take<double>((size_t)s * s);
@@ -811,6 +811,7 @@ static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* w
   const size_t jws_b = syevj_ws(s);
   void* jws = ar.take<char>(jws_b);
   if (!ar.ok) return NYS_ERR_WORKSPACE;
+  if (info_ext) info = info_ext;  // deferred: the caller checks the codes later
   int rc;
   for (int pass = 0; pass < 2; ++pass) {
     const double* src = pass == 0 ? Om : tmp;
@@ -839,6 +840,7 @@ static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* w
     }
     if (rc) return rc;
   }
+  if (info_ext) return NYS_OK;
   if (!careful) {
     int info_h[2] = {0, 0};
     if (cudaMemcpyAsync(info_h, info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -874,7 +876,7 @@ __global__ void nystrom_lam_kernel(int rr, const double* __restrict__ w, const d
 // eigh fallback of sketch.py:114-124 from the same inputs.
 static int nystrom_core(int64_t n, int s, int r, const double* Q, double* Y, double* U,
                         double* lam, int* r_out, void* ws, size_t ws_bytes, cudaStream_t st,
-                        bool careful) {
+                        bool careful, int* info_ext = nullptr) {
   Arena ar{reinterpret_cast<char*>(ws), ws_bytes};
   char* red = ar.take<char>(kRedBytesD);
   double* shift_d = ar.take<double>(4);
@@ -893,6 +895,7 @@ static int nystrom_core(int64_t n, int s, int r, const double* Q, double* Y, dou
   const size_t jws_b = syevj_ws(s);
   void* jws = ar.take<char>(jws_b);
   if (!ar.ok) return NYS_ERR_WORKSPACE;
+  if (info_ext) info = info_ext;  // deferred: the caller checks the code later
   const double eps = 2.220446049250313e-16;
   int rc;
   if (!careful) {
@@ -968,6 +971,10 @@ static int nystrom_core(int64_t n, int s, int r, const double* Q, double* Y, dou
   NYS_CHECK_LAUNCH();
   rc = gemm(0, 0, n, rr, s_eff, 1.0, B, s_eff, Cm, rr, 0.0, U, r, nullptr, 0, st);
   if (rc) return rc;
+  if (info_ext) {
+    *r_out = rr;
+    return NYS_OK;
+  }
   if (!careful) {
     int info_c = 0;
     if (cudaMemcpyAsync(&info_c, info, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -1005,7 +1012,20 @@ extern "C" int nys_orthonormalize_f64(int64_t n, int s, const double* Omega, dou
   return orthonormalize(n, s, Omega, Q, ws, ws_bytes, as_stream(stream), false);
 }
 
+extern "C" int nys_orthonormalize_async_f64(int64_t n, int s, const double* Omega, double* Q, int* info_dev,
+                                            void* ws, size_t ws_bytes, void* stream) {
+  if (n <= 0 || s <= 0 || s > n || !info_dev) return NYS_ERR_ARG;
+  return orthonormalize(n, s, Omega, Q, ws, ws_bytes, as_stream(stream), false, info_dev);
+}
+
 extern "C" size_t nys_nystrom_workspace(int64_t n, int s, int r) { return nystrom_ws(n, s, r); }
+
+extern "C" int nys_nystrom_core_async_f64(int64_t n, int s, int r, const double* Q, double* Y, double* U,
+                                          double* lam, int* info_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (n <= 0 || s <= 0 || s > n || r < 1 || r > s || !info_dev) return NYS_ERR_ARG;
+  int r_out = 0;
+  return nystrom_core(n, s, r, Q, Y, U, lam, &r_out, ws, ws_bytes, as_stream(stream), false, info_dev);
+}
 
 extern "C" int nys_nystrom_core_f64(int64_t n, int s, int r, const double* Q, double* Y, double* U,
                                     double* lam, int* r_out, void* ws, size_t ws_bytes,

@@ -317,13 +317,32 @@ using namespace nys;
 
 extern "C" size_t nys_gaussian_workspace(int64_t count) { return gauss_plan(count).bytes; }
 
+// flag = 1 when the draw buffer held fewer than `count` accepted normals
+__global__ void gauss_flag_kernel(const int64_t* total, int64_t count, int* flag) {
+  if (threadIdx.x == 0 && *total < count) *flag = 1;
+}
+
+static int gaussian_impl(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                         double* out, int* flag_dev, void* ws, size_t ws_bytes, cudaStream_t st);
+
+extern "C" int nys_gaussian_async_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                                      int64_t count, double* out, int* flag_dev, void* ws, size_t ws_bytes,
+                                      void* stream) {
+  if (count <= 0 || !flag_dev) return NYS_ERR_ARG;
+  return gaussian_impl(state_hi, state_lo, inc_hi, inc_lo, count, out, flag_dev, ws, ws_bytes, as_stream(stream));
+}
+
 extern "C" int nys_gaussian_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                                 uint64_t inc_lo, int64_t count, double* out, void* ws,
                                 size_t ws_bytes, void* stream) {
   if (count <= 0) return NYS_ERR_ARG;
+  return gaussian_impl(state_hi, state_lo, inc_hi, inc_lo, count, out, nullptr, ws, ws_bytes, as_stream(stream));
+}
+
+static int gaussian_impl(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
+                         double* out, int* flag_dev, void* ws, size_t ws_bytes, cudaStream_t st) {
   const GaussPlan p = gauss_plan(count);
   if (ws_bytes < p.bytes) return NYS_ERR_WORKSPACE;
-  cudaStream_t st = as_stream(stream);
   char* w = reinterpret_cast<char*>(ws);
   uint64_t* raw = reinterpret_cast<uint64_t*>(w + p.off_raw);
   double* V = reinterpret_cast<double*>(w + p.off_V);
@@ -352,6 +371,11 @@ extern "C" int nys_gaussian_f64(uint64_t state_hi, uint64_t state_lo, uint64_t i
   NYS_CHECK_LAUNCH();
   tile_write_kernel<<<(unsigned)p.ntiles, kChunksPerTile, 0, st>>>(L, V, p.Q, cx, cc, te, tb, count, out);
   NYS_CHECK_LAUNCH();
+  if (flag_dev) {  // deferred check (the caller reads the flag with its next sync)
+    gauss_flag_kernel<<<1, 32, 0, st>>>(total, count, flag_dev);
+    NYS_CHECK_LAUNCH();
+    return NYS_OK;
+  }
   int64_t tot = 0;
   if (cudaMemcpyAsync(&tot, total, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) return NYS_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;

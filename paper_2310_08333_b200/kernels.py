@@ -320,6 +320,37 @@ class Kernels:
                                           C.byref(rr), ws.data_ptr(), ws.numel(), self.sp), "nystrom")
         return int(rr.value)
 
+    # asynchronous sketch stages: failures land in device status words
+    def gaussian_async(self, seed: int, out: torch.Tensor, flag: torch.Tensor) -> None:
+        import numpy as np
+
+        st = np.random.PCG64(seed).state["state"]
+        s, inc = int(st["state"]), int(st["inc"])
+        m64 = (1 << 64) - 1
+        count = out.numel()
+        ws = self.workspace("gauss", self.L.nys_gaussian_workspace(count))
+        self.launches += 1
+        check(self.L.nys_gaussian_async_f64(s >> 64, s & m64, inc >> 64, inc & m64, count, out.data_ptr(),
+                                            flag.data_ptr(), ws.data_ptr(), ws.numel(), self.sp), "gaussian")
+
+    def sketch_workspace(self, n: int, s: int, r: int) -> torch.Tensor:
+        return self.workspace("sketch", max(self.L.nys_nystrom_workspace(n, s, r),
+                                            self.L.nys_orthonormalize_workspace(n, s)))
+
+    def orthonormalize_async(self, Om, Q, info: torch.Tensor, r: int) -> None:
+        n, s = Om.shape
+        ws = self.sketch_workspace(n, s, r)
+        self.launches += 1
+        check(self.L.nys_orthonormalize_async_f64(n, s, Om.data_ptr(), Q.data_ptr(), info.data_ptr(), ws.data_ptr(),
+                                                  ws.numel(), self.sp), "orthonormalize")
+
+    def nystrom_core_async(self, Q, Y, U, lam, r, info: torch.Tensor) -> None:
+        n, s = Q.shape
+        ws = self.sketch_workspace(n, s, r)
+        self.launches += 1
+        check(self.L.nys_nystrom_core_async_f64(n, s, r, Q.data_ptr(), Y.data_ptr(), U.data_ptr(), lam.data_ptr(),
+                                                info.data_ptr(), ws.data_ptr(), ws.numel(), self.sp), "nystrom")
+
     def syevj(self, A, V, w) -> None:
         s = A.shape[0]
         ws = self.workspace("syevj", self.L.nys_syevj_workspace(s))

@@ -67,6 +67,22 @@ def sketch_device(kx, apply_cols: Callable[[torch.Tensor], torch.Tensor], n: int
             kx.sync()
             t.append(time.perf_counter())
 
+    if omega is None and not trace and hasattr(kx, "gaussian_async") and reduce is None:
+        # pipelined: no host synchronisation inside the sketch, one status read
+        # at the end; a flagged failure (draw buffer short, singular Gram or core
+        # pivot) re-runs the synchronous path from the same seed
+        flags = torch.zeros(4, dtype=torch.int32, device=kx.device)
+        Om = kx.empty(n, s)
+        kx.gaussian_async(seed, Om, flags[0:1])
+        Q = kx.empty(n, s)
+        kx.orthonormalize_async(Om, Q, flags[1:3], r)
+        Y = apply_cols(Q).contiguous()
+        U = kx.empty(n, r)
+        lam = kx.empty(r)
+        kx.nystrom_core_async(Q, Y, U, lam, r, flags[3:4])
+        if not bool(flags.any().item()):
+            kx.d2h += 16
+            return U, lam
     if omega is None:
         # the reference's default_rng(seed).standard_normal((n, s)), drawn on the GPU
         Om = kx.empty(n, s)

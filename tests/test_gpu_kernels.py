@@ -305,3 +305,28 @@ def test_gaussian_matches_numpy_stream(kx, seed, count):
     diff = got != ref
     assert diff.sum() <= max(1, count // 100000), diff.sum()
     np.testing.assert_allclose(got, ref, rtol=1e-15, atol=0)
+
+
+@pytest.mark.parametrize("rank", [5, 40])
+def test_sketch_low_rank_operator(rank):
+    """A rank-deficient PSD operator: the core Cholesky may hit a tiny pivot
+    (the pipelined sketch then re-runs the synchronous path with the eigh
+    fallback of sketch.py:114-124); either way the Nystrom approximation of
+    an exactly low-rank operator is exact and the extra eigenvalues vanish."""
+    from paper_2310_08333_b200 import DenseOperator, nystrom_sketch
+
+    g = np.random.default_rng(rank)
+    B = g.standard_normal((200, rank))
+    M = B @ B.T
+    S = nystrom_sketch(DenseOperator(M), 20, rng_seed=rank)
+    A_hat = (S.U * S.lambda_hat) @ S.U.T
+    scale = np.linalg.norm(M, 2)
+    assert np.isfinite(S.lambda_hat).all() and np.isfinite(S.U).all()
+    if rank < 20:
+        top = np.sort(np.linalg.eigvalsh(M))[::-1][:rank]
+        np.testing.assert_allclose(S.lambda_hat[:rank], top, rtol=1e-8, atol=1e-10 * scale)
+        np.testing.assert_allclose(A_hat, M, atol=1e-8 * scale)
+        assert np.all(S.lambda_hat[rank:] <= 1e-9 * scale)
+    else:
+        # A_hat <= M in the Loewner order (test_sketch.py:57-67)
+        assert np.linalg.eigvalsh(M - A_hat).min() >= -1e-8 * scale
