@@ -160,22 +160,48 @@ struct TileMap {
   int cnt[kE];
 };
 
-// K3: chunk maps and their composition into a tile map
+// walk within a shared-memory copy of the tile's consumptions (positions
+// relative to the tile start)
+__device__ __forceinline__ int walk_s(const uint8_t* __restrict__ Ls, int start, int end, int* count) {
+  int q = start, c = 0;
+  while (q < end) {
+    const uint8_t l = Ls[q];
+    if (l == kUnknown) {
+      *count = c;
+      return -1;
+    }
+    ++c;
+    q += l;
+  }
+  *count = c;
+  return q;
+}
+
+// K3: chunk maps and their composition into a tile map (the tile's L staged
+// in shared memory: the walks are dependent load chains)
 __global__ void __launch_bounds__(kChunksPerTile)
 tile_map_kernel(const uint8_t* __restrict__ L, int64_t Q, TileMap* __restrict__ tiles,
                 int* __restrict__ chunk_exit, int* __restrict__ chunk_cnt) {
   __shared__ int ex[kChunksPerTile][kE];
   __shared__ int cn[kChunksPerTile][kE];
+  __shared__ uint8_t Ls[kTile + 256];
   const int64_t tile0 = (int64_t)blockIdx.x * kTile;
+  const int tlen = (int)tmin<int64_t>(kTile, Q - tile0);
+  for (int q = threadIdx.x; q < kTile + 256; q += blockDim.x) Ls[q] = q < tlen ? L[tile0 + q] : kUnknown;
+  __syncthreads();
   const int c = threadIdx.x;
-  const int64_t cs = tile0 + (int64_t)c * kChunk;
-  const int64_t ce = tmin<int64_t>(cs + kChunk, Q);
+  const int cs = c * kChunk;
+  const int ce = tmin(cs + kChunk, tlen);
   for (int e = 0; e < kE; ++e) {
     int cnt = 0;
-    int64_t x = -1;
-    if (cs + e < Q) x = walk(L, cs + e, ce, &cnt);
-    else x = cs + e, cnt = 0;
-    ex[c][e] = x < 0 ? -1 : (int)(x - ce);
+    int x;
+    if (cs + e < tlen) {
+      x = walk_s(Ls, cs + e, ce, &cnt);
+    } else {
+      x = cs + e;
+      cnt = 0;
+    }
+    ex[c][e] = x < 0 ? -1 : x - ce;
     cn[c][e] = cnt;
     chunk_exit[((int64_t)blockIdx.x * kChunksPerTile + c) * kE + e] = ex[c][e];
     chunk_cnt[((int64_t)blockIdx.x * kChunksPerTile + c) * kE + e] = cnt;
@@ -185,17 +211,17 @@ tile_map_kernel(const uint8_t* __restrict__ L, int64_t Q, TileMap* __restrict__ 
     int e = c, total = 0;
     bool bad = false;
     for (int k = 0; k < kChunksPerTile && !bad; ++k) {
-      const int64_t ks = tile0 + (int64_t)k * kChunk;
-      if (ks >= Q) break;
-      const int64_t ke_ = tmin<int64_t>(ks + kChunk, Q);
+      const int ks = k * kChunk;
+      if (ks >= tlen) break;
+      const int ke_ = tmin(ks + kChunk, tlen);
       int nx, nc;
       if (e < kE) {
         nx = ex[k][e];
         nc = cn[k][e];
       } else {
         int cnt = 0;
-        const int64_t x = walk(L, ks + e, ke_, &cnt);
-        nx = x < 0 ? -1 : (int)(x - ke_);
+        const int x = ks + e < kTile + 256 ? walk_s(Ls, ks + e, ke_, &cnt) : -1;
+        nx = x < 0 ? -1 : x - ke_;
         nc = cnt;
       }
       if (nx < 0) bad = true;
@@ -211,6 +237,10 @@ tile_map_kernel(const uint8_t* __restrict__ L, int64_t Q, TileMap* __restrict__ 
 __global__ void tile_resolve_kernel(const TileMap* __restrict__ tiles, const uint8_t* __restrict__ L,
                                     int64_t ntiles, int64_t Q, int* __restrict__ tile_entry,
                                     int64_t* __restrict__ tile_base, int64_t* __restrict__ total) {
+  // stage the tile maps in shared memory (coalesced), then one thread chains them
+  extern __shared__ TileMap tm_s[];
+  for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) tm_s[t] = tiles[t];
+  __syncthreads();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int e = 0;
   int64_t base = 0;
@@ -219,7 +249,7 @@ __global__ void tile_resolve_kernel(const TileMap* __restrict__ tiles, const uin
     tile_base[t] = base;
     if (e < 0) continue;
     if (e < kE) {
-      const TileMap m = tiles[t];
+      const TileMap m = tm_s[t];
       base += m.cnt[e];
       e = m.exit[e];
     } else {
@@ -241,7 +271,14 @@ tile_write_kernel(const uint8_t* __restrict__ L, const double* __restrict__ V, i
                   int64_t count, double* __restrict__ out) {
   __shared__ int entry[kChunksPerTile];
   __shared__ int64_t base[kChunksPerTile];
+  __shared__ int cx_s[kChunksPerTile * kE];
+  __shared__ int cc_s[kChunksPerTile * kE];
   const int64_t tile0 = (int64_t)blockIdx.x * kTile;
+  for (int q = threadIdx.x; q < kChunksPerTile * kE; q += blockDim.x) {
+    cx_s[q] = chunk_exit[(int64_t)blockIdx.x * kChunksPerTile * kE + q];
+    cc_s[q] = chunk_cnt[(int64_t)blockIdx.x * kChunksPerTile * kE + q];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     int e = tile_entry[blockIdx.x];
     int64_t b = tile_base[blockIdx.x];
@@ -255,9 +292,9 @@ tile_write_kernel(const uint8_t* __restrict__ L, const double* __restrict__ V, i
       }
       const int64_t ke_ = tmin<int64_t>(ks + kChunk, Q);
       if (e < kE) {
-        const int64_t ci = ((int64_t)blockIdx.x * kChunksPerTile + k) * kE + e;
-        b += chunk_cnt[ci];
-        e = chunk_exit[ci];
+        const int ci = k * kE + e;
+        b += cc_s[ci];
+        e = cx_s[ci];
       } else {
         int cnt = 0;
         const int64_t x = walk(L, ks + e, ke_, &cnt);
@@ -367,7 +404,12 @@ static int gaussian_impl(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, 
   NYS_CHECK_LAUNCH();
   tile_map_kernel<<<(unsigned)p.ntiles, kChunksPerTile, 0, st>>>(L, p.Q, tiles, cx, cc);
   NYS_CHECK_LAUNCH();
-  tile_resolve_kernel<<<1, 32, 0, st>>>(tiles, L, p.ntiles, p.Q, te, tb, total);
+  const size_t rsm = (size_t)p.ntiles * sizeof(TileMap);
+  if (rsm > 48 * 1024) {
+    if (rsm > 220 * 1024) return NYS_ERR_UNSUPPORTED;
+    cudaFuncSetAttribute(tile_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+  }
+  tile_resolve_kernel<<<1, 256, rsm, st>>>(tiles, L, p.ntiles, p.Q, te, tb, total);
   NYS_CHECK_LAUNCH();
   tile_write_kernel<<<(unsigned)p.ntiles, kChunksPerTile, 0, st>>>(L, V, p.Q, cx, cc, te, tb, count, out);
   NYS_CHECK_LAUNCH();
