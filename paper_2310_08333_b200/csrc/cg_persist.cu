@@ -30,7 +30,7 @@ namespace nys {
 constexpr int kCpThreads = 512;
 constexpr int kCpWarps = kCpThreads / 32;
 constexpr int kCpMaxK = 13;            // n <= 13312
-constexpr int kCpSmemBudget = 200 * 1024;
+constexpr int kCpSmemBudget = 226 * 1024;  // sm_100 per-block maximum less the static shared words
 
 struct CgPersistArgs {
   const double* A;
@@ -60,6 +60,7 @@ struct CgPersistArgs {
   unsigned int* counter;
   int W, S;
   int has_head;       // run the ADMM head (nys_admm_head) as the prologue
+  int u_smem;         // stage this CTA's rows of U in shared memory
   nys_admm_head h;
 };
 
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   double* sh = red + 32;                                                     // 32
   double* csh = sh + 32;                                                     // coef (r <= 512)
   double* ys = csh + 520;                                                    // slice sums
+  double* us = ys + 112;                                                     // U rows of the slice
   __shared__ double s_bcast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nctas = gridDim.x, cta = blockIdx.x;
@@ -113,6 +115,19 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   const bool writer = cta == 0 && tid == 0;  // the one thread that publishes sc
   const int64_t slice = ((n + nctas - 1) / nctas + 1) & ~1ll;
   const int64_t c0 = (int64_t)cta * slice, c1 = tmin<int64_t>(n, c0 + slice);
+  // the slice's rows of U go to shared memory asynchronously (LDGSTS); both
+  // preconditioner passes read them from there (waited for before the first)
+  const bool ush = a.u_smem && a.r > 0;
+  if (ush) {
+    const int tot = (int)(c1 - c0) * a.r;
+    for (int t = tid; t < tot; t += kCpThreads) {
+      const int ii = t / a.r, j = t - ii * a.r;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(us + t);
+      const double* src = a.U + (c0 + ii) * a.ldu + j;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
   // ---------------------------------------------------------- begin ----
   // every CTA evaluates the begin logic itself (same inputs, same result)
   double tol, b2, res2;
@@ -277,16 +292,14 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     if (tid < G * ncols) {
       const int col = tid % ncols, g = tid / ncols;
       const double* pc = P + col0 + col;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      double sv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // 8 load chains in flight
       int q = g;
-      for (; q + 3 * G < cnt; q += 4 * G) {
-        s0 += pc[(int64_t)q * ld];
-        s1 += pc[(int64_t)(q + G) * ld];
-        s2 += pc[(int64_t)(q + 2 * G) * ld];
-        s3 += pc[(int64_t)(q + 3 * G) * ld];
+      for (; q + 7 * G < cnt; q += 8 * G) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sv[u] += pc[(int64_t)(q + u * G) * ld];
       }
-      for (; q < cnt; q += G) s0 += pc[(int64_t)q * ld];
-      scr[g * ncols + col] = (s0 + s1) + (s2 + s3);
+      for (; q < cnt; q += G) sv[0] += pc[(int64_t)q * ld];
+      scr[g * ncols + col] = ((sv[0] + sv[1]) + (sv[2] + sv[3])) + ((sv[4] + sv[5]) + (sv[6] + sv[7]));
     }
     __syncthreads();
     for (int col = tid; col < ncols; col += kCpThreads) {
@@ -303,7 +316,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     for (int cc = 0; cc < MC; ++cc) acc[cc] = 0.0;
     for (int64_t i = c0 + warp; i < c1; i += kCpWarps) {
       const double wi = w[i];
-      const double* ui = a.U + i * a.ldu;
+      const double* ui = ush ? us + (i - c0) * a.r : a.U + i * a.ldu;
 #pragma unroll
       for (int cc = 0; cc < MC; ++cc) {
         const int j = lane + 32 * cc;
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     double acc = 0.0;
     if (a.r > 0) {
       for (int64_t i = c0 + warp; i < c1; i += kCpWarps) {
-        const double* ui = a.U + i * a.ldu;
+        const double* ui = ush ? us + (i - c0) * a.r : a.U + i * a.ldu;
         double s2 = 0.0;
         for (int j = lane; j < a.r; j += 32) s2 = fma(ui[j], csh[j], s2);
         s2 = warp_sum(s2);
@@ -362,6 +375,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
 
   // ------------------------------- begin + first preconditioning ----
   // (the head's r0 slice and the U^T r0 partials come from the same phase)
+  if (ush) asm volatile("cp.async.wait_all;\n" ::: "memory");
   if (a.r > 0) {
     __syncthreads();
     utw_slice(a.res);
@@ -524,7 +538,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
 }
 
 struct CpPlan {
-  int K, MC, W, S;
+  int K, MC, W, S, u_smem;
   size_t smem;
   bool ok;
 };
@@ -547,6 +561,10 @@ static CpPlan cp_plan(const nys_cg_problem* pb) {
   // the U^T r warp partials reuse the ring: 16 x r doubles must fit
   if ((size_t)kCpWarps * pb->r * 8 > (size_t)p.S * row_bytes) return p;
   p.smem = (size_t)p.S * row_bytes + (size_t)p.S * 8 + extra;
+  const int64_t slice = ((pb->n + kNumSMs - 1) / kNumSMs + 1) & ~1ll;
+  const size_t ubytes = (size_t)slice * (pb->r > 0 ? pb->r : 0) * 8;
+  p.u_smem = pb->r > 0 && p.smem + ubytes <= (size_t)kCpSmemBudget;
+  if (p.u_smem) p.smem += ubytes;
   p.ok = true;
   return p;
 }
@@ -556,7 +574,10 @@ static int cp_launch(const CpPlan& pl, const CgPersistArgs& args, cudaStream_t s
   static bool attr = false;
   auto fn = cg_persist_kernel<K, MC>;
   if (!attr) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kCpSmemBudget);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kCpSmemBudget) != cudaSuccess) {
+      cudaGetLastError();
+      return NYS_ERR_CUDA;
+    }
     attr = true;
   }
   CgPersistArgs a = args;
@@ -620,6 +641,7 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
   a.W = pl.W;
   a.S = pl.S;
   a.has_head = head != nullptr;
+  a.u_smem = pl.u_smem;
   if (head) a.h = *head;
 #define NYS_CP(k)                                                    \
   case k:                                                            \
