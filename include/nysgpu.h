@@ -109,6 +109,10 @@ typedef struct nys_cg_problem {
 /* dst[i] = src[i] by a kernel; dst may be device-mapped pinned host memory
  * (the per-iteration readback of the ADMM pipeline) */
 int nys_copy_f64(const double* src, double* dst, int64_t n, void* stream);
+/* nys_copy_f64 of a per-iteration readback block that also opens the next
+ * iteration's gate (*gate_next = 1) unless *pred != 0 (pred may be NULL). */
+int nys_readback_f64(const double* src, double* dst, int64_t n, double* gate_next, const double* pred,
+                     void* stream);
 int nys_abi_version(void);
 const char* nys_status_string(int status);
 /* NYS_OK when a compute-capability-10.x device is current */
@@ -227,6 +231,9 @@ typedef struct nys_admm_tail {
   double* conj_out;           /* NULL, or (ML, with_z, lambda2 == 0) the scaled-dual conjugate
                                  sums of problems.py:330-340 with c = lambda1 / max|atnu|,
                                  computed when max|atnu| > lambda1 (3 values)           */
+  int zu_done;                /* set by nys_admm_xupdate_f64 when its persistent kernel
+                                 already ran the relax/prox/dual update and the window
+                                 append of this descriptor; the tail then skips them   */
 } nys_admm_tail;
 int nys_admm_tail_f64(const nys_admm_tail* t, void* stream);
 
@@ -250,6 +257,11 @@ typedef struct nys_admm_head {
   const double* gate; double* gate_next;
   const double* prev; int norm_kind; double kpow; double tol_fixed; double* tol_out;
   void* ws_red;
+  nys_admm_tail* zu;          /* NULL, or the iteration's tail descriptor: when the
+                                 persistent kernel runs, it ends with the tail's z/u
+                                 update and window append on each CTA's slice of x
+                                 (admm.py:562-583, 622-623) and sets zu->zu_done = 1
+                                 (0 otherwise)                                         */
 } nys_admm_head;
 int nys_admm_head_f64(const nys_admm_head* h, void* stream);
 /* The x-update of admm.py:243-275: head + PCG.  One persistent cooperative

@@ -71,7 +71,7 @@ class AdmmTail(C.Structure):
         ("qp_infeas", C.c_int), ("inf_first", C.c_int), ("inf_last", C.c_int), ("width", F64),
         ("dx", P), ("Pdx", P), ("infeas", P), ("pdx2", P),
         ("ws_gemv", P), ("ws_gemv_bytes", SZ), ("ws_gemvT", P), ("ws_gemvT_bytes", SZ), ("ws_red", P),
-        ("pred", P), ("gate_next", P), ("conj_out", P),
+        ("pred", P), ("gate_next", P), ("conj_out", P), ("zu_done", C.c_int),
     ]
 
 
@@ -82,7 +82,7 @@ class AdmmHead(C.Structure):
         ("n", I64), ("hxA", P), ("gA", P), ("q", P), ("lambda2", F64), ("sigma", F64), ("rho", F64),
         ("shift", F64), ("x", P), ("z", P), ("u", P), ("xbar", P), ("zbar", P), ("rhs", P), ("r", P),
         ("sc", P), ("snap", P), ("gate", P), ("gate_next", P), ("prev", P), ("norm_kind", C.c_int),
-        ("kpow", F64), ("tol_fixed", F64), ("tol_out", P), ("ws_red", P),
+        ("kpow", F64), ("tol_fixed", F64), ("tol_out", P), ("ws_red", P), ("zu", P),
     ]
 
 
@@ -93,6 +93,7 @@ SIGNATURES = {
     "nys_admm_xupdate_f64": (I32, [C.POINTER(AdmmHead), C.POINTER(CgProblem), I32, P]),
     "nys_abi_version": (I32, []),
     "nys_copy_f64": (I32, [P, P, I64, P]),
+    "nys_readback_f64": (I32, [P, P, I64, P, P, P]),
     "nys_status_string": (C.c_char_p, [I32]),
     "nys_device_check": (I32, []),
     "nys_launch_count": (C.c_ulonglong, []),

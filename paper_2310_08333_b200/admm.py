@@ -28,6 +28,7 @@ buffer, HVP partials are all-reduced inside CG, the sketch Y is all-reduced.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import os
 import time
@@ -776,7 +777,7 @@ class _Engine:
         self.rbs_host = [_host_buffer(_RB_LEN, kx.device) for _ in range(2)]
         # pinned host memory is device-addressable under UVA: a kernel writes the
         # readback block straight into it (no copy engine in the pipeline)
-        self._kernel_readback = (hasattr(kx, "copy_to_pinned") and kx.device.type == "cuda"
+        self._kernel_readback = (hasattr(kx, "readback") and kx.device.type == "cuda"
                                  and os.environ.get("NYS_KERNEL_READBACK", "1") != "0")
         self.gates = kx.zeros(2)
         self.gates[1] = 1.0  # iteration 1 (parity 1) may run
@@ -804,7 +805,9 @@ class _Engine:
             t.pdx2 = st[_S_PDX:].data_ptr()
             t.width = float(DELTA_WINDOW)
             t.pred = sc[_lib.CG_RUNNING:].data_ptr()
-            t.gate_next = self.gates[1 - par:].data_ptr()
+            # the gate of k+1 opens after k's tail: in the readback kernel when
+            # there is one, else at the end of the tail
+            t.gate_next = None if self._kernel_readback else self.gates[1 - par:].data_ptr()
             if self.is_ml:
                 rows = self.rows
                 t.kind, t.loss, t.rows = 0, _lib.LOSS[self.loss], rows
@@ -846,6 +849,7 @@ class _Engine:
             h.norm_kind = 1 if self.opts.norm_kind == "linf" else 0
             h.tol_out = self.tols[par:].data_ptr()
             h.ws_red = kx.red.data_ptr()
+            h.zu = C.addressof(t)  # the persistent x-update may run the tail's z/u step
             self._heads.append(h)
             self._pbs.append(None)
 
@@ -926,7 +930,8 @@ class _Engine:
 
     def _readback(self, par):
         if self._kernel_readback:
-            self.kx.copy_to_pinned(self.rbs[par], self.rbs_host[par])
+            t = self._tails[par]
+            self.kx.readback(self.rbs[par], self.rbs_host[par], self.gates[1 - par:].data_ptr(), t.pred)
         else:
             self.rbs_host[par].copy_(self.rbs[par], non_blocking=True)
         self.kx.d2h += _RB_LEN * 8

@@ -400,6 +400,7 @@ extern "C" int nys_admm_head_f64(const nys_admm_head* h, void* stream);
 extern "C" int nys_admm_xupdate_f64(const nys_admm_head* h, const nys_cg_problem* pb, int count, void* stream) {
   if (!h || !pb) return NYS_ERR_ARG;
   cudaStream_t st = as_stream(stream);
+  if (h->zu) h->zu->zu_done = 0;
   if (pb->ws_cp && pb->op_kind == 0) {
     TimedLaunch tl{pb->timing_tag, 0, nullptr, nullptr};
     if (g_timing) {

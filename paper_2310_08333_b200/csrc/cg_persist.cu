@@ -62,6 +62,21 @@ struct CgPersistArgs {
   int has_head;       // run the ADMM head (nys_admm_head) as the prologue
   int u_smem;         // stage this CTA's rows of U in shared memory
   nys_admm_head h;
+  // the ADMM tail's relax/prox/dual update and window append, run on each
+  // CTA's slice of x once the CG has stopped (nys_admm_head.zu)
+  int has_zu;
+  struct {
+    double* z;
+    double* u;
+    double* xbar;
+    double* zbar;
+    double alpha, kappa;
+    int prox_kind, accum;
+    const double* lo;
+    const double* hi;
+    double* rx;  // window slot for x (NULL: no append)
+    double* ru;  // window slot for u (NULL: none)
+  } zu;
 };
 
 __device__ __forceinline__ double cp_tol(const CgPersistArgs& a) { return a.tolp ? *a.tolp : a.tol; }
@@ -128,6 +143,36 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
     asm volatile("cp.async.commit_group;\n" ::);
   }
+  // z/u step of the ADMM tail on the slice (vec.cu admm_zu_kernel +
+  // ring_copy_kernel, admm.py:562-583, 622-623); x of the slice was last
+  // written by this thread, so no grid barrier is needed
+  auto zu_slice = [&]() {
+    if (!a.has_zu) return;
+    const auto& q = a.zu;
+    const double beta = 1.0 - q.alpha;
+    for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
+      const double xi = a.x[i];
+      const double w = __dadd_rn(__dmul_rn(q.alpha, xi), __dmul_rn(beta, q.z[i]));
+      const double ui = q.u[i];
+      const double v = __dadd_rn(w, ui);
+      double zn;
+      if (q.prox_kind == NYS_PROX_SOFT) {
+        const double m = fmax(__dadd_rn(fabs(v), -q.kappa), 0.0);
+        zn = v > 0.0 ? m : (v < 0.0 ? -m : 0.0 * m);
+      } else {
+        zn = fmin(fmax(v, q.lo[i]), q.hi[i]);
+      }
+      const double un = __dadd_rn(__dadd_rn(ui, w), -zn);
+      q.z[i] = zn;
+      q.u[i] = un;
+      if (q.accum) {
+        q.xbar[i] = __dadd_rn(q.xbar[i], xi);
+        q.zbar[i] = __dadd_rn(q.zbar[i], zn);
+      }
+      if (q.rx) q.rx[i] = xi;
+      if (q.ru) q.ru[i] = un;
+    }
+  };
   // ---------------------------------------------------------- begin ----
   // every CTA evaluates the begin logic itself (same inputs, same result)
   double tol, b2, res2;
@@ -404,7 +449,10 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
         sc[NYS_CG_RUNNING] = 1.0;
       }
     }
-    if (done0) return;
+    if (done0) {
+      zu_slice();
+      return;
+    }
   }
   if (a.r > 0) make_coef();
   {
@@ -535,6 +583,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
     pb ^= 1;
   }
+  zu_slice();
 }
 
 struct CpPlan {
@@ -643,17 +692,37 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
   a.has_head = head != nullptr;
   a.u_smem = pl.u_smem;
   if (head) a.h = *head;
+  const nys_admm_tail* t = head ? head->zu : nullptr;
+  if (t && t->kind == 0 && t->XZ == pb->x && t->n == pb->n) {
+    a.has_zu = 1;
+    a.zu.z = t->XZ + t->n;
+    a.zu.u = t->u;
+    a.zu.xbar = t->xbar;
+    a.zu.zbar = t->zbar;
+    a.zu.alpha = t->alpha;
+    a.zu.kappa = t->kappa;
+    a.zu.prox_kind = NYS_PROX_SOFT;
+    a.zu.accum = t->accum;
+    a.zu.lo = t->lo;
+    a.zu.hi = t->hi;
+    a.zu.rx = t->ring ? t->ring + (int64_t)t->slot * t->ring_ld : nullptr;
+    a.zu.ru = t->ring && t->uring ? t->uring + (int64_t)t->slot * t->ring_ld : nullptr;
+  }
+  int rc = NYS_ERR_UNSUPPORTED;
 #define NYS_CP(k)                                                    \
   case k:                                                            \
-    if (pl.MC == 4) return cp_launch<k, 4>(pl, a, st);               \
-    if (pl.MC == 8) return cp_launch<k, 8>(pl, a, st);               \
-    return cp_launch<k, 16>(pl, a, st);
+    if (pl.MC == 4) rc = cp_launch<k, 4>(pl, a, st);                 \
+    else if (pl.MC == 8) rc = cp_launch<k, 8>(pl, a, st);            \
+    else rc = cp_launch<k, 16>(pl, a, st);                           \
+    break;
   switch (pl.K) {
     NYS_CP(1) NYS_CP(2) NYS_CP(3) NYS_CP(4) NYS_CP(5) NYS_CP(6) NYS_CP(7) NYS_CP(8) NYS_CP(9) NYS_CP(10)
     NYS_CP(11) NYS_CP(12) NYS_CP(13)
-    default: return NYS_ERR_UNSUPPORTED;
+    default: break;
   }
 #undef NYS_CP
+  if (rc == NYS_OK && a.has_zu) head->zu->zu_done = 1;
+  return rc;
 }
 
 }  // namespace nys

@@ -815,6 +815,23 @@ extern "C" int nys_copy_f64(const double* src, double* dst, int64_t n, void* str
   return NYS_OK;
 }
 
+__global__ void readback_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t n, double* gate,
+                                const double* __restrict__ pred) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  __threadfence_system();
+  if (gate && blockIdx.x == 0 && threadIdx.x == 0 && !(pred && *pred != 0.0)) *gate = 1.0;
+}
+
+extern "C" int nys_readback_f64(const double* src, double* dst, int64_t n, double* gate_next, const double* pred,
+                                void* stream) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return NYS_ERR_ARG;
+  readback_kernel<<<(unsigned)tmin<int64_t>(cdiv(tmax<int64_t>(n, 1), 256), 64), 256, 0, as_stream(stream)>>>(
+      src, dst, n, gate_next, pred);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
 extern "C" int nys_admm_head_f64(const nys_admm_head* h, void* stream) {
   if (!h || h->n <= 0 || !h->rhs || !h->r || !h->sc || !h->ws_red) return NYS_ERR_ARG;
   if (h->snap && (!h->xbar || !h->zbar)) return NYS_ERR_ARG;
@@ -953,13 +970,16 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   double* x = t->XZ;
   double* z = t->XZ + n;
   int rc;
-  // relax / prox / dual update + averages (admm.py:562-583)
-  admm_zu_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, z, t->u, t->alpha, t->kind == 0 ? NYS_PROX_SOFT
-                                                                                               : NYS_PROX_BOX,
-                                                        t->kappa, t->lo, t->hi, t->xbar, t->zbar, t->accum, pred);
-  NYS_CHECK_LAUNCH();
+  // relax / prox / dual update + averages (admm.py:562-583), unless the
+  // persistent x-update kernel already ran it (nys_admm_head.zu)
+  if (!t->zu_done) {
+    admm_zu_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, z, t->u, t->alpha,
+                                                          t->kind == 0 ? NYS_PROX_SOFT : NYS_PROX_BOX, t->kappa, t->lo,
+                                                          t->hi, t->xbar, t->zbar, t->accum, pred);
+    NYS_CHECK_LAUNCH();
+  }
   // window append (admm.py:622-623), speculative: the host commits it
-  if (t->ring) {
+  if (t->ring && !t->zu_done) {
     ring_copy_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, t->ring + (int64_t)t->slot * t->ring_ld, t->u,
                                                             t->uring ? t->uring + (int64_t)t->slot * t->ring_ld
                                                                      : nullptr,

@@ -194,6 +194,12 @@ class Kernels:
         self.launches += 1
         check(self.L.nys_copy_f64(src.data_ptr(), dst.data_ptr(), src.numel(), self.sp), "copy")
 
+    def readback(self, src: torch.Tensor, dst: torch.Tensor, gate_next: int, pred: int) -> None:
+        """copy_to_pinned that also opens the next iteration's gate."""
+        self.launches += 1
+        check(self.L.nys_readback_f64(src.data_ptr(), dst.data_ptr(), src.numel(), gate_next, pred, self.sp),
+              "readback")
+
     def admm_head(self, h) -> None:
         self.launches += 1
         check(self.L.nys_admm_head_f64(C.byref(h), self.sp), "admm_head")

@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--seq", type=int, default=-1, help="print the kernel sequence after the Nth cg_persist launch")
     args = ap.parse_args()
     import bench
     import paper_2310_08333_b200 as nys
@@ -70,6 +71,15 @@ def main():
         "gap_contexts": [{"between": k, "count": c, "total_ms": tot / 1e3}
                          for k, (c, tot) in sorted(ctx.items(), key=lambda kv: -kv[1][1])[:20]],
     }
+    if args.seq >= 0:
+        starts = [i for i, (_, _, nm) in enumerate(ivs) if "cg_persist" in nm]
+        if len(starts) > args.seq + 1:
+            a, b = starts[args.seq], starts[args.seq + 1]
+            t0 = ivs[a][0]
+            prev = t0
+            for s, t, nm in ivs[a:b + 1]:
+                print(f"seq {s - t0:9.1f} +{s - prev:6.1f} {t - s:8.1f} us  {nm.split('(')[0][-60:]}")
+                prev = t
     print(json.dumps(out, indent=1))
     if args.json:
         with open(args.json, "w") as f:
