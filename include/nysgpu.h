@@ -103,6 +103,12 @@ typedef struct nys_cg_problem {
   void* ws_cp; size_t ws_cp_bytes;     /* NULL, or nys_cg_persist_workspace(n, r) bytes,
                                           zero-filled once: the whole solve then runs as ONE
                                           persistent cooperative kernel when the shape allows */
+  const double* order_in; double* order_out; /* NULL, or the row order of the last pass over A
+                                          before / after this solve (0 ascending, 1 descending):
+                                          the persistent kernel alternates the order of its
+                                          passes starting opposite to *order_in so each pass
+                                          begins with the rows still in L2, and records its
+                                          last in *order_out (results depend only on *order_in) */
 } nys_cg_problem;
 
 /* ---------------------------------------------------------------- misc -- */
@@ -231,6 +237,10 @@ typedef struct nys_admm_tail {
   double* conj_out;           /* NULL, or (ML, with_z, lambda2 == 0) the scaled-dual conjugate
                                  sums of problems.py:330-340 with c = lambda1 / max|atnu|,
                                  computed when max|atnu| > lambda1 (3 values)           */
+  const double* order;        /* NULL, or the row order of the last pass over A before the
+                                 tail (nys_cg_problem.order_out): the data passes run
+                                 opposite to it, then along it (schedule only: results do
+                                 not depend on it)                                      */
   int zu_done;                /* set by nys_admm_xupdate_f64 when its persistent kernel
                                  already ran the relax/prox/dual update and the window
                                  append of this descriptor; the tail then skips them   */

@@ -54,7 +54,7 @@ class CgProblem(C.Structure):
         ("b", P), ("x", P), ("res", P), ("p", P), ("z", P), ("Ap", P), ("sc", P),
         ("tol", F64), ("max_iter", I64), ("ws_op", P), ("ws_op_bytes", SZ), ("ws_pc", P),
         ("ws_pc_bytes", SZ), ("ws_red", P), ("gate", P), ("tol_dev", P), ("timing_tag", I64),
-        ("ws_cp", P), ("ws_cp_bytes", SZ),
+        ("ws_cp", P), ("ws_cp_bytes", SZ), ("order_in", P), ("order_out", P),
     ]
 
 class AdmmTail(C.Structure):
@@ -71,7 +71,7 @@ class AdmmTail(C.Structure):
         ("qp_infeas", C.c_int), ("inf_first", C.c_int), ("inf_last", C.c_int), ("width", F64),
         ("dx", P), ("Pdx", P), ("infeas", P), ("pdx2", P),
         ("ws_gemv", P), ("ws_gemv_bytes", SZ), ("ws_gemvT", P), ("ws_gemvT_bytes", SZ), ("ws_red", P),
-        ("pred", P), ("gate_next", P), ("conj_out", P), ("zu_done", C.c_int),
+        ("pred", P), ("gate_next", P), ("conj_out", P), ("order", P), ("zu_done", C.c_int),
     ]
 
 

@@ -782,6 +782,8 @@ class _Engine:
         self.gates = kx.zeros(2)
         self.gates[1] = 1.0  # iteration 1 (parity 1) may run
         self.tols = kx.zeros(2)
+        # row order of the last pass over A of iteration parity p (L2 reuse)
+        self.orders = kx.zeros(2)
         self.snap = kx.zeros(5, n)
         self._done_ev = [torch.cuda.Event() for _ in range(2)]
         self._ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(2)]
@@ -805,6 +807,7 @@ class _Engine:
             t.pdx2 = st[_S_PDX:].data_ptr()
             t.width = float(DELTA_WINDOW)
             t.pred = sc[_lib.CG_RUNNING:].data_ptr()
+            t.order = self.orders[par:].data_ptr()
             # the gate of k+1 opens after k's tail: in the readback kernel when
             # there is one, else at the end of the tail
             t.gate_next = None if self._kernel_readback else self.gates[1 - par:].data_ptr()
@@ -869,6 +872,8 @@ class _Engine:
                                    1e-12, 10 * n)
             pb.gate = self.gates[par:].data_ptr()
             pb.tol_dev = self.tols[par:].data_ptr()
+            pb.order_in = self.orders[1 - par:].data_ptr()
+            pb.order_out = self.orders[par:].data_ptr()
             pb._key = key
             self._pbs[par] = pb
         return pb

@@ -61,6 +61,8 @@ struct CgPersistArgs {
   int W, S;
   int has_head;       // run the ADMM head (nys_admm_head) as the prologue
   int u_smem;         // stage this CTA's rows of U in shared memory
+  const double* order_in;  // row order of the previous pass over A (NULL: ascending first)
+  double* order_out;       // row order of this solve's last pass
   nys_admm_head h;
   // the ADMM tail's relax/prox/dual update and window append, run on each
   // CTA's slice of x once the CG has stopped (nys_admm_head.zu)
@@ -121,7 +123,8 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   double* sh = red + 32;                                                     // 32
   double* csh = sh + 32;                                                     // coef (r <= 512)
   double* ys = csh + 520;                                                    // slice sums
-  double* us = ys + 112;                                                     // U rows of the slice
+  double* scr = ys + 112;                                                    // colsum scratch (512)
+  double* us = scr + 512;                                                    // U rows of the slice
   __shared__ double s_bcast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nctas = gridDim.x, cta = blockIdx.x;
@@ -174,13 +177,9 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
   };
   // ---------------------------------------------------------- begin ----
-  // every CTA evaluates the begin logic itself (same inputs, same result)
-  double tol, b2, res2;
-  if (a.has_head) {
-    // ADMM head (nys_admm_head_f64) on this CTA's slice: gate, device CG
-    // tolerance, snapshot, rhs and r0 = rhs - H x0, ||rhs||^2, ||r0||^2
-    const nys_admm_head& h = a.h;
-    if (h.gate && *h.gate == 0.0) {  // previous ADMM iteration unfinished
+  {
+    const double* gp = a.has_head ? a.h.gate : a.gate;
+    if (gp && *gp == 0.0) {  // previous ADMM iteration unfinished: skip the solve
       if (writer) {
         sc[NYS_CG_DONE] = 5.0;
         sc[NYS_CG_ITERS] = 0.0;
@@ -188,6 +187,52 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       }
       return;
     }
+  }
+  // Passes over A alternate their row order, starting opposite to the pass
+  // before this kernel, so each begins with the rows still in L2; the first
+  // rows of a pass are requested before the work that leads up to it (they
+  // do not depend on it).  Row q of this CTA in order dir: cta + q' nctas,
+  // q' = q (ascending) or m - 1 - q (descending).
+  const int64_t nrows_mine = a.rows > cta ? (a.rows - cta + nctas - 1) / nctas : 0;
+  const unsigned rbytes = (unsigned)n * 8u;
+  int64_t g0 = 0;    // rows consumed so far by this CTA (mbarrier phase bookkeeping)
+  int pre_dir = -1;  // order of the next pass whose first rows are in flight
+  int last_dir = a.order_in ? (*a.order_in != 0.0 ? 1 : 0) : 1;
+  auto row_of = [&](int64_t q, int dir) -> int64_t {
+    return cta + (dir ? nrows_mine - 1 - q : q) * nctas;
+  };
+  auto prefetch = [&](int dir) {
+    if (tid == 0)
+      for (int64_t q = 0; q < a.S && q < nrows_mine; ++q) {
+        const int64_t g = g0 + q;
+        const int st = (int)(g % a.S);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[st], rbytes);
+        tma_load_1d(ring + (size_t)st * a.W, a.A + row_of(q, dir) * a.lda, rbytes, &full[st]);
+      }
+    pre_dir = dir;
+  };
+  if (tid == 0) {
+    for (int q = 0; q < a.S; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  prefetch(last_dir ^ 1);
+  // end of the solve: the speculative first rows of a next pass must land
+  // before the CTA exits; record the order of the last pass
+  auto finish = [&]() {
+    if (tid == 0 && pre_dir >= 0)
+      for (int64_t q = 0; q < a.S && q < nrows_mine; ++q) {
+        const int64_t g = g0 + q;
+        mbar_wait(&full[g % a.S], (unsigned)((g / a.S) & 1));
+      }
+    if (writer && a.order_out) *a.order_out = (double)last_dir;
+  };
+  // every CTA evaluates the begin logic itself (same inputs, same result)
+  double tol, b2, res2;
+  if (a.has_head) {
+    // ADMM head (nys_admm_head_f64) on this CTA's slice: device CG
+    // tolerance, snapshot, rhs and r0 = rhs - H x0, ||rhs||^2, ||r0||^2
+    const nys_admm_head& h = a.h;
     if (h.tol_fixed > 0.0) {
       tol = h.tol_fixed;
     } else {  // krylov.py:98-112 from the residual norms of the previous iteration
@@ -229,27 +274,11 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       a.part[cta * 8 + 5] = sr;
     }
   } else {
-    if (a.gate && *a.gate == 0.0) {
-      if (writer) {
-        sc[NYS_CG_DONE] = 5.0;
-        sc[NYS_CG_ITERS] = 0.0;
-        sc[NYS_CG_RUNNING] = 1.0;
-      }
-      return;
-    }
     tol = cp_tol(a);
     b2 = sc[NYS_CG_B2];
     res2 = sc[NYS_CG_RES2];
   }
-  if (tid == 0) {
-    for (int q = 0; q < a.S; ++q) mbar_init(&full[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
   __syncthreads();
-
-  const int64_t nrows_mine = a.rows > cta ? (a.rows - cta + nctas - 1) / nctas : 0;
-  const unsigned rbytes = (unsigned)n * 8u;
-  int64_t g0 = 0;  // rows consumed so far by this CTA (mbarrier phase bookkeeping)
 
   // fixed-order sum over the CTAs of slot q of part (nctas x 8), in every thread
   auto all_sum = [&](int q) -> double {
@@ -265,23 +294,18 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   };
   // y = A^T (d o A v) for this CTA's rows into ypart[cta]; v in registers.
   // Returns sum_rows d_i (a_i . v)^2 of this CTA's rows (valid in thread 0).
+  // The pass runs in the order of the rows already requested (pre_dir) and
+  // requests the first rows of the next pass (opposite order) at its end.
   auto hvp_rows = [&](double2 (&vr)[K]) -> double {
     double2 yr[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) yr[k] = make_double2(0.0, 0.0);
     double vav = 0.0;
-    if (tid == 0)
-      for (int64_t q = 0; q < a.S && q < nrows_mine; ++q) {
-        const int st = (int)((g0 + q) % a.S);
-        const int64_t i = cta + q * nctas;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&full[st], rbytes);
-        tma_load_1d(ring + (size_t)st * a.W, a.A + i * a.lda, rbytes, &full[st]);
-      }
+    const int dir = pre_dir;
     for (int64_t it = 0; it < nrows_mine; ++it) {
       const int64_t g = g0 + it;
       const int st = (int)(g % a.S);
-      const int64_t i = cta + it * nctas;
+      const int64_t i = row_of(it, dir);
       const double di = a.d ? __ldg(a.d + i) : 1.0;
       const double* row = ring + (size_t)st * a.W;
       mbar_wait(&full[st], (unsigned)((g / a.S) & 1));
@@ -312,13 +336,15 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       }
       __syncthreads();
       if (tid == 0 && it + a.S < nrows_mine) {
-        const int64_t inext = cta + (it + a.S) * nctas;
+        const int64_t inext = row_of(it + a.S, dir);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&full[st], rbytes);
         tma_load_1d(ring + (size_t)st * a.W, a.A + inext * a.lda, rbytes, &full[st]);
       }
     }
     g0 += nrows_mine;
+    last_dir = dir;
+    prefetch(dir ^ 1);
     double* yp = a.ypart + (int64_t)cta * n;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -331,7 +357,6 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   // all threads: G groups with independent loads in flight, combined in a
   // fixed order through the (idle) ring.  Valid in every thread after the call.
   auto colsum = [&](const double* P, int64_t ld, int cnt, int64_t col0, int ncols, double* out) {
-    double* scr = ring;
     const int G = ncols > 0 ? tmax(1, tmin(16, kCpThreads / ncols)) : 1;
     __syncthreads();
     if (tid < G * ncols) {
@@ -355,31 +380,23 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     __syncthreads();
   };
   // this CTA's share of h = U^T w over its slice -> hpart[cta]
+  // (thread j: four fixed-order chains over the slice's rows; w of the slice
+  // was written by this CTA before the last barrier)
   auto utw_slice = [&](const double* w) {
-    double acc[MC];
-#pragma unroll
-    for (int cc = 0; cc < MC; ++cc) acc[cc] = 0.0;
-    for (int64_t i = c0 + warp; i < c1; i += kCpWarps) {
-      const double wi = w[i];
-      const double* ui = ush ? us + (i - c0) * a.r : a.U + i * a.ldu;
-#pragma unroll
-      for (int cc = 0; cc < MC; ++cc) {
-        const int j = lane + 32 * cc;
-        if (j < a.r) acc[cc] = fma(ui[j], wi, acc[cc]);
-      }
-    }
-    double* ws = ring;  // warps in a fixed order (no TMA in flight here)
-    __syncthreads();
-#pragma unroll
-    for (int cc = 0; cc < MC; ++cc) {
-      const int j = lane + 32 * cc;
-      if (j < a.r) ws[warp * a.r + j] = acc[cc];
-    }
-    __syncthreads();
+    const int64_t len = c1 - c0;
     for (int j = tid; j < a.r; j += kCpThreads) {
-      double h = 0.0;
-      for (int w2 = 0; w2 < kCpWarps; ++w2) h += ws[w2 * a.r + j];
-      a.hpart[(int64_t)cta * a.r + j] = h;
+      const double* uj = ush ? us + j : a.U + c0 * a.ldu + j;
+      const int64_t ld = ush ? a.r : a.ldu;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int64_t q = 0;
+      for (; q + 3 < len; q += 4) {
+        s0 = fma(uj[q * ld], w[c0 + q], s0);
+        s1 = fma(uj[(q + 1) * ld], w[c0 + q + 1], s1);
+        s2 = fma(uj[(q + 2) * ld], w[c0 + q + 2], s2);
+        s3 = fma(uj[(q + 3) * ld], w[c0 + q + 3], s3);
+      }
+      for (; q < len; ++q) s0 = fma(uj[q * ld], w[c0 + q], s0);
+      a.hpart[(int64_t)cta * a.r + j] = (s0 + s1) + (s2 + s3);
     }
   };
   // every CTA: coef_j = (lam_{r-1}+nu)(h_j/(lam_j+nu)) - h_j into shared memory
@@ -451,6 +468,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
     if (done0) {
       zu_slice();
+      finish();
       return;
     }
   }
@@ -584,6 +602,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     pb ^= 1;
   }
   zu_slice();
+  finish();
 }
 
 struct CpPlan {
@@ -604,11 +623,9 @@ static CpPlan cp_plan(const nys_cg_problem* pb) {
   if (p.K > kCpMaxK) return p;
   p.MC = pb->r <= 128 ? 4 : (pb->r <= 256 ? 8 : 16);
   const size_t row_bytes = (size_t)p.W * 8;
-  const size_t extra = 64 * 8 + (size_t)(520 + 112) * 8 + 1024;  // red, sh, csh (r <= 512), slice sums
+  const size_t extra = 64 * 8 + (size_t)(520 + 112 + 512) * 8 + 1024;  // red, sh, csh, slice sums, scratch
   p.S = (int)tmin<int64_t>(4, (kCpSmemBudget - extra) / row_bytes);
   if (p.S < 2) return p;
-  // the U^T r warp partials reuse the ring: 16 x r doubles must fit
-  if ((size_t)kCpWarps * pb->r * 8 > (size_t)p.S * row_bytes) return p;
   p.smem = (size_t)p.S * row_bytes + (size_t)p.S * 8 + extra;
   const int64_t slice = ((pb->n + kNumSMs - 1) / kNumSMs + 1) & ~1ll;
   const size_t ubytes = (size_t)slice * (pb->r > 0 ? pb->r : 0) * 8;
@@ -691,6 +708,8 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
   a.S = pl.S;
   a.has_head = head != nullptr;
   a.u_smem = pl.u_smem;
+  a.order_in = pb->order_in;
+  a.order_out = pb->order_out;
   if (head) a.h = *head;
   const nys_admm_tail* t = head ? head->zu : nullptr;
   if (t && t->kind == 0 && t->XZ == pb->x && t->n == pb->n) {

@@ -244,12 +244,16 @@ template <int K, bool VEC>
 __global__ void __launch_bounds__(kGemvTThreads)
 gemv_t_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
               const double* __restrict__ T, int64_t ldt, double* __restrict__ out, int64_t ldo,
-              int64_t rows_per_split, int direct, const double* __restrict__ pred) {
+              int64_t rows_per_split, int direct, const double* __restrict__ pred,
+              const double* __restrict__ order = nullptr) {
   if (pred && *pred != 0.0) return;
   __shared__ double tsh[K][kGemvTTile];
+  // splits in descending row order when the previous pass over A ended at the
+  // top (L2 reuse; split s always writes partial s)
+  const int64_t by = (order && *order != 0.0) ? (int64_t)gridDim.y - 1 - blockIdx.y : (int64_t)blockIdx.y;
   constexpr int CPT = VEC ? 2 : 1;  // columns per thread
   const int64_t c = ((int64_t)blockIdx.x * kGemvTThreads + threadIdx.x) * CPT;
-  const int64_t i0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t i0 = by * rows_per_split;
   const int64_t i1 = min(rows, i0 + rows_per_split);
   double acc[K][CPT];
 #pragma unroll
@@ -303,7 +307,7 @@ gemv_t_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda
   }
   if (c >= n) return;
   const bool two = VEC && (c + 1 < n);
-  double* o = direct ? out : out + (int64_t)blockIdx.y * K * ldo;
+  double* o = direct ? out : out + by * K * ldo;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     if (two) {
@@ -425,7 +429,7 @@ static int gemv_t_launch(const double* A, int64_t rows, int64_t n, int64_t lda, 
 template <int K>
 static int gemv_t_partials_k(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T,
                              int64_t ldt, void* ws, size_t ws_bytes, cudaStream_t st, const double* pred,
-                             double** Pout, int* splits_out) {
+                             double** Pout, int* splits_out, const double* order) {
   const bool vec = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((n & 1) == 0);
   int splits;
   int64_t rps;
@@ -435,9 +439,9 @@ static int gemv_t_partials_k(const double* A, int64_t rows, int64_t n, int64_t l
   const int64_t strips = cdiv(n, (int64_t)kGemvTThreads * (vec ? 2 : 1));
   dim3 grid((unsigned)strips, (unsigned)splits);
   if (vec)
-    gemv_t_kernel<K, true><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt, P, n, rps, 0, pred);
+    gemv_t_kernel<K, true><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt, P, n, rps, 0, pred, order);
   else
-    gemv_t_kernel<K, false><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt, P, n, rps, 0, pred);
+    gemv_t_kernel<K, false><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt, P, n, rps, 0, pred, order);
   NYS_CHECK_LAUNCH();
   *Pout = P;
   *splits_out = splits;
@@ -445,10 +449,11 @@ static int gemv_t_partials_k(const double* A, int64_t rows, int64_t n, int64_t l
 }
 
 int gemv_t_partials(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt, int k,
-                    void* ws, size_t ws_bytes, cudaStream_t st, const double* pred, double** P, int* splits) {
+                    void* ws, size_t ws_bytes, cudaStream_t st, const double* pred, double** P, int* splits,
+                    const double* order) {
   switch (k) {
-    case 2: return gemv_t_partials_k<2>(A, rows, n, lda, T, ldt, ws, ws_bytes, st, pred, P, splits);
-    case 3: return gemv_t_partials_k<3>(A, rows, n, lda, T, ldt, ws, ws_bytes, st, pred, P, splits);
+    case 2: return gemv_t_partials_k<2>(A, rows, n, lda, T, ldt, ws, ws_bytes, st, pred, P, splits, order);
+    case 3: return gemv_t_partials_k<3>(A, rows, n, lda, T, ldt, ws, ws_bytes, st, pred, P, splits, order);
     default: return NYS_ERR_ARG;
   }
 }

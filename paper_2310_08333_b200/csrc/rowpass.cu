@@ -38,8 +38,12 @@ xz_rowpass_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t
                   const double* __restrict__ x, const double* __restrict__ z, const double* __restrict__ b,
                   int loss, int Wp, int S, double* __restrict__ tg, double* __restrict__ w,
                   double* __restrict__ thx, double* __restrict__ tnu, double* __restrict__ rowsums,
-                  double* part, unsigned int* counter, const double* __restrict__ pred) {
+                  double* part, unsigned int* counter, const double* __restrict__ pred,
+                  const double* __restrict__ order) {
   if (pred && *pred != 0.0) return;
+  // rows in the order opposite to the previous pass over A (L2 reuse); row
+  // results are stored by position, so the order does not change them
+  const bool desc = order && *order == 0.0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);                   // S x Wp
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * Wp);  // S
@@ -67,7 +71,8 @@ xz_rowpass_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t
       for (int64_t g = 0; g < npieces; ++g) {
         const int q = (int)(g % S);
         if (g >= S) mbar_wait(&empty[q], (unsigned)(((g / S) - 1) & 1));
-        const int64_t i = cta + (g / P) * nctas;
+        const int64_t qq = desc ? nrows_mine - 1 - g / P : g / P;
+        const int64_t i = cta + qq * nctas;
         mbar_expect_tx(&full[q], pbytes);
         tma_load_1d(ring + (size_t)q * Wp, A + i * lda + (g % P) * Wp, pbytes, &full[q]);
       }
@@ -86,7 +91,7 @@ xz_rowpass_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t
         zr[h][k] = (ok && WITH_Z) ? *reinterpret_cast<const double2*>(z + j) : make_double2(0.0, 0.0);
       }
     for (int64_t it = 0; it < nrows_mine; ++it) {
-      const int64_t i = cta + it * nctas;
+      const int64_t pos = desc ? nrows_mine - 1 - it : it;  // the row's position in this CTA
       double px = 0.0, pz = 0.0;
 #pragma unroll
       for (int h = 0; h < P; ++h) {
@@ -122,8 +127,8 @@ xz_rowpass_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t
         const double az =
             WITH_Z ? warp_sum(lane < kRpConsumers ? red[((it & 1) * 16 + lane) * 2 + 1] : 0.0) : 0.0;
         if (lane == 0) {
-          axz[2 * it] = ax;
-          axz[2 * it + 1] = az;
+          axz[2 * pos] = ax;
+          axz[2 * pos + 1] = az;
         }
       }
     }
@@ -214,7 +219,7 @@ template <int KP, int P>
 static int rowpass_launch(const RowpassPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda,
                           const double* x, const double* z, const double* b, int loss, double* tg, double* w,
                           double* thx, double* tnu, double* rowsums, double* part, unsigned int* counter,
-                          cudaStream_t st, const double* pred) {
+                          cudaStream_t st, const double* pred, const double* order) {
   const bool wz = z != nullptr;
   auto fn = wz ? xz_rowpass_kernel<KP, P, true> : xz_rowpass_kernel<KP, P, false>;
   static bool attr[2] = {false, false};
@@ -224,7 +229,7 @@ static int rowpass_launch(const RowpassPlan& p, const double* A, int64_t rows, i
   }
   const unsigned grid = (unsigned)tmin<int64_t>(kNumSMs, rows);
   fn<<<grid, kRpThreads, p.smem, st>>>(A, rows, n, lda, x, z, b, loss, p.Wp, p.S, tg, w, thx, tnu, rowsums, part,
-                                       counter, pred);
+                                       counter, pred, order);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -233,13 +238,13 @@ static int rowpass_launch(const RowpassPlan& p, const double* A, int64_t rows, i
 // then runs the separate GEMV + row-wise kernels)
 int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                const double* b, int loss, double* tg, double* w, double* thx, double* tnu, double* rowsums,
-               double* part, unsigned int* counter, cudaStream_t st, const double* pred) {
+               double* part, unsigned int* counter, cudaStream_t st, const double* pred, const double* order) {
   const RowpassPlan p = rowpass_plan(rows, n, lda, A, x, z);
   if (!p.ok) return NYS_ERR_UNSUPPORTED;
 #define NYS_RP(kp, pp)                                                                                        \
   if (p.KP == kp && p.P == pp)                                                                                \
     return rowpass_launch<kp, pp>(p, A, rows, n, lda, x, z, b, loss, tg, w, thx, tnu, rowsums, part, counter, \
-                                  st, pred);
+                                  st, pred, order);
   NYS_RP(1, 1) NYS_RP(2, 1) NYS_RP(3, 1) NYS_RP(4, 1) NYS_RP(5, 1) NYS_RP(6, 1) NYS_RP(7, 1) NYS_RP(8, 1)
   NYS_RP(9, 1) NYS_RP(10, 1) NYS_RP(11, 1) NYS_RP(12, 1)
   NYS_RP(1, 2) NYS_RP(2, 2) NYS_RP(3, 2) NYS_RP(4, 2) NYS_RP(5, 2) NYS_RP(6, 2) NYS_RP(7, 2) NYS_RP(8, 2)

@@ -956,10 +956,11 @@ int gemv_t(const double* A, int64_t rows, int64_t n, int64_t lda, const double* 
            int64_t ldy, const double* v, double shift, double* dot, void* ws, size_t ws_bytes, cudaStream_t st,
            const double* pred);
 int gemv_t_partials(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt, int k,
-                    void* ws, size_t ws_bytes, cudaStream_t st, const double* pred, double** P, int* splits);
+                    void* ws, size_t ws_bytes, cudaStream_t st, const double* pred, double** P, int* splits,
+                    const double* order);
 int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                const double* b, int loss, double* tg, double* w, double* thx, double* tnu, double* rowsums,
-               double* part, unsigned int* counter, cudaStream_t st, const double* pred);
+               double* part, unsigned int* counter, cudaStream_t st, const double* pred, const double* order);
 }  // namespace nys
 
 extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
@@ -992,7 +993,7 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
     // 2-RHS GEMV and the row-wise kernel
     rc = xz_rowpass(t->A, t->rows, n, t->lda, x, t->with_z ? z : nullptr, t->b, t->loss, t->T, t->w, t->T + t->rows,
                     t->with_z ? t->T + 2 * t->rows : nullptr, t->rowsums, red_part(t->ws_red), red_counter(t->ws_red),
-                    st, pred);
+                    st, pred, t->order);
     if (rc == NYS_ERR_UNSUPPORTED) {
       const int k = t->with_z ? 2 : 1;
       if ((rc = gemv_n(t->A, t->rows, n, t->lda, t->XZ, n, k, t->AXZ, t->rows, nullptr, t->ws_gemv,
@@ -1013,7 +1014,7 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       int splits = 0;
       const int K = t->with_z ? 3 : 2;
       if ((rc = gemv_t_partials(t->A, t->rows, n, t->lda, t->T, t->rows, K, t->ws_gemvT, t->ws_gemvT_bytes, st,
-                                pred, &P, &splits)))
+                                pred, &P, &splits, t->order)))
         return rc;
       SlotList sl;
       const int no = (t->ring && t->nothers > 0) ? t->nothers : 0;
