@@ -528,12 +528,22 @@ int hvp_fused(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_
 int hvp_row(const HvpPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
             const double* v, double* ypart, double* y, double shift, double* dot, double* part,
             unsigned int* counter, cudaStream_t st, const double* pred);
+struct StripPlan {
+  int W, K, WPR, S, L, nctas;
+  size_t smem;
+  bool ok;
+};
+size_t hvp_strip_ws();
+StripPlan hvp_strip_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
+int hvp_strip(const StripPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
+              const double* v, double* y, double shift, double* dot, void* ws, double* part,
+              unsigned int* counter, cudaStream_t st, const double* pred);
 
 size_t hvp_ws(int64_t rows, int64_t n) {
   // two-pass: t = d o (A v) (rows doubles) + the K1 split partials + the K2 workspace
   const size_t two = cdiv(rows, 2) * 2 * sizeof(double) + gemv_n_ws(rows, n, 1) + gemv_t_ws(rows, n, 1);
   // single pass: reduction scratch + one y partial per cluster (<= 148)
-  const size_t one = kRedBytes + (size_t)kNumSMs * n * sizeof(double);
+  const size_t one = kRedBytes + tmax((size_t)kNumSMs * n * sizeof(double), hvp_strip_ws());
   return tmax(two, one);
 }
 
@@ -558,6 +568,14 @@ int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const doubl
                                                  finish ? pAp : nullptr, red_part(ws), red_counter(ws), pred);
     NYS_CHECK_LAUNCH();
     return NYS_OK;
+  }
+  // wide rows: column strips over the whole grid, A still streamed once (csrc/hvp_strip.cu)
+  static const bool no_strip = getenv("NYS_HVP_NOSTRIP") != nullptr;
+  if (!plan.ok && !two_pass_only && !no_strip) {
+    const StripPlan sp = hvp_strip_plan(rows, n, lda, A, v);
+    if (sp.ok)
+      return hvp_strip(sp, A, rows, n, lda, d, v, y, finish ? shift : 0.0, finish ? pAp : nullptr,
+                       reinterpret_cast<char*>(ws) + kRedBytes, red_part(ws), red_counter(ws), st, pred);
   }
   char* base = reinterpret_cast<char*>(ws);
   // layout: [K2 ws (reduction scratch first)] [t] [K1 partials]

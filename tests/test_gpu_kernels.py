@@ -65,7 +65,9 @@ def test_gemv_odd_leading_dim(kx):
     np.testing.assert_allclose(Z.cpu().numpy(), t @ A, rtol=1e-12, atol=1e-12)
 
 
-@pytest.mark.parametrize("rows,n", [(70, 45), (1000, 2000), (5000, 3000), (33, 7)])
+@pytest.mark.parametrize("rows,n", [(70, 45), (1000, 2000), (5000, 3000), (33, 7),
+                                    # wide rows: column-strip kernel (csrc/hvp_strip.cu)
+                                    (7, 20000), (301, 100000), (1001, 30002), (50, 250000), (2, 12802)])
 def test_hvp_fused(kx, rows, n):
     g = np.random.default_rng(n)
     A = g.standard_normal((rows, n))
