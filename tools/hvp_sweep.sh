@@ -1,5 +1,8 @@
 # HVP launch timing sweep over the strip-kernel knobs (run on the GPU box)
-for cfg in "20000 100000" "12500 200000"; do
-  for m in 0 2; do for lag in 2 3; do echo "== $cfg mode$m lag $lag"; NYS_STRIP_MODE=$m NYS_STRIP_LAG=$lag python tools/hvp_bench.py $cfg 20; done; done
-  echo "== twopass"; NYS_HVP_TWOPASS=1 python tools/hvp_bench.py $cfg 20
-done
+python tools/hvp_bench.py 20000 100000 20
+python tools/hvp_bench.py 20000 100000 20 nod
+NYS_HVP_TWOPASS=1 python tools/hvp_bench.py 20000 100000 20 nod
+NYS_STRIP_FORCE=1 python tools/hvp_bench.py 12500 200000 20 nod
+NYS_STRIP_FORCE=1 NYS_STRIP_MODE=2 NYS_STRIP_LAG=3 python tools/hvp_bench.py 12500 200000 20 nod
+NYS_HVP_TWOPASS=1 python tools/hvp_bench.py 12500 200000 20 nod
+python tools/hvp_bench.py 5000 10000 50
