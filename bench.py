@@ -106,6 +106,51 @@ def build_problem(cfg: int, A_op=None):
     return d, opts
 
 
+class Cfg5Data:
+    """Config 5 (BASELINE.json configs[4]): generated in HBM per rank
+    (paper_2310_08333_b200/devgen.py), never on the host."""
+
+    cfg, kind, loss, rank, seed = 5, "lasso", "square", 300, 4
+
+    def __init__(self, N, n, lam, b):
+        self.N, self.n, self.lambda1, self.lambda2, self.b = N, n, lam, 0.0, b
+        self.A = None
+
+
+def build_cfg5(world, rank):
+    """This rank's row blocks of config 5 generated on its GPU; lambda =
+    0.1 ||A^T b||_inf with one n-vector all-reduce (SURVEY.md 8(e) setup)."""
+    import torch
+
+    import paper_2310_08333_b200 as nys
+    from paper_2310_08333_b200 import datagen, devgen
+    from paper_2310_08333_b200.kernels import get_kernels
+
+    kx = get_kernels()
+    nb = datagen.CFG5_BLOCKS
+    if nb % world:
+        raise SystemExit(f"config 5 shards whole 12500-row blocks: world size must divide {nb}")
+    blocks = range(rank * nb // world, (rank + 1) * nb // world)
+    A_loc, b_loc, _ = devgen.cfg5_device(kx, blocks)
+    N, n = devgen.CFG5_ROWS, devgen.CFG5_N
+    atb = kx.empty(1, n)
+    kx.gemvT(A_loc, b_loc.view(1, -1).contiguous(), atb)
+    b_parts = [torch.empty_like(b_loc) for _ in range(world)]
+    if world > 1:
+        torch.distributed.all_reduce(atb)
+        torch.distributed.all_gather(b_parts, b_loc)
+    else:
+        b_parts = [b_loc]
+    lam = 0.1 * float(atb.abs().max())
+    b = torch.cat(b_parts).cpu().numpy()
+    d = Cfg5Data(N, n, lam, b)
+    row0 = blocks[0] * devgen.CFG5_BLOCK_ROWS
+    op = nys.DenseOperator(A_loc) if world == 1 else nys.DenseOperator.from_local_rows(A_loc, N, row0)
+    prob = nys.MLProblem(nys.builtin_loss("square"), op, b, lam, 0.0)
+    opts = nys.SolverOptions(sketch_rank=d.rank, rng_seed=d.seed, eps_abs=1e-4, eps_rel=1e-4, eps_dual_gap=1e-4)
+    return d, opts, A_loc, prob
+
+
 def make_gpu_problem(d, A):
     import paper_2310_08333_b200 as nys
 
@@ -169,8 +214,11 @@ def run_reference(args):
 
 
 def config_block(args, d, world):
-    n = d.P.shape[0] if d.kind == "boxqp" else d.A.shape[1]
-    N = d.A.shape[0]
+    if d.A is None:  # config 5: device-generated
+        N, n = d.N, d.n
+    else:
+        n = d.P.shape[0] if d.kind == "boxqp" else d.A.shape[1]
+        N = d.A.shape[0]
     return {"workload": f"config {args.config}: {d.kind} {N}x{n} FP64, rank {d.rank}, tol 1e-4, solve to tolerance",
             "config_index": args.config, "rows": N, "features": n, "sketch_rank": d.rank,
             "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
@@ -189,12 +237,18 @@ def run_ours(args):
     import paper_2310_08333_b200 as nys
     from paper_2310_08333_b200.kernels import get_kernels
 
-    d, opts = build_problem(args.config)
-    host_A = d.P if d.kind == "boxqp" else d.A
     kx = get_kernels()
-    # A resident in HBM for the kernel-side metric (each rank: its row shard inside solve)
-    A_dev = torch.from_numpy(host_A).cuda()
-    prob = make_gpu_problem(d, A_dev)
+    if args.config == 5:
+        # 160 GB: generated in HBM per rank (each rank holds only its row blocks)
+        d, opts, A_dev, prob = build_cfg5(world, rank)
+        host_A = None
+        args.no_e2e = args.no_cpu = True
+    else:
+        d, opts = build_problem(args.config)
+        host_A = d.P if d.kind == "boxqp" else d.A
+        # A resident in HBM for the kernel-side metric (each rank: its row shard inside solve)
+        A_dev = torch.from_numpy(host_A).cuda()
+        prob = make_gpu_problem(d, A_dev)
 
     def barrier():
         if world > 1:
@@ -248,8 +302,11 @@ def run_ours(args):
 
     # roofline of the dominant kernel: algorithmic bytes per operator application
     # (8 N n + 8 (2n + N)) x applications / measured time
-    n = host_A.shape[1]
-    rows_loc = d.A.shape[0] // world if d.kind != "boxqp" else n
+    n = A_dev.shape[1]
+    if args.config == 5:
+        rows_loc = A_dev.shape[0]
+    else:
+        rows_loc = d.A.shape[0] // world if d.kind != "boxqp" else n
     alg_bytes = 8 * rows_loc * n + 8 * (2 * n + rows_loc)
     peak, peak_kind = _peaks()
     persistent = os.environ.get("NYS_CG_PERSIST", "1") != "0" and d.kind != "boxqp" and n <= 13312
@@ -274,7 +331,7 @@ def run_ours(args):
                 "timing": "CUDA events around every PCG launch of one extra instrumented solve (not the timed steps)"}
     # the HVP kernel alone (K3, csrc/hvp.cu), back to back on the same A and row weights
     hvp_alone = None
-    if d.kind != "boxqp" and world == 1:
+    if d.kind != "boxqp" and world == 1 and args.config != 5:
         v = torch.randn(n, dtype=torch.float64, device=A_dev.device)
         y = torch.empty_like(v)
         dw = torch.rand(A_dev.shape[0], dtype=torch.float64, device=A_dev.device)
@@ -320,6 +377,8 @@ def run_ours(args):
                "h2d_bytes_per_step": int(a_bytes + b_bytes + kx.h2d / steps_e),
                "d2h_bytes_per_step": int(kx.d2h / steps_e), "time_to_tolerance_s": e_ms / 1e3 / steps_e}
 
+    if args.config == 5:
+        e2e = {"unavailable": "config 5 is generated in HBM per rank (160 GB); there is no host copy to upload"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         times, its = cpu_reference_rate(d, opts, CPU_SAMPLE_ITERS, reps=1)

@@ -376,6 +376,13 @@ int nys_nystrom_core_async_f64(int64_t n, int s, int r, const double* Q, double*
 size_t nys_gaussian_workspace(int64_t count);
 int nys_gaussian_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                      int64_t count, double* out, void* ws, size_t ws_bytes, void* stream);
+/* Same stream, and *draws = the number of 64-bit PCG64 draws the `count`
+ * samples consumed, so a long stream (config 5's 2.5e9-sample row blocks,
+ * datagen.cfg5_block / bench/datagen.py:28-137 conventions) is generated in
+ * pieces: the next piece starts from the state advanced by *draws. */
+int nys_gaussian_draws_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                           int64_t count, double* out, void* ws, size_t ws_bytes, int64_t* draws,
+                           void* stream);
 /* Orthonormalise the raw Gaussian test matrix (sketch.py:97-99) by CholeskyQR2:
  * Q (n x s, row-major) spans the same range as Omega.  Synchronises `stream`. */
 size_t nys_orthonormalize_workspace(int64_t n, int s);

@@ -136,6 +136,7 @@ SIGNATURES = {
     "nys_orthonormalize_async_f64": (I32, [I64, I32, P, P, P, P, SZ, P]),
     "nys_nystrom_core_async_f64": (I32, [I64, I32, I32, P, P, P, P, P, P, SZ, P]),
     "nys_gaussian_f64": (I32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, I64, P, P, SZ, P]),
+    "nys_gaussian_draws_f64": (I32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, I64, P, P, SZ, P, P]),
     "nys_orthonormalize_workspace": (SZ, [I64, I32]),
     "nys_orthonormalize_f64": (I32, [I64, I32, P, P, P, SZ, P]),
     "nys_nystrom_workspace": (SZ, [I64, I32, I32]),

@@ -61,6 +61,7 @@ struct CgPersistArgs {
   int W, S;
   int has_head;       // run the ADMM head (nys_admm_head) as the prologue
   int u_smem;         // stage this CTA's rows of U in shared memory
+  int probe;               // development timing probe (NYS_CP_PROBE)
   const double* order_in;  // row order of the previous pass over A (NULL: ascending first)
   double* order_out;       // row order of this solve's last pass
   nys_admm_head h;
@@ -80,6 +81,16 @@ struct CgPersistArgs {
     double* ru;  // window slot for u (NULL: none)
   } zu;
 };
+
+// Development probe (NYS_CP_PROBE=1): CTA 0 stamps %globaltimer at the phase
+// boundaries of every launch and accumulates the deltas (tools/cp_probe.py).
+__device__ unsigned long long g_cp_probe_acc[16];
+__device__ unsigned long long g_cp_probe_cnt;
+__device__ __forceinline__ unsigned long long cp_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ double cp_tol(const CgPersistArgs& a) { return a.tolp ? *a.tolp : a.tol; }
 
@@ -127,6 +138,15 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   double* us = scr + 512;                                                    // U rows of the slice
   __shared__ double s_bcast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool probe = a.probe && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long pt0 = probe ? cp_now() : 0ull, plast = pt0;
+  auto stamp = [&](int slot) {
+    if (probe) {
+      const unsigned long long t = cp_now();
+      atomicAdd(&g_cp_probe_acc[slot], t - plast);
+      plast = t;
+    }
+  };
   const int nctas = gridDim.x, cta = blockIdx.x;
   const int64_t n = a.n;
   double* sc = a.sc;
@@ -442,7 +462,9 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     __syncthreads();
     utw_slice(a.res);
   }
+  stamp(0);  // head + U^T r0 partials
   if (a.has_head || a.r > 0) grid.sync();
+  stamp(1);  // barrier 1
   if (a.has_head) {
     b2 = all_sum(4);
     res2 = all_sum(5);
@@ -477,7 +499,9 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     const double rz = apply_slice(a.res);
     if (tid == 0) a.part[cta * 8 + 0] = rz;
   }
+  stamp(2);  // first preconditioner apply
   grid.sync();
+  stamp(3);  // barrier 2
   double rz = all_sum(0);
   if (writer) {
     sc[NYS_CG_RZNEW] = rz;
@@ -512,10 +536,13 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
         }
       }
       vv = cp_block_sum(pp, sh);  // ||p||^2, identical in every CTA
+      stamp(4);  // direction
       const double vav = hvp_rows(vr);
       if (tid == 0) a.part[cta * 8 + 1] = vav;
     }
+    stamp(5);  // rows of A
     grid.sync();
+    stamp(6);  // barrier 3
     // --------------------------------------------------- alpha + STEP ----
     // p.Ap = sum_i d_i (a_i.p)^2 + shift ||p||^2  (fixed order, every CTA)
     const double pap = fma(a.shift, vv, all_sum(1));
@@ -570,7 +597,9 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
     if (a.r > 0) utw_slice(a.res);
     if (tid == 0) a.part[cta * 8 + 2] = rr;
+    stamp(7);  // step (y partial sums, x, r, U^T r)
     grid.sync();
+    stamp(8);  // barrier 4
     // ------------------------------------------------ stop test + APPLY --
     {
       const double rtot = all_sum(2);
@@ -590,7 +619,9 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       const double rzp = apply_slice(a.res);
       if (tid == 0) a.part[cta * 8 + 3] = rzp;
     }
+    stamp(9);  // stop test + preconditioner apply
     grid.sync();
+    stamp(10);  // barrier 5
     const double rz_new = all_sum(3);
     beta = rz_new / rz;  // krylov.py:89-93
     rz = rz_new;
@@ -601,8 +632,11 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
     pb ^= 1;
   }
+  stamp(11);  // stop test
   zu_slice();
   finish();
+  stamp(12);  // z/u tail + finish
+  if (probe) atomicAdd(&g_cp_probe_cnt, 1ull);
 }
 
 struct CpPlan {
@@ -708,6 +742,8 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
   a.S = pl.S;
   a.has_head = head != nullptr;
   a.u_smem = pl.u_smem;
+  static const int probe = getenv("NYS_CP_PROBE") ? atoi(getenv("NYS_CP_PROBE")) : 0;
+  a.probe = probe;
   a.order_in = pb->order_in;
   a.order_out = pb->order_out;
   if (head) a.h = *head;
@@ -745,3 +781,14 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
 }
 
 }  // namespace nys
+
+// development: read (and clear) the accumulated phase times of the probe, ns
+extern "C" int nys_debug_cp_probe(unsigned long long* acc16, unsigned long long* count) {
+  if (cudaMemcpyFromSymbol(acc16, nys::g_cp_probe_acc, 16 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemcpyFromSymbol(count, nys::g_cp_probe_cnt, sizeof(unsigned long long)) != cudaSuccess)
+    return NYS_ERR_CUDA;
+  unsigned long long z[17] = {};
+  cudaMemcpyToSymbol(nys::g_cp_probe_acc, z, 16 * sizeof(unsigned long long));
+  cudaMemcpyToSymbol(nys::g_cp_probe_cnt, z, sizeof(unsigned long long));
+  return NYS_OK;
+}

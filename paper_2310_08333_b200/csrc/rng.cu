@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kChunksPerTile)
 tile_write_kernel(const uint8_t* __restrict__ L, const double* __restrict__ V, int64_t Q,
                   const int* __restrict__ chunk_exit, const int* __restrict__ chunk_cnt,
                   const int* __restrict__ tile_entry, const int64_t* __restrict__ tile_base,
-                  int64_t count, double* __restrict__ out) {
+                  int64_t count, double* __restrict__ out, int64_t* __restrict__ consumed) {
   __shared__ int entry[kChunksPerTile];
   __shared__ int64_t base[kChunksPerTile];
   __shared__ int cx_s[kChunksPerTile * kE];
@@ -315,6 +315,9 @@ tile_write_kernel(const uint8_t* __restrict__ L, const double* __restrict__ V, i
     if (l == kUnknown) break;
     out[j++] = V[q];
     q += l;
+    // the thread writing the last sample records the draws it ended at: the
+    // stream continues there (pieces of one long stream chain exactly)
+    if (j == count && consumed) *consumed = q;
   }
 }
 
@@ -343,7 +346,7 @@ static GaussPlan gauss_plan(int64_t count) {
   p.off_tiles = take(p.ntiles * sizeof(TileMap));
   p.off_te = take(p.ntiles * 4);
   p.off_tb = take(p.ntiles * 8);
-  p.off_total = take(8);
+  p.off_total = take(16);  // [total samples resolved, draws consumed by `count` samples]
   p.bytes = off + 256;
   return p;
 }
@@ -360,7 +363,16 @@ __global__ void gauss_flag_kernel(const int64_t* total, int64_t count, int* flag
 }
 
 static int gaussian_impl(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
-                         double* out, int* flag_dev, void* ws, size_t ws_bytes, cudaStream_t st);
+                         double* out, int* flag_dev, void* ws, size_t ws_bytes, cudaStream_t st,
+                         int64_t* draws = nullptr);
+
+extern "C" int nys_gaussian_draws_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                                      int64_t count, double* out, void* ws, size_t ws_bytes, int64_t* draws,
+                                      void* stream) {
+  if (count <= 0 || !draws) return NYS_ERR_ARG;
+  return gaussian_impl(state_hi, state_lo, inc_hi, inc_lo, count, out, nullptr, ws, ws_bytes, as_stream(stream),
+                       draws);
+}
 
 extern "C" int nys_gaussian_async_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                                       int64_t count, double* out, int* flag_dev, void* ws, size_t ws_bytes,
@@ -377,7 +389,8 @@ extern "C" int nys_gaussian_f64(uint64_t state_hi, uint64_t state_lo, uint64_t i
 }
 
 static int gaussian_impl(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t count,
-                         double* out, int* flag_dev, void* ws, size_t ws_bytes, cudaStream_t st) {
+                         double* out, int* flag_dev, void* ws, size_t ws_bytes, cudaStream_t st,
+                         int64_t* draws) {
   const GaussPlan p = gauss_plan(count);
   if (ws_bytes < p.bytes) return NYS_ERR_WORKSPACE;
   char* w = reinterpret_cast<char*>(ws);
@@ -411,16 +424,19 @@ static int gaussian_impl(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, 
   }
   tile_resolve_kernel<<<1, 256, rsm, st>>>(tiles, L, p.ntiles, p.Q, te, tb, total);
   NYS_CHECK_LAUNCH();
-  tile_write_kernel<<<(unsigned)p.ntiles, kChunksPerTile, 0, st>>>(L, V, p.Q, cx, cc, te, tb, count, out);
+  tile_write_kernel<<<(unsigned)p.ntiles, kChunksPerTile, 0, st>>>(L, V, p.Q, cx, cc, te, tb, count, out,
+                                                                    total + 1);
   NYS_CHECK_LAUNCH();
   if (flag_dev) {  // deferred check (the caller reads the flag with its next sync)
     gauss_flag_kernel<<<1, 32, 0, st>>>(total, count, flag_dev);
     NYS_CHECK_LAUNCH();
     return NYS_OK;
   }
-  int64_t tot = 0;
-  if (cudaMemcpyAsync(&tot, total, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) return NYS_ERR_CUDA;
+  int64_t tot2[2] = {0, 0};
+  if (cudaMemcpyAsync(tot2, total, 16, cudaMemcpyDeviceToHost, st) != cudaSuccess) return NYS_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return NYS_ERR_CUDA;
+  const int64_t tot = tot2[0];
+  if (draws) *draws = tot2[1];
   // the margin (3%) is ~400 standard deviations above the expected rejection
   // count; an exhausted buffer would mean a broken stream, not bad luck
   return (tot >= count) ? NYS_OK : NYS_ERR_NONFINITE;

@@ -104,7 +104,8 @@ def boxqp_data(N, n, seed):
 def cfg5_block(j, rows_per_block=12500, n=200000):
     """Config 5 row block j (of 8): A block then its noise from default_rng([4, j])."""
     g = np.random.default_rng([4, j])
-    Ab = g.standard_normal((rows_per_block, n)) * (1.0 / np.sqrt(100000))
+    Ab = g.standard_normal((rows_per_block, n))
+    Ab *= 1.0 / np.sqrt(100000)  # in place: same values as the product, half the peak memory
     noise = 0.01 * g.standard_normal(rows_per_block)
     return Ab, noise
 

@@ -309,6 +309,19 @@ class Kernels:
         check(self.L.nys_gaussian_f64(s >> 64, s & m64, inc >> 64, inc & m64, count, out.data_ptr(),
                                       ws.data_ptr(), ws.numel(), self.sp), "gaussian")
 
+    def gaussian_stream(self, state: int, inc: int, out: torch.Tensor) -> int:
+        """out <- the next out.numel() standard normals of the NumPy PCG64 stream at
+        (state, inc); returns the 64-bit draws they consumed (the stream continues
+        at state advanced by that many steps)."""
+        m64 = (1 << 64) - 1
+        count = out.numel()
+        ws = self.workspace("gauss_stream", self.L.nys_gaussian_workspace(count))
+        draws = C.c_int64(0)
+        self.launches += 1
+        check(self.L.nys_gaussian_draws_f64(state >> 64, state & m64, inc >> 64, inc & m64, count, out.data_ptr(),
+                                            ws.data_ptr(), ws.numel(), C.byref(draws), self.sp), "gaussian")
+        return int(draws.value)
+
     def orthonormalize(self, Om, Q) -> None:
         n, s = Om.shape
         ws = self.workspace("sketch", self.L.nys_orthonormalize_workspace(n, s))

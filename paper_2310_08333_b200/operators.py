@@ -151,6 +151,24 @@ class DenseOperator(LinearOperator):
         shape = (self._dev_full.shape if self._dev_full is not None else self.a.shape)
         super().__init__(shape[1], shape[0])
         self._shards: dict = {}
+        self._local = None  # (row_start, row_stop) when only a row block is resident
+
+    @classmethod
+    def from_local_rows(cls, a_local: torch.Tensor, rows_global: int, row_start: int) -> "DenseOperator":
+        """A rows_global x n operator of which this process holds only rows
+        [row_start, row_start + a_local.shape[0]) in HBM (config 5: every rank
+        generates its own row blocks, BASELINE.json configs[4]).  The solve's
+        shard must be exactly that row range."""
+        if not (isinstance(a_local, torch.Tensor) and a_local.is_cuda and a_local.ndim == 2):
+            raise DimensionMismatchError("local rows must be a 2-d CUDA tensor")
+        op = cls.__new__(cls)
+        op.a = None
+        op._dev_full = None
+        LinearOperator.__init__(op, a_local.shape[1], rows_global)
+        op._shards = {}
+        op._local = (row_start, row_start + a_local.shape[0])
+        op._shards[(row_start, row_start + a_local.shape[0], str(a_local.device))] = a_local.contiguous()
+        return op
 
     # -- device data ---------------------------------------------------------
     def device_rows(self, shard: Optional[Shard] = None, device=None) -> torch.Tensor:
@@ -161,6 +179,9 @@ class DenseOperator(LinearOperator):
             device = torch.device("cuda", torch.cuda.current_device())
         key = (shard.row_start, shard.row_stop, str(device))
         t = self._shards.get(key)
+        if t is None and self._local is not None:
+            raise DimensionMismatchError(f"rows {self._local} are resident here, the solve's shard is "
+                                         f"[{shard.row_start}, {shard.row_stop})")
         if t is None:
             if self._dev_full is not None:
                 t = self._dev_full[shard.row_start:shard.row_stop].to(device)

@@ -61,6 +61,17 @@ def _cfg(c):
     return dict(loss=d.loss, A=d.A, b=d.b, lambda1=d.lambda1, lambda2=d.lambda2)
 
 
+def _cfg5_shard(j=0):
+    """Config 5's row block j (12500 x 200000, 20 GB): exactly the rows one GPU
+    holds in the 8-GPU run, solved as a standalone LASSO with its own lambda
+    (0.1 ||A_j' b_j||_inf) - the per-GPU size of config 5 at a size the CPU
+    reference finishes in ~15 min."""
+    Ab, noise = datagen.cfg5_block(j)
+    b = Ab @ datagen.cfg5_truth() + noise
+    lam = 0.1 * float(np.max(np.abs(Ab.T @ b)))
+    return dict(loss="square", A=Ab, b=b, lambda1=lam, lambda2=0.0)
+
+
 # name: (problem builder, options dict)
 SOLVE_CASES = {
     "lasso_small": (lambda: _ml_small("square", 120, 200, 11), dict(sketch_rank=10, rng_seed=11)),
@@ -77,13 +88,14 @@ SOLVE_CASES = {
     "cfg3": (lambda: _cfg(3), dict(sketch_rank=100, rng_seed=2)),
     "cfg2": (lambda: _cfg(2), dict(sketch_rank=100, rng_seed=1)),
     "cfg4": (lambda: _cfg(4), dict(sketch_rank=200, rng_seed=3)),
+    "cfg5_shard": (lambda: _cfg5_shard(0), dict(sketch_rank=300, rng_seed=4)),
 }
 
 # tolerances of the configs: eps_abs = eps_rel = eps_dual_gap = 1e-4 (BASELINE.json)
 BASE_OPTIONS = dict(eps_abs=1e-4, eps_rel=1e-4, eps_dual_gap=1e-4)
 
-# cases the default generator run produces (cfg4 needs ~10 min of CPU: --big)
-DEFAULT_SOLVES = [k for k in SOLVE_CASES if k != "cfg4"]
+# cases the default generator run produces (cfg4 / cfg5_shard need 10-20 min of CPU: --only)
+DEFAULT_SOLVES = [k for k in SOLVE_CASES if k not in ("cfg4", "cfg5_shard")]
 
 
 def options_for(name):

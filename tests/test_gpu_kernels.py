@@ -332,3 +332,24 @@ def test_sketch_low_rank_operator(rank):
     else:
         # A_hat <= M in the Loewner order (test_sketch.py:57-67)
         assert np.linalg.eigvalsh(M - A_hat).min() >= -1e-8 * scale
+
+
+@pytest.mark.parametrize("piece", [1000, 7919, 1 << 26])
+def test_cfg5_block_generated_in_hbm_matches_host(kx, piece):
+    """Config 5's row blocks generated on the GPU (devgen.py) equal the host
+    recipe datagen.cfg5_block, including the noise drawn after the block; the
+    pieces of one long stream chain exactly (draws consumed per piece)."""
+    from paper_2310_08333_b200 import datagen, devgen
+
+    rows, n = 6, 5000
+    out = kx.empty(rows, n)
+    noise = devgen.cfg5_block_into(kx, 3, out, rows, n, piece)
+    A_ref, noise_ref = datagen.cfg5_block(3, rows, n)
+    got = out.cpu().numpy()
+    assert (got != A_ref).sum() <= 1
+    np.testing.assert_allclose(got, A_ref, rtol=1e-15, atol=0)
+    np.testing.assert_allclose(noise.cpu().numpy(), noise_ref, rtol=1e-15, atol=0)
+    # the stacked generator with b = A x_true + noise (x_true from the host recipe)
+    A2, b2, xt = devgen.cfg5_device(kx, [3], rows, n, piece)
+    assert torch.equal(A2, out)
+    np.testing.assert_allclose(b2.cpu().numpy(), A_ref @ xt.cpu().numpy() + noise_ref, rtol=1e-12, atol=1e-14)

@@ -131,3 +131,35 @@ def test_unsupported_problem_raises():
 
     with pytest.raises(nys.CapabilityError):
         nys.solve(nys.lasso_problem(sp.eye(5).tocsr(), np.ones(5), 0.1))
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(__file__), "golden", "solve_cfg5_shard.npz")),
+                    reason="config-5 shard golden not generated")
+def test_solve_config5_shard_lasso():
+    """Config 5's row block 0 (12500 x 200000, 20 GB: the rows one GPU holds in
+    the 8-GPU run) against the reference's own solve of the same rows.  The
+    block is generated in HBM (devgen.py, the host recipe's exact stream), so
+    b and lambda are formed on the device (roundoff-level differences from
+    the host's BLAS, far inside the parity bar)."""
+    import torch
+
+    import paper_2310_08333_b200 as nys
+    from paper_2310_08333_b200 import devgen
+    from paper_2310_08333_b200.kernels import get_kernels
+
+    kx = get_kernels()
+    gold = load_golden("solve_cfg5_shard.npz")
+    A, b, _ = devgen.cfg5_device(kx, [0])
+    atb = kx.empty(1, A.shape[1])
+    kx.gemvT(A, b.view(1, -1).contiguous(), atb)
+    lam = 0.1 * float(atb.abs().max())
+    prob = nys.MLProblem(nys.builtin_loss("square"), nys.DenseOperator(A), b.cpu().numpy(), lam, 0.0)
+    res = nys.solve(prob, nys.SolverOptions(**cases.options_for("cfg5_shard")))
+    assert res.status.value == str(gold["status"]), (res.status, gold["status"])
+    assert abs(res.iterations - int(gold["iterations"])) <= 2, (res.iterations, int(gold["iterations"]))
+    assert abs(res.objective - float(gold["objective"])) <= 1e-6 * abs(float(gold["objective"]))
+    assert rel(res.x, gold["x"]) <= 1e-5, rel(res.x, gold["x"])
+    assert rel(res.z, gold["z"]) <= 1e-5, rel(res.z, gold["z"])
+    del A, prob
+    torch.cuda.empty_cache()

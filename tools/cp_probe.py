@@ -1,0 +1,37 @@
+"""Phase times of the persistent PCG kernel over one config-2 solve
+(NYS_CP_PROBE=1: CTA 0 stamps %globaltimer at every phase boundary).
+
+    NYS_CP_PROBE=1 python tools/cp_probe.py [config]
+"""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2310_08333_b200 as nys  # noqa: E402
+from paper_2310_08333_b200 import _lib  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+d, opts = bench.build_problem(cfg)
+A = torch.from_numpy(d.A).cuda()
+prob = bench.make_gpu_problem(d, A)
+nys.solve(prob, opts)
+L = _lib.lib()
+acc = (C.c_ulonglong * 16)()
+cnt = C.c_ulonglong(0)
+L.nys_debug_cp_probe(acc, C.byref(cnt))
+res = nys.solve(prob, opts)
+L.nys_debug_cp_probe(acc, C.byref(cnt))
+names = ["head + U^T r0", "barrier 1", "first precond apply", "barrier 2", "direction", "rows of A (HVP)",
+         "barrier 3", "step (ysum, x, r, U^T r)", "barrier 4", "stop + precond apply", "barrier 5", "stop test",
+         "z/u tail + finish"]
+n = max(cnt.value, 1)
+tot = sum(acc[:13])
+print(f"launches {cnt.value}, iterations {res.iterations}, CG iterations {sum(h.cg_iters for h in res.history)}")
+for i, nm in enumerate(names):
+    print(f"{nm:28s} {acc[i] / n / 1e3:8.2f} us/launch  {100 * acc[i] / max(tot, 1):5.1f}%")
+print(f"{'total':28s} {tot / n / 1e3:8.2f} us/launch")
