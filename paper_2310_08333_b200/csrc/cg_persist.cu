@@ -62,6 +62,7 @@ struct CgPersistArgs {
   int has_head;       // run the ADMM head (nys_admm_head) as the prologue
   int u_smem;         // stage this CTA's rows of U in shared memory
   int probe;               // development timing probe (NYS_CP_PROBE)
+  int no_early_prefetch;   // development: no speculative first rows before the prologue
   const double* order_in;  // row order of the previous pass over A (NULL: ascending first)
   double* order_out;       // row order of this solve's last pass
   nys_admm_head h;
@@ -130,12 +131,14 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);                        // S x W
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)a.S * a.W);    // S
-  double* red = reinterpret_cast<double*>(full + a.S);                       // 2 x 16
+  uint64_t* ubar = full + a.S;                                               // U slice arrival
+  double* red = reinterpret_cast<double*>(full + ((a.S + 2) & ~1));          // 2 x 16 (16-B aligned)
   double* sh = red + 32;                                                     // 32
   double* csh = sh + 32;                                                     // coef (r <= 512)
   double* ys = csh + 520;                                                    // slice sums
-  double* scr = ys + 112;                                                    // colsum scratch (512)
-  double* us = scr + 512;                                                    // U rows of the slice
+  double* rsl = ys + 112;  // CG residual of the slice: the preconditioner passes read it from here
+  double* scr = rsl + 112;                                                   // colsum scratch (1024)
+  double* us = scr + 1024;                                                   // U rows of the slice
   __shared__ double s_bcast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool probe = a.probe && blockIdx.x == 0 && threadIdx.x == 0;
@@ -156,7 +159,12 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   // the slice's rows of U go to shared memory asynchronously (LDGSTS); both
   // preconditioner passes read them from there (waited for before the first)
   const bool ush = a.u_smem && a.r > 0;
-  if (ush) {
+  // contiguous U rows (ldu == r): one TMA bulk copy of the slice, issued after
+  // the gate check; otherwise 8-byte cp.async per element from here
+  const unsigned ubytes = (ush && c1 > c0) ? (unsigned)((c1 - c0) * a.r * 8) : 0u;
+  const bool utma = ush && a.ldu == a.r && ubytes > 0 && (ubytes & 15) == 0 &&
+                    (((uintptr_t)(a.U + c0 * a.r)) & 15) == 0;
+  if (ush && !utma) {
     const int tot = (int)(c1 - c0) * a.r;
     for (int t = tid; t < tot; t += kCpThreads) {
       const int ii = t / a.r, j = t - ii * a.r;
@@ -234,9 +242,14 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   };
   if (tid == 0) {
     for (int q = 0; q < a.S; ++q) mbar_init(&full[q], 1);
+    if (utma) mbar_init(ubar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (utma) {
+      mbar_expect_tx(ubar, ubytes);
+      tma_load_1d(us, a.U + c0 * a.r, ubytes, ubar);
+    }
   }
-  prefetch(last_dir ^ 1);
+  if (!a.no_early_prefetch) prefetch(last_dir ^ 1);
   // end of the solve: the speculative first rows of a next pass must land
   // before the CTA exits; record the order of the last pass
   auto finish = [&]() {
@@ -284,9 +297,11 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       const double ri = __dadd_rn(bb, -__dadd_rn(hx, __dmul_rn(h.shift, xi)));
       h.rhs[i] = bb;
       h.r[i] = ri;
+      rsl[i - c0] = ri;
       sb = fma(bb, bb, sb);
       sr = fma(ri, ri, sr);
     }
+    stamp(13);  // head loop
     sb = cp_block_sum(sb, sh);
     sr = cp_block_sum(sr, sh);
     if (tid == 0) {
@@ -297,6 +312,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     tol = cp_tol(a);
     b2 = sc[NYS_CG_B2];
     res2 = sc[NYS_CG_RES2];
+    for (int64_t i = c0 + tid; i < c1; i += kCpThreads) rsl[i - c0] = a.res[i];
   }
   __syncthreads();
 
@@ -321,6 +337,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
 #pragma unroll
     for (int k = 0; k < K; ++k) yr[k] = make_double2(0.0, 0.0);
     double vav = 0.0;
+    if (pre_dir < 0) prefetch(last_dir ^ 1);
     const int dir = pre_dir;
     for (int64_t it = 0; it < nrows_mine; ++it) {
       const int64_t g = g0 + it;
@@ -377,19 +394,55 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   // all threads: G groups with independent loads in flight, combined in a
   // fixed order through the (idle) ring.  Valid in every thread after the call.
   auto colsum = [&](const double* P, int64_t ld, int cnt, int64_t col0, int ncols, double* out) {
-    const int G = ncols > 0 ? tmax(1, tmin(16, kCpThreads / ncols)) : 1;
+    // G groups of ncols / 2 threads (16-byte loads of column pairs); group g
+    // sums the contiguous partials [g per, g per + per) with all of its loads
+    // in flight at once (one L2 round trip when per <= 16), then the G group
+    // sums are combined in a fixed order through the (idle) scratch.
+    const bool pairs = ((ncols | col0 | ld) & 1) == 0 && (((uintptr_t)P) & 15) == 0;
+    const int nc = pairs ? ncols / 2 : ncols;  // loaders per group
+    const int G = nc > 0 ? tmax(1, tmin(tmin(32, kCpThreads / nc), 1024 / tmax(ncols, 1))) : 1;  // scr: 1024
+    const int per = (cnt + G - 1) / G;
     __syncthreads();
-    if (tid < G * ncols) {
-      const int col = tid % ncols, g = tid / ncols;
-      const double* pc = P + col0 + col;
-      double sv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // 8 load chains in flight
-      int q = g;
-      for (; q + 7 * G < cnt; q += 8 * G) {
+    if (tid < G * nc) {
+      const int c = tid % nc, g = tid / nc;
+      const int q0 = g * per, q1 = tmin(cnt, q0 + per);
+      double2 t = make_double2(0.0, 0.0);
+      if (pairs && per <= 16) {
+        const double* pc = P + col0 + 2 * c;
+        double2 v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) sv[u] += pc[(int64_t)(q + u * G) * ld];
+        for (int u = 0; u < 16; ++u)
+          v[u] = (q0 + u < q1) ? *reinterpret_cast<const double2*>(pc + (int64_t)(q0 + u) * ld)
+                               : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int w = 8; w >= 1; w >>= 1)  // fixed pairwise tree
+#pragma unroll
+          for (int u = 0; u < w; ++u) {
+            v[u].x += v[u + w].x;
+            v[u].y += v[u + w].y;
+          }
+        t = v[0];
+      } else {
+        const int col = pairs ? 2 * c : c;
+        for (int h = 0; h < (pairs ? 2 : 1); ++h) {
+          const double* pc = P + col0 + col + h;
+          double sv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // 8 load chains in flight
+          int q = q0;
+          for (; q + 7 < q1; q += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sv[u] += pc[(int64_t)(q + u) * ld];
+          }
+          for (; q < q1; ++q) sv[0] += pc[(int64_t)q * ld];
+          const double tt = ((sv[0] + sv[1]) + (sv[2] + sv[3])) + ((sv[4] + sv[5]) + (sv[6] + sv[7]));
+          if (h == 0) t.x = tt; else t.y = tt;
+        }
       }
-      for (; q < cnt; q += G) sv[0] += pc[(int64_t)q * ld];
-      scr[g * ncols + col] = ((sv[0] + sv[1]) + (sv[2] + sv[3])) + ((sv[4] + sv[5]) + (sv[6] + sv[7]));
+      if (pairs) {
+        scr[g * ncols + 2 * c] = t.x;
+        scr[g * ncols + 2 * c + 1] = t.y;
+      } else {
+        scr[g * ncols + c] = t.x;
+      }
     }
     __syncthreads();
     for (int col = tid; col < ncols; col += kCpThreads) {
@@ -402,7 +455,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   // this CTA's share of h = U^T w over its slice -> hpart[cta]
   // (thread j: four fixed-order chains over the slice's rows; w of the slice
   // was written by this CTA before the last barrier)
-  auto utw_slice = [&](const double* w) {
+  auto utw_slice = [&]() {
     const int64_t len = c1 - c0;
     for (int j = tid; j < a.r; j += kCpThreads) {
       const double* uj = ush ? us + j : a.U + c0 * a.ldu + j;
@@ -410,12 +463,12 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       int64_t q = 0;
       for (; q + 3 < len; q += 4) {
-        s0 = fma(uj[q * ld], w[c0 + q], s0);
-        s1 = fma(uj[(q + 1) * ld], w[c0 + q + 1], s1);
-        s2 = fma(uj[(q + 2) * ld], w[c0 + q + 2], s2);
-        s3 = fma(uj[(q + 3) * ld], w[c0 + q + 3], s3);
+        s0 = fma(uj[q * ld], rsl[q], s0);
+        s1 = fma(uj[(q + 1) * ld], rsl[q + 1], s1);
+        s2 = fma(uj[(q + 2) * ld], rsl[q + 2], s2);
+        s3 = fma(uj[(q + 3) * ld], rsl[q + 3], s3);
       }
-      for (; q < len; ++q) s0 = fma(uj[q * ld], w[c0 + q], s0);
+      for (; q < len; ++q) s0 = fma(uj[q * ld], rsl[q], s0);
       a.hpart[(int64_t)cta * a.r + j] = (s0 + s1) + (s2 + s3);
     }
   };
@@ -432,7 +485,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   };
   // z (slice) = U coef + w (Eq. (11) second pass, coef in shared memory);
   // returns the w.z partial of the slice (every thread)
-  auto apply_slice = [&](const double* w) -> double {
+  auto apply_slice = [&]() -> double {
     double acc = 0.0;
     if (a.r > 0) {
       for (int64_t i = c0 + warp; i < c1; i += kCpWarps) {
@@ -441,15 +494,15 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
         for (int j = lane; j < a.r; j += 32) s2 = fma(ui[j], csh[j], s2);
         s2 = warp_sum(s2);
         if (lane == 0) {
-          const double zi = __dadd_rn(s2, w[i]);
+          const double zi = __dadd_rn(s2, rsl[i - c0]);
           a.z[i] = zi;
-          acc = fma(w[i], zi, acc);
+          acc = fma(rsl[i - c0], zi, acc);
         }
       }
     } else {
       for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
-        a.z[i] = w[i];
-        acc = fma(w[i], w[i], acc);
+        a.z[i] = rsl[i - c0];
+        acc = fma(rsl[i - c0], rsl[i - c0], acc);
       }
     }
     return cp_block_sum(acc, sh);
@@ -457,10 +510,11 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
 
   // ------------------------------- begin + first preconditioning ----
   // (the head's r0 slice and the U^T r0 partials come from the same phase)
-  if (ush) asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (utma) mbar_wait(ubar, 0);
+  else if (ush) asm volatile("cp.async.wait_all;\n" ::: "memory");
   if (a.r > 0) {
     __syncthreads();
-    utw_slice(a.res);
+    utw_slice();
   }
   stamp(0);  // head + U^T r0 partials
   if (a.has_head || a.r > 0) grid.sync();
@@ -494,9 +548,11 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       return;
     }
   }
+  stamp(14);  // all_sum x2 + stop test
   if (a.r > 0) make_coef();
+  stamp(15);  // coef (colsum of the U^T r partials)
   {
-    const double rz = apply_slice(a.res);
+    const double rz = apply_slice();
     if (tid == 0) a.part[cta * 8 + 0] = rz;
   }
   stamp(2);  // first preconditioner apply
@@ -567,8 +623,9 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
         const double api = fma(a.shift, pc[i], ys[i - c0]);
         a.Ap[i] = api;
         a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, pc[i]));
-        const double ri = __dadd_rn(a.res[i], -__dmul_rn(alpha, api));
+        const double ri = __dadd_rn(rsl[i - c0], -__dmul_rn(alpha, api));
         a.res[i] = ri;
+        rsl[i - c0] = ri;
         acc = fma(ri, ri, acc);
       }
       rr = cp_block_sum(acc, sh);
@@ -591,11 +648,12 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
         a.Ap[i] = axi;
         const double ri = __dadd_rn(a.b[i], -axi);
         a.res[i] = ri;
+        rsl[i - c0] = ri;
         acc = fma(ri, ri, acc);
       }
       rr = cp_block_sum(acc, sh);
     }
-    if (a.r > 0) utw_slice(a.res);
+    if (a.r > 0) utw_slice();
     if (tid == 0) a.part[cta * 8 + 2] = rr;
     stamp(7);  // step (y partial sums, x, r, U^T r)
     grid.sync();
@@ -616,7 +674,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
     if (a.r > 0) make_coef();
     {
-      const double rzp = apply_slice(a.res);
+      const double rzp = apply_slice();
       if (tid == 0) a.part[cta * 8 + 3] = rzp;
     }
     stamp(9);  // stop test + preconditioner apply
@@ -657,10 +715,10 @@ static CpPlan cp_plan(const nys_cg_problem* pb) {
   if (p.K > kCpMaxK) return p;
   p.MC = pb->r <= 128 ? 4 : (pb->r <= 256 ? 8 : 16);
   const size_t row_bytes = (size_t)p.W * 8;
-  const size_t extra = 64 * 8 + (size_t)(520 + 112 + 512) * 8 + 1024;  // red, sh, csh, slice sums, scratch
+  const size_t extra = 64 * 8 + (size_t)(520 + 112 + 112 + 1024) * 8 + 1024;  // red, sh, csh, slice sums, scratch
   p.S = (int)tmin<int64_t>(4, (kCpSmemBudget - extra) / row_bytes);
   if (p.S < 2) return p;
-  p.smem = (size_t)p.S * row_bytes + (size_t)p.S * 8 + extra;
+  p.smem = (size_t)p.S * row_bytes + (size_t)(p.S + 2) * 8 + extra;
   const int64_t slice = ((pb->n + kNumSMs - 1) / kNumSMs + 1) & ~1ll;
   const size_t ubytes = (size_t)slice * (pb->r > 0 ? pb->r : 0) * 8;
   p.u_smem = pb->r > 0 && p.smem + ubytes <= (size_t)kCpSmemBudget;
@@ -744,6 +802,8 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
   a.u_smem = pl.u_smem;
   static const int probe = getenv("NYS_CP_PROBE") ? atoi(getenv("NYS_CP_PROBE")) : 0;
   a.probe = probe;
+  static const int nopf = getenv("NYS_CP_NOPREFETCH") ? 1 : 0;
+  a.no_early_prefetch = nopf;
   a.order_in = pb->order_in;
   a.order_out = pb->order_out;
   if (head) a.h = *head;

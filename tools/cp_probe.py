@@ -26,12 +26,14 @@ cnt = C.c_ulonglong(0)
 L.nys_debug_cp_probe(acc, C.byref(cnt))
 res = nys.solve(prob, opts)
 L.nys_debug_cp_probe(acc, C.byref(cnt))
-names = ["head + U^T r0", "barrier 1", "first precond apply", "barrier 2", "direction", "rows of A (HVP)",
-         "barrier 3", "step (ysum, x, r, U^T r)", "barrier 4", "stop + precond apply", "barrier 5", "stop test",
-         "z/u tail + finish"]
+names = ["head: block sums, U wait, U^T r0", "barrier 1", "first precond: apply_slice", "barrier 2",
+         "direction", "rows of A (HVP)", "barrier 3", "step (ysum, x, r, U^T r)", "barrier 4",
+         "stop + precond apply", "barrier 5", "stop test", "z/u tail + finish", "head loop (gate..rhs, r0)",
+         "first precond: all_sum x2 + stop", "first precond: coef colsum"]
 n = max(cnt.value, 1)
-tot = sum(acc[:13])
+tot = sum(acc[:16])
 print(f"launches {cnt.value}, iterations {res.iterations}, CG iterations {sum(h.cg_iters for h in res.history)}")
-for i, nm in enumerate(names):
-    print(f"{nm:28s} {acc[i] / n / 1e3:8.2f} us/launch  {100 * acc[i] / max(tot, 1):5.1f}%")
-print(f"{'total':28s} {tot / n / 1e3:8.2f} us/launch")
+for i in (13, 0, 1, 14, 15, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12):
+    nm = names[i]
+    print(f"{nm:36s} {acc[i] / n / 1e3:8.2f} us/launch  {100 * acc[i] / max(tot, 1):5.1f}%")
+print(f"{'total':36s} {tot / n / 1e3:8.2f} us/launch")
