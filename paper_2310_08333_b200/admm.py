@@ -46,7 +46,8 @@ from .errors import CapabilityError, DataError, NotSPDError, NumericalError
 from .krylov import CgReport, CgWork, cg_tolerance, pcg_batched, pcg_device
 from .operators import DenseOperator, IdentityOperator, to_device
 from .problems import GenericProblem, lower
-from .sketch import NystromPreconditioner, NystromSketch, default_sketch_rank, raw_test_matrix, sketch_device, sketch_width
+from .sketch import (NystromPreconditioner, NystromSketch, default_sketch_rank, raw_test_matrix, sketch_device,
+                     sketch_device_launch, sketch_width)
 
 PENALTY_ADAPT_CUTOFF = 1000  # admm.py:29
 DELTA_WINDOW = 25  # admm.py:33
@@ -370,7 +371,9 @@ class _Engine:
         return lambda v, out, rdot, rz: kx.precond_apply(self.U, self.lam, self.pc_nu, v, out, rdot, rz)
 
     # ----------------------------------------------------------- sketch --
-    def sketch(self, seed: int, omega: Optional[np.ndarray] = None) -> None:
+    def _sketch_target(self):
+        """(cols, reduce): Y = H Q for the sketch target and the all-reduce of
+        Y's row-shard partials (None unsharded)."""
         kx = self.kx
         n = self.n
         if self.is_ml:
@@ -398,11 +401,29 @@ class _Engine:
                 return Y
 
             reduce = None
-        U, lam = sketch_device(kx, cols, n, self.r_sk, seed, omega=omega, reduce=reduce)
+        return cols, reduce
+
+    def sketch(self, seed: int, omega: Optional[np.ndarray] = None) -> None:
+        cols, reduce = self._sketch_target()
+        U, lam = sketch_device(self.kx, cols, self.n, self.r_sk, seed, omega=omega, reduce=reduce)
         if U.shape[1] == 0:
             self.U, self.lam = None, None
         else:
             self.U, self.lam = U, lam
+        self.n_sketches += 1
+
+    def sketch_launch(self, seed: int):
+        """Enqueue the sketch of iteration k (seed rng_seed + k) right behind
+        iteration k-1 on the stream, before the host has read k-1: its input
+        (the Hessian weights at k-1's iterate) is what k-1's tail leaves on the
+        device.  None where only the synchronous sketch applies."""
+        cols, reduce = self._sketch_target()
+        if reduce is not None:
+            return None
+        return sketch_device_launch(self.kx, cols, self.n, self.r_sk, seed)
+
+    def sketch_adopt(self, launch) -> None:
+        self.U, self.lam = launch.U, launch.lam
         self.n_sketches += 1
 
     # ------------------------------------------------------------- run ---
@@ -482,6 +503,7 @@ class _Engine:
         bar_count = 0
         k_done = 0
         omega_next = None
+        early = None  # sketch of the next iteration, enqueued behind the current one
 
         for k in range(1, opts.max_iter + 1):
             if opts.time_limit is not None and time.perf_counter() - t_start > opts.time_limit:
@@ -492,9 +514,17 @@ class _Engine:
             k_done = k
             # resketch on the cadence for iterate-dependent Hessians (admm.py:545-551)
             # (never due for an iteration launched ahead, by the lookahead rule)
+            early_check = None
             if have_pc and not self.const_hess and k - last_sketch >= opts.resketch_every:
                 t0 = time.perf_counter()
-                self.sketch(opts.rng_seed + k)
+                if early is not None and early.seed == opts.rng_seed + k:
+                    # enqueued behind iteration k-1 (see below); its status is read
+                    # once iteration k is queued behind it
+                    self.sketch_adopt(early)
+                    early_check = early
+                else:
+                    self.sketch(opts.rng_seed + k)
+                early = None
                 timings.precond_s += time.perf_counter() - t0
                 self.pc_nu = nu_identity(self.rho)
                 last_sketch = k
@@ -508,9 +538,27 @@ class _Engine:
                 # test, predicated tail (z/u, data passes, norms, windows), readback
                 it = pending if pending is not None else self._issue(k, shift, list(win), opts.exact_x_solve)
                 pending = None
+                if early_check is not None and not early_check.ok():
+                    # the pipelined sketch flagged a failure (never expected for a
+                    # Hessian + shift): undo iteration k, sketch synchronously
+                    # (its fallbacks), and issue k again
+                    self._rollback(resume=True, k=k - 1)
+                    t0 = time.perf_counter()
+                    self.sketch(opts.rng_seed + k)
+                    timings.precond_s += time.perf_counter() - t0
+                    it = self._issue(k, shift, list(win), opts.exact_x_solve)
                 if lookahead and self._may_speculate(k, it, have_pc, last_sketch, rho_frozen, cycle_hits):
                     pending = self._issue(k + 1, shift, it.after, opts.exact_x_solve)
+                elif (lookahead and have_pc and not self.const_hess and k + 1 <= opts.max_iter
+                      and (k + 1) - last_sketch >= opts.resketch_every):
+                    # the next iteration resketches: enqueue the sketch now, behind
+                    # iteration k (wasted only if k terminates the solve)
+                    t0 = time.perf_counter()
+                    early = self.sketch_launch(opts.rng_seed + k + 1)
+                    timings.precond_s += time.perf_counter() - t0
                 rep, st, linsys_s, prox_s = self._retire(it, pending)
+                if early is not None and self._cg_continued:
+                    early = None  # k's CG needed more launches: the sketch saw a no-op tail
                 if pending is not None and pending.reissue is not None:
                     pending = pending.reissue
                 spec = it.slot
@@ -958,6 +1006,7 @@ class _Engine:
         lin_ms = ev[0].elapsed_time(ev[1])
         tail_ms = ev[1].elapsed_time(ev[2])
         k_last, batch = it.batch, it.batch
+        self._cg_continued = False
         max_iter = 10 * self.n
         done = int(sc[_lib.CG_DONE])
         while done == 0 and k_last < max_iter:
@@ -974,6 +1023,7 @@ class _Engine:
             lin_ms += ev[0].elapsed_time(ev[1])
             tail_ms += ev[1].elapsed_time(ev[2])
             done = int(sc[_lib.CG_DONE])
+            self._cg_continued = True
         if hasattr(kx, "timing_commit"):
             kx.timing_commit(it.tag, int(sc[_lib.CG_ITERS]) if done else k_last, int(sc[_lib.CG_NHVP]))
         if nxt is not None and k_last > it.batch:

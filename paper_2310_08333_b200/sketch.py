@@ -108,6 +108,44 @@ def sketch_device(kx, apply_cols: Callable[[torch.Tensor], torch.Tensor], n: int
     return U[:, :rr], lam[:rr]
 
 
+class SketchLaunch:
+    """A pipelined sketch enqueued on the stream with no host synchronisation:
+    its status words are copied to pinned host memory behind an event, so the
+    host can queue more work before it looks (`ok()` waits for the sketch only)."""
+
+    def __init__(self, U, lam, flags_h, event, seed):
+        self.U, self.lam, self.flags_h, self.event, self.seed = U, lam, flags_h, event, seed
+
+    def ok(self) -> bool:
+        self.event.synchronize()
+        return not bool(self.flags_h.any())
+
+
+def sketch_device_launch(kx, apply_cols: Callable[[torch.Tensor], torch.Tensor], n: int, r: int, seed: int,
+                         oversample: Optional[int] = None) -> Optional[SketchLaunch]:
+    """The pipelined branch of ``sketch_device`` without its final status read
+    (None where the pipelined path does not apply).  A flagged launch must be
+    replaced by the synchronous ``sketch_device`` (same seed)."""
+    if not (1 <= r <= n) or _TRACE is not None or not hasattr(kx, "gaussian_async"):
+        return None
+    s = sketch_width(n, r, oversample)
+    flags = torch.zeros(4, dtype=torch.int32, device=kx.device)
+    Om = kx.empty(n, s)
+    kx.gaussian_async(seed, Om, flags[0:1])
+    Q = kx.empty(n, s)
+    kx.orthonormalize_async(Om, Q, flags[1:3], r)
+    Y = apply_cols(Q).contiguous()
+    U = kx.empty(n, r)
+    lam = kx.empty(r)
+    kx.nystrom_core_async(Q, Y, U, lam, r, flags[3:4])
+    flags_h = torch.empty(4, dtype=torch.int32, pin_memory=True)
+    flags_h.copy_(flags, non_blocking=True)
+    kx.d2h += 16
+    ev = torch.cuda.Event()
+    ev.record(kx.stream)
+    return SketchLaunch(U, lam, flags_h, ev, seed)
+
+
 # development instrumentation: set to a list to collect per-stage sketch times
 _TRACE: Optional[list] = None
 
