@@ -835,6 +835,7 @@ class _Engine:
         self.snap = kx.zeros(5, n)
         self._done_ev = [torch.cuda.Event() for _ in range(2)]
         self._ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(2)]
+        self._iter_events = os.environ.get("NYS_ITER_EVENTS", "1") != "0"
         self._seq = 0
         ptr = lambda x: x.data_ptr() if x is not None else None
         self._tails, self._pbs, self._heads = [], [], []
@@ -963,11 +964,14 @@ class _Engine:
             t.inf_first, t.inf_last = after[0], after[-1]
         batch = min(16, max(2, self._last_cg + 1))
         ev = self._ev[par]
-        ev[0].record(kx.stream)
+        if self._iter_events:
+            ev[0].record(kx.stream)
         kx.admm_xupdate(h, pb, batch)  # head + PCG (one persistent kernel when it fits)
-        ev[1].record(kx.stream)
+        if self._iter_events:
+            ev[1].record(kx.stream)
         kx.admm_tail(t)
-        ev[2].record(kx.stream)
+        if self._iter_events:
+            ev[2].record(kx.stream)
         self._readback(par)
         return _Issued(k, par, slot, after, batch, self._seq, shift, exact, list(win_before))
 
@@ -1003,8 +1007,8 @@ class _Engine:
         kx, par = self.kx, it.par
         sc, st = self._read(par)
         ev = self._ev[par]
-        lin_ms = ev[0].elapsed_time(ev[1])
-        tail_ms = ev[1].elapsed_time(ev[2])
+        lin_ms = ev[0].elapsed_time(ev[1]) if self._iter_events else 0.0
+        tail_ms = ev[1].elapsed_time(ev[2]) if self._iter_events else 0.0
         k_last, batch = it.batch, it.batch
         self._cg_continued = False
         max_iter = 10 * self.n

@@ -127,6 +127,7 @@ __device__ __forceinline__ double cp_block_sum(double v, double* sh) {
 
 template <int K, int MC>
 __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs a) {
+  pdl_begin();  // chain kernel (common.cuh)
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);                        // S x W
@@ -739,10 +740,8 @@ static int cp_launch(const CpPlan& pl, const CgPersistArgs& args, cudaStream_t s
     attr = true;
   }
   CgPersistArgs a = args;
-  void* kargs[] = {(void*)&a};
   const unsigned grid = (unsigned)tmin<int64_t>(kNumSMs, a.rows);
-  if (cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kCpThreads), kargs, pl.smem, st) != cudaSuccess)
-    return NYS_ERR_CUDA;
+  if (launch_chain(fn, dim3(grid), dim3(kCpThreads), pl.smem, st, true, a) != cudaSuccess) return NYS_ERR_CUDA;
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
   return debug_sync_check(__FILE__, __LINE__) ? NYS_ERR_CUDA : NYS_OK;
 }

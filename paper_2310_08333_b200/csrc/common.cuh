@@ -7,6 +7,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <utility>
 #include "../../include/nysgpu.h"
 
 namespace nys {
@@ -136,5 +138,49 @@ __host__ __device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Programmatic dependent launch (PDL) for the per-iteration kernel chain
+// (x-update -> A{x,z} -> A^T -> epilogue -> conj -> gate -> readback -> next
+// x-update).  A chain kernel starts with pdl_begin(): it lets its successor be
+// scheduled as soon as all of its own CTAs are resident, then waits until its
+// predecessor has completed and its memory is visible (griddepcontrol.wait),
+// so the successor's launch latency and CTA ramp-up hide behind this kernel's
+// tail.  Both instructions are no-ops for kernels launched without the
+// attribute.  NYS_PDL=0 disables the attribute.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = !(getenv("NYS_PDL") && getenv("NYS_PDL")[0] == '0');
+  return on;
+}
+
+// launch `kern` with the PDL attribute (and the cooperative one when coop)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                bool coop, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  unsigned na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace nys

@@ -246,6 +246,7 @@ gemv_t_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda
               const double* __restrict__ T, int64_t ldt, double* __restrict__ out, int64_t ldo,
               int64_t rows_per_split, int direct, const double* __restrict__ pred,
               const double* __restrict__ order = nullptr) {
+  pdl_begin();  // chain kernel (common.cuh)
   if (pred && *pred != 0.0) return;
   __shared__ double tsh[K][kGemvTTile];
   // splits in descending row order when the previous pass over A ended at the
@@ -438,10 +439,14 @@ static int gemv_t_partials_k(const double* A, int64_t rows, int64_t n, int64_t l
   double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
   const int64_t strips = cdiv(n, (int64_t)kGemvTThreads * (vec ? 2 : 1));
   dim3 grid((unsigned)strips, (unsigned)splits);
+  const int64_t ldP = n;
+  const int64_t direct = 0;
   if (vec)
-    gemv_t_kernel<K, true><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt, P, n, rps, 0, pred, order);
+    launch_chain(gemv_t_kernel<K, true>, grid, dim3(kGemvTThreads), 0, st, false, A, rows, n, lda, T, ldt, P, ldP,
+                 rps, (int)direct, pred, order);
   else
-    gemv_t_kernel<K, false><<<grid, kGemvTThreads, 0, st>>>(A, rows, n, lda, T, ldt, P, n, rps, 0, pred, order);
+    launch_chain(gemv_t_kernel<K, false>, grid, dim3(kGemvTThreads), 0, st, false, A, rows, n, lda, T, ldt, P, ldP,
+                 rps, (int)direct, pred, order);
   NYS_CHECK_LAUNCH();
   *Pout = P;
   *splits_out = splits;

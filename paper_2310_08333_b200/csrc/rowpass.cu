@@ -40,6 +40,7 @@ xz_rowpass_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t
                   double* __restrict__ thx, double* __restrict__ tnu, double* __restrict__ rowsums,
                   double* part, unsigned int* counter, const double* __restrict__ pred,
                   const double* __restrict__ order) {
+  pdl_begin();  // chain kernel (common.cuh)
   if (pred && *pred != 0.0) return;
   // rows in the order opposite to the previous pass over A (L2 reuse); row
   // results are stored by position, so the order does not change them
@@ -228,8 +229,8 @@ static int rowpass_launch(const RowpassPlan& p, const double* A, int64_t rows, i
     attr[wz] = true;
   }
   const unsigned grid = (unsigned)tmin<int64_t>(kNumSMs, rows);
-  fn<<<grid, kRpThreads, p.smem, st>>>(A, rows, n, lda, x, z, b, loss, p.Wp, p.S, tg, w, thx, tnu, rowsums, part,
-                                       counter, pred, order);
+  launch_chain(fn, dim3(grid), dim3(kRpThreads), p.smem, st, false, A, rows, n, lda, x, z, b, loss, p.Wp, p.S, tg,
+               w, thx, tnu, rowsums, part, counter, pred, order);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -441,6 +441,7 @@ __global__ void ml_conj_dev_kernel(int64_t rows, int loss, const double* __restr
                                    const double* __restrict__ denom, double lambda1,
                                    const double* __restrict__ b, double* out, double* part,
                                    unsigned int* counter, const double* __restrict__ pred) {
+  pdl_begin();  // chain kernel (common.cuh)
   if (pred && *pred != 0.0) return;
   const double dn = *denom;
   if (!(dn > lambda1)) return;
@@ -458,6 +459,7 @@ __global__ void ml_conj_dev_kernel(int64_t rows, int loss, const double* __restr
 }
 
 __global__ void open_gate_kernel(double* gate, const double* __restrict__ pred) {
+  pdl_begin();  // chain kernel (common.cuh)
   if (pred && *pred != 0.0) return;
   if (threadIdx.x == 0) *gate = 1.0;
 }
@@ -505,6 +507,7 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
                    double lambda2, double rho, double lambda1, const double* __restrict__ ring, int64_t ld,
                    int cur, SlotList others, int nothers, double* out, int woff, double* part,
                    unsigned int* counter, const double* __restrict__ pred) {
+  pdl_begin();  // chain kernel (common.cuh)
   if (pred && *pred != 0.0) return;
   __shared__ double cs[4][K][kEpiCols];
   const int tid = threadIdx.x, cx = tid & (kEpiCols - 1), ch = tid >> 6;
@@ -817,6 +820,7 @@ extern "C" int nys_copy_f64(const double* src, double* dst, int64_t n, void* str
 
 __global__ void readback_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t n, double* gate,
                                 const double* __restrict__ pred) {
+  pdl_begin();  // chain kernel (common.cuh)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
   __threadfence_system();
@@ -826,8 +830,8 @@ __global__ void readback_kernel(const double* __restrict__ src, double* __restri
 extern "C" int nys_readback_f64(const double* src, double* dst, int64_t n, double* gate_next, const double* pred,
                                 void* stream) {
   if (n < 0 || (n > 0 && (!src || !dst))) return NYS_ERR_ARG;
-  readback_kernel<<<(unsigned)tmin<int64_t>(cdiv(tmax<int64_t>(n, 1), 256), 64), 256, 0, as_stream(stream)>>>(
-      src, dst, n, gate_next, pred);
+  launch_chain(readback_kernel, dim3((unsigned)tmin<int64_t>(cdiv(tmax<int64_t>(n, 1), 256), 64)), dim3(256), 0,
+               as_stream(stream), false, src, dst, n, gate_next, pred);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -1020,14 +1024,20 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       const int no = (t->ring && t->nothers > 0) ? t->nothers : 0;
       for (int j = 0; j < 16; ++j) sl.idx[j] = j < no ? t->others[j] : 0;
       const unsigned eb = (unsigned)cdiv(n, (int64_t)kEpiCols);
+      const double* Pc = P;
+      const double* uc = t->u;
+      const double* ringc = t->ring;
+      double* normsp = t->norms;
+      double* rp = red_part(t->ws_red);
+      unsigned int* rc2 = red_counter(t->ws_red);
       if (K == 3)
-        ml_epilogue_kernel<3><<<eb, 256, 0, st>>>(n, P, splits, t->AT, x, z, t->u, t->lambda2, t->rho, t->lambda1,
-                                                 t->ring, t->ring_ld, t->slot, sl, no, t->norms, (int)woff,
-                                                 red_part(t->ws_red), red_counter(t->ws_red), pred);
+        launch_chain(ml_epilogue_kernel<3>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
+                     t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
+                     pred);
       else
-        ml_epilogue_kernel<2><<<eb, 256, 0, st>>>(n, P, splits, t->AT, x, z, t->u, t->lambda2, t->rho, t->lambda1,
-                                                 t->ring, t->ring_ld, t->slot, sl, no, t->norms, (int)woff,
-                                                 red_part(t->ws_red), red_counter(t->ws_red), pred);
+        launch_chain(ml_epilogue_kernel<2>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
+                     t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
+                     pred);
       NYS_CHECK_LAUNCH();
     } else {
       if ((rc = gemv_t(t->A, t->rows, n, t->lda, t->T, t->rows, t->with_z ? 3 : 2, t->AT, n, nullptr, 0.0, nullptr,
@@ -1074,13 +1084,14 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   }
   // scaled-dual conjugate sums for the gap (problems.py:330-340), device-side c
   if (t->kind == 0 && t->with_z && t->conj_out) {
-    ml_conj_dev_kernel<<<vec_blocks(t->rows), kVecThreads, 0, st>>>(
-        t->rows, t->loss, t->T + 2 * t->rows, t->norms + 13, t->lambda1, t->b, t->conj_out, red_part(t->ws_red),
-        red_counter(t->ws_red), pred);
+    const double* nuc = t->T + 2 * t->rows;
+    const double* sc13 = t->norms + 13;
+    launch_chain(ml_conj_dev_kernel, dim3((unsigned)vec_blocks(t->rows)), dim3(kVecThreads), 0, st, false, t->rows,
+                 t->loss, nuc, sc13, t->lambda1, t->b, t->conj_out, red_part(t->ws_red), red_counter(t->ws_red), pred);
     NYS_CHECK_LAUNCH();
   }
   if (t->gate_next) {
-    open_gate_kernel<<<1, 32, 0, st>>>(t->gate_next, pred);
+    launch_chain(open_gate_kernel, dim3(1), dim3(32), 0, st, false, t->gate_next, pred);
     NYS_CHECK_LAUNCH();
   }
   return NYS_OK;
