@@ -790,7 +790,7 @@ size_t ortho_ws(int64_t n, int s) {
          8 * s * sizeof(double) + 8192;
 }
 
-// CholeskyQR2: Q = Omega R^{-1}, twice.  The fast path runs without a host
+// CholeskyQR: Q = Omega R^{-1} (one pass; see below).  The fast path runs without a host
 // sync and checks both Cholesky codes once at the end; if either pass hit a
 // numerically singular Gram matrix the careful path (per-pass checks, eigen
 // fallback) recomputes Q from Omega.
@@ -812,10 +812,19 @@ static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* w
   void* jws = ar.take<char>(jws_b);
   if (!ar.ok) return NYS_ERR_WORKSPACE;
   if (info_ext) info = info_ext;  // deferred: the caller checks the codes later
+  // One CholeskyQR pass by default: the sketch input is a Gaussian n x s
+  // matrix (n >> s), condition number ~ (1 + sqrt(s/n)) / (1 - sqrt(s/n)) <= 1.3
+  // for the configs, so one pass leaves ||Q^T Q - I|| at the 1e-15 level; the
+  // Nystrom approximation (H+nu)Q (Q^T (H+nu) Q)^-1 Q^T (H+nu) is invariant to
+  // Q -> Q R anyway.  NYS_CHOLQR_PASSES=2 restores CholeskyQR2; the careful
+  // (fallback) path always runs two.
+  static const int env_passes = getenv("NYS_CHOLQR_PASSES") ? atoi(getenv("NYS_CHOLQR_PASSES")) : 1;
+  const int passes = careful ? 2 : (env_passes == 2 ? 2 : 1);
+  if (passes == 1 && cudaMemsetAsync(info + 1, 0, sizeof(int), st) != cudaSuccess) return NYS_ERR_CUDA;
   int rc;
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = 0; pass < passes; ++pass) {
     const double* src = pass == 0 ? Om : tmp;
-    double* dst = pass == 0 ? tmp : Q;
+    double* dst = (pass == passes - 1) ? Q : tmp;
     rc = gemm(1, 0, s, s, n, 1.0, src, s, src, s, 0.0, G, s, gws, gws_b, st);
     if (rc) return rc;
     int info_h = 0;
