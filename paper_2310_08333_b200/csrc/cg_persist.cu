@@ -85,7 +85,7 @@ struct CgPersistArgs {
 
 // Development probe (NYS_CP_PROBE=1): CTA 0 stamps %globaltimer at the phase
 // boundaries of every launch and accumulates the deltas (tools/cp_probe.py).
-__device__ unsigned long long g_cp_probe_acc[16];
+__device__ unsigned long long g_cp_probe_acc[24];
 __device__ unsigned long long g_cp_probe_cnt;
 __device__ __forceinline__ unsigned long long cp_now() {
   unsigned long long t;
@@ -206,6 +206,25 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
   };
   // ---------------------------------------------------------- begin ----
+  // The head's inputs for this thread's element of the slice (slice <= 90 <
+  // kCpThreads, so at most one) are requested together with the gate word, so
+  // the begin phase costs one memory round trip instead of two.
+  const int64_t hi_ = c0 + tid;
+  const bool hmine = a.has_head && hi_ < c1;
+  double hx_ = 0.0, hz_ = 0.0, hu_ = 0.0, hxb_ = 0.0, hzb_ = 0.0, hhx_ = 0.0, hg_ = 0.0, hq_ = 0.0;
+  if (hmine) {
+    const nys_admm_head& h = a.h;
+    hx_ = h.x[hi_];
+    hz_ = h.z[hi_];
+    hu_ = h.u[hi_];
+    if (h.snap) {
+      hxb_ = h.xbar[hi_];
+      hzb_ = h.zbar[hi_];
+    }
+    hhx_ = h.hxA[hi_];
+    hg_ = h.gA[hi_];
+    if (h.q) hq_ = h.q[hi_];
+  }
   {
     const double* gp = a.has_head ? a.h.gate : a.gate;
     if (gp && *gp == 0.0) {  // previous ADMM iteration unfinished: skip the solve
@@ -280,19 +299,20 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       if (h.tol_out) *h.tol_out = tol;
     }
     double sb = 0.0, sr = 0.0;
-    for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
-      const double xi = h.x[i], zi = h.z[i], ui = h.u[i];
+    if (hmine) {
+      const int64_t i = hi_;
+      const double xi = hx_, zi = hz_, ui = hu_;
       if (h.snap) {
         h.snap[i] = xi;
         h.snap[n + i] = zi;
         h.snap[2 * n + i] = ui;
-        h.snap[3 * n + i] = h.xbar[i];
-        h.snap[4 * n + i] = h.zbar[i];
+        h.snap[3 * n + i] = hxb_;
+        h.snap[4 * n + i] = hzb_;
       }
       const double l2x = __dmul_rn(h.lambda2, xi);
-      const double hx = __dadd_rn(h.hxA[i], l2x);
-      double g = __dadd_rn(h.gA[i], l2x);
-      if (h.q) g = __dadd_rn(g, h.q[i]);
+      const double hx = __dadd_rn(hhx_, l2x);
+      double g = __dadd_rn(hg_, l2x);
+      if (h.q) g = __dadd_rn(g, hq_);
       double bb = __dadd_rn(__dadd_rn(hx, __dmul_rn(h.sigma, xi)), -g);
       bb = __dadd_rn(bb, __dmul_rn(h.rho, __dadd_rn(zi, -ui)));
       const double ri = __dadd_rn(bb, -__dadd_rn(hx, __dmul_rn(h.shift, xi)));
@@ -317,6 +337,27 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   }
   __syncthreads();
 
+  // fixed-order sums of two slots in one pass (one round trip)
+  __shared__ double s_bcast2;
+  auto all_sum2 = [&](int q1, int q2, double& o2) -> double {
+    __syncthreads();
+    if (warp == 0) {
+      double t1 = 0.0, t2 = 0.0;
+      for (int c = lane; c < nctas; c += 32) {
+        t1 += a.part[c * 8 + q1];
+        t2 += a.part[c * 8 + q2];
+      }
+      t1 = warp_sum(t1);
+      t2 = warp_sum(t2);
+      if (lane == 0) {
+        s_bcast = t1;
+        s_bcast2 = t2;
+      }
+    }
+    __syncthreads();
+    o2 = s_bcast2;
+    return s_bcast;
+  };
   // fixed-order sum over the CTAs of slot q of part (nctas x 8), in every thread
   auto all_sum = [&](int q) -> double {
     __syncthreads();
@@ -520,10 +561,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   stamp(0);  // head + U^T r0 partials
   if (a.has_head || a.r > 0) grid.sync();
   stamp(1);  // barrier 1
-  if (a.has_head) {
-    b2 = all_sum(4);
-    res2 = all_sum(5);
-  }
+  if (a.has_head) b2 = all_sum2(4, 5, res2);
   {
     const double denom = b2 > 0.0 ? sqrt(b2) : 1.0;
     const double res = sqrt(res2);
@@ -560,6 +598,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   grid.sync();
   stamp(3);  // barrier 2
   double rz = all_sum(0);
+  stamp(19);  // r.z sum
   if (writer) {
     sc[NYS_CG_RZNEW] = rz;
     sc[NYS_CG_RZ] = rz;
@@ -602,7 +641,14 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     stamp(6);  // barrier 3
     // --------------------------------------------------- alpha + STEP ----
     // p.Ap = sum_i d_i (a_i.p)^2 + shift ||p||^2  (fixed order, every CTA)
+    // this thread's element of the p and x slices, requested before the sums
+    // below so their round trips overlap (slice <= 90: one element per thread)
+    const int64_t si_ = c0 + tid;
+    const bool smine = si_ < c1;
+    const double p_si = smine ? a.p[pb][si_] : 0.0;
+    const double x_si = smine ? a.x[si_] : 0.0;
     const double pap = fma(a.shift, vv, all_sum(1));
+    stamp(16);  // step: p.Ap sum
     if (!isfinite(pap) || pap <= 0.0) {  // krylov.py:74-77
       if (writer) {
         sc[NYS_CG_PAP] = pap;
@@ -619,11 +665,13 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     double rr;
     if (!refresh) {
       colsum(a.ypart, n, nctas, c0, (int)(c1 - c0), ys);
+      stamp(17);  // step: y partial sums
       double acc = 0.0;
-      for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
-        const double api = fma(a.shift, pc[i], ys[i - c0]);
+      if (smine) {
+        const int64_t i = si_;
+        const double api = fma(a.shift, p_si, ys[i - c0]);
         a.Ap[i] = api;
-        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, pc[i]));
+        a.x[i] = __dadd_rn(x_si, __dmul_rn(alpha, p_si));
         const double ri = __dadd_rn(rsl[i - c0], -__dmul_rn(alpha, api));
         a.res[i] = ri;
         rsl[i - c0] = ri;
@@ -654,6 +702,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       }
       rr = cp_block_sum(acc, sh);
     }
+    stamp(18);  // step: x, r update + ||r||^2
     if (a.r > 0) utw_slice();
     if (tid == 0) a.part[cta * 8 + 2] = rr;
     stamp(7);  // step (y partial sums, x, r, U^T r)
@@ -682,6 +731,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     grid.sync();
     stamp(10);  // barrier 5
     const double rz_new = all_sum(3);
+    stamp(19);  // r.z sum
     beta = rz_new / rz;  // krylov.py:89-93
     rz = rz_new;
     if (writer) {
@@ -714,6 +764,8 @@ static CpPlan cp_plan(const nys_cg_problem* pb) {
   p.W = (int)pb->n;
   p.K = (int)cdiv(pb->n, (int64_t)2 * kCpThreads);
   if (p.K > kCpMaxK) return p;
+  // every slice of n / 148 columns has at most one element per thread (<= 90)
+  static_assert(((kCpMaxK * 2 * kCpThreads + kNumSMs - 1) / kNumSMs + 1) <= kCpThreads, "slice");
   p.MC = pb->r <= 128 ? 4 : (pb->r <= 256 ? 8 : 16);
   const size_t row_bytes = (size_t)p.W * 8;
   const size_t extra = 64 * 8 + (size_t)(520 + 112 + 112 + 1024) * 8 + 1024;  // red, sh, csh, slice sums, scratch
@@ -842,12 +894,12 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
 }  // namespace nys
 
 // development: read (and clear) the accumulated phase times of the probe, ns
-extern "C" int nys_debug_cp_probe(unsigned long long* acc16, unsigned long long* count) {
-  if (cudaMemcpyFromSymbol(acc16, nys::g_cp_probe_acc, 16 * sizeof(unsigned long long)) != cudaSuccess ||
+extern "C" int nys_debug_cp_probe(unsigned long long* acc24, unsigned long long* count) {
+  if (cudaMemcpyFromSymbol(acc24, nys::g_cp_probe_acc, 24 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemcpyFromSymbol(count, nys::g_cp_probe_cnt, sizeof(unsigned long long)) != cudaSuccess)
     return NYS_ERR_CUDA;
-  unsigned long long z[17] = {};
-  cudaMemcpyToSymbol(nys::g_cp_probe_acc, z, 16 * sizeof(unsigned long long));
+  unsigned long long z[25] = {};
+  cudaMemcpyToSymbol(nys::g_cp_probe_acc, z, 24 * sizeof(unsigned long long));
   cudaMemcpyToSymbol(nys::g_cp_probe_cnt, z, sizeof(unsigned long long));
   return NYS_OK;
 }

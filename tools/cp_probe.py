@@ -21,19 +21,20 @@ A = torch.from_numpy(d.A).cuda()
 prob = bench.make_gpu_problem(d, A)
 nys.solve(prob, opts)
 L = _lib.lib()
-acc = (C.c_ulonglong * 16)()
+acc = (C.c_ulonglong * 24)()
 cnt = C.c_ulonglong(0)
 L.nys_debug_cp_probe(acc, C.byref(cnt))
 res = nys.solve(prob, opts)
 L.nys_debug_cp_probe(acc, C.byref(cnt))
 names = ["head: block sums, U wait, U^T r0", "barrier 1", "first precond: apply_slice", "barrier 2",
-         "direction", "rows of A (HVP)", "barrier 3", "step (ysum, x, r, U^T r)", "barrier 4",
+         "direction (after the r.z sum)", "rows of A (HVP)", "barrier 3", "step: U^T r", "barrier 4",
          "stop + precond apply", "barrier 5", "stop test", "z/u tail + finish", "head loop (gate..rhs, r0)",
-         "first precond: all_sum x2 + stop", "first precond: coef colsum"]
+         "first precond: all_sum x2 + stop", "first precond: coef colsum", "step: p.Ap sum",
+         "step: y partial sums", "step: x, r update + ||r||^2", "r.z sum"]
 n = max(cnt.value, 1)
-tot = sum(acc[:16])
+tot = sum(acc[:20])
 print(f"launches {cnt.value}, iterations {res.iterations}, CG iterations {sum(h.cg_iters for h in res.history)}")
-for i in (13, 0, 1, 14, 15, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12):
+for i in (13, 0, 1, 14, 15, 2, 3, 19, 4, 5, 6, 16, 17, 18, 7, 8, 9, 10, 11, 12):
     nm = names[i]
     print(f"{nm:36s} {acc[i] / n / 1e3:8.2f} us/launch  {100 * acc[i] / max(tot, 1):5.1f}%")
 print(f"{'total':36s} {tot / n / 1e3:8.2f} us/launch")
