@@ -539,6 +539,14 @@ struct StripPlan {
   bool ok;
 };
 size_t hvp_strip_ws();
+struct HcPlan {
+  int W, K, S, L, nclusters;
+  size_t smem;
+  bool ok;
+};
+HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
+int hvp_cluster(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
+                const double* v, double* ypart, cudaStream_t st, const double* pred);
 StripPlan hvp_strip_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
 int hvp_strip(const StripPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
               const double* v, double* y, double shift, double* dot, void* ws, double* part,
@@ -573,6 +581,23 @@ int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const doubl
                                                  finish ? pAp : nullptr, red_part(ws), red_counter(ws), pred);
     NYS_CHECK_LAUNCH();
     return NYS_OK;
+  }
+  // wide rows, first choice: clusters of 16 CTAs split each row's columns and
+  // exchange the row totals through distributed shared memory (csrc/hvp_cluster.cu)
+  if (!plan.ok && !two_pass_only) {
+    HcPlan hp = hvp_cluster_plan(rows, n, lda, A, v);
+    if (hp.ok) {
+      double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
+      int rc = hvp_cluster(hp, A, rows, n, lda, d, v, P, st, pred);
+      if (rc == NYS_OK) {
+        const int64_t rb = tmin<int64_t>(cdiv(n, 32), kRedPartials);
+        gemv_t_reduce<<<(unsigned)rb, 256, 0, st>>>(P, n, 1, hp.nclusters, y, n, finish ? v : nullptr, shift,
+                                                     finish ? pAp : nullptr, red_part(ws), red_counter(ws), pred);
+        NYS_CHECK_LAUNCH();
+        return NYS_OK;
+      }
+      if (rc != NYS_ERR_UNSUPPORTED) return rc;
+    }
   }
   // wide rows: column strips over the whole grid, A still streamed once (csrc/hvp_strip.cu)
   static const bool no_strip = getenv("NYS_HVP_NOSTRIP") != nullptr;
