@@ -513,15 +513,26 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
   const int tid = threadIdx.x, cx = tid & (kEpiCols - 1), ch = tid >> 6;
   const int64_t c = (int64_t)blockIdx.x * kEpiCols + cx;
   {
-    double acc[K];
+    // splits ch, ch + 4, ... of column c: four independent chains so four
+    // groups of loads are in flight per round trip (fixed combination order)
+    double acc[4][K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) acc[j] = 0.0;
-    if (c < n)
-      for (int q = ch; q < splits; q += 4)
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int j = 0; j < K; ++j) acc[j] += P[((int64_t)q * K + j) * n + c];
+      for (int j = 0; j < K; ++j) acc[u][j] = 0.0;
+    if (c < n) {
+      int q = ch;
+      for (; q + 12 < splits; q += 16)
 #pragma unroll
-    for (int j = 0; j < K; ++j) cs[ch][j][cx] = acc[j];
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc[u][j] += P[((int64_t)(q + 4 * u) * K + j) * n + c];
+      for (; q < splits; q += 4)
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[0][j] += P[((int64_t)q * K + j) * n + c];
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) cs[ch][j][cx] = (acc[0][j] + acc[1][j]) + (acc[2][j] + acc[3][j]);
   }
   __syncthreads();
   double s[9 + 17], m[7];
