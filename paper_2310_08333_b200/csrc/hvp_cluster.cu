@@ -35,6 +35,20 @@ constexpr int kHcX = 2;                         // exchange (relay) warps
 constexpr int kHcThreads = (kHcWarps + 1 + kHcX) * 32;  // + producer + relays
 constexpr int kHcNT = 16;                       // row-total slots (> S + L + margin)
 constexpr int kHcSmemBudget = 220 * 1024;
+constexpr int kHcMaxS = 6;                      // named barriers 1..6 (empty), 7..12 (dot)
+constexpr int kHcBarThreads = (kHcWarps + 1) * 32;  // 16 compute warps + the producer / one relay
+
+// Hardware named barriers for the intra-CTA stage hand-offs (a 16-warp mbarrier
+// arrival per row serialised on the shared-memory atomics).  bar.arrive by the
+// 16 compute warps, bar.sync by the producer (stage free) or a relay warp
+// (partials written); the arrive orders the warps' prior shared-memory
+// accesses before the sync returns.
+__device__ __forceinline__ void nbar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kHcBarThreads) : "memory");
+}
+__device__ __forceinline__ void nbar_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kHcBarThreads) : "memory");
+}
 
 template <int K>
 __global__ void __launch_bounds__(kHcThreads, 1)
@@ -47,9 +61,7 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
   double* psl = ring + (size_t)S * W;                                  // S x 16 warp partials
   double* tsl = psl + (size_t)S * kHcWarps;                            // NT x 16 CTA partials
   uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * kHcC);    // S
-  uint64_t* empty = full + S;                                          // S (16 warp arrivals)
-  uint64_t* dotb = empty + S;                                          // S (16 warp arrivals)
-  uint64_t* totb = dotb + S;                                           // NT (tx from the cluster)
+  uint64_t* totb = full + S;                                           // NT (tx from the cluster)
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int cluster_id = blockIdx.x / kHcC, nclusters = gridDim.x / kHcC;
@@ -60,11 +72,7 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
   const int64_t nrows_mine = rows > cluster_id ? (rows - cluster_id + nclusters - 1) / nclusters : 0;
 
   if (tid == 0) {
-    for (int q = 0; q < S; ++q) {
-      mbar_init(&full[q], 1);
-      mbar_init(&empty[q], kHcWarps);
-      mbar_init(&dotb[q], kHcWarps);
-    }
+    for (int q = 0; q < S; ++q) mbar_init(&full[q], 1);
     for (int q = 0; q < kHcNT; ++q) mbar_init(&totb[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // first use of every total slot: one local arrival + 16 x 8 bytes from the cluster
@@ -74,30 +82,40 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
 
   if (warp == kHcWarps) {
     // ---------------------------------------------------------- producer --
-    if (lane == 0 && bytes > 0) {
-      for (int64_t g = 0; g < nrows_mine; ++g) {
-        const int q = (int)(g % S);
-        if (g >= S) mbar_wait(&empty[q], (unsigned)(((g / S) - 1) & 1));
-        const int64_t i = cluster_id + g * nclusters;
+    // (the whole warp takes part in the stage barriers; lane 0 issues the copies)
+    // (stage indices kept incrementally: no 64-bit divisions in the row loops)
+    const int nr = (int)nrows_mine;
+    const double* arow = A + (int64_t)cluster_id * lda + c0;
+    const int64_t rstep = (int64_t)nclusters * lda;
+    for (int g = 0, q = 0; g < nr; ++g, arow += rstep) {
+      if (g >= S) nbar_sync(1 + q);  // the 16 compute warps are done with row g - S
+      if (lane == 0 && bytes > 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&full[q], bytes);
-        tma_load_1d(ring + (size_t)q * W, A + i * lda + c0, bytes, &full[q]);
+        tma_load_1d(ring + (size_t)q * W, arow, bytes, &full[q]);
       }
+      if (++q == S) q = 0;
     }
+    // consume the stage-free arrivals of the last rows (no refill follows them)
+    for (int g = tmax(0, nr - S); g < nr; ++g) nbar_sync(1 + g % S);
   } else if (warp > kHcWarps) {
     // --------------------------------------------------- exchange (relay) --
     const int xr = warp - kHcWarps - 1;  // rows g = xr (mod kHcX)
-    for (int64_t g = xr; g < nrows_mine; g += kHcX) {
-      const int q = (int)(g % S);
-      const int64_t i = cluster_id + g * nclusters;
+    const int nr = (int)nrows_mine;
+    int q = xr % S;
+    for (int g = xr; g < nr; g += kHcX) {
+      const int64_t i = cluster_id + (int64_t)g * nclusters;
       const double di = d ? __ldg(d + i) : 1.0;
-      mbar_wait(&dotb[q], (unsigned)((g / S) & 1));
+      nbar_sync(1 + kHcMaxS + q);  // the 16 warp partials of row g are in psl
       double p = lane < kHcWarps ? psl[q * kHcWarps + lane] : 0.0;
       // fixed-order tree over the 16 warp partials (lanes 0..15)
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
       p *= di;
-      const int s = (int)(g % kHcNT);
+      const int s = g & (kHcNT - 1);
       if (lane < kHcC) st_async_remote_f64(tsl + s * kHcC + rank, &totb[s], (unsigned)lane, p);
+      q += kHcX;
+      while (q >= S) q -= S;
     }
   } else {
     // ---------------------------------------------------------- compute --
@@ -108,10 +126,17 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
       vr[k] = (j < w_here) ? *reinterpret_cast<const double2*>(v + c0 + j) : make_double2(0.0, 0.0);
       yr[k] = make_double2(0.0, 0.0);
     }
-    for (int64_t it = 0; it < nrows_mine + L; ++it) {
-      if (it < nrows_mine) {
-        const int q = (int)(it % S);
-        if (bytes > 0) mbar_wait(&full[q], (unsigned)((it / S) & 1));
+    const int nr = (int)nrows_mine;
+    int qi = 0, pi = 0;  // stage and phase of row it
+    int qj = 0;          // stage of row jt = it - L
+    for (int it = 0; it < nr + L; ++it) {
+      if (it < nr) {
+        const int q = qi;
+        if (bytes > 0) mbar_wait(&full[q], (unsigned)pi);
+        if (++qi == S) {
+          qi = 0;
+          pi ^= 1;
+        }
         const double* row = ring + (size_t)q * W;
         double pt = 0.0;
 #pragma unroll
@@ -124,20 +149,20 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
           }
         }
         pt = warp_sum(pt);
-        if (lane == 0) {
-          psl[q * kHcWarps + warp] = pt;
-          mbar_arrive(&dotb[q]);  // release: the slot write is visible to the relay warp
-        }
+        if (lane == 0) psl[q * kHcWarps + warp] = pt;
+        __syncwarp();
+        nbar_arrive(1 + kHcMaxS + q);
       }
-      const int64_t jt = it - L;
+      const int jt = it - L;
       if (jt < 0) continue;
-      const int s = (int)(jt % kHcNT);
+      const int s = jt & (kHcNT - 1);
       mbar_wait_cluster(&totb[s], (unsigned)((jt / kHcNT) & 1));
       double t = 0.0;  // d_i (a_i . v): the 16 CTA partials (already scaled) in a fixed order
 #pragma unroll
       for (int q2 = 0; q2 < kHcC; ++q2) t += tsl[s * kHcC + q2];
       if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kHcC * 8u);  // re-arm for row jt + NT
-      const int q = (int)(jt % S);
+      const int q = qj;
+      if (++qj == S) qj = 0;
       const double* row = ring + (size_t)q * W;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -149,7 +174,7 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[q]);
+      nbar_arrive(1 + q);  // stage q free for the producer
     }
     double* yp = ypart + (int64_t)cluster_id * n + c0;
 #pragma unroll
@@ -177,13 +202,15 @@ HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, c
   if (p.K > 12) return p;
   const size_t fixed = (size_t)(kHcNT * kHcC) * 8 + kHcNT * 8 + 1024;
   const size_t row_bytes = (size_t)p.W * 8;
-  p.S = (int)tmin<int64_t>(8, (int64_t)((kHcSmemBudget - fixed) / (row_bytes + kHcWarps * 8 + 24)));
+  p.S = (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / (row_bytes + kHcWarps * 8 + 24)));
   if (p.S < 3) return p;
   static const int forced_lag = getenv("NYS_HVP_CLUSTER_LAG") ? atoi(getenv("NYS_HVP_CLUSTER_LAG")) : 0;
-  p.L = forced_lag > 0 ? forced_lag : p.S - 2;
+  // lag 1 measured best on B200 (n = 1e5, S = 4: 2.32 ms vs 2.80 ms at lag 2 -
+  // the exchange is sub-microsecond, the extra stage in flight is worth more)
+  p.L = forced_lag > 0 ? forced_lag : 1;
   p.L = tmax(1, tmin(p.L, p.S - 1));
   if (p.S + p.L + 2 > kHcNT) return p;
-  p.smem = (size_t)p.S * (row_bytes + kHcWarps * 8) + (size_t)kHcNT * kHcC * 8 + (size_t)(3 * p.S + kHcNT) * 8;
+  p.smem = (size_t)p.S * (row_bytes + kHcWarps * 8) + (size_t)kHcNT * kHcC * 8 + (size_t)(p.S + kHcNT) * 8;
   p.nclusters = 0;
   p.ok = true;
   return p;
