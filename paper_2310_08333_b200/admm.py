@@ -835,7 +835,9 @@ class _Engine:
         self.snap = kx.zeros(5, n)
         self._done_ev = [torch.cuda.Event() for _ in range(2)]
         self._ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(2)]
-        self._iter_events = os.environ.get("NYS_ITER_EVENTS", "1") != "0"
+        # 1: events around the x-update and the tail; 2: only around the whole
+        # iteration (no event between the two kernel groups); 0: none
+        self._iter_events = int(os.environ.get("NYS_ITER_EVENTS", "1"))
         self._seq = 0
         ptr = lambda x: x.data_ptr() if x is not None else None
         self._tails, self._pbs, self._heads = [], [], []
@@ -967,7 +969,7 @@ class _Engine:
         if self._iter_events:
             ev[0].record(kx.stream)
         kx.admm_xupdate(h, pb, batch)  # head + PCG (one persistent kernel when it fits)
-        if self._iter_events:
+        if self._iter_events == 1:
             ev[1].record(kx.stream)
         kx.admm_tail(t)
         if self._iter_events:
@@ -1007,8 +1009,12 @@ class _Engine:
         kx, par = self.kx, it.par
         sc, st = self._read(par)
         ev = self._ev[par]
-        lin_ms = ev[0].elapsed_time(ev[1]) if self._iter_events else 0.0
-        tail_ms = ev[1].elapsed_time(ev[2]) if self._iter_events else 0.0
+        if self._iter_events == 1:
+            lin_ms, tail_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+        elif self._iter_events == 2:
+            lin_ms, tail_ms = ev[0].elapsed_time(ev[2]), 0.0
+        else:
+            lin_ms = tail_ms = 0.0
         k_last, batch = it.batch, it.batch
         self._cg_continued = False
         max_iter = 10 * self.n
