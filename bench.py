@@ -309,7 +309,7 @@ def run_ours(args):
         rows_loc = d.A.shape[0] // world if d.kind != "boxqp" else n
     alg_bytes = 8 * rows_loc * n + 8 * (2 * n + rows_loc)
     peak, peak_kind = _peaks()
-    persistent = os.environ.get("NYS_CG_PERSIST", "1") != "0" and d.kind != "boxqp" and n <= 13312
+    persistent = os.environ.get("NYS_CG_PERSIST", "1") != "0" and n <= 13312 and (d.kind == "boxqp" or world == 1)
     kname = "cg_persist_kernel" if persistent else "hvp"
     roof = None
     traffic_db = {}

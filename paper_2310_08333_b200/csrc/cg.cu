@@ -401,7 +401,7 @@ extern "C" int nys_admm_xupdate_f64(const nys_admm_head* h, const nys_cg_problem
   if (!h || !pb) return NYS_ERR_ARG;
   cudaStream_t st = as_stream(stream);
   if (h->zu) h->zu->zu_done = 0;
-  if (pb->ws_cp && pb->op_kind == 0) {
+  if (pb->ws_cp) {
     TimedLaunch tl{pb->timing_tag, 0, nullptr, nullptr};
     if (g_timing) {
       tl.a = pool_get();

@@ -61,6 +61,7 @@ struct CgPersistArgs {
   int W, S;
   int has_head;       // run the ADMM head (nys_admm_head) as the prologue
   int u_smem;         // stage this CTA's rows of U in shared memory
+  int qp;                  // operator P v (QP, P symmetric n x n) instead of A^T (d o A v)
   int probe;               // development timing probe (NYS_CP_PROBE)
   int no_early_prefetch;   // development: no speculative first rows before the prologue
   const double* order_in;  // row order of the previous pass over A (NULL: ascending first)
@@ -138,7 +139,8 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   double* csh = sh + 32;                                                     // coef (r <= 512)
   double* ys = csh + 520;                                                    // slice sums
   double* rsl = ys + 112;  // CG residual of the slice: the preconditioner passes read it from here
-  double* scr = rsl + 112;                                                   // colsum scratch (1024)
+  double* vrow = rsl + 112;  // QP: the direction at this CTA's rows (p_i of p^T P p)
+  double* scr = vrow + 112;                                                  // colsum scratch (1024)
   double* us = scr + 1024;                                                   // U rows of the slice
   __shared__ double s_bcast;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -402,15 +404,23 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       if (lane == 0) red[(it & 1) * 16 + warp] = pt;
       __syncthreads();
       const double tot = warp_sum(lane < kCpWarps ? red[(it & 1) * 16 + lane] : 0.0);
-      const double t = a.d ? di * tot : tot;
-      if (tid == 0) vav = fma(t, tot, vav);
+      if (a.qp) {
+        // (P v)_i is the row's dot itself: written directly, p^T P p from v_i
+        if (tid == 0) {
+          a.ypart[i] = tot;
+          vav = fma(vrow[dir ? nrows_mine - 1 - it : it], tot, vav);
+        }
+      } else {
+        const double t = a.d ? di * tot : tot;
+        if (tid == 0) vav = fma(t, tot, vav);
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int j = 2 * (tid + k * kCpThreads);
-        if (j < n) {
-          const double2 v2 = *reinterpret_cast<const double2*>(row + j);
-          yr[k].x = fma(t, v2.x, yr[k].x);
-          yr[k].y = fma(t, v2.y, yr[k].y);
+        for (int k = 0; k < K; ++k) {
+          const int j = 2 * (tid + k * kCpThreads);
+          if (j < n) {
+            const double2 v2 = *reinterpret_cast<const double2*>(row + j);
+            yr[k].x = fma(t, v2.x, yr[k].x);
+            yr[k].y = fma(t, v2.y, yr[k].y);
+          }
         }
       }
       __syncthreads();
@@ -424,11 +434,13 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     g0 += nrows_mine;
     last_dir = dir;
     prefetch(dir ^ 1);
-    double* yp = a.ypart + (int64_t)cta * n;
+    if (!a.qp) {
+      double* yp = a.ypart + (int64_t)cta * n;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int j = 2 * (tid + k * kCpThreads);
-      if (j < n) *reinterpret_cast<double2*>(yp + j) = yr[k];
+      for (int k = 0; k < K; ++k) {
+        const int j = 2 * (tid + k * kCpThreads);
+        if (j < n) *reinterpret_cast<double2*>(yp + j) = yr[k];
+      }
     }
     return vav;
   };
@@ -493,6 +505,15 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       out[col] = t;
     }
     __syncthreads();
+  };
+  auto y_slice = [&]() {  // ys = (A^T D A p or P p) on this CTA's column slice
+    if (a.qp) {
+      __syncthreads();
+      for (int64_t i = c0 + tid; i < c1; i += kCpThreads) ys[i - c0] = a.ypart[i];
+      __syncthreads();
+    } else {
+      colsum(a.ypart, n, nctas, c0, (int)(c1 - c0), ys);
+    }
   };
   // this CTA's share of h = U^T w over its slice -> hpart[cta]
   // (thread j: four fixed-order chains over the slice's rows; w of the slice
@@ -631,7 +652,12 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
           vr[kk] = make_double2(0.0, 0.0);
         }
       }
-      vv = cp_block_sum(pp, sh);  // ||p||^2, identical in every CTA
+      if (a.qp)  // the direction at this CTA's rows, same arithmetic as vr
+        for (int64_t q2 = tid; q2 < nrows_mine; q2 += kCpThreads) {
+          const int64_t i = cta + q2 * nctas;
+          vrow[q2] = k > 1 ? __dadd_rn(a.z[i], __dmul_rn(beta, pold[i])) : a.z[i];
+        }
+      vv = cp_block_sum(pp, sh);  // ||p||^2, identical in every CTA (barriers order vrow too)
       stamp(4);  // direction
       const double vav = hvp_rows(vr);
       if (tid == 0) a.part[cta * 8 + 1] = vav;
@@ -664,7 +690,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     const double* pc = a.p[pb];
     double rr;
     if (!refresh) {
-      colsum(a.ypart, n, nctas, c0, (int)(c1 - c0), ys);
+      y_slice();
       stamp(17);  // step: y partial sums
       double acc = 0.0;
       if (smine) {
@@ -688,9 +714,13 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
         const int j = 2 * (tid + kk * kCpThreads);
         vr[kk] = j < n ? *reinterpret_cast<const double2*>(a.x + j) : make_double2(0.0, 0.0);
       }
+      if (a.qp) {
+        for (int64_t q2 = tid; q2 < nrows_mine; q2 += kCpThreads) vrow[q2] = a.x[cta + q2 * nctas];
+        __syncthreads();
+      }
       hvp_rows(vr);
       grid.sync();
-      colsum(a.ypart, n, nctas, c0, (int)(c1 - c0), ys);
+      y_slice();
       double acc = 0.0;
       for (int64_t i = c0 + tid; i < c1; i += kCpThreads) {
         const double axi = fma(a.shift, a.x[i], ys[i - c0]);
@@ -758,7 +788,8 @@ static CpPlan cp_plan(const nys_cg_problem* pb) {
   CpPlan p{};
   p.ok = false;
   static const bool off = getenv("NYS_CG_PERSIST_OFF") != nullptr;
-  if (off || pb->op_kind != 0 || pb->rows < kNumSMs || (pb->n & 1) || (pb->lda & 1) ||
+  if (off || (pb->op_kind != 0 && !(pb->op_kind == 1 && pb->rows == pb->n)) || pb->rows < kNumSMs ||
+      (pb->n & 1) || (pb->lda & 1) ||
       ((uintptr_t)pb->A & 15) || pb->r > 512)
     return p;
   p.W = (int)pb->n;
@@ -768,7 +799,7 @@ static CpPlan cp_plan(const nys_cg_problem* pb) {
   static_assert(((kCpMaxK * 2 * kCpThreads + kNumSMs - 1) / kNumSMs + 1) <= kCpThreads, "slice");
   p.MC = pb->r <= 128 ? 4 : (pb->r <= 256 ? 8 : 16);
   const size_t row_bytes = (size_t)p.W * 8;
-  const size_t extra = 64 * 8 + (size_t)(520 + 112 + 112 + 1024) * 8 + 1024;  // red, sh, csh, slice sums, scratch
+  const size_t extra = 64 * 8 + (size_t)(520 + 112 + 112 + 112 + 1024) * 8 + 1024;  // red, sh, csh, slice sums, scratch
   p.S = (int)tmin<int64_t>(4, (kCpSmemBudget - extra) / row_bytes);
   if (p.S < 2) return p;
   p.smem = (size_t)p.S * row_bytes + (size_t)(p.S + 2) * 8 + extra;
@@ -853,13 +884,14 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
   a.u_smem = pl.u_smem;
   static const int probe = getenv("NYS_CP_PROBE") ? atoi(getenv("NYS_CP_PROBE")) : 0;
   a.probe = probe;
+  a.qp = pb->op_kind == 1 ? 1 : 0;
   static const int nopf = getenv("NYS_CP_NOPREFETCH") ? 1 : 0;
   a.no_early_prefetch = nopf;
   a.order_in = pb->order_in;
   a.order_out = pb->order_out;
   if (head) a.h = *head;
   const nys_admm_tail* t = head ? head->zu : nullptr;
-  if (t && t->kind == 0 && t->XZ == pb->x && t->n == pb->n) {
+  if (t && t->XZ == pb->x && t->n == pb->n) {
     a.has_zu = 1;
     a.zu.z = t->XZ + t->n;
     a.zu.u = t->u;
@@ -867,7 +899,7 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
     a.zu.zbar = t->zbar;
     a.zu.alpha = t->alpha;
     a.zu.kappa = t->kappa;
-    a.zu.prox_kind = NYS_PROX_SOFT;
+    a.zu.prox_kind = t->kind == 0 ? NYS_PROX_SOFT : NYS_PROX_BOX;
     a.zu.accum = t->accum;
     a.zu.lo = t->lo;
     a.zu.hi = t->hi;

@@ -166,7 +166,7 @@ class Kernels:
             Ap=work.Ap.data_ptr(), sc=work.sc.data_ptr(), tol=float(tol), max_iter=int(max_iter),
             ws_op=w_op.data_ptr(), ws_op_bytes=w_op.numel(), ws_pc=w_pc.data_ptr(), ws_pc_bytes=w_pc.numel(),
             ws_red=w_red.data_ptr())
-        if op_kind == 0 and os.environ.get("NYS_CG_PERSIST", "1") != "0":
+        if os.environ.get("NYS_CG_PERSIST", "1") != "0":
             w_cp = self.workspace("cgpersist", self.L.nys_cg_persist_workspace(n, 512))
             pb.ws_cp, pb.ws_cp_bytes = w_cp.data_ptr(), w_cp.numel()
         return pb
