@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     if (tid == 0)
       for (int64_t q = 0; q < a.S && q < nrows_mine; ++q) {
         const int64_t g = g0 + q;
-        const int st = (int)(g % a.S);
+        const int st = (int)((unsigned)g % (unsigned)a.S);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&full[st], rbytes);
         tma_load_1d(ring + (size_t)st * a.W, a.A + row_of(q, dir) * a.lda, rbytes, &full[st]);
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     if (tid == 0 && pre_dir >= 0)
       for (int64_t q = 0; q < a.S && q < nrows_mine; ++q) {
         const int64_t g = g0 + q;
-        mbar_wait(&full[g % a.S], (unsigned)((g / a.S) & 1));
+        mbar_wait(&full[(unsigned)g % (unsigned)a.S], ((unsigned)g / (unsigned)a.S) & 1u);
       }
     if (writer && a.order_out) *a.order_out = (double)last_dir;
   };
@@ -385,11 +385,11 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     const int dir = pre_dir;
     for (int64_t it = 0; it < nrows_mine; ++it) {
       const int64_t g = g0 + it;
-      const int st = (int)(g % a.S);
+      const int st = (int)((unsigned)g % (unsigned)a.S);
       const int64_t i = row_of(it, dir);
       const double di = a.d ? __ldg(a.d + i) : 1.0;
       const double* row = ring + (size_t)st * a.W;
-      mbar_wait(&full[st], (unsigned)((g / a.S) & 1));
+      mbar_wait(&full[st], ((unsigned)g / (unsigned)a.S) & 1u);
       double pt = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {

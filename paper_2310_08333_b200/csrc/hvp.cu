@@ -99,9 +99,9 @@ hvp_fused_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t 
   constexpr int LAG = CLUSTER ? 1 : 0;
   for (int64_t it = 0; it < nrows_mine + LAG; ++it) {
     if (it < nrows_mine) {
-      const int s = (int)(it % S);
+      const int s = (int)((unsigned)it % (unsigned)S);
       const double* row = ring + (size_t)s * W;
-      if (bytes > 0) mbar_wait(&full[s], (unsigned)((it / S) & 1));
+      if (bytes > 0) mbar_wait(&full[s], (((unsigned)it / (unsigned)S) & 1u));
       double part = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -124,7 +124,7 @@ hvp_fused_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t 
     }
     const int64_t jt = it - LAG;  // the row finished in this iteration
     if (jt < 0) continue;
-    const int sj = (int)(jt % S);
+    const int sj = (int)((unsigned)jt % (unsigned)S);
     const int64_t i = cluster_id + jt * nclusters;
     const double* row = ring + (size_t)sj * W;
     if (tid == 0) {
@@ -209,7 +209,7 @@ hvp_row_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t ld
   const int64_t npieces = nrows_mine * P;
   const unsigned pbytes = (unsigned)Wp * 8u;
   auto issue = [&](int64_t g) {  // piece g = row g / P, part g % P, into stage g % S
-    const int q = (int)(g % S);
+    const int q = (int)((unsigned)g % (unsigned)S);
     const int64_t i = cta + (g / P) * nctas;
     mbar_expect_tx(&full[q], pbytes);
     tma_load_1d(ring + (size_t)q * Wp, A + i * lda + (g % P) * Wp, pbytes, &full[q]);
@@ -224,9 +224,9 @@ hvp_row_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t ld
 #pragma unroll
     for (int h = 0; h < P; ++h) {
       const int64_t g = it * P + h;
-      const int q = (int)(g % S);
+      const int q = (int)((unsigned)g % (unsigned)S);
       pc[h] = ring + (size_t)q * Wp;
-      mbar_wait(&full[q], (unsigned)((g / S) & 1));
+      mbar_wait(&full[q], ((unsigned)g / (unsigned)S) & 1u);
     }
     const double* pc0 = pc[0];
     const double* pc1 = pc[P - 1] - Wp;  // P == 2: pc1 + j addresses the second half

@@ -70,8 +70,8 @@ xz_rowpass_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t
     // ---------------------------------------------------------- producer --
     if (lane == 0) {
       for (int64_t g = 0; g < npieces; ++g) {
-        const int q = (int)(g % S);
-        if (g >= S) mbar_wait(&empty[q], (unsigned)(((g / S) - 1) & 1));
+        const int q = (int)((unsigned)g % (unsigned)S);
+        if (g >= S) mbar_wait(&empty[q], (((unsigned)g / (unsigned)S) - 1u) & 1u);
         const int64_t qq = desc ? nrows_mine - 1 - g / P : g / P;
         const int64_t i = cta + qq * nctas;
         mbar_expect_tx(&full[q], pbytes);
@@ -97,8 +97,8 @@ xz_rowpass_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t
 #pragma unroll
       for (int h = 0; h < P; ++h) {
         const int64_t g = it * P + h;
-        const int q = (int)(g % S);
-        mbar_wait(&full[q], (unsigned)((g / S) & 1));
+        const int q = (int)((unsigned)g % (unsigned)S);
+        mbar_wait(&full[q], ((unsigned)g / (unsigned)S) & 1u);
         const double* pc = ring + (size_t)q * Wp;
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
