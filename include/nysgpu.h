@@ -73,6 +73,10 @@ enum nys_cg_slot {
 /* One PCG solve for nys_cg_iterate_f64 (krylov.py:35-95).  All pointers are
  * device pointers; `sc` is the NYS_CG_NSLOTS scalar block with B2 and RES2
  * already set for r = b - A x0 (e.g. by nys_admm_rhs_f64 or nys_cg_start_f64). */
+/* Sum `count` doubles at `buf` over all ranks in place, ordered on `stream`
+ * (the host layer's all-reduce; called from inside the drivers below). */
+typedef void (*nys_reduce_fn)(double* buf, int64_t count, void* user, void* stream);
+
 typedef struct nys_cg_problem {
   int op_kind;          /* 0: y = A^T (d o A v) + shift v (ML Hessian, A rows x n)
                            1: y = A v + shift v (dense symmetric A, n x n)          */
@@ -109,6 +113,13 @@ typedef struct nys_cg_problem {
                                           passes starting opposite to *order_in so each pass
                                           begins with the rows still in L2, and records its
                                           last in *order_out (results depend only on *order_in) */
+  nys_reduce_fn reduce; void* reduce_user; /* NULL, or the row-sharded exchange:
+                                          each operator application then produces this rank's
+                                          partial A_i^T (d o A_i v), calls reduce(y, n, ...) to
+                                          sum it over the ranks (enqueued on the stream by the
+                                          host layer: torch.distributed / NCCL), and adds the
+                                          shift and p.Ap after it.  The solve stays device-
+                                          predicated: no host round trip per CG iteration.  */
 } nys_cg_problem;
 
 /* ---------------------------------------------------------------- misc -- */
@@ -244,6 +255,10 @@ typedef struct nys_admm_tail {
   int zu_done;                /* set by nys_admm_xupdate_f64 when its persistent kernel
                                  already ran the relax/prox/dual update and the window
                                  append of this descriptor; the tail then skips them   */
+  nys_reduce_fn reduce; void* reduce_user;  /* NULL, or the row-sharded exchange: the A^T
+                                 outputs (AT), the row sums (NYS_ROWS_NOUT) and the
+                                 conjugate sums (3) are summed over the ranks before the
+                                 norms that use them                                      */
 } nys_admm_tail;
 int nys_admm_tail_f64(const nys_admm_tail* t, void* stream);
 

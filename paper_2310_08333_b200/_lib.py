@@ -55,6 +55,7 @@ class CgProblem(C.Structure):
         ("tol", F64), ("max_iter", I64), ("ws_op", P), ("ws_op_bytes", SZ), ("ws_pc", P),
         ("ws_pc_bytes", SZ), ("ws_red", P), ("gate", P), ("tol_dev", P), ("timing_tag", I64),
         ("ws_cp", P), ("ws_cp_bytes", SZ), ("order_in", P), ("order_out", P),
+        ("reduce", P), ("reduce_user", P),
     ]
 
 class AdmmTail(C.Structure):
@@ -72,7 +73,11 @@ class AdmmTail(C.Structure):
         ("dx", P), ("Pdx", P), ("infeas", P), ("pdx2", P),
         ("ws_gemv", P), ("ws_gemv_bytes", SZ), ("ws_gemvT", P), ("ws_gemvT_bytes", SZ), ("ws_red", P),
         ("pred", P), ("gate_next", P), ("conj_out", P), ("order", P), ("zu_done", C.c_int),
+        ("reduce", P), ("reduce_user", P),
     ]
+
+# nys_reduce_fn (include/nysgpu.h): the host-side all-reduce hook of the sharded drivers
+REDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
 
 
 class AdmmHead(C.Structure):

@@ -452,10 +452,12 @@ class _Engine:
         if use_gap and not self.is_ml:
             raise DataError("the duality-gap criterion requires an ML problem")
         self.use_gap = use_gap
-        # single-process CUDA path: batched CG + predicated iteration tail (one
-        # host round trip per ADMM iteration); sharded runs keep the per-step path
-        # because their all-reduces sit between the kernels
-        self.fast = hasattr(kx, "admm_tail") and not self.shard.sharded
+        # CUDA path: batched CG + predicated iteration tail (one host round trip
+        # per ADMM iteration).  Row-sharded runs use it too: the drivers call the
+        # all-reduce hook (nys_reduce_fn) between a rank's partials and their use,
+        # so the exchange is enqueued on the stream like any kernel.
+        self.fast = hasattr(kx, "admm_tail") and (
+            not self.shard.sharded or os.environ.get("NYS_SHARD_FAST", "1") != "0")
         self.sigma_eff = sigma_eff
         if self.fast:
             self._make_tail()
@@ -689,7 +691,7 @@ class _Engine:
             x_bar=x_bar, z_bar=z_bar, certificate_primal=cert_p, certificate_dual=cert_d,
             penalty_events=events, iterates=iterates, gap=gap,
             device_stats={"kernel_launches": kx.launches, "sketches": self.n_sketches,
-                          "world": self.shard.world},
+                          "world": self.shard.world, "pipelined": bool(self.fast)},
         )
 
     # ------------------------------------------------------ host maths ----
@@ -840,6 +842,19 @@ class _Engine:
         self._iter_events = int(os.environ.get("NYS_ITER_EVENTS", "1"))
         self._seq = 0
         ptr = lambda x: x.data_ptr() if x is not None else None
+        self._reduce_fn = None
+        if self.shard.sharded:
+            # the all-reduce hook of the C drivers: buffers are recognised by address
+            self._reduce_views = {}
+
+            def _reduce(buf, count, user, stream):
+                base = self._reduce_views[buf]
+                self.shard.allreduce(base.view(-1)[:count])
+
+            self._reduce_fn = _lib.REDUCE_FN(_reduce)  # kept alive with the engine
+            for v in (self.AT if self.is_ml else None, self.cg.Ap):
+                if v is not None:
+                    self._reduce_views[v.data_ptr()] = v
         self._tails, self._pbs, self._heads = [], [], []
         for par in range(2):
             blk = self.rbs[par]
@@ -883,6 +898,11 @@ class _Engine:
                 wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(n, n, 1))
                 wt = kx.workspace("tail_gemvT", 256)
             wr = kx.workspace("tail_red", L.nys_reduce_workspace())
+            if self._reduce_fn is not None:
+                t.reduce = C.cast(self._reduce_fn, C.c_void_p)
+                self._reduce_views[blk.data_ptr()] = blk
+                if t.conj_out:
+                    self._reduce_views[st[_S_CONJ:].data_ptr()] = st[_S_CONJ:]
             t.ws_gemv, t.ws_gemv_bytes = wg.data_ptr(), wg.numel()
             t.ws_gemvT, t.ws_gemvT_bytes = wt.data_ptr(), wt.numel()
             t.ws_red = wr.data_ptr()
@@ -923,6 +943,9 @@ class _Engine:
                                    1e-12, 10 * n)
             pb.gate = self.gates[par:].data_ptr()
             pb.tol_dev = self.tols[par:].data_ptr()
+            if self._reduce_fn is not None:
+                pb.reduce = C.cast(self._reduce_fn, C.c_void_p)
+                self._reduce_views[pb.Ap] = self.cg.Ap
             pb.order_in = self.orders[1 - par:].data_ptr()
             pb.order_out = self.orders[par:].data_ptr()
             pb._key = key

@@ -313,8 +313,20 @@ static int precondition(const nys_cg_problem* pb, cudaStream_t st, const double*
                        pb->res, pb->sc + NYS_CG_RZNEW, pb->ws_pc, pb->ws_pc_bytes, st, pred);
 }
 
+int shift_dot_pred(int64_t n, const double* v, double shift, double* y, double* dot, void* ws, cudaStream_t st,
+                   const double* pred);
+
 static int matvec(const nys_cg_problem* pb, const double* v, double* y, double* pAp, cudaStream_t st,
                   const double* pred) {
+  if (pb->op_kind == 0 && pb->reduce) {
+    // row-sharded: this rank's partial, the host layer's all-reduce, then shift and p.Ap
+    int rc = hvp_apply(pb->A, pb->rows, pb->n, pb->lda, pb->d, v, 0.0, y, nullptr, 0, pb->ws_op, pb->ws_op_bytes,
+                       st, pred);
+    if (rc) return rc;
+    pb->reduce(y, pb->n, pb->reduce_user, st);
+    if (cudaPeekAtLastError() != cudaSuccess) return NYS_ERR_CUDA;
+    return shift_dot_pred(pb->n, v, pb->shift, y, pAp, pb->ws_op, st, pred);
+  }
   if (pb->op_kind == 0)
     return hvp_apply(pb->A, pb->rows, pb->n, pb->lda, pb->d, v, pb->shift, y, pAp, 1, pb->ws_op, pb->ws_op_bytes,
                      st, pred);
@@ -401,7 +413,7 @@ extern "C" int nys_admm_xupdate_f64(const nys_admm_head* h, const nys_cg_problem
   if (!h || !pb) return NYS_ERR_ARG;
   cudaStream_t st = as_stream(stream);
   if (h->zu) h->zu->zu_done = 0;
-  if (pb->ws_cp) {
+  if (pb->ws_cp && !pb->reduce) {
     TimedLaunch tl{pb->timing_tag, 0, nullptr, nullptr};
     if (g_timing) {
       tl.a = pool_get();
@@ -441,7 +453,7 @@ extern "C" int nys_cg_iterate_f64(const nys_cg_problem* pb, int64_t k_first, int
   // the cg_dir ticket lives in the spare slot of the scalar block
   unsigned int* dir_counter = reinterpret_cast<unsigned int*>(sc + NYS_CG_TICKET);
   int rc;
-  if (k_first == 1 && pb->ws_cp) {
+  if (k_first == 1 && pb->ws_cp && !pb->reduce) {
     // the whole solve as one persistent cooperative kernel (cg_persist.cu)
     TimedLaunch tl{pb->timing_tag, 0, nullptr, nullptr};
     if (g_timing) {

@@ -511,6 +511,15 @@ __global__ void shift_dot_kernel(int64_t n, const double* __restrict__ v, double
   }
 }
 
+// y += shift v and dot = v.y, predicated (sharded operator: after the all-reduce)
+int shift_dot_pred(int64_t n, const double* v, double shift, double* y, double* dot, void* ws, cudaStream_t st,
+                   const double* pred) {
+  const int64_t blocks = tmin<int64_t>(cdiv(n, 256), kNumSMs * 4);
+  shift_dot_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, v, shift, y, dot, red_part(ws), red_counter(ws), pred);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
 int shift_dot(int64_t n, const double* v, double shift, double* y, double* dot, void* ws,
               cudaStream_t st) {
   if (n <= 0) return NYS_ERR_ARG;

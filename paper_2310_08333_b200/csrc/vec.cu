@@ -1022,7 +1022,10 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       return rc;
     }
     const int64_t woff = t->wnorms - t->norms;
-    const bool fuse = woff >= 16 && woff <= 64 && cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
+    // (row-sharded: the A^T outputs are all-reduced before the norms, so the
+    // split sum cannot be fused with them)
+    const bool fuse = !t->reduce && woff >= 16 && woff <= 64 &&
+                      cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
     if (fuse) {
       // A^T split partials, then one epilogue kernel: split sum -> AT, norms, window norms
       double* P = nullptr;
@@ -1054,6 +1057,11 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       if ((rc = gemv_t(t->A, t->rows, n, t->lda, t->T, t->rows, t->with_z ? 3 : 2, t->AT, n, nullptr, 0.0, nullptr,
                        t->ws_gemvT, t->ws_gemvT_bytes, st, pred)))
         return rc;
+      if (t->reduce) {  // this rank's A^T outputs and row sums: sum over the ranks
+        t->reduce(t->AT, (int64_t)(t->with_z ? 3 : 2) * n, t->reduce_user, st);
+        t->reduce(t->rowsums, NYS_ROWS_NOUT, t->reduce_user, st);
+        if (cudaPeekAtLastError() != cudaSuccess) return NYS_ERR_CUDA;
+      }
       admm_norms_kernel<<<vec_blocks(n), kVecThreads, 0, st>>>(n, x, z, t->u, t->AT, nullptr, t->lambda2, t->rho,
                                                                t->with_z ? t->AT + 2 * n : nullptr, t->lambda1,
                                                                nullptr, nullptr, t->norms, red_part(t->ws_red),
@@ -1070,8 +1078,8 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   }
   // cycle-guard norms for the window after the append (admm.py:645-655);
   // the ML epilogue kernel already computed them when it ran fused
-  const bool ml_fused = t->kind == 0 && (t->wnorms - t->norms) >= 16 && (t->wnorms - t->norms) <= 64 &&
-                        cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
+  const bool ml_fused = t->kind == 0 && !t->reduce && (t->wnorms - t->norms) >= 16 &&
+                        (t->wnorms - t->norms) <= 64 && cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
   if (t->ring && t->nothers > 0 && !ml_fused) {
     SlotList sl;
     for (int j = 0; j < 16; ++j) sl.idx[j] = j < t->nothers ? t->others[j] : 0;
@@ -1100,6 +1108,10 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
     launch_chain(ml_conj_dev_kernel, dim3((unsigned)vec_blocks(t->rows)), dim3(kVecThreads), 0, st, false, t->rows,
                  t->loss, nuc, sc13, t->lambda1, t->b, t->conj_out, red_part(t->ws_red), red_counter(t->ws_red), pred);
     NYS_CHECK_LAUNCH();
+    if (t->reduce) {  // sums over this rank's rows
+      t->reduce(t->conj_out, 3, t->reduce_user, st);
+      if (cudaPeekAtLastError() != cudaSuccess) return NYS_ERR_CUDA;
+    }
   }
   if (t->gate_next) {
     launch_chain(open_gate_kernel, dim3(1), dim3(32), 0, st, false, t->gate_next, pred);

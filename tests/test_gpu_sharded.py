@@ -60,8 +60,9 @@ def _solve(spec, opts, shard=None):
     return nys.solve(prob, nys.SolverOptions(**opts), shard=shard)
 
 
-def _worker(rank, world, port, name, out_path):
+def _worker(rank, world, port, name, out_path, pipelined=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ["NYS_SHARD_FAST"] = "1" if pipelined else "0"
     torch.cuda.set_device(0)
     torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -73,18 +74,23 @@ def _worker(rank, world, port, name, out_path):
         assert shard.world == world and shard.sharded
         res = _solve(spec, opts, shard)
         np.savez(out_path + f".{rank}.npz", x=res.x, z=res.z, it=res.iterations, obj=res.objective,
-                 cg=np.array([h.cg_iters for h in res.history]), rows=shard.row_stop - shard.row_start)
+                 cg=np.array([h.cg_iters for h in res.history]), rows=shard.row_stop - shard.row_start,
+                 pipelined=bool(res.device_stats["pipelined"]))
     finally:
         torch.distributed.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["lasso_small", "logistic_small", "enet_small", "cfg2_small", "cfg4_small"])
-def test_gpu_row_sharded_solve_matches_single(tmp_path, name):
+@pytest.mark.parametrize("name,pipelined", [("lasso_small", True), ("logistic_small", True), ("enet_small", True),
+                                           ("cfg2_small", True), ("cfg4_small", True), ("cfg2_small", False)])
+def test_gpu_row_sharded_solve_matches_single(tmp_path, name, pipelined):
+    """pipelined: the one-round-trip-per-iteration schedule with the all-reduce
+    hook inside the C drivers (default); else the per-step schedule."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     out = str(tmp_path / "r")
-    mp.spawn(_worker, args=(2, _free_port(), name, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), name, out, pipelined), nprocs=2, join=True)
     r0, r1 = (np.load(out + f".{r}.npz") for r in (0, 1))
+    assert bool(r0["pipelined"]) == pipelined
     spec, opts = _problem(name)
     ref = _solve(spec, opts)
     N = spec["A"].shape[0]
