@@ -230,8 +230,11 @@ def run_ours(args):
 
     rank, world, local = _env_rank()
     if world > 1:
+        local = local % max(1, torch.cuda.device_count())  # (ranks sharing a GPU: gloo test mode)
         torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl")
+        # NCCL over NVLink; NYS_DIST_BACKEND=gloo lets several ranks share one GPU
+        # to exercise this multi-rank code path (host-staged collectives, not a measurement)
+        torch.distributed.init_process_group(os.environ.get("NYS_DIST_BACKEND", "nccl"))
     else:
         torch.cuda.set_device(0)
     import paper_2310_08333_b200 as nys
@@ -324,7 +327,7 @@ def run_ours(args):
         achieved = alg_bytes / (avg_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic_db.get(f"cfg{args.config}_{kname}"),
+                "traffic": traffic_db.get(f"cfg{args.config}_{kname}") if world == 1 else None,
                 "alg_bytes_per_unit": alg_bytes, "unit_of_work": "one Hessian application (HVP) of the PCG, "
                 "incl. the CG vector phases when the persistent solver runs", "ms_per_unit": avg_ms,
                 "units_timed": k_count, "share_of_step": k_total_ms / inst_ms,
