@@ -118,7 +118,14 @@ class SketchLaunch:
 
     def ok(self) -> bool:
         self.event.synchronize()
+        if _FORCE_FLAG and _FORCE_FLAG.pop():
+            return False  # test hook: exercise the recovery path
         return not bool(self.flags_h.any())
+
+
+# test hook: a list of booleans; each launched sketch's status check pops one and
+# reports a failure when it is True (tests/test_gpu_solve.py)
+_FORCE_FLAG: list = []
 
 
 def sketch_device_launch(kx, apply_cols: Callable[[torch.Tensor], torch.Tensor], n: int, r: int, seed: int,

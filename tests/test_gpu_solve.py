@@ -163,3 +163,26 @@ def test_solve_config5_shard_lasso():
     assert rel(res.z, gold["z"]) <= 1e-5, rel(res.z, gold["z"])
     del A, prob
     torch.cuda.empty_cache()
+
+
+def test_early_sketch_failure_recovers():
+    """A flagged pipelined sketch (enqueued behind the previous iteration) is
+    undone: the iteration that used it is rolled back from its snapshot, the
+    synchronous sketch runs, and the iteration is issued again.  The solve
+    must end where the undisturbed one does."""
+    import paper_2310_08333_b200 as nys
+    from paper_2310_08333_b200 import sketch as sk
+
+    spec = cases.SOLVE_CASES["logistic_small"][0]()
+    opts = nys.SolverOptions(**dict(cases.options_for("logistic_small"), resketch_every=5))
+    ref = nys.solve(gpu_problem(spec), opts)
+    assert ref.device_stats["sketches"] >= 3
+    sk._FORCE_FLAG[:] = [True, False, True]  # popped from the end: 1st and 3rd early sketches fail
+    try:
+        res = nys.solve(gpu_problem(spec), opts)
+    finally:
+        sk._FORCE_FLAG[:] = []
+    assert res.status == ref.status
+    assert abs(res.iterations - ref.iterations) <= 2
+    assert abs(res.objective - ref.objective) <= 1e-9 * abs(ref.objective)
+    assert rel(res.x, ref.x) <= 1e-7
