@@ -368,7 +368,8 @@ __global__ void gemv_t_reduce(const double* __restrict__ P, int64_t n, int K, in
 
 static void gemv_t_plan(int64_t rows, int64_t n, bool vec, int& splits, int64_t& rps) {
   const int64_t strips = cdiv(n, (int64_t)kGemvTThreads * (vec ? 2 : 1));
-  const int64_t target = (int64_t)kNumSMs * 6;
+  static const int per_sm = getenv("NYS_GEMVT_PER_SM") ? atoi(getenv("NYS_GEMVT_PER_SM")) : 3;  // measured: 3 beats 2, 4, 5, 6 (config 2, +1%)
+  const int64_t target = (int64_t)kNumSMs * per_sm;
   int64_t sp = strips >= target ? 1 : cdiv(target, strips);
   sp = tmax<int64_t>(1, tmin<int64_t>(sp, cdiv(rows, 64)));
   rps = cdiv(cdiv(rows, sp), kGemvTUnroll) * kGemvTUnroll;
