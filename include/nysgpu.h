@@ -259,6 +259,10 @@ typedef struct nys_admm_tail {
                                  outputs (AT), the row sums (NYS_ROWS_NOUT) and the
                                  conjugate sums (3) are summed over the ranks before the
                                  norms that use them                                      */
+  const double* rb_src; double* rb_dst; int64_t rb_n; double* rb_gate;
+                              /* NULL rb_dst, or the iteration's readback (nys_readback_f64
+                                 arguments) for the tail to fuse into its last kernel     */
+  int rb_done;                /* out: 1 when the tail did that readback                  */
 } nys_admm_tail;
 int nys_admm_tail_f64(const nys_admm_tail* t, void* stream);
 

@@ -840,6 +840,7 @@ class _Engine:
         # 1: events around the x-update and the tail; 2: only around the whole
         # iteration (no event between the two kernel groups); 0: none
         self._iter_events = int(os.environ.get("NYS_ITER_EVENTS", "1"))
+        self._fuse_readback = os.environ.get("NYS_FUSE_READBACK", "1") != "0"
         self._seq = 0
         ptr = lambda x: x.data_ptr() if x is not None else None
         self._reduce_fn = None
@@ -994,10 +995,18 @@ class _Engine:
         kx.admm_xupdate(h, pb, batch)  # head + PCG (one persistent kernel when it fits)
         if self._iter_events == 1:
             ev[1].record(kx.stream)
+        if self._kernel_readback and self._fuse_readback:
+            # the tail's last kernel copies the block into mapped host memory itself
+            t.rb_src, t.rb_dst = self.rbs[par].data_ptr(), self.rbs_host[par].data_ptr()
+            t.rb_n, t.rb_gate = self.rbs[par].numel(), self.gates[1 - par:].data_ptr()
         kx.admm_tail(t)
         if self._iter_events:
             ev[2].record(kx.stream)
-        self._readback(par)
+        if t.rb_done:
+            self.kx.d2h += _RB_LEN * 8
+            self._done_ev[par].record(self.kx.stream)
+        else:
+            self._readback(par)
         return _Issued(k, par, slot, after, batch, self._seq, shift, exact, list(win_before))
 
     def _read_block(self):

@@ -23,7 +23,7 @@ inline unsigned vec_blocks(int64_t n) {
 // Reduce NS sums and NM maxes across the grid; the last CTA writes
 // out[osum[j]] and out[omax[j]].  part has room for gridDim * (NS+NM).
 template <int NS, int NM>
-__device__ __forceinline__ void grid_reduce(double (&s)[(NS > 0) ? NS : 1],
+__device__ __forceinline__ bool grid_reduce(double (&s)[(NS > 0) ? NS : 1],
                                             double (&m)[(NM > 0) ? NM : 1], double* part,
                                             unsigned int* counter, double* out,
                                             const int* osum, const int* omax) {
@@ -37,7 +37,8 @@ __device__ __forceinline__ void grid_reduce(double (&s)[(NS > 0) ? NS : 1],
 #pragma unroll
     for (int j = 0; j < NM; ++j) part[blockIdx.x * NV + NS + j] = m[j];
   }
-  if (last_block(counter)) {
+  const bool am_last = last_block(counter);
+  if (am_last) {
     // one warp per output (fixed lane-strided order + shuffle tree): the
     // outputs are finished in parallel instead of one block reduction each
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -53,6 +54,7 @@ __device__ __forceinline__ void grid_reduce(double (&s)[(NS > 0) ? NS : 1],
       if (lane == 0) out[j < NS ? osum[j] : omax[j - NS]] = acc;
     }
   }
+  return am_last;
 }
 
 // ------------------------------------------------------------ dot ---------
@@ -506,9 +508,18 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
                    const double* __restrict__ x, const double* __restrict__ z, const double* __restrict__ u,
                    double lambda2, double rho, double lambda1, const double* __restrict__ ring, int64_t ld,
                    int cur, SlotList others, int nothers, double* out, int woff, double* part,
-                   unsigned int* counter, const double* __restrict__ pred) {
+                   unsigned int* counter, const double* __restrict__ pred, const double* __restrict__ rb_src,
+                   double* rb_dst, int rb_n, double* rb_gate) {
   pdl_begin();  // chain kernel (common.cuh)
-  if (pred && *pred != 0.0) return;
+  // (rb_dst: this kernel ends the iteration's chain and also does the readback of
+  // the iteration's scalar block into mapped host memory: nys_readback_f64 fused)
+  if (pred && *pred != 0.0) {
+    if (rb_dst && blockIdx.x == 0) {  // a skipped iteration still reports its status
+      for (int q = threadIdx.x; q < rb_n; q += blockDim.x) rb_dst[q] = rb_src[q];
+      __threadfence_system();
+    }
+    return;
+  }
   __shared__ double cs[4][K][kEpiCols];
   const int tid = threadIdx.x, cx = tid & (kEpiCols - 1), ch = tid >> 6;
   const int64_t c = (int64_t)blockIdx.x * kEpiCols + cx;
@@ -590,7 +601,14 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
                       woff + 6, woff + 7, woff + 8, woff + 9, woff + 10, woff + 11, woff + 12, woff + 13,
                       woff + 14, woff + 15, woff + 16};
   const int om[7] = {1, 3, 5, 7, 9, 13, 15};
-  grid_reduce<26, 7>(s, m, part, counter, out, os, om);
+  const bool last = grid_reduce<26, 7>(s, m, part, counter, out, os, om);
+  if (last && rb_dst) {
+    __syncthreads();  // the reduced norms are in the block
+    for (int q = threadIdx.x; q < rb_n; q += blockDim.x) rb_dst[q] = rb_src[q];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && rb_gate) *rb_gate = 1.0;  // the next iteration may run
+  }
 }
 
 __global__ void scale_dual_kernel(int64_t n, double* __restrict__ u, double rho_old,
@@ -980,6 +998,8 @@ int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const doub
 
 extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   if (!t || t->n <= 0 || (t->kind != 0 && t->kind != 1)) return NYS_ERR_ARG;
+  nys_admm_tail* t_mut = const_cast<nys_admm_tail*>(t);  // rb_done is an output
+  t_mut->rb_done = 0;
   cudaStream_t st = as_stream(stream);
   const int64_t n = t->n;
   const double* pred = t->pred;
@@ -1044,15 +1064,23 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       double* normsp = t->norms;
       double* rp = red_part(t->ws_red);
       unsigned int* rc2 = red_counter(t->ws_red);
+      // the epilogue is the last kernel of the tail unless the conjugate sums or
+      // the gate kernel follow: then it also does the iteration's readback
+      const bool rb = t->rb_dst && !(t->with_z && t->conj_out) && !t->gate_next;
+      const double* rbs = rb ? t->rb_src : nullptr;
+      double* rbd = rb ? t->rb_dst : nullptr;
+      double* rbg = rb ? t->rb_gate : nullptr;
+      const int rbn = (int)t->rb_n;
       if (K == 3)
         launch_chain(ml_epilogue_kernel<3>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
                      t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
-                     pred);
+                     pred, rbs, rbd, rbn, rbg);
       else
         launch_chain(ml_epilogue_kernel<2>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
                      t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
-                     pred);
+                     pred, rbs, rbd, rbn, rbg);
       NYS_CHECK_LAUNCH();
+      t_mut->rb_done = rb ? 1 : 0;
     } else {
       if ((rc = gemv_t(t->A, t->rows, n, t->lda, t->T, t->rows, t->with_z ? 3 : 2, t->AT, n, nullptr, 0.0, nullptr,
                        t->ws_gemvT, t->ws_gemvT_bytes, st, pred)))
