@@ -20,6 +20,37 @@ inline unsigned vec_blocks(int64_t n) {
   return (unsigned)tmax<int64_t>(1, tmin<int64_t>(cdiv(n, kVecThreads), kVecMaxBlocks));
 }
 
+// Block sums of NS (8 <= NS <= 32) values per thread, written by warp 0 to
+// dst[0..NS).  In a warp, a butterfly reduce-scatter (31 shuffles for up to 32
+// values instead of 5 per value) leaves lane l with the warp sum of value l;
+// warp 0 then adds the warps' sums in a fixed order.  Deterministic.
+template <int NS>
+__device__ __forceinline__ void block_sum_to(const double (&s)[NS], double* shT, double* dst) {
+  static_assert(NS >= 1 && NS <= 32, "block_sum_to");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = j < NS ? s[j] : 0.0;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;  // keeps the upper half of the current block of slots
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const double send = up ? v[i] : v[i + o];
+      const double keep = up ? v[i + o] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  __syncthreads();
+  shT[wid * 32 + lane] = v[0];  // slot 0 of lane l = value l
+  __syncthreads();
+  if (wid == 0 && lane < NS) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += shT[w * 32 + lane];
+    dst[lane] = t;
+  }
+}
+
 // Reduce NS sums and NM maxes across the grid; the last CTA writes
 // out[osum[j]] and out[omax[j]].  part has room for gridDim * (NS+NM).
 template <int NS, int NM>
@@ -29,11 +60,18 @@ __device__ __forceinline__ bool grid_reduce(double (&s)[(NS > 0) ? NS : 1],
                                             const int* osum, const int* omax) {
   __shared__ double sh[32 * ((NS > 0 ? NS : 1) + (NM > 0 ? NM : 1))];
   constexpr int NV = NS + NM;
-  if (NS > 0) block_sum<((NS > 0) ? NS : 1)>(s, sh);
+  constexpr bool kScatter = NS >= 8;  // many sums: reduce-scatter instead of one tree per value
+  if (kScatter) {
+    __shared__ double shT[32 * 32];
+    block_sum_to<((NS > 0) ? NS : 1)>(s, shT, part + (size_t)blockIdx.x * NV);
+  } else if (NS > 0) {
+    block_sum<((NS > 0) ? NS : 1)>(s, sh);
+  }
   if (NM > 0) block_max<((NM > 0) ? NM : 1)>(m, sh);
   if (threadIdx.x == 0) {
+    if (!kScatter)
 #pragma unroll
-    for (int j = 0; j < NS; ++j) part[blockIdx.x * NV + j] = s[j];
+      for (int j = 0; j < NS; ++j) part[blockIdx.x * NV + j] = s[j];
 #pragma unroll
     for (int j = 0; j < NM; ++j) part[blockIdx.x * NV + NS + j] = m[j];
   }
