@@ -259,9 +259,11 @@ typedef struct nys_admm_tail {
                                  outputs (AT), the row sums (NYS_ROWS_NOUT) and the
                                  conjugate sums (3) are summed over the ranks before the
                                  norms that use them                                      */
-  const double* rb_src; double* rb_dst; int64_t rb_n; double* rb_gate;
+  const double* rb_src; double* rb_dst; int64_t rb_n; double* rb_gate; double rb_tag;
                               /* NULL rb_dst, or the iteration's readback (nys_readback_f64
-                                 arguments) for the tail to fuse into its last kernel     */
+                                 arguments) for the tail to fuse into its last kernel;
+                                 rb_tag != 0 is then stored at rb_dst[rb_n] once the block
+                                 is complete (the host may poll it instead of an event)   */
   int rb_done;                /* out: 1 when the tail did that readback                  */
 } nys_admm_tail;
 int nys_admm_tail_f64(const nys_admm_tail* t, void* stream);

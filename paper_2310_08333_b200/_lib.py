@@ -74,7 +74,7 @@ class AdmmTail(C.Structure):
         ("ws_gemv", P), ("ws_gemv_bytes", SZ), ("ws_gemvT", P), ("ws_gemvT_bytes", SZ), ("ws_red", P),
         ("pred", P), ("gate_next", P), ("conj_out", P), ("order", P), ("zu_done", C.c_int),
         ("reduce", P), ("reduce_user", P),
-        ("rb_src", P), ("rb_dst", P), ("rb_n", I64), ("rb_gate", P), ("rb_done", C.c_int),
+        ("rb_src", P), ("rb_dst", P), ("rb_n", I64), ("rb_gate", P), ("rb_tag", F64), ("rb_done", C.c_int),
     ]
 
 # nys_reduce_fn (include/nysgpu.h): the host-side all-reduce hook of the sharded drivers

@@ -237,6 +237,8 @@ class _Issued:
     exact: bool
     win_before: list
     reissue: Optional["_Issued"] = None
+    polled: bool = False  # the readback block carries tag `tag` (no stream event to wait on)
+    ring: bool = False    # iteration time from the per-iteration mark ring (no ev[0], ev[2])
 
 
 class _ParityWork:
@@ -824,7 +826,7 @@ class _Engine:
         under the descriptors."""
         kx, L, n = self.kx, self.kx.L, self.n
         self.rbs = kx.zeros(2, _RB_LEN)
-        self.rbs_host = [_host_buffer(_RB_LEN, kx.device) for _ in range(2)]
+        self.rbs_host = [_host_buffer(_RB_LEN + 1, kx.device) for _ in range(2)]  # + completion tag
         # pinned host memory is device-addressable under UVA: a kernel writes the
         # readback block straight into it (no copy engine in the pipeline)
         self._kernel_readback = (hasattr(kx, "readback") and kx.device.type == "cuda"
@@ -841,6 +843,10 @@ class _Engine:
         # iteration (no event between the two kernel groups); 0: none
         self._iter_events = int(os.environ.get("NYS_ITER_EVENTS", "1"))
         self._fuse_readback = os.environ.get("NYS_FUSE_READBACK", "1") != "0"
+        # with the fused readback the host polls the block's completion tag, so no
+        # stream event sits between an iteration's last kernel and the next x-update
+        self._poll = self._fuse_readback and os.environ.get("NYS_POLL_READBACK", "1") != "0"
+        self._ev_ring = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         self._seq = 0
         ptr = lambda x: x.data_ptr() if x is not None else None
         self._reduce_fn = None
@@ -990,24 +996,34 @@ class _Engine:
             t.inf_first, t.inf_last = after[0], after[-1]
         batch = min(16, max(2, self._last_cg + 1))
         ev = self._ev[par]
-        if self._iter_events:
+        fused = self._kernel_readback and self._fuse_readback
+        poll = fused and self._poll
+        if self._iter_events and not poll:
             ev[0].record(kx.stream)
         kx.admm_xupdate(h, pb, batch)  # head + PCG (one persistent kernel when it fits)
         if self._iter_events == 1:
             ev[1].record(kx.stream)
-        if self._kernel_readback and self._fuse_readback:
+            if poll:
+                self._ev_ring[k % 4].record(kx.stream)
+        if fused:
             # the tail's last kernel copies the block into mapped host memory itself
             t.rb_src, t.rb_dst = self.rbs[par].data_ptr(), self.rbs_host[par].data_ptr()
             t.rb_n, t.rb_gate = self.rbs[par].numel(), self.gates[1 - par:].data_ptr()
+            t.rb_tag = float(self._seq) if poll else 0.0
         kx.admm_tail(t)
-        if self._iter_events:
+        if self._iter_events and not poll:
             ev[2].record(kx.stream)
+        polled = False
         if t.rb_done:
             self.kx.d2h += _RB_LEN * 8
-            self._done_ev[par].record(self.kx.stream)
+            if poll:
+                polled = True
+            else:
+                self._done_ev[par].record(self.kx.stream)
         else:
             self._readback(par)
-        return _Issued(k, par, slot, after, batch, self._seq, shift, exact, list(win_before))
+        return _Issued(k, par, slot, after, batch, self._seq, shift, exact, list(win_before), polled=polled,
+                       ring=poll)
 
     def _read_block(self):
         """The setup / per-step readback block in one D2H copy; returns
@@ -1024,13 +1040,26 @@ class _Engine:
             t = self._tails[par]
             self.kx.readback(self.rbs[par], self.rbs_host[par], self.gates[1 - par:].data_ptr(), t.pred)
         else:
-            self.rbs_host[par].copy_(self.rbs[par], non_blocking=True)
+            self.rbs_host[par][:_RB_LEN].copy_(self.rbs[par], non_blocking=True)
         self.kx.d2h += _RB_LEN * 8
         self._done_ev[par].record(self.kx.stream)
 
-    def _read(self, par):
-        self._done_ev[par].synchronize()
-        h = self.rbs_host[par].numpy().copy()
+    def _read(self, par, tag=None):
+        if tag is None:
+            self._done_ev[par].synchronize()
+        else:
+            # spin on the completion tag the tail's last kernel stores after the block
+            buf = self.rbs_host[par].numpy()
+            spins = 0
+            while buf[_RB_LEN] != tag:
+                spins += 1
+                if spins % 4096 == 0:
+                    time.sleep(0)
+                    if spins % (4096 * 64) == 0:
+                        self.kx.sync()  # surfaces a device error; the tag must be there after it
+                        if buf[_RB_LEN] != tag:
+                            raise NumericalError("readback block of the iteration never arrived")
+        h = self.rbs_host[par].numpy()[:_RB_LEN].copy()
         C = _lib.CG_NSLOTS
         return h[8:8 + C], np.concatenate([h[8 + C:], h[:8]])
 
@@ -1039,9 +1068,15 @@ class _Engine:
         re-launch the speculated successor, whose closed gate made it a
         no-op), and return (CgReport, stats, linsys_s, prox_s)."""
         kx, par = self.kx, it.par
-        sc, st = self._read(par)
+        sc, st = self._read(par, float(it.tag) if it.polled else None)
         ev = self._ev[par]
-        if self._iter_events == 1:
+        if it.ring:
+            # no events around the x-update and the tail: the whole iteration, from
+            # the ring of per-iteration marks between the two kernel groups
+            lin_ms = (self._ev_ring[(it.k - 1) % 4].elapsed_time(self._ev_ring[it.k % 4])
+                      if self._iter_events == 1 and it.k > 1 else 0.0)
+            tail_ms = 0.0
+        elif self._iter_events == 1:
             lin_ms, tail_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
         elif self._iter_events == 2:
             lin_ms, tail_ms = ev[0].elapsed_time(ev[2]), 0.0

@@ -547,7 +547,7 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
                    double lambda2, double rho, double lambda1, const double* __restrict__ ring, int64_t ld,
                    int cur, SlotList others, int nothers, double* out, int woff, double* part,
                    unsigned int* counter, const double* __restrict__ pred, const double* __restrict__ rb_src,
-                   double* rb_dst, int rb_n, double* rb_gate) {
+                   double* rb_dst, int rb_n, double* rb_gate, double rb_tag) {
   pdl_begin();  // chain kernel (common.cuh)
   // (rb_dst: this kernel ends the iteration's chain and also does the readback of
   // the iteration's scalar block into mapped host memory: nys_readback_f64 fused)
@@ -555,6 +555,8 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
     if (rb_dst && blockIdx.x == 0) {  // a skipped iteration still reports its status
       for (int q = threadIdx.x; q < rb_n; q += blockDim.x) rb_dst[q] = rb_src[q];
       __threadfence_system();
+      __syncthreads();
+      if (threadIdx.x == 0 && rb_tag != 0.0) *(volatile double*)(rb_dst + rb_n) = rb_tag;  // block complete
     }
     return;
   }
@@ -645,7 +647,12 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
     for (int q = threadIdx.x; q < rb_n; q += blockDim.x) rb_dst[q] = rb_src[q];
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0 && rb_gate) *rb_gate = 1.0;  // the next iteration may run
+    if (threadIdx.x == 0) {
+      if (rb_gate) *rb_gate = 1.0;  // the next iteration may run
+      // the host polls this tag instead of waiting on a stream event (an event
+      // between this kernel and the next x-update would serialise their launches)
+      if (rb_tag != 0.0) *(volatile double*)(rb_dst + rb_n) = rb_tag;
+    }
   }
 }
 
@@ -1109,14 +1116,15 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       double* rbd = rb ? t->rb_dst : nullptr;
       double* rbg = rb ? t->rb_gate : nullptr;
       const int rbn = (int)t->rb_n;
+      const double rbt = t->rb_tag;
       if (K == 3)
         launch_chain(ml_epilogue_kernel<3>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
                      t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
-                     pred, rbs, rbd, rbn, rbg);
+                     pred, rbs, rbd, rbn, rbg, rbt);
       else
         launch_chain(ml_epilogue_kernel<2>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
                      t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
-                     pred, rbs, rbd, rbn, rbg);
+                     pred, rbs, rbd, rbn, rbg, rbt);
       NYS_CHECK_LAUNCH();
       t_mut->rb_done = rb ? 1 : 0;
     } else {
