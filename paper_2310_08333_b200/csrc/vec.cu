@@ -184,7 +184,25 @@ precond_utv_kernel(const double* __restrict__ U, int64_t n, int r, int64_t ldu,
   for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
   const int64_t i0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t i1 = min(n, i0 + rows_per_block);
-  for (int64_t i = i0 + warp; i < i1; i += NW) {
+  int64_t i = i0 + warp;
+  // four rows per step: all of their loads are issued before the FMAs, which
+  // still accumulate the rows in order (same sums as one row at a time)
+  for (; i + 3 * NW < i1; i += 4 * NW) {
+    const double v0 = v[i], v1 = v[i + NW], v2 = v[i + 2 * NW], v3 = v[i + 3 * NW];
+    const double* u0 = U + i * ldu;
+    const double* u1 = u0 + NW * ldu;
+    const double* u2 = u1 + NW * ldu;
+    const double* u3 = u2 + NW * ldu;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int j = lane + 32 * c;
+      if (j < r) {
+        const double a0 = u0[j], a1 = u1[j], a2 = u2[j], a3 = u3[j];
+        acc[c] = fma(a3, v3, fma(a2, v2, fma(a1, v1, fma(a0, v0, acc[c]))));
+      }
+    }
+  }
+  for (; i < i1; i += NW) {
     const double vi = v[i];
     const double* ui = U + i * ldu;
 #pragma unroll
@@ -204,6 +222,7 @@ precond_utv_kernel(const double* __restrict__ U, int64_t n, int r, int64_t ldu,
     for (int w = 0; w < NW; ++w) s += wsum[w * r + j];
     part[(int64_t)blockIdx.x * r + j] = s;
   }
+  if (!counter) return;  // the column sums run in utv_reduce_kernel (many CTAs)
   if (last_block(counter)) {
     const double lr = lam[r - 1] + nu;
     for (int j = threadIdx.x; j < r; j += kPcThreads) {
@@ -220,6 +239,25 @@ precond_utv_kernel(const double* __restrict__ U, int64_t n, int r, int64_t ldu,
       const double head = __dmul_rn(lr, h / __dadd_rn(lam[j], nu));
       coef[j] = __dadd_rn(head, -h);
     }
+  }
+}
+
+// the column sums of the U^T v block partials, one CTA per column (the single
+// last CTA of precond_utv_kernel walks ~300 partials per column serially:
+// 74 us of the 82 at n = 1e5), then the Eq. (11) coefficient of that column
+__global__ void __launch_bounds__(256)
+utv_reduce_kernel(const double* __restrict__ part, int nparts, int r, const double* __restrict__ lam, double nu,
+                  double* __restrict__ coef, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  __shared__ double sh[8];
+  const int j = blockIdx.x;
+  double h[1] = {0.0};
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x) h[0] += part[(int64_t)b * r + j];
+  block_sum<1>(h, sh);
+  if (threadIdx.x == 0) {
+    const double lr = lam[r - 1] + nu;
+    const double head = __dmul_rn(lr, h[0] / __dadd_rn(lam[j], nu));
+    coef[j] = __dadd_rn(head, -h[0]);
   }
 }
 
@@ -834,9 +872,15 @@ int precond_apply(const double* U, int64_t n, int r, int64_t ldu, const double* 
   const int64_t blocks = tmin<int64_t>(kNumSMs * 2, tmax<int64_t>(1, cdiv(n, 32)));
   const int64_t rpb = cdiv(n, blocks);
   const int64_t nb = cdiv(n, rpb);
+  // many row blocks: their column sums in a separate reduction kernel
+  const bool split = nb > 32;
   precond_utv_kernel<<<(unsigned)nb, kPcThreads, (kPcThreads / 32) * r * sizeof(double), st>>>(
-      U, n, r, ldu, v, rpb, hpart, red_counter(ws), lam, nu, coef, pred);
+      U, n, r, ldu, v, rpb, hpart, split ? nullptr : red_counter(ws), lam, nu, coef, pred);
   NYS_CHECK_LAUNCH();
+  if (split) {
+    utv_reduce_kernel<<<(unsigned)r, 256, 0, st>>>(hpart, (int)nb, r, lam, nu, coef, pred);
+    NYS_CHECK_LAUNCH();
+  }
   return precond_apply_z(U, n, r, ldu, v, z, rdot, rz, ws, st, pred);
 }
 
