@@ -600,7 +600,17 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
   }
   __shared__ double cs[4][K][kEpiCols];
   const int tid = threadIdx.x, cx = tid & (kEpiCols - 1), ch = tid >> 6;
-  const int64_t c = (int64_t)blockIdx.x * kEpiCols + cx;
+  double s[9 + 17], m[7];
+#pragma unroll
+  for (int j = 0; j < 26; ++j) s[j] = 0.0;
+#pragma unroll
+  for (int j = 0; j < 7; ++j) m[j] = 0.0;
+  double viol = -INFINITY;
+  // column tiles of kEpiCols, grid-stride (a capped grid keeps the final
+  // reduction short for large n: 1563 tiles at n = 1e5)
+  const int64_t ntiles = cdiv(n, (int64_t)kEpiCols);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int64_t c = tile * kEpiCols + cx;
   {
     // splits ch, ch + 4, ... of column c: four independent chains so four
     // groups of loads are in flight per round trip (fixed combination order)
@@ -624,12 +634,6 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
     for (int j = 0; j < K; ++j) cs[ch][j][cx] = (acc[0][j] + acc[1][j]) + (acc[2][j] + acc[3][j]);
   }
   __syncthreads();
-  double s[9 + 17], m[7];
-#pragma unroll
-  for (int j = 0; j < 26; ++j) s[j] = 0.0;
-#pragma unroll
-  for (int j = 0; j < 7; ++j) m[j] = 0.0;
-  double viol = -INFINITY;
   if (ch == 0 && c < n) {
     double at[K];
 #pragma unroll
@@ -643,36 +647,38 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
     const double g = __dadd_rn(at[0], __dmul_rn(lambda2, xi));
     const double ru = __dmul_rn(rho, ui);
     const double rd = __dadd_rn(g, ru);
-    s[0] = rp * rp;
-    s[1] = rd * rd;
-    s[2] = xi * xi;
-    s[3] = zi * zi;
-    s[4] = ru * ru;
-    s[5] = fabs(zi);
-    s[6] = xi * at[0];
-    m[0] = fabs(rp);
-    m[1] = fabs(rd);
-    m[2] = fabs(xi);
-    m[3] = fabs(zi);
-    m[4] = fabs(ru);
+    s[0] += rp * rp;
+    s[1] += rd * rd;
+    s[2] += xi * xi;
+    s[3] += zi * zi;
+    s[4] += ru * ru;
+    s[5] += fabs(zi);
+    s[6] += xi * at[0];
+    m[0] = fmax(m[0], fabs(rp));
+    m[1] = fmax(m[1], fabs(rd));
+    m[2] = fmax(m[2], fabs(xi));
+    m[3] = fmax(m[3], fabs(zi));
+    m[4] = fmax(m[4], fabs(ru));
     if (K == 3) {
       const double a = fabs(at[K - 1]);
-      m[5] = a;
+      m[5] = fmax(m[5], a);
       const double e = fmax(a - lambda1, 0.0);
-      s[8] = e * e;
+      s[8] += e * e;
     }
     // window_norms_kernel, element c
     if (nothers > 0) {
       const double xc = ring[(int64_t)cur * ld + c];
-      s[9] = xc * xc;
+      s[9] += xc * xc;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j < nothers) {
           const double dd = __dadd_rn(xc, -ring[(int64_t)others.idx[j] * ld + c]);
-          s[10 + j] = dd * dd;
+          s[10 + j] += dd * dd;
         }
       }
     }
+  }
+  __syncthreads();  // cs is rewritten by the next tile
   }
   m[6] = viol;
   const int os[26] = {0, 2, 4, 6, 8, 10, 11, 12, 14, woff, woff + 1, woff + 2, woff + 3, woff + 4, woff + 5,
@@ -1146,7 +1152,7 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       SlotList sl;
       const int no = (t->ring && t->nothers > 0) ? t->nothers : 0;
       for (int j = 0; j < 16; ++j) sl.idx[j] = j < no ? t->others[j] : 0;
-      const unsigned eb = (unsigned)cdiv(n, (int64_t)kEpiCols);
+      const unsigned eb = (unsigned)tmin<int64_t>(cdiv(n, (int64_t)kEpiCols), 2 * kNumSMs);
       const double* Pc = P;
       const double* uc = t->u;
       const double* ringc = t->ring;
