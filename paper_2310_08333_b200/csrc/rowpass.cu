@@ -229,8 +229,16 @@ static int rowpass_launch(const RowpassPlan& p, const double* A, int64_t rows, i
     attr[wz] = true;
   }
   const unsigned grid = (unsigned)tmin<int64_t>(kNumSMs, rows);
-  launch_chain(fn, dim3(grid), dim3(kRpThreads), p.smem, st, false, A, rows, n, lda, x, z, b, loss, p.Wp, p.S, tg,
-               w, thx, tnu, rowsums, part, counter, pred, order);
+  // launched without the PDL attribute: the persistent solve before it is a
+  // cooperative kernel, and letting this pass be scheduled early into it was
+  // measured slower
+  static const bool pdl = getenv("NYS_RP_PDL") && getenv("NYS_RP_PDL")[0] == '1';
+  if (pdl)
+    launch_chain(fn, dim3(grid), dim3(kRpThreads), p.smem, st, false, A, rows, n, lda, x, z, b, loss, p.Wp, p.S, tg,
+                 w, thx, tnu, rowsums, part, counter, pred, order);
+  else
+    fn<<<grid, kRpThreads, p.smem, st>>>(A, rows, n, lda, x, z, b, loss, p.Wp, p.S, tg, w, thx, tnu, rowsums, part,
+                                         counter, pred, order);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
