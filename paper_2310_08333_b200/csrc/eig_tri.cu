@@ -159,6 +159,213 @@ tridiag_kernel(int s, const double* __restrict__ A, double* __restrict__ d, doub
   if (tid == 0 && s >= 1) e[s - 1] = 0.0;
 }
 
+// Same reduction with the next column's symv fused into the rank-2 update
+// (look-ahead by one column) and ONE barrier per column:
+//   A  every warp recomputes the updated first row of A22 in registers (the
+//      column the next reflector comes from; only its diagonal is stored), then the
+//      next reflector v' from it: norms by warp_sum, identical in all warps;
+//   B  each warp updates its rows of A22 (columns >= 1) and, while the new
+//      values are in registers, takes their dot with v' -> p' = tau' A'' v'
+//      (one warp_sum per row; two rows in flight).
+// A22 is read and written once per column instead of read twice and written
+// once, and p.v is re-summed from shared memory after the barrier.
+__device__ __forceinline__ void tri_reflector(double alpha, double xn2, double& tk, double& beta, double& scal) {
+  if (xn2 == 0.0) {
+    tk = 0.0;
+    beta = alpha;
+    scal = 0.0;
+  } else {
+    beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+    tk = (beta - alpha) / beta;
+    scal = 1.0 / (alpha - beta);
+  }
+}
+
+// One column of tridiag_fused_kernel with NC = ceil(m / 32) column chunks per
+// lane (the trailing block shrinks: no issue slots on dead chunks).
+template <int NC>
+__device__ __forceinline__ double tri_fused_step(int s, int k, int ld, double* __restrict__ a,
+                                                 double* __restrict__ vsb, double* __restrict__ pwb,
+                                                 double* __restrict__ d, double* __restrict__ e,
+                                                 double* __restrict__ VhT, double* __restrict__ tau, double tk) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int m = s - k - 1;
+  const double* vs = vsb + (k & 1) * s;
+  const double* pw = pwb + (k & 1) * s;
+  double* vsn = vsb + ((k + 1) & 1) * s;
+  double* pwn = pwb + ((k + 1) & 1) * s;
+  double vj[NC], wj[NC];
+  double pv = 0.0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = lane + 32 * c;
+    vj[c] = j < m ? vs[j] : 0.0;
+    wj[c] = j < m ? pw[j] : 0.0;
+    pv = fma(wj[c], vj[c], pv);
+  }
+  pv = warp_sum(pv);
+  const double hpv = 0.5 * tk * pv;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) wj[c] = fma(-hpv, vj[c], wj[c]);
+  // A: updated row 0 of A22 (global row k+1)
+  const double v0 = __shfl_sync(0xffffffffu, vj[0], 0), w0 = __shfl_sync(0xffffffffu, wj[0], 0);
+  double t0[NC];
+  double* a0 = a + (k + 1) * ld + (k + 1);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = lane + 32 * c;
+    t0[c] = j < m ? a0[j] - fma(v0, wj[c], w0 * vj[c]) : 0.0;
+  }
+  // row k+1 is final after this update (no write-back: other warps are
+  // still reading it): its diagonal, and at the last column its e
+  if (tid == 0) d[k + 1] = t0[0];
+  if (tid == 1 && k + 3 == s) e[k + 1] = t0[0];
+  const bool next = k + 3 < s;  // a reflector for column k+1 exists
+  double vn[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) vn[c] = 0.0;
+  double tkn = 0.0;
+  if (next) {
+    double xn2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int j = lane + 32 * c;
+      if (j >= 2) xn2 = fma(t0[c], t0[c], xn2);
+    }
+    xn2 = warp_sum(xn2);
+    const double alpha = __shfl_sync(0xffffffffu, t0[0], 1);
+    double beta, scal;
+    tri_reflector(alpha, xn2, tkn, beta, scal);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int j = lane + 32 * c;
+      vn[c] = j == 1 ? 1.0 : ((j >= 2 && j < m) ? t0[c] * scal : 0.0);
+      if (warp == 0 && j >= 1 && j < m) {
+        vsn[j - 1] = vn[c];
+        VhT[(size_t)(k + 1) * s + (k + 1 + j)] = vn[c];
+      }
+    }
+    if (tid == 0) {
+      tau[k + 1] = tkn;
+      e[k + 1] = beta;
+    }
+  }
+  // B: rows 1..m-1 of A22, columns >= 1; fused dot with v'
+  auto row = [&](int i) -> double {
+    double* ar = a + (k + 1 + i) * ld + (k + 1);
+    const double vi = vs[i], wi = fma(-hpv, vi, pw[i]);
+    double dot = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int j = lane + 32 * c;
+      if (j >= 1 && j < m) {
+        const double t = ar[j] - fma(vi, wj[c], wi * vj[c]);
+        ar[j] = t;
+        dot = fma(t, vn[c], dot);
+      }
+    }
+    return dot;
+  };
+  int i = 1 + warp;
+  for (; i + nw < m; i += 2 * nw) {
+    double d0 = row(i), d1 = row(i + nw);
+    if (next) {
+      d0 = warp_sum(d0);
+      d1 = warp_sum(d1);
+      if (lane == 0) {
+        pwn[i - 1] = tkn * d0;
+        pwn[i + nw - 1] = tkn * d1;
+      }
+    }
+  }
+  if (i < m) {
+    double d0 = row(i);
+    if (next) {
+      d0 = warp_sum(d0);
+      if (lane == 0) pwn[i - 1] = tkn * d0;
+    }
+  }
+  return tkn;
+}
+
+__global__ void __launch_bounds__(kTriThreads)
+tridiag_fused_kernel(int s, const double* __restrict__ A, double* __restrict__ d, double* __restrict__ e,
+                     double* __restrict__ VhT, double* __restrict__ tau) {
+  extern __shared__ double sm[];
+  const int ld = s | 1;
+  double* a = sm;                   // s x ld
+  double* vsb = a + (size_t)s * ld;  // 2 x s: v of the current / next reflector
+  double* pwb = vsb + 2 * s;         // 2 x s: p = tau A22 v
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int t = tid; t < s * s; t += blockDim.x) {
+    const int i = t / s, j = t - i * s;
+    a[i * ld + j] = A[t];
+  }
+  __syncthreads();
+  double tk = 0.0;
+  if (s >= 3) {  // first reflector (column 0 = row 0) and its symv
+    const int m = s - 1;
+    double x[kTriCols], v[kTriCols];
+    double xn2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < kTriCols; ++c) {
+      const int j = lane + 32 * c;
+      x[c] = j < m ? a[1 + j] : 0.0;
+      if (j >= 1) xn2 = fma(x[c], x[c], xn2);
+    }
+    xn2 = warp_sum(xn2);
+    const double alpha = __shfl_sync(0xffffffffu, x[0], 0);
+    double beta, scal;
+    tri_reflector(alpha, xn2, tk, beta, scal);
+#pragma unroll
+    for (int c = 0; c < kTriCols; ++c) {
+      const int j = lane + 32 * c;
+      v[c] = j == 0 ? 1.0 : (j < m ? x[c] * scal : 0.0);
+      if (warp == 0 && j < m) {
+        vsb[j] = v[c];
+        VhT[1 + j] = v[c];
+      }
+    }
+    if (tid == 0) {
+      tau[0] = tk;
+      e[0] = beta;
+    }
+    for (int i = warp; i < m; i += nw) {
+      const double* ar = a + (1 + i) * ld + 1;
+      double dot = 0.0;
+#pragma unroll
+      for (int c = 0; c < kTriCols; ++c) {
+        const int j = lane + 32 * c;
+        if (j < m) dot = fma(ar[j], v[c], dot);
+      }
+      dot = warp_sum(dot);
+      if (lane == 0) pwb[i] = tk * dot;
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k + 2 < s; ++k) {
+    switch ((s - k + 30) >> 5) {  // ceil(m / 32), m = s - k - 1
+      case 1: tk = tri_fused_step<1>(s, k, ld, a, vsb, pwb, d, e, VhT, tau, tk); break;
+      case 2: tk = tri_fused_step<2>(s, k, ld, a, vsb, pwb, d, e, VhT, tau, tk); break;
+      case 3: tk = tri_fused_step<3>(s, k, ld, a, vsb, pwb, d, e, VhT, tau, tk); break;
+      case 4: tk = tri_fused_step<4>(s, k, ld, a, vsb, pwb, d, e, VhT, tau, tk); break;
+      default: tk = tri_fused_step<kTriCols>(s, k, ld, a, vsb, pwb, d, e, VhT, tau, tk); break;
+    }
+    __syncthreads();
+  }
+  if (s >= 3) {
+    if (tid == 0) {
+      d[0] = a[0];
+      d[s - 1] = a[(s - 1) * ld + (s - 1)];
+      e[s - 1] = 0.0;
+    }
+  } else {
+    for (int i = tid; i < s; i += blockDim.x) d[i] = a[i * ld + i];
+    if (tid == 0 && s >= 2) e[s - 2] = a[(s - 1) * ld + (s - 2)];
+    if (tid == 0 && s >= 1) e[s - 1] = 0.0;
+  }
+}
+
 // --------------------------------------------------------------- K_b ------
 // number of eigenvalues of T strictly below x (LDL^T inertia), e2 = e^2;
 // two shifts per call.  1/q by the MUFU reciprocal approximation and two
@@ -500,7 +707,18 @@ int eig_tri(int s, const double* A, double* V, double* w, void* ws, cudaStream_t
     cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  tridiag_kernel<<<1, kTriThreads, smem, st>>>(s, A, d, e, Vh, tau);
+  static const bool fused = !getenv("NYS_TRI_FUSED") || atoi(getenv("NYS_TRI_FUSED")) != 0;
+  if (fused) {
+    static bool fattr = false;
+    if (!fattr) {
+      cudaFuncSetAttribute(tridiag_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      fattr = true;
+    }
+    tridiag_fused_kernel<<<1, kTriThreads, ((size_t)s * (s | 1) + 4 * (size_t)s) * sizeof(double), st>>>(
+        s, A, d, e, Vh, tau);
+  } else {
+    tridiag_kernel<<<1, kTriThreads, smem, st>>>(s, A, d, e, Vh, tau);
+  }
   NYS_CHECK_LAUNCH();
   bisect_kernel<<<(unsigned)s, 32, 2 * s * sizeof(double), st>>>(s, d, e, w);
   NYS_CHECK_LAUNCH();
