@@ -80,15 +80,23 @@ __device__ __forceinline__ bool grid_reduce(double (&s)[(NS > 0) ? NS : 1],
     // one warp per output (fixed lane-strided order + shuffle tree): the
     // outputs are finished in parallel instead of one block reduction each
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // (the partials are loaded 8 per lane before they are combined, so one L2
+    // round trip covers 256 blocks; the combination order is unchanged)
+    constexpr int kB = 8;
     for (int j = wid; j < NV; j += nw) {
       double acc = 0.0;
-      if (j < NS) {
-        for (unsigned b = lane; b < gridDim.x; b += 32) acc += part[(size_t)b * NV + j];
-        acc = warp_sum(acc);
-      } else {
-        for (unsigned b = lane; b < gridDim.x; b += 32) acc = fmax(acc, part[(size_t)b * NV + j]);
-        acc = warp_max(acc);
+      for (unsigned b0 = lane; b0 < gridDim.x; b0 += 32 * kB) {
+        double v[kB];
+#pragma unroll
+        for (int t = 0; t < kB; ++t) {
+          const unsigned b = b0 + 32 * t;
+          v[t] = b < gridDim.x ? part[(size_t)b * NV + j] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kB; ++t)
+          if (b0 + 32 * t < gridDim.x) acc = j < NS ? acc + v[t] : fmax(acc, v[t]);
       }
+      acc = j < NS ? warp_sum(acc) : warp_max(acc);
       if (lane == 0) out[j < NS ? osum[j] : omax[j - NS]] = acc;
     }
   }
