@@ -165,6 +165,10 @@ size_t nys_hvp_workspace(int64_t rows, int64_t n);
 int nys_hvp_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
                 const double* v, double shift, double* y, double* pAp, int finish, void* ws,
                 size_t ws_bytes, void* stream);
+/* The single-pass plan nys_hvp_f64 takes for a (rows x n, lda) operand:
+ * 1 whole rows per CTA, 2 column-split clusters, 3 16-CTA DSMEM clusters,
+ * 4 grid column strips, 0 two passes (K1 + K2); -1 bad arguments. */
+int nys_hvp_plan(int64_t rows, int64_t n, int64_t lda);
 /* y += shift * v; *dot = v . y when dot != NULL (device scalar). */
 int nys_shift_dot_f64(int64_t n, const double* v, double shift, double* y, double* dot,
                       void* ws, void* stream);

@@ -370,6 +370,18 @@ def ml_dual_value(p: MLSpec, nu):  # problems.py:321-332
     return val
 
 
+def huber_subdiff_distance(p: MLSpec, x):  # problems.py:354-368
+    w = ml_gradient(p, x)
+    active = x != 0.0
+    d2 = float(np.sum((w[active] + p.lambda1 * np.sign(x[active])) ** 2))
+    d2 += float(np.sum(np.maximum(np.abs(w[~active]) - p.lambda1, 0.0) ** 2))
+    return float(np.sqrt(d2))
+
+
+def huber_subdiff_stop(tol=1e-4):  # problems.py:371-384 (on the sparse iterate z)
+    return lambda p, z: huber_subdiff_distance(p, z) <= tol
+
+
 def ml_dual_gap(p: MLSpec, x):  # problems.py:335-351
     nu = ml_dual_point(p, x)
     primal = ml_objective(p, x)
@@ -412,6 +424,8 @@ class Options:
     use_dual_gap: Optional[bool] = None
     eps_dual_gap: float = 1e-4
     rng_seed: int = 0
+    custom_stop: Optional[Callable] = None  # (problem spec, z) -> bool, replaces the built-in test
+    callback: Optional[Callable] = None  # callback(k) after every iteration (admm.py:610-611; bench timing)
 
 
 @dataclass
@@ -434,6 +448,7 @@ class OracleResult:
     penalty_events: list = field(default_factory=list)
     x_bar: Optional[np.ndarray] = None
     z_bar: Optional[np.ndarray] = None
+    certificate: Optional[np.ndarray] = None
     n_sketches: int = 0
     total_s: float = 0.0
     setup_s: float = 0.0
@@ -537,7 +552,7 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
     best = np.inf
     trend = deque(maxlen=26)
     k = 0
-    for k in range(1, opts.max_iter + 1):
+    for k in range(1, opts.max_iter + 1):  # (k is state.k before the time check, admm.py:534-537)
         if opts.time_limit is not None and time.perf_counter() - t_start > opts.time_limit:
             status = "time_limit"
             break
@@ -580,8 +595,12 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
         res.rp_hist.append(rpn)
         res.rd_hist.append(rdn)
 
-        # check_termination (admm.py:227-240)
-        if gap is not None:
+        if opts.callback is not None:
+            opts.callback(k)
+        # check_termination (admm.py:227-240), or the custom rule (admm.py:613-616)
+        if opts.custom_stop is not None:
+            done = bool(opts.custom_stop(problem, z))
+        elif gap is not None:
             done = gap <= opts.eps_dual_gap
         else:
             done = rpn <= np.sqrt(n) * opts.eps_abs + opts.eps_rel * ps and rdn <= np.sqrt(
@@ -601,6 +620,8 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
                 rho_frozen = True
             if st is not None:
                 status = st
+                # admm.py:391, 405 (the certificate property prefers the primal one)
+                res.certificate = rho * du if st.startswith("primal") else dx.copy()
                 break
 
         # cycle guard (admm.py:643-675)

@@ -110,6 +110,7 @@ SIGNATURES = {
     "nys_gemvT_f64": (I32, [P, I64, I64, I64, P, I64, I32, P, I64, P, SZ, P]),
     "nys_hvp_workspace": (SZ, [I64, I64]),
     "nys_hvp_f64": (I32, [P, I64, I64, I64, P, P, F64, P, P, I32, P, SZ, P]),
+    "nys_hvp_plan": (I32, [I64, I64, I64]),
     "nys_shift_dot_f64": (I32, [I64, P, F64, P, P, P, P]),
     "nys_dot_f64": (I32, [I64, P, P, P, P, P]),
     "nys_precond_workspace": (SZ, [I64, I32]),

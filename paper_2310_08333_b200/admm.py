@@ -510,12 +510,12 @@ class _Engine:
         early = None  # sketch of the next iteration, enqueued behind the current one
 
         for k in range(1, opts.max_iter + 1):
+            k_done = k  # the reference sets state.k = k before its time check (admm.py:534-537)
             if opts.time_limit is not None and time.perf_counter() - t_start > opts.time_limit:
                 status = Status.TIME_LIMIT
                 if pending is not None:
                     self._rollback()
                 break
-            k_done = k
             # resketch on the cadence for iterate-dependent Hessians (admm.py:545-551)
             # (never due for an iteration launched ahead, by the lookahead rule)
             early_check = None
@@ -1175,7 +1175,7 @@ class _Engine:
             near_p = t_map < 10 * eps * du and t_sup < 10 * eps * du
             if primal:
                 last, first = win[-1], win[0]
-                cp =self.rho * ((self.uring[last] - self.uring[first]) / DELTA_WINDOW).cpu().numpy()
+                cp = self.rho * ((self.uring[last] - self.uring[first]) / DELTA_WINDOW).cpu().numpy()
         dxn = math.sqrt(max(s[3], 0.0))
         if dxn > 1e-14:
             s_obj = math.sqrt(max(st[_S_PDX], 0.0))
@@ -1184,7 +1184,10 @@ class _Engine:
             dual = s_obj < eps * dxn and s_cone < eps * dxn and s_lin < eps * dxn
             near_d = s_obj < 10 * eps * dxn and s_cone < 10 * eps * dxn and s_lin < 10 * eps * dxn
             if dual:
-                cd = self.dx[0].cpu().numpy().copy()
+                # from the ring slots of k's window (never written by a speculated
+                # k+1), not from the shared dx buffer k+1's tail may already reuse
+                last, first = win[-1], win[0]
+                cd = ((self.ring[last] - self.ring[first]) / DELTA_WINDOW).cpu().numpy()
         if primal and dual:
             status = Status.PRIMAL_AND_DUAL_INFEASIBLE
         elif primal:

@@ -824,7 +824,15 @@ static int cp_launch(const CpPlan& pl, const CgPersistArgs& args, cudaStream_t s
   }
   CgPersistArgs a = args;
   const unsigned grid = (unsigned)tmin<int64_t>(kNumSMs, a.rows);
-  if (launch_chain(fn, dim3(grid), dim3(kCpThreads), pl.smem, st, true, a) != cudaSuccess) return NYS_ERR_CUDA;
+  // one CTA per SM must be co-resident: fewer free SMs -> the batched plan
+  static int fits = -1;
+  if (fits < 0) fits = coop_fits((const void*)fn, grid, kCpThreads, pl.smem) ? 1 : 0;
+  if (!fits) return NYS_ERR_UNSUPPORTED;
+  const int rc = coop_launch_status(launch_chain(fn, dim3(grid), dim3(kCpThreads), pl.smem, st, true, a));
+  if (rc) {
+    if (rc == NYS_ERR_UNSUPPORTED) fits = 0;
+    return rc;
+  }
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
   return debug_sync_check(__FILE__, __LINE__) ? NYS_ERR_CUDA : NYS_OK;
 }

@@ -36,7 +36,52 @@ void debug_report(cudaError_t e, const char* file, int line);
 namespace nys {
 
 constexpr int kWarp = 32;
-constexpr int kNumSMs = 148;  // B200
+// B200: the grid sizes of the streaming kernels and the slice layout of the
+// one-CTA-per-SM cooperative kernels are compiled for 148 SMs.  On a device
+// (or an MPS / green-context share) with fewer SMs the non-cooperative kernels
+// still run correctly (more waves); the cooperative plans check co-residency
+// at launch (coop_fits) and report NYS_ERR_UNSUPPORTED so callers take their
+// non-cooperative plan.
+constexpr int kNumSMs = 148;
+
+// SM count of the current device (cached per device ordinal)
+inline int device_sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  static int cache[64] = {0};
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    v = 0;
+  }
+  if (dev >= 0 && dev < 64) cache[dev] = v;
+  return v;
+}
+
+// Can `grid` CTAs of `fn` (threads, dynamic smem) all be resident at once, as a
+// cooperative launch requires?  (The max-dynamic-smem attribute must be set.)
+inline bool coop_fits(const void* fn, int64_t grid, int threads, size_t smem) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (int64_t)occ * device_sm_count() >= grid;
+}
+
+// Status of a failed cooperative launch: a grid that does not fit (fewer free
+// SMs than planned) is UNSUPPORTED so the caller falls back; the sticky-free
+// launch error is cleared so it is not blamed on the next kernel.
+inline int coop_launch_status(cudaError_t e) {
+  if (e == cudaSuccess) return NYS_OK;
+  cudaGetLastError();
+  return (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorInvalidConfiguration) ? NYS_ERR_UNSUPPORTED
+                                                                                         : NYS_ERR_CUDA;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -581,16 +581,20 @@ int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const doubl
     // single pass over A (csrc/hvp.cu), then a fixed-order sum of the cluster partials
     double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
     static const bool legacy = getenv("NYS_HVP_LEGACY") != nullptr;
-    if (plan.C == 1 && !legacy)
-      return hvp_row(plan, A, rows, n, lda, d, v, P, y, finish ? shift : 0.0, finish ? pAp : nullptr, red_part(ws),
-                     red_counter(ws), st, pred);
-    int rc = hvp_fused(plan, A, rows, n, lda, d, v, P, st, pred);
-    if (rc) return rc;
-    const int64_t rb = tmin<int64_t>(cdiv(n, 32), kRedPartials);
-    gemv_t_reduce<<<(unsigned)rb, 256, 0, st>>>(P, n, 1, plan.nclusters, y, n, finish ? v : nullptr, shift,
-                                                 finish ? pAp : nullptr, red_part(ws), red_counter(ws), pred);
-    NYS_CHECK_LAUNCH();
-    return NYS_OK;
+    int rc = NYS_ERR_UNSUPPORTED;
+    if (plan.C == 1 && !legacy) {
+      rc = hvp_row(plan, A, rows, n, lda, d, v, P, y, finish ? shift : 0.0, finish ? pAp : nullptr, red_part(ws),
+                   red_counter(ws), st, pred);
+      if (rc != NYS_ERR_UNSUPPORTED) return rc;  // else: not co-resident, two passes below
+    } else {
+      rc = hvp_fused(plan, A, rows, n, lda, d, v, P, st, pred);
+      if (rc) return rc;
+      const int64_t rb = tmin<int64_t>(cdiv(n, 32), kRedPartials);
+      gemv_t_reduce<<<(unsigned)rb, 256, 0, st>>>(P, n, 1, plan.nclusters, y, n, finish ? v : nullptr, shift,
+                                                   finish ? pAp : nullptr, red_part(ws), red_counter(ws), pred);
+      NYS_CHECK_LAUNCH();
+      return NYS_OK;
+    }
   }
   // wide rows, first choice: clusters of 16 CTAs split each row's columns and
   // exchange the row totals through distributed shared memory (csrc/hvp_cluster.cu)
@@ -613,9 +617,11 @@ int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const doubl
   static const bool no_strip = getenv("NYS_HVP_NOSTRIP") != nullptr;
   if (!plan.ok && !two_pass_only && !no_strip) {
     const StripPlan sp = hvp_strip_plan(rows, n, lda, A, v);
-    if (sp.ok)
-      return hvp_strip(sp, A, rows, n, lda, d, v, y, finish ? shift : 0.0, finish ? pAp : nullptr,
-                       reinterpret_cast<char*>(ws) + kRedBytes, red_part(ws), red_counter(ws), st, pred);
+    if (sp.ok) {
+      const int rc = hvp_strip(sp, A, rows, n, lda, d, v, y, finish ? shift : 0.0, finish ? pAp : nullptr,
+                               reinterpret_cast<char*>(ws) + kRedBytes, red_part(ws), red_counter(ws), st, pred);
+      if (rc != NYS_ERR_UNSUPPORTED) return rc;
+    }
   }
   char* base = reinterpret_cast<char*>(ws);
   // layout: [K2 ws (reduction scratch first)] [t] [K1 partials]
@@ -684,6 +690,21 @@ extern "C" int nys_hvp_f64(const double* A, int64_t rows, int64_t n, int64_t lda
                            void* ws, size_t ws_bytes, void* stream) {
   if (rows <= 0 || n <= 0 || lda < n) return NYS_ERR_ARG;
   return hvp_apply(A, rows, n, lda, d, v, shift, y, pAp, finish, ws, ws_bytes, as_stream(stream), nullptr);
+}
+
+// which single-pass plan nys_hvp_f64 takes for this shape (16-byte aligned A, v):
+// 1 whole rows per CTA (hvp_row_kernel), 2 column-split clusters with a fused
+// reduction (hvp_fused_kernel), 3 16-CTA DSMEM clusters (hvp_cluster_kernel),
+// 4 grid column strips (hvp_strip_kernel), 0 two passes (gemv_n + gemv_t)
+extern "C" int nys_hvp_plan(int64_t rows, int64_t n, int64_t lda) {
+  if (rows <= 0 || n <= 0 || lda < n) return -1;
+  const double* al = reinterpret_cast<const double*>(uintptr_t(256));
+  if (getenv("NYS_HVP_TWOPASS")) return 0;
+  const HvpPlan plan = hvp_plan(rows, n, lda, al, al);
+  if (plan.ok) return (plan.C == 1 && !getenv("NYS_HVP_LEGACY")) ? 1 : 2;
+  if (hvp_cluster_plan(rows, n, lda, al, al).ok) return 3;
+  if (!getenv("NYS_HVP_NOSTRIP") && hvp_strip_plan(rows, n, lda, al, al).ok) return 4;
+  return 0;
 }
 
 extern "C" int nys_shift_dot_f64(int64_t n, const double* v, double shift, double* y,

@@ -363,9 +363,10 @@ static int hvp_strip_launch_k(const StripPlan& p, const double* A, int64_t rows,
   void* args[] = {(void*)&A, (void*)&rows, (void*)&n, (void*)&lda, (void*)&d, (void*)&v, (void*)&W,
                   (void*)&S, (void*)&L, (void*)&y, (void*)&shift, (void*)&dot, (void*)&xch,
                   (void*)&epoch, (void*)&part, (void*)&counter, (void*)&pred};
-  if (cudaLaunchCooperativeKernel((const void*)fn, dim3(p.nctas), dim3(nthreads), args, p.smem, st) !=
-      cudaSuccess)
-    return NYS_ERR_CUDA;
+  if (!coop_fits((const void*)fn, p.nctas, nthreads, p.smem)) return NYS_ERR_UNSUPPORTED;
+  const int rc = coop_launch_status(
+      cudaLaunchCooperativeKernel((const void*)fn, dim3(p.nctas), dim3(nthreads), args, p.smem, st));
+  if (rc) return rc;
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
   return debug_sync_check(__FILE__, __LINE__) ? NYS_ERR_CUDA : NYS_OK;
 }

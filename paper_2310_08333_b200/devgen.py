@@ -79,3 +79,45 @@ def cfg5_device(kx, blocks=None, rows_per_block: int = CFG5_BLOCK_ROWS, n: int =
     kx.gemv(A, xt.view(1, -1), b)
     b = b.view(-1) + noise
     return A, b, xt
+
+
+def lasso_device(kx, N: int, n: int, seed: int, nnz_frac: float, rows=None, host_b: bool = False):
+    """Configs 1 and 4 (``datagen.lasso_data``) with A generated in HBM: the
+    first N*n draws of ``default_rng(seed)`` (scaled by 1/sqrt(N) exactly as
+    the host recipe), then support, values and noise from the same host
+    stream.  Returns (A rows [rows] on the device, b (host, N), lambda,
+    x_true).  ``host_b``: b and lambda from a host copy of A with NumPy
+    (bitwise the host recipe; needs the 8 N n bytes on the host, returned as
+    the fifth value), else from the device GEMVs (roundoff-level
+    differences).  Every rank of a sharded run computes the same b and lambda
+    and keeps only its rows."""
+    dev = kx.device
+    bg = np.random.PCG64(seed)
+    A = torch.empty(N, n, dtype=torch.float64, device=dev)
+    normals_into(kx, bg, A)
+    A.mul_(1.0 / np.sqrt(N))
+    rng = np.random.Generator(bg)
+    k = max(1, int(round(nnz_frac * n)))
+    support = rng.choice(n, size=k, replace=False)
+    x_true = np.zeros(n)
+    x_true[support] = rng.standard_normal(k)
+    noise = 0.01 * rng.standard_normal(N)
+    A_host = None
+    if host_b:
+        A_host = torch.empty(N, n, dtype=torch.float64, pin_memory=True)
+        A_host.copy_(A)
+        Ah = A_host.numpy()
+        b = Ah @ x_true + noise
+        lam = 0.1 * float(np.max(np.abs(Ah.T @ b)))
+    else:
+        bt = torch.empty(1, N, dtype=torch.float64, device=dev)
+        kx.gemv(A, torch.from_numpy(x_true).to(dev).view(1, -1), bt)
+        b = bt.view(-1).cpu().numpy() + noise
+        atb = torch.empty(1, n, dtype=torch.float64, device=dev)
+        kx.gemvT(A, torch.from_numpy(b).to(dev).view(1, -1), atb)
+        lam = 0.1 * float(atb.abs().max())
+    if rows is not None and tuple(rows) != (0, N):
+        A = A[rows[0]:rows[1]].clone()
+        torch.cuda.empty_cache()
+    return A, b, lam, x_true, A_host
+

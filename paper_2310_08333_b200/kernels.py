@@ -106,6 +106,14 @@ class Kernels:
                                    Y.data_ptr(), Y.stride(0), ws.data_ptr(), ws.numel(), self.sp), "gemvT")
         self._t1(e)
 
+    HVP_PLANS = {0: "gemv_n_kernel + gemv_t_kernel (two passes)", 1: "hvp_row_kernel",
+                 2: "hvp_fused_kernel + gemv_t_reduce", 3: "hvp_cluster_kernel + gemv_t_reduce",
+                 4: "hvp_strip_kernel"}
+
+    def hvp_plan_name(self, rows: int, n: int) -> str:
+        """The kernel(s) nys_hvp_f64 runs for a rows x n operand."""
+        return self.HVP_PLANS.get(int(self.L.nys_hvp_plan(rows, n, n)), "hvp")
+
     def hvp(self, A, d, v, shift, y, pAp=None, finish=True) -> None:
         rows, n = A.shape
         ws = self.workspace("hvp", self.L.nys_hvp_workspace(rows, n))

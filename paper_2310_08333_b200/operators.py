@@ -152,6 +152,7 @@ class DenseOperator(LinearOperator):
         super().__init__(shape[1], shape[0])
         self._shards: dict = {}
         self._local = None  # (row_start, row_stop) when only a row block is resident
+        self._host_local = None
 
     @classmethod
     def from_local_rows(cls, a_local: torch.Tensor, rows_global: int, row_start: int) -> "DenseOperator":
@@ -159,15 +160,23 @@ class DenseOperator(LinearOperator):
         [row_start, row_start + a_local.shape[0]) in HBM (config 5: every rank
         generates its own row blocks, BASELINE.json configs[4]).  The solve's
         shard must be exactly that row range."""
-        if not (isinstance(a_local, torch.Tensor) and a_local.is_cuda and a_local.ndim == 2):
-            raise DimensionMismatchError("local rows must be a 2-d CUDA tensor")
+        if isinstance(a_local, np.ndarray):
+            a_local = torch.from_numpy(np.ascontiguousarray(a_local, dtype=float))
+        if not (isinstance(a_local, torch.Tensor) and a_local.ndim == 2):
+            raise DimensionMismatchError("local rows must be a 2-d array")
         op = cls.__new__(cls)
         op.a = None
         op._dev_full = None
         LinearOperator.__init__(op, a_local.shape[1], rows_global)
         op._shards = {}
         op._local = (row_start, row_start + a_local.shape[0])
-        op._shards[(row_start, row_start + a_local.shape[0], str(a_local.device))] = a_local.contiguous()
+        op._host_local = None
+        if a_local.is_cuda:
+            op._shards[(row_start, row_start + a_local.shape[0], str(a_local.device))] = a_local.contiguous()
+        else:
+            # host rows (pinned for the bench's end-to-end leg): uploaded by the
+            # first device_rows() call of the solve, like a full host matrix
+            op._host_local = a_local.to(dtype=F64).contiguous()
         return op
 
     # -- device data ---------------------------------------------------------
@@ -179,6 +188,10 @@ class DenseOperator(LinearOperator):
             device = torch.device("cuda", torch.cuda.current_device())
         key = (shard.row_start, shard.row_stop, str(device))
         t = self._shards.get(key)
+        if t is None and self._local is not None and getattr(self, "_host_local", None) is not None \
+                and (shard.row_start, shard.row_stop) == self._local:
+            t = self._host_local.to(device, non_blocking=self._host_local.is_pinned())
+            self._shards[key] = t
         if t is None and self._local is not None:
             raise DimensionMismatchError(f"rows {self._local} are resident here, the solve's shard is "
                                          f"[{shard.row_start}, {shard.row_stop})")

@@ -385,3 +385,30 @@ def ml_dual_gap(p: MLProblem, x) -> float:
     if denom <= 1e-16:
         return 0.0 if abs(num) <= 1e-12 else np.inf
     return num / denom
+
+
+def huber_subdiff_distance(p: MLProblem, x) -> float:
+    """l2 distance from 0 to the subdifferential of the huber-fit objective
+    (problems.py:354-368): the gradient w = A' l'(Ax - b) + lambda2 x comes from
+    the device passes; the support split is host arithmetic on n values."""
+    if p.loss.kind != "huber":
+        raise DataError("subdifferential stopping rule is defined for the huber loss")
+    xh = x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x, dtype=float)
+    w = ml_gradient(p, xh)
+    w = w.detach().cpu().numpy() if isinstance(w, torch.Tensor) else np.asarray(w)
+    active = xh != 0.0
+    d2 = float(np.sum((w[active] + p.lambda1 * np.sign(xh[active])) ** 2))
+    d2 += float(np.sum(np.maximum(np.abs(w[~active]) - p.lambda1, 0.0) ** 2))
+    return float(np.sqrt(d2))
+
+
+def huber_subdiff_stop(tol: float = 1e-4) -> Callable:
+    """Termination rule on the sparse iterate z (problems.py:371-384)."""
+
+    def stop(problem: GenericProblem, state) -> bool:
+        if problem.ml is None:
+            return False
+        return huber_subdiff_distance(problem.ml, state.z) <= tol
+
+    return stop
+

@@ -72,6 +72,30 @@ def _cfg5_shard(j=0):
     return dict(loss="square", A=Ab, b=b, lambda1=lam, lambda2=0.0)
 
 
+def _from_inputs(name):
+    """Inputs produced by a reference generator (``make_golden.py`` stores them
+    next to the outputs: ``input_<name>.npz``), e.g. the robust-regression data
+    of the reference's cycle-guard test (``tests/test_admm.py:577-589``)."""
+    import os
+
+    d = dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), f"input_{name}.npz")))
+    if "P" in d:
+        return dict(P=d["P"], q=d["q"], lo=d["lo"], hi=d["hi"])
+    return dict(loss=str(d["loss"]), A=d["A"], b=d["b"], lambda1=float(d["lambda1"]), lambda2=float(d["lambda2"]))
+
+
+def _qp_unbounded(n=10, seed=9):
+    """P = 0, q < 0, box [0, inf): dual infeasible (tests/test_admm.py:391-401,
+    with M = I as the identity operator)."""
+    rng = np.random.default_rng(seed)
+    q = -np.abs(rng.standard_normal(n))
+    return dict(P=np.zeros((n, n)), q=q, lo=np.zeros(n), hi=np.full(n, np.inf))
+
+
+# penalty adaptation from the first iterations (admm.py:677-698): rho0 far from
+# balance makes the balanced-residual rule fire every 5 iterations
+_PEN = dict(penalty_warmup=5, penalty_update_every=5)
+
 # name: (problem builder, options dict)
 SOLVE_CASES = {
     "lasso_small": (lambda: _ml_small("square", 120, 200, 11), dict(sketch_rank=10, rng_seed=11)),
@@ -84,6 +108,20 @@ SOLVE_CASES = {
     "lasso_linf": (lambda: _ml_small("square", 120, 200, 18), dict(sketch_rank=10, rng_seed=18, norm_kind="linf", use_dual_gap=False)),
     "lasso_exact": (lambda: _ml_small("square", 100, 150, 19), dict(sketch_rank=10, rng_seed=19, exact_x_solve=True)),
     "boxqp_small": (lambda: _qp_small(400, 200, 20), dict(sketch_rank=20, rng_seed=20)),
+    # --- adaptive control flow: penalty changes, cycle guard, certificates, time limit
+    "lasso_rho_hi": (lambda: _ml_small("square", 120, 200, 11), dict(sketch_rank=10, rng_seed=11, rho0=100.0, **_PEN)),
+    "lasso_rho_lo": (lambda: _ml_small("square", 120, 200, 11), dict(sketch_rank=10, rng_seed=11, rho0=0.01, **_PEN)),
+    "logistic_rho_hi": (lambda: _ml_small("logistic", 300, 150, 14, lam2=1e-3, lam_frac=0.1),
+                        dict(sketch_rank=10, rng_seed=14, rho0=100.0, **_PEN)),
+    "logistic_rho_lo": (lambda: _ml_small("logistic", 300, 150, 14, lam2=1e-3, lam_frac=0.1),
+                        dict(sketch_rank=10, rng_seed=14, rho0=0.01, **_PEN)),
+    "boxqp_rho": (lambda: _qp_small(400, 200, 20), dict(sketch_rank=20, rng_seed=20, rho0=50.0, **_PEN)),
+    "huber_cycle_a": (lambda: _from_inputs("huber_cycle_a"),
+                      dict(huber_stop=1e-4, max_iter=8000, use_dual_gap=False)),
+    "huber_cycle_b": (lambda: _from_inputs("huber_cycle_b"),
+                      dict(huber_stop=1e-4, max_iter=8000, use_dual_gap=False)),
+    "qp_unbounded": (lambda: _qp_unbounded(), dict(max_iter=4000)),
+    "lasso_time0": (lambda: _ml_small("square", 120, 200, 11), dict(sketch_rank=10, rng_seed=11, time_limit=0.0)),
     "cfg1": (lambda: _cfg(1), dict(sketch_rank=50, rng_seed=0)),
     "cfg3": (lambda: _cfg(3), dict(sketch_rank=100, rng_seed=2)),
     "cfg2": (lambda: _cfg(2), dict(sketch_rank=100, rng_seed=1)),
@@ -99,9 +137,18 @@ DEFAULT_SOLVES = [k for k in SOLVE_CASES if k not in ("cfg4", "cfg5_shard")]
 
 
 def options_for(name):
+    """Options of a case; a ``huber_stop`` entry stands for
+    ``custom_stop=huber_subdiff_stop(tol)`` (see ``split_stop``)."""
     opts = dict(BASE_OPTIONS)
     opts.update(SOLVE_CASES[name][1])
     return opts
+
+
+def split_stop(opts):
+    """(options without ``huber_stop``, its tolerance or None): each consumer
+    builds the custom stop from its own package's ``huber_subdiff_stop``."""
+    opts = dict(opts)
+    return opts, opts.pop("huber_stop", None)
 
 
 # ---- kernel-level cases -------------------------------------------------------

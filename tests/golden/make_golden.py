@@ -51,9 +51,22 @@ def ref_problem(spec):
     return MLProblem(builtin_loss(spec["loss"]), spec["A"], spec["b"], spec["lambda1"], spec["lambda2"])
 
 
+def make_inputs():
+    """Inputs made by the reference's own generators (stored, not re-derived)."""
+    from nysopt.bench import gen_huber_data
+
+    for name, (n, seed) in (("huber_cycle_a", (100, 2)), ("huber_cycle_b", (60, 0))):
+        A, b, lam1 = gen_huber_data(n, seed)  # tests/test_admm.py:577-589
+        np.savez_compressed(os.path.join(HERE, f"input_{name}.npz"), loss=np.array("huber"), A=A, b=b,
+                            lambda1=np.float64(lam1), lambda2=np.float64(0.0))
+
+
 def run_solve(name):
     spec = cases.SOLVE_CASES[name][0]()
-    opts = SolverOptions(**cases.options_for(name))
+    o, stop_tol = cases.split_stop(cases.options_for(name))
+    if stop_tol is not None:
+        o["custom_stop"] = nysopt.huber_subdiff_stop(stop_tol)
+    opts = SolverOptions(**o)
     t0 = time.perf_counter()
     res = nysopt.solve(ref_problem(spec), opts)
     dt = time.perf_counter() - t0
@@ -76,6 +89,8 @@ def run_solve(name):
         rd_hist=np.array([h.rd_norm for h in hist]),
         gap_hist=np.array([np.nan if h.gap is None else h.gap for h in hist]),
         penalty_events=np.array([[e.k, e.rho_old, e.rho_new, e.dual_jump_rel] for e in res.penalty_events]).reshape(-1, 4),
+        certificate=res.certificate if res.certificate is not None else np.zeros(0),
+        n_history=np.int64(len(hist)),
         x_bar=res.x_bar if res.x_bar is not None else np.zeros(0),
         z_bar=res.z_bar if res.z_bar is not None else np.zeros(0),
         ref_total_s=np.float64(dt),
@@ -135,6 +150,7 @@ def main():
     ap.add_argument("--only", nargs="*", default=None)
     args = ap.parse_args()
     names = args.only if args.only else list(cases.DEFAULT_SOLVES) + (["cfg4"] if args.big else [])
+    make_inputs()
     if not args.only:
         run_kernels()
     for name in names:

@@ -353,3 +353,30 @@ def test_cfg5_block_generated_in_hbm_matches_host(kx, piece):
     A2, b2, xt = devgen.cfg5_device(kx, [3], rows, n, piece)
     assert torch.equal(A2, out)
     np.testing.assert_allclose(b2.cpu().numpy(), A_ref @ xt.cpu().numpy() + noise_ref, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("host_b", [True, False])
+def test_lasso_generated_in_hbm_matches_host(kx, host_b):
+    """Configs 1/4's recipe with A generated on the GPU (devgen.lasso_device,
+    used by bench.py for the 16 GB config 4): A bit-for-bit the host stream,
+    the support / values / noise drawn after it from the continued host
+    generator; with host_b, b and lambda bit-for-bit datagen.lasso_data."""
+    from paper_2310_08333_b200 import datagen, devgen
+
+    N, n, seed, frac = 300, 700, 3, 0.01
+    A_ref, b_ref, lam_ref = datagen.lasso_data(N, n, seed, frac)
+    A, b, lam, xt, A_host = devgen.lasso_device(kx, N, n, seed, frac, host_b=host_b)
+    got = A.cpu().numpy()
+    # the device ziggurat's tail (exp/log) may round one draw in 10^5 by an ulp
+    assert (got != A_ref).sum() <= max(1, got.size // 100000)
+    np.testing.assert_allclose(got, A_ref, rtol=1e-15, atol=0)
+    if host_b:
+        assert np.array_equal(A_host.numpy(), got)
+        np.testing.assert_allclose(b, b_ref, rtol=1e-13, atol=1e-15)
+        assert abs(lam - lam_ref) <= 1e-13 * lam_ref
+    else:
+        np.testing.assert_allclose(b, b_ref, rtol=1e-13, atol=1e-15)
+        assert abs(lam - lam_ref) <= 1e-13 * lam_ref
+    # a rank's rows of a sharded run: the same numbers
+    A2, b2, lam2, _, _ = devgen.lasso_device(kx, N, n, seed, frac, rows=(100, 200), host_b=host_b)
+    assert np.array_equal(A2.cpu().numpy(), got[100:200]) and np.array_equal(b2, b) and lam2 == lam

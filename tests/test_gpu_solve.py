@@ -32,12 +32,21 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
+def gpu_options(name):
+    import paper_2310_08333_b200 as nys
+
+    o, stop_tol = cases.split_stop(cases.options_for(name))
+    if stop_tol is not None:
+        o["custom_stop"] = nys.huber_subdiff_stop(stop_tol)
+    return nys.SolverOptions(**o)
+
+
 def check_case(name, strict_hist=True):
     import paper_2310_08333_b200 as nys
 
     gold = load_golden(f"solve_{name}.npz")
     spec = cases.SOLVE_CASES[name][0]()
-    opts = nys.SolverOptions(**cases.options_for(name))
+    opts = gpu_options(name)
     res = nys.solve(gpu_problem(spec), opts)
     it_ref = int(gold["iterations"])
     assert res.status.value == str(gold["status"]), (res.status, gold["status"])
@@ -52,6 +61,28 @@ def check_case(name, strict_hist=True):
     if strict_hist:
         # roundoff never moves an inner iteration count by more than one
         assert np.abs(cg_gpu[:m] - cg_ref[:m]).max(initial=0) <= 1, (cg_gpu[:m], cg_ref[:m])
+    # adaptive control flow (admm.py:303-350, 643-698): the same penalty
+    # events at the same iterations, hence the same rho on every iteration
+    ev = [(e.k, e.rho_old, e.rho_new) for e in res.penalty_events]
+    ev_ref = [(int(r[0]), float(r[1]), float(r[2])) for r in gold["penalty_events"]]
+    assert ev == ev_ref, (ev, ev_ref)
+    assert all(abs(e.dual_jump_rel - r[3]) <= 1e-12 for e, r in zip(res.penalty_events, gold["penalty_events"]))
+    rho_gpu = np.array([h.rho for h in res.history])
+    assert np.array_equal(rho_gpu[:m], gold["rho"][:m]), (rho_gpu[:m], gold["rho"][:m])
+    # averaged iterates (admm.py:580-583)
+    if gold["x_bar"].size:
+        assert res.x_bar is not None and res.z_bar is not None
+        assert rel(res.x_bar, gold["x_bar"]) <= 1e-5, rel(res.x_bar, gold["x_bar"])
+        assert rel(res.z_bar, gold["z_bar"]) <= 1e-5, rel(res.z_bar, gold["z_bar"])
+    else:
+        assert res.x_bar is None
+    # infeasibility certificate (admm.py:361-415)
+    cert = gold["certificate"] if "certificate" in gold else np.zeros(0)
+    if cert.size:
+        assert res.certificate is not None
+        assert rel(res.certificate, cert) <= 1e-5, rel(res.certificate, cert)
+    else:
+        assert res.certificate is None
     return res, gold
 
 
@@ -101,7 +132,7 @@ def test_lookahead_is_bitwise_neutral(name, monkeypatch):
     import paper_2310_08333_b200 as nys
 
     spec = cases.SOLVE_CASES[name][0]()
-    opts = nys.SolverOptions(**cases.options_for(name))
+    opts = gpu_options(name)
     r1 = nys.solve(gpu_problem(spec), opts)
     monkeypatch.setenv("NYS_LOOKAHEAD", "0")
     r0 = nys.solve(gpu_problem(spec), opts)

@@ -24,7 +24,9 @@ def oracle_problem(spec):
 
 
 def oracle_options(name):
-    o = cases.options_for(name)
+    o, tol = cases.split_stop(cases.options_for(name))
+    if tol is not None:
+        o["custom_stop"] = port.huber_subdiff_stop(tol)
     return port.Options(**o)
 
 
@@ -43,6 +45,17 @@ def test_oracle_matches_reference_solve(name):
     np.testing.assert_allclose(res.u, gold["u"], rtol=1e-9, atol=1e-12)
     if gold["x_bar"].size:
         np.testing.assert_allclose(res.x_bar, gold["x_bar"], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(res.z_bar, gold["z_bar"], rtol=1e-9, atol=1e-12)
+    # penalty events: same iterations and penalties exactly, jumps to roundoff
+    ev = np.array(res.penalty_events, dtype=float).reshape(-1, 4)
+    pe = gold["penalty_events"]
+    assert ev.shape == pe.shape, (ev, pe)
+    np.testing.assert_array_equal(ev[:, :3], pe[:, :3])
+    np.testing.assert_allclose(ev[:, 3], pe[:, 3], rtol=0, atol=1e-12)
+    if "certificate" in gold and gold["certificate"].size:
+        np.testing.assert_allclose(res.certificate, gold["certificate"], rtol=1e-9, atol=1e-12)
+    else:
+        assert res.certificate is None
 
 
 def test_oracle_kernels_match_reference():
