@@ -291,10 +291,10 @@ hvp_row_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t ld
       double a = cs_acc[0][cx];
 #pragma unroll
       for (int q = 1; q < 8; ++q) a += cs_acc[q][cx];
-      if (dot) {
-        a += shift * v[c];
-        dacc[0] = fma(v[c], a, dacc[0]);
-      }
+      // the shift is part of the operator whether or not p.Ap is wanted (the
+      // CG's true-residual refresh applies it to x with no dot, krylov.py:80-81)
+      if (dot || shift != 0.0) a += shift * v[c];
+      if (dot) dacc[0] = fma(v[c], a, dacc[0]);
       y[c] = a;
     }
     __syncthreads();

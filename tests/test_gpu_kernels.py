@@ -79,6 +79,10 @@ def test_hvp_fused(kx, rows, n):
     ref = A.T @ (d * (A @ v)) + 0.7 * v
     np.testing.assert_allclose(y.cpu().numpy(), ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
     assert abs(float(pAp) - v @ ref) <= 1e-11 * abs(v @ ref)
+    # the shift without p.Ap (the CG's true-residual refresh, krylov.py:80-81)
+    y1 = kx.empty(n)
+    kx.hvp(dev(A), dev(d), dev(v), 0.7, y1, None, True)
+    np.testing.assert_allclose(y1.cpu().numpy(), ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
     # partial form (row shard) + finish
     y2 = kx.empty(n)
     kx.hvp(dev(A), None, dev(v), 0.0, y2, None, False)
