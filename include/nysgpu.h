@@ -429,6 +429,54 @@ size_t nys_syevj_workspace(int s);
 int nys_syevj_f64(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* ------------------------------------- sparse / general-operator engine -- */
+/* CSR data operator (SparseOperator._apply, operators.py:129-131 -- scipy's
+ * `a @ v`): row pointer int64 (rows+1), column indices int32, values FP64.
+ *   y_i = alpha * s_i * (a_i . x) + beta * zin_i,  s = dscale (NULL: 1);
+ *   beta == 0 ignores zin (which may alias y).  `group` = lanes per row, a power
+ *   of two <= 32 (the host picks it from the mean row length).
+ * The adjoint (operators.py:133-134, `a.T @ u`) is the same call on the
+ * transpose built by nys_csr_transpose. */
+int nys_csr_spmv_f64(int64_t rows, const int64_t* rowptr, const int* col, const double* val,
+                     const double* x, double alpha, const double* dscale, double beta, const double* zin,
+                     double* y, int group, void* stream);
+/* Y = diag(s) A X for a row-major cols x s block X (the sketch's column
+ * applies, sketch.py:69-71, done as one multi-column product). */
+int nys_csr_spmm_f64(int64_t rows, const int64_t* rowptr, const int* col, const double* val,
+                     const double* X, int64_t ldx, int s, const double* dscale, double* Y, int64_t ldy,
+                     void* stream);
+/* CSR of A^T on the device (deterministic counting transpose: the entries of
+ * every transposed row are ordered by original row).  trowptr has cols+1
+ * entries, tcol / tval nnz.  The workspace need not be zeroed. */
+size_t nys_csr_transpose_workspace(int64_t rows, int64_t cols);
+int nys_csr_transpose(int64_t rows, int64_t cols, const int64_t* rowptr, const int* col, const double* val,
+                      int64_t* trowptr, int* tcol, double* tval, void* ws, size_t ws_bytes, void* stream);
+/* y = a (d o x) + b y  (DiagonalOperator, DiagPlusLowRank's diagonal,
+ * operators.py:89-101, 152-153) */
+int nys_vmul_f64(int64_t n, double a, const double* d, const double* x, double b, double* y, void* stream);
+/* y[:] = scale * src[0] (OnesRowOperator adjoint, operators.py:202-203) */
+int nys_bcast_f64(int64_t n, const double* src, double scale, double* y, void* stream);
+/* v = x - y (y may be NULL): out = [sum v, sum v^2, max |v|]  (the l2 / linf
+ * norms of admm.py:203-208; OnesRowOperator apply = out[0]) */
+int nys_vstats_f64(int64_t n, const double* x, const double* y, double* out, void* ws, void* stream);
+/* l1 norm and dual-norm pieces (g(z) = lambda1 ||z||_1, problems.py:308-331):
+ *   out = [sum |v|, sum (|v| - lambda1)_+^2, max |v|] */
+int nys_absstats_f64(int64_t n, const double* v, double lambda1, double* out, void* ws, void* stream);
+/* dual residual of admm.py:219-222 with a general M: t = rho * Mtu,
+ * rd = grad + t;  out = [sum rd^2, sum t^2, max |rd|, max |t|] */
+int nys_gdual_f64(int64_t n, const double* grad, const double* mtu, double rho, double* out, void* ws,
+                  void* stream);
+/* box certificates of check_infeasibility (admm.py:386-396, prox.py:96-135):
+ *   du (may be NULL): out[0] = sum_{du>0} hi du, out[1] = sum_{du<0} lo du,
+ *                     out[2] = number of (infinite bound x nonzero) terms;
+ *   md (may be NULL): out[3] = ||md - proj_recession(md)||^2 */
+int nys_box_cert_f64(int64_t m, const double* du, const double* md, const double* lo, const double* hi,
+                     double* out, void* ws, void* stream);
+/* box membership (box_indicator, prox.py:138-144):
+ *   out = [max(lo - z), max(z - hi), max |z|] */
+int nys_box_violation_f64(int64_t m, const double* z, const double* lo, const double* hi, double* out,
+                          void* ws, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

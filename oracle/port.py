@@ -8,7 +8,9 @@ loudly when its CUDA library is missing.
 
 Scope: the north-star path of SURVEY.md §8(a) -- dense ML problems (square,
 logistic, huber losses; M = I, c = 0) and box-constrained QPs with a dense P
-and M = I.  Every function cites the reference ``file:line`` it restates
+and M = I -- and the §8(f) rows built after it: sparse (scipy CSR) data,
+structured P (diagonal-plus-low-rank), a general constraint map M with the
+composite sketch target, the Lanczos rank probe and the adaptive sketch.  Every function cites the reference ``file:line`` it restates
 (paths relative to ``/root/reference/pkg/src/nysopt``).  The arithmetic is
 written in the same operation order as the reference so that, on identical
 inputs, the oracle agrees with the reference bit for bit; this is pinned by
@@ -309,16 +311,155 @@ class MLSpec:
 
 @dataclass
 class QPSpec:
-    """problems.py:160-188 with M = I and a dense P."""
+    """problems.py:160-188.  P and M are anything with ``@`` and ``.T``
+    (ndarray, scipy sparse, ``DiagLowRank``); M = None is the identity."""
 
-    P: np.ndarray
+    P: object
     q: np.ndarray
     lo: np.ndarray
     hi: np.ndarray
+    M: object = None
 
     @property
     def n(self):
         return self.P.shape[0]
+
+    @property
+    def m(self):
+        return self.n if self.M is None else self.M.shape[0]
+
+
+class DiagLowRank:
+    """diag(d) + F F^T in factored form (operators.py:138-160)."""
+
+    def __init__(self, d, F):
+        self.d = np.asarray(d, dtype=float)
+        self.F = np.asarray(F, dtype=float)
+        self.shape = (self.d.size, self.d.size)
+
+    def __matmul__(self, v):
+        return self.d * v + self.F @ (self.F.T @ v)
+
+    @property
+    def T(self):
+        return self
+
+
+class StackOp:
+    """[A_1; A_2; ...] (operators.py:163-191); parts with ``@`` and ``.T``."""
+
+    def __init__(self, parts):
+        self.parts = list(parts)
+        self.off = np.cumsum([0] + [p.shape[0] for p in self.parts])
+        self.shape = (int(self.off[-1]), self.parts[0].shape[1])
+
+    def __matmul__(self, v):
+        return np.concatenate([np.atleast_1d(p @ v) for p in self.parts])
+
+    @property
+    def T(self):
+        outer = self
+
+        class _Adj:
+            shape = (outer.shape[1], outer.shape[0])
+
+            def __matmul__(self, u):
+                out = np.zeros(outer.shape[1])
+                for p, lo, hi in zip(outer.parts, outer.off[:-1], outer.off[1:]):
+                    out += p.T @ u[lo:hi]
+                return out
+
+        return _Adj()
+
+
+class OnesRow:
+    """v -> [sum v]; adjoint broadcasts (operators.py:194-203)."""
+
+    def __init__(self, n):
+        self.shape = (1, n)
+
+    def __matmul__(self, v):
+        return np.array([v.sum()])
+
+    @property
+    def T(self):
+        n = self.shape[1]
+
+        class _Adj:
+            shape = (n, 1)
+
+            def __matmul__(self, u):
+                return np.full(n, u[0])
+
+        return _Adj()
+
+
+def estimate_extreme_eigs(matvec, n, iters, rng_seed):  # sketch.py:240-282
+    if iters < 2:
+        raise OracleDataError("iters >= 2")
+    iters = min(iters, n)
+    rng = np.random.default_rng(rng_seed)
+    q = rng.standard_normal(n)
+    q /= np.linalg.norm(q)
+    Q = np.zeros((n, iters))
+    alphas, betas = [], []
+    Q[:, 0] = q
+    scale = 0.0
+    for j in range(iters):
+        w = matvec(Q[:, j])
+        alpha = float(Q[:, j] @ w)
+        alphas.append(alpha)
+        scale = max(scale, abs(alpha))
+        w -= alpha * Q[:, j]
+        if j > 0:
+            w -= betas[-1] * Q[:, j - 1]
+        for _ in range(2):
+            w -= Q[:, : j + 1] @ (Q[:, : j + 1].T @ w)
+        beta = float(np.linalg.norm(w))
+        if j == iters - 1 or beta <= 1e-12 * max(scale, 1.0):
+            break
+        betas.append(beta)
+        Q[:, j + 1] = w / beta
+    T = np.diag(alphas)
+    if betas:
+        k = len(alphas)
+        T += np.diag(betas[: k - 1], 1) + np.diag(betas[: k - 1], -1)
+    ritz = np.linalg.eigvalsh(T)
+    return float(ritz[-1]), float(ritz[0])
+
+
+def estimate_error_norm(matvec, U, lam, n, iters, rng_seed):  # sketch.py:176-195
+    rng = np.random.default_rng(rng_seed)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    est = 0.0
+    for _ in range(iters):
+        w = matvec(v) - (U @ (lam * (U.T @ v)) if U.shape[1] else 0.0)
+        est = float(np.linalg.norm(w))
+        if est <= 0.0 or not np.isfinite(est):
+            return max(est, 0.0)
+        v = w / est
+    return est
+
+
+def adaptive_sketch(matvec, n, r0, r_max, nu, kappa_target, rng_seed, power_iters=10):  # sketch.py:204-237
+    ranks = []
+    r = r0
+    while r < r_max:
+        ranks.append(r)
+        r *= 2
+    ranks.append(r_max)
+    seeds = np.random.SeedSequence(rng_seed).generate_state(2 * len(ranks))
+    cols = lambda V: np.column_stack([matvec(V[:, j]) for j in range(V.shape[1])])
+    out = None
+    for i, rank in enumerate(ranks):
+        U, lam = nystrom_sketch(cols, n, rank, int(seeds[2 * i]))
+        out = (U, lam)
+        err = estimate_error_norm(matvec, U, lam, n, power_iters, int(seeds[2 * i + 1]))
+        tail = lam[-1] if lam.size else 0.0
+        if 1.0 + (tail + err) / nu <= kappa_target:
+            return out
+    return out
 
 
 def ml_residuals(p: MLSpec, x):  # problems.py:219-220
@@ -424,6 +565,8 @@ class Options:
     use_dual_gap: Optional[bool] = None
     eps_dual_gap: float = 1e-4
     rng_seed: int = 0
+    assume_full_rank: bool = False
+    check_rank: bool = False
     custom_stop: Optional[Callable] = None  # (problem spec, z) -> bool, replaces the built-in test
     callback: Optional[Callable] = None  # callback(k) after every iteration (admm.py:610-611; bench timing)
 
@@ -463,12 +606,18 @@ def _norm(v, kind):  # admm.py:203-208
 
 
 def solve(problem, opts: Optional[Options] = None) -> OracleResult:
-    """admm.py:422-719 for dense ML problems and identity-M box QPs."""
+    """admm.py:422-719 for ML problems (dense or sparse A) and box QPs with a
+    general constraint map M."""
     t_start = time.perf_counter()
     opts = opts or Options()
     is_ml = isinstance(problem, MLSpec)
     n = problem.n
     kind = opts.norm_kind
+    Mop = None if is_ml else problem.M
+    identity_M = Mop is None
+    m = n if identity_M else Mop.shape[0]
+    M_apply = (lambda v: v) if identity_M else (lambda v: np.asarray(Mop @ v, dtype=float))
+    M_adj = (lambda v: v) if identity_M else (lambda v: np.asarray(Mop.T @ v, dtype=float))
 
     # lowering (problems.py:387-450): f, grad, hess, g, prox with M = I, c = 0
     if is_ml:
@@ -501,16 +650,24 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
         return np.column_stack([qp.P @ V[:, j] for j in range(V.shape[1])])
 
     x = np.zeros(n)
-    z = np.zeros(n)
-    u = np.zeros(n)
+    z = np.zeros(m)
+    u = np.zeros(m)
     rho = opts.rho0
     if is_ml:
         weights = ml_weights(p, x)  # admm.py:457
-    Mx = x.copy()
+    Mx = M_apply(x).copy()
     x_bar_sum = np.zeros(n)
-    z_bar_sum = np.zeros(n)
+    z_bar_sum = np.zeros(m)
     bar_count = 0
-    sigma_eff = 0.0  # full_rank (admm.py:464-466)
+    # offset policy (admm.py:462-474): ML lowerings and M = I QPs are full rank
+    sigma_eff = opts.sigma
+    if is_ml or identity_M or opts.assume_full_rank:
+        sigma_eff = 0.0
+    elif opts.check_rank:
+        comp0 = lambda v: hess_apply(v) + rho * M_adj(M_apply(v))
+        _, lam_min = estimate_extreme_eigs(comp0, n, min(max(2, n), 60), opts.rng_seed + 7)
+        if lam_min > 1e-8:
+            sigma_eff = 0.0
 
     use_gap = opts.use_dual_gap
     if use_gap is None:
@@ -525,16 +682,27 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
     pc_nu = None
     n_sk = 0
     last_sketch = 0
+    rho_at_sketch = rho
+
+    def build(seed):  # admm.py:493-507
+        if identity_M:
+            return nystrom_sketch(smooth_cols, n, r_sk, seed), nu_of(rho)
+        rho_now = rho
+        comp = lambda v: hess_apply(v) + rho_now * M_adj(M_apply(v))
+        cols = lambda V: np.column_stack([comp(V[:, j]) for j in range(V.shape[1])])
+        return nystrom_sketch(cols, n, r_sk, seed), max(sigma_eff, 1e-8)
+
     if opts.use_preconditioner:
-        sketch = nystrom_sketch(smooth_cols, n, r_sk, opts.rng_seed)
-        pc_nu = nu_of(rho)
+        sketch, pc_nu = build(opts.rng_seed)
+        rho_at_sketch = rho
         n_sk += 1
 
     def residuals():  # admm.py:215-224
         rp = Mx - z
-        rd = grad(x) + rho * u
-        ps = max(_norm(Mx, kind), _norm(z, kind), _norm(np.zeros(n), kind))
-        ds = _norm(rho * u, kind)
+        Mtu = M_adj(u)
+        rd = grad(x) + rho * Mtu
+        ps = max(_norm(Mx, kind), _norm(z, kind), _norm(np.zeros(m), kind))
+        ds = _norm(rho * Mtu, kind)
         return rp, rd, _norm(rp, kind), _norm(rd, kind), ps, ds
 
     rp, rd, rpn, rdn, ps, ds = residuals()
@@ -558,22 +726,29 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
             break
         if not const_hess:
             weights = ml_weights(p, x)  # admm.py:539-540
-        if sketch is not None and not const_hess and k - last_sketch >= opts.resketch_every:
-            sketch = nystrom_sketch(smooth_cols, n, r_sk, opts.rng_seed + k)  # admm.py:545-551
-            pc_nu = nu_of(rho)
-            n_sk += 1
-            last_sketch = k
+        if sketch is not None:  # admm.py:545-551
+            stale_hess = not const_hess and k - last_sketch >= opts.resketch_every
+            stale_rho = not identity_M and rho != rho_at_sketch
+            if stale_hess or stale_rho:
+                sketch, pc_nu = build(opts.rng_seed + k)
+                n_sk += 1
+                last_sketch = k
+                rho_at_sketch = rho
         tol = 1e-12 if opts.exact_x_solve else cg_tolerance(k, rpn, rdn, opts.gamma)
 
-        # x_update (admm.py:243-275), identity M
+        # x_update (admm.py:243-275)
         shift = rho + sigma_eff
-        matvec = lambda v: hess_apply(v) + shift * v
+        if identity_M:
+            matvec = lambda v: hess_apply(v) + shift * v
+        else:
+            matvec = lambda v, _r=rho: hess_apply(v) + _r * M_adj(M_apply(v)) + sigma_eff * v
         rhs = hess_apply(x) + sigma_eff * x - grad(x)
-        rhs = rhs + rho * (z + 0.0 - u)
+        target = z + 0.0 - u
+        rhs = rhs + (rho * target if identity_M else rho * M_adj(target))
         Minv = (lambda v: precond_apply(sketch[0], sketch[1], pc_nu, v)) if sketch is not None else None
         x_new, cg = pcg(matvec, rhs, x0=x, Minv=Minv, tol_rel=tol, max_iter=10 * n)
 
-        Mx_new = x_new
+        Mx_new = x_new if identity_M else M_apply(x_new)
         w = opts.alpha * Mx_new + (1.0 - opts.alpha) * (z + 0.0)  # admm.py:278-280
         x_prev, u_prev = x, u.copy()
         x = x_new
@@ -603,7 +778,7 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
         elif gap is not None:
             done = gap <= opts.eps_dual_gap
         else:
-            done = rpn <= np.sqrt(n) * opts.eps_abs + opts.eps_rel * ps and rdn <= np.sqrt(
+            done = rpn <= np.sqrt(m) * opts.eps_abs + opts.eps_rel * ps and rdn <= np.sqrt(
                 n
             ) * opts.eps_abs + opts.eps_rel * ds
         if done:
@@ -615,7 +790,7 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
         if not is_ml and len(uw) == 26:  # admm.py:621-634
             dx = (xw[-1] - xw[0]) / 25
             du = (uw[-1] - uw[0]) / 25
-            st, near = _infeasibility(dx, du, qp, opts)
+            st, near = _infeasibility(dx, du, qp, opts, M_apply, M_adj)
             if near:
                 rho_frozen = True
             if st is not None:
@@ -642,7 +817,7 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
                 trend.clear()
                 rho, u, ev = _change_penalty(rho, u, rho * opts.tau, k)
                 res.penalty_events.append(ev)
-                if sketch is not None:
+                if sketch is not None and identity_M:
                     pc_nu = nu_of(rho)
                 xw.clear()
                 uw.clear()
@@ -671,7 +846,7 @@ def solve(problem, opts: Optional[Options] = None) -> OracleResult:
             if new is not None:
                 rho, u, ev = _change_penalty(rho, u, new, k)
                 res.penalty_events.append(ev)
-                if sketch is not None:
+                if sketch is not None and identity_M:
                     pc_nu = nu_of(rho)
                 xw.clear()
                 uw.clear()
@@ -701,19 +876,19 @@ def _change_penalty(rho_old, u, rho_new, k):  # admm.py:303-319
     return rho_new, u, (k, rho_old, rho_new, jump)
 
 
-def _infeasibility(dx, du, qp: QPSpec, opts: Options):  # admm.py:361-415, M = I
+def _infeasibility(dx, du, qp: QPSpec, opts: Options, M_apply=lambda v: v, M_adj=lambda v: v):  # admm.py:361-415
     eps = opts.eps_inf
     primal = dual = near_p = near_d = False
     dun = float(np.linalg.norm(du))
     if dun > 1e-14:
-        t_map = float(np.linalg.norm(du))
+        t_map = float(np.linalg.norm(M_adj(du)))
         t_sup = box_support(du, qp.lo, qp.hi)
         primal = t_map < eps * dun and t_sup < eps * dun
         near_p = t_map < 10 * eps * dun and t_sup < 10 * eps * dun
     dxn = float(np.linalg.norm(dx))
     if dxn > 1e-14:
         s_obj = float(np.linalg.norm(qp.P @ dx))
-        s_cone = box_recession_distance(dx, qp.lo, qp.hi)
+        s_cone = box_recession_distance(M_apply(dx), qp.lo, qp.hi)
         s_lin = float(qp.q @ dx)
         dual = s_obj < eps * dxn and s_cone < eps * dxn and s_lin < eps * dxn
         near_d = s_obj < 10 * eps * dxn and s_cone < 10 * eps * dxn and s_lin < 10 * eps * dxn

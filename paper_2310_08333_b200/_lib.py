@@ -150,6 +150,17 @@ SIGNATURES = {
     "nys_nystrom_core_f64": (I32, [I64, I32, I32, P, P, P, P, C.POINTER(C.c_int), P, SZ, P]),
     "nys_syevj_workspace": (SZ, [I32]),
     "nys_syevj_f64": (I32, [I32, P, P, P, P, SZ, P]),
+    "nys_csr_spmv_f64": (I32, [I64, P, P, P, P, F64, P, F64, P, P, I32, P]),
+    "nys_csr_spmm_f64": (I32, [I64, P, P, P, P, I64, I32, P, P, I64, P]),
+    "nys_csr_transpose_workspace": (SZ, [I64, I64]),
+    "nys_csr_transpose": (I32, [I64, I64, P, P, P, P, P, P, P, SZ, P]),
+    "nys_vmul_f64": (I32, [I64, F64, P, P, F64, P, P]),
+    "nys_bcast_f64": (I32, [I64, P, F64, P, P]),
+    "nys_vstats_f64": (I32, [I64, P, P, P, P, P]),
+    "nys_gdual_f64": (I32, [I64, P, P, F64, P, P, P]),
+    "nys_absstats_f64": (I32, [I64, P, F64, P, P, P]),
+    "nys_box_cert_f64": (I32, [I64, P, P, P, P, P, P, P]),
+    "nys_box_violation_f64": (I32, [I64, P, P, P, P, P, P]),
 }
 
 _lock = threading.Lock()

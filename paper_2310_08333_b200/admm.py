@@ -1238,10 +1238,26 @@ def solve(problem, options: Optional[SolverOptions] = None, x0=None, z0=None, u0
     options = options or SolverOptions()
     gp = lower(problem)
     if gp.ml is None and gp.qp is None:
-        raise CapabilityError("generic problems (user f/prox callables) are outside the dense B200 path")
+        raise CapabilityError("generic problems (user f/prox callables) are outside the B200 path")
     if kernels is None:
         from .kernels import get_kernels
 
         kernels = get_kernels()
+    if not _dense_path(gp):
+        # sparse data, structured P, general constraint maps: the general-operator
+        # engine (general.py), same control flow, one device pass per operator
+        if shard is not None and shard.sharded:
+            raise CapabilityError("row sharding covers dense data matrices only")
+        from .general import _GeneralEngine
+
+        return _GeneralEngine(gp, options, kernels).run(x0, z0, u0, callback, t_start)
     eng = _Engine(gp, options, kernels, shard)
     return eng.run(x0, z0, u0, callback, t_start)
+
+
+def _dense_path(gp: GenericProblem) -> bool:
+    """Problems the fused dense engine takes: dense ML data, or a dense QP
+    matrix with M = I (BASELINE.json's configs)."""
+    if gp.ml is not None:
+        return isinstance(gp.ml.A, DenseOperator) and gp.ml.loss.kind in _lib.LOSS
+    return isinstance(gp.qp.P, DenseOperator) and isinstance(gp.qp.M, IdentityOperator)

@@ -197,6 +197,11 @@ class Kernels:
         self.launches += 1
         check(self.L.nys_admm_tail_f64(C.byref(t), self.sp), "admm_tail")
 
+    def copy(self, src: torch.Tensor, dst: torch.Tensor) -> None:
+        """dst[:] = src[:] (contiguous FP64, device or mapped pinned memory)."""
+        self.launches += 1
+        check(self.L.nys_copy_f64(src.data_ptr(), dst.data_ptr(), src.numel(), self.sp), "copy")
+
     def copy_to_pinned(self, src: torch.Tensor, dst: torch.Tensor) -> None:
         """Kernel copy of a small device vector into pinned host memory."""
         self.launches += 1
@@ -384,6 +389,65 @@ class Kernels:
         self.launches += 1
         check(self.L.nys_syevj_f64(s, A.data_ptr(), V.data_ptr(), w.data_ptr(), ws.data_ptr(), ws.numel(),
                                    self.sp), "syevj")
+
+    # ------------------------------------- sparse / general-operator engine --
+    def csr_spmv(self, csr, x, y, alpha=1.0, dscale=None, beta=0.0, zin=None) -> None:
+        """y = alpha * dscale o (A x) + beta * zin for a device CSR ``csr``."""
+        self.launches += 1
+        check(self.L.nys_csr_spmv_f64(csr.rows, csr.rowptr.data_ptr(), csr.col.data_ptr(), csr.val.data_ptr(),
+                                      x.data_ptr(), float(alpha), _p(dscale), float(beta), _p(zin), y.data_ptr(),
+                                      csr.group, self.sp), "csr_spmv")
+
+    def csr_spmm(self, csr, X, Y, dscale=None) -> None:
+        """Y = diag(dscale) A X (X: cols x s row-major)."""
+        self.launches += 1
+        check(self.L.nys_csr_spmm_f64(csr.rows, csr.rowptr.data_ptr(), csr.col.data_ptr(), csr.val.data_ptr(),
+                                      X.data_ptr(), X.stride(0), X.shape[1], _p(dscale), Y.data_ptr(), Y.stride(0),
+                                      self.sp), "csr_spmm")
+
+    def csr_transpose(self, rows, cols, rowptr, col, val, trowptr, tcol, tval) -> None:
+        ws = self.workspace("csrT", self.L.nys_csr_transpose_workspace(rows, cols))
+        self.launches += 1
+        check(self.L.nys_csr_transpose(rows, cols, rowptr.data_ptr(), col.data_ptr(), val.data_ptr(),
+                                       trowptr.data_ptr(), tcol.data_ptr(), tval.data_ptr(), ws.data_ptr(),
+                                       ws.numel(), self.sp), "csr_transpose")
+
+    def vmul(self, a, d, x, b, y) -> None:
+        """y = a (d o x) + b y."""
+        self.launches += 1
+        check(self.L.nys_vmul_f64(x.numel(), float(a), d.data_ptr(), x.data_ptr(), float(b), y.data_ptr(),
+                                  self.sp), "vmul")
+
+    def bcast(self, src, scale, y) -> None:
+        self.launches += 1
+        check(self.L.nys_bcast_f64(y.numel(), src.data_ptr(), float(scale), y.data_ptr(), self.sp), "bcast")
+
+    def vstats(self, x, y, out) -> None:
+        """out = [sum v, sum v^2, max|v|] of v = x - y (y may be None)."""
+        self.launches += 1
+        check(self.L.nys_vstats_f64(x.numel(), x.data_ptr(), _p(y), out.data_ptr(), self.red.data_ptr(),
+                                    self.sp), "vstats")
+
+    def absstats(self, v, lambda1, out) -> None:
+        """out = [sum |v|, sum (|v| - lambda1)_+^2, max |v|]."""
+        self.launches += 1
+        check(self.L.nys_absstats_f64(v.numel(), v.data_ptr(), float(lambda1), out.data_ptr(), self.red.data_ptr(),
+                                      self.sp), "absstats")
+
+    def gdual(self, grad, mtu, rho, out) -> None:
+        self.launches += 1
+        check(self.L.nys_gdual_f64(grad.numel(), grad.data_ptr(), mtu.data_ptr(), float(rho), out.data_ptr(),
+                                   self.red.data_ptr(), self.sp), "gdual")
+
+    def box_cert(self, du, md, lo, hi, out) -> None:
+        self.launches += 1
+        check(self.L.nys_box_cert_f64(lo.numel(), _p(du), _p(md), lo.data_ptr(), hi.data_ptr(), out.data_ptr(),
+                                      self.red.data_ptr(), self.sp), "box_cert")
+
+    def box_violation(self, z, lo, hi, out) -> None:
+        self.launches += 1
+        check(self.L.nys_box_violation_f64(z.numel(), z.data_ptr(), lo.data_ptr(), hi.data_ptr(), out.data_ptr(),
+                                           self.red.data_ptr(), self.sp), "box_violation")
 
 
 _CACHE: dict = {}

@@ -6,10 +6,12 @@
 device).  The dense operator runs the sm_100a GEMV kernels (K1/K2) through the
 C ABI; there is no CPU fallback.
 
-In scope: Identity, Dense, MatrixFree, the Hessian
-contract and ConstantHessian.  Structured/sparse operators (operators.py:89-228)
-are outside the north-star path and raise ``CapabilityError`` if handed to
-``solve``.
+Dense operators run the GEMV kernels of the hot path (SURVEY.md §8(a)
+R6-R8).  The structured and sparse operators of operators.py:89-228 (CSR data,
+diagonal, diagonal-plus-low-rank, vertical stacks, the summing row,
+function-defined Hessians) run the general-operator kernels
+(``csrc/general.cu``); ``solve`` routes problems that use them to the
+general-operator engine (``general.py``).
 """
 
 from __future__ import annotations
@@ -125,6 +127,9 @@ class IdentityOperator(LinearOperator):
     def apply_columns_dev(self, V):
         return V.clone()
 
+    def apply_adjoint_columns_dev(self, U):
+        return U.clone()
+
 
 class DenseOperator(LinearOperator):
     """Operator backed by a dense 2-d array (operators.py:104-118).
@@ -233,6 +238,281 @@ class DenseOperator(LinearOperator):
         return Y
 
 
+class DeviceCSR:
+    """A CSR matrix resident in HBM: int64 row pointer, int32 columns, FP64 values,
+    and the lanes-per-row group the SpMV kernel uses for it."""
+
+    def __init__(self, rows: int, cols: int, rowptr: torch.Tensor, col: torch.Tensor, val: torch.Tensor):
+        self.rows, self.cols = int(rows), int(cols)
+        self.rowptr, self.col, self.val = rowptr, col, val
+        nnz = int(val.numel())
+        mean = nnz / max(self.rows, 1)
+        g = 1
+        while g < 32 and g < mean:
+            g *= 2
+        self.group = g
+
+    @classmethod
+    def upload(cls, a, device) -> "DeviceCSR":
+        rowptr = torch.from_numpy(np.ascontiguousarray(a.indptr, dtype=np.int64)).to(device)
+        col = torch.from_numpy(np.ascontiguousarray(a.indices, dtype=np.int32)).to(device)
+        val = torch.from_numpy(np.ascontiguousarray(a.data, dtype=np.float64)).to(device)
+        if val.numel() == 0:  # keep valid pointers for an all-zero matrix
+            col = torch.zeros(1, dtype=torch.int32, device=device)
+            val = torch.zeros(1, dtype=torch.float64, device=device)
+        return cls(a.shape[0], a.shape[1], rowptr, col, val)
+
+    def transpose(self, kx) -> "DeviceCSR":
+        """CSR of the transpose, built on the device (deterministic counting transpose)."""
+        dev = self.rowptr.device
+        nnz = int(self.rowptr[-1])
+        trowptr = torch.empty(self.cols + 1, dtype=torch.int64, device=dev)
+        tcol = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        tval = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+        if nnz == 0:  # all-zero matrix: valid pointers, nothing to place
+            trowptr.zero_()
+            tcol.zero_()
+            tval.zero_()
+        else:
+            kx.csr_transpose(self.rows, self.cols, self.rowptr, self.col, self.val, trowptr, tcol, tval)
+        return DeviceCSR(self.cols, self.rows, trowptr, tcol, tval)
+
+
+class SparseOperator(LinearOperator):
+    """Operator backed by a scipy sparse matrix stored as CSR (operators.py:121-135).
+
+    The CSR arrays are uploaded to HBM on first use together with the CSR of the
+    transpose (built on the device), so ``apply`` (``a @ v``) and
+    ``apply_adjoint`` (``a.T @ u``) are both row-parallel SpMV kernels."""
+
+    def __init__(self, a):
+        import scipy.sparse as sp
+
+        if not sp.issparse(a):
+            raise DimensionMismatchError("SparseOperator requires a scipy sparse matrix")
+        a = a.tocsr()
+        if not a.has_canonical_format:
+            a = a.copy()
+            a.sum_duplicates()  # the device transpose needs distinct columns per row
+        super().__init__(a.shape[1], a.shape[0])
+        self.a = a
+        self._dev: dict = {}
+
+    def device_csr(self, device=None):
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        key = str(device)
+        pair = self._dev.get(key)
+        if pair is None:
+            kx = _kx()
+            fwd = DeviceCSR.upload(self.a, device)
+            pair = (fwd, fwd.transpose(kx))
+            self._dev[key] = pair
+        return pair
+
+    def release(self) -> None:
+        self._dev.clear()
+
+    def _apply_dev(self, v):
+        kx = _kx()
+        fwd, _ = self.device_csr()
+        y = kx.empty(self.output_dim)
+        kx.csr_spmv(fwd, v, y)
+        return y
+
+    def _apply_adjoint_dev(self, u):
+        kx = _kx()
+        _, bwd = self.device_csr()
+        y = kx.empty(self.input_dim)
+        kx.csr_spmv(bwd, u, y)
+        return y
+
+    def apply_columns_dev(self, V):
+        kx = _kx()
+        fwd, _ = self.device_csr()
+        Y = kx.empty(self.output_dim, V.shape[1])
+        kx.csr_spmm(fwd, V.contiguous(), Y)
+        return Y
+
+    def apply_adjoint_columns_dev(self, U):
+        kx = _kx()
+        _, bwd = self.device_csr()
+        Y = kx.empty(self.input_dim, U.shape[1])
+        kx.csr_spmm(bwd, U.contiguous(), Y)
+        return Y
+
+
+class DiagonalOperator(LinearOperator):
+    """Multiplication by diag(d) (operators.py:89-101)."""
+
+    def __init__(self, d):
+        d = np.asarray(d.detach().cpu().numpy() if isinstance(d, torch.Tensor) else d, dtype=float)
+        super().__init__(d.size, d.size)
+        self.d = d
+        self._dd = None
+
+    def _ddev(self):
+        if self._dd is None:
+            self._dd = to_device(self.d)
+        return self._dd
+
+    def _apply_dev(self, v):
+        kx = _kx()
+        y = kx.empty(self.output_dim)
+        kx.vmul(1.0, self._ddev(), v, 0.0, y)
+        return y
+
+    def _apply_adjoint_dev(self, u):
+        return self._apply_dev(u)
+
+    def apply_columns_dev(self, V):
+        Y = V.contiguous().clone()
+        _kx().row_scale(Y, self._ddev())
+        return Y
+
+    def apply_adjoint_columns_dev(self, U):
+        return self.apply_columns_dev(U)
+
+
+class DiagPlusLowRank(LinearOperator):
+    """Symmetric diag(d) + F F^T kept in factored form (operators.py:138-160):
+    apply = d o v + F (F^T v), two skinny GEMVs and one elementwise pass."""
+
+    def __init__(self, d, F):
+        d = np.asarray(d, dtype=float)
+        F = np.asarray(F, dtype=float)
+        if F.ndim != 2 or F.shape[0] != d.size:
+            raise DimensionMismatchError("factor F must be n-by-k with n = len(d)")
+        super().__init__(d.size, d.size)
+        self.d = d
+        self.F = F
+        self._dev = None
+
+    def _devs(self):
+        if self._dev is None:
+            self._dev = (to_device(self.d), to_device(np.ascontiguousarray(self.F)))
+        return self._dev
+
+    def _apply_dev(self, v):
+        kx = _kx()
+        d, F = self._devs()
+        t = kx.empty(1, F.shape[1])
+        kx.gemvT(F, v.view(1, -1), t)  # F^T v
+        y = kx.empty(1, self.output_dim)
+        kx.gemv(F, t, y)  # F (F^T v)
+        y = y.view(-1)
+        kx.vmul(1.0, d, v, 1.0, y)  # d o v + F (F^T v)
+        return y
+
+    def _apply_adjoint_dev(self, u):
+        return self._apply_dev(u)
+
+    def apply_columns_dev(self, V):
+        kx = _kx()
+        d, F = self._devs()
+        n, k = F.shape
+        s = V.shape[1]
+        V = V.contiguous()
+        T = kx.empty(k, s)
+        kx.gemm(1, 0, k, s, n, 1.0, F, F.stride(0), V, V.stride(0), 0.0, T, s)
+        Y = V.clone()
+        kx.row_scale(Y, d)
+        kx.gemm(0, 0, n, s, k, 1.0, F, F.stride(0), T, s, 1.0, Y, s)
+        return Y
+
+    def apply_adjoint_columns_dev(self, U):
+        return self.apply_columns_dev(U)
+
+
+class StackedOperator(LinearOperator):
+    """Vertical concatenation [A_1; A_2; ...] on a common domain
+    (operators.py:163-191); the adjoint sums the part adjoints."""
+
+    def __init__(self, ops):
+        ops = list(ops)
+        if not ops:
+            raise DimensionMismatchError("stack_vertical requires at least one operator")
+        n = ops[0].input_dim
+        for op in ops:
+            if op.input_dim != n:
+                raise DimensionMismatchError("stacked operators must share input_dim")
+        super().__init__(n, sum(op.output_dim for op in ops))
+        self.ops = ops
+        self._offsets = np.cumsum([0] + [op.output_dim for op in ops])
+
+    @property
+    def has_adjoint(self) -> bool:
+        return all(op.has_adjoint for op in self.ops)
+
+    def _apply_dev(self, v):
+        kx = _kx()
+        y = kx.empty(self.output_dim)
+        for op, lo, hi in zip(self.ops, self._offsets[:-1], self._offsets[1:]):
+            kx.copy(op._apply_dev(v), y[lo:hi])
+        return y
+
+    def _apply_adjoint_dev(self, u):
+        kx = _kx()
+        out = kx.zeros(self.input_dim)
+        for op, lo, hi in zip(self.ops, self._offsets[:-1], self._offsets[1:]):
+            kx.axpby(1.0, op._apply_adjoint_dev(u[lo:hi].contiguous()), 1.0, out)
+        return out
+
+    def apply_columns_dev(self, V):
+        return torch.cat([op.apply_columns_dev(V) for op in self.ops], dim=0).contiguous()
+
+    def apply_adjoint_columns_dev(self, U):
+        kx = _kx()
+        out = kx.zeros(self.input_dim, U.shape[1])
+        flat = out.view(-1)
+        for op, lo, hi in zip(self.ops, self._offsets[:-1], self._offsets[1:]):
+            kx.axpby(1.0, adjoint_columns_dev(op, U[lo:hi].contiguous()).reshape(-1), 1.0, flat)
+        return out
+
+
+class OnesRowOperator(LinearOperator):
+    """The 1-by-n summing map v -> (sum v); adjoint broadcasts a scalar
+    (operators.py:194-203)."""
+
+    def __init__(self, dim: int):
+        super().__init__(dim, 1)
+
+    def _apply_dev(self, v):
+        out = _kx().empty(3)
+        _kx().vstats(v, None, out)
+        return out[:1]
+
+    def _apply_adjoint_dev(self, u):
+        y = _kx().empty(self.input_dim)
+        _kx().bcast(u, 1.0, y)
+        return y
+
+    def apply_columns_dev(self, V):
+        kx = _kx()
+        n, s = V.shape
+        ones = torch.ones(1, n, dtype=F64, device=V.device)
+        Y = kx.empty(1, s)
+        kx.gemm(0, 0, 1, s, n, 1.0, ones, n, V.contiguous(), s, 0.0, Y, s)
+        return Y
+
+    def apply_adjoint_columns_dev(self, U):
+        kx = _kx()
+        s = U.shape[1]
+        ones = torch.ones(self.input_dim, 1, dtype=F64, device=U.device)
+        Y = kx.empty(self.input_dim, s)
+        kx.gemm(0, 0, self.input_dim, s, 1, 1.0, ones, 1, U.contiguous(), s, 0.0, Y, s)
+        return Y
+
+
+def adjoint_columns_dev(op: LinearOperator, U: torch.Tensor) -> torch.Tensor:
+    """op^T applied to every column of the row-major m x s matrix U."""
+    f = getattr(op, "apply_adjoint_columns_dev", None)
+    if f is not None:
+        return f(U)
+    cols = [op._apply_adjoint_dev(U[:, j].contiguous()) for j in range(U.shape[1])]
+    return torch.stack(cols, dim=1).contiguous()
+
+
 class MatrixFreeOperator(LinearOperator):
     """Operator defined by device callables (operators.py:206-228): ``matvec``
     and ``rmatvec`` take and return CUDA tensors."""
@@ -280,6 +560,24 @@ class HessianOperator(LinearOperator):
         return self._apply_dev(u)
 
 
+class FunctionHessian(HessianOperator):
+    """Hessian-vector product supplied as a callable ``hvp(x, v)`` on CUDA
+    tensors (operators.py:280-297); ``update`` stores the evaluation point."""
+
+    is_constant = False
+
+    def __init__(self, dim: int, hvp: Callable, x0=None):
+        super().__init__(dim)
+        self._hvp = hvp
+        self._x = torch.zeros(dim, dtype=F64, device="cuda") if x0 is None else to_device(x0)
+
+    def update(self, x) -> None:
+        self._x = to_device(x).clone()
+
+    def _apply_dev(self, v):
+        return to_device(self._hvp(self._x, v))
+
+
 class ConstantHessian(HessianOperator):
     """Hessian that never changes (quadratic objectives), operators.py:267-277."""
 
@@ -297,23 +595,25 @@ class ConstantHessian(HessianOperator):
 
 
 def as_operator(a) -> LinearOperator:
-    """Coerce an ndarray / CUDA tensor / operator into a LinearOperator
-    (operators.py:300-309).  Sparse input is outside the dense hot path."""
+    """Coerce an ndarray / CUDA tensor / scipy sparse matrix / operator into a
+    LinearOperator (operators.py:300-309)."""
     if isinstance(a, LinearOperator):
         return a
-    try:
-        import scipy.sparse as sp
+    import scipy.sparse as sp
 
-        if sp.issparse(a):
-            raise CapabilityError("sparse operators are not implemented on the B200 path (dense only)")
-    except ImportError:  # pragma: no cover
-        pass
+    if sp.issparse(a):
+        return SparseOperator(a)
     if isinstance(a, torch.Tensor):
         return DenseOperator(a)
     arr = np.asarray(a, dtype=float)
     if arr.ndim != 2:
         raise DimensionMismatchError("expected a 2-d matrix or a LinearOperator")
     return DenseOperator(arr)
+
+
+def stack_vertical(ops) -> "StackedOperator":
+    """Vertically stack operators sharing a common input dimension (operators.py:312-314)."""
+    return StackedOperator(ops)
 
 
 def update_hessian(op: HessianOperator, x) -> None:

@@ -20,7 +20,7 @@ from typing import Callable, Optional
 import numpy as np
 import torch
 
-from .errors import CapabilityError, DataError
+from .errors import DataError
 from .operators import (
     ConstantHessian,
     DenseOperator,
@@ -173,6 +173,26 @@ def huber_problem(A, b, lambda1: float) -> MLProblem:
     return MLProblem(huber_loss(), A, b, lambda1=lambda1, lambda2=0.0)
 
 
+def lasso_as_qp(A, b, lambda1: float) -> QPProblem:
+    """Block QP reformulation of the lasso with auxiliary magnitudes t
+    (problems.py:484-502): variables (x, t), |x| <= t by two stacked identity
+    blocks; P and the constraint matrix are kept sparse (CSR on the device)."""
+    import scipy.sparse as sp
+
+    A = np.asarray(A, dtype=float)
+    b = np.asarray(b, dtype=float)
+    n = A.shape[1]
+    P = sp.bmat([[sp.csr_matrix(A.T @ A), None], [None, sp.csr_matrix((n, n))]])
+    q = np.concatenate([-A.T @ b, lambda1 * np.ones(n)])
+    eye = sp.eye(n)
+    M = sp.bmat([[eye, eye], [eye, -eye]])
+    lo = np.concatenate([np.zeros(n), np.full(n, -np.inf)])
+    hi = np.concatenate([np.full(n, np.inf), np.zeros(n)])
+    from .operators import SparseOperator
+
+    return QPProblem(SparseOperator(P.tocsr()), q, SparseOperator(M.tocsr()), Box(lo, hi))
+
+
 def qp_lower(qp: QPProblem) -> GenericProblem:
     """problems.py:387-421 (full_rank iff M is the identity)."""
     return GenericProblem(n=qp.n, m=qp.m, M=qp.M, c=np.zeros(qp.m), hess=ConstantHessian(qp.P),
@@ -200,10 +220,36 @@ def lower(problem) -> GenericProblem:
 # solver uses fused, sharded versions of the same kernels.
 
 
-def _dense_A(p: MLProblem) -> torch.Tensor:
-    if not isinstance(p.A, DenseOperator):
-        raise CapabilityError("the B200 path supports dense data matrices only")
-    return p.A.device_rows()
+def _dense_A(p: MLProblem) -> Optional[torch.Tensor]:
+    """The data matrix in HBM when A is dense (the GEMV/HVP kernels), else None."""
+    return p.A.device_rows() if isinstance(p.A, DenseOperator) else None
+
+
+def _a_rows(p: MLProblem, X: torch.Tensor) -> torch.Tensor:
+    """A X[j] for the k rows of X: one multi-RHS GEMV for dense data, the
+    operator's own kernel (CSR SpMV, ...) otherwise."""
+    from .kernels import get_kernels
+
+    kx = get_kernels()
+    A = _dense_A(p)
+    if A is not None:
+        Y = kx.empty(X.shape[0], p.N)
+        kx.gemv(A, X, Y)
+        return Y
+    return torch.stack([p.A._apply_dev(X[j].contiguous()) for j in range(X.shape[0])])
+
+
+def _at_rows(p: MLProblem, T: torch.Tensor) -> torch.Tensor:
+    """A^T T[j] for the k rows of T."""
+    from .kernels import get_kernels
+
+    kx = get_kernels()
+    A = _dense_A(p)
+    if A is not None:
+        Y = kx.empty(T.shape[0], p.n)
+        kx.gemvT(A, T, Y)
+        return Y
+    return torch.stack([p.A._apply_adjoint_dev(T[j].contiguous()) for j in range(T.shape[0])])
 
 
 class _MLEval:
@@ -214,15 +260,13 @@ class _MLEval:
 
         self.p = p
         self.kx = get_kernels()
-        self.A = _dense_A(p)
         self.b = to_device(p.b)
-        self.N, self.n = self.A.shape
+        self.N, self.n = p.N, p.n
 
     def at(self, x, z=None):
         kx = self.kx
         X = torch.stack([to_device(x)] + ([to_device(z)] if z is not None else [])).contiguous()
-        AX = kx.empty(X.shape[0], self.N)
-        kx.gemv(self.A, X, AX)
+        AX = _a_rows(self.p, X)
         tg, w, thx, tnu = (kx.empty(self.N) for _ in range(4))
         out = kx.zeros(8)
         kx.ml_rowwise(self.p.loss.kind, AX[0], AX[1] if z is not None else None, self.b, tg, w, thx,
@@ -246,9 +290,7 @@ def ml_gradient(p: MLProblem, x):
     """A' l'(Ax - b) + lambda2 x (problems.py:238-242)."""
     ev = _MLEval(p)
     _, tg, _, _, _, _ = ev.at(x)
-    g = ev.kx.empty(1, ev.n)
-    ev.kx.gemvT(ev.A, tg.view(1, -1), g)
-    g = g.view(-1)
+    g = _at_rows(p, tg.view(1, -1)).view(-1).contiguous()
     ev.kx.axpby(p.lambda2, to_device(x), 1.0, g)
     return like_input(g, x)
 
@@ -280,19 +322,36 @@ class MLHessian(HessianOperator):
             return np.ones(self.p.N)
         return self._w.cpu().numpy()
 
-    def _apply_dev(self, v):
+    def _hvp(self, v, shift):
         from .kernels import get_kernels
 
         kx = get_kernels()
         y = kx.empty(self.input_dim)
-        kx.hvp(self._A, self._w, v, self.diag_shift, y, None, True)
+        if self._A is not None:
+            kx.hvp(self._A, self._w, v, shift, y, None, True)
+            return y
+        t = self.p.A._apply_dev(v)
+        if self._w is not None:
+            kx.vmul(1.0, self._w, t, 0.0, t)
+        y = self.p.A._apply_adjoint_dev(t)
+        if shift != 0.0:
+            kx.axpby(shift, v, 1.0, y)
         return y
+
+    def _apply_dev(self, v):
+        return self._hvp(v, self.diag_shift)
 
     def _smooth_cols(self, V):
         from .kernels import get_kernels
+        from .operators import adjoint_columns_dev
 
         kx = get_kernels()
         A = self._A
+        if A is None:
+            Z = self.p.A.apply_columns_dev(V.contiguous())
+            if self._w is not None:
+                kx.row_scale(Z, self._w)
+            return adjoint_columns_dev(self.p.A, Z)
         N, n = A.shape
         s = V.shape[1]
         Z = kx.empty(N, s)
@@ -305,13 +364,9 @@ class MLHessian(HessianOperator):
 
     def smooth_part(self) -> LinearOperator:
         """A' diag(w) A, the sketching target (problems.py:266-273)."""
-        from .kernels import get_kernels
 
         def mv(v):
-            kx = get_kernels()
-            y = kx.empty(self.input_dim)
-            kx.hvp(self._A, self._w, to_device(v), 0.0, y, None, True)
-            return y
+            return self._hvp(to_device(v), 0.0)
 
         op = MatrixFreeOperator(self.input_dim, self.output_dim, mv, mv)
         op.apply_columns_dev = self._smooth_cols
@@ -343,8 +398,7 @@ def ml_dual_point(p: MLProblem, x):
     AX, tg, _, _, _, _ = ev.at(x)
     nu = tg
     if p.lambda2 == 0.0:
-        at = ev.kx.empty(1, ev.n)
-        ev.kx.gemvT(ev.A, nu.view(1, -1), at)
+        at = _at_rows(p, nu.view(1, -1))
         denom = float(at.abs().max()) if at.numel() else 0.0
         if denom > p.lambda1:
             nu = nu * (p.lambda1 / denom)
@@ -365,9 +419,7 @@ def ml_dual_value(p: MLProblem, nu) -> float:
         return -np.inf
     val = -float(o[0]) - float(o[2])
     if p.lambda2 > 0.0:
-        A = _dense_A(p)
-        at = kx.empty(1, A.shape[1])
-        kx.gemvT(A, nut.view(1, -1), at)
+        at = _at_rows(p, nut.view(1, -1))
         excess = torch.clamp(at.abs() - p.lambda1, min=0.0)
         val -= float(torch.sum(excess * excess)) / (2.0 * p.lambda2)
     return val

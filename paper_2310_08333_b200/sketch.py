@@ -193,11 +193,22 @@ class NystromSketch:
     def empty(cls, n: int) -> "NystromSketch":
         return cls(np.zeros((n, 0)), np.zeros(0))
 
-    def approx_apply(self, v):
-        vt = to_device(v)
+    def approx_apply_dev(self, v: torch.Tensor) -> torch.Tensor:
+        """U diag(lambda) U^T v (sketch.py:53-58): two skinny GEMVs + one scaling."""
+        from .kernels import get_kernels
+
+        kx = get_kernels()
         if self.rank == 0:
-            return like_input(torch.zeros_like(vt), v)
-        return like_input(self.U_dev @ (self.lam_dev * (self.U_dev.T @ vt)), v)
+            return kx.zeros(self._n)
+        h = kx.empty(1, self._r)
+        kx.gemvT(self.U_dev, v.view(1, -1), h)  # U^T v
+        kx.vmul(1.0, self.lam_dev, h.view(-1), 0.0, h.view(-1))
+        y = kx.empty(1, self._n)
+        kx.gemv(self.U_dev, h, y)
+        return y.view(-1)
+
+    def approx_apply(self, v):
+        return like_input(self.approx_apply_dev(to_device(v)), v)
 
     def to_dense(self) -> np.ndarray:
         return (self.U * self.lambda_hat) @ self.U.T
@@ -268,3 +279,151 @@ def precond_apply(P: NystromPreconditioner, v):
 
 def update_shift(P: NystromPreconditioner, nu_new: float) -> None:
     P.update_shift(nu_new)
+
+
+# ---------------------------------------------------------------------------
+# Adaptive sizing and spectrum probes (sketch.py:176-306), on the device: every
+# operator apply, norm and reorthogonalisation is a libnysgpu kernel; the host
+# keeps the scalar recurrences (the reference's Python floats).
+
+
+def _unit_gaussian(kx, n: int, seed: int) -> torch.Tensor:
+    """default_rng(seed).standard_normal(n) drawn on the GPU, scaled to unit norm."""
+    v = kx.empty(n)
+    kx.gaussian(seed, v)
+    st = kx.zeros(3)
+    kx.vstats(v, None, st)
+    nrm = math.sqrt(max(float(st[1]), 0.0))
+    kx.axpby(0.0, v, 1.0 / nrm, v)
+    return v
+
+
+def estimate_error_norm(A: LinearOperator, S: NystromSketch, iters: int, rng_seed: int) -> float:
+    """Power-method estimate of ||A - A_hat||_2 (sketch.py:176-195)."""
+    from .kernels import get_kernels
+
+    if iters < 1:
+        raise DataError("estimate_error_norm requires iters >= 1")
+    kx = get_kernels()
+    n = A.input_dim
+    v = _unit_gaussian(kx, n, rng_seed)
+    est = 0.0
+    st = kx.zeros(3)
+    for _ in range(iters):
+        w = A._apply_dev(v)
+        kx.axpby(-1.0, S.approx_apply_dev(v), 1.0, w)
+        kx.vstats(w, None, st)
+        est = math.sqrt(max(float(st[1]), 0.0)) if math.isfinite(float(st[1])) else float(st[1])
+        if est <= 0.0 or not np.isfinite(est):
+            return max(est, 0.0)
+        kx.axpby(0.0, w, 1.0 / est, w)
+        v = w
+    return est
+
+
+def condition_bound(sketch: NystromSketch, err_norm: float, nu: float) -> float:
+    """1 + (lam_r + ||E||) / nu, an upper bound on the preconditioned condition
+    number (sketch.py:198-201)."""
+    tail = float(sketch.lambda_hat[-1]) if sketch.rank > 0 else 0.0
+    return 1.0 + (tail + err_norm) / nu
+
+
+def adaptive_sketch(A: LinearOperator, r0: int, r_max: int, nu: float, kappa_target: float, rng_seed: int,
+                    power_iters: int = 10) -> NystromSketch:
+    """Doubling-rank sketch until the condition bound meets kappa_target
+    (sketch.py:204-237); the seeds follow the reference's SeedSequence."""
+    n = A.input_dim
+    if not 1 <= r0 <= r_max <= n:
+        raise DataError("adaptive_sketch requires 1 <= r0 <= r_max <= n")
+    ranks = []
+    r = r0
+    while r < r_max:
+        ranks.append(r)
+        r *= 2
+    ranks.append(r_max)
+    seeds = np.random.SeedSequence(rng_seed).generate_state(2 * len(ranks))
+    sketch = None
+    for i, rank in enumerate(ranks):
+        sketch = nystrom_sketch(A, rank, int(seeds[2 * i]))
+        err = estimate_error_norm(A, sketch, power_iters, int(seeds[2 * i + 1]))
+        if condition_bound(sketch, err, nu) <= kappa_target:
+            return sketch
+    return sketch
+
+
+def estimate_extreme_eigs(A: LinearOperator, iters: int, rng_seed: int):
+    """Extreme Ritz values (lambda_max, lambda_min) of a symmetric operator by
+    Lanczos with full reorthogonalisation, twice (sketch.py:240-282).  The Lanczos
+    basis lives in HBM as rows of Q; the projections Q w and Q^T h are GEMV
+    kernels, the tridiagonal eigenvalues come from the device eigensolver."""
+    from .kernels import get_kernels
+
+    if iters < 2:
+        raise DataError("estimate_extreme_eigs requires iters >= 2")
+    kx = get_kernels()
+    n = A.input_dim
+    iters = min(iters, n)
+    Q = kx.zeros(iters, n)
+    Q[0].copy_(_unit_gaussian(kx, n, rng_seed))
+    alphas: list = []
+    betas: list = []
+    scale = 0.0
+    st = kx.zeros(4)
+    for j in range(iters):
+        qj = Q[j]
+        w = A._apply_dev(qj).contiguous()
+        kx.dot(qj, w, st[0:1])
+        alpha = float(st[0])
+        alphas.append(alpha)
+        scale = max(scale, abs(alpha))
+        kx.axpby(-alpha, qj, 1.0, w)
+        if j > 0:
+            kx.axpby(-betas[-1], Q[j - 1], 1.0, w)
+        for _ in range(2):  # full reorthogonalisation, twice
+            h = kx.empty(1, j + 1)
+            kx.gemv(Q[:j + 1], w.view(1, -1), h)  # Q_j^T w  (Q stored by rows)
+            c = kx.empty(1, n)
+            kx.gemvT(Q[:j + 1], h, c)
+            kx.axpby(-1.0, c.view(-1), 1.0, w)
+        kx.vstats(w, None, st[1:4])
+        beta = math.sqrt(max(float(st[2]), 0.0))
+        if j == iters - 1 or beta <= 1e-12 * max(scale, 1.0):
+            break
+        betas.append(beta)
+        kx.axpby(0.0, w, 1.0 / beta, w)
+        Q[j + 1].copy_(w)
+    k = len(alphas)
+    if k == 1:
+        return alphas[0], alphas[0]
+    T = np.diag(alphas)
+    T += np.diag(betas[:k - 1], 1) + np.diag(betas[:k - 1], -1)
+    Td = to_device(T)
+    V = kx.empty(k, k)
+    lam = kx.empty(k)
+    kx.syevj(Td, V, lam)  # descending
+    ritz = lam.cpu().numpy()
+    return float(ritz[0]), float(ritz[-1])
+
+
+def diagonal_reduce(A: LinearOperator, d):
+    """(D^{-1/2} A D^{-1/2}, d^{-1/2}) for the unit-shift form of (A + diag(d)) w = b
+    (sketch.py:285-306)."""
+    from .kernels import get_kernels
+    from .operators import MatrixFreeOperator
+
+    dh = np.asarray(d.detach().cpu().numpy() if isinstance(d, torch.Tensor) else d, dtype=float)
+    if dh.size != A.input_dim:
+        raise DataError("diagonal length must match the operator dimension")
+    if np.any(dh <= 0):
+        raise DataError("diagonal_reduce requires strictly positive d")
+    s_dev = torch.rsqrt(to_device(dh))
+
+    def matvec(v, _A=A, _s=s_dev):
+        kx = get_kernels()
+        t = kx.empty(_A.input_dim)
+        kx.vmul(1.0, _s, to_device(v), 0.0, t)
+        y = _A._apply_dev(t)
+        kx.vmul(1.0, _s, y, 0.0, y)
+        return y
+
+    return MatrixFreeOperator(A.input_dim, A.input_dim, matvec, matvec), like_input(s_dev, d)

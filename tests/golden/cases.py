@@ -92,6 +92,148 @@ def _qp_unbounded(n=10, seed=9):
     return dict(P=np.zeros((n, n)), q=q, lo=np.zeros(n), hi=np.full(n, np.inf))
 
 
+# ---- general-operator cases (sparse data, structured P, general M) ----------
+
+
+def _sparse(N, n, seed, density):
+    """Seeded CSR data with ragged rows, one empty row and one empty column."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(seed)
+    mask = rng.random((N, n)) < density
+    vals = rng.standard_normal((N, n)) / np.sqrt(N * density)
+    D = np.where(mask, vals, 0.0)
+    D[7, :] = 0.0
+    D[:, 3] = 0.0
+    return sp.csr_matrix(D)
+
+
+def _sparse_ml(kind, N, n, seed, density=0.05, lam2=0.0, lam_frac=0.1):
+    A = _sparse(N, n, seed, density)
+    rng = np.random.default_rng(seed + 1000)
+    xt = np.zeros(n)
+    sup = rng.choice(n, size=max(1, n // 10), replace=False)
+    xt[sup] = rng.standard_normal(sup.size)
+    if kind == "logistic":
+        y = np.where(rng.random(N) < 1.0 / (1.0 + np.exp(-(A @ xt) * 3.0)), 1.0, -1.0)
+        A = A.multiply(-y[:, None]).tocsr()
+        b = np.zeros(N)
+        lam1 = lam_frac * float(np.max(np.abs(A.T @ np.ones(N)))) / 2.0
+    else:
+        b = A @ xt + 0.05 * rng.standard_normal(N)
+        lam1 = lam_frac * float(np.max(np.abs(A.T @ b)))
+    return dict(loss=kind, A=A, b=b, lambda1=lam1, lambda2=lam2)
+
+
+def _lasso_qp(N=60, n=30, seed=31):
+    """lasso_as_qp inputs (problems.py:484-502): the QP itself is built by each
+    consumer's own lasso_as_qp (sparse P and a sparse 2x2-block M)."""
+    d = _ml_small("square", N, n, seed)
+    return dict(lasso_qp=(d["A"], d["b"], d["lambda1"]))
+
+
+def _portfolio(path):
+    """Portfolio allocation on the reference generator's data (stored inputs):
+    path "operators" = diag-plus-low-rank P and the stacked [1'; I] map
+    (datagen.py:180-193); "qp" = the lifted QP with a sparse M (datagen.py:148-177)."""
+    import os
+
+    import scipy.sparse as sp
+
+    f = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "input_portfolio.npz"))
+    d, F, mu, gamma = f["d"], f["F"], f["mu"], float(f["gamma"])
+    n, k = F.shape
+    if path == "operators":
+        return dict(P={"dplr": (gamma * d, np.sqrt(gamma) * F)}, q=-mu, M={"stack": ["ones", "eye"]},
+                    lo=np.concatenate([[1.0], np.zeros(n)]), hi=np.concatenate([[1.0], np.full(n, np.inf)]))
+    P = {"diag": np.concatenate([gamma * d, gamma * np.ones(k)])}
+    M = sp.bmat([[sp.csr_matrix(F.T), -sp.eye(k)], [sp.csr_matrix(np.ones((1, n))), None],
+                 [sp.eye(n), None]]).tocsr()
+    return dict(P=P, q=np.concatenate([-mu, np.zeros(k)]), M=M,
+                lo=np.concatenate([np.zeros(k), [1.0], np.zeros(n)]),
+                hi=np.concatenate([np.zeros(k), [1.0], np.full(n, np.inf)]))
+
+
+def _qp_primal_infeasible(n=20, m=60, seed=4):
+    """Contradictory parallel rows planted in a random sparse-pattern dense M
+    (the construction of tests/test_admm.py:365-388)."""
+    rng = np.random.default_rng(seed)
+    Pt = rng.random((n, n))
+    P = Pt.T @ Pt
+    q = rng.random(n)
+    M = rng.standard_normal((m, n)) * (rng.random((m, n)) < 0.3)
+    hi = 3 + rng.standard_normal(m)
+    lo = -3 + rng.standard_normal(m)
+    lo, hi = np.minimum(lo, hi), np.maximum(lo, hi)
+    j = m // 2
+    M[j] = M[j + 1]
+    lo[j] = hi[j + 1] + 10 * rng.random()
+    hi[j] = lo[j] + 0.5
+    return dict(P=P, q=q, M=M, lo=lo, hi=hi)
+
+
+def _qp_check_rank(seed=12345):
+    """PD P (6x6) with a dense 8x6 M (tests/test_admm.py:605-615 shapes)."""
+    rng = np.random.default_rng(seed)
+    P = rng.standard_normal((6, 6))
+    P = P @ P.T + 0.5 * np.eye(6)
+    M = rng.standard_normal((8, 6))
+    return dict(P=P, q=rng.standard_normal(6), M=M, lo=-np.ones(8), hi=np.ones(8))
+
+
+def _qp_dense_M(n=40, m=60, seed=41):
+    """Rank-deficient P (rank n/2) with a tall dense M: sigma_eff = sigma."""
+    rng = np.random.default_rng(seed)
+    P = random_psd(n, rng, rank=n // 2)
+    M = rng.standard_normal((m, n)) / np.sqrt(n)
+    return dict(P=P, q=rng.standard_normal(n), M=M, lo=-np.ones(m), hi=np.ones(m))
+
+
+def build_problem(spec, ns):
+    """Problem of a case spec in the namespace ``ns`` (the reference package or
+    this repo's: both export the same constructors)."""
+    if "lasso_qp" in spec:
+        return ns.lasso_as_qp(*spec["lasso_qp"])
+    if "P" not in spec:
+        return ns.MLProblem(ns.builtin_loss(spec["loss"]), spec["A"], spec["b"], spec["lambda1"], spec["lambda2"])
+    import scipy.sparse as sp
+
+    def op(a, n):
+        if isinstance(a, dict) and "dplr" in a:
+            return ns.DiagPlusLowRank(*a["dplr"])
+        if isinstance(a, dict) and "diag" in a:
+            return ns.DiagonalOperator(a["diag"])
+        if isinstance(a, dict) and "stack" in a:
+            parts = [ns.OnesRowOperator(n) if t == "ones" else ns.IdentityOperator(n) for t in a["stack"]]
+            return ns.stack_vertical(parts)
+        if sp.issparse(a):
+            return ns.SparseOperator(a)
+        return ns.DenseOperator(a)
+
+    P = op(spec["P"], None)
+    n = P.input_dim
+    M = ns.IdentityOperator(n) if spec.get("M") is None else op(spec["M"], n)
+    return ns.QPProblem(P, spec["q"], M, ns.Box(spec["lo"], spec["hi"]))
+
+
+GENERAL_CASES = {
+    "sparse_lasso": (lambda: _sparse_ml("square", 300, 200, 51), dict(sketch_rank=10, rng_seed=51)),
+    "sparse_logistic": (lambda: _sparse_ml("logistic", 400, 150, 52, density=0.08, lam2=1e-3),
+                        dict(sketch_rank=10, rng_seed=52)),
+    "sparse_enet_rho": (lambda: _sparse_ml("square", 250, 120, 53, density=0.1, lam2=0.05),
+                        dict(sketch_rank=8, rng_seed=53, rho0=0.02, penalty_warmup=5, penalty_update_every=5)),
+    "lasso_as_qp": (lambda: _lasso_qp(), dict(sketch_rank=10, rng_seed=31, max_iter=3000)),
+    "lasso_as_qp_rho": (lambda: _lasso_qp(), dict(sketch_rank=10, rng_seed=31, max_iter=3000, rho0=10.0,
+                                                  penalty_warmup=5, penalty_update_every=5)),
+    "portfolio_ops": (lambda: _portfolio("operators"), dict(rng_seed=5, max_iter=3000)),
+    "portfolio_qp": (lambda: _portfolio("qp"), dict(rng_seed=5, max_iter=3000)),
+    "qp_primal_infeas_M": (lambda: _qp_primal_infeasible(), dict(max_iter=4000, eps_inf=1e-4)),
+    "qp_check_rank": (lambda: _qp_check_rank(), dict(check_rank=True, max_iter=300, rng_seed=2)),
+    "qp_assume_rank": (lambda: _qp_check_rank(), dict(assume_full_rank=True, max_iter=300, rng_seed=2)),
+    "qp_dense_M": (lambda: _qp_dense_M(), dict(sketch_rank=8, rng_seed=41, max_iter=3000)),
+}
+
+
 # penalty adaptation from the first iterations (admm.py:677-698): rho0 far from
 # balance makes the balanced-residual rule fire every 5 iterations
 _PEN = dict(penalty_warmup=5, penalty_update_every=5)
@@ -129,6 +271,8 @@ SOLVE_CASES = {
     "cfg5_shard": (lambda: _cfg5_shard(0), dict(sketch_rank=300, rng_seed=4)),
 }
 
+ALL_CASES = {**SOLVE_CASES, **GENERAL_CASES}
+
 # tolerances of the configs: eps_abs = eps_rel = eps_dual_gap = 1e-4 (BASELINE.json)
 BASE_OPTIONS = dict(eps_abs=1e-4, eps_rel=1e-4, eps_dual_gap=1e-4)
 
@@ -140,7 +284,7 @@ def options_for(name):
     """Options of a case; a ``huber_stop`` entry stands for
     ``custom_stop=huber_subdiff_stop(tol)`` (see ``split_stop``)."""
     opts = dict(BASE_OPTIONS)
-    opts.update(SOLVE_CASES[name][1])
+    opts.update(ALL_CASES[name][1])
     return opts
 
 

@@ -45,16 +45,17 @@ import cases  # noqa: E402
 
 
 def ref_problem(spec):
-    if "P" in spec:
-        n = spec["P"].shape[0]
-        return QPProblem(DenseOperator(spec["P"]), spec["q"], IdentityOperator(n), Box(spec["lo"], spec["hi"]))
-    return MLProblem(builtin_loss(spec["loss"]), spec["A"], spec["b"], spec["lambda1"], spec["lambda2"])
+    return cases.build_problem(spec, nysopt)
 
 
 def make_inputs():
     """Inputs made by the reference's own generators (stored, not re-derived)."""
     from nysopt.bench import gen_huber_data
 
+    from nysopt.bench import gen_portfolio_data
+
+    d, F, mu, gamma = gen_portfolio_data(2, 5)  # n = 200 assets, k = 2 factors
+    np.savez_compressed(os.path.join(HERE, "input_portfolio.npz"), d=d, F=F, mu=mu, gamma=np.float64(gamma))
     for name, (n, seed) in (("huber_cycle_a", (100, 2)), ("huber_cycle_b", (60, 0))):
         A, b, lam1 = gen_huber_data(n, seed)  # tests/test_admm.py:577-589
         np.savez_compressed(os.path.join(HERE, f"input_{name}.npz"), loss=np.array("huber"), A=A, b=b,
@@ -62,7 +63,7 @@ def make_inputs():
 
 
 def run_solve(name):
-    spec = cases.SOLVE_CASES[name][0]()
+    spec = cases.ALL_CASES[name][0]()
     o, stop_tol = cases.split_stop(cases.options_for(name))
     if stop_tol is not None:
         o["custom_stop"] = nysopt.huber_subdiff_stop(stop_tol)
@@ -141,6 +142,33 @@ def run_kernels():
         os.path.join(HERE, "kernels_pcg.npz"),
         x_plain=x1, it_plain=np.int64(rep1.iterations), x_prec=x2, it_prec=np.int64(rep2.iterations),
     )
+    # spectrum probes and adaptive sizing (sketch.py:176-282)
+    from nysopt import adaptive_sketch, condition_bound, estimate_error_norm, estimate_extreme_eigs
+
+    out = {}
+    rng = np.random.default_rng(404)
+    Apsd = cases.random_psd(50, rng, decay=np.logspace(2, -2, 50))
+    hi, lo = estimate_extreme_eigs(DenseOperator(Apsd), iters=30, rng_seed=4)
+    out["eig_hi"], out["eig_lo"] = np.float64(hi), np.float64(lo)
+    hi2, lo2 = estimate_extreme_eigs(DenseOperator(np.eye(10)), iters=10, rng_seed=0)  # breakdown
+    out["eye_hi"], out["eye_lo"] = np.float64(hi2), np.float64(lo2)
+    S = nystrom_sketch(DenseOperator(Apsd), 6, rng_seed=8)
+    out["err6"] = np.float64(estimate_error_norm(DenseOperator(Apsd), S, 20, rng_seed=9))
+    out["cond6"] = np.float64(condition_bound(S, float(out["err6"]), 0.5))
+    for tgt in (10.0, 30.0, 100.0, 1e3, np.inf):
+        Sa = adaptive_sketch(DenseOperator(Apsd), r0=2, r_max=32, nu=0.5, kappa_target=tgt, rng_seed=3)
+        key = "inf" if not np.isfinite(tgt) else f"{tgt:g}"
+        out[f"adapt_rank_{key}"] = np.int64(Sa.rank)
+        out[f"adapt_lam_{key}"] = Sa.lambda_hat
+    out["A"] = Apsd
+    np.savez_compressed(os.path.join(HERE, "kernels_spectrum.npz"), **out)
+
+    # sparse operator applies (operators.py:121-135) on the ragged CSR data
+    d = cases._sparse_ml("square", 300, 200, 51)
+    A = nysopt.SparseOperator(d["A"])
+    v = np.random.default_rng(5).standard_normal(200)
+    t = np.random.default_rng(6).standard_normal(300)
+    np.savez_compressed(os.path.join(HERE, "kernels_sparse.npz"), v=v, t=t, Av=A.apply(v), Atv=A.apply_adjoint(t))
     print("kernel fixtures written", flush=True)
 
 
@@ -149,7 +177,8 @@ def main():
     ap.add_argument("--big", action="store_true", help="also run config 4 (~10 min)")
     ap.add_argument("--only", nargs="*", default=None)
     args = ap.parse_args()
-    names = args.only if args.only else list(cases.DEFAULT_SOLVES) + (["cfg4"] if args.big else [])
+    names = args.only if args.only else (list(cases.DEFAULT_SOLVES) + list(cases.GENERAL_CASES)
+                                         + (["cfg4"] if args.big else []))
     make_inputs()
     if not args.only:
         run_kernels()

@@ -21,11 +21,7 @@ FAST = [k for k in cases.SOLVE_CASES if not k.startswith("cfg")]
 def gpu_problem(spec):
     import paper_2310_08333_b200 as nys
 
-    if "P" in spec:
-        n = spec["P"].shape[0]
-        return nys.QPProblem(nys.DenseOperator(spec["P"]), spec["q"], nys.IdentityOperator(n),
-                             nys.Box(spec["lo"], spec["hi"]))
-    return nys.MLProblem(nys.builtin_loss(spec["loss"]), spec["A"], spec["b"], spec["lambda1"], spec["lambda2"])
+    return cases.build_problem(spec, nys)
 
 
 def rel(a, b):
@@ -45,7 +41,7 @@ def check_case(name, strict_hist=True):
     import paper_2310_08333_b200 as nys
 
     gold = load_golden(f"solve_{name}.npz")
-    spec = cases.SOLVE_CASES[name][0]()
+    spec = cases.ALL_CASES[name][0]()
     opts = gpu_options(name)
     res = nys.solve(gpu_problem(spec), opts)
     it_ref = int(gold["iterations"])
@@ -156,12 +152,46 @@ def test_callback_and_history():
     assert seen[-1][0] == res.iterations
 
 
-def test_unsupported_problem_raises():
+@pytest.mark.parametrize("name", list(cases.GENERAL_CASES))
+def test_solve_general_cases(name):
+    """Sparse data, structured P, general constraint maps (the general-operator
+    engine) against the reference's own outputs."""
+    res, _ = check_case(name)
+    assert res.device_stats.get("engine") == "general"
+
+
+def test_check_rank_probe_matches_assertion():
+    """check_rank certifies the PD composite: the same trajectory as the
+    explicit full-rank assertion (test_admm.py:605-615)."""
+    import paper_2310_08333_b200 as nys
+
+    spec = cases.ALL_CASES["qp_check_rank"][0]()
+    r_probe = nys.solve(gpu_problem(spec), gpu_options("qp_check_rank"))
+    r_assert = nys.solve(gpu_problem(spec), gpu_options("qp_assume_rank"))
+    assert np.array_equal(r_assert.x, r_probe.x)
+    assert [h.rp_norm for h in r_assert.history] == [h.rp_norm for h in r_probe.history]
+
+
+def test_sparse_matches_dense():
+    """The same lasso with CSR and dense data (test_admm.py:591-602)."""
     import paper_2310_08333_b200 as nys
     import scipy.sparse as sp
 
+    spec = cases.ALL_CASES["sparse_lasso"][0]()
+    A = spec["A"]
+    opts = nys.SolverOptions(**cases.options_for("sparse_lasso"))
+    r_d = nys.solve(nys.lasso_problem(A.toarray(), spec["b"], spec["lambda1"]), opts)
+    r_s = nys.solve(nys.lasso_problem(sp.csr_matrix(A), spec["b"], spec["lambda1"]), opts)
+    assert r_d.status == r_s.status == nys.Status.OPTIMAL
+    assert np.allclose(r_d.z, r_s.z, atol=1e-10)
+
+
+def test_unsupported_problem_raises():
+    import paper_2310_08333_b200 as nys
+
+    gp = nys.GenericProblem(n=3, m=3, M=nys.IdentityOperator(3), c=np.zeros(3))
     with pytest.raises(nys.CapabilityError):
-        nys.solve(nys.lasso_problem(sp.eye(5).tocsr(), np.ones(5), 0.1))
+        nys.solve(gp)
 
 
 @pytest.mark.slow

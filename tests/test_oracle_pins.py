@@ -14,12 +14,35 @@ import cases
 
 from oracle import port
 
-FAST = [k for k in cases.SOLVE_CASES if not k.startswith("cfg")] + ["cfg1"]
+FAST = [k for k in cases.SOLVE_CASES if not k.startswith("cfg")] + ["cfg1"] + list(cases.GENERAL_CASES)
 
 
 def oracle_problem(spec):
+    if "lasso_qp" in spec:  # problems.py:484-502 in the port's own types
+        import scipy.sparse as sp
+
+        A, b, lam = spec["lasso_qp"]
+        n = A.shape[1]
+        P = sp.bmat([[sp.csr_matrix(A.T @ A), None], [None, sp.csr_matrix((n, n))]]).tocsr()
+        q = np.concatenate([-A.T @ b, lam * np.ones(n)])
+        eye = sp.eye(n)
+        M = sp.bmat([[eye, eye], [eye, -eye]]).tocsr()
+        lo = np.concatenate([np.zeros(n), np.full(n, -np.inf)])
+        hi = np.concatenate([np.full(n, np.inf), np.zeros(n)])
+        return port.QPSpec(P, q, lo, hi, M)
     if "P" in spec:
-        return port.QPSpec(spec["P"], spec["q"], spec["lo"], spec["hi"])
+        def op(a, n):
+            if isinstance(a, dict) and "dplr" in a:
+                return port.DiagLowRank(*a["dplr"])
+            if isinstance(a, dict) and "diag" in a:
+                return port.DiagLowRank(a["diag"], np.zeros((a["diag"].size, 0)))
+            if isinstance(a, dict) and "stack" in a:
+                return port.StackOp([port.OnesRow(n) if t == "ones" else np.eye(n) for t in a["stack"]])
+            return a
+
+        P = op(spec["P"], None)
+        M = spec.get("M")
+        return port.QPSpec(P, spec["q"], spec["lo"], spec["hi"], None if M is None else op(M, P.shape[0]))
     return port.MLSpec(spec["loss"], spec["A"], spec["b"], spec["lambda1"], spec["lambda2"])
 
 
@@ -33,7 +56,7 @@ def oracle_options(name):
 @pytest.mark.parametrize("name", FAST)
 def test_oracle_matches_reference_solve(name):
     gold = load_golden(f"solve_{name}.npz")
-    spec = cases.SOLVE_CASES[name][0]()
+    spec = cases.ALL_CASES[name][0]()
     res = port.solve(oracle_problem(spec), oracle_options(name))
     assert res.status == str(gold["status"])
     assert res.iterations == int(gold["iterations"])
@@ -110,3 +133,30 @@ def test_oracle_known_answers():
     np.testing.assert_allclose(port.soft_threshold(np.array([3.0, -0.5, 1.0, -2.0]), 1.0), [2.0, 0.0, 0.0, -1.0])
     with pytest.raises(port.OracleDataError):
         port.nystrom_sketch(port.dense_operator_columns(np.diag([1.0, -1.0, 0.5])), 3, 3, 0)
+
+
+def test_oracle_spectrum_probes_match_reference():
+    """Lanczos extreme eigenvalues, power-method error norm and the adaptive
+    rank schedule (sketch.py:176-282)."""
+    gold = load_golden("kernels_spectrum.npz")
+    A = gold["A"]
+    n = A.shape[0]
+    hi, lo = port.estimate_extreme_eigs(lambda v: A @ v, n, 30, 4)
+    assert hi == pytest.approx(float(gold["eig_hi"]), rel=1e-12)
+    assert lo == pytest.approx(float(gold["eig_lo"]), rel=1e-9)
+    hi2, lo2 = port.estimate_extreme_eigs(lambda v: v.copy(), 10, 10, 0)
+    assert (hi2, lo2) == pytest.approx((float(gold["eye_hi"]), float(gold["eye_lo"])), rel=1e-14)
+    U, lam = port.nystrom_sketch(port.dense_operator_columns(A), n, 6, 8)
+    err = port.estimate_error_norm(lambda v: A @ v, U, lam, n, 20, 9)
+    assert err == pytest.approx(float(gold["err6"]), rel=1e-12)
+    for key, tgt in (("10", 10.0), ("30", 30.0), ("100", 100.0), ("1000", 1e3), ("inf", np.inf)):
+        U, lam = port.adaptive_sketch(lambda v: A @ v, n, 2, 32, 0.5, tgt, 3)
+        assert lam.size == int(gold[f"adapt_rank_{key}"])
+        np.testing.assert_allclose(lam, gold[f"adapt_lam_{key}"], rtol=1e-12)
+
+
+def test_oracle_sparse_apply_matches_reference():
+    gold = load_golden("kernels_sparse.npz")
+    A = cases._sparse_ml("square", 300, 200, 51)["A"]
+    np.testing.assert_allclose(A @ gold["v"], gold["Av"], rtol=1e-14, atol=1e-14)
+    np.testing.assert_allclose(A.T @ gold["t"], gold["Atv"], rtol=1e-14, atol=1e-14)
