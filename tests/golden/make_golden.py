@@ -172,6 +172,34 @@ def run_kernels():
     print("kernel fixtures written", flush=True)
 
 
+def run_bench_goldens():
+    """The reference's benchmark generators and runner (bench/datagen.py,
+    bench/runner.py): generator outputs and run records of small configs."""
+    from nysopt.bench import (BenchConfig, gen_bounded_ls, gen_huber_data, gen_logistic_data, gen_portfolio_data,
+                              gen_regression_data, run_bench)
+
+    out = {}
+    out["reg_A"], out["reg_b"] = gen_regression_data(20, 10, 1)
+    out["hub_A"], out["hub_b"], lam = gen_huber_data(20, 3)
+    out["hub_lam"] = np.float64(lam)
+    out["pf_d"], out["pf_F"], out["pf_mu"], g = gen_portfolio_data(1, 2)
+    out["log_A"], lam = gen_logistic_data(20, 10, 4)
+    out["log_lam"] = np.float64(lam)
+    qp = gen_bounded_ls(20, 5)
+    out["bls_P"], out["bls_q"] = qp.P.a, qp.q
+    runs = [("lasso", dict(n=60)), ("elastic_net", dict(n=50)), ("logistic", dict(n=40)), ("huber", dict(n=60)),
+            ("bounded_ls", dict(n=80)), ("portfolio", dict(k=1, portfolio_path="qp")),
+            ("portfolio", dict(k=1, portfolio_path="operators")), ("lasso", dict(n=40, norm="linf", tol=1e-6))]
+    for i, (prob, kw) in enumerate(runs):
+        rec = run_bench(BenchConfig(problem=prob, seed=3, **kw))
+        out[f"run{i}_status"] = np.array(rec.status)
+        out[f"run{i}_iters"] = np.int64(rec.iters)
+        out[f"run{i}_objective"] = np.float64(rec.objective)
+        out[f"run{i}_n"] = np.int64(rec.n)
+        print(f"bench run {prob} {kw}: {rec.status} {rec.iters} {rec.objective:.10e}", flush=True)
+    np.savez_compressed(os.path.join(HERE, "bench_runs.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run config 4 (~10 min)")
@@ -182,6 +210,7 @@ def main():
     make_inputs()
     if not args.only:
         run_kernels()
+        run_bench_goldens()
     for name in names:
         run_solve(name)
 
