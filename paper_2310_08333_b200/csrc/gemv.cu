@@ -16,6 +16,7 @@
 //   * grids are sized in multiples of the 148 SMs.
 #include <stdlib.h>
 #include "common.cuh"
+#include "hvp_plan.cuh"
 
 namespace nys {
 
@@ -549,14 +550,7 @@ struct StripPlan {
   bool ok;
 };
 size_t hvp_strip_ws();
-struct HcPlan {
-  int W, K, S, L, nclusters;
-  size_t smem;
-  bool ok;
-};
-HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
-int hvp_cluster(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
-                const double* v, double* ypart, cudaStream_t st, const double* pred);
+
 StripPlan hvp_strip_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v);
 int hvp_strip(const StripPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
               const double* v, double* y, double shift, double* dot, void* ws, double* part,

@@ -21,9 +21,11 @@
 // cluster writes its y partial; a fixed-order reduction over the clusters adds
 // shift v and p.Ap (gemv.cu: gemv_t_reduce).
 #include <cooperative_groups.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include "common.cuh"
 #include "tma.cuh"
+#include "hvp_plan.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -186,11 +188,252 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
   cl.sync();  // no CTA leaves while a peer may still write into its shared memory
 }
 
-struct HcPlan {
-  int W, K, S, L, nclusters;
-  size_t smem;
-  bool ok;
-};
+// Wide rows whose per-CTA segment (W = n / 16 columns) cannot be staged whole
+// with v and y in registers (n = 200000: 100 KB of a row per CTA, the per-GPU
+// shape of config 5).  The segment is split into Q sub-segments of Wq columns;
+// y stays in registers, v moves to TENSOR MEMORY (tcgen05.st once, one
+// tcgen05.ld of 16 words per sub-segment and row: TMEM has its own datapath,
+// so v costs neither registers nor shared memory), and the freed shared memory
+// becomes a deep ring of sub-segment stages.  Per row the producer streams the
+// Q sub-segments once for the dot (HBM) and, after the cluster exchange of the
+// row total (one row later), once more for the axpy y += t a -- the second read
+// hits L2 (the row was read microseconds earlier), so HBM still sees A exactly
+// once.  Stage uses, in the order both the producer and the compute warps walk
+// them:
+//     for it: [dot(it, 0..Q-1) if it < nr] [axpy(it - L, 0..Q-1) if it >= L]
+// Named barriers: 1..S stage free (compute arrive, producer sync), 9..12 row
+// partials written (compute arrive, relay sync; 4 row slots, so an id is reused
+// only after its relay has synced, which the stream order guarantees for L = 1).
+constexpr int kHqNR = 4;    // row slots of the warp partials
+constexpr int kHqMaxS = 8;  // stage barriers 1..8, row barriers 9..12
+constexpr int kHqTmemCols = 256;
+// 14 compute warps + producer + relay = 16 warps: 4 per SM sub-partition, so
+// each thread may use 128 registers (18 warps would cap it at 96 and spill)
+constexpr int kHqWarps = 14;
+constexpr int kHqX = 1;
+constexpr int kHqThreads = (kHqWarps + 1 + kHqX) * 32;
+constexpr int kHqBarThreads = (kHqWarps + 1) * 32;
+__device__ __forceinline__ void qbar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kHqBarThreads) : "memory");
+}
+__device__ __forceinline__ void qbar_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kHqBarThreads) : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const double2 (&x)[4]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(__double2loint(x[0].x)), "r"(__double2hiint(x[0].x)), "r"(__double2loint(x[0].y)),
+      "r"(__double2hiint(x[0].y)), "r"(__double2loint(x[1].x)), "r"(__double2hiint(x[1].x)),
+      "r"(__double2loint(x[1].y)), "r"(__double2hiint(x[1].y)), "r"(__double2loint(x[2].x)),
+      "r"(__double2hiint(x[2].x)), "r"(__double2loint(x[2].y)), "r"(__double2hiint(x[2].y)),
+      "r"(__double2loint(x[3].x)), "r"(__double2hiint(x[3].x)), "r"(__double2loint(x[3].y)),
+      "r"(__double2hiint(x[3].y))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, double2 (&x)[4]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+      "[%16];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    x[k].x = __hiloint2double((int)r[4 * k + 1], (int)r[4 * k + 0]);
+    x[k].y = __hiloint2double((int)r[4 * k + 3], (int)r[4 * k + 2]);
+  }
+}
+
+template <int Q, int KQ>
+__global__ void __launch_bounds__(kHqThreads, 1)
+hvp_cluster_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
+                     const double* __restrict__ d, const double* __restrict__ v, int W, int Wq, int S,
+                     double* __restrict__ ypart, const double* __restrict__ pred) {
+  static_assert(KQ <= 4 && Q * 4 * 4 <= kHqTmemCols / 4, "v slice of a thread: <= 64 TMEM columns");
+  constexpr int L = 1;
+  if (pred && *pred != 0.0) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);             // S x Wq
+  double* psl = ring + (size_t)S * Wq;                            // NR x 16 warp partials
+  double* tsl = psl + kHqNR * kHqWarps;                           // NT x 16 CTA partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * kHcC);  // S
+  uint64_t* totb = full + S;                                      // NT
+  uint32_t* tmem_base = reinterpret_cast<uint32_t*>(totb + kHcNT);
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int cluster_id = blockIdx.x / kHcC, nclusters = gridDim.x / kHcC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)rank * W;
+  const int w_here = (int)tmax<int64_t>(0, tmin<int64_t>((int64_t)W, n - c0));
+  const int64_t nrows_mine = rows > cluster_id ? (rows - cluster_id + nclusters - 1) / nclusters : 0;
+
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(&full[q], 1);
+    for (int q = 0; q < kHcNT; ++q) mbar_init(&totb[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < kHcNT; ++q) mbar_expect_tx(&totb[q], kHcC * 8u);
+  }
+  if (warp == 0) {  // TMEM for v: one warp allocates (and later frees) the columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base)),
+                 "n"(kHqTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cl.sync();  // barriers armed cluster-wide, TMEM address published
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // this warp's TMEM slice: lanes of its sub-partition, 64 columns per warp
+  const uint32_t tv = *tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * ((warp >> 2) & 3));
+
+  const int nr = (int)nrows_mine;
+  if (warp == kHqWarps) {
+    // ---------------------------------------------------------- producer --
+    const int64_t rstep = (int64_t)nclusters * lda;
+    int u = 0, slot = 0;
+    auto issue = [&](const double* seg_row) {
+#pragma unroll 1
+      for (int q = 0; q < Q; ++q, ++u) {
+        if (u >= S) qbar_sync(1 + slot);  // use u - S is done with this slot
+        const int wq = tmin(Wq, w_here - q * Wq);
+        if (lane == 0) {
+          if (wq > 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&full[slot], (unsigned)wq * 8u);
+            tma_load_1d(ring + (size_t)slot * Wq, seg_row + (int64_t)q * Wq, (unsigned)wq * 8u, &full[slot]);
+          } else {
+            mbar_arrive(&full[slot]);  // empty sub-segment: complete the phase anyway
+          }
+        }
+        if (++slot == S) slot = 0;
+      }
+    };
+    const double* base = A + (int64_t)cluster_id * lda + c0;
+    for (int it = 0; it < nr + L; ++it) {
+      if (it < nr) issue(base + (int64_t)it * rstep);
+      if (it >= L) issue(base + (int64_t)(it - L) * rstep);  // the axpy re-read (L2)
+    }
+    for (int w = tmax(0, u - S); w < u; ++w) qbar_sync(1 + w % S);
+  } else if (warp > kHqWarps) {
+    // --------------------------------------------------- exchange (relay) --
+    const int xr = warp - kHqWarps - 1;
+    for (int g = xr; g < nr; g += kHqX) {
+      const int64_t i = cluster_id + (int64_t)g * nclusters;
+      const double di = d ? __ldg(d + i) : 1.0;
+      const int rs = g % kHqNR;
+      qbar_sync(1 + kHqMaxS + rs);
+      double p = lane < kHqWarps ? psl[rs * kHqWarps + lane] : 0.0;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      p *= di;
+      const int s = g & (kHcNT - 1);
+      if (lane < kHcC) st_async_remote_f64(tsl + s * kHcC + rank, &totb[s], (unsigned)lane, p);
+    }
+  } else {
+    // ---------------------------------------------------------- compute --
+    // v -> TMEM: sub-segment q of this thread at columns 16 q .. 16 q + 15
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double2 x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = 2 * (tid + k * kHqWarps * 32);
+        const int wq = tmin(Wq, w_here - q * Wq);
+        x[k] = (k < KQ && j < wq) ? *reinterpret_cast<const double2*>(v + c0 + (int64_t)q * Wq + j)
+                                  : make_double2(0.0, 0.0);
+      }
+      tmem_st16(tv + 16 * q, x);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    double2 yr[Q][KQ];
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) yr[q][k] = make_double2(0.0, 0.0);
+    int slot = 0, ph = 0;
+    auto next = [&]() {
+      if (++slot == S) {
+        slot = 0;
+        ph ^= 1;
+      }
+    };
+    for (int it = 0; it < nr + L; ++it) {
+      if (it < nr) {
+        double pt = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int wq = tmin(Wq, w_here - q * Wq);
+          double2 x[4];
+          tmem_ld16(tv + 16 * q, x);
+          mbar_wait(&full[slot], (unsigned)ph);
+          const double* seg = ring + (size_t)slot * Wq;
+#pragma unroll
+          for (int k = 0; k < KQ; ++k) {
+            const int j = 2 * (tid + k * kHqWarps * 32);
+            if (j < wq) {
+              const double2 a = *reinterpret_cast<const double2*>(seg + j);
+              pt = fma(a.x, x[k].x, pt);
+              pt = fma(a.y, x[k].y, pt);
+            }
+          }
+          __syncwarp();
+          qbar_arrive(1 + slot);
+          next();
+        }
+        pt = warp_sum(pt);
+        const int rs = it % kHqNR;
+        if (lane == 0) psl[rs * kHqWarps + warp] = pt;
+        __syncwarp();
+        qbar_arrive(1 + kHqMaxS + rs);
+      }
+      const int jt = it - L;
+      if (jt < 0) continue;
+      const int s = jt & (kHcNT - 1);
+      mbar_wait_cluster(&totb[s], (unsigned)((jt / kHcNT) & 1));
+      double t = 0.0;
+#pragma unroll
+      for (int q2 = 0; q2 < kHcC; ++q2) t += tsl[s * kHcC + q2];
+      if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kHcC * 8u);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int wq = tmin(Wq, w_here - q * Wq);
+        mbar_wait(&full[slot], (unsigned)ph);
+        const double* seg = ring + (size_t)slot * Wq;
+#pragma unroll
+        for (int k = 0; k < KQ; ++k) {
+          const int j = 2 * (tid + k * kHqWarps * 32);
+          if (j < wq) {
+            const double2 a = *reinterpret_cast<const double2*>(seg + j);
+            yr[q][k].x = fma(t, a.x, yr[q][k].x);
+            yr[q][k].y = fma(t, a.y, yr[q][k].y);
+          }
+        }
+        __syncwarp();
+        qbar_arrive(1 + slot);
+        next();
+      }
+    }
+    double* yp = ypart + (int64_t)cluster_id * n + c0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) {
+        const int j = 2 * (tid + k * kHqWarps * 32);
+        if (j < tmin(Wq, w_here - q * Wq)) *reinterpret_cast<double2*>(yp + q * Wq + j) = yr[q][k];
+      }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cl.sync();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base), "n"(kHqTmemCols)
+                 : "memory");
+  }
+}
 
 HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v) {
   HcPlan p{};
@@ -199,10 +442,39 @@ HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, c
   if (off || (lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)v & 15) || rows < 1) return p;
   p.W = (int)cdiv(cdiv(n, kHcC), 2) * 2;
   p.K = (int)cdiv(p.W / 2, kHcWarps * 32);
-  if (p.K > 12) return p;
+  p.Q = 1;
+  p.Wq = p.W;
   const size_t fixed = (size_t)(kHcNT * kHcC) * 8 + kHcNT * 8 + 1024;
   const size_t row_bytes = (size_t)p.W * 8;
-  p.S = (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / (row_bytes + kHcWarps * 8 + 24)));
+  p.S = p.K > 12 ? 0
+                 : (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / (row_bytes + kHcWarps * 8 + 24)));
+  static const bool no_q = getenv("NYS_HVP_CLUSTER_NOQ") != nullptr;
+  static const bool force_q = getenv("NYS_HVP_CLUSTER_Q") != nullptr;
+  if ((p.S < 3 || force_q) && !no_q) {
+    // sub-segment plan: the smallest split with >= 4 stages in flight and the
+    // y segment (Q x KQ double2 per thread) in registers
+    const size_t qfixed = fixed + (size_t)kHqNR * kHqWarps * 8 + 16;
+    static const int forced_q = getenv("NYS_HVP_CLUSTER_Q") ? atoi(getenv("NYS_HVP_CLUSTER_Q")) : 0;
+    for (int Q = 2; Q <= 4; ++Q) {
+      if (forced_q > 1 && Q != forced_q) continue;
+      const int Wq = (int)cdiv(cdiv(p.W, Q), 2) * 2;
+      const int KQ = (int)cdiv(Wq / 2, kHqWarps * 32);
+      if (KQ > 4) continue;
+      const int S = (int)tmin<int64_t>(kHqMaxS, (int64_t)((kHcSmemBudget - qfixed) / ((size_t)Wq * 8 + 8)));
+      if (S < 4) continue;
+      p.Q = Q;
+      p.Wq = Wq;
+      p.K = KQ;
+      p.S = S;
+      p.L = 1;
+      p.smem = (size_t)S * Wq * 8 + (size_t)kHqNR * kHqWarps * 8 + (size_t)kHcNT * kHcC * 8 +
+               (size_t)(S + kHcNT) * 8 + 16;
+      p.nclusters = 0;
+      p.ok = true;
+      return p;
+    }
+    return p;
+  }
   if (p.S < 3) return p;
   static const int forced_lag = getenv("NYS_HVP_CLUSTER_LAG") ? atoi(getenv("NYS_HVP_CLUSTER_LAG")) : 0;
   // lag 1 measured best on B200 (n = 1e5, S = 4: 2.32 ms vs 2.80 ms at lag 2 -
@@ -216,10 +488,14 @@ HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, c
   return p;
 }
 
-template <int K>
+template <int K, int Q = 1>
 static int hvp_cluster_launch_k(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
                                 const double* v, double* ypart, cudaStream_t st, const double* pred) {
-  auto fn = hvp_cluster_kernel<K>;
+  const void* fn;
+  if constexpr (Q == 1)
+    fn = (const void*)hvp_cluster_kernel<K>;
+  else
+    fn = (const void*)hvp_cluster_q_kernel<Q, K>;
   static bool attr = false;
   static int maxc = 0;
   if (!attr) {
@@ -228,7 +504,7 @@ static int hvp_cluster_launch_k(HcPlan& p, const double* A, int64_t rows, int64_
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(kHcThreads, 1, 1);
+  cfg.blockDim = dim3(Q == 1 ? kHcThreads : kHqThreads, 1, 1);
   cfg.dynamicSmemBytes = p.smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -243,7 +519,11 @@ static int hvp_cluster_launch_k(HcPlan& p, const double* A, int64_t rows, int64_
     // double the tail), at most 148 / 16
     cfg.gridDim = dim3(kHcC * (kNumSMs / kHcC), 1, 1);
     int mc = 0;
-    if (cudaOccupancyMaxActiveClusters(&mc, (void*)fn, &cfg) != cudaSuccess || mc < 1) {
+    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&mc, (void*)fn, &cfg);
+    if (oe != cudaSuccess || mc < 1) {
+      if (getenv("NYS_HVP_DEBUG"))
+        fprintf(stderr, "hvp_cluster Q=%d K=%d: occupancy %s, %d clusters (smem %zu)\n", Q, K,
+                cudaGetErrorString(oe), mc, p.smem);
       cudaGetLastError();
       return NYS_ERR_UNSUPPORTED;
     }
@@ -251,8 +531,15 @@ static int hvp_cluster_launch_k(HcPlan& p, const double* A, int64_t rows, int64_
   }
   p.nclusters = (int)tmax<int64_t>(1, tmin<int64_t>(maxc, rows));
   cfg.gridDim = dim3(kHcC * p.nclusters, 1, 1);
-  int W = p.W, S = p.S, L = p.L;
-  if (cudaLaunchKernelEx(&cfg, fn, A, rows, n, lda, d, v, W, S, L, ypart, pred) != cudaSuccess) return NYS_ERR_CUDA;
+  int W = p.W, S = p.S, L = p.L, Wq = p.Wq;
+  cudaError_t e;
+  if constexpr (Q == 1)
+    e = cudaLaunchKernelEx(&cfg, hvp_cluster_kernel<K>, A, rows, n, lda, d, v, W, S, L, ypart, pred);
+  else
+    e = cudaLaunchKernelEx(&cfg, hvp_cluster_q_kernel<Q, K>, A, rows, n, lda, d, v, W, Wq, S, ypart, pred);
+  (void)L;
+  (void)Wq;
+  if (e != cudaSuccess) return NYS_ERR_CUDA;
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
   return debug_sync_check(__FILE__, __LINE__) ? NYS_ERR_CUDA : NYS_OK;
 }
@@ -260,6 +547,16 @@ static int hvp_cluster_launch_k(HcPlan& p, const double* A, int64_t rows, int64_
 // ypart: (plan.nclusters <= 9) x n partials; returns the cluster count used in *ncl
 int hvp_cluster(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* d,
                 const double* v, double* ypart, cudaStream_t st, const double* pred) {
+  if (p.Q > 1) {
+    switch (p.Q * 8 + p.K) {
+#define NYS_QK(q, k) \
+  case q * 8 + k: return hvp_cluster_launch_k<k, q>(p, A, rows, n, lda, d, v, ypart, st, pred);
+      NYS_QK(2, 1) NYS_QK(2, 2) NYS_QK(2, 3) NYS_QK(2, 4) NYS_QK(3, 1) NYS_QK(3, 2) NYS_QK(3, 3) NYS_QK(3, 4)
+      NYS_QK(4, 1) NYS_QK(4, 2) NYS_QK(4, 3) NYS_QK(4, 4)
+#undef NYS_QK
+      default: return NYS_ERR_UNSUPPORTED;
+    }
+  }
   switch (p.K) {
 #define NYS_K(k) \
   case k: return hvp_cluster_launch_k<k>(p, A, rows, n, lda, d, v, ypart, st, pred);

@@ -67,7 +67,9 @@ def test_gemv_odd_leading_dim(kx):
 
 @pytest.mark.parametrize("rows,n", [(70, 45), (1000, 2000), (5000, 3000), (33, 7),
                                     # wide rows: column-strip kernel (csrc/hvp_strip.cu)
-                                    (7, 20000), (301, 100000), (1001, 30002), (50, 250000), (2, 12802)])
+                                    (7, 20000), (301, 100000), (1001, 30002), (50, 250000), (2, 12802),
+                                    # sub-segment cluster plan (L2 re-read for the axpy): config 5's width
+                                    (37, 200000), (301, 150000), (3, 199998)])
 def test_hvp_fused(kx, rows, n):
     g = np.random.default_rng(n)
     A = g.standard_normal((rows, n))
