@@ -250,6 +250,8 @@ SOLVE_CASES = {
     "lasso_linf": (lambda: _ml_small("square", 120, 200, 18), dict(sketch_rank=10, rng_seed=18, norm_kind="linf", use_dual_gap=False)),
     "lasso_exact": (lambda: _ml_small("square", 100, 150, 19), dict(sketch_rank=10, rng_seed=19, exact_x_solve=True)),
     "boxqp_small": (lambda: _qp_small(400, 200, 20), dict(sketch_rank=20, rng_seed=20)),
+    # wide rows (n > 12800: the cluster HVP), also solved row-sharded (tests/test_gpu_sharded.py)
+    "lasso_wide": (lambda: _ml_small("square", 400, 20000, 61), dict(sketch_rank=20, rng_seed=61)),
     # --- adaptive control flow: penalty changes, cycle guard, certificates, time limit
     "lasso_rho_hi": (lambda: _ml_small("square", 120, 200, 11), dict(sketch_rank=10, rng_seed=11, rho0=100.0, **_PEN)),
     "lasso_rho_lo": (lambda: _ml_small("square", 120, 200, 11), dict(sketch_rank=10, rng_seed=11, rho0=0.01, **_PEN)),

@@ -81,7 +81,8 @@ def _worker(rank, world, port, name, out_path, pipelined=True):
 
 
 @pytest.mark.parametrize("name,pipelined", [("lasso_small", True), ("logistic_small", True), ("enet_small", True),
-                                           ("cfg2_small", True), ("cfg4_small", True), ("cfg2_small", False)])
+                                           ("cfg2_small", True), ("cfg4_small", True), ("cfg2_small", False),
+                                           ("lasso_wide", True), ("lasso_wide", False)])
 def test_gpu_row_sharded_solve_matches_single(tmp_path, name, pipelined):
     """pipelined: the one-round-trip-per-iteration schedule with the all-reduce
     hook inside the C drivers (default); else the per-step schedule."""
@@ -103,3 +104,11 @@ def test_gpu_row_sharded_solve_matches_single(tmp_path, name, pipelined):
     assert abs(float(r0["obj"]) - ref.objective) <= 1e-6 * abs(ref.objective)
     assert np.linalg.norm(r0["x"] - ref.x) <= 1e-5 * max(np.linalg.norm(ref.x), 1e-30)
     assert np.linalg.norm(r0["z"] - ref.z) <= 1e-5 * max(np.linalg.norm(ref.z), 1e-30)
+
+    # cases with a reference fixture: the sharded solve against the reference itself
+    gpath = os.path.join(HERE, "golden", f"solve_{name}.npz")
+    if os.path.exists(gpath):
+        gold = np.load(gpath)
+        assert abs(int(r0["it"]) - int(gold["iterations"])) <= 2
+        assert abs(float(r0["obj"]) - float(gold["objective"])) <= 1e-6 * abs(float(gold["objective"]))
+        assert np.linalg.norm(r0["x"] - gold["x"]) <= 1e-5 * max(np.linalg.norm(gold["x"]), 1e-30)
