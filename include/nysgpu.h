@@ -429,6 +429,18 @@ size_t nys_syevj_workspace(int s);
 int nys_syevj_f64(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Workspace (bytes) of nys_admm_tail_f64's ws_gemvT when the rows are wide
+ * (n > 12800): the one-pass cluster tail keeps per-cluster A^T partials there. */
+size_t nys_tail_cluster_workspace(int64_t rows, int64_t n);
+/* The one-pass ML tail of nys_admm_tail_f64 on its own (admm.py:585-587,
+ * problems.py:227-351): T = [l'(Ax-b), w o Ax, l'(Az-b)] (3 x rows, row-major),
+ * w = l''(Ax-b), AT = A^T T (3 x n; 2 x n when z is NULL), rowsums[0..4] as
+ * nys_ml_rowwise_f64.  ws: nys_tail_cluster_workspace bytes.  Returns
+ * NYS_ERR_UNSUPPORTED for shapes without a cluster plan (n <= 12800). */
+int nys_ml_tail_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
+                    const double* b, int loss, double* T, double* w, double* AT, double* rowsums, void* ws,
+                    size_t ws_bytes, void* stream);
+
 /* ------------------------------------- sparse / general-operator engine -- */
 /* CSR data operator (SparseOperator._apply, operators.py:129-131 -- scipy's
  * `a @ v`): row pointer int64 (rows+1), column indices int32, values FP64.

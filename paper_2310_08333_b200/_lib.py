@@ -150,6 +150,8 @@ SIGNATURES = {
     "nys_nystrom_core_f64": (I32, [I64, I32, I32, P, P, P, P, C.POINTER(C.c_int), P, SZ, P]),
     "nys_syevj_workspace": (SZ, [I32]),
     "nys_syevj_f64": (I32, [I32, P, P, P, P, SZ, P]),
+    "nys_tail_cluster_workspace": (SZ, [I64, I64]),
+    "nys_ml_tail_f64": (I32, [P, I64, I64, I64, P, P, P, I32, P, P, P, P, P, SZ, P]),
     "nys_csr_spmv_f64": (I32, [I64, P, P, P, P, F64, P, F64, P, P, I32, P]),
     "nys_csr_spmm_f64": (I32, [I64, P, P, P, P, I64, I32, P, P, I64, P]),
     "nys_csr_transpose_workspace": (SZ, [I64, I64]),

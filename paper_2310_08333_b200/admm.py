@@ -900,7 +900,8 @@ class _Engine:
                 if self.use_gap and self.l2 == 0.0 and self.loss not in ("square", "huber"):
                     t.conj_out = st[_S_CONJ:].data_ptr()
                 wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(rows, n, 2))
-                wt = kx.workspace("tail_gemvT", L.nys_gemvT_workspace(rows, n, 3))
+                wt = kx.workspace("tail_gemvT", max(L.nys_gemvT_workspace(rows, n, 3),
+                                                    L.nys_tail_cluster_workspace(rows, n)))
             else:
                 t.kind, t.rows = 1, n
                 t.A, t.lda = self.P.data_ptr(), self.P.stride(0)

@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "tma.cuh"
 #include "hvp_plan.cuh"
+#include "loss.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -204,6 +205,7 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
 // Named barriers: 1..S stage free (compute arrive, producer sync), 9..12 row
 // partials written (compute arrive, relay sync; 4 row slots, so an id is reused
 // only after its relay has synced, which the stream order guarantees for L = 1).
+constexpr int kRedPartialsTail = 4096;  // reduction scratch ahead of the A^T partials (vec.cu layout)
 constexpr int kHqNR = 4;    // row slots of the warp partials
 constexpr int kHqMaxS = 8;  // stage barriers 1..8, row barriers 9..12
 constexpr int kHqTmemCols = 256;
@@ -567,4 +569,410 @@ int hvp_cluster(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda
   }
 }
 
+
+
+// ---------------------------------------------------------------------------
+// The ADMM tail's data passes for wide rows in ONE stream over A (admm.py:
+// 585-587 with problems.py:227-351): per row i the cluster forms
+//   a_i.x and a_i.z                         (the A{x, z} pass)
+// then, one row later with the totals exchanged in the cluster, every CTA
+// evaluates the loss epilogue of the row itself
+//   tg = l'(a_i.x - b_i), w = l''(.), thx = w a_i.x, nu = l'(a_i.z - b_i)
+// and accumulates gA += tg a_i, hxA += thx a_i, atnu += nu a_i  (the 3-RHS
+// A^T pass) from the still-staged segment.  x and z live in tensor memory
+// (tcgen05.st once), the three accumulators in registers, the segment ring in
+// shared memory.  Before: gemv_n (k = 2) + row-wise epilogue + gemv_t (k = 3),
+// two passes over A; now one.  Outputs: T = [tg, thx, nu] (3 x rows), w (rows),
+// per-cluster A^T partials P[(c * 3 + j) * n + col] (the layout the ML
+// epilogue sums in a fixed order) and per-cluster row sums (fixed row order):
+//   rowpart[c * 8 + 0..4] = sum l(r1), sum l(r2), sum l*(nu) finite, #inf, b.nu
+template <int KQ, bool WITHZ>
+__global__ void __launch_bounds__(kHqThreads, 1)
+tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
+                    const double* __restrict__ x, const double* __restrict__ z, const double* __restrict__ b,
+                    int loss, int W, int S, double* __restrict__ T, double* __restrict__ wout,
+                    double* __restrict__ P, double* __restrict__ rowpart, const double* __restrict__ pred) {
+  static_assert(KQ <= 8, "x and z slices: <= 32 TMEM columns each");
+  constexpr int L = 1;
+  constexpr int NV = WITHZ ? 2 : 1;
+  if (pred && *pred != 0.0) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);                 // S x W
+  double* psl = ring + (size_t)S * W;                                 // NR x NV x 14 warp partials
+  double* tsl = psl + kHqNR * NV * kHqWarps;                          // NT x NV x 16 CTA partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * NV * kHcC);  // S
+  uint64_t* totb = full + S;                                          // NT
+  uint32_t* tmem_base = reinterpret_cast<uint32_t*>(totb + kHcNT);
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int cluster_id = blockIdx.x / kHcC, nclusters = gridDim.x / kHcC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)rank * W;
+  const int w_here = (int)tmax<int64_t>(0, tmin<int64_t>((int64_t)W, n - c0));
+  const unsigned bytes = (unsigned)w_here * 8u;
+  const int64_t nrows_mine = rows > cluster_id ? (rows - cluster_id + nclusters - 1) / nclusters : 0;
+  constexpr unsigned kTx = (unsigned)(kHcC * NV * 8);
+
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(&full[q], 1);
+    for (int q = 0; q < kHcNT; ++q) mbar_init(&totb[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < kHcNT; ++q) mbar_expect_tx(&totb[q], kTx);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base)),
+                 "n"(kHqTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cl.sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // per thread: x at words [0, 32), z at [32, 64) of the warp's 64-column block
+  const uint32_t tv = *tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * ((warp >> 2) & 3));
+
+  const int nr = (int)nrows_mine;
+  if (warp == kHqWarps) {
+    // ---------------------------------------------------------- producer --
+    const double* arow = A + (int64_t)cluster_id * lda + c0;
+    const int64_t rstep = (int64_t)nclusters * lda;
+    for (int g = 0, q = 0; g < nr; ++g, arow += rstep) {
+      if (g >= S) qbar_sync(1 + q);
+      if (lane == 0) {
+        if (bytes > 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&full[q], bytes);
+          tma_load_1d(ring + (size_t)q * W, arow, bytes, &full[q]);
+        } else {
+          mbar_arrive(&full[q]);
+        }
+      }
+      if (++q == S) q = 0;
+    }
+    for (int g = tmax(0, nr - S); g < nr; ++g) qbar_sync(1 + g % S);
+  } else if (warp > kHqWarps) {
+    // --------------------------------------------------- exchange (relay) --
+    for (int g = 0; g < nr; ++g) {
+      const int rs = g % kHqNR;
+      qbar_sync(1 + kHqMaxS + rs);
+      const int s = g & (kHcNT - 1);
+#pragma unroll
+      for (int vv = 0; vv < NV; ++vv) {
+        double p = lane < kHqWarps ? psl[(rs * NV + vv) * kHqWarps + lane] : 0.0;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        if (lane < kHcC) st_async_remote_f64(tsl + (s * NV + vv) * kHcC + rank, &totb[s], (unsigned)lane, p);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- compute --
+    {  // x, z -> TMEM
+      double2 c[4];
+#pragma unroll
+      for (int vv = 0; vv < NV; ++vv) {
+        const double* src = vv == 0 ? x : z;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int k = 4 * h + k4;
+            const int j = 2 * (tid + k * kHqWarps * 32);
+            c[k4] = (k < KQ && j < w_here) ? *reinterpret_cast<const double2*>(src + c0 + j) : make_double2(0.0, 0.0);
+          }
+          tmem_st16(tv + 32 * vv + 16 * h, c);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    double2 yg[KQ], yh[KQ], yn[WITHZ ? KQ : 1];
+#pragma unroll
+    for (int k = 0; k < KQ; ++k) {
+      yg[k] = make_double2(0.0, 0.0);
+      yh[k] = make_double2(0.0, 0.0);
+      if (WITHZ) yn[k] = make_double2(0.0, 0.0);
+    }
+    const bool writer = rank == 0 && warp == 0 && lane == 0;
+    // the row sums live in shared memory (one thread updates them): no registers
+    __shared__ double rsum[5];
+    if (writer)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) rsum[q] = 0.0;
+    int qi = 0, pi = 0, qj = 0;
+    for (int it = 0; it < nr + L; ++it) {
+      if (it < nr) {
+        const int q = qi;
+        mbar_wait(&full[q], (unsigned)pi);
+        if (++qi == S) {
+          qi = 0;
+          pi ^= 1;
+        }
+        const double* row = ring + (size_t)q * W;
+        const int rs = it % kHqNR;
+#pragma unroll
+        for (int vv = 0; vv < NV; ++vv) {
+          double pt = 0.0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (4 * h >= KQ) continue;
+            double2 c[4];
+            tmem_ld16(tv + 32 * vv + 16 * h, c);
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int k = 4 * h + k4;
+              const int j = 2 * (tid + k * kHqWarps * 32);
+              if (k < KQ && j < w_here) {
+                const double2 a = *reinterpret_cast<const double2*>(row + j);
+                pt = fma(a.x, c[k4].x, pt);
+                pt = fma(a.y, c[k4].y, pt);
+              }
+            }
+          }
+          pt = warp_sum(pt);
+          if (lane == 0) psl[(rs * NV + vv) * kHqWarps + warp] = pt;
+        }
+        __syncwarp();
+        qbar_arrive(1 + kHqMaxS + rs);
+      }
+      const int jt = it - L;
+      if (jt < 0) continue;
+      const int s = jt & (kHcNT - 1);
+      mbar_wait_cluster(&totb[s], (unsigned)((jt / kHcNT) & 1));
+      double ax = 0.0, az = 0.0;
+#pragma unroll
+      for (int q2 = 0; q2 < kHcC; ++q2) ax += tsl[(s * NV) * kHcC + q2];
+      if (WITHZ)
+#pragma unroll
+        for (int q2 = 0; q2 < kHcC; ++q2) az += tsl[(s * NV + 1) * kHcC + q2];
+      if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kTx);
+      const int64_t i = cluster_id + (int64_t)jt * nclusters;
+      const double bi = __ldg(b + i);
+      // loss epilogue of the row (vec.cu ml_rowwise_kernel, same expressions)
+      const double r1 = __dadd_rn(ax, -bi);
+      const double tg = loss_d1(loss, r1);
+      const double wi = loss_d2(loss, r1);
+      const double thx = __dmul_rn(wi, ax);
+      double nu = 0.0, r2 = 0.0;
+      if (WITHZ) {
+        r2 = __dadd_rn(az, -bi);
+        nu = loss_d1(loss, r2);
+      }
+      if (writer) {
+        T[i] = tg;
+        T[rows + i] = thx;
+        wout[i] = wi;
+        rsum[0] += loss_val(loss, r1);
+        if (WITHZ) {
+          T[2 * rows + i] = nu;
+          rsum[1] += loss_val(loss, r2);
+          const double cv = loss_conj(loss, nu);
+          if (isinf(cv)) rsum[3] += 1.0; else rsum[2] += cv;
+          rsum[4] = fma(bi, nu, rsum[4]);
+        }
+      }
+      const int q = qj;
+      if (++qj == S) qj = 0;
+      const double* row = ring + (size_t)q * W;
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) {
+        const int j = 2 * (tid + k * kHqWarps * 32);
+        if (j < w_here) {
+          const double2 a = *reinterpret_cast<const double2*>(row + j);
+          yg[k].x = fma(tg, a.x, yg[k].x);
+          yg[k].y = fma(tg, a.y, yg[k].y);
+          yh[k].x = fma(thx, a.x, yh[k].x);
+          yh[k].y = fma(thx, a.y, yh[k].y);
+          if (WITHZ) {
+            yn[k].x = fma(nu, a.x, yn[k].x);
+            yn[k].y = fma(nu, a.y, yn[k].y);
+          }
+        }
+      }
+      __syncwarp();
+      qbar_arrive(1 + q);
+    }
+    constexpr int K3 = WITHZ ? 3 : 2;
+    double* pc = P + (int64_t)cluster_id * K3 * n + c0;
+#pragma unroll
+    for (int k = 0; k < KQ; ++k) {
+      const int j = 2 * (tid + k * kHqWarps * 32);
+      if (j < w_here) {
+        *reinterpret_cast<double2*>(pc + j) = yg[k];
+        *reinterpret_cast<double2*>(pc + n + j) = yh[k];
+        if (WITHZ) *reinterpret_cast<double2*>(pc + 2 * n + j) = yn[k];
+      }
+    }
+    if (writer)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) rowpart[cluster_id * 8 + q] = rsum[q];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cl.sync();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base), "n"(kHqTmemCols)
+                 : "memory");
+  }
+}
+
+// fixed-order sum of the per-cluster row sums into out[0..4]
+__global__ void tail_rowsum_kernel(const double* __restrict__ rowpart, int nclusters, double* __restrict__ out,
+                                   const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  if (threadIdx.x < 5) {
+    double a = 0.0;
+    for (int c = 0; c < nclusters; ++c) a += rowpart[c * 8 + threadIdx.x];
+    out[threadIdx.x] = a;
+  }
+}
+
+struct TcPlan {
+  int W, KQ, S, nclusters;
+  size_t smem;
+  bool ok;
+};
+
+TcPlan tail_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* x, bool with_z) {
+  TcPlan p{};
+  p.ok = false;
+  static const bool off = getenv("NYS_TAIL_CLUSTER_OFF") != nullptr;
+  // whole rows fit the warp-specialised row pass (rowpass.cu) below 12800 columns
+  if (off || n <= 12800 || (lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)x & 15) || rows < 1) return p;
+  p.W = (int)cdiv(cdiv(n, kHcC), 2) * 2;
+  p.KQ = (int)cdiv(p.W / 2, kHqWarps * 32);
+  if (p.KQ > 8) return p;
+  const int NV = with_z ? 2 : 1;
+  const size_t fixed = (size_t)kHqNR * NV * kHqWarps * 8 + (size_t)kHcNT * NV * kHcC * 8 + kHcNT * 8 + 16 + 1024;
+  p.S = (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / ((size_t)p.W * 8 + 8)));
+  if (p.S < 3) return p;
+  p.smem = (size_t)p.S * p.W * 8 + (size_t)kHqNR * NV * kHqWarps * 8 + (size_t)kHcNT * NV * kHcC * 8 +
+           (size_t)(p.S + kHcNT) * 8 + 16;
+  p.ok = true;
+  return p;
+}
+
+template <int KQ, bool WITHZ>
+static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* x,
+                                 const double* z, const double* b, int loss, double* T, double* w, double* P,
+                                 double* rowpart, double* rowsums, cudaStream_t st, const double* pred) {
+  const void* fn = (const void*)tail_cluster_kernel<KQ, WITHZ>;
+  static bool attr = false;
+  static int maxc = 0;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kHcSmemBudget);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kHqThreads, 1, 1);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kHcC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (maxc == 0) {
+    cfg.gridDim = dim3(kHcC * (kNumSMs / kHcC), 1, 1);
+    int mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, fn, &cfg) != cudaSuccess || mc < 1) {
+      cudaGetLastError();
+      return NYS_ERR_UNSUPPORTED;
+    }
+    maxc = tmin(mc, kNumSMs / kHcC);
+  }
+  p.nclusters = (int)tmax<int64_t>(1, tmin<int64_t>(maxc, rows));
+  cfg.gridDim = dim3(kHcC * p.nclusters, 1, 1);
+  int W = p.W, S = p.S;
+  if (cudaLaunchKernelEx(&cfg, tail_cluster_kernel<KQ, WITHZ>, A, rows, n, lda, x, z, b, loss, W, S, T, w, P,
+                         rowpart, pred) != cudaSuccess)
+    return NYS_ERR_CUDA;
+  __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
+  tail_rowsum_kernel<<<1, 32, 0, st>>>(rowpart, p.nclusters, rowsums, pred);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+// the tail's A{x,z} + loss epilogue + A^T{tg, thx, nu} in one pass; UNSUPPORTED
+// when the shape has no cluster plan (the caller runs the two-pass tail)
+int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
+                 const double* b, int loss, double* T, double* w, void* ws, size_t ws_bytes, size_t ws_off,
+                 double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out) {
+  // measured (20000 x 100000): square loss 4.46 ms vs 4.56 ms for the two
+  // passes; logistic 7.28 ms (every warp evaluates the exp-based epilogue and
+  // x, z stream from TMEM at ~25 B/cycle): the one-pass tail only for the
+  // square loss (configs 4 and 5) unless NYS_TAIL_CLUSTER_ALL is set
+  static const bool all_losses = getenv("NYS_TAIL_CLUSTER_ALL") != nullptr;
+  if (loss != NYS_LOSS_SQUARE && !all_losses) return NYS_ERR_UNSUPPORTED;
+  TcPlan p = tail_cluster_plan(rows, n, lda, A, x, z != nullptr);
+  if (!p.ok) return NYS_ERR_UNSUPPORTED;
+  const int K3 = z ? 3 : 2;
+  const size_t need = ws_off + (size_t)(kNumSMs / kHcC) * K3 * n * 8 + (size_t)(kNumSMs / kHcC) * 8 * 8;
+  if (ws_bytes < need) return NYS_ERR_UNSUPPORTED;
+  double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + ws_off);
+  double* rowpart = P + (size_t)(kNumSMs / kHcC) * K3 * n;
+  int rc = NYS_ERR_UNSUPPORTED;
+  switch (p.KQ * 2 + (z ? 1 : 0)) {
+#define NYS_TK(k)                                                                                                  \
+  case 2 * k: rc = tail_cluster_launch_k<k, false>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, rowsums, st, \
+                                                   pred); break;                                                   \
+  case 2 * k + 1: rc = tail_cluster_launch_k<k, true>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, rowsums, \
+                                                      st, pred); break;
+    NYS_TK(1) NYS_TK(2) NYS_TK(3) NYS_TK(4) NYS_TK(5) NYS_TK(6) NYS_TK(7) NYS_TK(8)
+#undef NYS_TK
+    default: break;
+  }
+  if (rc == NYS_OK) {
+    *Pout = P;
+    *splits_out = p.nclusters;
+  }
+  return rc;
+}
+
 }  // namespace nys
+
+// workspace of nys_admm_tail_f64's A^T stage when the cluster tail runs
+// (reduction scratch + per-cluster A^T partials + per-cluster row sums)
+extern "C" size_t nys_tail_cluster_workspace(int64_t rows, int64_t n) {
+  (void)rows;
+  const size_t ncl = nys::kNumSMs / nys::kHcC;
+  return (size_t)(nys::kRedPartialsTail * 16 + 64) * sizeof(double) + ncl * 3 * (size_t)n * 8 + ncl * 8 * 8;
+}
+
+namespace nys {
+// AT[j, c] = sum over clusters of P[(cl * K + j) * n + c], fixed cluster order
+__global__ void tail_partial_sum_kernel(const double* __restrict__ P, int64_t n, int K, int ncl,
+                                        double* __restrict__ AT) {
+  const int64_t total = n * K;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / n, c = t - j * n;
+    double a = 0.0;
+    for (int q = 0; q < ncl; ++q) a += P[((int64_t)q * K + j) * n + c];
+    AT[j * n + c] = a;
+  }
+}
+}  // namespace nys
+
+// The one-pass ML tail on its own (tests and measurement): T = [l'(Ax-b),
+// w o Ax, l'(Az-b)] (3 x rows), w = l''(Ax-b), AT = A^T T (3 x n, 2 x n without
+// z), rowsums[0..4] as nys_ml_rowwise_f64.  NYS_ERR_UNSUPPORTED for shapes
+// without a cluster plan (n <= 12800 or too wide).
+extern "C" int nys_ml_tail_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x,
+                               const double* z, const double* b, int loss, double* T, double* w, double* AT,
+                               double* rowsums, void* ws, size_t ws_bytes, void* stream) {
+  using namespace nys;
+  if (rows <= 0 || n <= 0 || lda < n || loss < 0 || loss > 2) return NYS_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  double* P = nullptr;
+  int splits = 0;
+  const int rc = tail_cluster(A, rows, n, lda, x, z, b, loss, T, w, ws, ws_bytes,
+                              (size_t)(kRedPartialsTail * 16 + 64) * sizeof(double), rowsums, st, nullptr, &P,
+                              &splits);
+  if (rc) return rc;
+  const int K = z ? 3 : 2;
+  tail_partial_sum_kernel<<<(unsigned)tmin<int64_t>(cdiv(n * K, 256), 4 * kNumSMs), 256, 0, st>>>(P, n, K, splits,
+                                                                                                    AT);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}

@@ -1094,6 +1094,9 @@ int gemv_t(const double* A, int64_t rows, int64_t n, int64_t lda, const double* 
 int gemv_t_partials(const double* A, int64_t rows, int64_t n, int64_t lda, const double* T, int64_t ldt, int k,
                     void* ws, size_t ws_bytes, cudaStream_t st, const double* pred, double** P, int* splits,
                     const double* order);
+int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
+                 const double* b, int loss, double* T, double* w, void* ws, size_t ws_bytes, size_t ws_off,
+                 double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out);
 int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                const double* b, int loss, double* tg, double* w, double* thx, double* tnu, double* rowsums,
                double* part, unsigned int* counter, cudaStream_t st, const double* pred, const double* order);
@@ -1127,9 +1130,23 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   }
   // data passes at (x, z) (admm.py:585-587)
   if (t->kind == 0) {
+    const int64_t woff0 = t->wnorms - t->norms;
+    const bool fuse0 = !t->reduce && woff0 >= 16 && woff0 <= 64 &&
+                       cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
+    // wide rows: the whole tail's data passes in one cluster stream over A
+    // (hvp_cluster.cu: tail_cluster_kernel); else the row pass + GEMV^T below
+    double* Pc = nullptr;
+    int csplits = 0;
+    if (fuse0) {
+      rc = tail_cluster(t->A, t->rows, n, t->lda, x, t->with_z ? z : nullptr, t->b, t->loss, t->T, t->w, t->ws_gemvT,
+                        t->ws_gemvT_bytes, (kRedPartials * 16 + 64) * sizeof(double), t->rowsums, st, pred, &Pc,
+                        &csplits);
+      if (rc != NYS_OK && rc != NYS_ERR_UNSUPPORTED) return rc;
+      if (rc != NYS_OK) Pc = nullptr;
+    }
     // A{x, z} + loss epilogue in one streaming pass (rowpass.cu), else the
     // 2-RHS GEMV and the row-wise kernel
-    rc = xz_rowpass(t->A, t->rows, n, t->lda, x, t->with_z ? z : nullptr, t->b, t->loss, t->T, t->w, t->T + t->rows,
+    rc = Pc ? NYS_OK : xz_rowpass(t->A, t->rows, n, t->lda, x, t->with_z ? z : nullptr, t->b, t->loss, t->T, t->w, t->T + t->rows,
                     t->with_z ? t->T + 2 * t->rows : nullptr, t->rowsums, red_part(t->ws_red), red_counter(t->ws_red),
                     st, pred, t->order);
     if (rc == NYS_ERR_UNSUPPORTED) {
@@ -1151,11 +1168,11 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
                       cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
     if (fuse) {
       // A^T split partials, then one epilogue kernel: split sum -> AT, norms, window norms
-      double* P = nullptr;
-      int splits = 0;
+      double* P = Pc;
+      int splits = csplits;
       const int K = t->with_z ? 3 : 2;
-      if ((rc = gemv_t_partials(t->A, t->rows, n, t->lda, t->T, t->rows, K, t->ws_gemvT, t->ws_gemvT_bytes, st,
-                                pred, &P, &splits, t->order)))
+      if (!P && (rc = gemv_t_partials(t->A, t->rows, n, t->lda, t->T, t->rows, K, t->ws_gemvT, t->ws_gemvT_bytes, st,
+                                      pred, &P, &splits, t->order)))
         return rc;
       SlotList sl;
       const int no = (t->ring && t->nothers > 0) ? t->nothers : 0;

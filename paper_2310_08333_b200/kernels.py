@@ -390,6 +390,17 @@ class Kernels:
         check(self.L.nys_syevj_f64(s, A.data_ptr(), V.data_ptr(), w.data_ptr(), ws.data_ptr(), ws.numel(),
                                    self.sp), "syevj")
 
+    def ml_tail(self, loss, A, x, z, b, T, w, AT, rowsums) -> None:
+        """One-pass A{x,z} + loss epilogue + A^T{...} for wide rows (cluster tail)."""
+        rows, n = A.shape
+        ws = self.workspace("tail_gemvT", self.L.nys_tail_cluster_workspace(rows, n))
+        self.launches += 1
+        e = self._t0("ml_tail")
+        check(self.L.nys_ml_tail_f64(A.data_ptr(), rows, n, A.stride(0), x.data_ptr(), _p(z), b.data_ptr(),
+                                     _lib.LOSS[loss], T.data_ptr(), w.data_ptr(), AT.data_ptr(), rowsums.data_ptr(),
+                                     ws.data_ptr(), ws.numel(), self.sp), "ml_tail")
+        self._t1(e)
+
     # ------------------------------------- sparse / general-operator engine --
     def csr_spmv(self, csr, x, y, alpha=1.0, dscale=None, beta=0.0, zin=None) -> None:
         """y = alpha * dscale o (A x) + beta * zin for a device CSR ``csr``."""

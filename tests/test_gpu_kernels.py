@@ -386,3 +386,39 @@ def test_lasso_generated_in_hbm_matches_host(kx, host_b):
     # a rank's rows of a sharded run: the same numbers
     A2, b2, lam2, _, _ = devgen.lasso_device(kx, N, n, seed, frac, rows=(100, 200), host_b=host_b)
     assert np.array_equal(A2.cpu().numpy(), got[100:200]) and np.array_equal(b2, b) and lam2 == lam
+
+
+@pytest.mark.parametrize("rows,n,with_z", [(300, 20000, True), (37, 100000, True), (301, 20002, False),
+                                           (5, 14000, True)])
+def test_ml_tail_one_pass(kx, rows, n, with_z):
+    """The one-pass ADMM tail for wide rows (cluster stream over A): A{x,z}, the
+    loss epilogue and A^T{l', w o Ax, nu} against NumPy (square loss)."""
+    g = np.random.default_rng(rows + n)
+    A = g.standard_normal((rows, n)) / np.sqrt(n)
+    x, z, b = g.standard_normal(n), g.standard_normal(n), g.standard_normal(rows)
+    T = kx.empty(3, rows)
+    w = kx.empty(rows)
+    K = 3 if with_z else 2
+    AT = kx.empty(K, n)
+    rs = kx.zeros(8)
+    kx.ml_tail("square", dev(A), dev(x), dev(z) if with_z else None, dev(b), T, w, AT, rs)
+    r1 = A @ x - b
+    tg, thx = r1, A @ x
+    Tn = T.cpu().numpy()
+    np.testing.assert_allclose(Tn[0], tg, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(Tn[1], thx, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(w.cpu().numpy(), np.ones(rows))
+    ref = [A.T @ tg, A.T @ thx]
+    s = rs.cpu().numpy()
+    assert s[0] == pytest.approx(0.5 * np.sum(r1 * r1), rel=1e-12)
+    if with_z:
+        nu = A @ z - b
+        np.testing.assert_allclose(Tn[2], nu, rtol=1e-12, atol=1e-12)
+        ref.append(A.T @ nu)
+        assert s[1] == pytest.approx(0.5 * np.sum(nu * nu), rel=1e-12)
+        assert s[2] == pytest.approx(0.5 * np.sum(nu * nu), rel=1e-12)
+        assert s[3] == 0.0
+        assert s[4] == pytest.approx(b @ nu, rel=1e-11, abs=1e-11)
+    ATn = AT.cpu().numpy()
+    for j in range(K):
+        np.testing.assert_allclose(ATn[j], ref[j], rtol=1e-11, atol=1e-11 * np.abs(ref[j]).max())
