@@ -265,9 +265,12 @@ class _Engine:
             if p.loss.kind not in _lib.LOSS:
                 raise CapabilityError(f"loss {p.loss.kind!r} is not implemented on the B200 path")
             self.shard = shard or current_shard(p.N)
-            self.A = p.A.device_rows(self.shard, kx.device)
-            rows = self.rows = self.A.shape[0]
+            # b first: a host->device copy queued behind A's would wait for all of it
             self.b = to_device(p.b[self.shard.row_start:self.shard.row_stop], kx.device)
+            # a pinned host matrix uploads in row chunks behind the setup (run())
+            self.A = p.A.device_rows(self.shard, kx.device, overlap=True)
+            self._a_chunks = p.A.take_pending(self.A)
+            rows = self.rows = self.A.shape[0]
             self.loss = p.loss.kind
             self.l1, self.l2 = float(p.lambda1), float(p.lambda2)
             self.const_hess = p.loss.deriv2_constant
@@ -289,6 +292,7 @@ class _Engine:
                 raise CapabilityError("the B200 path supports QPs with M = I only")
             self.shard = Shard(0, 1, 0, n, n)  # P is replicated
             self.P = qp.P.device_rows(None, kx.device)
+            self._a_chunks = None
             self.q = to_device(qp.q, kx.device)
             self.lo = to_device(qp.box.l, kx.device)
             self.hi = to_device(qp.box.u, kx.device)
@@ -373,11 +377,29 @@ class _Engine:
         return lambda v, out, rdot, rz: kx.precond_apply(self.U, self.lam, self.pc_nu, v, out, rdot, rz)
 
     # ----------------------------------------------------------- sketch --
-    def _sketch_target(self):
+    def _sketch_target(self, chunks=None):
         """(cols, reduce): Y = H Q for the sketch target and the all-reduce of
-        Y's row-shard partials (None unsharded)."""
+        Y's row-shard partials (None unsharded).  ``chunks``: A is still being
+        uploaded in row blocks [(r0, r1, event)]: Y = sum_c A_c^T (A_c Q), each
+        block's GEMMs queued behind its copy (square loss: no row weights)."""
         kx = self.kx
         n = self.n
+        if self.is_ml and chunks:
+            A = self.A
+
+            def cols(Q):
+                rows = A.shape[0]
+                s = Q.shape[1]
+                Z = kx.empty(rows, s)
+                Y = kx.empty(n, s)
+                for c, (r0, r1, ev) in enumerate(chunks):
+                    kx.stream.wait_event(ev)
+                    kx.gemm(0, 0, r1 - r0, s, n, 1.0, A[r0:r1], A.stride(0), Q, s, 0.0, Z[r0:r1], s)
+                    kx.gemm(1, 0, n, s, r1 - r0, 1.0, A[r0:r1], A.stride(0), Z[r0:r1], s, 0.0 if c == 0 else 1.0,
+                            Y, s)
+                return Y
+
+            return cols, None
         if self.is_ml:
             A, w = self.A, (None if self.loss == "square" else self.w)
 
@@ -405,8 +427,8 @@ class _Engine:
             reduce = None
         return cols, reduce
 
-    def sketch(self, seed: int, omega: Optional[np.ndarray] = None) -> None:
-        cols, reduce = self._sketch_target()
+    def sketch(self, seed: int, omega: Optional[np.ndarray] = None, chunks=None) -> None:
+        cols, reduce = self._sketch_target(chunks)
         U, lam = sketch_device(self.kx, cols, self.n, self.r_sk, seed, omega=omega, reduce=reduce)
         if U.shape[1] == 0:
             self.U, self.lam = None, None
@@ -476,16 +498,32 @@ class _Engine:
         self.r_sk = max(1, min(r_sk, n))
         nu_identity = lambda rho: rho + sigma_eff + self.diag_shift  # admm.py:490-491
 
-        # hess.update(x0) and the data passes at x0
-        self.evaluate(with_z=False)
+        # hess.update(x0) and the data passes at x0.  While A is still arriving
+        # over PCIe (a pinned host matrix), a square-loss problem -- whose sketch
+        # target A^T A does not depend on x0 -- sketches first, block by block
+        # behind the copies; the data passes then wait for the whole matrix.
+        chunks, self._a_chunks = self._a_chunks, None
+        sketch_first = bool(chunks) and self.is_ml and self.loss == "square" and opts.use_preconditioner \
+            and not self.shard.sharded
+
+        def wait_all():
+            for _, _, ev in chunks or ():
+                kx.stream.wait_event(ev)
+
+        if not sketch_first:
+            wait_all()
+            self.evaluate(with_z=False)
         last_sketch = 0
         have_pc = False
         if opts.use_preconditioner:
             t0 = time.perf_counter()
-            self.sketch(opts.rng_seed)
+            self.sketch(opts.rng_seed, chunks=chunks if sketch_first else None)
             timings.precond_s += time.perf_counter() - t0
             self.pc_nu = nu_identity(self.rho)
             have_pc = True
+        if sketch_first:
+            wait_all()
+            self.evaluate(with_z=False)
         self.norms(with_nu=False)
         st = self.read_stats()
         res = self._residuals(st)

@@ -16,6 +16,7 @@ general-operator engine (``general.py``).
 
 from __future__ import annotations
 
+import os
 from typing import Callable, Optional
 
 import numpy as np
@@ -140,12 +141,15 @@ class DenseOperator(LinearOperator):
     """
 
     def __init__(self, a):
+        self._host_t = None
         if isinstance(a, torch.Tensor):
             if a.ndim != 2:
                 raise DimensionMismatchError("dense operator requires a 2-d array")
             self._dev_full = a.to(dtype=F64).contiguous() if a.is_cuda else None
             self.a = a if not a.is_cuda else None
             if self.a is not None:
+                if a.dtype == F64 and a.is_contiguous():
+                    self._host_t = a  # pinned host data can be uploaded in overlapped chunks
                 self.a = self.a.numpy()
         else:
             arr = np.asarray(a, dtype=float)
@@ -156,6 +160,7 @@ class DenseOperator(LinearOperator):
         shape = (self._dev_full.shape if self._dev_full is not None else self.a.shape)
         super().__init__(shape[1], shape[0])
         self._shards: dict = {}
+        self._pending: dict = {}
         self._local = None  # (row_start, row_stop) when only a row block is resident
         self._host_local = None
 
@@ -174,6 +179,8 @@ class DenseOperator(LinearOperator):
         op._dev_full = None
         LinearOperator.__init__(op, a_local.shape[1], rows_global)
         op._shards = {}
+        op._pending = {}
+        op._host_t = None
         op._local = (row_start, row_start + a_local.shape[0])
         op._host_local = None
         if a_local.is_cuda:
@@ -185,14 +192,39 @@ class DenseOperator(LinearOperator):
         return op
 
     # -- device data ---------------------------------------------------------
-    def device_rows(self, shard: Optional[Shard] = None, device=None) -> torch.Tensor:
-        """The (row-shard of the) matrix in HBM, uploaded once."""
+    UPLOAD_CHUNKS = 8
+
+    def _pinned_rows(self, shard: Shard) -> Optional[torch.Tensor]:
+        """A pinned host tensor view of the shard's rows, when the host copy is pinned."""
+        host = getattr(self, "_host_t", None)
+        if host is None or not host.is_pinned():
+            return None
+        return host[shard.row_start:shard.row_stop]
+
+    def device_rows(self, shard: Optional[Shard] = None, device=None, overlap: bool = False) -> torch.Tensor:
+        """The (row-shard of the) matrix in HBM, uploaded once.
+
+        ``overlap``: a pinned host matrix is copied in row chunks on a side
+        stream and the tensor is returned at once; the caller takes the chunk
+        events with ``take_pending`` and makes its stream wait on each chunk
+        before touching those rows (the solve overlaps the upload with its
+        setup sketch).  Without it every pending chunk is waited for."""
         if shard is None:
             shard = Shard(0, 1, 0, self.output_dim, self.output_dim)
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         key = (shard.row_start, shard.row_stop, str(device))
         t = self._shards.get(key)
+        if t is not None and not overlap:
+            self._wait_pending(t)
+        if overlap and os.environ.get("NYS_UPLOAD_OVERLAP", "1") == "0":
+            overlap = False
+        if t is None and overlap and self._dev_full is None and self._local is None:
+            src = self._pinned_rows(shard)
+            if src is not None:
+                t = torch.empty(tuple(src.shape), dtype=F64, device=device)
+                self._pending[t.data_ptr()] = _chunked_upload(src, t, self.UPLOAD_CHUNKS)
+                self._shards[key] = t
         if t is None and self._local is not None and getattr(self, "_host_local", None) is not None \
                 and (shard.row_start, shard.row_stop) == self._local:
             t = self._host_local.to(device, non_blocking=self._host_local.is_pinned())
@@ -209,9 +241,22 @@ class DenseOperator(LinearOperator):
             self._shards[key] = t
         return t
 
+    def take_pending(self, t: torch.Tensor):
+        """[(row0, row1, event)] of an overlapped upload into ``t`` (None when
+        complete); the caller now owns the waits."""
+        return self._pending.pop(t.data_ptr(), None)
+
+    def _wait_pending(self, t: torch.Tensor) -> None:
+        chunks = self._pending.pop(t.data_ptr(), None)
+        if chunks:
+            cur = torch.cuda.current_stream(t.device)
+            for _, _, ev in chunks:
+                cur.wait_event(ev)
+
     def release(self) -> None:
         """Drop cached device copies (the host array is kept)."""
         self._shards.clear()
+        self._pending.clear()
 
     # -- apply -------------------------------------------------------------------
     def _apply_dev(self, v):
@@ -236,6 +281,34 @@ class DenseOperator(LinearOperator):
         Y = kx.empty(rows, s)
         kx.gemm(0, 0, rows, s, n, 1.0, A, A.stride(0), V, V.stride(0), 0.0, Y, s)
         return Y
+
+
+_UPLOAD_STREAMS: dict = {}
+
+
+def _chunked_upload(src: torch.Tensor, dst: torch.Tensor, chunks: int):
+    """Copy pinned host rows into ``dst`` in ``chunks`` row blocks on a side
+    stream; returns [(row0, row1, event)] (PCIe runs while the caller computes)."""
+    dev = dst.device
+    us = _UPLOAD_STREAMS.get(dev)
+    if us is None:
+        us = torch.cuda.Stream(dev)
+        _UPLOAD_STREAMS[dev] = us
+    # dst's memory may have just been freed on the current stream; the current
+    # stream in turn waits on every chunk event before using (or freeing) dst,
+    # so the allocator's stream-ordered reuse stays safe without record_stream
+    us.wait_stream(torch.cuda.current_stream(dev))
+    rows = dst.shape[0]
+    step = -(-rows // max(1, chunks))
+    out = []
+    with torch.cuda.stream(us):
+        for r0 in range(0, rows, step):
+            r1 = min(rows, r0 + step)
+            dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(us)
+            out.append((r0, r1, ev, src))
+    return [(r0, r1, ev) for r0, r1, ev, _ in out]
 
 
 class DeviceCSR:
