@@ -159,7 +159,7 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
       const int jt = it - L;
       if (jt < 0) continue;
       const int s = jt & (kHcNT - 1);
-      mbar_wait_cluster(&totb[s], (unsigned)((jt / kHcNT) & 1));
+      mbar_wait(&totb[s], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire (no L1 invalidation)
       double t = 0.0;  // d_i (a_i . v): the 16 CTA partials (already scaled) in a fixed order
 #pragma unroll
       for (int q2 = 0; q2 < kHcC; ++q2) t += tsl[s * kHcC + q2];
@@ -395,7 +395,7 @@ hvp_cluster_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int6
       const int jt = it - L;
       if (jt < 0) continue;
       const int s = jt & (kHcNT - 1);
-      mbar_wait_cluster(&totb[s], (unsigned)((jt / kHcNT) & 1));
+      mbar_wait(&totb[s], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire (no L1 invalidation)
       double t = 0.0;
 #pragma unroll
       for (int q2 = 0; q2 < kHcC; ++q2) t += tsl[s * kHcC + q2];
@@ -736,7 +736,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       const int jt = it - L;
       if (jt < 0) continue;
       const int s = jt & (kHcNT - 1);
-      mbar_wait_cluster(&totb[s], (unsigned)((jt / kHcNT) & 1));
+      mbar_wait(&totb[s], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire (no L1 invalidation)
       double ax = 0.0, az = 0.0;
 #pragma unroll
       for (int q2 = 0; q2 < kHcC; ++q2) ax += tsl[(s * NV) * kHcC + q2];
