@@ -53,6 +53,17 @@ __device__ __forceinline__ void nbar_sync(int id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kHcBarThreads) : "memory");
 }
 
+// The 16 CTA partials of a row total, summed by a fixed shuffle tree within
+// each 16-lane half of the warp (lanes l and l + 16 load partial l & 15 of
+// slot p + (l >> 4) * 16): one shared-memory load and four adds per thread
+// instead of sixteen each.  Every thread of every CTA gets the same bits.
+__device__ __forceinline__ double cluster_total_halves(const double* p, int lane) {
+  double v = p[(lane >> 4) * kHcC + (lane & 15)];
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int K>
 __global__ void __launch_bounds__(kHcThreads, 1)
 hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
@@ -160,9 +171,8 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
       if (jt < 0) continue;
       const int s = jt & (kHcNT - 1);
       mbar_wait(&totb[s], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire (no L1 invalidation)
-      double t = 0.0;  // d_i (a_i . v): the 16 CTA partials (already scaled) in a fixed order
-#pragma unroll
-      for (int q2 = 0; q2 < kHcC; ++q2) t += tsl[s * kHcC + q2];
+      // d_i (a_i . v): the 16 CTA partials (already scaled), fixed-order tree
+      const double t = __shfl_sync(0xffffffffu, cluster_total_halves(tsl + s * kHcC, lane & 15), 0);
       if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kHcC * 8u);  // re-arm for row jt + NT
       const int q = qj;
       if (++qj == S) qj = 0;
@@ -396,9 +406,7 @@ hvp_cluster_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int6
       if (jt < 0) continue;
       const int s = jt & (kHcNT - 1);
       mbar_wait(&totb[s], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire (no L1 invalidation)
-      double t = 0.0;
-#pragma unroll
-      for (int q2 = 0; q2 < kHcC; ++q2) t += tsl[s * kHcC + q2];
+      const double t = __shfl_sync(0xffffffffu, cluster_total_halves(tsl + s * kHcC, lane & 15), 0);
       if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kHcC * 8u);
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
@@ -737,12 +745,10 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       if (jt < 0) continue;
       const int s = jt & (kHcNT - 1);
       mbar_wait(&totb[s], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire (no L1 invalidation)
-      double ax = 0.0, az = 0.0;
-#pragma unroll
-      for (int q2 = 0; q2 < kHcC; ++q2) ax += tsl[(s * NV) * kHcC + q2];
-      if (WITHZ)
-#pragma unroll
-        for (int q2 = 0; q2 < kHcC; ++q2) az += tsl[(s * NV + 1) * kHcC + q2];
+      // lanes 0-15: the x partials, 16-31: the z partials (fixed-order trees)
+      const double tot = cluster_total_halves(tsl + (s * NV) * kHcC, WITHZ ? lane : (lane & 15));
+      const double ax = __shfl_sync(0xffffffffu, tot, 0);
+      const double az = WITHZ ? __shfl_sync(0xffffffffu, tot, 16) : 0.0;
       if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kTx);
       const int64_t i = cluster_id + (int64_t)jt * nclusters;
       const double bi = __ldg(b + i);
