@@ -261,6 +261,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, double2 (&x)[4]) {
   }
 }
 
+// x and z slices of one pair of double2 columns each (two x8 loads, one wait)
+__device__ __forceinline__ void tmem_ld8x2(uint32_t ta, uint32_t tb, double2 (&x)[2], double2 (&z)[2]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%16];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8, %9, %10, %11, %12, %13, %14, %15}, [%17];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta), "r"(tb)
+      : "memory");
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    x[k].x = __hiloint2double((int)r[4 * k + 1], (int)r[4 * k + 0]);
+    x[k].y = __hiloint2double((int)r[4 * k + 3], (int)r[4 * k + 2]);
+    z[k].x = __hiloint2double((int)r[8 + 4 * k + 1], (int)r[8 + 4 * k + 0]);
+    z[k].y = __hiloint2double((int)r[8 + 4 * k + 3], (int)r[8 + 4 * k + 2]);
+  }
+}
+
 template <int Q, int KQ>
 __global__ void __launch_bounds__(kHqThreads, 1)
 hvp_cluster_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
@@ -716,14 +736,39 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
         }
         const double* row = ring + (size_t)q * W;
         const int rs = it % kHqNR;
+        if (WITHZ) {
+          // one pass over the staged row for both dots: a read once per element
+          double px = 0.0, pz = 0.0;
 #pragma unroll
-        for (int vv = 0; vv < NV; ++vv) {
+          for (int k2 = 0; k2 < (KQ + 1) / 2; ++k2) {
+            double2 cx[2], cz[2];
+            tmem_ld8x2(tv + 8 * k2, tv + 32 + 8 * k2, cx, cz);
+#pragma unroll
+            for (int k1 = 0; k1 < 2; ++k1) {
+              const int k = 2 * k2 + k1;
+              const int j = 2 * (tid + k * kHqWarps * 32);
+              if (k < KQ && j < w_here) {
+                const double2 a = *reinterpret_cast<const double2*>(row + j);
+                px = fma(a.x, cx[k1].x, px);
+                px = fma(a.y, cx[k1].y, px);
+                pz = fma(a.x, cz[k1].x, pz);
+                pz = fma(a.y, cz[k1].y, pz);
+              }
+            }
+          }
+          px = warp_sum(px);
+          pz = warp_sum(pz);
+          if (lane == 0) {
+            psl[(rs * NV) * kHqWarps + warp] = px;
+            psl[(rs * NV + 1) * kHqWarps + warp] = pz;
+          }
+        } else {
           double pt = 0.0;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (4 * h >= KQ) continue;
             double2 c[4];
-            tmem_ld16(tv + 32 * vv + 16 * h, c);
+            tmem_ld16(tv + 16 * h, c);
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4) {
               const int k = 4 * h + k4;
@@ -736,7 +781,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
             }
           }
           pt = warp_sum(pt);
-          if (lane == 0) psl[(rs * NV + vv) * kHqWarps + warp] = pt;
+          if (lane == 0) psl[(rs * NV) * kHqWarps + warp] = pt;
         }
         __syncwarp();
         qbar_arrive(1 + kHqMaxS + rs);
