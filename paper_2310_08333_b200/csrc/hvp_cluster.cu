@@ -638,6 +638,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
   const int64_t c0 = (int64_t)rank * W;
   const int w_here = (int)tmax<int64_t>(0, tmin<int64_t>((int64_t)W, n - c0));
   const unsigned bytes = (unsigned)w_here * 8u;
+  const int jmax = tmax(0, w_here - 2);  // last valid double2 of the staged segment
   const int64_t nrows_mine = rows > cluster_id ? (rows - cluster_id + nclusters - 1) / nclusters : 0;
   constexpr unsigned kTx = (unsigned)(kHcC * NV * 8);
 
@@ -746,9 +747,8 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
 #pragma unroll
             for (int k1 = 0; k1 < 2; ++k1) {
               const int k = 2 * k2 + k1;
-              const int j = 2 * (tid + k * kHqWarps * 32);
-              if (k < KQ && j < w_here) {
-                const double2 a = *reinterpret_cast<const double2*>(row + j);
+              if (k < KQ) {  // compile-time; out-of-range columns: x = z = 0 in TMEM, a read clamped
+                const double2 a = *reinterpret_cast<const double2*>(row + tmin(2 * (tid + k * kHqWarps * 32), jmax));
                 px = fma(a.x, cx[k1].x, px);
                 px = fma(a.y, cx[k1].y, px);
                 pz = fma(a.x, cz[k1].x, pz);
@@ -823,19 +823,18 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       const int q = qj;
       if (++qj == S) qj = 0;
       const double* row = ring + (size_t)q * W;
+      // branch-free: columns past the segment accumulate into registers that are
+      // never stored (reads clamped to the staged row)
 #pragma unroll
       for (int k = 0; k < KQ; ++k) {
-        const int j = 2 * (tid + k * kHqWarps * 32);
-        if (j < w_here) {
-          const double2 a = *reinterpret_cast<const double2*>(row + j);
-          yg[k].x = fma(tg, a.x, yg[k].x);
-          yg[k].y = fma(tg, a.y, yg[k].y);
-          yh[k].x = fma(thx, a.x, yh[k].x);
-          yh[k].y = fma(thx, a.y, yh[k].y);
-          if (WITHZ) {
-            yn[k].x = fma(nu, a.x, yn[k].x);
-            yn[k].y = fma(nu, a.y, yn[k].y);
-          }
+        const double2 a = *reinterpret_cast<const double2*>(row + tmin(2 * (tid + k * kHqWarps * 32), jmax));
+        yg[k].x = fma(tg, a.x, yg[k].x);
+        yg[k].y = fma(tg, a.y, yg[k].y);
+        yh[k].x = fma(thx, a.x, yh[k].x);
+        yh[k].y = fma(thx, a.y, yh[k].y);
+        if (WITHZ) {
+          yn[k].x = fma(nu, a.x, yn[k].x);
+          yn[k].y = fma(nu, a.y, yn[k].y);
         }
       }
       __syncwarp();
