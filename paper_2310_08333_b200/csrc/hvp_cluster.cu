@@ -720,12 +720,15 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       yh[k] = make_double2(0.0, 0.0);
       if (WITHZ) yn[k] = make_double2(0.0, 0.0);
     }
-    const bool writer = rank == 0 && warp == 0 && lane == 0;
-    // the row sums live in shared memory (one thread updates them): no registers
-    __shared__ double rsum[5];
-    if (writer)
+    // rank 0 writes T, w and the row sums; the row's writer warp rotates
+    // (row jt -> warp jt mod 14) so no warp carries the extra work every row.
+    // Each warp sums its rows in row order into its own shared slots; the 14
+    // slots are combined in warp order at the end (deterministic).
+    __shared__ double rsum[kHqWarps][5];
+    if (rank == 0 && lane == 0)
 #pragma unroll
-      for (int q = 0; q < 5; ++q) rsum[q] = 0.0;
+      for (int q = 0; q < 5; ++q) rsum[warp][q] = 0.0;
+    int wturn = 0;  // jt mod kHqWarps, kept incrementally
     int qi = 0, pi = 0, qj = 0;
     for (int it = 0; it < nr + L; ++it) {
       if (it < nr) {
@@ -807,19 +810,21 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
         r2 = __dadd_rn(az, -bi);
         nu = loss_d1(loss, r2);
       }
-      if (writer) {
+      if (rank == 0 && lane == 0 && warp == wturn) {
+        double* rw = rsum[warp];
         T[i] = tg;
         T[rows + i] = thx;
         wout[i] = wi;
-        rsum[0] += loss_val(loss, r1);
+        rw[0] += loss_val(loss, r1);
         if (WITHZ) {
           T[2 * rows + i] = nu;
-          rsum[1] += loss_val(loss, r2);
+          rw[1] += loss_val(loss, r2);
           const double cv = loss_conj(loss, nu);
-          if (isinf(cv)) rsum[3] += 1.0; else rsum[2] += cv;
-          rsum[4] = fma(bi, nu, rsum[4]);
+          if (isinf(cv)) rw[3] += 1.0; else rw[2] += cv;
+          rw[4] = fma(bi, nu, rw[4]);
         }
       }
+      if (++wturn == kHqWarps) wturn = 0;
       const int q = qj;
       if (++qj == S) qj = 0;
       const double* row = ring + (size_t)q * W;
@@ -851,9 +856,14 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
         if (WITHZ) *reinterpret_cast<double2*>(pc + 2 * n + j) = yn[k];
       }
     }
-    if (writer)
-#pragma unroll
-      for (int q = 0; q < 5; ++q) rowpart[cluster_id * 8 + q] = rsum[q];
+    if (rank == 0) {
+      asm volatile("bar.sync %0, %1;" ::"r"(14), "r"(kHqWarps * 32) : "memory");  // all compute warps done
+      if (warp == 0 && lane < 5) {
+        double a = 0.0;
+        for (int w2 = 0; w2 < kHqWarps; ++w2) a += rsum[w2][lane];
+        rowpart[cluster_id * 8 + lane] = a;
+      }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cl.sync();
