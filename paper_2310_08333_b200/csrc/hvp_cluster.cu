@@ -614,6 +614,8 @@ int hvp_cluster(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda
 // per-cluster A^T partials P[(c * 3 + j) * n + col] (the layout the ML
 // epilogue sums in a fixed order) and per-cluster row sums (fixed row order):
 //   rowpart[c * 8 + 0..4] = sum l(r1), sum l(r2), sum l*(nu) finite, #inf, b.nu
+constexpr int kTcNR = 2;  // row slots of the lane partials (safe for L = 1: see the Q kernel)
+
 template <int KQ, bool WITHZ>
 __global__ void __launch_bounds__(kHqThreads, 1)
 tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
@@ -626,8 +628,8 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
   if (pred && *pred != 0.0) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);                 // S x W
-  double* psl = ring + (size_t)S * W;                                 // NR x NV x 14 warp partials
-  double* tsl = psl + kHqNR * NV * kHqWarps;                          // NT x NV x 16 CTA partials
+  double* psl = ring + (size_t)S * W;                                 // NR x NV x 448 lane partials
+  double* tsl = psl + kTcNR * NV * kHqWarps * 32;                     // NT x NV x 16 CTA partials
   uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * NV * kHcC);  // S
   uint64_t* totb = full + S;                                          // NT
   uint32_t* tmem_base = reinterpret_cast<uint32_t*>(totb + kHcNT);
@@ -681,15 +683,19 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
     for (int g = tmax(0, nr - S); g < nr; ++g) qbar_sync(1 + g % S);
   } else if (warp > kHqWarps) {
     // --------------------------------------------------- exchange (relay) --
+    // the compute warps leave one partial per lane; this warp reduces them
+    // (lane l: the 14 warps' lane-l partials in warp order, then a shuffle tree)
     for (int g = 0; g < nr; ++g) {
-      const int rs = g % kHqNR;
+      const int rs = g % kTcNR;
       qbar_sync(1 + kHqMaxS + rs);
       const int s = g & (kHcNT - 1);
 #pragma unroll
       for (int vv = 0; vv < NV; ++vv) {
-        double p = lane < kHqWarps ? psl[(rs * NV + vv) * kHqWarps + lane] : 0.0;
+        const double* pp = psl + (rs * NV + vv) * kHqWarps * 32 + lane;
+        double p = 0.0;
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        for (int w2 = 0; w2 < kHqWarps; ++w2) p += pp[w2 * 32];
+        p = warp_sum(p);
         if (lane < kHcC) st_async_remote_f64(tsl + (s * NV + vv) * kHcC + rank, &totb[s], (unsigned)lane, p);
       }
     }
@@ -739,7 +745,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
           pi ^= 1;
         }
         const double* row = ring + (size_t)q * W;
-        const int rs = it % kHqNR;
+        const int rs = it % kTcNR;
         if (WITHZ) {
           // one pass over the staged row for both dots: a read once per element
           double px = 0.0, pz = 0.0;
@@ -759,12 +765,8 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
               }
             }
           }
-          px = warp_sum(px);
-          pz = warp_sum(pz);
-          if (lane == 0) {
-            psl[(rs * NV) * kHqWarps + warp] = px;
-            psl[(rs * NV + 1) * kHqWarps + warp] = pz;
-          }
+          psl[((rs * NV) * kHqWarps + warp) * 32 + lane] = px;
+          psl[((rs * NV + 1) * kHqWarps + warp) * 32 + lane] = pz;
         } else {
           double pt = 0.0;
 #pragma unroll
@@ -783,8 +785,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
               }
             }
           }
-          pt = warp_sum(pt);
-          if (lane == 0) psl[(rs * NV) * kHqWarps + warp] = pt;
+          psl[((rs * NV) * kHqWarps + warp) * 32 + lane] = pt;
         }
         __syncwarp();
         qbar_arrive(1 + kHqMaxS + rs);
@@ -901,10 +902,10 @@ TcPlan tail_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, 
   p.KQ = (int)cdiv(p.W / 2, kHqWarps * 32);
   if (p.KQ > 8) return p;
   const int NV = with_z ? 2 : 1;
-  const size_t fixed = (size_t)kHqNR * NV * kHqWarps * 8 + (size_t)kHcNT * NV * kHcC * 8 + kHcNT * 8 + 16 + 1024;
+  const size_t fixed = (size_t)kTcNR * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * kHcC * 8 + kHcNT * 8 + 16 + 1024;
   p.S = (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / ((size_t)p.W * 8 + 8)));
   if (p.S < 3) return p;
-  p.smem = (size_t)p.S * p.W * 8 + (size_t)kHqNR * NV * kHqWarps * 8 + (size_t)kHcNT * NV * kHcC * 8 +
+  p.smem = (size_t)p.S * p.W * 8 + (size_t)kTcNR * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * kHcC * 8 +
            (size_t)(p.S + kHcNT) * 8 + 16;
   p.ok = true;
   return p;
