@@ -72,8 +72,8 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
   if (pred && *pred != 0.0) return;  // every CTA of every cluster sees the same flag
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);                  // S x W
-  double* psl = ring + (size_t)S * W;                                  // S x 16 warp partials
-  double* tsl = psl + (size_t)S * kHcWarps;                            // NT x 16 CTA partials
+  double* psl = ring + (size_t)S * W;                                  // S x 512 lane partials
+  double* tsl = psl + (size_t)S * kHcWarps * 32;                       // NT x 16 CTA partials
   uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * kHcC);    // S
   uint64_t* totb = full + S;                                           // NT (tx from the cluster)
   cg::cluster_group cl = cg::this_cluster();
@@ -120,12 +120,13 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
     for (int g = xr; g < nr; g += kHcX) {
       const int64_t i = cluster_id + (int64_t)g * nclusters;
       const double di = d ? __ldg(d + i) : 1.0;
-      nbar_sync(1 + kHcMaxS + q);  // the 16 warp partials of row g are in psl
-      double p = lane < kHcWarps ? psl[q * kHcWarps + lane] : 0.0;
-      // fixed-order tree over the 16 warp partials (lanes 0..15)
+      nbar_sync(1 + kHcMaxS + q);  // the 512 lane partials of row g are in psl
+      // lane l: the 16 warps' lane-l partials in warp order, then a shuffle tree
+      const double* pp = psl + (size_t)q * kHcWarps * 32 + lane;
+      double p = 0.0;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-      p *= di;
+      for (int w2 = 0; w2 < kHcWarps; ++w2) p += pp[w2 * 32];
+      p = warp_sum(p) * di;
       const int s = g & (kHcNT - 1);
       if (lane < kHcC) st_async_remote_f64(tsl + s * kHcC + rank, &totb[s], (unsigned)lane, p);
       q += kHcX;
@@ -162,8 +163,7 @@ hvp_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_
             pt = fma(a.y, vr[k].y, pt);
           }
         }
-        pt = warp_sum(pt);
-        if (lane == 0) psl[q * kHcWarps + warp] = pt;
+        psl[((size_t)q * kHcWarps + warp) * 32 + lane] = pt;  // reduced by a relay warp
         __syncwarp();
         nbar_arrive(1 + kHcMaxS + q);
       }
@@ -291,8 +291,8 @@ hvp_cluster_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int6
   if (pred && *pred != 0.0) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);             // S x Wq
-  double* psl = ring + (size_t)S * Wq;                            // NR x 16 warp partials
-  double* tsl = psl + kHqNR * kHqWarps;                           // NT x 16 CTA partials
+  double* psl = ring + (size_t)S * Wq;                            // NR x 448 lane partials
+  double* tsl = psl + kHqNR * kHqWarps * 32;                      // NT x 16 CTA partials
   uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * kHcC);  // S
   uint64_t* totb = full + S;                                      // NT
   uint32_t* tmem_base = reinterpret_cast<uint32_t*>(totb + kHcNT);
@@ -358,10 +358,11 @@ hvp_cluster_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int6
       const double di = d ? __ldg(d + i) : 1.0;
       const int rs = g % kHqNR;
       qbar_sync(1 + kHqMaxS + rs);
-      double p = lane < kHqWarps ? psl[rs * kHqWarps + lane] : 0.0;
+      const double* pp = psl + rs * kHqWarps * 32 + lane;
+      double p = 0.0;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-      p *= di;
+      for (int w2 = 0; w2 < kHqWarps; ++w2) p += pp[w2 * 32];
+      p = warp_sum(p) * di;
       const int s = g & (kHcNT - 1);
       if (lane < kHcC) st_async_remote_f64(tsl + s * kHcC + rank, &totb[s], (unsigned)lane, p);
     }
@@ -416,9 +417,8 @@ hvp_cluster_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int6
           qbar_arrive(1 + slot);
           next();
         }
-        pt = warp_sum(pt);
         const int rs = it % kHqNR;
-        if (lane == 0) psl[rs * kHqWarps + warp] = pt;
+        psl[(rs * kHqWarps + warp) * 32 + lane] = pt;
         __syncwarp();
         qbar_arrive(1 + kHqMaxS + rs);
       }
@@ -477,13 +477,13 @@ HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, c
   const size_t fixed = (size_t)(kHcNT * kHcC) * 8 + kHcNT * 8 + 1024;
   const size_t row_bytes = (size_t)p.W * 8;
   p.S = p.K > 12 ? 0
-                 : (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / (row_bytes + kHcWarps * 8 + 24)));
+                 : (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / (row_bytes + kHcWarps * 256 + 24)));
   static const bool no_q = getenv("NYS_HVP_CLUSTER_NOQ") != nullptr;
   static const bool force_q = getenv("NYS_HVP_CLUSTER_Q") != nullptr;
   if ((p.S < 3 || force_q) && !no_q) {
     // sub-segment plan: the smallest split with >= 4 stages in flight and the
     // y segment (Q x KQ double2 per thread) in registers
-    const size_t qfixed = fixed + (size_t)kHqNR * kHqWarps * 8 + 16;
+    const size_t qfixed = fixed + (size_t)kHqNR * kHqWarps * 32 * 8 + 16;
     static const int forced_q = getenv("NYS_HVP_CLUSTER_Q") ? atoi(getenv("NYS_HVP_CLUSTER_Q")) : 0;
     for (int Q = 2; Q <= 4; ++Q) {
       if (forced_q > 1 && Q != forced_q) continue;
@@ -497,7 +497,7 @@ HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, c
       p.K = KQ;
       p.S = S;
       p.L = 1;
-      p.smem = (size_t)S * Wq * 8 + (size_t)kHqNR * kHqWarps * 8 + (size_t)kHcNT * kHcC * 8 +
+      p.smem = (size_t)S * Wq * 8 + (size_t)kHqNR * kHqWarps * 32 * 8 + (size_t)kHcNT * kHcC * 8 +
                (size_t)(S + kHcNT) * 8 + 16;
       p.nclusters = 0;
       p.ok = true;
@@ -512,7 +512,7 @@ HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, c
   p.L = forced_lag > 0 ? forced_lag : 1;
   p.L = tmax(1, tmin(p.L, p.S - 1));
   if (p.S + p.L + 2 > kHcNT) return p;
-  p.smem = (size_t)p.S * (row_bytes + kHcWarps * 8) + (size_t)kHcNT * kHcC * 8 + (size_t)(p.S + kHcNT) * 8;
+  p.smem = (size_t)p.S * (row_bytes + kHcWarps * 256) + (size_t)kHcNT * kHcC * 8 + (size_t)(p.S + kHcNT) * 8;
   p.nclusters = 0;
   p.ok = true;
   return p;
