@@ -960,12 +960,9 @@ static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64
 int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                  const double* b, int loss, double* T, double* w, void* ws, size_t ws_bytes, size_t ws_off,
                  double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out) {
-  // measured (20000 x 100000): square loss 4.46 ms vs 4.56 ms for the two
-  // passes; logistic 7.28 ms (every warp evaluates the exp-based epilogue and
-  // x, z stream from TMEM at ~25 B/cycle): the one-pass tail only for the
-  // square loss (configs 4 and 5) unless NYS_TAIL_CLUSTER_ALL is set
-  static const bool all_losses = getenv("NYS_TAIL_CLUSTER_ALL") != nullptr;
-  if (loss != NYS_LOSS_SQUARE && !all_losses) return NYS_ERR_UNSUPPORTED;
+  // measured (20000 x 100000): square loss 2.84 ms, logistic 4.29 ms (every
+  // warp evaluates the exp-based epilogue of each row) against 4.57 ms for the
+  // two passes
   TcPlan p = tail_cluster_plan(rows, n, lda, A, x, z != nullptr);
   if (!p.ok) return NYS_ERR_UNSUPPORTED;
   const int K3 = z ? 3 : 2;
