@@ -616,12 +616,24 @@ int hvp_cluster(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda
 //   rowpart[c * 8 + 0..4] = sum l(r1), sum l(r2), sum l*(nu) finite, #inf, b.nu
 constexpr int kTcNR = 2;  // row slots of the lane partials (safe for L = 1: see the Q kernel)
 
-template <int KQ, bool WITHZ>
+// C = CTAs per cluster: 16 for the widest rows (configs 4 and 5), 4 or 8 for
+// rows of 4096-12800 columns (config 2's width)
+template <int C>
+__device__ __forceinline__ double cluster_total_c(const double* p, int lane) {
+  // lanes 0-15: the x partials of the C CTAs, lanes 16-31: the z partials;
+  // fixed-order trees over C lanes (identical bits in every thread and CTA)
+  double v = p[(lane >> 4) * C + (lane & (C - 1))];
+#pragma unroll
+  for (int o = C / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int C, int KQ, bool WITHZ>
 __global__ void __launch_bounds__(kHqThreads, 1)
 tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
                     const double* __restrict__ x, const double* __restrict__ z, const double* __restrict__ b,
                     int loss, int W, int S, double* __restrict__ T, double* __restrict__ wout,
-                    double* __restrict__ P, double* __restrict__ rowpart, const double* __restrict__ pred) {
+                    double* __restrict__ P, double* __restrict__ R, const double* __restrict__ pred) {
   static_assert(KQ <= 8, "x and z slices: <= 32 TMEM columns each");
   constexpr int L = 1;
   constexpr int NV = WITHZ ? 2 : 1;
@@ -630,19 +642,19 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
   double* ring = reinterpret_cast<double*>(smem_raw);                 // S x W
   double* psl = ring + (size_t)S * W;                                 // NR x NV x 448 lane partials
   double* tsl = psl + kTcNR * NV * kHqWarps * 32;                     // NT x NV x 16 CTA partials
-  uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * NV * kHcC);  // S
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * NV * C);  // S
   uint64_t* totb = full + S;                                          // NT
   uint32_t* tmem_base = reinterpret_cast<uint32_t*>(totb + kHcNT);
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
-  const int cluster_id = blockIdx.x / kHcC, nclusters = gridDim.x / kHcC;
+  const int cluster_id = blockIdx.x / C, nclusters = gridDim.x / C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = (int64_t)rank * W;
   const int w_here = (int)tmax<int64_t>(0, tmin<int64_t>((int64_t)W, n - c0));
   const unsigned bytes = (unsigned)w_here * 8u;
   const int jmax = tmax(0, w_here - 2);  // last valid double2 of the staged segment
   const int64_t nrows_mine = rows > cluster_id ? (rows - cluster_id + nclusters - 1) / nclusters : 0;
-  constexpr unsigned kTx = (unsigned)(kHcC * NV * 8);
+  constexpr unsigned kTx = (unsigned)(C * NV * 8);
 
   if (tid == 0) {
     for (int q = 0; q < S; ++q) mbar_init(&full[q], 1);
@@ -696,7 +708,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
 #pragma unroll
         for (int w2 = 0; w2 < kHqWarps; ++w2) p += pp[w2 * 32];
         p = warp_sum(p);
-        if (lane < kHcC) st_async_remote_f64(tsl + (s * NV + vv) * kHcC + rank, &totb[s], (unsigned)lane, p);
+        if (lane < C) st_async_remote_f64(tsl + (s * NV + vv) * C + rank, &totb[s], (unsigned)lane, p);
       }
     }
   } else {
@@ -726,14 +738,9 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       yh[k] = make_double2(0.0, 0.0);
       if (WITHZ) yn[k] = make_double2(0.0, 0.0);
     }
-    // rank 0 writes T, w and the row sums; the row's writer warp rotates
-    // (row jt -> warp jt mod 14) so no warp carries the extra work every row.
-    // Each warp sums its rows in row order into its own shared slots; the 14
-    // slots are combined in warp order at the end (deterministic).
-    __shared__ double rsum[kHqWarps][5];
-    if (rank == 0 && lane == 0)
-#pragma unroll
-      for (int q = 0; q < 5; ++q) rsum[warp][q] = 0.0;
+    // rank 0 writes T, w and the residuals r1, r2 of each row (the row sums
+    // of loss values and conjugates run afterwards, row-parallel, in
+    // tail_rowsums_kernel); the writer warp rotates (row jt -> warp jt mod 14)
     int wturn = 0;  // jt mod kHqWarps, kept incrementally
     int qi = 0, pi = 0, qj = 0;
     for (int it = 0; it < nr + L; ++it) {
@@ -795,7 +802,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       const int s = jt & (kHcNT - 1);
       mbar_wait(&totb[s], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire (no L1 invalidation)
       // lanes 0-15: the x partials, 16-31: the z partials (fixed-order trees)
-      const double tot = cluster_total_halves(tsl + (s * NV) * kHcC, WITHZ ? lane : (lane & 15));
+      const double tot = cluster_total_c<C>(tsl + (s * NV) * C, WITHZ ? lane : (lane & 15));
       const double ax = __shfl_sync(0xffffffffu, tot, 0);
       const double az = WITHZ ? __shfl_sync(0xffffffffu, tot, 16) : 0.0;
       if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kTx);
@@ -803,26 +810,31 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       const double bi = __ldg(b + i);
       // loss epilogue of the row (vec.cu ml_rowwise_kernel, same expressions)
       const double r1 = __dadd_rn(ax, -bi);
-      const double tg = loss_d1(loss, r1);
-      const double wi = loss_d2(loss, r1);
-      const double thx = __dmul_rn(wi, ax);
-      double nu = 0.0, r2 = 0.0;
-      if (WITHZ) {
-        r2 = __dadd_rn(az, -bi);
-        nu = loss_d1(loss, r2);
+      double tg, wi, nu = 0.0, r2 = 0.0;
+      if (WITHZ) r2 = __dadd_rn(az, -bi);
+      if (loss == NYS_LOSS_LOGISTIC) {
+        // the three sigmoids of the row, one per lane (lanes 0, 1, 2: expit(r1),
+        // expit(-r1), expit(r2)), gathered by shuffles: one FP64 exp/div chain
+        // per warp instead of four (same expressions, same bits)
+        const double arg = lane == 0 ? r1 : (lane == 1 ? -r1 : r2);
+        const double e = expit_d(arg);
+        tg = __shfl_sync(0xffffffffu, e, 0);
+        wi = tg * __shfl_sync(0xffffffffu, e, 1);  // loss_d2 = expit(w) * expit(-w)
+        if (WITHZ) nu = __shfl_sync(0xffffffffu, e, 2);
+      } else {
+        tg = loss_d1(loss, r1);
+        wi = loss_d2(loss, r1);
+        if (WITHZ) nu = loss_d1(loss, r2);
       }
+      const double thx = __dmul_rn(wi, ax);
       if (rank == 0 && lane == 0 && warp == wturn) {
-        double* rw = rsum[warp];
         T[i] = tg;
         T[rows + i] = thx;
         wout[i] = wi;
-        rw[0] += loss_val(loss, r1);
+        R[i] = r1;
         if (WITHZ) {
           T[2 * rows + i] = nu;
-          rw[1] += loss_val(loss, r2);
-          const double cv = loss_conj(loss, nu);
-          if (isinf(cv)) rw[3] += 1.0; else rw[2] += cv;
-          rw[4] = fma(bi, nu, rw[4]);
+          R[rows + i] = r2;
         }
       }
       if (++wturn == kHqWarps) wturn = 0;
@@ -857,14 +869,6 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
         if (WITHZ) *reinterpret_cast<double2*>(pc + 2 * n + j) = yn[k];
       }
     }
-    if (rank == 0) {
-      asm volatile("bar.sync %0, %1;" ::"r"(14), "r"(kHqWarps * 32) : "memory");  // all compute warps done
-      if (warp == 0 && lane < 5) {
-        double a = 0.0;
-        for (int w2 = 0; w2 < kHqWarps; ++w2) a += rsum[w2][lane];
-        rowpart[cluster_id * 8 + lane] = a;
-      }
-    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cl.sync();
@@ -875,19 +879,45 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
   }
 }
 
-// fixed-order sum of the per-cluster row sums into out[0..4]
-__global__ void tail_rowsum_kernel(const double* __restrict__ rowpart, int nclusters, double* __restrict__ out,
+// the row sums of the tail (nys_ml_rowwise_f64's out[0..4]) from the stored
+// residuals r1 = Ax - b, r2 = Az - b and nu = T[2]: sum l(r1), sum l(r2),
+// sum l*(nu) finite, #inf, b.nu -- row-parallel, fixed-order reduction
+__global__ void tail_rowsums_kernel(int64_t rows, int loss, const double* __restrict__ R,
+                                    const double* __restrict__ nu, const double* __restrict__ b, int withz,
+                                    double* part, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    v[0] += loss_val(loss, R[i]);
+    if (withz) {
+      v[1] += loss_val(loss, R[rows + i]);
+      const double y = nu[i];
+      const double cv = loss_conj(loss, y);
+      if (isinf(cv)) v[3] += 1.0; else v[2] += cv;
+      v[4] = fma(b[i], y, v[4]);
+    }
+  }
+  __shared__ double sh[5 * 32];
+  block_sum<5>(v, sh);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) part[blockIdx.x * 5 + q] = v[q];
+}
+// (no last-block ticket: the scratch moves with `rows`, so a second tiny
+// kernel sums the block partials in block order)
+__global__ void tail_rowsums_final(const double* __restrict__ part, int nblocks, double* __restrict__ out,
                                    const double* __restrict__ pred) {
   if (pred && *pred != 0.0) return;
   if (threadIdx.x < 5) {
     double a = 0.0;
-    for (int c = 0; c < nclusters; ++c) a += rowpart[c * 8 + threadIdx.x];
+    for (int q = 0; q < nblocks; ++q) a += part[q * 5 + threadIdx.x];
     out[threadIdx.x] = a;
   }
 }
+constexpr int kTailSumBlocks = 2 * kNumSMs;
 
 struct TcPlan {
-  int W, KQ, S, nclusters;
+  int C, W, KQ, S, nclusters;
   size_t smem;
   bool ok;
 };
@@ -897,25 +927,28 @@ TcPlan tail_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, 
   p.ok = false;
   static const bool off = getenv("NYS_TAIL_CLUSTER_OFF") != nullptr;
   // whole rows fit the warp-specialised row pass (rowpass.cu) below 12800 columns
-  if (off || n <= 12800 || (lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)x & 15) || rows < 1) return p;
-  p.W = (int)cdiv(cdiv(n, kHcC), 2) * 2;
+  static const int forced_c = getenv("NYS_TAIL_C") ? atoi(getenv("NYS_TAIL_C")) : 0;
+  static const int min_n = getenv("NYS_TAIL_MIN_N") ? atoi(getenv("NYS_TAIL_MIN_N")) : 12801;
+  if (off || n < min_n || (lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)x & 15) || rows < 1) return p;
+  p.C = forced_c == 4 || forced_c == 8 || forced_c == 16 ? forced_c : (n > 12800 ? 16 : 4);
+  p.W = (int)cdiv(cdiv(n, p.C), 2) * 2;
   p.KQ = (int)cdiv(p.W / 2, kHqWarps * 32);
   if (p.KQ > 8) return p;
   const int NV = with_z ? 2 : 1;
-  const size_t fixed = (size_t)kTcNR * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * kHcC * 8 + kHcNT * 8 + 16 + 1024;
+  const size_t fixed = (size_t)kTcNR * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * p.C * 8 + kHcNT * 8 + 16 + 1024;
   p.S = (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / ((size_t)p.W * 8 + 8)));
   if (p.S < 3) return p;
-  p.smem = (size_t)p.S * p.W * 8 + (size_t)kTcNR * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * kHcC * 8 +
+  p.smem = (size_t)p.S * p.W * 8 + (size_t)kTcNR * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * p.C * 8 +
            (size_t)(p.S + kHcNT) * 8 + 16;
   p.ok = true;
   return p;
 }
 
-template <int KQ, bool WITHZ>
+template <int C, int KQ, bool WITHZ>
 static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* x,
                                  const double* z, const double* b, int loss, double* T, double* w, double* P,
-                                 double* rowpart, double* rowsums, cudaStream_t st, const double* pred) {
-  const void* fn = (const void*)tail_cluster_kernel<KQ, WITHZ>;
+                                 double* R, double* rowsums, cudaStream_t st, const double* pred) {
+  const void* fn = (const void*)tail_cluster_kernel<C, KQ, WITHZ>;
   static bool attr = false;
   static int maxc = 0;
   if (!attr) {
@@ -929,28 +962,32 @@ static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kHcC;
+  at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (maxc == 0) {
-    cfg.gridDim = dim3(kHcC * (kNumSMs / kHcC), 1, 1);
+    cfg.gridDim = dim3(C * (kNumSMs / C), 1, 1);
     int mc = 0;
     if (cudaOccupancyMaxActiveClusters(&mc, fn, &cfg) != cudaSuccess || mc < 1) {
       cudaGetLastError();
       return NYS_ERR_UNSUPPORTED;
     }
-    maxc = tmin(mc, kNumSMs / kHcC);
+    maxc = tmin(mc, kNumSMs / C);
   }
   p.nclusters = (int)tmax<int64_t>(1, tmin<int64_t>(maxc, rows));
-  cfg.gridDim = dim3(kHcC * p.nclusters, 1, 1);
+  cfg.gridDim = dim3(C * p.nclusters, 1, 1);
   int W = p.W, S = p.S;
-  if (cudaLaunchKernelEx(&cfg, tail_cluster_kernel<KQ, WITHZ>, A, rows, n, lda, x, z, b, loss, W, S, T, w, P,
-                         rowpart, pred) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, tail_cluster_kernel<C, KQ, WITHZ>, A, rows, n, lda, x, z, b, loss, W, S, T, w, P,
+                         R, pred) != cudaSuccess)
     return NYS_ERR_CUDA;
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
-  tail_rowsum_kernel<<<1, 32, 0, st>>>(rowpart, p.nclusters, rowsums, pred);
+  double* part = R + 2 * rows;
+  const unsigned blocks = (unsigned)tmax<int64_t>(1, tmin<int64_t>(cdiv(rows, 256), kTailSumBlocks));
+  tail_rowsums_kernel<<<blocks, 256, 0, st>>>(rows, loss, R, T + 2 * rows, b, WITHZ ? 1 : 0, part, pred);
+  NYS_CHECK_LAUNCH();
+  tail_rowsums_final<<<1, 32, 0, st>>>(part, (int)blocks, rowsums, pred);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -966,18 +1003,25 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
   TcPlan p = tail_cluster_plan(rows, n, lda, A, x, z != nullptr);
   if (!p.ok) return NYS_ERR_UNSUPPORTED;
   const int K3 = z ? 3 : 2;
-  const size_t need = ws_off + (size_t)(kNumSMs / kHcC) * K3 * n * 8 + (size_t)(kNumSMs / kHcC) * 8 * 8;
+  const size_t ncl = (size_t)(kNumSMs / p.C);
+  const size_t need = ws_off + ncl * K3 * n * 8 + (2 * (size_t)rows + kTailSumBlocks * 5 + 8) * 8;
   if (ws_bytes < need) return NYS_ERR_UNSUPPORTED;
   double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + ws_off);
-  double* rowpart = P + (size_t)(kNumSMs / kHcC) * K3 * n;
+  double* rowpart = P + ncl * K3 * n;  // residuals r1, r2 (2 x rows), then the row-sum scratch
   int rc = NYS_ERR_UNSUPPORTED;
-  switch (p.KQ * 2 + (z ? 1 : 0)) {
-#define NYS_TK(k)                                                                                                  \
-  case 2 * k: rc = tail_cluster_launch_k<k, false>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, rowsums, st, \
-                                                   pred); break;                                                   \
-  case 2 * k + 1: rc = tail_cluster_launch_k<k, true>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, rowsums, \
-                                                      st, pred); break;
-    NYS_TK(1) NYS_TK(2) NYS_TK(3) NYS_TK(4) NYS_TK(5) NYS_TK(6) NYS_TK(7) NYS_TK(8)
+  const int key = (p.C == 16 ? 0 : p.C == 8 ? 1 : 2) * 32 + p.KQ * 2 + (z ? 1 : 0);
+  switch (key) {
+#define NYS_TK(c, ci, k)                                                                                             \
+  case ci * 32 + 2 * k: rc = tail_cluster_launch_k<c, k, false>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, \
+                                                                rowsums, st, pred); break;                          \
+  case ci * 32 + 2 * k + 1: rc = tail_cluster_launch_k<c, k, true>(p, A, rows, n, lda, x, z, b, loss, T, w, P,     \
+                                                                   rowpart, rowsums, st, pred); break;
+    NYS_TK(16, 0, 1) NYS_TK(16, 0, 2) NYS_TK(16, 0, 3) NYS_TK(16, 0, 4) NYS_TK(16, 0, 5) NYS_TK(16, 0, 6)
+    NYS_TK(16, 0, 7) NYS_TK(16, 0, 8)
+    NYS_TK(8, 1, 1) NYS_TK(8, 1, 2) NYS_TK(8, 1, 3) NYS_TK(8, 1, 4) NYS_TK(8, 1, 5) NYS_TK(8, 1, 6) NYS_TK(8, 1, 7)
+    NYS_TK(8, 1, 8)
+    NYS_TK(4, 2, 1) NYS_TK(4, 2, 2) NYS_TK(4, 2, 3) NYS_TK(4, 2, 4) NYS_TK(4, 2, 5) NYS_TK(4, 2, 6) NYS_TK(4, 2, 7)
+    NYS_TK(4, 2, 8)
 #undef NYS_TK
     default: break;
   }
@@ -994,8 +1038,9 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
 // (reduction scratch + per-cluster A^T partials + per-cluster row sums)
 extern "C" size_t nys_tail_cluster_workspace(int64_t rows, int64_t n) {
   (void)rows;
-  const size_t ncl = nys::kNumSMs / nys::kHcC;
-  return (size_t)(nys::kRedPartialsTail * 16 + 64) * sizeof(double) + ncl * 3 * (size_t)n * 8 + ncl * 8 * 8;
+  const size_t ncl = nys::kNumSMs / 4;  // the smallest cluster size a plan picks
+  return (size_t)(nys::kRedPartialsTail * 16 + 64) * sizeof(double) + ncl * 3 * (size_t)n * 8 +
+         (2 * (size_t)rows + nys::kTailSumBlocks * 5 + 8) * 8;
 }
 
 namespace nys {
