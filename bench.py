@@ -228,6 +228,17 @@ def cpu_sample(d, W, K, A_host=None, prefer_reference=True):
     per-iteration marks from its callback).  Returns a dict with the rate
     iterations / (time after setup), the setup time and what ran."""
     A = A_host if A_host is not None else d.A
+    # all host threads for the BLAS, whatever a launcher set (torchrun exports
+    # OMP_NUM_THREADS=1 to every rank)
+    try:
+        from threadpoolctl import threadpool_limits
+
+        _limits = threadpool_limits(limits=os.cpu_count(), user_api="blas")
+        from threadpoolctl import threadpool_info
+
+        threads = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:  # pragma: no cover - threadpoolctl missing
+        _limits, threads = None, None
     mod = _ref_nysopt() if prefer_reference else None
     marks = []
     cb = lambda *a: marks.append(time.perf_counter())
@@ -257,12 +268,15 @@ def cpu_sample(d, W, K, A_host=None, prefer_reference=True):
         res = port.solve(prob, o)
         setup = res.setup_s
         its = res.iterations
+    if _limits is not None:
+        _limits.restore_original_limits()
     t_setup = t0 + setup
     w = min(W, max(0, len(marks) - 1))
     start = marks[w - 1] if w > 0 else t_setup
     timed = len(marks) - w
     el = marks[-1] - start if timed > 0 else float("nan")
     return {"value": timed / el if timed > 0 else None, "kind": kind, "setup_s": setup, "timed_iters": timed,
+            "threads": threads,
             "untimed_iters": w, "timed_s": el, "s_per_iter": el / timed if timed > 0 else None,
             "iterations_run": its}
 
@@ -340,7 +354,8 @@ def run_reference(args):
         "steps": K, "warmup": W, "ms_per_step": 1e3 * r["s_per_iter"] if r["s_per_iter"] else None,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(cfg, d, world) if cfg != 5 else config_block(5, _cfg5_desc(), world),
-        "cpu_baseline": {"value": r["value"], "unit": "iters/s", "cores": hi.get("blas_threads", os.cpu_count()),
+        "cpu_baseline": {"value": r["value"], "unit": "iters/s",
+                         "cores": r.get("threads") or hi.get("blas_threads", os.cpu_count()),
                          "kind": r["kind"],
                          "sample": f"{sample_note}one setup ({r['setup_s']:.1f} s), then {r['untimed_iters']} "
                                    f"untimed + {r['timed_iters']} timed ADMM iterations (one step = one "
@@ -550,7 +565,7 @@ def run_ours(args):
         W, K = CPU_SAMPLE
         r = cpu_sample(d, W, K, A_host=A_host)
         hi = host_info()
-        cpu = {"value": r["value"], "unit": "iters/s", "cores": hi.get("blas_threads", os.cpu_count()),
+        cpu = {"value": r["value"], "unit": "iters/s", "cores": r.get("threads") or hi.get("blas_threads", os.cpu_count()),
                "kind": r["kind"], "setup_s": r["setup_s"], "host": hi,
                "sample": f"config {cfg}: one setup ({r['setup_s']:.1f} s), then {r['untimed_iters']} untimed + "
                          f"{r['timed_iters']} timed ADMM iterations ({r['timed_s']:.1f} s), iterations / time "
