@@ -269,6 +269,14 @@ typedef struct nys_admm_tail {
                                  rb_tag != 0 is then stored at rb_dst[rb_n] once the block
                                  is complete (the host may poll it instead of an event)   */
   int rb_done;                /* out: 1 when the tail did that readback                  */
+  /* device-side termination (admm.py:227-240 with problems.py:335-351): when
+   * stop_on, the fused ML epilogue's last CTA evaluates the stop test from the
+   * reduced norms and row sums exactly as the host does, stores 1.0 / 0.0 at
+   * norms[stop_slot], and leaves the next iteration's gate closed when the
+   * test holds (an iteration launched ahead then does nothing); stop_ran
+   * (out) tells whether this launch ran the device test */
+  int stop_on, stop_gap, stop_linf, stop_slot, stop_ran;
+  double stop_eps_gap, stop_eps_abs, stop_eps_rel, stop_sqrt_n;
 } nys_admm_tail;
 int nys_admm_tail_f64(const nys_admm_tail* t, void* stream);
 

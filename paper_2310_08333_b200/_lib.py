@@ -75,6 +75,9 @@ class AdmmTail(C.Structure):
         ("pred", P), ("gate_next", P), ("conj_out", P), ("order", P), ("zu_done", C.c_int),
         ("reduce", P), ("reduce_user", P),
         ("rb_src", P), ("rb_dst", P), ("rb_n", I64), ("rb_gate", P), ("rb_tag", F64), ("rb_done", C.c_int),
+        ("stop_on", C.c_int), ("stop_gap", C.c_int), ("stop_linf", C.c_int), ("stop_slot", C.c_int),
+        ("stop_ran", C.c_int),
+        ("stop_eps_gap", F64), ("stop_eps_abs", F64), ("stop_eps_rel", F64), ("stop_sqrt_n", F64),
     ]
 
 # nys_reduce_fn (include/nysgpu.h): the host-side all-reduce hook of the sharded drivers

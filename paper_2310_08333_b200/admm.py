@@ -213,6 +213,7 @@ _S_INF = 33  # 6 (QP infeasibility pieces)
 _S_PDX = 39  # 1 (||P dx||^2)
 _S_CONJ = 40  # 3 (scaled conjugate sums)
 _S_DUAL = 44  # 2 (penalty change)
+_S_STOP = 46  # 1 (the device's termination decision, nys_admm_tail.stop_slot)
 _S_LEN = 48
 # device readback block: row sums (8) | CG scalars (16) | stats (_S_LEN)
 _RB_LEN = 8 + 16 + _S_LEN
@@ -239,6 +240,7 @@ class _Issued:
     reissue: Optional["_Issued"] = None
     polled: bool = False  # the readback block carries tag `tag` (no stream event to wait on)
     ring: bool = False    # iteration time from the per-iteration mark ring (no ev[0], ev[2])
+    dev_stop: bool = False  # the tail ran the device stop test (it closes k+1's gate when it holds)
 
 
 class _ParityWork:
@@ -492,6 +494,16 @@ class _Engine:
         lookahead = (self.fast and opts.custom_stop is None and not opts.record_iterates
                      and not opts.track_averaged_objective and os.environ.get("NYS_LOOKAHEAD", "1") != "0")
         pending: Optional[_Issued] = None
+        # device-side termination (admm.py:227-240): the fused ML epilogue runs the
+        # stop test itself and keeps the gate of an iteration launched ahead closed,
+        # so a solve that stops at k never executes k+1 (no rollback)
+        if lookahead and self.is_ml and not self.shard.sharded and os.environ.get("NYS_DEVICE_STOP", "1") != "0":
+            for t in self._tails:
+                t.stop_on, t.stop_gap = 1, 1 if self.use_gap else 0
+                t.stop_linf = 1 if opts.norm_kind == "linf" else 0
+                t.stop_slot = _S_STOP
+                t.stop_eps_gap, t.stop_eps_abs, t.stop_eps_rel = opts.eps_dual_gap, opts.eps_abs, opts.eps_rel
+                t.stop_sqrt_n = math.sqrt(n)
 
         timings = Timings()
         r_sk = opts.sketch_rank or default_sketch_rank(n)
@@ -656,8 +668,19 @@ class _Engine:
             elif self._terminated(res, gap):
                 status = Status.OPTIMAL
                 if pending is not None:
-                    self._rollback()
+                    if it.dev_stop and st[_S_STOP] == 1.0:
+                        pending = None  # the device kept k+1's gate closed: k+1 did nothing
+                    else:
+                        self._rollback()
                 break
+            if self.fast and it.dev_stop and st[_S_STOP] == 1.0:
+                # the device stopped where the host continues (not expected: the same
+                # operations on the same values): open k+1's gate, launch it again
+                if os.environ.get("NYS_STOP_DEBUG"):
+                    print(f"device/host stop mismatch at k={k}: gap={gap} res={res}", flush=True)
+                self.gates[(k + 1) % 2] = 1.0
+                if pending is not None:
+                    pending = self._issue(pending.k, pending.shift, pending.win_before, pending.exact)
 
             # windows (admm.py:621-634): commit the speculative append
             self._win_commit(win, spec)
@@ -1067,7 +1090,7 @@ class _Engine:
         else:
             self._readback(par)
         return _Issued(k, par, slot, after, batch, self._seq, shift, exact, list(win_before), polled=polled,
-                       ring=poll)
+                       ring=poll, dev_stop=bool(t.stop_ran))
 
     def _read_block(self):
         """The setup / per-step readback block in one D2H copy; returns
@@ -1082,7 +1105,10 @@ class _Engine:
     def _readback(self, par):
         if self._kernel_readback:
             t = self._tails[par]
-            self.kx.readback(self.rbs[par], self.rbs_host[par], self.gates[1 - par:].data_ptr(), t.pred)
+            # a tail that ran the device stop test already opened (or kept closed)
+            # the next gate: the extra copy must not reopen it
+            gate = None if t.stop_ran else self.gates[1 - par:].data_ptr()
+            self.kx.readback(self.rbs[par], self.rbs_host[par], gate, t.pred)
         else:
             self.rbs_host[par][:_RB_LEN].copy_(self.rbs[par], non_blocking=True)
         self.kx.d2h += _RB_LEN * 8

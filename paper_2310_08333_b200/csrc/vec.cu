@@ -555,6 +555,53 @@ struct SlotList {
   int idx[16];
 };
 
+// the host's termination test (admm.py:_terminated/_gap of the B200 engine,
+// = admm.py:227-240 and problems.py:335-351 of the reference) on the reduced
+// norms `s` (nys_admm_norms_f64 layout) and row sums `rs` (nys_ml_rowwise_f64
+// layout), operation for operation (no contraction), so host and device agree
+struct StopArgs {
+  int on, gap, linf, loss, slot;
+  double eps_gap, eps_abs, eps_rel, sqrt_n, l1, l2;
+};
+
+__device__ bool device_stop(const StopArgs& a, const double* s, const double* rs) {
+  if (a.gap) {
+    const double primal =
+        __dadd_rn(__dadd_rn(rs[1], __dmul_rn(__dmul_rn(0.5, a.l2), s[6])), __dmul_rn(a.l1, s[10]));
+    double conj_sum = rs[2], b_nu = rs[4];
+    const double n_inf = rs[3];
+    if (a.l2 == 0.0) {
+      const double denom = s[13];
+      if (denom > a.l1) {
+        const double c = a.l1 / denom;
+        conj_sum = __dmul_rn(__dmul_rn(conj_sum, c), c);  // square / huber (homogeneous)
+        b_nu = __dmul_rn(b_nu, c);
+      }
+    }
+    if (n_inf > 0.0) return false;  // gap = inf
+    double dual = __dadd_rn(-conj_sum, -b_nu);
+    if (a.l2 > 0.0) dual = __dadd_rn(dual, -(s[14] / __dmul_rn(2.0, a.l2)));
+    if (!isfinite(dual)) return false;
+    const double num = __dadd_rn(primal, -dual);
+    const double den = fmin(primal, fabs(dual));
+    double gap;
+    if (den <= 1e-16) gap = fabs(num) <= 1e-12 ? 0.0 : INFINITY;
+    else gap = num / den;
+    return gap <= a.eps_gap;
+  }
+  double rp, rd, nx, nz, nru;
+  if (a.linf) {
+    rp = s[1], rd = s[3], nx = s[5], nz = s[7], nru = s[9];
+  } else {
+    rp = sqrt(fmax(s[0], 0.0)), rd = sqrt(fmax(s[2], 0.0)), nx = sqrt(fmax(s[4], 0.0));
+    nz = sqrt(fmax(s[6], 0.0)), nru = sqrt(fmax(s[8], 0.0));
+  }
+  const double ps = fmax(fmax(nx, nz), 0.0);
+  const double tp = __dadd_rn(__dmul_rn(a.sqrt_n, a.eps_abs), __dmul_rn(a.eps_rel, ps));
+  const double td = __dadd_rn(__dmul_rn(a.sqrt_n, a.eps_abs), __dmul_rn(a.eps_rel, nru));
+  return rp <= tp && rd <= td;
+}
+
 __global__ void window_norms_kernel(int64_t n, const double* __restrict__ ring, int64_t ld,
                                     int cur, SlotList others, int nothers, double* out,
                                     double* part, unsigned int* counter,
@@ -593,7 +640,7 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
                    double lambda2, double rho, double lambda1, const double* __restrict__ ring, int64_t ld,
                    int cur, SlotList others, int nothers, double* out, int woff, double* part,
                    unsigned int* counter, const double* __restrict__ pred, const double* __restrict__ rb_src,
-                   double* rb_dst, int rb_n, double* rb_gate, double rb_tag) {
+                   double* rb_dst, int rb_n, double* rb_gate, double rb_tag, StopArgs stop) {
   pdl_begin();  // chain kernel (common.cuh)
   // (rb_dst: this kernel ends the iteration's chain and also does the readback of
   // the iteration's scalar block into mapped host memory: nys_readback_f64 fused)
@@ -694,13 +741,23 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
                       woff + 14, woff + 15, woff + 16};
   const int om[7] = {1, 3, 5, 7, 9, 13, 15};
   const bool last = grid_reduce<26, 7>(s, m, part, counter, out, os, om);
+  __shared__ bool s_stop;
+  if (last && stop.on) {
+    __syncthreads();  // the reduced norms are in `out`; the row sums lead the readback block
+    if (threadIdx.x == 0) {
+      s_stop = device_stop(stop, out, rb_src);
+      out[stop.slot] = s_stop ? 1.0 : 0.0;
+    }
+    __syncthreads();
+  }
   if (last && rb_dst) {
     __syncthreads();  // the reduced norms are in the block
     for (int q = threadIdx.x; q < rb_n; q += blockDim.x) rb_dst[q] = rb_src[q];
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (rb_gate) *rb_gate = 1.0;  // the next iteration may run
+      // the next iteration may run -- unless the device stop test held
+      if (rb_gate && !(stop.on && s_stop)) *rb_gate = 1.0;
       // the host polls this tag instead of waiting on a stream event (an event
       // between this kernel and the next x-update would serialise their launches)
       if (rb_tag != 0.0) *(volatile double*)(rb_dst + rb_n) = rb_tag;
@@ -1104,8 +1161,9 @@ int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const doub
 
 extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   if (!t || t->n <= 0 || (t->kind != 0 && t->kind != 1)) return NYS_ERR_ARG;
-  nys_admm_tail* t_mut = const_cast<nys_admm_tail*>(t);  // rb_done is an output
+  nys_admm_tail* t_mut = const_cast<nys_admm_tail*>(t);  // rb_done, stop_ran are outputs
   t_mut->rb_done = 0;
+  t_mut->stop_ran = 0;
   cudaStream_t st = as_stream(stream);
   const int64_t n = t->n;
   const double* pred = t->pred;
@@ -1192,14 +1250,23 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       double* rbg = rb ? t->rb_gate : nullptr;
       const int rbn = (int)t->rb_n;
       const double rbt = t->rb_tag;
+      StopArgs sa{};
+      // the device decision is only valid where this kernel is the iteration's
+      // last (it reads the row sums and opens the gate) and no conjugate-sum
+      // kernel follows (the logistic gap with lambda2 = 0 needs it)
+      sa.on = (t->stop_on && rb && !t->conj_out) ? 1 : 0;
+      sa.gap = t->stop_gap, sa.linf = t->stop_linf, sa.loss = t->loss, sa.slot = t->stop_slot;
+      sa.eps_gap = t->stop_eps_gap, sa.eps_abs = t->stop_eps_abs, sa.eps_rel = t->stop_eps_rel;
+      sa.sqrt_n = t->stop_sqrt_n, sa.l1 = t->lambda1, sa.l2 = t->lambda2;
+      t_mut->stop_ran = sa.on;  // out: whether the device test ran
       if (K == 3)
         launch_chain(ml_epilogue_kernel<3>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
                      t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
-                     pred, rbs, rbd, rbn, rbg, rbt);
+                     pred, rbs, rbd, rbn, rbg, rbt, sa);
       else
         launch_chain(ml_epilogue_kernel<2>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
                      t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
-                     pred, rbs, rbd, rbn, rbg, rbt);
+                     pred, rbs, rbd, rbn, rbg, rbt, sa);
       NYS_CHECK_LAUNCH();
       t_mut->rb_done = rb ? 1 : 0;
     } else {
