@@ -30,6 +30,7 @@ namespace nys {
 constexpr int kCpThreads = 512;
 constexpr int kCpWarps = kCpThreads / 32;
 constexpr int kCpMaxK = 13;            // n <= 13312
+constexpr int kCpMaxSum = (kNumSMs + 31) / 32;  // CTA partials per lane of a fixed-order sum
 constexpr int kCpSmemBudget = 226 * 1024;  // sm_100 per-block maximum less the static shared words
 
 struct CgPersistArgs {
@@ -94,6 +95,9 @@ __device__ __forceinline__ unsigned long long cp_now() {
   return t;
 }
 
+// coefficient arrays in shared memory: r rounded up to an even count
+__host__ __device__ inline int cp_r2(int r) { return r > 0 ? (r + 1) & ~1 : 2; }
+
 __device__ __forceinline__ double cp_tol(const CgPersistArgs& a) { return a.tolp ? *a.tolp : a.tol; }
 
 // the reference's stop test on ||r||^2 (krylov.py:84-88)
@@ -126,7 +130,7 @@ __device__ __forceinline__ double cp_block_sum(double v, double* sh) {
   return warp_sum(lane < kCpWarps ? sh[lane] : 0.0);
 }
 
-template <int K, int MC>
+template <int K>
 __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs a) {
   pdl_begin();  // chain kernel (common.cuh)
   cg::grid_group grid = cg::this_grid();
@@ -136,8 +140,10 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   uint64_t* ubar = full + a.S;                                               // U slice arrival
   double* red = reinterpret_cast<double*>(full + ((a.S + 2) & ~1));          // 2 x 16 (16-B aligned)
   double* sh = red + 32;                                                     // 32
+  const int r2 = cp_r2(a.r);
   double* csh = sh + 32;                                                     // coef (r <= 512)
-  double* ys = csh + 520;                                                    // slice sums
+  double* lnu = csh + r2;                                                    // lam_j + nu
+  double* ys = lnu + r2;                                                     // slice sums
   double* rsl = ys + 112;  // CG residual of the slice: the preconditioner passes read it from here
   double* vrow = rsl + 112;  // QP: the direction at this CTA's rows (p_i of p^T P p)
   double* scr = vrow + 112;                                                  // colsum scratch (1024)
@@ -272,6 +278,9 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
     }
   }
   if (!a.no_early_prefetch) prefetch(last_dir ^ 1);
+  // the preconditioner's denominators lam_j + nu, once per launch (make_coef
+  // then has no global load on its path)
+  for (int j = tid; j < a.r; j += kCpThreads) lnu[j] = __dadd_rn(a.lam[j], a.nu);
   // end of the solve: the speculative first rows of a next pass must land
   // before the CTA exits; record the order of the last pass
   auto finish = [&]() {
@@ -344,11 +353,20 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   auto all_sum2 = [&](int q1, int q2, double& o2) -> double {
     __syncthreads();
     if (warp == 0) {
-      double t1 = 0.0, t2 = 0.0;
-      for (int c = lane; c < nctas; c += 32) {
-        t1 += a.part[c * 8 + q1];
-        t2 += a.part[c * 8 + q2];
+      double v1[kCpMaxSum], v2[kCpMaxSum];  // every load in flight at once
+#pragma unroll
+      for (int u = 0; u < kCpMaxSum; ++u) {
+        const int c = lane + 32 * u;
+        v1[u] = c < nctas ? a.part[c * 8 + q1] : 0.0;
+        v2[u] = c < nctas ? a.part[c * 8 + q2] : 0.0;
       }
+      double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+      for (int u = 0; u < kCpMaxSum; ++u)
+        if (lane + 32 * u < nctas) {
+          t1 += v1[u];
+          t2 += v2[u];
+        }
       t1 = warp_sum(t1);
       t2 = warp_sum(t2);
       if (lane == 0) {
@@ -364,8 +382,16 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   auto all_sum = [&](int q) -> double {
     __syncthreads();
     if (warp == 0) {
+      double v[kCpMaxSum];  // every load in flight at once, summed in CTA order
+#pragma unroll
+      for (int u = 0; u < kCpMaxSum; ++u) {
+        const int c = lane + 32 * u;
+        v[u] = c < nctas ? a.part[c * 8 + q] : 0.0;
+      }
       double t = 0.0;
-      for (int c = lane; c < nctas; c += 32) t += a.part[c * 8 + q];
+#pragma unroll
+      for (int u = 0; u < kCpMaxSum; ++u)
+        if (lane + 32 * u < nctas) t += v[u];
       t = warp_sum(t);
       if (lane == 0) s_bcast = t;
     }
@@ -537,11 +563,11 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
   };
   // every CTA: coef_j = (lam_{r-1}+nu)(h_j/(lam_j+nu)) - h_j into shared memory
   auto make_coef = [&]() {
-    const double lr = a.lam[a.r - 1] + a.nu;
-    colsum(a.hpart, a.r, nctas, 0, a.r, csh);
+    colsum(a.hpart, a.r, nctas, 0, a.r, csh);  // (its barriers order the lnu writes too)
+    const double lr = lnu[a.r - 1];
     for (int j = tid; j < a.r; j += kCpThreads) {
       const double h = csh[j];
-      const double head = __dmul_rn(lr, h / __dadd_rn(a.lam[j], a.nu));
+      const double head = __dmul_rn(lr, h / lnu[j]);
       csh[j] = __dadd_rn(head, -h);
     }
     __syncthreads();
@@ -634,16 +660,26 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
       const double* pold = a.p[pb ^ 1];
       double* pnew = a.p[pb];
       double pp = 0.0;
+      // every load of z and the old direction before the first store of the
+      // new one (the store could alias them: issued in between, each load
+      // would wait for the one before).  (Keeping the whole direction in
+      // registers across iterations instead spills at n = 10000.)
+      double2 po[K];
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const int j = 2 * (tid + kk * kCpThreads);
+        vr[kk] = j < n ? *reinterpret_cast<const double2*>(a.z + j) : make_double2(0.0, 0.0);
+        po[kk] = (j < n && k > 1) ? *reinterpret_cast<const double2*>(pold + j) : make_double2(0.0, 0.0);
+      }
 #pragma unroll
       for (int kk = 0; kk < K; ++kk) {
         const int j = 2 * (tid + kk * kCpThreads);
         if (j < n) {
-          const double2 zz = *reinterpret_cast<const double2*>(a.z + j);
+          const double2 zz = vr[kk];
           double2 v = zz;
           if (k > 1) {
-            const double2 po = *reinterpret_cast<const double2*>(pold + j);
-            v.x = __dadd_rn(zz.x, __dmul_rn(beta, po.x));
-            v.y = __dadd_rn(zz.y, __dmul_rn(beta, po.y));
+            v.x = __dadd_rn(zz.x, __dmul_rn(beta, po[kk].x));
+            v.y = __dadd_rn(zz.y, __dmul_rn(beta, po[kk].y));
           }
           vr[kk] = v;
           pp = fma(v.x, v.x, fma(v.y, v.y, pp));
@@ -779,7 +815,7 @@ __global__ void __launch_bounds__(kCpThreads, 1) cg_persist_kernel(CgPersistArgs
 }
 
 struct CpPlan {
-  int K, MC, W, S, u_smem;
+  int K, W, S, u_smem;
   size_t smem;
   bool ok;
 };
@@ -797,9 +833,9 @@ static CpPlan cp_plan(const nys_cg_problem* pb) {
   if (p.K > kCpMaxK) return p;
   // every slice of n / 148 columns has at most one element per thread (<= 90)
   static_assert(((kCpMaxK * 2 * kCpThreads + kNumSMs - 1) / kNumSMs + 1) <= kCpThreads, "slice");
-  p.MC = pb->r <= 128 ? 4 : (pb->r <= 256 ? 8 : 16);
   const size_t row_bytes = (size_t)p.W * 8;
-  const size_t extra = 64 * 8 + (size_t)(520 + 112 + 112 + 112 + 1024) * 8 + 1024;  // red, sh, csh, slice sums, scratch
+  // red, sh, coef, lam + nu, slice sums, scratch
+  const size_t extra = 64 * 8 + (size_t)(2 * cp_r2(pb->r) + 112 + 112 + 112 + 1024) * 8 + 1024;
   p.S = (int)tmin<int64_t>(4, (kCpSmemBudget - extra) / row_bytes);
   if (p.S < 2) return p;
   p.smem = (size_t)p.S * row_bytes + (size_t)(p.S + 2) * 8 + extra;
@@ -811,10 +847,10 @@ static CpPlan cp_plan(const nys_cg_problem* pb) {
   return p;
 }
 
-template <int K, int MC>
+template <int K>
 static int cp_launch(const CpPlan& pl, const CgPersistArgs& args, cudaStream_t st) {
   static bool attr = false;
-  auto fn = cg_persist_kernel<K, MC>;
+  auto fn = cg_persist_kernel<K>;
   if (!attr) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kCpSmemBudget) != cudaSuccess) {
       cudaGetLastError();
@@ -915,11 +951,9 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
     a.zu.ru = t->ring && t->uring ? t->uring + (int64_t)t->slot * t->ring_ld : nullptr;
   }
   int rc = NYS_ERR_UNSUPPORTED;
-#define NYS_CP(k)                                                    \
-  case k:                                                            \
-    if (pl.MC == 4) rc = cp_launch<k, 4>(pl, a, st);                 \
-    else if (pl.MC == 8) rc = cp_launch<k, 8>(pl, a, st);            \
-    else rc = cp_launch<k, 16>(pl, a, st);                           \
+#define NYS_CP(k)                  \
+  case k:                          \
+    rc = cp_launch<k>(pl, a, st);  \
     break;
   switch (pl.K) {
     NYS_CP(1) NYS_CP(2) NYS_CP(3) NYS_CP(4) NYS_CP(5) NYS_CP(6) NYS_CP(7) NYS_CP(8) NYS_CP(9) NYS_CP(10)

@@ -25,8 +25,11 @@ def main():
     import bench
     import paper_2310_08333_b200 as nys
 
-    d, opts = bench.build_problem(args.config)
-    A = torch.from_numpy(d.P if d.kind == "boxqp" else d.A).cuda()
+    if args.config == 4:
+        d, opts, A = bench.build_cfg4_device(1, 0, False)
+    else:
+        d, opts = bench.build_problem(args.config)
+        A = torch.from_numpy(d.P if d.kind == "boxqp" else d.A).cuda()
     prob = bench.make_gpu_problem(d, A)
     nys.solve(prob, opts)
     torch.cuda.synchronize()
