@@ -614,10 +614,16 @@ int hvp_cluster(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda
 // per-cluster A^T partials P[(c * 3 + j) * n + col] (the layout the ML
 // epilogue sums in a fixed order) and per-cluster row sums (fixed row order):
 //   rowpart[c * 8 + 0..4] = sum l(r1), sum l(r2), sum l*(nu) finite, #inf, b.nu
-constexpr int kTcNR = 2;  // row slots of the lane partials (safe for L = 1: see the Q kernel)
+// L = 1 row between a row's dot and its accumulation (the exchange in
+// flight); L + 1 row slots of lane partials (named barriers 9, 10), S >= L + 2
+// ring stages, kHcNT >= 2 L + 2 total slots (a remote relay can be at most
+// 2 L + 1 rows ahead of this CTA's consumer).  (Measured at 5000 x 10000:
+// L = 2, 3 gain < 2 %; the exchange is not what bounds a row.)
+constexpr int kTcL = 1;
+static_assert(1 + kHqMaxS + kTcL < 16 && kHcNT >= 2 * kTcL + 2, "tail pipeline depth");
 
-// C = CTAs per cluster: 16 for the widest rows (configs 4 and 5), 4 or 8 for
-// rows of 4096-12800 columns (config 2's width)
+// C = CTAs per cluster: 16 for the widest rows (configs 4 and 5), 2, 4 or 8
+// for rows of 4096-12800 columns (config 2's width)
 template <int C>
 __device__ __forceinline__ double cluster_total_c(const double* p, int lane) {
   // lanes 0-15: the x partials of the C CTAs, lanes 16-31: the z partials;
@@ -635,13 +641,13 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
                     int loss, int W, int S, double* __restrict__ T, double* __restrict__ wout,
                     double* __restrict__ P, double* __restrict__ R, const double* __restrict__ pred) {
   static_assert(KQ <= 8, "x and z slices: <= 32 TMEM columns each");
-  constexpr int L = 1;
   constexpr int NV = WITHZ ? 2 : 1;
+  constexpr int L = kTcL, NR = L + 1;
   if (pred && *pred != 0.0) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);                 // S x W
   double* psl = ring + (size_t)S * W;                                 // NR x NV x 448 lane partials
-  double* tsl = psl + kTcNR * NV * kHqWarps * 32;                     // NT x NV x 16 CTA partials
+  double* tsl = psl + NR * NV * kHqWarps * 32;                        // NT x NV x C CTA partials
   uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * NV * C);  // S
   uint64_t* totb = full + S;                                          // NT
   uint32_t* tmem_base = reinterpret_cast<uint32_t*>(totb + kHcNT);
@@ -697,8 +703,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
     // --------------------------------------------------- exchange (relay) --
     // the compute warps leave one partial per lane; this warp reduces them
     // (lane l: the 14 warps' lane-l partials in warp order, then a shuffle tree)
-    for (int g = 0; g < nr; ++g) {
-      const int rs = g % kTcNR;
+    for (int g = 0, rs = 0; g < nr; ++g, rs = rs + 1 == NR ? 0 : rs + 1) {
       qbar_sync(1 + kHqMaxS + rs);
       const int s = g & (kHcNT - 1);
 #pragma unroll
@@ -742,9 +747,14 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
     // of loss values and conjugates run afterwards, row-parallel, in
     // tail_rowsums_kernel); the writer warp rotates (row jt -> warp jt mod 14)
     int wturn = 0;  // jt mod kHqWarps, kept incrementally
-    int qi = 0, pi = 0, qj = 0;
+    int qi = 0, pi = 0, qj = 0, rs = 0;
+    // b of a row is requested at the row's dot and used at its epilogue one
+    // iteration later (L = 1): the load's latency stays off the per-row path
+    double b_ld = 0.0;
     for (int it = 0; it < nr + L; ++it) {
+      const double b_prev = b_ld;
       if (it < nr) {
+        b_ld = __ldg(b + cluster_id + (int64_t)it * nclusters);
         const int q = qi;
         mbar_wait(&full[q], (unsigned)pi);
         if (++qi == S) {
@@ -752,7 +762,6 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
           pi ^= 1;
         }
         const double* row = ring + (size_t)q * W;
-        const int rs = it % kTcNR;
         if (WITHZ) {
           // one pass over the staged row for both dots: a read once per element
           double px = 0.0, pz = 0.0;
@@ -796,6 +805,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
         }
         __syncwarp();
         qbar_arrive(1 + kHqMaxS + rs);
+        if (++rs == NR) rs = 0;
       }
       const int jt = it - L;
       if (jt < 0) continue;
@@ -807,7 +817,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       const double az = WITHZ ? __shfl_sync(0xffffffffu, tot, 16) : 0.0;
       if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kTx);
       const int64_t i = cluster_id + (int64_t)jt * nclusters;
-      const double bi = __ldg(b + i);
+      const double bi = b_prev;
       // loss epilogue of the row (vec.cu ml_rowwise_kernel, same expressions)
       const double r1 = __dadd_rn(ax, -bi);
       double tg, wi, nu = 0.0, r2 = 0.0;
@@ -917,7 +927,7 @@ __global__ void tail_rowsums_final(const double* __restrict__ part, int nblocks,
 constexpr int kTailSumBlocks = 2 * kNumSMs;
 
 struct TcPlan {
-  int C, W, KQ, S, nclusters;
+  int C, W, KQ, S, L, nclusters;
   size_t smem;
   bool ok;
 };
@@ -926,19 +936,33 @@ TcPlan tail_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, 
   TcPlan p{};
   p.ok = false;
   static const bool off = getenv("NYS_TAIL_CLUSTER_OFF") != nullptr;
-  // whole rows fit the warp-specialised row pass (rowpass.cu) below 12800 columns
   static const int forced_c = getenv("NYS_TAIL_C") ? atoi(getenv("NYS_TAIL_C")) : 0;
-  static const int min_n = getenv("NYS_TAIL_MIN_N") ? atoi(getenv("NYS_TAIL_MIN_N")) : 12801;
-  if (off || n < min_n || (lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)x & 15) || rows < 1) return p;
-  p.C = forced_c == 4 || forced_c == 8 || forced_c == 16 ? forced_c : (n > 12800 ? 16 : 4);
+  // a row costs the cluster ~1.1 us of fixed work (exchange, epilogue) on top
+  // of its share of the stream; slices narrower than this lose to the two
+  // streaming passes (measured 5000 x 10000: C = 2 74 us against 131 us for
+  // the row pass + GEMV^T; C = 4 (2500-column slices) 143 us)
+  static const int min_w = getenv("NYS_TAIL_MIN_W") ? atoi(getenv("NYS_TAIL_MIN_W")) : 3500;
+  if (off || (lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)x & 15) || rows < 1) return p;
+  // the smallest cluster whose slices fit the x/z tensor-memory columns
+  // (KQ <= 8: <= 7168 columns per CTA), i.e. the widest slices
+  p.C = 0;
+  if (forced_c == 2 || forced_c == 4 || forced_c == 8 || forced_c == 16) {
+    p.C = forced_c;
+  } else {
+    for (int c = 2; c <= 16 && !p.C; c *= 2)
+      if (cdiv(n, (int64_t)c) <= 8 * kHqWarps * 32 * 2) p.C = c;
+    if (!p.C || cdiv(n, (int64_t)p.C) < min_w) return p;
+  }
+  p.L = kTcL;
   p.W = (int)cdiv(cdiv(n, p.C), 2) * 2;
   p.KQ = (int)cdiv(p.W / 2, kHqWarps * 32);
   if (p.KQ > 8) return p;
   const int NV = with_z ? 2 : 1;
-  const size_t fixed = (size_t)kTcNR * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * p.C * 8 + kHcNT * 8 + 16 + 1024;
-  p.S = (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / ((size_t)p.W * 8 + 8)));
-  if (p.S < 3) return p;
-  p.smem = (size_t)p.S * p.W * 8 + (size_t)kTcNR * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * p.C * 8 +
+  const size_t fixed =
+      (size_t)(p.L + 1) * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * p.C * 8 + kHcNT * 8 + 16 + 1024;
+  p.S = (int)tmin<int64_t>(kHqMaxS, (int64_t)((kHcSmemBudget - fixed) / ((size_t)p.W * 8 + 8)));
+  if (p.S < p.L + 2) return p;
+  p.smem = (size_t)p.S * p.W * 8 + (size_t)(p.L + 1) * NV * kHqWarps * 32 * 8 + (size_t)kHcNT * NV * p.C * 8 +
            (size_t)(p.S + kHcNT) * 8 + 16;
   p.ok = true;
   return p;
@@ -1009,7 +1033,7 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
   double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + ws_off);
   double* rowpart = P + ncl * K3 * n;  // residuals r1, r2 (2 x rows), then the row-sum scratch
   int rc = NYS_ERR_UNSUPPORTED;
-  const int key = (p.C == 16 ? 0 : p.C == 8 ? 1 : 2) * 32 + p.KQ * 2 + (z ? 1 : 0);
+  const int key = (p.C == 16 ? 0 : p.C == 8 ? 1 : p.C == 4 ? 2 : 3) * 32 + p.KQ * 2 + (z ? 1 : 0);
   switch (key) {
 #define NYS_TK(c, ci, k)                                                                                             \
   case ci * 32 + 2 * k: rc = tail_cluster_launch_k<c, k, false>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, \
@@ -1022,6 +1046,8 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
     NYS_TK(8, 1, 8)
     NYS_TK(4, 2, 1) NYS_TK(4, 2, 2) NYS_TK(4, 2, 3) NYS_TK(4, 2, 4) NYS_TK(4, 2, 5) NYS_TK(4, 2, 6) NYS_TK(4, 2, 7)
     NYS_TK(4, 2, 8)
+    NYS_TK(2, 3, 1) NYS_TK(2, 3, 2) NYS_TK(2, 3, 3) NYS_TK(2, 3, 4) NYS_TK(2, 3, 5) NYS_TK(2, 3, 6) NYS_TK(2, 3, 7)
+    NYS_TK(2, 3, 8)
 #undef NYS_TK
     default: break;
   }
@@ -1038,7 +1064,7 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
 // (reduction scratch + per-cluster A^T partials + per-cluster row sums)
 extern "C" size_t nys_tail_cluster_workspace(int64_t rows, int64_t n) {
   (void)rows;
-  const size_t ncl = nys::kNumSMs / 4;  // the smallest cluster size a plan picks
+  const size_t ncl = nys::kNumSMs / 2;  // the smallest cluster size a plan picks
   return (size_t)(nys::kRedPartialsTail * 16 + 64) * sizeof(double) + ncl * 3 * (size_t)n * 8 +
          (2 * (size_t)rows + nys::kTailSumBlocks * 5 + 8) * 8;
 }

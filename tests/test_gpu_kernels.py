@@ -388,11 +388,17 @@ def test_lasso_generated_in_hbm_matches_host(kx, host_b):
     assert np.array_equal(A2.cpu().numpy(), got[100:200]) and np.array_equal(b2, b) and lam2 == lam
 
 
-@pytest.mark.parametrize("rows,n,with_z", [(300, 20000, True), (37, 100000, True), (301, 20002, False),
-                                           (5, 14000, True)])
-def test_ml_tail_one_pass(kx, rows, n, with_z):
-    """The one-pass ADMM tail for wide rows (cluster stream over A): A{x,z}, the
-    loss epilogue and A^T{l', w o Ax, nu} against NumPy (square loss)."""
+@pytest.mark.parametrize("rows,n,with_z,loss", [
+    (300, 20000, True, "square"), (37, 100000, True, "square"), (301, 20002, False, "square"),
+    (5, 14000, True, "square"),
+    # every cluster size: C = 2 (config 2's width; the narrowest slices the plan
+    # takes), 4, 8 and 16, with the logistic epilogue
+    (400, 10000, True, "logistic"), (149, 7000, True, "logistic"), (64, 28000, True, "logistic"),
+    (40, 50000, False, "logistic"), (23, 100000, True, "logistic")])
+def test_ml_tail_one_pass(kx, rows, n, with_z, loss):
+    """The one-pass ADMM tail (cluster stream over A): A{x,z}, the loss epilogue
+    and A^T{l', w o Ax, nu} against NumPy, with the row sums of
+    nys_ml_rowwise_f64 (problems.py:35-111 expressions)."""
     g = np.random.default_rng(rows + n)
     A = g.standard_normal((rows, n)) / np.sqrt(n)
     x, z, b = g.standard_normal(n), g.standard_normal(n), g.standard_normal(rows)
@@ -401,22 +407,33 @@ def test_ml_tail_one_pass(kx, rows, n, with_z):
     K = 3 if with_z else 2
     AT = kx.empty(K, n)
     rs = kx.zeros(8)
-    kx.ml_tail("square", dev(A), dev(x), dev(z) if with_z else None, dev(b), T, w, AT, rs)
-    r1 = A @ x - b
-    tg, thx = r1, A @ x
+    kx.ml_tail(loss, dev(A), dev(x), dev(z) if with_z else None, dev(b), T, w, AT, rs)
+    ax = A @ x
+    r1 = ax - b
+    if loss == "square":
+        tg, wr = r1, np.ones(rows)
+        lval = lambda r: 0.5 * r * r  # noqa: E731
+        conj = lambda y: 0.5 * y * y  # noqa: E731
+    else:
+        expit = lambda t: 1.0 / (1.0 + np.exp(-t))  # noqa: E731
+        tg, wr = expit(r1), expit(r1) * expit(-r1)
+        lval = lambda r: np.logaddexp(0.0, r)  # noqa: E731
+        conj = lambda y: y * np.log(y) + (1.0 - y) * np.log1p(-y)  # noqa: E731
+    thx = wr * ax
     Tn = T.cpu().numpy()
     np.testing.assert_allclose(Tn[0], tg, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(Tn[1], thx, rtol=1e-12, atol=1e-12)
-    np.testing.assert_allclose(w.cpu().numpy(), np.ones(rows))
+    np.testing.assert_allclose(w.cpu().numpy(), wr, rtol=1e-12, atol=1e-14)
     ref = [A.T @ tg, A.T @ thx]
     s = rs.cpu().numpy()
-    assert s[0] == pytest.approx(0.5 * np.sum(r1 * r1), rel=1e-12)
+    assert s[0] == pytest.approx(np.sum(lval(r1)), rel=1e-12)
     if with_z:
-        nu = A @ z - b
+        r2 = A @ z - b
+        nu = r2 if loss == "square" else 1.0 / (1.0 + np.exp(-r2))
         np.testing.assert_allclose(Tn[2], nu, rtol=1e-12, atol=1e-12)
         ref.append(A.T @ nu)
-        assert s[1] == pytest.approx(0.5 * np.sum(nu * nu), rel=1e-12)
-        assert s[2] == pytest.approx(0.5 * np.sum(nu * nu), rel=1e-12)
+        assert s[1] == pytest.approx(np.sum(lval(r2)), rel=1e-12)
+        assert s[2] == pytest.approx(np.sum(conj(nu)), rel=1e-11)
         assert s[3] == 0.0
         assert s[4] == pytest.approx(b @ nu, rel=1e-11, abs=1e-11)
     ATn = AT.cpu().numpy()
