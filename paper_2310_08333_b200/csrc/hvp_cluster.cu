@@ -614,11 +614,12 @@ int hvp_cluster(HcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda
 // per-cluster A^T partials P[(c * 3 + j) * n + col] (the layout the ML
 // epilogue sums in a fixed order) and per-cluster row sums (fixed row order):
 //   rowpart[c * 8 + 0..4] = sum l(r1), sum l(r2), sum l*(nu) finite, #inf, b.nu
-// L = 1 row between a row's dot and its accumulation (the exchange in
-// flight); L + 1 row slots of lane partials (named barriers 9, 10), S >= L + 2
-// ring stages, kHcNT >= 2 L + 2 total slots (a remote relay can be at most
-// 2 L + 1 rows ahead of this CTA's consumer).  (Measured at 5000 x 10000:
-// L = 2, 3 gain < 2 %; the exchange is not what bounds a row.)
+// L = 1 row between a row's dot and its accumulation (its exchange overlaps
+// the next row's dot); L + 1 row slots of lane partials (named barriers 9,
+// 10), S >= L + 2 ring stages, kHcNT >= 2 L + 2 total slots (a remote relay
+// can be at most 2 L + 1 rows ahead of this CTA's consumer).  Measured at
+// 5000 x 10000 (C = 2): L = 2, 3 within 2 %; L = 2 with both waits first and
+// dot + epilogue + accumulation as one straight block 7 % slower.
 constexpr int kTcL = 1;
 static_assert(1 + kHqMaxS + kTcL < 16 && kHcNT >= 2 * kTcL + 2, "tail pipeline depth");
 
@@ -634,7 +635,7 @@ __device__ __forceinline__ double cluster_total_c(const double* p, int lane) {
   return v;
 }
 
-template <int C, int KQ, bool WITHZ>
+template <int C, int KQ, bool WITHZ, bool LOGI>
 __global__ void __launch_bounds__(kHqThreads, 1)
 tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
                     const double* __restrict__ x, const double* __restrict__ z, const double* __restrict__ b,
@@ -748,81 +749,64 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
     // tail_rowsums_kernel); the writer warp rotates (row jt -> warp jt mod 14)
     int wturn = 0;  // jt mod kHqWarps, kept incrementally
     int qi = 0, pi = 0, qj = 0, rs = 0;
-    // b of a row is requested at the row's dot and used at its epilogue one
-    // iteration later (L = 1): the load's latency stays off the per-row path
-    double b_ld = 0.0;
-    for (int it = 0; it < nr + L; ++it) {
-      const double b_prev = b_ld;
-      if (it < nr) {
-        b_ld = __ldg(b + cluster_id + (int64_t)it * nclusters);
-        const int q = qi;
-        mbar_wait(&full[q], (unsigned)pi);
-        if (++qi == S) {
-          qi = 0;
-          pi ^= 1;
-        }
-        const double* row = ring + (size_t)q * W;
-        if (WITHZ) {
-          // one pass over the staged row for both dots: a read once per element
-          double px = 0.0, pz = 0.0;
+    // the dots of a staged row with x (and z): lane partials into psl slot rs
+    auto dot = [&](const double* row) {
+      if (WITHZ) {
+        // one pass over the staged row for both dots: a read once per element
+        double px = 0.0, pz = 0.0;
 #pragma unroll
-          for (int k2 = 0; k2 < (KQ + 1) / 2; ++k2) {
-            double2 cx[2], cz[2];
-            tmem_ld8x2(tv + 8 * k2, tv + 32 + 8 * k2, cx, cz);
+        for (int k2 = 0; k2 < (KQ + 1) / 2; ++k2) {
+          double2 cx[2], cz[2];
+          tmem_ld8x2(tv + 8 * k2, tv + 32 + 8 * k2, cx, cz);
 #pragma unroll
-            for (int k1 = 0; k1 < 2; ++k1) {
-              const int k = 2 * k2 + k1;
-              if (k < KQ) {  // compile-time; out-of-range columns: x = z = 0 in TMEM, a read clamped
-                const double2 a = *reinterpret_cast<const double2*>(row + tmin(2 * (tid + k * kHqWarps * 32), jmax));
-                px = fma(a.x, cx[k1].x, px);
-                px = fma(a.y, cx[k1].y, px);
-                pz = fma(a.x, cz[k1].x, pz);
-                pz = fma(a.y, cz[k1].y, pz);
-              }
+          for (int k1 = 0; k1 < 2; ++k1) {
+            const int k = 2 * k2 + k1;
+            if (k < KQ) {  // compile-time; out-of-range columns: x = z = 0 in TMEM, a read clamped
+              const double2 a = *reinterpret_cast<const double2*>(row + tmin(2 * (tid + k * kHqWarps * 32), jmax));
+              px = fma(a.x, cx[k1].x, px);
+              px = fma(a.y, cx[k1].y, px);
+              pz = fma(a.x, cz[k1].x, pz);
+              pz = fma(a.y, cz[k1].y, pz);
             }
           }
-          psl[((rs * NV) * kHqWarps + warp) * 32 + lane] = px;
-          psl[((rs * NV + 1) * kHqWarps + warp) * 32 + lane] = pz;
-        } else {
-          double pt = 0.0;
+        }
+        psl[((rs * NV) * kHqWarps + warp) * 32 + lane] = px;
+        psl[((rs * NV + 1) * kHqWarps + warp) * 32 + lane] = pz;
+      } else {
+        double pt = 0.0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (4 * h >= KQ) continue;
-            double2 c[4];
-            tmem_ld16(tv + 16 * h, c);
+        for (int h = 0; h < 2; ++h) {
+          if (4 * h >= KQ) continue;
+          double2 c[4];
+          tmem_ld16(tv + 16 * h, c);
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
-              const int k = 4 * h + k4;
-              const int j = 2 * (tid + k * kHqWarps * 32);
-              if (k < KQ && j < w_here) {
-                const double2 a = *reinterpret_cast<const double2*>(row + j);
-                pt = fma(a.x, c[k4].x, pt);
-                pt = fma(a.y, c[k4].y, pt);
-              }
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int k = 4 * h + k4;
+            if (k < KQ) {
+              const double2 a = *reinterpret_cast<const double2*>(row + tmin(2 * (tid + k * kHqWarps * 32), jmax));
+              pt = fma(a.x, c[k4].x, pt);
+              pt = fma(a.y, c[k4].y, pt);
             }
           }
-          psl[((rs * NV) * kHqWarps + warp) * 32 + lane] = pt;
         }
-        __syncwarp();
-        qbar_arrive(1 + kHqMaxS + rs);
-        if (++rs == NR) rs = 0;
+        psl[((rs * NV) * kHqWarps + warp) * 32 + lane] = pt;
       }
-      const int jt = it - L;
-      if (jt < 0) continue;
+    };
+    // row jt: the cluster totals (landed in tsl), the loss epilogue of the row
+    // (vec.cu ml_rowwise_kernel, same expressions), the writer's stores and the
+    // A^T accumulation from the still-staged row
+    auto epi_acc = [&](int jt, double bi, const double* row) {
       const int s = jt & (kHcNT - 1);
-      mbar_wait(&totb[s], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire (no L1 invalidation)
       // lanes 0-15: the x partials, 16-31: the z partials (fixed-order trees)
       const double tot = cluster_total_c<C>(tsl + (s * NV) * C, WITHZ ? lane : (lane & 15));
       const double ax = __shfl_sync(0xffffffffu, tot, 0);
       const double az = WITHZ ? __shfl_sync(0xffffffffu, tot, 16) : 0.0;
       if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kTx);
       const int64_t i = cluster_id + (int64_t)jt * nclusters;
-      const double bi = b_prev;
-      // loss epilogue of the row (vec.cu ml_rowwise_kernel, same expressions)
       const double r1 = __dadd_rn(ax, -bi);
       double tg, wi, nu = 0.0, r2 = 0.0;
       if (WITHZ) r2 = __dadd_rn(az, -bi);
-      if (loss == NYS_LOSS_LOGISTIC) {
+      if constexpr (LOGI) {
         // the three sigmoids of the row, one per lane (lanes 0, 1, 2: expit(r1),
         // expit(-r1), expit(r2)), gathered by shuffles: one FP64 exp/div chain
         // per warp instead of four (same expressions, same bits)
@@ -848,9 +832,6 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
         }
       }
       if (++wturn == kHqWarps) wturn = 0;
-      const int q = qj;
-      if (++qj == S) qj = 0;
-      const double* row = ring + (size_t)q * W;
       // branch-free: columns past the segment accumulate into registers that are
       // never stored (reads clamped to the staged row)
 #pragma unroll
@@ -865,6 +846,44 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
           yn[k].y = fma(nu, a.y, yn[k].y);
         }
       }
+    };
+    auto wait_row = [&]() -> const double* {
+      const int q = qi;
+      mbar_wait(&full[q], (unsigned)pi);
+      if (++qi == S) {
+        qi = 0;
+        pi ^= 1;
+      }
+      return ring + (size_t)q * W;
+    };
+    auto dot_done = [&]() {
+      __syncwarp();
+      qbar_arrive(1 + kHqMaxS + rs);
+      if (++rs == NR) rs = 0;
+    };
+    auto acc_row = [&]() -> int {  // ring slot of the row accumulated next
+      const int q = qj;
+      if (++qj == S) qj = 0;
+      return q;
+    };
+    // b of a row is requested at the row's dot and used at its epilogue L
+    // iterations later: the load's latency stays off the per-row path
+    double bq[L + 1];
+#pragma unroll
+    for (int u = 0; u <= L; ++u) bq[u] = 0.0;
+    for (int it = 0; it < nr + L; ++it) {
+#pragma unroll
+      for (int u = L; u > 0; --u) bq[u] = bq[u - 1];  // bq[L]: b of row it - L
+      if (it < nr) {
+        bq[0] = __ldg(b + cluster_id + (int64_t)it * nclusters);
+        dot(wait_row());
+        dot_done();
+      }
+      const int jt = it - L;
+      if (jt < 0) continue;
+      mbar_wait(&totb[jt & (kHcNT - 1)], (unsigned)((jt / kHcNT) & 1));  // st.async complete_tx: CTA-scope acquire
+      const int q = acc_row();
+      epi_acc(jt, bq[L], ring + (size_t)q * W);
       __syncwarp();
       qbar_arrive(1 + q);
     }
@@ -968,11 +987,11 @@ TcPlan tail_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, 
   return p;
 }
 
-template <int C, int KQ, bool WITHZ>
+template <int C, int KQ, bool WITHZ, bool LOGI>
 static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* x,
                                  const double* z, const double* b, int loss, double* T, double* w, double* P,
                                  double* R, double* rowsums, cudaStream_t st, const double* pred) {
-  const void* fn = (const void*)tail_cluster_kernel<C, KQ, WITHZ>;
+  const void* fn = (const void*)tail_cluster_kernel<C, KQ, WITHZ, LOGI>;
   static bool attr = false;
   static int maxc = 0;
   if (!attr) {
@@ -1003,7 +1022,7 @@ static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64
   p.nclusters = (int)tmax<int64_t>(1, tmin<int64_t>(maxc, rows));
   cfg.gridDim = dim3(C * p.nclusters, 1, 1);
   int W = p.W, S = p.S;
-  if (cudaLaunchKernelEx(&cfg, tail_cluster_kernel<C, KQ, WITHZ>, A, rows, n, lda, x, z, b, loss, W, S, T, w, P,
+  if (cudaLaunchKernelEx(&cfg, tail_cluster_kernel<C, KQ, WITHZ, LOGI>, A, rows, n, lda, x, z, b, loss, W, S, T, w, P,
                          R, pred) != cudaSuccess)
     return NYS_ERR_CUDA;
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
@@ -1033,22 +1052,21 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
   double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + ws_off);
   double* rowpart = P + ncl * K3 * n;  // residuals r1, r2 (2 x rows), then the row-sum scratch
   int rc = NYS_ERR_UNSUPPORTED;
-  const int key = (p.C == 16 ? 0 : p.C == 8 ? 1 : p.C == 4 ? 2 : 3) * 32 + p.KQ * 2 + (z ? 1 : 0);
+  // slices of >= 3500 columns (the plan's minimum): KQ = 4 .. 8
+  const bool logi = loss == NYS_LOSS_LOGISTIC;
+  const int key = ((p.C == 16 ? 0 : p.C == 8 ? 1 : p.C == 4 ? 2 : 3) * 16 + p.KQ) * 4 + (z ? 2 : 0) + (logi ? 1 : 0);
   switch (key) {
-#define NYS_TK(c, ci, k)                                                                                             \
-  case ci * 32 + 2 * k: rc = tail_cluster_launch_k<c, k, false>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, \
-                                                                rowsums, st, pred); break;                          \
-  case ci * 32 + 2 * k + 1: rc = tail_cluster_launch_k<c, k, true>(p, A, rows, n, lda, x, z, b, loss, T, w, P,     \
-                                                                   rowpart, rowsums, st, pred); break;
-    NYS_TK(16, 0, 1) NYS_TK(16, 0, 2) NYS_TK(16, 0, 3) NYS_TK(16, 0, 4) NYS_TK(16, 0, 5) NYS_TK(16, 0, 6)
-    NYS_TK(16, 0, 7) NYS_TK(16, 0, 8)
-    NYS_TK(8, 1, 1) NYS_TK(8, 1, 2) NYS_TK(8, 1, 3) NYS_TK(8, 1, 4) NYS_TK(8, 1, 5) NYS_TK(8, 1, 6) NYS_TK(8, 1, 7)
-    NYS_TK(8, 1, 8)
-    NYS_TK(4, 2, 1) NYS_TK(4, 2, 2) NYS_TK(4, 2, 3) NYS_TK(4, 2, 4) NYS_TK(4, 2, 5) NYS_TK(4, 2, 6) NYS_TK(4, 2, 7)
-    NYS_TK(4, 2, 8)
-    NYS_TK(2, 3, 1) NYS_TK(2, 3, 2) NYS_TK(2, 3, 3) NYS_TK(2, 3, 4) NYS_TK(2, 3, 5) NYS_TK(2, 3, 6) NYS_TK(2, 3, 7)
-    NYS_TK(2, 3, 8)
+#define NYS_TK1(c, ci, k, zz, lg)                                                                                 \
+  case ((ci * 16 + k) * 4 + (zz ? 2 : 0) + (lg ? 1 : 0)):                                                        \
+    rc = tail_cluster_launch_k<c, k, zz, lg>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, rowsums, st, pred); \
+    break;
+#define NYS_TK(c, ci, k) \
+  NYS_TK1(c, ci, k, false, false) NYS_TK1(c, ci, k, false, true) NYS_TK1(c, ci, k, true, false) NYS_TK1(c, ci, k, true, true)
+#define NYS_TKC(c, ci) NYS_TK(c, ci, 4) NYS_TK(c, ci, 5) NYS_TK(c, ci, 6) NYS_TK(c, ci, 7) NYS_TK(c, ci, 8)
+    NYS_TKC(16, 0) NYS_TKC(8, 1) NYS_TKC(4, 2) NYS_TKC(2, 3)
+#undef NYS_TKC
 #undef NYS_TK
+#undef NYS_TK1
     default: break;
   }
   if (rc == NYS_OK) {
