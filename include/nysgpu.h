@@ -277,6 +277,11 @@ typedef struct nys_admm_tail {
    * (out) tells whether this launch ran the device test */
   int stop_on, stop_gap, stop_linf, stop_slot, stop_ran;
   double stop_eps_gap, stop_eps_abs, stop_eps_rel, stop_sqrt_n;
+  /* NULL, or (square loss, with_z) g_b = A^T b (n): the one-pass cluster tail
+   * then streams two products A^T (A x), A^T (A z) instead of three, and the
+   * epilogue forms A^T (Ax - b) = A^T (A x) - g_b, A^T (Az - b) = A^T (A z) - g_b
+   * (problems.py:227-351 with l'(r) = r, l'' = 1) */
+  const double* gb;
 } nys_admm_tail;
 int nys_admm_tail_f64(const nys_admm_tail* t, void* stream);
 
@@ -448,6 +453,12 @@ size_t nys_tail_cluster_workspace(int64_t rows, int64_t n);
 int nys_ml_tail_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                     const double* b, int loss, double* T, double* w, double* AT, double* rowsums, void* ws,
                     size_t ws_bytes, void* stream);
+/* The same with g_b = A^T b (n): for the square loss with z the cluster stream
+ * then accumulates A^T (A x) and A^T (A z) only (two products instead of three)
+ * and AT = [A^T(Ax) - g_b, A^T(Ax), A^T(Az) - g_b]; other losses ignore g_b. */
+int nys_ml_tail_gb_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
+                       const double* b, int loss, const double* gb, double* T, double* w, double* AT,
+                       double* rowsums, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------- sparse / general-operator engine -- */
 /* CSR data operator (SparseOperator._apply, operators.py:129-131 -- scipy's

@@ -78,6 +78,7 @@ class AdmmTail(C.Structure):
         ("stop_on", C.c_int), ("stop_gap", C.c_int), ("stop_linf", C.c_int), ("stop_slot", C.c_int),
         ("stop_ran", C.c_int),
         ("stop_eps_gap", F64), ("stop_eps_abs", F64), ("stop_eps_rel", F64), ("stop_sqrt_n", F64),
+        ("gb", P),
     ]
 
 # nys_reduce_fn (include/nysgpu.h): the host-side all-reduce hook of the sharded drivers
@@ -155,6 +156,7 @@ SIGNATURES = {
     "nys_syevj_f64": (I32, [I32, P, P, P, P, SZ, P]),
     "nys_tail_cluster_workspace": (SZ, [I64, I64]),
     "nys_ml_tail_f64": (I32, [P, I64, I64, I64, P, P, P, I32, P, P, P, P, P, SZ, P]),
+    "nys_ml_tail_gb_f64": (I32, [P, I64, I64, I64, P, P, P, I32, P, P, P, P, P, P, SZ, P]),
     "nys_csr_spmv_f64": (I32, [I64, P, P, P, P, F64, P, F64, P, P, I32, P]),
     "nys_csr_spmm_f64": (I32, [I64, P, P, P, P, I64, I32, P, P, I64, P]),
     "nys_csr_transpose_workspace": (SZ, [I64, I64]),

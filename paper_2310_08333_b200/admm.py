@@ -286,6 +286,10 @@ class _Engine:
             self.red = kx.zeros(3 * n + _RB_LEN)
             self.AT = self.red[:3 * n].view(3, n)  # gA, hxA, atnu
             self.rb_dev = self.red[3 * n:]
+            # g_b = A^T b for the square loss: the one-pass tail then streams
+            # A^T (A x) and A^T (A z) and subtracts it (nys_admm_tail.gb)
+            self.gb = kx.empty(n) if (self.loss == "square" and not self.shard.sharded) else None
+            self._gb_ready = False
         else:
             qp = gp.qp
             if not isinstance(qp.P, DenseOperator):
@@ -332,7 +336,17 @@ class _Engine:
             kx.ml_rowwise(self.loss, self.AXZ[0], self.AXZ[1] if with_z else None, self.b,
                           self.T[0], self.w, self.T[1], self.T[2] if with_z else None, self.rowsums)
             kT = 3 if with_z else 2
-            kx.gemvT(self.A, self.T[:kT], self.AT[:kT])
+            if self.gb is not None and not self._gb_ready and not with_z:
+                # A^T b rides along as the third product of the setup pass
+                self.T[2].copy_(self.b)
+                kx.gemvT(self.A, self.T[:3], self.AT[:3])
+                self.gb.copy_(self.AT[2])
+                self._gb_ready = True
+            else:
+                kx.gemvT(self.A, self.T[:kT], self.AT[:kT])
+                if self.gb is not None and not self._gb_ready:
+                    kx.gemvT(self.A, self.b.view(1, -1), self.gb.view(1, -1))
+                    self._gb_ready = True
             if self.shard.sharded:
                 self.shard.allreduce(self.red[:3 * self.n + 8])
         else:
@@ -958,6 +972,8 @@ class _Engine:
                 t.with_z = 1 if self.use_gap else 0
                 t.AXZ, t.T, t.w, t.AT = self.AXZ.data_ptr(), self.T.data_ptr(), self.w.data_ptr(), self.AT.data_ptr()
                 t.rowsums = blk.data_ptr()
+                if self.gb is not None and self.use_gap:
+                    t.gb = self.gb.data_ptr()
                 if self.use_gap and self.l2 == 0.0 and self.loss not in ("square", "huber"):
                     t.conj_out = st[_S_CONJ:].data_ptr()
                 wg = kx.workspace("tail_gemv", L.nys_gemv_workspace(rows, n, 2))

@@ -635,13 +635,18 @@ __device__ __forceinline__ double cluster_total_c(const double* p, int lane) {
   return v;
 }
 
-template <int C, int KQ, bool WITHZ, bool LOGI>
+// SQ (square loss with z, g_b = A^T b known): l' = r, l'' = 1, so the three
+// products A^T{Ax - b, Ax, Az - b} follow from two, A^T (A x) and A^T (A z):
+// two axpys per element instead of three; the ML epilogue subtracts g_b
+// (vec.cu ml_epilogue_kernel).  P row 0 is then not written.
+template <int C, int KQ, bool WITHZ, bool LOGI, bool SQ>
 __global__ void __launch_bounds__(kHqThreads, 1)
 tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda,
                     const double* __restrict__ x, const double* __restrict__ z, const double* __restrict__ b,
                     int loss, int W, int S, double* __restrict__ T, double* __restrict__ wout,
                     double* __restrict__ P, double* __restrict__ R, const double* __restrict__ pred) {
   static_assert(KQ <= 8, "x and z slices: <= 32 TMEM columns each");
+  static_assert(!SQ || (WITHZ && !LOGI), "SQ: square loss with z");
   constexpr int NV = WITHZ ? 2 : 1;
   constexpr int L = kTcL, NR = L + 1;
   if (pred && *pred != 0.0) return;
@@ -737,10 +742,11 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
-    double2 yg[KQ], yh[KQ], yn[WITHZ ? KQ : 1];
+    double2 yg[SQ ? 1 : KQ], yh[KQ], yn[WITHZ ? KQ : 1];
+    yg[0] = make_double2(0.0, 0.0);
 #pragma unroll
     for (int k = 0; k < KQ; ++k) {
-      yg[k] = make_double2(0.0, 0.0);
+      if (!SQ) yg[k] = make_double2(0.0, 0.0);
       yh[k] = make_double2(0.0, 0.0);
       if (WITHZ) yn[k] = make_double2(0.0, 0.0);
     }
@@ -815,6 +821,10 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
         tg = __shfl_sync(0xffffffffu, e, 0);
         wi = tg * __shfl_sync(0xffffffffu, e, 1);  // loss_d2 = expit(w) * expit(-w)
         if (WITHZ) nu = __shfl_sync(0xffffffffu, e, 2);
+      } else if constexpr (SQ) {
+        tg = r1;  // problems.py:35-45: l'(r) = r, l''(r) = 1
+        wi = 1.0;
+        nu = r2;
       } else {
         tg = loss_d1(loss, r1);
         wi = loss_d2(loss, r1);
@@ -837,13 +847,16 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
 #pragma unroll
       for (int k = 0; k < KQ; ++k) {
         const double2 a = *reinterpret_cast<const double2*>(row + tmin(2 * (tid + k * kHqWarps * 32), jmax));
-        yg[k].x = fma(tg, a.x, yg[k].x);
-        yg[k].y = fma(tg, a.y, yg[k].y);
-        yh[k].x = fma(thx, a.x, yh[k].x);
+        if (!SQ) {
+          yg[k].x = fma(tg, a.x, yg[k].x);
+          yg[k].y = fma(tg, a.y, yg[k].y);
+        }
+        yh[k].x = fma(thx, a.x, yh[k].x);  // SQ: thx = a_i.x
         yh[k].y = fma(thx, a.y, yh[k].y);
         if (WITHZ) {
-          yn[k].x = fma(nu, a.x, yn[k].x);
-          yn[k].y = fma(nu, a.y, yn[k].y);
+          const double m = SQ ? az : nu;
+          yn[k].x = fma(m, a.x, yn[k].x);
+          yn[k].y = fma(m, a.y, yn[k].y);
         }
       }
     };
@@ -893,7 +906,7 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
     for (int k = 0; k < KQ; ++k) {
       const int j = 2 * (tid + k * kHqWarps * 32);
       if (j < w_here) {
-        *reinterpret_cast<double2*>(pc + j) = yg[k];
+        if (!SQ) *reinterpret_cast<double2*>(pc + j) = yg[SQ ? 0 : k];
         *reinterpret_cast<double2*>(pc + n + j) = yh[k];
         if (WITHZ) *reinterpret_cast<double2*>(pc + 2 * n + j) = yn[k];
       }
@@ -987,11 +1000,11 @@ TcPlan tail_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, 
   return p;
 }
 
-template <int C, int KQ, bool WITHZ, bool LOGI>
+template <int C, int KQ, bool WITHZ, bool LOGI, bool SQ>
 static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* x,
                                  const double* z, const double* b, int loss, double* T, double* w, double* P,
                                  double* R, double* rowsums, cudaStream_t st, const double* pred) {
-  const void* fn = (const void*)tail_cluster_kernel<C, KQ, WITHZ, LOGI>;
+  const void* fn = (const void*)tail_cluster_kernel<C, KQ, WITHZ, LOGI, SQ>;
   static bool attr = false;
   static int maxc = 0;
   if (!attr) {
@@ -1022,7 +1035,7 @@ static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64
   p.nclusters = (int)tmax<int64_t>(1, tmin<int64_t>(maxc, rows));
   cfg.gridDim = dim3(C * p.nclusters, 1, 1);
   int W = p.W, S = p.S;
-  if (cudaLaunchKernelEx(&cfg, tail_cluster_kernel<C, KQ, WITHZ, LOGI>, A, rows, n, lda, x, z, b, loss, W, S, T, w, P,
+  if (cudaLaunchKernelEx(&cfg, tail_cluster_kernel<C, KQ, WITHZ, LOGI, SQ>, A, rows, n, lda, x, z, b, loss, W, S, T, w, P,
                          R, pred) != cudaSuccess)
     return NYS_ERR_CUDA;
   __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
@@ -1039,7 +1052,8 @@ static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64
 // when the shape has no cluster plan (the caller runs the two-pass tail)
 int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                  const double* b, int loss, double* T, double* w, void* ws, size_t ws_bytes, size_t ws_off,
-                 double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out) {
+                 double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out,
+                 const double* gb, int* sq_out) {
   // measured (20000 x 100000): square loss 2.84 ms, logistic 4.29 ms (every
   // warp evaluates the exp-based epilogue of each row) against 4.57 ms for the
   // two passes
@@ -1054,14 +1068,20 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
   int rc = NYS_ERR_UNSUPPORTED;
   // slices of >= 3500 columns (the plan's minimum): KQ = 4 .. 8
   const bool logi = loss == NYS_LOSS_LOGISTIC;
-  const int key = ((p.C == 16 ? 0 : p.C == 8 ? 1 : p.C == 4 ? 2 : 3) * 16 + p.KQ) * 4 + (z ? 2 : 0) + (logi ? 1 : 0);
+  // square loss with z and g_b: two A^T products instead of three (SQ)
+  const bool sq = gb && z && loss == NYS_LOSS_SQUARE;
+  // mode: 0 no z, 1 no z logistic, 2 z, 3 z logistic, 4 z square (SQ)
+  const int mode = sq ? 4 : (z ? 2 : 0) + (logi ? 1 : 0);
+  const int key = ((p.C == 16 ? 0 : p.C == 8 ? 1 : p.C == 4 ? 2 : 3) * 16 + p.KQ) * 8 + mode;
   switch (key) {
-#define NYS_TK1(c, ci, k, zz, lg)                                                                                 \
-  case ((ci * 16 + k) * 4 + (zz ? 2 : 0) + (lg ? 1 : 0)):                                                        \
-    rc = tail_cluster_launch_k<c, k, zz, lg>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, rowsums, st, pred); \
+#define NYS_TK1(c, ci, k, zz, lg, sqq)                                                                              \
+  case ((ci * 16 + k) * 8 + (sqq ? 4 : (zz ? 2 : 0) + (lg ? 1 : 0))):                                               \
+    rc = tail_cluster_launch_k<c, k, zz, lg, sqq>(p, A, rows, n, lda, x, z, b, loss, T, w, P, rowpart, rowsums, st, \
+                                                  pred);                                                            \
     break;
-#define NYS_TK(c, ci, k) \
-  NYS_TK1(c, ci, k, false, false) NYS_TK1(c, ci, k, false, true) NYS_TK1(c, ci, k, true, false) NYS_TK1(c, ci, k, true, true)
+#define NYS_TK(c, ci, k)                                                                                      \
+  NYS_TK1(c, ci, k, false, false, false) NYS_TK1(c, ci, k, false, true, false)                                 \
+  NYS_TK1(c, ci, k, true, false, false) NYS_TK1(c, ci, k, true, true, false) NYS_TK1(c, ci, k, true, false, true)
 #define NYS_TKC(c, ci) NYS_TK(c, ci, 4) NYS_TK(c, ci, 5) NYS_TK(c, ci, 6) NYS_TK(c, ci, 7) NYS_TK(c, ci, 8)
     NYS_TKC(16, 0) NYS_TKC(8, 1) NYS_TKC(4, 2) NYS_TKC(2, 3)
 #undef NYS_TKC
@@ -1072,6 +1092,7 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
   if (rc == NYS_OK) {
     *Pout = P;
     *splits_out = p.nclusters;
+    if (sq_out) *sq_out = sq ? 1 : 0;
   }
   return rc;
 }
@@ -1088,18 +1109,40 @@ extern "C" size_t nys_tail_cluster_workspace(int64_t rows, int64_t n) {
 }
 
 namespace nys {
-// AT[j, c] = sum over clusters of P[(cl * K + j) * n + c], fixed cluster order
+// AT[j, c] = sum over clusters of P[(cl * K + j) * n + c], fixed cluster order;
+// with gb (the SQ tail): AT[0] = AT[1] - gb, AT[2] = (sum of row 2) - gb
 __global__ void tail_partial_sum_kernel(const double* __restrict__ P, int64_t n, int K, int ncl,
-                                        double* __restrict__ AT) {
+                                        double* __restrict__ AT, const double* __restrict__ gb) {
   const int64_t total = n * K;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = t / n, c = t - j * n;
+    const int64_t js = (gb && j == 0) ? 1 : j;
     double a = 0.0;
-    for (int q = 0; q < ncl; ++q) a += P[((int64_t)q * K + j) * n + c];
+    for (int q = 0; q < ncl; ++q) a += P[((int64_t)q * K + js) * n + c];
+    if (gb && j != 1) a = a - gb[c];
     AT[j * n + c] = a;
   }
 }
 }  // namespace nys
+
+static int ml_tail_impl(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
+                        const double* b, int loss, double* T, double* w, double* AT, double* rowsums,
+                        const double* gb, void* ws, size_t ws_bytes, void* stream) {
+  using namespace nys;
+  if (rows <= 0 || n <= 0 || lda < n || loss < 0 || loss > 2) return NYS_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  double* P = nullptr;
+  int splits = 0, sq = 0;
+  const int rc = tail_cluster(A, rows, n, lda, x, z, b, loss, T, w, ws, ws_bytes,
+                              (size_t)(kRedPartialsTail * 16 + 64) * sizeof(double), rowsums, st, nullptr, &P,
+                              &splits, gb, &sq);
+  if (rc) return rc;
+  const int K = z ? 3 : 2;
+  tail_partial_sum_kernel<<<(unsigned)tmin<int64_t>(cdiv(n * K, 256), 4 * kNumSMs), 256, 0, st>>>(
+      P, n, K, splits, AT, sq ? gb : nullptr);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
 
 // The one-pass ML tail on its own (tests and measurement): T = [l'(Ax-b),
 // w o Ax, l'(Az-b)] (3 x rows), w = l''(Ax-b), AT = A^T T (3 x n, 2 x n without
@@ -1108,18 +1151,13 @@ __global__ void tail_partial_sum_kernel(const double* __restrict__ P, int64_t n,
 extern "C" int nys_ml_tail_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x,
                                const double* z, const double* b, int loss, double* T, double* w, double* AT,
                                double* rowsums, void* ws, size_t ws_bytes, void* stream) {
-  using namespace nys;
-  if (rows <= 0 || n <= 0 || lda < n || loss < 0 || loss > 2) return NYS_ERR_ARG;
-  cudaStream_t st = as_stream(stream);
-  double* P = nullptr;
-  int splits = 0;
-  const int rc = tail_cluster(A, rows, n, lda, x, z, b, loss, T, w, ws, ws_bytes,
-                              (size_t)(kRedPartialsTail * 16 + 64) * sizeof(double), rowsums, st, nullptr, &P,
-                              &splits);
-  if (rc) return rc;
-  const int K = z ? 3 : 2;
-  tail_partial_sum_kernel<<<(unsigned)tmin<int64_t>(cdiv(n * K, 256), 4 * kNumSMs), 256, 0, st>>>(P, n, K, splits,
-                                                                                                    AT);
-  NYS_CHECK_LAUNCH();
-  return NYS_OK;
+  return ml_tail_impl(A, rows, n, lda, x, z, b, loss, T, w, AT, rowsums, nullptr, ws, ws_bytes, stream);
+}
+
+// The same with g_b = A^T b: the square loss with z then runs the two-product
+// SQ tail (A^T (A x), A^T (A z); g_b subtracted in the partial sum)
+extern "C" int nys_ml_tail_gb_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x,
+                                  const double* z, const double* b, int loss, const double* gb, double* T, double* w,
+                                  double* AT, double* rowsums, void* ws, size_t ws_bytes, void* stream) {
+  return ml_tail_impl(A, rows, n, lda, x, z, b, loss, T, w, AT, rowsums, gb, ws, ws_bytes, stream);
 }

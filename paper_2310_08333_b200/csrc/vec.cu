@@ -640,7 +640,8 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
                    double lambda2, double rho, double lambda1, const double* __restrict__ ring, int64_t ld,
                    int cur, SlotList others, int nothers, double* out, int woff, double* part,
                    unsigned int* counter, const double* __restrict__ pred, const double* __restrict__ rb_src,
-                   double* rb_dst, int rb_n, double* rb_gate, double rb_tag, StopArgs stop) {
+                   double* rb_dst, int rb_n, double* rb_gate, double rb_tag, StopArgs stop,
+                   const double* __restrict__ gb) {
   pdl_begin();  // chain kernel (common.cuh)
   // (rb_dst: this kernel ends the iteration's chain and also does the readback of
   // the iteration's scalar block into mapped host memory: nys_readback_f64 fused)
@@ -676,14 +677,18 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
       for (int j = 0; j < K; ++j) acc[u][j] = 0.0;
     if (c < n) {
       int q = ch;
+      // gb (the SQ cluster tail, K = 3): row 0 of the partials is not written
+      const int j0 = gb ? 1 : 0;
       for (; q + 12 < splits; q += 16)
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int j = 0; j < K; ++j) acc[u][j] += P[((int64_t)(q + 4 * u) * K + j) * n + c];
+          for (int j = 0; j < K; ++j)
+            if (j >= j0) acc[u][j] += P[((int64_t)(q + 4 * u) * K + j) * n + c];
       for (; q < splits; q += 4)
 #pragma unroll
-        for (int j = 0; j < K; ++j) acc[0][j] += P[((int64_t)q * K + j) * n + c];
+        for (int j = 0; j < K; ++j)
+          if (j >= j0) acc[0][j] += P[((int64_t)q * K + j) * n + c];
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) cs[ch][j][cx] = (acc[0][j] + acc[1][j]) + (acc[2][j] + acc[3][j]);
@@ -692,10 +697,14 @@ ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* 
   if (ch == 0 && c < n) {
     double at[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      at[j] = ((cs[0][j][cx] + cs[1][j][cx]) + cs[2][j][cx]) + cs[3][j][cx];
-      AT[(int64_t)j * n + c] = at[j];
+    for (int j = 0; j < K; ++j) at[j] = ((cs[0][j][cx] + cs[1][j][cx]) + cs[2][j][cx]) + cs[3][j][cx];
+    if (K == 3 && gb) {  // A^T (Ax - b) = A^T (A x) - g_b, A^T (Az - b) = A^T (A z) - g_b
+      const double g = gb[c];
+      at[0] = at[1] - g;
+      at[K - 1] = at[K - 1] - g;
     }
+#pragma unroll
+    for (int j = 0; j < K; ++j) AT[(int64_t)j * n + c] = at[j];
     // admm_norms_kernel, element c (gA = at[0], atnu = at[2])
     const double xi = x[c], zi = z[c], ui = u[c];
     const double rp = __dadd_rn(xi, -zi);
@@ -1153,7 +1162,8 @@ int gemv_t_partials(const double* A, int64_t rows, int64_t n, int64_t lda, const
                     const double* order);
 int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                  const double* b, int loss, double* T, double* w, void* ws, size_t ws_bytes, size_t ws_off,
-                 double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out);
+                 double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out,
+                 const double* gb, int* sq_out);
 int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                const double* b, int loss, double* tg, double* w, double* thx, double* tnu, double* rowsums,
                double* part, unsigned int* counter, cudaStream_t st, const double* pred, const double* order);
@@ -1194,11 +1204,11 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
     // wide rows: the whole tail's data passes in one cluster stream over A
     // (hvp_cluster.cu: tail_cluster_kernel); else the row pass + GEMV^T below
     double* Pc = nullptr;
-    int csplits = 0;
+    int csplits = 0, csq = 0;
     if (fuse0) {
       rc = tail_cluster(t->A, t->rows, n, t->lda, x, t->with_z ? z : nullptr, t->b, t->loss, t->T, t->w, t->ws_gemvT,
                         t->ws_gemvT_bytes, (kRedPartials * 16 + 64) * sizeof(double), t->rowsums, st, pred, &Pc,
-                        &csplits);
+                        &csplits, t->gb, &csq);
       if (rc != NYS_OK && rc != NYS_ERR_UNSUPPORTED) return rc;
       if (rc != NYS_OK) Pc = nullptr;
     }
@@ -1262,11 +1272,11 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       if (K == 3)
         launch_chain(ml_epilogue_kernel<3>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
                      t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
-                     pred, rbs, rbd, rbn, rbg, rbt, sa);
+                     pred, rbs, rbd, rbn, rbg, rbt, sa, (Pc && csq) ? t->gb : nullptr);
       else
         launch_chain(ml_epilogue_kernel<2>, dim3(eb), dim3(256), 0, st, false, n, Pc, splits, t->AT, x, z, uc,
                      t->lambda2, t->rho, t->lambda1, ringc, t->ring_ld, t->slot, sl, no, normsp, (int)woff, rp, rc2,
-                     pred, rbs, rbd, rbn, rbg, rbt, sa);
+                     pred, rbs, rbd, rbn, rbg, rbt, sa, nullptr);
       NYS_CHECK_LAUNCH();
       t_mut->rb_done = rb ? 1 : 0;
     } else {

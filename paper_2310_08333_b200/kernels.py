@@ -390,15 +390,22 @@ class Kernels:
         check(self.L.nys_syevj_f64(s, A.data_ptr(), V.data_ptr(), w.data_ptr(), ws.data_ptr(), ws.numel(),
                                    self.sp), "syevj")
 
-    def ml_tail(self, loss, A, x, z, b, T, w, AT, rowsums) -> None:
-        """One-pass A{x,z} + loss epilogue + A^T{...} for wide rows (cluster tail)."""
+    def ml_tail(self, loss, A, x, z, b, T, w, AT, rowsums, gb=None) -> None:
+        """One-pass A{x,z} + loss epilogue + A^T{...} for wide rows (cluster tail);
+        with gb = A^T b the square loss streams two products instead of three."""
         rows, n = A.shape
         ws = self.workspace("tail_gemvT", self.L.nys_tail_cluster_workspace(rows, n))
         self.launches += 1
         e = self._t0("ml_tail")
-        check(self.L.nys_ml_tail_f64(A.data_ptr(), rows, n, A.stride(0), x.data_ptr(), _p(z), b.data_ptr(),
-                                     _lib.LOSS[loss], T.data_ptr(), w.data_ptr(), AT.data_ptr(), rowsums.data_ptr(),
-                                     ws.data_ptr(), ws.numel(), self.sp), "ml_tail")
+        if gb is None:
+            check(self.L.nys_ml_tail_f64(A.data_ptr(), rows, n, A.stride(0), x.data_ptr(), _p(z), b.data_ptr(),
+                                         _lib.LOSS[loss], T.data_ptr(), w.data_ptr(), AT.data_ptr(),
+                                         rowsums.data_ptr(), ws.data_ptr(), ws.numel(), self.sp), "ml_tail")
+        else:
+            check(self.L.nys_ml_tail_gb_f64(A.data_ptr(), rows, n, A.stride(0), x.data_ptr(), _p(z), b.data_ptr(),
+                                            _lib.LOSS[loss], gb.data_ptr(), T.data_ptr(), w.data_ptr(),
+                                            AT.data_ptr(), rowsums.data_ptr(), ws.data_ptr(), ws.numel(), self.sp),
+                  "ml_tail")
         self._t1(e)
 
     # ------------------------------------- sparse / general-operator engine --

@@ -439,3 +439,34 @@ def test_ml_tail_one_pass(kx, rows, n, with_z, loss):
     ATn = AT.cpu().numpy()
     for j in range(K):
         np.testing.assert_allclose(ATn[j], ref[j], rtol=1e-11, atol=1e-11 * np.abs(ref[j]).max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,n", [(400, 10000), (149, 7000), (64, 28000), (40, 50000), (23, 100000)])
+def test_ml_tail_square_two_products(kx, rows, n):
+    """The square-loss one-pass tail given g_b = A^T b (nys_ml_tail_gb_f64):
+    two streamed products A^T(Ax), A^T(Az), then A^T(Ax - b) = A^T(Ax) - g_b and
+    A^T(Az - b) = A^T(Az) - g_b, against NumPy; every cluster size (2, 4, 8, 16)
+    and both halves of the row outputs."""
+    g = np.random.default_rng(7 * rows + n)
+    A = g.standard_normal((rows, n)) / np.sqrt(n)
+    x, z, b = g.standard_normal(n), g.standard_normal(n), g.standard_normal(rows)
+    T, w, AT, rs = kx.empty(3, rows), kx.empty(rows), kx.empty(3, n), kx.zeros(8)
+    gb = dev(A.T @ b)
+    kx.ml_tail("square", dev(A), dev(x), dev(z), dev(b), T, w, AT, rs, gb=gb)
+    ax, az = A @ x, A @ z
+    r1, r2 = ax - b, az - b
+    Tn = T.cpu().numpy()
+    np.testing.assert_allclose(Tn[0], r1, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(Tn[1], ax, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(Tn[2], r2, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(w.cpu().numpy(), np.ones(rows))
+    s = rs.cpu().numpy()
+    assert s[0] == pytest.approx(0.5 * r1 @ r1, rel=1e-12)
+    assert s[1] == pytest.approx(0.5 * r2 @ r2, rel=1e-12)
+    assert s[4] == pytest.approx(b @ r2, rel=1e-11, abs=1e-11)
+    ATn = AT.cpu().numpy()
+    for j, ref in enumerate((A.T @ r1, A.T @ ax, A.T @ r2)):
+        # the difference of two products: absolute error at the scale of the products
+        scale = max(np.abs(A.T @ ax).max(), np.abs(A.T @ b).max(), np.abs(A.T @ az).max())
+        np.testing.assert_allclose(ATn[j], ref, rtol=0, atol=1e-12 * scale)

@@ -21,4 +21,4 @@ pr.enable()
 nys.solve(prob, opts)
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(25)
+st.sort_stats("tottime").print_stats(45)

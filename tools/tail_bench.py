@@ -24,8 +24,15 @@ rs = kx.zeros(8)
 AXZ = kx.empty(2, rows)
 
 
+gb = kx.empty(n).normal_()
+
+
 def fused():
     kx.ml_tail(LOSS, A, XZ[0], XZ[1], b, T, w, AT, rs)
+
+
+def fused_gb():
+    kx.ml_tail(LOSS, A, XZ[0], XZ[1], b, T, w, AT, rs, gb=gb)
 
 
 def split():
@@ -34,7 +41,7 @@ def split():
     kx.gemvT(A, T, AT)
 
 
-for name, f in (("cluster tail", fused), ("gemv_n + rowwise + gemv_t", split)):
+for name, f in (("cluster tail", fused), ("cluster tail with g_b", fused_gb), ("gemv_n + rowwise + gemv_t", split)):
     for _ in range(3):
         f()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
