@@ -27,6 +27,15 @@ NYS_ERR_UNSUPPORTED = 6
 NYS_ERR_WORKSPACE = 7
 NYS_ERR_NO_DEVICE = 8
 
+def dev_env(name, default=None):
+    """Development switch ``name`` (an ``NYS_*`` A/B variable of DESIGN.md §5):
+    honoured only when ``NYS_DEV_SWITCHES=1`` is set as well; otherwise the
+    default (the measured-best choice) applies and the environment is ignored."""
+    if os.environ.get("NYS_DEV_SWITCHES") == "1":
+        return os.environ.get(name, default)
+    return default
+
+
 LOSS = {"square": 0, "logistic": 1, "huber": 2}
 PROX_SOFT, PROX_BOX = 0, 1
 

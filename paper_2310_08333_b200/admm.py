@@ -511,7 +511,7 @@ class _Engine:
         # device-side termination (admm.py:227-240): the fused ML epilogue runs the
         # stop test itself and keeps the gate of an iteration launched ahead closed,
         # so a solve that stops at k never executes k+1 (no rollback)
-        if lookahead and self.is_ml and not self.shard.sharded and os.environ.get("NYS_DEVICE_STOP", "1") != "0":
+        if lookahead and self.is_ml and not self.shard.sharded and _lib.dev_env("NYS_DEVICE_STOP", "1") != "0":
             for t in self._tails:
                 t.stop_on, t.stop_gap = 1, 1 if self.use_gap else 0
                 t.stop_linf = 1 if opts.norm_kind == "linf" else 0
@@ -690,7 +690,7 @@ class _Engine:
             if self.fast and it.dev_stop and st[_S_STOP] == 1.0:
                 # the device stopped where the host continues (not expected: the same
                 # operations on the same values): open k+1's gate, launch it again
-                if os.environ.get("NYS_STOP_DEBUG"):
+                if _lib.dev_env("NYS_STOP_DEBUG", None):
                     print(f"device/host stop mismatch at k={k}: gap={gap} res={res}", flush=True)
                 self.gates[(k + 1) % 2] = 1.0
                 if pending is not None:
@@ -905,7 +905,7 @@ class _Engine:
         # pinned host memory is device-addressable under UVA: a kernel writes the
         # readback block straight into it (no copy engine in the pipeline)
         self._kernel_readback = (hasattr(kx, "readback") and kx.device.type == "cuda"
-                                 and os.environ.get("NYS_KERNEL_READBACK", "1") != "0")
+                                 and _lib.dev_env("NYS_KERNEL_READBACK", "1") != "0")
         self.gates = kx.zeros(2)
         self.gates[1] = 1.0  # iteration 1 (parity 1) may run
         self.tols = kx.zeros(2)
@@ -920,12 +920,12 @@ class _Engine:
         # launch gap: measured 2585 vs 2557 iters/s on config 2); the history's
         # linsys_s is then the host wall time between retired iterations, as the
         # reference's per-iteration timings are wall times
-        self._iter_events = int(os.environ.get("NYS_ITER_EVENTS", "0"))
+        self._iter_events = int(_lib.dev_env("NYS_ITER_EVENTS", "0"))
         self._t_retire = None
-        self._fuse_readback = os.environ.get("NYS_FUSE_READBACK", "1") != "0"
+        self._fuse_readback = _lib.dev_env("NYS_FUSE_READBACK", "1") != "0"
         # with the fused readback the host polls the block's completion tag, so no
         # stream event sits between an iteration's last kernel and the next x-update
-        self._poll = self._fuse_readback and os.environ.get("NYS_POLL_READBACK", "1") != "0"
+        self._poll = self._fuse_readback and _lib.dev_env("NYS_POLL_READBACK", "1") != "0"
         self._ev_ring = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         self._seq = 0
         ptr = lambda x: x.data_ptr() if x is not None else None

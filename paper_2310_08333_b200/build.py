@@ -52,6 +52,10 @@ def _needs(obj, src):
 
 GEN = os.path.join(OBJ, "gen")
 NVCC_FLAGS += ["-I", GEN]
+# development library: the NYS_* A/B switches of csrc/ (common.cuh dev_env) are
+# compiled in; rebuild with -f when toggling (objects are cached by mtime only)
+if os.environ.get("NYS_DEV_SWITCHES") == "1":
+    NVCC_FLAGS += ["-DNYS_DEV_SWITCHES"]
 
 
 def build(verbose: bool = False, force: bool = False) -> str:

@@ -823,7 +823,7 @@ struct CpPlan {
 static CpPlan cp_plan(const nys_cg_problem* pb) {
   CpPlan p{};
   p.ok = false;
-  static const bool off = getenv("NYS_CG_PERSIST_OFF") != nullptr;
+  static const bool off = dev_env("NYS_CG_PERSIST_OFF") != nullptr;
   if (off || (pb->op_kind != 0 && !(pb->op_kind == 1 && pb->rows == pb->n)) || pb->rows < kNumSMs ||
       (pb->n & 1) || (pb->lda & 1) ||
       ((uintptr_t)pb->A & 15) || pb->r > 512)
@@ -926,10 +926,10 @@ int cg_persist(const nys_cg_problem* pb, const nys_admm_head* head, void* ws, si
   a.S = pl.S;
   a.has_head = head != nullptr;
   a.u_smem = pl.u_smem;
-  static const int probe = getenv("NYS_CP_PROBE") ? atoi(getenv("NYS_CP_PROBE")) : 0;
+  static const int probe = dev_env("NYS_CP_PROBE") ? atoi(dev_env("NYS_CP_PROBE")) : 0;
   a.probe = probe;
   a.qp = pb->op_kind == 1 ? 1 : 0;
-  static const int nopf = getenv("NYS_CP_NOPREFETCH") ? 1 : 0;
+  static const int nopf = dev_env("NYS_CP_NOPREFETCH") ? 1 : 0;
   a.no_early_prefetch = nopf;
   a.order_in = pb->order_in;
   a.order_out = pb->order_out;

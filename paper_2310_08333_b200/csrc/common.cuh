@@ -14,6 +14,16 @@
 namespace nys {
 // Number of kernels this library has launched (reported as gpu_launches).
 extern unsigned long long g_launches;
+
+// Development switches (the NYS_* environment variables of DESIGN.md §5: forced
+// plans and rejected variants for A/B measurements) exist only in a library
+// built with -DNYS_DEV_SWITCHES (NYS_DEV_SWITCHES=1 python -m ...build -f).
+// The product build reads no environment: every plan is the measured-best one.
+#ifdef NYS_DEV_SWITCHES
+inline const char* dev_env(const char* name) { return getenv(name); }
+#else
+inline const char* dev_env(const char*) { return nullptr; }
+#endif
 }
 
 namespace nys {
@@ -198,7 +208,7 @@ __device__ __forceinline__ void pdl_begin() {
 }
 
 inline bool pdl_enabled() {
-  static const bool on = !(getenv("NYS_PDL") && getenv("NYS_PDL")[0] == '0');
+  static const bool on = !(dev_env("NYS_PDL") && dev_env("NYS_PDL")[0] == '0');
   return on;
 }
 

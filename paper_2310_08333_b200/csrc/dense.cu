@@ -300,7 +300,7 @@ static GemmPlan gemm_plan(int ta, int tb, int64_t M, int64_t N, int64_t K, size_
     }
   }
   if (best.kps == 0) best.kps = K;
-  static const bool dbg = getenv("NYS_GEMM_DEBUG") != nullptr;
+  static const bool dbg = dev_env("NYS_GEMM_DEBUG") != nullptr;
   if (dbg)
     fprintf(stderr, "[nys] gemm %d%d %lldx%lldx%lld: shape %d (%dx%d, occ %d) splits %d kps %lld est %.1f us\n", ta, tb,
             (long long)M, (long long)N, (long long)K, best.shape, kShapes[best.shape].bm, kShapes[best.shape].bn,
@@ -818,7 +818,7 @@ static int orthonormalize(int64_t n, int s, const double* Om, double* Q, void* w
   // Nystrom approximation (H+nu)Q (Q^T (H+nu) Q)^-1 Q^T (H+nu) is invariant to
   // Q -> Q R anyway.  NYS_CHOLQR_PASSES=2 restores CholeskyQR2; the careful
   // (fallback) path always runs two.
-  static const int env_passes = getenv("NYS_CHOLQR_PASSES") ? atoi(getenv("NYS_CHOLQR_PASSES")) : 1;
+  static const int env_passes = dev_env("NYS_CHOLQR_PASSES") ? atoi(dev_env("NYS_CHOLQR_PASSES")) : 1;
   const int passes = careful ? 2 : (env_passes == 2 ? 2 : 1);
   if (passes == 1 && cudaMemsetAsync(info + 1, 0, sizeof(int), st) != cudaSuccess) return NYS_ERR_CUDA;
   int rc;
@@ -1058,12 +1058,12 @@ extern "C" int nys_syevj_f64(int s, double* A, double* V, double* w, void* ws, s
 unsigned long long nys::g_launches = 0ull;
 
 void nys::debug_report(cudaError_t e, const char* file, int line) {
-  static const bool on = getenv("NYS_SYNC_DEBUG") != nullptr;
+  static const bool on = dev_env("NYS_SYNC_DEBUG") != nullptr;
   if (on) fprintf(stderr, "[nys] launch error at %s:%d: %s\n", file, line, cudaGetErrorString(e));
 }
 
 int nys::debug_sync_check(const char* file, int line) {
-  static const bool on = getenv("NYS_SYNC_DEBUG") != nullptr;
+  static const bool on = dev_env("NYS_SYNC_DEBUG") != nullptr;
   if (!on) return 0;
   const cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {

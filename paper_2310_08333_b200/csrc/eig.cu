@@ -366,7 +366,7 @@ static int jacobi2(int s, const double* A, double* V, double* w, void* ws, cudaS
     attr = true;
   }
   const double tol = fmax(1e-15, (double)s * 2.220446049250313e-16);
-  static const bool dbg = getenv("NYS_EIG_DEBUG") != nullptr;
+  static const bool dbg = dev_env("NYS_EIG_DEBUG") != nullptr;
   cudaEvent_t ev[4];
   if (dbg) {
     for (int i = 0; i < 4; ++i) cudaEventCreate(&ev[i]);
@@ -445,7 +445,7 @@ int eig_tri(int s, const double* A, double* V, double* w, void* ws, cudaStream_t
 // s <= 160: tridiagonal path (eig_tri.cu) unless NYS_EIG=jacobi selects the
 // single-CTA two-sided Jacobi (kept for cross-checking)
 static bool use_jacobi_small() {
-  static const bool j = getenv("NYS_EIG") && getenv("NYS_EIG")[0] == 'j';
+  static const bool j = dev_env("NYS_EIG") && dev_env("NYS_EIG")[0] == 'j';
   return j;
 }
 
@@ -493,7 +493,7 @@ int syevj(int s, double* A, double* V, double* w, void* ws, size_t ws_bytes, cud
   cfg.numAttrs = 1;
   // roundoff floor of gamma / sqrt(alpha beta) for s-term dot products
   const double tol = fmax(1e-15, (double)s * 2.220446049250313e-16);
-  static const bool dbg = getenv("NYS_EIG_DEBUG") != nullptr;
+  static const bool dbg = dev_env("NYS_EIG_DEBUG") != nullptr;
   cudaEvent_t e0, e1;
   if (dbg) {
     cudaEventCreate(&e0);

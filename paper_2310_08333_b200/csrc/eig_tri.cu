@@ -707,7 +707,7 @@ int eig_tri(int s, const double* A, double* V, double* w, void* ws, cudaStream_t
     cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  static const bool fused = !getenv("NYS_TRI_FUSED") || atoi(getenv("NYS_TRI_FUSED")) != 0;
+  static const bool fused = !dev_env("NYS_TRI_FUSED") || atoi(dev_env("NYS_TRI_FUSED")) != 0;
   if (fused) {
     static bool fattr = false;
     if (!fattr) {

@@ -163,7 +163,7 @@ static void gemv_n_plan(int64_t rows, int64_t n, int rw, int& splits, int64_t& c
 // register blocking per number of right-hand sides: rows per warp (RW) and
 // 128-bit loads in flight per row (U); overridable for tuning (NYS_GEMV_VARIANT)
 static int gemv_variant(int K) {
-  static const int forced = getenv("NYS_GEMV_VARIANT") ? atoi(getenv("NYS_GEMV_VARIANT")) : -1;
+  static const int forced = dev_env("NYS_GEMV_VARIANT") ? atoi(dev_env("NYS_GEMV_VARIANT")) : -1;
   if (forced >= 0) return forced;
   // measured on B200 (tools/micro.py): k<=2 one row per warp with 4 loads in
   // flight per lane; k=3 two rows x 2 loads; k=4 two rows x 1 load
@@ -369,7 +369,7 @@ __global__ void gemv_t_reduce(const double* __restrict__ P, int64_t n, int K, in
 
 static void gemv_t_plan(int64_t rows, int64_t n, bool vec, int& splits, int64_t& rps) {
   const int64_t strips = cdiv(n, (int64_t)kGemvTThreads * (vec ? 2 : 1));
-  static const int per_sm = getenv("NYS_GEMVT_PER_SM") ? atoi(getenv("NYS_GEMVT_PER_SM")) : 3;  // measured: 3 beats 2, 4, 5, 6 (config 2, +1%)
+  static const int per_sm = dev_env("NYS_GEMVT_PER_SM") ? atoi(dev_env("NYS_GEMVT_PER_SM")) : 3;  // measured: 3 beats 2, 4, 5, 6 (config 2, +1%)
   const int64_t target = (int64_t)kNumSMs * per_sm;
   int64_t sp = strips >= target ? 1 : cdiv(target, strips);
   sp = tmax<int64_t>(1, tmin<int64_t>(sp, cdiv(rows, 64)));
@@ -569,12 +569,12 @@ int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const doubl
               double shift, double* y, double* pAp, int finish, void* ws, size_t ws_bytes, cudaStream_t st,
               const double* pred) {
   if (ws_bytes < hvp_ws(rows, n)) return NYS_ERR_WORKSPACE;
-  static const bool two_pass_only = getenv("NYS_HVP_TWOPASS") != nullptr;
+  static const bool two_pass_only = dev_env("NYS_HVP_TWOPASS") != nullptr;
   const HvpPlan plan = hvp_plan(rows, n, lda, A, v);
   if (plan.ok && !two_pass_only) {
     // single pass over A (csrc/hvp.cu), then a fixed-order sum of the cluster partials
     double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + kRedBytes);
-    static const bool legacy = getenv("NYS_HVP_LEGACY") != nullptr;
+    static const bool legacy = dev_env("NYS_HVP_LEGACY") != nullptr;
     int rc = NYS_ERR_UNSUPPORTED;
     if (plan.C == 1 && !legacy) {
       rc = hvp_row(plan, A, rows, n, lda, d, v, P, y, finish ? shift : 0.0, finish ? pAp : nullptr, red_part(ws),
@@ -608,7 +608,7 @@ int hvp_apply(const double* A, int64_t rows, int64_t n, int64_t lda, const doubl
     }
   }
   // wide rows: column strips over the whole grid, A still streamed once (csrc/hvp_strip.cu)
-  static const bool no_strip = getenv("NYS_HVP_NOSTRIP") != nullptr;
+  static const bool no_strip = dev_env("NYS_HVP_NOSTRIP") != nullptr;
   if (!plan.ok && !two_pass_only && !no_strip) {
     const StripPlan sp = hvp_strip_plan(rows, n, lda, A, v);
     if (sp.ok) {
@@ -693,11 +693,11 @@ extern "C" int nys_hvp_f64(const double* A, int64_t rows, int64_t n, int64_t lda
 extern "C" int nys_hvp_plan(int64_t rows, int64_t n, int64_t lda) {
   if (rows <= 0 || n <= 0 || lda < n) return -1;
   const double* al = reinterpret_cast<const double*>(uintptr_t(256));
-  if (getenv("NYS_HVP_TWOPASS")) return 0;
+  if (dev_env("NYS_HVP_TWOPASS")) return 0;
   const HvpPlan plan = hvp_plan(rows, n, lda, al, al);
-  if (plan.ok) return (plan.C == 1 && !getenv("NYS_HVP_LEGACY")) ? 1 : 2;
+  if (plan.ok) return (plan.C == 1 && !dev_env("NYS_HVP_LEGACY")) ? 1 : 2;
   if (hvp_cluster_plan(rows, n, lda, al, al).ok) return 3;
-  if (!getenv("NYS_HVP_NOSTRIP") && hvp_strip_plan(rows, n, lda, al, al).ok) return 4;
+  if (!dev_env("NYS_HVP_NOSTRIP") && hvp_strip_plan(rows, n, lda, al, al).ok) return 4;
   return 0;
 }
 

@@ -325,7 +325,7 @@ HvpPlan hvp_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const do
   // n = 100000 on B200 (per-row fixed cost ~2 us), so it is opt-in
   // (NYS_HVP_C) until that is fixed; larger n use the two-pass path.
   p.C = 1;
-  static const int forced = getenv("NYS_HVP_C") ? atoi(getenv("NYS_HVP_C")) : 0;
+  static const int forced = dev_env("NYS_HVP_C") ? atoi(dev_env("NYS_HVP_C")) : 0;
   if (forced > 0) p.C = forced;
   if (p.C > 16 || cdiv(cdiv(n, p.C), 2) * 2 > kHvpMaxW) return p;
   p.W = (int)cdiv(cdiv(n, p.C), 2) * 2;

@@ -468,7 +468,7 @@ hvp_cluster_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int6
 HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* v) {
   HcPlan p{};
   p.ok = false;
-  static const bool off = getenv("NYS_HVP_CLUSTER_OFF") != nullptr;
+  static const bool off = dev_env("NYS_HVP_CLUSTER_OFF") != nullptr;
   if (off || (lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)v & 15) || rows < 1) return p;
   p.W = (int)cdiv(cdiv(n, kHcC), 2) * 2;
   p.K = (int)cdiv(p.W / 2, kHcWarps * 32);
@@ -478,13 +478,13 @@ HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, c
   const size_t row_bytes = (size_t)p.W * 8;
   p.S = p.K > 12 ? 0
                  : (int)tmin<int64_t>(kHcMaxS, (int64_t)((kHcSmemBudget - fixed) / (row_bytes + kHcWarps * 256 + 24)));
-  static const bool no_q = getenv("NYS_HVP_CLUSTER_NOQ") != nullptr;
-  static const bool force_q = getenv("NYS_HVP_CLUSTER_Q") != nullptr;
+  static const bool no_q = dev_env("NYS_HVP_CLUSTER_NOQ") != nullptr;
+  static const bool force_q = dev_env("NYS_HVP_CLUSTER_Q") != nullptr;
   if ((p.S < 3 || force_q) && !no_q) {
     // sub-segment plan: the smallest split with >= 4 stages in flight and the
     // y segment (Q x KQ double2 per thread) in registers
     const size_t qfixed = fixed + (size_t)kHqNR * kHqWarps * 32 * 8 + 16;
-    static const int forced_q = getenv("NYS_HVP_CLUSTER_Q") ? atoi(getenv("NYS_HVP_CLUSTER_Q")) : 0;
+    static const int forced_q = dev_env("NYS_HVP_CLUSTER_Q") ? atoi(dev_env("NYS_HVP_CLUSTER_Q")) : 0;
     for (int Q = 2; Q <= 4; ++Q) {
       if (forced_q > 1 && Q != forced_q) continue;
       const int Wq = (int)cdiv(cdiv(p.W, Q), 2) * 2;
@@ -506,7 +506,7 @@ HcPlan hvp_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, c
     return p;
   }
   if (p.S < 3) return p;
-  static const int forced_lag = getenv("NYS_HVP_CLUSTER_LAG") ? atoi(getenv("NYS_HVP_CLUSTER_LAG")) : 0;
+  static const int forced_lag = dev_env("NYS_HVP_CLUSTER_LAG") ? atoi(dev_env("NYS_HVP_CLUSTER_LAG")) : 0;
   // lag 1 measured best on B200 (n = 1e5, S = 4: 2.32 ms vs 2.80 ms at lag 2 -
   // the exchange is sub-microsecond, the extra stage in flight is worth more)
   p.L = forced_lag > 0 ? forced_lag : 1;
@@ -551,7 +551,7 @@ static int hvp_cluster_launch_k(HcPlan& p, const double* A, int64_t rows, int64_
     int mc = 0;
     const cudaError_t oe = cudaOccupancyMaxActiveClusters(&mc, (void*)fn, &cfg);
     if (oe != cudaSuccess || mc < 1) {
-      if (getenv("NYS_HVP_DEBUG"))
+      if (dev_env("NYS_HVP_DEBUG"))
         fprintf(stderr, "hvp_cluster Q=%d K=%d: occupancy %s, %d clusters (smem %zu)\n", Q, K,
                 cudaGetErrorString(oe), mc, p.smem);
       cudaGetLastError();
@@ -967,13 +967,13 @@ struct TcPlan {
 TcPlan tail_cluster_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* x, bool with_z) {
   TcPlan p{};
   p.ok = false;
-  static const bool off = getenv("NYS_TAIL_CLUSTER_OFF") != nullptr;
-  static const int forced_c = getenv("NYS_TAIL_C") ? atoi(getenv("NYS_TAIL_C")) : 0;
+  static const bool off = dev_env("NYS_TAIL_CLUSTER_OFF") != nullptr;
+  static const int forced_c = dev_env("NYS_TAIL_C") ? atoi(dev_env("NYS_TAIL_C")) : 0;
   // a row costs the cluster ~1.1 us of fixed work (exchange, epilogue) on top
   // of its share of the stream; slices narrower than this lose to the two
   // streaming passes (measured 5000 x 10000: C = 2 74 us against 131 us for
   // the row pass + GEMV^T; C = 4 (2500-column slices) 143 us)
-  static const int min_w = getenv("NYS_TAIL_MIN_W") ? atoi(getenv("NYS_TAIL_MIN_W")) : 3500;
+  static const int min_w = dev_env("NYS_TAIL_MIN_W") ? atoi(dev_env("NYS_TAIL_MIN_W")) : 3500;
   if (off || (lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)x & 15) || rows < 1) return p;
   // the smallest cluster whose slices fit the x/z tensor-memory columns
   // (KQ <= 8: <= 7168 columns per CTA), i.e. the widest slices

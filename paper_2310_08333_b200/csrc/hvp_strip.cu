@@ -319,10 +319,10 @@ StripPlan hvp_strip_plan(int64_t rows, int64_t n, int64_t lda, const double* A, 
   // Measured on B200 (tools/hvp_sweep.sh): 4.82 ms vs 5.01 ms for the two-pass
   // path at 20000 x 100000 (W = 676), but 9.4 vs 5.9 ms at 12500 x 200000
   // (W = 1352: fewer rows fit the ring, so less exchange latency is hidden).
-  static const bool force = getenv("NYS_STRIP_FORCE") != nullptr;
+  static const bool force = dev_env("NYS_STRIP_FORCE") != nullptr;
   if (p.W > 800 && !force) return p;
   // column parts per row: keep K = double2 per lane <= 16; WPR = 1 gives 8 rows per stage
-  static const int forced_wpr = getenv("NYS_STRIP_WPR") ? atoi(getenv("NYS_STRIP_WPR")) : 0;
+  static const int forced_wpr = dev_env("NYS_STRIP_WPR") ? atoi(dev_env("NYS_STRIP_WPR")) : 0;
   p.WPR = 1;
   while (p.WPR < kStripWarps && cdiv(p.W / 2, 32 * p.WPR) > 12) p.WPR *= 2;
   if (forced_wpr == 1 || forced_wpr == 2 || forced_wpr == 4 || forced_wpr == 8) p.WPR = tmax(p.WPR, forced_wpr);
@@ -333,10 +333,10 @@ StripPlan hvp_strip_plan(int64_t rows, int64_t n, int64_t lda, const double* A, 
   const size_t stage = (size_t)R * p.W * 8;
   p.S = (int)tmin<int64_t>(16, (kStripSmemBudget - 512) / stage);
   if (p.S < 3) return p;
-  static const int forced_lag = getenv("NYS_STRIP_LAG") ? atoi(getenv("NYS_STRIP_LAG")) : 0;
+  static const int forced_lag = dev_env("NYS_STRIP_LAG") ? atoi(dev_env("NYS_STRIP_LAG")) : 0;
   p.L = forced_lag > 0 ? forced_lag : 2;  // measured best on B200 (S = 4 stages of 43 KB at n = 1e5)
   p.L = tmin(p.L, tmin(kStripMaxLag, p.S - 1));
-  static const int forced_mode = getenv("NYS_STRIP_MODE") ? atoi(getenv("NYS_STRIP_MODE")) : 0;
+  static const int forced_mode = dev_env("NYS_STRIP_MODE") ? atoi(dev_env("NYS_STRIP_MODE")) : 0;
   p.mode = forced_mode == 2 ? 2 : 0;
   p.smem = (size_t)p.S * stage + (size_t)p.S * 16;
   if ((size_t)kStripWarps * p.W * 8 > (size_t)p.S * stage) return p;  // final y reduction reuses the ring

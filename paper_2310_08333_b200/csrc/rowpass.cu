@@ -192,7 +192,7 @@ static RowpassPlan rowpass_plan(int64_t rows, int64_t n, int64_t lda, const doub
   p.ok = false;
   if ((lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)x & 15) || (z && ((uintptr_t)z & 15))) return p;
   if (rows < kNumSMs || cdiv(rows, (int64_t)kNumSMs) > 1024) return p;
-  static const bool off = getenv("NYS_ROWPASS_OFF") != nullptr;
+  static const bool off = dev_env("NYS_ROWPASS_OFF") != nullptr;
   if (off) return p;
   for (int P = 1; P <= 4; P *= 2) {
     if (n % P) continue;
@@ -232,7 +232,7 @@ static int rowpass_launch(const RowpassPlan& p, const double* A, int64_t rows, i
   // launched without the PDL attribute: the persistent solve before it is a
   // cooperative kernel, and letting this pass be scheduled early into it was
   // measured slower
-  static const bool pdl = getenv("NYS_RP_PDL") && getenv("NYS_RP_PDL")[0] == '1';
+  static const bool pdl = dev_env("NYS_RP_PDL") && dev_env("NYS_RP_PDL")[0] == '1';
   if (pdl)
     launch_chain(fn, dim3(grid), dim3(kRpThreads), p.smem, st, false, A, rows, n, lda, x, z, b, loss, p.Wp, p.S, tg,
                  w, thx, tnu, rowsums, part, counter, pred, order);

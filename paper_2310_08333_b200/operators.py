@@ -22,6 +22,7 @@ from typing import Callable, Optional
 import numpy as np
 import torch
 
+from . import _lib
 from .dist import Shard, current_shard
 from .errors import CapabilityError, DimensionMismatchError
 
@@ -217,7 +218,7 @@ class DenseOperator(LinearOperator):
         t = self._shards.get(key)
         if t is not None and not overlap:
             self._wait_pending(t)
-        if overlap and os.environ.get("NYS_UPLOAD_OVERLAP", "1") == "0":
+        if overlap and _lib.dev_env("NYS_UPLOAD_OVERLAP", "1") == "0":
             overlap = False
         if t is None and overlap and self._dev_full is None and self._local is None:
             src = self._pinned_rows(shard)
