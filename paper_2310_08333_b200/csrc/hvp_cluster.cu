@@ -742,6 +742,71 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
+    // Sparse z (the prox output: soft-thresholded, a few percent nonzeros at
+    // most): when this CTA's slice of z holds at most one nonzero per compute
+    // thread, a_i.z is one product per thread -- thread t keeps entry t of the
+    // slice's compacted nonzeros (column order) in registers -- instead of a
+    // second dense dot (half of the dot's FP64 work and tensor-memory reads).
+    // zc: -2 dense dot, -1 sparse and no entry here, >= 0 the entry's column.
+    // A zero term contributes exactly 0 to a sum, so only the order of the
+    // nonzero terms differs from the dense dot.  CTAs of a cluster may choose
+    // differently (the exchanged partials do not care).
+    // (three-axpy variants of 7-8 column tiles per thread have no registers to spare)
+    constexpr bool ZS = WITHZ && (SQ || KQ <= 6);
+    int zc = -2;
+    double zv = 0.0;
+    if constexpr (ZS) {
+      constexpr int kNT = kHqWarps * 32;
+      int* wtot = reinterpret_cast<int*>(psl);  // psl is idle until the first dot
+      int* lcol = wtot + 16;
+      double* lval = reinterpret_cast<double*>(lcol + kNT);
+      int cnt = 0;
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) {
+        const int j = 2 * (tid + k * kNT);
+        if (j < w_here) {
+          const double2 z2 = *reinterpret_cast<const double2*>(z + c0 + j);
+          cnt += (z2.x != 0.0 ? 1 : 0) + (z2.y != 0.0 ? 1 : 0);
+        }
+      }
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wtot[warp] = incl;
+      asm volatile("bar.sync 15, %0;" ::"n"(kNT) : "memory");
+      int base = 0, total = 0;
+#pragma unroll
+      for (int w2 = 0; w2 < kHqWarps; ++w2) {
+        const int t = wtot[w2];
+        if (w2 < warp) base += t;
+        total += t;
+      }
+      if (total <= kNT && w_here > 0) {
+        int pos = base + incl - cnt;
+#pragma unroll
+        for (int k = 0; k < KQ; ++k) {
+          const int j = 2 * (tid + k * kNT);
+          if (j < w_here) {
+            const double2 z2 = *reinterpret_cast<const double2*>(z + c0 + j);
+            if (z2.x != 0.0) {
+              lcol[pos] = j;
+              lval[pos++] = z2.x;
+            }
+            if (z2.y != 0.0) {
+              lcol[pos] = j + 1;
+              lval[pos++] = z2.y;
+            }
+          }
+        }
+        asm volatile("bar.sync 15, %0;" ::"n"(kNT) : "memory");
+        zc = tid < total ? lcol[tid] : -1;
+        zv = tid < total ? lval[tid] : 0.0;
+      }
+      asm volatile("bar.sync 15, %0;" ::"n"(kNT) : "memory");  // psl is the dots' from here
+    }
     double2 yg[SQ ? 1 : KQ], yh[KQ], yn[WITHZ ? KQ : 1];
     yg[0] = make_double2(0.0, 0.0);
 #pragma unroll
@@ -757,7 +822,28 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
     int qi = 0, pi = 0, qj = 0, rs = 0;
     // the dots of a staged row with x (and z): lane partials into psl slot rs
     auto dot = [&](const double* row) {
-      if (WITHZ) {
+      if (ZS && zc != -2) {
+        // sparse z: the dense dot with x, one product for z
+        double px = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (4 * h >= KQ) continue;
+          double2 c[4];
+          tmem_ld16(tv + 16 * h, c);
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int k = 4 * h + k4;
+            if (k < KQ) {
+              const double2 a = *reinterpret_cast<const double2*>(row + tmin(2 * (tid + k * kHqWarps * 32), jmax));
+              px = fma(a.x, c[k4].x, px);
+              px = fma(a.y, c[k4].y, px);
+            }
+          }
+        }
+        const double pz = zc >= 0 ? __dmul_rn(row[zc], zv) : 0.0;
+        psl[((rs * NV) * kHqWarps + warp) * 32 + lane] = px;
+        psl[((rs * NV + 1) * kHqWarps + warp) * 32 + lane] = pz;
+      } else if (WITHZ) {
         // one pass over the staged row for both dots: a read once per element
         double px = 0.0, pz = 0.0;
 #pragma unroll

@@ -442,6 +442,43 @@ def test_ml_tail_one_pass(kx, rows, n, with_z, loss):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("loss", ["square", "logistic"])
+@pytest.mark.parametrize("rows,n,dens", [
+    (400, 10000, 0.01), (400, 10000, 0.085), (149, 7000, 0.0), (64, 28000, 0.03), (40, 50000, 0.07),
+    (23, 100000, 0.005), (23, 100000, 0.0716), (300, 100000, 0.0065)])
+def test_ml_tail_sparse_z(kx, rows, n, dens, loss):
+    """The one-pass tail with a sparse z (the prox output): a CTA whose slice of z
+    holds at most one nonzero per compute thread (448) forms a_i.z as one product
+    per thread.  Densities below, around (CTAs of one cluster choosing
+    differently) and above that limit, z = 0, both epilogues, with and without
+    g_b; against NumPy and against the dense-z arithmetic on the same inputs."""
+    g = np.random.default_rng(rows + n + int(1e4 * dens))
+    A = g.standard_normal((rows, n)) / np.sqrt(n)
+    x, b = g.standard_normal(n), g.standard_normal(rows)
+    z = np.where(g.random(n) < dens, g.standard_normal(n), 0.0)
+    az = A @ z
+    r2 = az - b
+    nu = r2 if loss == "square" else 1.0 / (1.0 + np.exp(-r2))
+    for use_gb in ([False, True] if loss == "square" else [False]):
+        T, w, AT, rs = kx.empty(3, rows), kx.empty(rows), kx.empty(3, n), kx.zeros(8)
+        kw = {"gb": dev(A.T @ b)} if use_gb else {}
+        kx.ml_tail(loss, dev(A), dev(x), dev(z), dev(b), T, w, AT, rs, **kw)
+        Tn = T.cpu().numpy()
+        np.testing.assert_allclose(Tn[2], nu, rtol=1e-12, atol=1e-12)
+        ref = A.T @ nu
+        scale = max(np.abs(ref).max(), np.abs(A.T @ b).max())
+        np.testing.assert_allclose(AT.cpu().numpy()[2], ref, rtol=0, atol=1e-11 * scale)
+        s = rs.cpu().numpy()
+        lval = (lambda r: 0.5 * r * r) if loss == "square" else (lambda r: np.logaddexp(0.0, r))  # noqa: E731
+        assert s[1] == pytest.approx(np.sum(lval(r2)), rel=1e-12)
+        assert s[4] == pytest.approx(b @ nu, rel=1e-11, abs=1e-11)
+        # the x side is untouched by the choice
+        np.testing.assert_allclose(Tn[1], (np.ones(rows) if loss == "square" else
+                                           (1.0 / (1.0 + np.exp(-(A @ x - b)))) * (1.0 / (1.0 + np.exp(A @ x - b)))) * (A @ x),
+                                   rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("rows,n", [(400, 10000), (149, 7000), (64, 28000), (40, 50000), (23, 100000)])
 def test_ml_tail_square_two_products(kx, rows, n):
     """The square-loss one-pass tail given g_b = A^T b (nys_ml_tail_gb_f64):

@@ -13,9 +13,12 @@ rows = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 LOSS = sys.argv[4] if len(sys.argv) > 4 else "logistic"
+ZDENS = float(sys.argv[5]) if len(sys.argv) > 5 else 1.0  # density of z (the prox output is sparse)
 kx = get_kernels()
 A = kx.empty(rows, n).normal_()
 XZ = kx.empty(2, n).normal_()
+if ZDENS < 1.0:
+    XZ[1].mul_((torch.rand(n, device=XZ.device) < ZDENS).double())
 b = kx.empty(rows).normal_()
 T = kx.empty(3, rows)
 w = kx.empty(rows)
@@ -52,4 +55,4 @@ for name, f in (("cluster tail", fused), ("cluster tail with g_b", fused_gb), ("
     e1.record(kx.stream)
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
-    print(f"{name} {rows}x{n}: {us:.1f} us, {8 * rows * n / (us * 1e-6) / 1e9:.0f} GB/s of A per pass")
+    print(f"{name} {rows}x{n} z density {ZDENS}: {us:.1f} us, {8 * rows * n / (us * 1e-6) / 1e9:.0f} GB/s of A per pass")
