@@ -288,7 +288,9 @@ class _Engine:
             self.rb_dev = self.red[3 * n:]
             # g_b = A^T b for the square loss: the one-pass tail then streams
             # A^T (A x) and A^T (A z) and subtracts it (nys_admm_tail.gb)
-            self.gb = kx.empty(n) if (self.loss == "square" and not self.shard.sharded) else None
+            # (row-sharded: this rank's A_loc^T b_loc, never all-reduced -- it is
+            # subtracted from the rank's partial before the ranks' AT are summed)
+            self.gb = kx.empty(n) if self.loss == "square" else None
             self._gb_ready = False
         else:
             qp = gp.qp

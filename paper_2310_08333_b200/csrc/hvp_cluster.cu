@@ -1198,7 +1198,9 @@ namespace nys {
 // AT[j, c] = sum over clusters of P[(cl * K + j) * n + c], fixed cluster order;
 // with gb (the SQ tail): AT[0] = AT[1] - gb, AT[2] = (sum of row 2) - gb
 __global__ void tail_partial_sum_kernel(const double* __restrict__ P, int64_t n, int K, int ncl,
-                                        double* __restrict__ AT, const double* __restrict__ gb) {
+                                        double* __restrict__ AT, const double* __restrict__ gb,
+                                        const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
   const int64_t total = n * K;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = t / n, c = t - j * n;
@@ -1208,6 +1210,16 @@ __global__ void tail_partial_sum_kernel(const double* __restrict__ P, int64_t n,
     if (gb && j != 1) a = a - gb[c];
     AT[j * n + c] = a;
   }
+}
+// the cluster tail's per-cluster A^T partials -> AT (K x n), for callers that do
+// not fuse the sum into the ML epilogue (row-sharded solves: the ranks' AT are
+// all-reduced before the norms)
+int tail_partial_sum(const double* P, int64_t n, int K, int ncl, double* AT, const double* gb, cudaStream_t st,
+                     const double* pred) {
+  tail_partial_sum_kernel<<<(unsigned)tmin<int64_t>(cdiv(n * K, 256), 4 * kNumSMs), 256, 0, st>>>(P, n, K, ncl, AT,
+                                                                                                  gb, pred);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
 }
 }  // namespace nys
 
@@ -1224,10 +1236,7 @@ static int ml_tail_impl(const double* A, int64_t rows, int64_t n, int64_t lda, c
                               &splits, gb, &sq);
   if (rc) return rc;
   const int K = z ? 3 : 2;
-  tail_partial_sum_kernel<<<(unsigned)tmin<int64_t>(cdiv(n * K, 256), 4 * kNumSMs), 256, 0, st>>>(
-      P, n, K, splits, AT, sq ? gb : nullptr);
-  NYS_CHECK_LAUNCH();
-  return NYS_OK;
+  return tail_partial_sum(P, n, K, splits, AT, sq ? gb : nullptr, st, nullptr);
 }
 
 // The one-pass ML tail on its own (tests and measurement): T = [l'(Ax-b),

@@ -1164,6 +1164,8 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
                  const double* b, int loss, double* T, double* w, void* ws, size_t ws_bytes, size_t ws_off,
                  double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out,
                  const double* gb, int* sq_out);
+int tail_partial_sum(const double* P, int64_t n, int K, int ncl, double* AT, const double* gb, cudaStream_t st,
+                     const double* pred);
 int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                const double* b, int loss, double* tg, double* w, double* thx, double* tnu, double* rowsums,
                double* part, unsigned int* counter, cudaStream_t st, const double* pred, const double* order);
@@ -1203,9 +1205,11 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
                        cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
     // wide rows: the whole tail's data passes in one cluster stream over A
     // (hvp_cluster.cu: tail_cluster_kernel); else the row pass + GEMV^T below
+    // (row-sharded: the same stream, its partials summed into this rank's AT,
+    // which is all-reduced before the norms)
     double* Pc = nullptr;
     int csplits = 0, csq = 0;
-    if (fuse0) {
+    if (fuse0 || t->reduce) {
       rc = tail_cluster(t->A, t->rows, n, t->lda, x, t->with_z ? z : nullptr, t->b, t->loss, t->T, t->w, t->ws_gemvT,
                         t->ws_gemvT_bytes, (kRedPartials * 16 + 64) * sizeof(double), t->rowsums, st, pred, &Pc,
                         &csplits, t->gb, &csq);
@@ -1280,9 +1284,13 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       NYS_CHECK_LAUNCH();
       t_mut->rb_done = rb ? 1 : 0;
     } else {
-      if ((rc = gemv_t(t->A, t->rows, n, t->lda, t->T, t->rows, t->with_z ? 3 : 2, t->AT, n, nullptr, 0.0, nullptr,
-                       t->ws_gemvT, t->ws_gemvT_bytes, st, pred)))
+      if (Pc) {
+        if ((rc = tail_partial_sum(Pc, n, t->with_z ? 3 : 2, csplits, t->AT, csq ? t->gb : nullptr, st, pred)))
+          return rc;
+      } else if ((rc = gemv_t(t->A, t->rows, n, t->lda, t->T, t->rows, t->with_z ? 3 : 2, t->AT, n, nullptr, 0.0,
+                              nullptr, t->ws_gemvT, t->ws_gemvT_bytes, st, pred))) {
         return rc;
+      }
       if (t->reduce) {  // this rank's A^T outputs and row sums: sum over the ranks
         t->reduce(t->AT, (int64_t)(t->with_z ? 3 : 2) * n, t->reduce_user, st);
         t->reduce(t->rowsums, NYS_ROWS_NOUT, t->reduce_user, st);

@@ -41,6 +41,10 @@ def _problem(name):
         d = make_config(2, scale=0.2)  # 1000 x 2000 logistic, same recipe as config 2
         return dict(loss="logistic", A=d.A, b=d.b, lambda1=d.lambda1, lambda2=d.lambda2), dict(
             sketch_rank=d.rank, rng_seed=d.seed, eps_abs=1e-4, eps_rel=1e-4, eps_dual_gap=1e-4)
+    if name == "cfg2_wide":
+        d = make_config(2, scale=0.8)  # 4000 x 8000 logistic: rows wide enough for the one-pass cluster tail
+        return dict(loss="logistic", A=d.A, b=d.b, lambda1=d.lambda1, lambda2=d.lambda2), dict(
+            sketch_rank=d.rank, rng_seed=d.seed, eps_abs=1e-4, eps_rel=1e-4, eps_dual_gap=1e-4)
     if name == "cfg4_small":
         d = make_config(4, scale=0.03)  # 600 x 3000 lasso, same recipe as config 4
         return dict(loss="square", A=d.A, b=d.b, lambda1=d.lambda1, lambda2=0.0), dict(
@@ -82,7 +86,7 @@ def _worker(rank, world, port, name, out_path, pipelined=True):
 
 @pytest.mark.parametrize("name,pipelined", [("lasso_small", True), ("logistic_small", True), ("enet_small", True),
                                            ("cfg2_small", True), ("cfg4_small", True), ("cfg2_small", False),
-                                           ("lasso_wide", True), ("lasso_wide", False)])
+                                           ("lasso_wide", True), ("lasso_wide", False), ("cfg2_wide", True)])
 def test_gpu_row_sharded_solve_matches_single(tmp_path, name, pipelined):
     """pipelined: the one-round-trip-per-iteration schedule with the all-reduce
     hook inside the C drivers (default); else the per-step schedule."""
