@@ -1007,6 +1007,341 @@ tail_cluster_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64
   }
 }
 
+// ---------------------------------------------------------------------------
+// The one-pass square-loss tail for rows too wide for tail_cluster_kernel
+// (114688 < n <= ~262000: config 5's n = 200000, the shape every rank holds in
+// its 8-GPU run).  A CTA's column slice (12500 doubles at n = 2e5) is too wide
+// for two register accumulators and whole-slice stages, so, as in
+// hvp_cluster_q_kernel, the slice is staged in Q sub-segments (the dot streams
+// each from HBM, the accumulation one row later re-reads it from L2) and the
+// operands are spread over the SM's three large stores:
+//   x slice               tensor memory, columns [0, 64) of the warp's block
+//   A^T (A z) accumulator tensor memory, columns [64, 128)  (ld / fma / st per row)
+//   A^T (A x) accumulator registers
+//   z                     its nonzeros only: the prox output is sparse, so a_i.z is a
+//                         gather over the compacted entries of each sub-segment
+//                         (zlist_kernel), typically <= 1 entry per thread
+// A dense z stays correct (every entry is visited, 448 per step) and only
+// slows the dot.  Outputs as tail_cluster_kernel's SQ mode.
+constexpr int kTqTmemCols = 512;
+constexpr int kTqNR = 2;  // row slots of the lane partials (L + 1)
+
+// nonzeros of sub-segment (rank, q) of z in column order: columns relative to
+// the sub-segment into zcol / zval[(rank Q + q) Wq ...), their count in zcnt
+__global__ void zlist_kernel(const double* __restrict__ z, int64_t n, int W, int Wq, int Q, int* __restrict__ zcol,
+                             double* __restrict__ zval, int* __restrict__ zcnt, const double* __restrict__ pred) {
+  if (pred && *pred != 0.0) return;
+  const int rank = blockIdx.x / Q, q = blockIdx.x - rank * Q;
+  const int64_t c0 = (int64_t)rank * W + (int64_t)q * Wq;
+  const int wq = (int)tmax<int64_t>(0, tmin<int64_t>(tmin<int64_t>(Wq, (int64_t)W - (int64_t)q * Wq), n - c0));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ int wsum[32];
+  __shared__ int s_base;
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  int* oc = zcol + (int64_t)blockIdx.x * Wq;
+  double* ov = zval + (int64_t)blockIdx.x * Wq;
+  for (int j0 = 0; j0 < wq; j0 += blockDim.x) {
+    const int j = j0 + tid;
+    const double v = j < wq ? z[c0 + j] : 0.0;
+    const bool nz = v != 0.0;
+    const unsigned m = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) wsum[warp] = __popc(m);
+    __syncthreads();
+    int before = s_base, total = 0;
+    for (int w2 = 0; w2 < nw; ++w2) {
+      const int t = wsum[w2];
+      if (w2 < warp) before += t;
+      total += t;
+    }
+    if (nz) {
+      const int pos = before + __popc(m & ((1u << lane) - 1u));
+      oc[pos] = j;
+      ov[pos] = v;
+    }
+    __syncthreads();
+    if (tid == 0) s_base += total;
+  }
+  __syncthreads();
+  if (tid == 0) zcnt[blockIdx.x] = s_base;
+}
+
+template <int Q, int KQ>
+__global__ void __launch_bounds__(kHqThreads, 1)
+tail_q_kernel(const double* __restrict__ A, int64_t rows, int64_t n, int64_t lda, const double* __restrict__ x,
+              const int* __restrict__ zcol, const double* __restrict__ zval, const int* __restrict__ zcnt,
+              const double* __restrict__ b, int W, int Wq, int S, double* __restrict__ T, double* __restrict__ wout,
+              double* __restrict__ P, double* __restrict__ R, const double* __restrict__ pred) {
+  static_assert(KQ <= 4 && Q <= 4, "x and accumulator slices of a thread: <= 64 TMEM columns each");
+  // Rows go through the pipeline in PAIRS: tensor memory reads at 64 B/clk per
+  // SM (writes at 256), so one read of the x slice feeds the dots of two rows
+  // and one read + write of the accumulator slice takes both rows' updates
+  // (a row at a time the tensor-memory traffic alone filled the row period:
+  // 6.3 ms at 12500 x 200000, no faster than the two streaming passes).
+  constexpr int C = kHcC, NV = 4, L = 1, NR = kTqNR;  // NV: (x, z) of the pair's two rows
+  constexpr int kNT = kHqWarps * 32;
+  if (pred && *pred != 0.0) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);                  // S x Wq
+  double* psl = ring + (size_t)S * Wq;                                 // NR x NV x 448 lane partials
+  double* tsl = psl + NR * NV * kNT;                                   // NT x NV x C CTA partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsl + kHcNT * NV * C);  // S
+  uint64_t* totb = full + S;                                           // NT
+  uint32_t* tmem_base = reinterpret_cast<uint32_t*>(totb + kHcNT);
+  int* s_cnt = reinterpret_cast<int*>(tmem_base + 2);                  // Q
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int cluster_id = blockIdx.x / C, nclusters = gridDim.x / C;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)rank * W;
+  const int w_here = (int)tmax<int64_t>(0, tmin<int64_t>((int64_t)W, n - c0));
+  const int64_t nrows_mine = rows > cluster_id ? (rows - cluster_id + nclusters - 1) / nclusters : 0;
+  constexpr unsigned kTx = (unsigned)(C * NV * 8);
+
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(&full[q], 1);
+    for (int q = 0; q < kHcNT; ++q) mbar_init(&totb[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < kHcNT; ++q) mbar_expect_tx(&totb[q], kTx);
+  }
+  if (tid < Q) s_cnt[tid] = zcnt[rank * Q + tid];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base)),
+                 "n"(kTqTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cl.sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // this warp's TMEM block: lanes of its sub-partition, 128 columns per warp
+  // (x at [0, 64), the A^T (A z) accumulator at [64, 128))
+  const uint32_t tv = *tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(128 * ((warp >> 2) & 3));
+  const uint32_t tz = tv + 64;
+
+  const int nr = (int)nrows_mine;
+  const int npairs = (nr + 1) >> 1;
+  if (warp == kHqWarps) {
+    // ---------------------------------------------------------- producer --
+    // slot order of a pair: sub-segment 0 of its rows, sub-segment 1 of its rows, ...
+    const int64_t rstep = (int64_t)nclusters * lda;
+    const double* base = A + (int64_t)cluster_id * lda + c0;
+    int u = 0, slot = 0;
+    auto issue = [&](int pp) {
+#pragma unroll 1
+      for (int q = 0; q < Q; ++q) {
+        const int wq = tmin(Wq, w_here - q * Wq);
+#pragma unroll 1
+        for (int r = 0; r < 2; ++r) {
+          const int g = 2 * pp + r;
+          if (g >= nr) continue;
+          if (u >= S) qbar_sync(1 + slot);
+          if (lane == 0) {
+            if (wq > 0) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              mbar_expect_tx(&full[slot], (unsigned)wq * 8u);
+              tma_load_1d(ring + (size_t)slot * Wq, base + (int64_t)g * rstep + (int64_t)q * Wq, (unsigned)wq * 8u,
+                          &full[slot]);
+            } else {
+              mbar_arrive(&full[slot]);
+            }
+          }
+          ++u;
+          if (++slot == S) slot = 0;
+        }
+      }
+    };
+    for (int pp = 0; pp < npairs + L; ++pp) {
+      if (pp < npairs) issue(pp);
+      if (pp >= L) issue(pp - L);  // the accumulation's re-read (L2)
+    }
+    for (int w2 = tmax(0, u - S); w2 < u; ++w2) qbar_sync(1 + w2 % S);
+  } else if (warp > kHqWarps) {
+    // --------------------------------------------------- exchange (relay) --
+    for (int g = 0, rs = 0; g < npairs; ++g, rs = rs + 1 == NR ? 0 : rs + 1) {
+      qbar_sync(1 + kHqMaxS + rs);
+      const int s = g & (kHcNT - 1);
+#pragma unroll
+      for (int vv = 0; vv < NV; ++vv) {
+        const double* pp = psl + (rs * NV + vv) * kNT + lane;
+        double p = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < kHqWarps; ++w2) p += pp[w2 * 32];
+        p = warp_sum(p);
+        if (lane < C) st_async_remote_f64(tsl + (s * NV + vv) * C + rank, &totb[s], (unsigned)lane, p);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- compute --
+    const int* zc = zcol + (int64_t)rank * Q * Wq;
+    const double* zv = zval + (int64_t)rank * Q * Wq;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double2 c[4];
+      const int wq = tmin(Wq, w_here - q * Wq);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = 2 * (tid + k * kNT);
+        c[k] = (k < KQ && j < wq) ? *reinterpret_cast<const double2*>(x + c0 + (int64_t)q * Wq + j)
+                                  : make_double2(0.0, 0.0);
+      }
+      tmem_st16(tv + 16 * q, c);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) c[k] = make_double2(0.0, 0.0);
+      tmem_st16(tz + 16 * q, c);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    double2 yx[Q][KQ];
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) yx[q][k] = make_double2(0.0, 0.0);
+    int slot = 0, ph = 0, wturn = 0, rs = 0;
+    auto next = [&]() {
+      if (++slot == S) {
+        slot = 0;
+        ph ^= 1;
+      }
+    };
+    for (int pp = 0; pp < npairs + L; ++pp) {
+      if (pp < npairs) {
+        const bool has1 = 2 * pp + 1 < nr;
+        double px0 = 0.0, pz0 = 0.0, px1 = 0.0, pz1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int wq = tmin(Wq, w_here - q * Wq);
+          // this thread's nonzero of z in the sub-segment (requested before the waits)
+          const int cq = s_cnt[q];
+          int ce = 0;
+          double ve = 0.0;
+          if (tid < cq) {
+            ce = __ldg(zc + q * Wq + tid);
+            ve = __ldg(zv + q * Wq + tid);
+          }
+          double2 c[4];
+          tmem_ld16(tv + 16 * q, c);
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (r == 1 && !has1) break;
+            mbar_wait(&full[slot], (unsigned)ph);
+            const double* seg = ring + (size_t)slot * Wq;
+            double px = 0.0, pz = 0.0;
+#pragma unroll
+            for (int k = 0; k < KQ; ++k) {
+              const int j = 2 * (tid + k * kNT);
+              if (j < wq) {
+                const double2 a = *reinterpret_cast<const double2*>(seg + j);
+                px = fma(a.x, c[k].x, px);
+                px = fma(a.y, c[k].y, px);
+              }
+            }
+            if (tid < cq) pz = __dmul_rn(seg[ce], ve);
+            for (int e = tid + kNT; e < cq; e += kNT)  // a denser z: the remaining entries
+              pz = fma(seg[__ldg(zc + q * Wq + e)], __ldg(zv + q * Wq + e), pz);
+            if (r == 0) {
+              px0 += px;
+              pz0 += pz;
+            } else {
+              px1 += px;
+              pz1 += pz;
+            }
+            __syncwarp();
+            qbar_arrive(1 + slot);
+            next();
+          }
+        }
+        double* ps = psl + ((rs * NV) * kHqWarps + warp) * 32 + lane;
+        ps[0] = px0;
+        ps[kNT] = pz0;
+        ps[2 * kNT] = px1;
+        ps[3 * kNT] = pz1;
+        __syncwarp();
+        qbar_arrive(1 + kHqMaxS + rs);
+        if (++rs == NR) rs = 0;
+      }
+      const int jp = pp - L;
+      if (jp < 0) continue;
+      const int s = jp & (kHcNT - 1);
+      const bool hasj1 = 2 * jp + 1 < nr;
+      mbar_wait(&totb[s], (unsigned)((jp / kHcNT) & 1));
+      const double tot0 = cluster_total_c<C>(tsl + (s * NV) * C, lane);
+      const double tot1 = cluster_total_c<C>(tsl + (s * NV + 2) * C, lane);
+      const double ax0 = __shfl_sync(0xffffffffu, tot0, 0), az0 = __shfl_sync(0xffffffffu, tot0, 16);
+      const double ax1 = __shfl_sync(0xffffffffu, tot1, 0), az1 = __shfl_sync(0xffffffffu, tot1, 16);
+      if (warp == 0 && lane == 0) mbar_expect_tx(&totb[s], kTx);
+      // the rows' epilogue (problems.py:35-45: l'(r) = r, l'' = 1): the writer's stores
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (r == 1 && !hasj1) break;
+        if (rank == 0 && lane == 0 && warp == wturn) {
+          const int64_t i = cluster_id + (int64_t)(2 * jp + r) * nclusters;
+          const double bi = __ldg(b + i);
+          const double ax = r ? ax1 : ax0, az = r ? az1 : az0;
+          const double r1 = __dadd_rn(ax, -bi), r2 = __dadd_rn(az, -bi);
+          T[i] = r1;
+          T[rows + i] = ax;
+          T[2 * rows + i] = r2;
+          wout[i] = 1.0;
+          R[i] = r1;
+          R[rows + i] = r2;
+        }
+        if (++wturn == kHqWarps) wturn = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int wq = tmin(Wq, w_here - q * Wq);
+        double2 yz[4];
+        tmem_ld16(tz + 16 * q, yz);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (r == 1 && !hasj1) break;
+          const double ax = r ? ax1 : ax0, az = r ? az1 : az0;
+          mbar_wait(&full[slot], (unsigned)ph);
+          const double* seg = ring + (size_t)slot * Wq;
+#pragma unroll
+          for (int k = 0; k < KQ; ++k) {
+            const int j = 2 * (tid + k * kNT);
+            if (j < wq) {
+              const double2 a = *reinterpret_cast<const double2*>(seg + j);
+              yx[q][k].x = fma(ax, a.x, yx[q][k].x);
+              yx[q][k].y = fma(ax, a.y, yx[q][k].y);
+              yz[k].x = fma(az, a.x, yz[k].x);
+              yz[k].y = fma(az, a.y, yz[k].y);
+            }
+          }
+          __syncwarp();
+          qbar_arrive(1 + slot);
+          next();
+        }
+        tmem_st16(tz + 16 * q, yz);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // P rows 1 and 2 of this cluster (row 0 is not written in the SQ layout)
+    double* pc = P + (int64_t)cluster_id * 3 * n + c0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      double2 yz[4];
+      tmem_ld16(tz + 16 * q, yz);
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) {
+        const int j = 2 * (tid + k * kNT);
+        if (j < tmin(Wq, w_here - q * Wq)) {
+          *reinterpret_cast<double2*>(pc + n + q * Wq + j) = yx[q][k];
+          *reinterpret_cast<double2*>(pc + 2 * n + q * Wq + j) = yz[k];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cl.sync();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_base), "n"(kTqTmemCols)
+                 : "memory");
+  }
+}
+
 // the row sums of the tail (nys_ml_rowwise_f64's out[0..4]) from the stored
 // residuals r1 = Ax - b, r2 = Az - b and nu = T[2]: sum l(r1), sum l(r2),
 // sum l*(nu) finite, #inf, b.nu -- row-parallel, fixed-order reduction
@@ -1134,6 +1469,121 @@ static int tail_cluster_launch_k(TcPlan& p, const double* A, int64_t rows, int64
   return NYS_OK;
 }
 
+// plan and launch of tail_q_kernel (square loss with z and g_b only)
+struct TqPlan {
+  int W, Wq, Q, KQ, S, nclusters;
+  size_t smem;
+  bool ok;
+};
+
+static TqPlan tail_q_plan(int64_t rows, int64_t n, int64_t lda, const double* A, const double* x) {
+  TqPlan p{};
+  p.ok = false;
+  if ((lda & 1) || (n & 1) || ((uintptr_t)A & 15) || ((uintptr_t)x & 15) || rows < 1) return p;
+  p.W = (int)cdiv(cdiv(n, (int64_t)kHcC), 2) * 2;
+  const size_t fixed = (size_t)kTqNR * 4 * kHqWarps * 32 * 8 + (size_t)kHcNT * 4 * kHcC * 8 + kHcNT * 8 + 64 + 1024;
+  for (int Q = 2; Q <= 4; ++Q) {
+    const int Wq = (int)cdiv(cdiv(p.W, Q), 2) * 2;
+    const int KQ = (int)cdiv(Wq / 2, kHqWarps * 32);
+    if (KQ > 4) continue;
+    const int S = (int)tmin<int64_t>(kHqMaxS, (int64_t)((kHcSmemBudget - fixed) / ((size_t)Wq * 8 + 8)));
+    if (S < 4) continue;
+    p.Q = Q;
+    p.Wq = Wq;
+    p.KQ = KQ;
+    p.S = S;
+    p.smem = (size_t)S * Wq * 8 + (size_t)kTqNR * 4 * kHqWarps * 32 * 8 + (size_t)kHcNT * 4 * kHcC * 8 +
+             (size_t)(S + kHcNT) * 8 + 64;
+    p.ok = true;
+    return p;
+  }
+  return p;
+}
+
+template <int Q, int KQ>
+static int tail_q_launch_k(TqPlan& p, const double* A, int64_t rows, int64_t n, int64_t lda, const double* x,
+                           const int* zcol, const double* zval, const int* zcnt, const double* b, double* T,
+                           double* w, double* P, double* R, cudaStream_t st, const double* pred) {
+  const void* fn = (const void*)tail_q_kernel<Q, KQ>;
+  static bool attr = false;
+  static int maxc = 0;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kHcSmemBudget);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kHqThreads, 1, 1);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kHcC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (maxc == 0) {
+    cfg.gridDim = dim3(kHcC * (kNumSMs / kHcC), 1, 1);
+    int mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, fn, &cfg) != cudaSuccess || mc < 1) {
+      cudaGetLastError();
+      return NYS_ERR_UNSUPPORTED;
+    }
+    maxc = tmin(mc, kNumSMs / kHcC);
+  }
+  p.nclusters = (int)tmax<int64_t>(1, tmin<int64_t>(maxc, rows));
+  cfg.gridDim = dim3(kHcC * p.nclusters, 1, 1);
+  int W = p.W, Wq = p.Wq, S = p.S;
+  if (cudaLaunchKernelEx(&cfg, tail_q_kernel<Q, KQ>, A, rows, n, lda, x, zcol, zval, zcnt, b, W, Wq, S, T, w, P, R,
+                         pred) != cudaSuccess)
+    return NYS_ERR_CUDA;
+  __atomic_fetch_add(&g_launches, 1ull, __ATOMIC_RELAXED);
+  return NYS_OK;
+}
+
+// the SQ tail for rows beyond tail_cluster_plan: z's nonzeros compacted per
+// sub-segment, then the one stream over A, then the row sums
+static int tail_q(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
+                  const double* b, double* T, double* w, void* ws, size_t ws_bytes, size_t ws_off, double* rowsums,
+                  cudaStream_t st, const double* pred, double** Pout, int* splits_out) {
+  TqPlan p = tail_q_plan(rows, n, lda, A, x);
+  if (!p.ok) return NYS_ERR_UNSUPPORTED;
+  const size_t ncl = (size_t)(kNumSMs / kHcC);
+  const size_t nlist = (size_t)kHcC * p.Q * p.Wq;
+  const size_t need =
+      ws_off + (ncl * 3 * n + 2 * (size_t)rows + kTailSumBlocks * 5 + 8) * 8 + nlist * 12 + 64 * 4 + 64;
+  if (ws_bytes < need) return NYS_ERR_UNSUPPORTED;
+  double* P = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + ws_off);
+  double* rowpart = P + ncl * 3 * n;
+  double* zval = rowpart + 2 * (size_t)rows + kTailSumBlocks * 5 + 8;
+  int* zcol = reinterpret_cast<int*>(zval + nlist);
+  int* zcnt = zcol + nlist;
+  zlist_kernel<<<kHcC * p.Q, 256, 0, st>>>(z, n, p.W, p.Wq, p.Q, zcol, zval, zcnt, pred);
+  NYS_CHECK_LAUNCH();
+  int rc = NYS_ERR_UNSUPPORTED;
+  switch (p.Q * 8 + p.KQ) {
+#define NYS_TQ(q, k)                                                                                        \
+  case (q * 8 + k):                                                                                         \
+    rc = tail_q_launch_k<q, k>(p, A, rows, n, lda, x, zcol, zval, zcnt, b, T, w, P, rowpart, st, pred); \
+    break;
+    NYS_TQ(2, 1) NYS_TQ(2, 2) NYS_TQ(2, 3) NYS_TQ(2, 4) NYS_TQ(3, 1) NYS_TQ(3, 2) NYS_TQ(3, 3) NYS_TQ(3, 4)
+    NYS_TQ(4, 1) NYS_TQ(4, 2) NYS_TQ(4, 3) NYS_TQ(4, 4)
+#undef NYS_TQ
+    default: break;
+  }
+  if (rc) return rc;
+  double* part = rowpart + 2 * rows;
+  const unsigned blocks = (unsigned)tmax<int64_t>(1, tmin<int64_t>(cdiv(rows, 256), kTailSumBlocks));
+  tail_rowsums_kernel<<<blocks, 256, 0, st>>>(rows, NYS_LOSS_SQUARE, rowpart, T + 2 * rows, b, 1, part, pred);
+  NYS_CHECK_LAUNCH();
+  tail_rowsums_final<<<1, 32, 0, st>>>(part, (int)blocks, rowsums, pred);
+  NYS_CHECK_LAUNCH();
+  *Pout = P;
+  *splits_out = p.nclusters;
+  return NYS_OK;
+}
+
 // the tail's A{x,z} + loss epilogue + A^T{tg, thx, nu} in one pass; UNSUPPORTED
 // when the shape has no cluster plan (the caller runs the two-pass tail)
 int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
@@ -1144,7 +1594,14 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
   // warp evaluates the exp-based epilogue of each row) against 4.57 ms for the
   // two passes
   TcPlan p = tail_cluster_plan(rows, n, lda, A, x, z != nullptr);
-  if (!p.ok) return NYS_ERR_UNSUPPORTED;
+  if (!p.ok) {
+    // wider rows (config 5's n = 200000): the square loss with g_b has its own one-pass plan
+    if (!(gb && z && loss == NYS_LOSS_SQUARE) || cdiv(n, (int64_t)kHcC) <= 8 * kHqWarps * 32 * 2)
+      return NYS_ERR_UNSUPPORTED;
+    const int rq = tail_q(A, rows, n, lda, x, z, b, T, w, ws, ws_bytes, ws_off, rowsums, st, pred, Pout, splits_out);
+    if (rq == NYS_OK && sq_out) *sq_out = 1;
+    return rq;
+  }
   const int K3 = z ? 3 : 2;
   const size_t ncl = (size_t)(kNumSMs / p.C);
   const size_t need = ws_off + ncl * K3 * n * 8 + (2 * (size_t)rows + kTailSumBlocks * 5 + 8) * 8;

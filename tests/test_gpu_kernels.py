@@ -479,6 +479,39 @@ def test_ml_tail_sparse_z(kx, rows, n, dens, loss):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("rows,n,dens", [
+    (23, 200000, 0.005), (40, 150000, 0.01), (30, 120000, 0.0), (17, 229376, 0.02), (23, 200000, 0.2),
+    (12, 200000, 1.0), (300, 200000, 0.004), (9, 114690, 0.03)])
+def test_ml_tail_square_very_wide_rows(kx, rows, n, dens):
+    """The one-pass square-loss tail for rows beyond the whole-slice plan
+    (114688 < n <= 229376, config 5's n = 200000): x and the A^T(Az) accumulator
+    in tensor memory, z through its compacted nonzeros (tail_q_kernel); sparse,
+    empty, denser (several entries per thread) and dense z, every (Q, KQ) the
+    plan picks; against NumPy."""
+    g = np.random.default_rng(3 * rows + n + int(1e3 * dens))
+    A = g.standard_normal((rows, n)) / np.sqrt(n)
+    x, b = g.standard_normal(n), g.standard_normal(rows)
+    z = np.where(g.random(n) < dens, g.standard_normal(n), 0.0)
+    T, w, AT, rs = kx.empty(3, rows), kx.empty(rows), kx.empty(3, n), kx.zeros(8)
+    kx.ml_tail("square", dev(A), dev(x), dev(z), dev(b), T, w, AT, rs, gb=dev(A.T @ b))
+    ax, az = A @ x, A @ z
+    r1, r2 = ax - b, az - b
+    Tn = T.cpu().numpy()
+    np.testing.assert_allclose(Tn[0], r1, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(Tn[1], ax, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(Tn[2], r2, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(w.cpu().numpy(), np.ones(rows))
+    s = rs.cpu().numpy()
+    assert s[0] == pytest.approx(0.5 * r1 @ r1, rel=1e-12)
+    assert s[1] == pytest.approx(0.5 * r2 @ r2, rel=1e-12)
+    assert s[4] == pytest.approx(b @ r2, rel=1e-11, abs=1e-11)
+    ATn = AT.cpu().numpy()
+    scale = max(np.abs(A.T @ ax).max(), np.abs(A.T @ b).max(), np.abs(A.T @ az).max())
+    for j, ref in enumerate((A.T @ r1, A.T @ ax, A.T @ r2)):
+        np.testing.assert_allclose(ATn[j], ref, rtol=0, atol=1e-12 * scale)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("rows,n", [(400, 10000), (149, 7000), (64, 28000), (40, 50000), (23, 100000)])
 def test_ml_tail_square_two_products(kx, rows, n):
     """The square-loss one-pass tail given g_b = A^T b (nys_ml_tail_gb_f64):

@@ -45,8 +45,12 @@ def split():
 
 
 for name, f in (("cluster tail", fused), ("cluster tail with g_b", fused_gb), ("gemv_n + rowwise + gemv_t", split)):
-    for _ in range(3):
-        f()
+    try:
+        for _ in range(3):
+            f()
+    except Exception as e:  # no plan for this variant at this width
+        print(f"{name} {rows}x{n}: {type(e).__name__}")
+        continue
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(kx.stream)
