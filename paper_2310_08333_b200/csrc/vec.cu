@@ -633,6 +633,10 @@ __global__ void window_norms_kernel(int64_t n, const double* __restrict__ ring, 
 // admm_norms_kernel and the cycle-guard window norms of window_norms_kernel,
 // all reduced in one grid reduction.  Block b owns columns [64 b, 64 b + 64).
 constexpr int kEpiCols = 64;
+// CTAs of the epilogue (grid-stride over the column tiles, capped) and whether
+// their 33 partials each fit the reduction scratch
+static inline int64_t epi_blocks(int64_t n) { return tmin<int64_t>(cdiv(n, (int64_t)kEpiCols), 2 * kNumSMs); }
+static inline bool epi_fits(int64_t n) { return epi_blocks(n) * 33 <= (int64_t)kRedPartials * 16; }
 template <int K>
 __global__ void __launch_bounds__(256)
 ml_epilogue_kernel(int64_t n, const double* __restrict__ P, int splits, double* __restrict__ AT,
@@ -1202,7 +1206,7 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   if (t->kind == 0) {
     const int64_t woff0 = t->wnorms - t->norms;
     const bool fuse0 = !t->reduce && woff0 >= 16 && woff0 <= 64 &&
-                       cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
+                       epi_fits(n);
     // wide rows: the whole tail's data passes in one cluster stream over A
     // (hvp_cluster.cu: tail_cluster_kernel); else the row pass + GEMV^T below
     // (row-sharded: the same stream, its partials summed into this rank's AT,
@@ -1237,7 +1241,7 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
     // (row-sharded: the A^T outputs are all-reduced before the norms, so the
     // split sum cannot be fused with them)
     const bool fuse = !t->reduce && woff >= 16 && woff <= 64 &&
-                      cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
+                      epi_fits(n);
     if (fuse) {
       // A^T split partials, then one epilogue kernel: split sum -> AT, norms, window norms
       double* P = Pc;
@@ -1249,7 +1253,7 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
       SlotList sl;
       const int no = (t->ring && t->nothers > 0) ? t->nothers : 0;
       for (int j = 0; j < 16; ++j) sl.idx[j] = j < no ? t->others[j] : 0;
-      const unsigned eb = (unsigned)tmin<int64_t>(cdiv(n, (int64_t)kEpiCols), 2 * kNumSMs);
+      const unsigned eb = (unsigned)epi_blocks(n);
       const double* Pc = P;
       const double* uc = t->u;
       const double* ringc = t->ring;
@@ -1313,7 +1317,7 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
   // cycle-guard norms for the window after the append (admm.py:645-655);
   // the ML epilogue kernel already computed them when it ran fused
   const bool ml_fused = t->kind == 0 && !t->reduce && (t->wnorms - t->norms) >= 16 &&
-                        (t->wnorms - t->norms) <= 64 && cdiv(n, (int64_t)kEpiCols) * 33 <= (int64_t)kRedPartials * 16;
+                        (t->wnorms - t->norms) <= 64 && epi_fits(n);
   if (t->ring && t->nothers > 0 && !ml_fused) {
     SlotList sl;
     for (int j = 0; j < 16; ++j) sl.idx[j] = j < t->nothers ? t->others[j] : 0;

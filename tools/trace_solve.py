@@ -27,6 +27,8 @@ def main():
 
     if args.config == 4:
         d, opts, A = bench.build_cfg4_device(1, 0, False)
+    elif args.config == 5:
+        d, opts, A = bench.build_cfg5(1, 0)
     else:
         d, opts = bench.build_problem(args.config)
         A = torch.from_numpy(d.P if d.kind == "boxqp" else d.A).cuda()
