@@ -394,6 +394,10 @@ size_t nys_gemm_workspace(int64_t M, int64_t N, int64_t K);
 int nys_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
                  const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                  double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+/* Tuning / test hook of nys_gemm_f64's planner: every later call uses CTA tile
+ * shape `shape` (0 .. count-1; split-K still planned), -1 restores the cost
+ * model's choice.  Returns the number of tile shapes. */
+int nys_gemm_tile(int shape);
 /* The raw Gaussian test matrix itself (sketch.py:97-98): fills out[0..count)
  * with exactly np.random.Generator(PCG64).standard_normal(count) continued
  * from the given 128-bit PCG64 (state, inc) -- for default_rng(seed) that is

@@ -150,6 +150,7 @@ SIGNATURES = {
     "nys_box_project_f64": (I32, [I64, P, P, P, P, P]),
     "nys_row_scale_f64": (I32, [I64, I64, P, I64, P, P]),
     "nys_gemm_workspace": (SZ, [I64, I64, I64]),
+    "nys_gemm_tile": (I32, [I32]),
     "nys_gemm_f64": (I32, [I32, I32, I64, I64, I64, F64, P, I64, P, I64, F64, P, I64, P, SZ, P]),
     "nys_gaussian_workspace": (SZ, [I64]),
     "nys_gaussian_async_f64": (I32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, I64, P, P, P, SZ, P]),

@@ -28,10 +28,13 @@ namespace nys {
 // (gemm_plan) picks tile shape and split-K per call from a cost model of
 // padded work, wave quantisation and split-K partial traffic.
 constexpr int GBK = 16, GSTAGES = 3, GTHREADS = 256;
-constexpr int GWM = 4, GWN = 2;  // 8 warps: 4 along M, 2 along N
+// 8 warps: 4 along M x 2 along N for the 32/48/64-column tiles; the odd widths
+// (56, 136: picked so that ceil(N / BN) BN hugs a sketch width such as 133,
+// 258 or 390 -- the 48/64-column tiles pad those by 8-15 %) put all 8 along M
+constexpr int gemm_wn(int bn) { return (bn % 16 == 0 && bn <= 64) ? 2 : 1; }
 // shared-memory row strides (doubles) chosen so DMMA fragment loads are
 // 2-wavefront (conflict-free for 256 B per warp request)
-constexpr int kStrideKmaj(int mn) { return mn + 8; }  // tile stored [k][m]
+constexpr int kStrideKmaj(int mn) { return (mn + 15) / 16 * 16 + 8; }  // tile stored [k][m]: stride = 8 mod 16
 constexpr int kStrideMmaj = GBK + 4;                   // tile stored [m][k]
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
@@ -59,13 +62,14 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 // TA: op(A) = A^T (A stored K x M). TB: op(B) = B^T (B stored N x K).
 template <bool TA, bool TB, int BM, int BN>
 struct GemmCfg {
+  static constexpr int GWN = gemm_wn(BN), GWM = 8 / GWN;
   static constexpr int FM = BM / (GWM * 8), FN = BN / (GWN * 8);  // 8x8 fragments per warp
   static constexpr int A_ELEMS = TA ? GBK * kStrideKmaj(BM) : BM * kStrideMmaj;
   static constexpr int B_ELEMS = TB ? BN * kStrideMmaj : GBK * kStrideKmaj(BN);
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
   static constexpr size_t BYTES = (size_t)STAGE * GSTAGES * sizeof(double);
   static_assert(FM >= 1 && FN >= 1 && BM % (GWM * 8) == 0 && BN % (GWN * 8) == 0, "tile");
-  static_assert((BM * GBK) % GTHREADS == 0 && (BN * GBK) % GTHREADS == 0, "loader");
+  static_assert((BM * GBK) % GTHREADS == 0, "loader");
 };
 
 // VA: op(A) tiles loaded as 16-byte pairs (lda even, A 16-byte aligned)
@@ -76,7 +80,7 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
              double* __restrict__ C, int64_t ldc, int64_t k_per_split, double* __restrict__ P) {
   extern __shared__ __align__(16) double smem[];
   using S = GemmCfg<TA, TB, BM, BN>;
-  constexpr int FM = S::FM, FN = S::FN;
+  constexpr int FM = S::FM, FN = S::FN, GWM = S::GWM, GWN = S::GWN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % GWM, wn = warp / GWM;
   const int64_t n0 = (int64_t)blockIdx.x * BN, m0 = (int64_t)blockIdx.y * BM;
@@ -133,6 +137,86 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
     }
   };
 
+  // The loader of tiles wholly inside [kb, ke) -- every tile but a ragged last
+  // one: each thread's copies sit at fixed places of the tile, so their global
+  // pointers, shared-memory offsets and row / column validity are formed once
+  // and a tile costs one cp.async per copy plus one pointer advance (the
+  // general loader above recomputes 64-bit addresses and three bounds tests per
+  // copy; an ncu capture at 20000 x 258 x 100000 put 56 % of the kernel's
+  // instructions and two thirds of its stall samples there).
+  constexpr int NA = VA ? BM * GBK / 2 / GTHREADS : BM * GBK / GTHREADS;  // copies of op(A) per thread and tile
+  constexpr int NB = (BN * GBK + GTHREADS - 1) / GTHREADS;               // copies of op(B) (8 bytes each)
+  constexpr int AW = VA ? 2 : 1;                                          // doubles per copy of op(A)
+  constexpr int ACOLS = (TA ? BM : GBK) / AW;                             // copies per stored row of the A tile
+  constexpr int ARPP = GTHREADS / ACOLS;                                  // stored rows per pass of the CTA
+  constexpr int ASTRIDE = TA ? kStrideKmaj(BM) : kStrideMmaj;
+  const int ar = tid / ACOLS, ac = (tid - ar * ACOLS) * AW;
+  const double* pA = TA ? A + (kb + ar) * lda + m0 + ac : A + (m0 + ar) * lda + kb + ac;
+  const int64_t a_step = (int64_t)ARPP * lda;
+  const int sa0 = ar * ASTRIDE + ac;
+  unsigned a_mask = 0;  // !TA: rows of the tile inside M
+  int a_nv = AW;        // TA: doubles of this thread's copy inside M (the same for every k row)
+  if (TA) {
+    a_nv = (int)tmax<int64_t>(0, tmin<int64_t>(AW, M - (m0 + ac)));
+  } else {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) a_mask |= (m0 + ar + i * ARPP < M ? 1u : 0u) << i;
+  }
+  const double* pB;
+  int b_g[NB], b_s[NB];  // !TB: global and shared offsets of copy i (TB: uniform strides)
+  unsigned b_mask = 0;
+  if (TB) {
+    const int br = tid / GBK, bc = tid - br * GBK;
+    pB = B + (n0 + br) * ldb + kb + bc;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      b_g[i] = 0;
+      b_s[i] = (br + i * (GTHREADS / GBK)) * kStrideMmaj + bc;
+      b_mask |= ((br + i * (GTHREADS / GBK) < BN && n0 + br + i * (GTHREADS / GBK) < N) ? 1u : 0u) << i;
+    }
+  } else {
+    pB = B + kb * ldb + n0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int e = tid + i * GTHREADS, kk = e / BN, nn = e - kk * BN;
+      b_g[i] = kk * (int)ldb + nn;
+      b_s[i] = kk * kStrideKmaj(BN) + nn;
+      b_mask |= ((e < BN * GBK && n0 + nn < N) ? 1u : 0u) << i;
+    }
+  }
+  const int64_t b_step = (int64_t)(GTHREADS / GBK) * ldb;  // TB: rows of B between a thread's copies
+  const bool fast_ok = TB || ldb < (int64_t)(1 << 26);     // b_g in 32 bits
+  auto load_fast = [&](int stage) {
+    double* As = smem + stage * S::STAGE;
+    double* Bs = As + S::A_ELEMS;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const int nv = TA ? a_nv : (((a_mask >> i) & 1u) ? AW : 0);
+      const double* src = nv ? pA + i * a_step : A;
+      if (VA)
+        cp_async16(As + sa0 + i * (ARPP * ASTRIDE), src, nv);
+      else
+        cp_async8(As + sa0 + i * (ARPP * ASTRIDE), src, nv != 0);
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      if (!TB && (i + 1) * GTHREADS > BN * GBK && tid + i * GTHREADS >= BN * GBK) continue;  // past the tile
+      if (TB && (i + 1) * (GTHREADS / GBK) > BN && tid / GBK + i * (GTHREADS / GBK) >= BN) continue;
+      const bool v = (b_mask >> i) & 1u;
+      const double* src = v ? (TB ? pB + i * b_step : pB + b_g[i]) : B;
+      cp_async8(Bs + b_s[i], src, v);
+    }
+    pA += TA ? (int64_t)GBK * lda : (int64_t)GBK;
+    pB += TB ? (int64_t)GBK : (int64_t)GBK * ldb;
+  };
+  // tiles are loaded in order, so the fast loader's pointers always stand at the next one
+  auto load_any = [&](int stage, int64_t k0) {
+    if (fast_ok && k0 + GBK <= ke)
+      load_fast(stage);
+    else
+      load_tile(stage, k0);
+  };
+
   double acc[FM][FN][2];
 #pragma unroll
   for (int i = 0; i < FM; ++i)
@@ -141,7 +225,7 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
 
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) {
-    if (s < ktiles) load_tile(s, kb + (int64_t)s * GBK);
+    if (s < ktiles) load_any(s, kb + (int64_t)s * GBK);
     cp_async_commit();
   }
   const int fr = lane >> 2, fc = lane & 3;
@@ -150,7 +234,7 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
     __syncthreads();
     {  // prefetch tile kt + STAGES - 1
       const int nk = kt + GSTAGES - 1;
-      if (nk < ktiles) load_tile(nk % GSTAGES, kb + (int64_t)nk * GBK);
+      if (nk < ktiles) load_any(nk % GSTAGES, kb + (int64_t)nk * GBK);
       cp_async_commit();
     }
     const double* As = smem + (kt % GSTAGES) * S::STAGE;
@@ -216,9 +300,17 @@ struct TileShape {
   int bm, bn;
   double eff;
 };
-constexpr int kNumShapes = 5;
-static const TileShape kShapes[kNumShapes] = {
-    {128, 64, 1.00}, {128, 48, 0.96}, {64, 64, 0.90}, {64, 48, 0.86}, {64, 32, 0.78}};
+// (eff from tools/gemm_bench.py on B200, in padded work per second: the DMMA
+// stream runs at 30-33 TF/s of padded work for every shape, so the narrow-
+// padding shapes gain where their own efficiency holds up)
+constexpr int kNumShapes = 7;
+static const TileShape kShapes[kNumShapes] = {{128, 64, 1.00}, {128, 48, 1.00}, {64, 64, 0.97}, {64, 48, 0.98},
+                                              {64, 32, 0.92},  {128, 56, 0.95}, {128, 136, 0.92}};
+// every shape of the table, by index (the instantiation lists below)
+#define NYS_GEMM_SHAPES(X) X(0, 128, 64) X(1, 128, 48) X(2, 64, 64) X(3, 64, 48) X(4, 64, 32) X(5, 128, 56) X(6, 128, 136)
+
+// tile shape every plan must use (nys_gemm_tile: tuning / test hook), -1: the cost model's choice
+static int g_gemm_tile = -1;
 
 struct GemmPlan {
   int shape = 0, splits = 1;
@@ -246,11 +338,11 @@ static int gemm_occ_k() {
 template <bool TA, bool TB>
 static int gemm_occ_t(int shape) {
   switch (shape) {
-    case 0: return gemm_occ_k<TA, TB, 128, 64>();
-    case 1: return gemm_occ_k<TA, TB, 128, 48>();
-    case 2: return gemm_occ_k<TA, TB, 64, 64>();
-    case 3: return gemm_occ_k<TA, TB, 64, 48>();
-    default: return gemm_occ_k<TA, TB, 64, 32>();
+#define NYS_X(i, bm, bn) \
+  case i: return gemm_occ_k<TA, TB, bm, bn>();
+    NYS_GEMM_SHAPES(NYS_X)
+#undef NYS_X
+    default: return 1;
   }
 }
 static int gemm_occ(int ta, int tb, int shape) {
@@ -265,8 +357,7 @@ static int gemm_occ(int ta, int tb, int shape) {
 // CTA's padded work; waves = ceil(CTAs / (148 O)).  Split-K adds the partial
 // traffic (write + read) and one reduction launch.
 static GemmPlan gemm_plan(int ta, int tb, int64_t M, int64_t N, int64_t K, size_t ws_cap) {
-  const char* force = getenv("NYS_GEMM_SHAPE");
-  const int only = force ? atoi(force) : -1;
+  const int only = g_gemm_tile;
   GemmPlan best;
   double best_t = 1e300;
   const double sm_rate = 68.0 * 1.9e9;  // FP64 DMMA FMA/s per SM (~40 TF/148)
@@ -345,11 +436,11 @@ static int gemm_launch(int64_t M, int64_t N, int64_t K, double alpha, const doub
                        int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
   const GemmPlan pl = gemm_plan(TA ? 1 : 0, TB ? 1 : 0, M, N, K, ws ? ws_bytes : 0);
   switch (pl.shape) {
-    case 0: return gemm_launch_shape<TA, TB, 128, 64>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
-    case 1: return gemm_launch_shape<TA, TB, 128, 48>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
-    case 2: return gemm_launch_shape<TA, TB, 64, 64>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
-    case 3: return gemm_launch_shape<TA, TB, 64, 48>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
-    default: return gemm_launch_shape<TA, TB, 64, 32>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
+#define NYS_X(i, bm, bn) \
+  case i: return gemm_launch_shape<TA, TB, bm, bn>(pl, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, st);
+    NYS_GEMM_SHAPES(NYS_X)
+#undef NYS_X
+    default: return NYS_ERR_ARG;
   }
 }
 
@@ -1002,6 +1093,11 @@ static int nystrom_core(int64_t n, int s, int r, const double* Q, double* Y, dou
 using namespace nys;
 
 extern "C" size_t nys_gemm_workspace(int64_t M, int64_t N, int64_t K) { return gemm_ws(M, N, K); }
+
+extern "C" int nys_gemm_tile(int shape) {
+  nys::g_gemm_tile = (shape >= 0 && shape < nys::kNumShapes) ? shape : -1;
+  return nys::kNumShapes;
+}
 
 extern "C" int nys_gemm_f64(int transA, int transB, int64_t M, int64_t N, int64_t K, double alpha,
                             const double* A, int64_t lda, const double* B, int64_t ldb,

@@ -176,18 +176,21 @@ def test_syevj_degenerate_spectra(kx, kind, s):
     np.testing.assert_allclose(M @ Vn, Vn * wn, atol=1e-11 * scale * s)
 
 
-@pytest.mark.parametrize("shape", [0, 1, 2, 3, 4])
-@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1)])
-@pytest.mark.parametrize("M,N,K", [(5000, 133, 3000), (133, 133, 10000), (77, 45, 33)])
-def test_dgemm_every_tile_shape(kx, monkeypatch, shape, ta, tb, M, N, K):
-    """Each CTA tile shape of the planner (NYS_GEMM_SHAPE forces it), with
+@pytest.mark.parametrize("shape", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(5000, 133, 3000), (133, 133, 10000), (77, 45, 33), (300, 258, 1001)])
+def test_dgemm_every_tile_shape(kx, shape, ta, tb, M, N, K):
+    """Each CTA tile shape of the planner (nys_gemm_tile forces it), with
     split-K where the planner picks it, against NumPy FP64."""
-    monkeypatch.setenv("NYS_GEMM_SHAPE", str(shape))
     g = np.random.default_rng(M * 7 + N + K + shape)
     A = g.standard_normal((K, M) if ta else (M, K))
     B = g.standard_normal((N, K) if tb else (K, N))
     Cd = kx.empty(M, N)
-    kx.gemm(ta, tb, M, N, K, 1.0, dev(A), A.shape[1], dev(B), B.shape[1], 0.0, Cd, N)
+    assert kx.L.nys_gemm_tile(shape) == 7
+    try:
+        kx.gemm(ta, tb, M, N, K, 1.0, dev(A), A.shape[1], dev(B), B.shape[1], 0.0, Cd, N)
+    finally:
+        kx.L.nys_gemm_tile(-1)
     ref = (A.T if ta else A) @ (B.T if tb else B)
     np.testing.assert_allclose(Cd.cpu().numpy(), ref, rtol=1e-11, atol=1e-12 * np.sqrt(K) * 10)
 
