@@ -1584,6 +1584,13 @@ static int tail_q(const double* A, int64_t rows, int64_t n, int64_t lda, const d
   return NYS_OK;
 }
 
+// true when the only one-pass plan for this shape is tail_q (rows beyond the
+// whole-slice plan): it visits z through its nonzeros, so callers whose prox
+// leaves z dense (no l1 term) keep the two streaming passes there
+bool tail_wants_sparse_z(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x) {
+  return !tail_cluster_plan(rows, n, lda, A, x, true).ok && tail_q_plan(rows, n, lda, A, x).ok;
+}
+
 // the tail's A{x,z} + loss epilogue + A^T{tg, thx, nu} in one pass; UNSUPPORTED
 // when the shape has no cluster plan (the caller runs the two-pass tail)
 int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,

@@ -1168,6 +1168,7 @@ int tail_cluster(const double* A, int64_t rows, int64_t n, int64_t lda, const do
                  const double* b, int loss, double* T, double* w, void* ws, size_t ws_bytes, size_t ws_off,
                  double* rowsums, cudaStream_t st, const double* pred, double** Pout, int* splits_out,
                  const double* gb, int* sq_out);
+bool tail_wants_sparse_z(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x);
 int tail_partial_sum(const double* P, int64_t n, int K, int ncl, double* AT, const double* gb, cudaStream_t st,
                      const double* pred);
 int xz_rowpass(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
@@ -1213,7 +1214,10 @@ extern "C" int nys_admm_tail_f64(const nys_admm_tail* t, void* stream) {
     // which is all-reduced before the norms)
     double* Pc = nullptr;
     int csplits = 0, csq = 0;
-    if (fuse0 || t->reduce) {
+    // (without an l1 term the prox leaves z dense: the very-wide-row plan, which
+    // walks z's nonzeros, would lose to the two passes)
+    const bool dense_z = t->with_z && !(t->kappa > 0.0) && tail_wants_sparse_z(t->A, t->rows, n, t->lda, x);
+    if ((fuse0 || t->reduce) && !dense_z) {
       rc = tail_cluster(t->A, t->rows, n, t->lda, x, t->with_z ? z : nullptr, t->b, t->loss, t->T, t->w, t->ws_gemvT,
                         t->ws_gemvT_bytes, (kRedPartials * 16 + 64) * sizeof(double), t->rowsums, st, pred, &Pc,
                         &csplits, t->gb, &csq);
