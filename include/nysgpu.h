@@ -381,6 +381,10 @@ int nys_qp_infeas_f64(int64_t n, const double* xa, const double* xb, const doubl
 /* elementwise helpers used by the operator API */
 int nys_axpby_f64(int64_t n, double a, const double* x, double b, double* y, void* stream);
 int nys_soft_threshold_f64(int64_t n, const double* v, double kappa, double* out, void* stream);
+/* out[i] = the loss (NYS_LOSS_*) evaluated elementwise at w[i]: what = 0 value,
+ * 1 first derivative, 2 second derivative, 3 convex conjugate (+inf outside its
+ * domain) -- the callables of the reference's Loss (problems.py:35-111). */
+int nys_loss_eval_f64(int loss, int what, int64_t n, const double* w, double* out, void* stream);
 int nys_box_project_f64(int64_t n, const double* v, const double* lo, const double* hi,
                         double* out, void* stream);
 int nys_row_scale_f64(int64_t rows, int64_t cols, double* X, int64_t ldx, const double* d,

@@ -147,6 +147,7 @@ SIGNATURES = {
     "nys_qp_infeas_f64": (I32, [I64, P, P, P, P, F64, P, P, P, P, P, P, P]),
     "nys_axpby_f64": (I32, [I64, F64, P, F64, P, P]),
     "nys_soft_threshold_f64": (I32, [I64, P, F64, P, P]),
+    "nys_loss_eval_f64": (I32, [I32, I32, I64, P, P, P]),
     "nys_box_project_f64": (I32, [I64, P, P, P, P, P]),
     "nys_row_scale_f64": (I32, [I64, I64, P, I64, P, P]),
     "nys_gemm_workspace": (SZ, [I64, I64, I64]),

@@ -137,6 +137,12 @@ class SolverState:
 
 @dataclass
 class Residuals:
+    """admm.py:36-43 (same field order).  The engines fill the norms from their
+    fused reductions and leave the vectors None; the single-step API
+    (``compute_residuals``) returns them."""
+
+    rp: Optional[np.ndarray]
+    rd: Optional[np.ndarray]
     rp_norm: float
     rd_norm: float
     primal_scale: float
@@ -781,7 +787,7 @@ class _Engine:
             rp, rd, nx, nz, nru = s[1], s[3], s[5], s[7], s[9]
         else:
             rp, rd, nx, nz, nru = (math.sqrt(max(s[i], 0.0)) for i in (0, 2, 4, 6, 8))
-        return Residuals(rp, rd, max(nx, nz, 0.0), nru, self.n)
+        return Residuals(None, None, rp, rd, max(nx, nz, 0.0), nru, self.n)
 
     def _objective(self, st) -> float:
         s = st[_S_NORMS:]
@@ -1320,8 +1326,6 @@ def solve(problem, options: Optional[SolverOptions] = None, x0=None, z0=None, u0
     t_start = time.perf_counter()
     options = options or SolverOptions()
     gp = lower(problem)
-    if gp.ml is None and gp.qp is None:
-        raise CapabilityError("generic problems (user f/prox callables) are outside the B200 path")
     if kernels is None:
         from .kernels import get_kernels
 
@@ -1343,4 +1347,26 @@ def _dense_path(gp: GenericProblem) -> bool:
     matrix with M = I (BASELINE.json's configs)."""
     if gp.ml is not None:
         return isinstance(gp.ml.A, DenseOperator) and gp.ml.loss.kind in _lib.LOSS
+    if gp.qp is None:
+        return False  # oracles given as callables (GenericProblem): the general engine
     return isinstance(gp.qp.P, DenseOperator) and isinstance(gp.qp.M, IdentityOperator)
+
+
+# the reference's single-step API (admm.py:215-415) and the names its admm module
+# re-exports; imported last: steps.py needs the classes above
+from .krylov import pcg  # noqa: E402,F401
+from .operators import MatrixFreeOperator  # noqa: E402,F401
+from .problems import ml_dual_gap  # noqa: E402,F401
+from .prox import box_recession_distance, box_support  # noqa: E402,F401
+from .sketch import estimate_extreme_eigs, nystrom_sketch  # noqa: E402,F401
+from .steps import (  # noqa: E402,F401
+    InfeasibilityCheck,
+    check_infeasibility,
+    check_termination,
+    compute_residuals,
+    relaxed_constraint_point,
+    u_update,
+    update_penalty,
+    x_update,
+    z_update,
+)

@@ -115,3 +115,33 @@ def portfolio_operator_qp(d, F, mu, gamma: float):
     lo = np.concatenate([[1.0], np.zeros(n)])
     hi = np.concatenate([[1.0], np.full(n, np.inf)])
     return QPProblem(DiagPlusLowRank(gamma * d, np.sqrt(gamma) * F), -mu, M, Box(lo, hi))
+
+
+def portfolio_generic_problem(d, F, mu, gamma: float, prox_tol: float = 1e-8):
+    """The splitting form with the simplex handled by direct projection
+    (datagen.py:184-214): f(x) = (gamma/2) x'(D + F F')x - mu'x with a
+    diagonal-plus-low-rank Hessian, g the simplex indicator with an inexact
+    (bisection) projection as its prox."""
+    import torch
+
+    from ..operators import ConstantHessian, DiagPlusLowRank, IdentityOperator, device_fn, like_input, to_device
+    from ..problems import GenericProblem
+    from ..prox import simplex_indicator, simplex_project
+
+    d, F, mu = (np.asarray(a, dtype=float) for a in (d, F, mu))
+    n = d.size
+    P = DiagPlusLowRank(gamma * d, np.sqrt(gamma) * F)
+
+    @device_fn
+    def f(x):
+        xt = to_device(x)
+        return 0.5 * float(torch.dot(xt, P._apply_dev(xt))) - float(torch.dot(to_device(mu), xt))
+
+    @device_fn
+    def grad(x):
+        xt = to_device(x)
+        return like_input(P._apply_dev(xt) - to_device(mu), x)
+
+    return GenericProblem(n=n, m=n, f=f, grad_f=grad, hess=ConstantHessian(P), g=device_fn(lambda z: simplex_indicator(z)),
+                          prox_g=device_fn(lambda v, rho, tol: simplex_project(v, min(tol, prox_tol))),
+                          M=IdentityOperator(n), c=np.zeros(n), is_quadratic=True, full_rank=True, prox_inexact=True)

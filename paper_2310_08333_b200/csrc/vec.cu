@@ -867,6 +867,18 @@ __global__ void soft_kernel(int64_t n, const double* __restrict__ v, double kapp
     o[i] = soft1(v[i], kappa);
 }
 
+// elementwise loss evaluation (problems.py:35-111): what = 0 value, 1 first
+// derivative, 2 second derivative, 3 conjugate (+inf outside its domain)
+__global__ void loss_eval_kernel(int loss, int what, int64_t n, const double* __restrict__ w,
+                                 double* __restrict__ o) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = w[i];
+    o[i] = what == 0 ? loss_val(loss, x) : what == 1 ? loss_d1(loss, x) : what == 2 ? loss_d2(loss, x)
+                                                                                    : loss_conj(loss, x);
+  }
+}
+
 __global__ void box_kernel(int64_t n, const double* __restrict__ v, const double* __restrict__ lo,
                            const double* __restrict__ hi, double* __restrict__ o) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1133,6 +1145,13 @@ extern "C" int nys_soft_threshold_f64(int64_t n, const double* v, double kappa, 
                                       void* stream) {
   if (n <= 0 || kappa < 0) return NYS_ERR_ARG;
   soft_kernel<<<vec_blocks(n), kVecThreads, 0, as_stream(stream)>>>(n, v, kappa, out);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" int nys_loss_eval_f64(int loss, int what, int64_t n, const double* w, double* out, void* stream) {
+  if (n <= 0 || what < 0 || what > 3 || loss < NYS_LOSS_SQUARE || loss > NYS_LOSS_HUBER) return NYS_ERR_ARG;
+  loss_eval_kernel<<<vec_blocks(n), kVecThreads, 0, as_stream(stream)>>>(loss, what, n, w, out);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -34,9 +34,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import DataError
+from .errors import CapabilityError, DataError
 from .krylov import CgReport, CgWork, cg_tolerance, pcg_device
-from .operators import (IdentityOperator, LinearOperator, MatrixFreeOperator, SparseOperator, adjoint_columns_dev,
+from .operators import (IdentityOperator, LinearOperator, MatrixFreeOperator, SparseOperator, UserFn, adjoint_columns_dev,
+                        device_fn,
                         to_device)
 from .problems import GenericProblem
 from .sketch import NystromPreconditioner, NystromSketch, default_sketch_rank, sketch_device
@@ -156,6 +157,23 @@ class _MLPart:
         return self.a_adj(self.tg, self.l2, x) if self.l2 != 0.0 else self.a_adj(self.tg)
 
 
+class _GenericPart:
+    """The oracles of a GenericProblem given as callables (problems.py:125-157):
+    f, grad f, the Hessian operator, g and its (possibly inexact) prox.  NumPy
+    callables, the reference's contract, get host copies; callables marked
+    ``device_fn`` get the device tensors (operators.UserFn); everything around them -- the PCG solve, the
+    sketch, residuals, windows, penalty logic -- is the engine's device path."""
+
+    def __init__(self, gp: GenericProblem):
+        missing = [nm for nm in ("f", "grad_f", "hess", "g", "prox_g") if getattr(gp, nm) is None]
+        if missing:
+            raise CapabilityError(f"generic problem without {', '.join(missing)}: nothing to solve")
+        if np.any(gp.c != 0.0):
+            raise CapabilityError("generic problems with a nonzero offset c are outside the B200 path")
+        self.f, self.grad_f, self.g, self.prox_g = UserFn(gp.f), UserFn(gp.grad_f), UserFn(gp.g), UserFn(gp.prox_g)
+        self.hess = gp.hess
+
+
 class _GeneralEngine:
     def __init__(self, gp: GenericProblem, opts, kx):
         self.gp, self.opts, self.kx = gp, opts, kx
@@ -163,7 +181,12 @@ class _GeneralEngine:
         self.M: LinearOperator = gp.M
         self.identity_M = isinstance(gp.M, IdentityOperator)
         self.ml = _MLPart(gp.ml, kx) if gp.ml is not None else None
-        if self.ml is None:
+        self.gen = _GenericPart(gp) if gp.ml is None and gp.qp is None else None
+        if self.gen is not None:
+            self.P = self.gen.hess
+            self.const_hess = bool(getattr(self.gen.hess, "is_constant", False)) or gp.is_quadratic
+            self.diag_shift = float(getattr(self.gen.hess, "diag_shift", 0.0))
+        elif self.ml is None:
             qp = gp.qp
             self.P = qp.P
             self.q = to_device(qp.q, kx.device)
@@ -195,7 +218,11 @@ class _GeneralEngine:
             return self._grad_x[1], self._grad_x[2]
         kx = self.kx
         fout = self.stats.slot(8)
-        if self.ml:
+        if self.gen:
+            g = self.gen.grad_f(x)
+            fout.zero_()
+            fout[0:1].fill_(self.gen.f.scalar(x))
+        elif self.ml:
             self.ml.evaluate(x, fout)
             g = self.ml.grad(x)
             kx.dot(x, x, fout[5:6])
@@ -209,19 +236,26 @@ class _GeneralEngine:
         return g, fout
 
     def f_value(self, fout_h) -> float:
+        if self.gen:
+            return float(fout_h[0])
         if self.ml:
             return float(fout_h[0]) + 0.5 * self.ml.l2 * float(fout_h[5])  # problems.py:227-230
         return 0.5 * float(fout_h[0]) + float(fout_h[1])  # problems.py:396-397
 
     def g_launch(self, z):
         out = self.stats.slot(3)
-        if self.ml:
+        if self.gen:
+            out.zero_()
+            out[0:1].fill_(self.gen.g.scalar(z))
+        elif self.ml:
             self.kx.absstats(z, self.ml.l1, out)
         else:
             self.kx.box_violation(z, self.lo, self.hi, out)
         return out
 
     def g_value(self, o) -> float:
+        if self.gen:
+            return float(o[0])
         if self.ml:
             return self.ml.l1 * float(o[0])
         scale = 1.0 + float(o[2])  # prox.py:138-144
@@ -276,6 +310,8 @@ class _GeneralEngine:
     def sketch_cols(self, rho):
         kx = self.kx
         if self.identity_M:
+            if self.gen:
+                return self.gen.hess.smooth_part().apply_columns_dev
             if self.ml:
                 return self.ml.smooth_cols  # hess.smooth_part() (problems.py:266-273)
             return self.P.apply_columns_dev  # ConstantHessian: diag_shift == 0
@@ -320,6 +356,8 @@ class _GeneralEngine:
         bar_count = 0
         self._xver += 1
         g_x, _ = self.eval_at_x(x)
+        if self.gen:
+            self.gen.hess.update(x)
         if self.ml:
             self.ml.update_hessian()  # hess.update(x0) (admm.py:455)
         Mx = self.M_apply(x).clone()
@@ -330,8 +368,8 @@ class _GeneralEngine:
             sigma_eff = 0.0
         elif opts.check_rank:
             rho_probe = rho
-            probe = MatrixFreeOperator(n, n, lambda v: self.composite(to_device(v), rho_probe),
-                                       lambda v: self.composite(to_device(v), rho_probe))
+            probe = MatrixFreeOperator(n, n, device_fn(lambda v: self.composite(to_device(v), rho_probe)),
+                                       device_fn(lambda v: self.composite(to_device(v), rho_probe)))
             _, lam_min = estimate_extreme_eigs(probe, min(max(2, n), 60), opts.rng_seed + 7)
             if lam_min > 1e-8:
                 sigma_eff = 0.0
@@ -381,7 +419,7 @@ class _GeneralEngine:
                 rd, ds = float(d[2]), float(d[3])
             else:
                 rd, ds = math.sqrt(max(d[0], 0.0)), math.sqrt(max(d[1], 0.0))
-            return Residuals(rp, rd, max(nmx, nz, 0.0), ds, m)
+            return Residuals(None, None, rp, rd, max(nmx, nz, 0.0), ds, m)
 
         def offs(t):
             return int(t.data_ptr() - self.stats.dev.data_ptr()) // 8
@@ -426,6 +464,8 @@ class _GeneralEngine:
             if opts.time_limit is not None and time.perf_counter() - t_start > opts.time_limit:
                 status = Status.TIME_LIMIT
                 break
+            if self.gen and not self.const_hess:
+                self.gen.hess.update(x)  # admm.py:539-540
             if self.ml and not self.const_hess:
                 self.eval_at_x(x)
                 self.ml.update_hessian()
@@ -479,7 +519,18 @@ class _GeneralEngine:
             x = x_new
             self._xver += 1
             Mx = Mx_new
-            if self.ml:
+            if self.gen:
+                # w = alpha Mx + (1 - alpha) z; z = prox_g(w + u, rho, tol_k); u += w - z with
+                # tol_k = prox_tol0 / k^(2 gamma) (admm.py:278-300)
+                w = Mx.clone()
+                kx.axpby(1.0 - opts.alpha, z, opts.alpha, w)
+                v = w.clone()
+                kx.axpby(1.0, u, 1.0, v)
+                prox_tol = opts.prox_tol0 / max(k, 1) ** (2.0 * opts.gamma)
+                z = self.gen.prox_g(v, rho, max(prox_tol, 1e-15)).clone()
+                kx.axpby(1.0, w, 1.0, u)
+                kx.axpby(-1.0, z, 1.0, u)
+            elif self.ml:
                 kx.admm_zu(Mx, z, u, opts.alpha, _lib.PROX_SOFT, self.ml.l1 / rho, None, None, None, None, False)
             else:
                 kx.admm_zu(Mx, z, u, opts.alpha, _lib.PROX_BOX, 0.0, lo, hi, None, None, False)
@@ -678,6 +729,8 @@ class _GeneralEngine:
         kx.axpby(0.0, zb, 1.0 / bar_count, zb)
         st = _Stats(kx, 16)
         fo = st.slot(8)
+        if self.gen:
+            return self.gen.f.scalar(xb) + self.gen.g.scalar(zb)
         if self.ml:
             kx.ml_rowwise(self.ml.loss, self.ml.a_fwd(xb), None, self.ml.b, None, None, None, None, fo)
             kx.dot(xb, xb, fo[5:6])

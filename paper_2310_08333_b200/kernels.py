@@ -286,6 +286,12 @@ class Kernels:
         self.launches += 1
         check(self.L.nys_axpby_f64(x.numel(), float(a), x.data_ptr(), float(b), y.data_ptr(), self.sp), "axpby")
 
+    def loss_eval(self, loss: str, what: int, w, out) -> None:
+        """out = loss value (0) / l' (1) / l'' (2) / conjugate (3) elementwise at w."""
+        self.launches += 1
+        check(self.L.nys_loss_eval_f64(_lib.LOSS[loss], int(what), w.numel(), w.data_ptr(), out.data_ptr(), self.sp),
+              "loss_eval")
+
     def soft_threshold(self, v, kappa, out) -> None:
         self.launches += 1
         check(self.L.nys_soft_threshold_f64(v.numel(), v.data_ptr(), float(kappa), out.data_ptr(), self.sp),

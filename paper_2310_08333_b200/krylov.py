@@ -157,7 +157,7 @@ def pcg_batched(work: CgWork, pb, max_iter: int, first_batch: int = 2, max_batch
     return CgReport(iters if done == 4 else max_iter, resrel, False)
 
 
-def _matvec_for(A) -> MatvecInto:
+def _matvec_for(A, host_io: bool = False) -> MatvecInto:
     from .kernels import get_kernels
 
     kx = get_kernels()
@@ -174,6 +174,10 @@ def _matvec_for(A) -> MatvecInto:
 
             return mv
         f = A._apply_dev
+    elif host_io:
+        # a caller working in NumPy hands in NumPy callables (krylov.py:35-44): its
+        # own code runs on the host, the CG vectors and reductions stay on the device
+        f = lambda v: to_device(np.asarray(A(v.cpu().numpy()), dtype=float))
     else:
         f = lambda v: to_device(A(v))
 
@@ -185,7 +189,7 @@ def _matvec_for(A) -> MatvecInto:
     return mv
 
 
-def _precond_for(Minv) -> Optional[PrecondInto]:
+def _precond_for(Minv, host_io: bool = False) -> Optional[PrecondInto]:
     if Minv is None:
         return None
     from .kernels import get_kernels
@@ -198,7 +202,7 @@ def _precond_for(Minv) -> Optional[PrecondInto]:
         return lambda v, out, rdot, rz: pc.apply_into(kx, v, out, rdot, rz)
 
     def pre(v, out, rdot, rz):
-        out.copy_(to_device(Minv(v)))
+        out.copy_(to_device(np.asarray(Minv(v.cpu().numpy()), dtype=float)) if host_io else to_device(Minv(v)))
         if rz is not None:
             kx.dot(rdot, out, rz)
 
@@ -218,5 +222,6 @@ def pcg(A, b, x0=None, Minv=None, tol_rel: float = 1e-8, max_iter: Optional[int]
         max_iter = 10 * n
     x = torch.zeros_like(bt) if x0 is None else to_device(x0).clone()
     work = CgWork(kx, n)
-    rep = pcg_device(work, _matvec_for(A), bt, x, _precond_for(Minv), tol_rel, max_iter)
+    host_io = not isinstance(b, torch.Tensor)
+    rep = pcg_device(work, _matvec_for(A, host_io), bt, x, _precond_for(Minv, host_io), tol_rel, max_iter)
     return like_input(x, b), rep

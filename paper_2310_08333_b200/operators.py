@@ -52,6 +52,42 @@ def like_input(t: torch.Tensor, ref):
     return t.cpu().numpy()
 
 
+def device_fn(fn: Callable) -> Callable:
+    """Mark a callable as taking and returning CUDA tensors (see ``UserFn``)."""
+    fn.accepts_device = True
+    return fn
+
+
+class UserFn:
+    """A callable supplied through the reference's API (a matrix-free operator's
+    matvec, a Hessian-vector product, f / grad f / prox of a GenericProblem).
+    The reference's contract is NumPy in, NumPy out, so that is what an unmarked
+    callable gets: host copies of the device vectors, its result sent straight
+    back.  The user's code is then the only thing that runs on the host.
+    Callables marked with ``device_fn`` (this package's own lowered oracles, or
+    device-aware user code) get the CUDA tensors themselves."""
+
+    def __init__(self, fn: Callable):
+        self.fn = fn
+        self.host = not getattr(fn, "accepts_device", False)
+
+    @staticmethod
+    def _to_host(a):
+        return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a
+
+    def raw(self, *args):
+        if self.host:
+            return self.fn(*[self._to_host(a) for a in args])
+        return self.fn(*args)
+
+    def __call__(self, *args) -> torch.Tensor:
+        out = self.raw(*args)
+        return to_device(out if isinstance(out, torch.Tensor) else np.asarray(out, dtype=float))
+
+    def scalar(self, *args) -> float:
+        return float(self.raw(*args))
+
+
 class LinearOperator:
     """A map v -> Av with known dimensions and an optional adjoint
     (operators.py:20-73)."""
@@ -588,23 +624,24 @@ def adjoint_columns_dev(op: LinearOperator, U: torch.Tensor) -> torch.Tensor:
 
 
 class MatrixFreeOperator(LinearOperator):
-    """Operator defined by device callables (operators.py:206-228): ``matvec``
-    and ``rmatvec`` take and return CUDA tensors."""
+    """Operator defined by callables (operators.py:206-228): ``matvec`` and
+    ``rmatvec`` on CUDA tensors, or NumPy-only callables as the reference takes
+    them (``UserFn``)."""
 
     def __init__(self, input_dim: int, output_dim: int, matvec: Callable, rmatvec: Optional[Callable] = None):
         super().__init__(input_dim, output_dim)
-        self._matvec = matvec
-        self._rmatvec = rmatvec
+        self._matvec = UserFn(matvec)
+        self._rmatvec = UserFn(rmatvec) if rmatvec is not None else None
 
     @property
     def has_adjoint(self) -> bool:
         return self._rmatvec is not None
 
     def _apply_dev(self, v):
-        return to_device(self._matvec(v))
+        return self._matvec(v)
 
     def _apply_adjoint_dev(self, u):
-        return to_device(self._rmatvec(u))
+        return self._rmatvec(u)
 
 
 class HessianOperator(LinearOperator):
@@ -626,8 +663,8 @@ class HessianOperator(LinearOperator):
         shift = self.diag_shift
         return MatrixFreeOperator(
             self.input_dim, self.output_dim,
-            lambda v: self._apply_dev(to_device(v)) - shift * to_device(v),
-            lambda u: self._apply_dev(to_device(u)) - shift * to_device(u),
+            device_fn(lambda v: self._apply_dev(to_device(v)) - shift * to_device(v)),
+            device_fn(lambda u: self._apply_dev(to_device(u)) - shift * to_device(u)),
         )
 
     def _apply_adjoint_dev(self, u):
@@ -635,21 +672,24 @@ class HessianOperator(LinearOperator):
 
 
 class FunctionHessian(HessianOperator):
-    """Hessian-vector product supplied as a callable ``hvp(x, v)`` on CUDA
-    tensors (operators.py:280-297); ``update`` stores the evaluation point."""
+    """Hessian-vector product supplied as a callable ``hvp(x, v)`` (on CUDA
+    tensors, or NumPy-only as the reference takes it: ``UserFn``;
+    operators.py:280-297); ``update`` stores the evaluation point."""
 
     is_constant = False
 
     def __init__(self, dim: int, hvp: Callable, x0=None):
         super().__init__(dim)
-        self._hvp = hvp
-        self._x = torch.zeros(dim, dtype=F64, device="cuda") if x0 is None else to_device(x0)
+        self._hvp = UserFn(hvp)
+        self._x = None if x0 is None else x0  # moved to the device at first use
 
     def update(self, x) -> None:
         self._x = to_device(x).clone()
 
     def _apply_dev(self, v):
-        return to_device(self._hvp(self._x, v))
+        if not isinstance(self._x, torch.Tensor):
+            self._x = torch.zeros_like(v) if self._x is None else to_device(self._x)
+        return self._hvp(self._x, v)
 
 
 class ConstantHessian(HessianOperator):

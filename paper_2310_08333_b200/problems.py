@@ -28,26 +28,62 @@ from .operators import (
     IdentityOperator,
     LinearOperator,
     MatrixFreeOperator,
+    SparseOperator,
     as_operator,
+    device_fn,
     like_input,
     to_device,
 )
-from .prox import Box
+from .prox import Box, box_indicator, box_project, soft_threshold
+
+
+def _loss_eval(kind: str, what: int) -> Callable:
+    """Elementwise evaluation of a built-in loss on the device (nys_loss_eval_f64):
+    NumPy (any shape, scalars) or device arrays in, the same kind out."""
+
+    def fn(w):
+        from .kernels import get_kernels
+
+        shape = np.shape(w) if not isinstance(w, torch.Tensor) else tuple(w.shape)
+        wt = to_device(np.asarray(w, dtype=float).reshape(-1) if not isinstance(w, torch.Tensor)
+                       else w.reshape(-1)).contiguous()
+        out = torch.empty_like(wt)
+        if wt.numel():
+            get_kernels().loss_eval(kind, what, wt, out)
+        if isinstance(w, torch.Tensor):
+            return out.reshape(shape)
+        res = out.cpu().numpy().reshape(shape)
+        return res if res.shape else float(res)
+
+    return fn
 
 
 @dataclass(frozen=True)
 class Loss:
-    """Per-sample convex loss (problems.py:35-50), identified by kind."""
+    """Scalar convex per-sample loss with its derivatives and optional conjugate
+    (problems.py:35-50; the same fields in the same order).  ``value``,
+    ``deriv``, ``deriv2`` and ``conj`` act elementwise; for the built-in kinds
+    they default to the device evaluation of csrc/loss.cuh -- the expressions
+    the fused kernels of ``solve`` use (``conj`` gives +inf outside its domain).
+    ``solve`` itself selects its kernels by ``kind``."""
 
     kind: str
+    value: Optional[Callable] = None
+    deriv: Optional[Callable] = None
+    deriv2: Optional[Callable] = None
+    conj: Optional[Callable] = None
     deriv2_constant: bool = False
-    has_conj: bool = True
+
+    def __post_init__(self):
+        if self.kind in ("square", "logistic", "huber"):
+            for what, name in enumerate(("value", "deriv", "deriv2", "conj")):
+                if getattr(self, name) is None:
+                    object.__setattr__(self, name, _loss_eval(self.kind, what))
 
     @property
-    def conj(self):
-        # the reference exposes the conjugate callable; its presence enables the
-        # duality-gap stopping rule (admm.py:476-478)
-        return True if self.has_conj else None
+    def has_conj(self) -> bool:
+        # the conjugate's presence enables the duality-gap stopping rule (admm.py:476-478)
+        return self.conj is not None
 
 
 def square_loss() -> Loss:
@@ -148,13 +184,33 @@ class GenericProblem:
 
     n: int
     m: int
-    M: LinearOperator
-    c: np.ndarray
+    # the reference's field order (problems.py:137-150).  The oracles of a lowered
+    # ML / QP problem run on the device (NumPy or device arrays in, the same kind
+    # out); the single-step API of admm.py (x_update, z_update, ...) uses them.
+    f: Optional[Callable] = None
+    grad_f: Optional[Callable] = None
     hess: Optional[HessianOperator] = None
+    g: Optional[Callable] = None
+    prox_g: Optional[Callable] = None
+    M: Optional[LinearOperator] = None
+    c: Optional[np.ndarray] = None
     is_quadratic: bool = False
     full_rank: bool = False
+    prox_inexact: bool = False
     qp: Optional[QPProblem] = None
     ml: Optional[MLProblem] = None
+
+    def __post_init__(self):
+        # problems.py:152-158
+        if self.M is None:
+            self.M = IdentityOperator(self.n)
+        self.c = np.zeros(self.m) if self.c is None else np.asarray(self.c, dtype=float)
+        if self.M.input_dim != self.n or self.M.output_dim != self.m:
+            raise DataError("constraint operator dimensions do not match (n, m)")
+        if self.c.shape != (self.m,):
+            raise DataError("offset c must have length m")
+        if self.hess is not None and self.hess.input_dim != self.n:
+            raise DataError("Hessian dimension must equal n")
 
 
 def lasso_problem(A, b, lambda1: float) -> MLProblem:
@@ -188,20 +244,37 @@ def lasso_as_qp(A, b, lambda1: float) -> QPProblem:
     M = sp.bmat([[eye, eye], [eye, -eye]])
     lo = np.concatenate([np.zeros(n), np.full(n, -np.inf)])
     hi = np.concatenate([np.full(n, np.inf), np.zeros(n)])
-    from .operators import SparseOperator
-
     return QPProblem(SparseOperator(P.tocsr()), q, SparseOperator(M.tocsr()), Box(lo, hi))
 
 
 def qp_lower(qp: QPProblem) -> GenericProblem:
     """problems.py:387-421 (full_rank iff M is the identity)."""
-    return GenericProblem(n=qp.n, m=qp.m, M=qp.M, c=np.zeros(qp.m), hess=ConstantHessian(qp.P),
+    P, q, box = qp.P, qp.q, qp.box
+
+    @device_fn
+    def f(x):
+        xt = to_device(x)
+        return 0.5 * float(torch.dot(xt, P._apply_dev(xt))) + float(torch.dot(to_device(q), xt))
+
+    @device_fn
+    def grad(x):
+        xt = to_device(x)
+        return like_input(P._apply_dev(xt) + to_device(q), x)
+
+    return GenericProblem(n=qp.n, m=qp.m, f=f, grad_f=grad, hess=ConstantHessian(qp.P),
+                          g=device_fn(lambda z: box_indicator(z, box)),
+                          prox_g=device_fn(lambda v, rho, tol: box_project(v, box)),
+                          M=qp.M, c=np.zeros(qp.m),
                           is_quadratic=True, full_rank=isinstance(qp.M, IdentityOperator), qp=qp)
 
 
 def ml_lower(p: MLProblem) -> GenericProblem:
     """problems.py:424-450: M = I, c = 0, full rank."""
-    return GenericProblem(n=p.n, m=p.n, M=IdentityOperator(p.n), c=np.zeros(p.n), hess=None,
+    return GenericProblem(n=p.n, m=p.n, f=device_fn(lambda x: ml_smooth_value(p, x)),
+                          grad_f=device_fn(lambda x: ml_gradient(p, x)), hess=MLHessian(p),
+                          g=device_fn(lambda z: p.lambda1 * float(to_device(z).abs().sum())),
+                          prox_g=device_fn(lambda v, rho, tol: soft_threshold(v, p.lambda1 / rho)),
+                          M=IdentityOperator(p.n), c=np.zeros(p.n),
                           is_quadratic=p.loss.deriv2_constant, full_rank=True, ml=p)
 
 
@@ -304,11 +377,22 @@ class MLHessian(HessianOperator):
         self.p = p
         self.diag_shift = p.lambda2
         self.is_constant = p.loss.deriv2_constant
-        self._A = _dense_A(p)
+        # nothing touches the device until the operator is used (ml_lower builds
+        # one for every lowered problem; the engines have their own fused HVP)
+        self._A = None
         self._w = None
-        self.update(np.zeros(p.n) if x is None else x)
+        self._x0 = x
+        self._started = False
+
+    def _ensure(self) -> None:
+        if not self._started:
+            self.update(np.zeros(self.p.n) if self._x0 is None else self._x0)
 
     def update(self, x) -> None:
+        if not self._started:
+            self._started = True
+            self._x0 = None
+            self._A = _dense_A(self.p)
         if self.p.loss.kind == "square":
             self._w = None  # l'' == 1
             return
@@ -318,6 +402,7 @@ class MLHessian(HessianOperator):
 
     @property
     def _weights(self):
+        self._ensure()
         if self._w is None:
             return np.ones(self.p.N)
         return self._w.cpu().numpy()
@@ -326,6 +411,7 @@ class MLHessian(HessianOperator):
         from .kernels import get_kernels
 
         kx = get_kernels()
+        self._ensure()
         y = kx.empty(self.input_dim)
         if self._A is not None:
             kx.hvp(self._A, self._w, v, shift, y, None, True)
@@ -346,6 +432,7 @@ class MLHessian(HessianOperator):
         from .operators import adjoint_columns_dev
 
         kx = get_kernels()
+        self._ensure()
         A = self._A
         if A is None:
             Z = self.p.A.apply_columns_dev(V.contiguous())
@@ -365,6 +452,7 @@ class MLHessian(HessianOperator):
     def smooth_part(self) -> LinearOperator:
         """A' diag(w) A, the sketching target (problems.py:266-273)."""
 
+        @device_fn
         def mv(v):
             return self._hvp(to_device(v), 0.0)
 

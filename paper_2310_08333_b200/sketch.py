@@ -426,4 +426,5 @@ def diagonal_reduce(A: LinearOperator, d):
         kx.vmul(1.0, _s, y, 0.0, y)
         return y
 
+    matvec.accepts_device = True  # operators.device_fn
     return MatrixFreeOperator(A.input_dim, A.input_dim, matvec, matvec), like_input(s_dev, d)

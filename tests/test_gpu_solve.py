@@ -190,7 +190,7 @@ def test_unsupported_problem_raises():
     import paper_2310_08333_b200 as nys
 
     gp = nys.GenericProblem(n=3, m=3, M=nys.IdentityOperator(3), c=np.zeros(3))
-    with pytest.raises(nys.CapabilityError):
+    with pytest.raises(nys.CapabilityError):  # no oracles at all
         nys.solve(gp)
 
 
