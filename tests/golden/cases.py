@@ -321,3 +321,18 @@ def pcg_case(seed=303, n=30):
     b = rng.standard_normal(n)
     x0 = rng.standard_normal(n) * 0.1
     return H, b, x0
+
+
+def steps_inputs(seed=77):
+    """Seeded inputs of the single-step fixtures (shared with tests/test_gpu_steps.py)."""
+    g = np.random.default_rng(seed)
+    n, m, N = 14, 19, 30
+    B = g.standard_normal((n, n))
+    inp = dict(P=B @ B.T + 0.3 * np.eye(n), q=g.standard_normal(n), M=g.standard_normal((m, n)),
+               lo=-np.abs(g.standard_normal(m)), hi=np.abs(g.standard_normal(m)),
+               A=g.standard_normal((N, n)), b=np.sign(g.standard_normal(N)),
+               x=g.standard_normal(n), z_qp=g.standard_normal(m), u_qp=g.standard_normal(m),
+               z_ml=g.standard_normal(n), u_ml=g.standard_normal(n), Mx_new=g.standard_normal(m))
+    inp["hi"][:3] = np.inf
+    inp["lo"][2:5] = -np.inf
+    return inp

@@ -200,6 +200,51 @@ def run_bench_goldens():
     np.savez_compressed(os.path.join(HERE, "bench_runs.npz"), **out)
 
 
+def run_steps():
+    """The reference's single-step API (admm.py:215-415) on a general-M QP and a
+    logistic problem: residuals, x-update (plain and Nystrom-preconditioned),
+    relax / prox / dual steps, the penalty rule and the infeasibility tests."""
+    from nysopt.admm import (SolverState, check_infeasibility, check_termination, compute_residuals,
+                             relaxed_constraint_point, u_update, update_penalty, x_update, z_update)
+    from nysopt import logistic_problem, lower, qp_lower
+
+    inp = cases.steps_inputs()
+    out = {}
+    qp = QPProblem(inp["P"], inp["q"], inp["M"], Box(inp["lo"], inp["hi"]))
+    ml = logistic_problem(inp["A"], inp["b"], 0.2, 0.05)
+    for tag, gp, z, u in (("qp", qp_lower(qp), inp["z_qp"], inp["u_qp"]), ("ml", lower(ml), inp["z_ml"], inp["u_ml"])):
+        st = SolverState(x=inp["x"].copy(), z=z.copy(), u=u.copy(), rho=0.8, x_bar_sum=np.zeros(gp.n),
+                         z_bar_sum=np.zeros(gp.m))
+        st.k = 4
+        gp.hess.update(st.x)
+        for kind in ("l2", "linf"):
+            opts = SolverOptions(norm_kind=kind)
+            res = compute_residuals(gp, st, opts)
+            out[f"{tag}_{kind}_res"] = np.array([res.rp_norm, res.rd_norm, res.primal_scale, res.dual_scale])
+            out[f"{tag}_{kind}_term"] = np.int64(check_termination(res, st, opts))
+            if kind == "l2":
+                out[f"{tag}_rp"], out[f"{tag}_rd"] = res.rp, res.rd
+        opts = SolverOptions()
+        x_new, rep = x_update(gp, st, opts, None, 1e-11, 1e-4)
+        out[f"{tag}_xnew"], out[f"{tag}_cg_iters"] = x_new, np.int64(rep.iterations)
+        Mx_new = gp.M.apply(x_new)
+        w = relaxed_constraint_point(Mx_new, st, gp, opts.alpha)
+        z_new = z_update(gp, st, opts, w)
+        out[f"{tag}_w"], out[f"{tag}_znew"], out[f"{tag}_unew"] = w, z_new, u_update(st, w, z_new, gp)
+        res = compute_residuals(gp, st, opts)
+        ev = update_penalty(st, res, SolverOptions(mu=1.05))
+        out[f"{tag}_pen"] = np.array([np.nan] * 3 if ev is None else [ev.rho_old, ev.rho_new, ev.dual_jump_rel])
+        out[f"{tag}_u_after_pen"] = st.u.copy()
+    gpq = qp_lower(qp)
+    dx, du = inp["x"], inp["u_qp"]
+    chk = check_infeasibility(dx, du, gpq, SolverOptions(eps_inf=10.0), 0.8)
+    out["inf_status"] = np.array(str(chk.status.value if chk.status else "none"))
+    out["inf_near"] = np.int64(chk.near_trigger)
+    np.savez_compressed(os.path.join(HERE, "kernels_steps.npz"), **out)
+    print("steps:", {k: (v.shape if hasattr(v, "shape") and v.shape else v) for k, v in out.items()
+                     if k.endswith(("iters", "pen", "status"))}, flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run config 4 (~10 min)")
@@ -211,6 +256,7 @@ def main():
     if not args.only:
         run_kernels()
         run_bench_goldens()
+        run_steps()
     for name in names:
         run_solve(name)
 

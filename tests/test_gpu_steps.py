@@ -250,3 +250,49 @@ def test_portfolio_three_formulations_agree(nys):
     obj = lambda x: 0.5 * gamma * (x @ (d * x) + np.sum((F.T @ x) ** 2)) - mu @ x  # noqa: E731
     vals = [obj(r_qp.x[:n]), obj(r_op.x), obj(r_gen.z)]
     assert max(vals) - min(vals) <= 1e-3 * max(1.0, abs(min(vals)))
+
+
+def test_steps_match_reference_golden(nys):
+    """Every single-step function on a general-M QP and a logistic problem against the
+    REFERENCE's outputs on the same seeded inputs (tests/golden/kernels_steps.npz,
+    written by make_golden.run_steps from the nysopt package itself)."""
+    import cases
+    from conftest import load_golden
+    from paper_2310_08333_b200.admm import (SolverState, check_infeasibility, check_termination, compute_residuals,
+                                            relaxed_constraint_point, u_update, update_penalty, x_update, z_update)
+
+    gold = load_golden("kernels_steps.npz")
+    inp = cases.steps_inputs()
+    qp = nys.QPProblem(inp["P"], inp["q"], inp["M"], nys.Box(inp["lo"], inp["hi"]))
+    ml = nys.logistic_problem(inp["A"], inp["b"], 0.2, 0.05)
+    for tag, gp, z, u in (("qp", nys.qp_lower(qp), inp["z_qp"], inp["u_qp"]),
+                          ("ml", nys.lower(ml), inp["z_ml"], inp["u_ml"])):
+        st = SolverState(x=inp["x"].copy(), z=z.copy(), u=u.copy(), rho=0.8, x_bar_sum=np.zeros(gp.n),
+                         z_bar_sum=np.zeros(gp.m))
+        st.k = 4
+        gp.hess.update(st.x)
+        for kind in ("l2", "linf"):
+            opts = nys.SolverOptions(norm_kind=kind)
+            res = compute_residuals(gp, st, opts)
+            got = [res.rp_norm, res.rd_norm, res.primal_scale, res.dual_scale]
+            np.testing.assert_allclose(got, gold[f"{tag}_{kind}_res"], rtol=1e-12)
+            assert int(check_termination(res, st, opts)) == int(gold[f"{tag}_{kind}_term"])
+            if kind == "l2":
+                np.testing.assert_allclose(res.rp, gold[f"{tag}_rp"], rtol=1e-12, atol=1e-13)
+                np.testing.assert_allclose(res.rd, gold[f"{tag}_rd"], rtol=1e-12, atol=1e-12)
+        opts = nys.SolverOptions()
+        x_new, rep = x_update(gp, st, opts, None, 1e-11, 1e-4)
+        np.testing.assert_allclose(x_new, gold[f"{tag}_xnew"], rtol=1e-8, atol=1e-10)
+        assert abs(rep.iterations - int(gold[f"{tag}_cg_iters"])) <= 1
+        w = relaxed_constraint_point(gp.M.apply(gold[f"{tag}_xnew"]), st, gp, opts.alpha)
+        np.testing.assert_allclose(w, gold[f"{tag}_w"], rtol=1e-12, atol=1e-13)
+        z_new = z_update(gp, st, opts, w)
+        np.testing.assert_allclose(z_new, gold[f"{tag}_znew"], rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(u_update(st, w, z_new, gp), gold[f"{tag}_unew"], rtol=1e-12, atol=1e-13)
+        ev = update_penalty(st, compute_residuals(gp, st, opts), nys.SolverOptions(mu=1.05))
+        pen = gold[f"{tag}_pen"]
+        assert ev is not None and [ev.rho_old, ev.rho_new] == [pen[0], pen[1]] and abs(ev.dual_jump_rel - pen[2]) < 1e-12
+        np.testing.assert_allclose(st.u, gold[f"{tag}_u_after_pen"], rtol=1e-13)
+    chk = check_infeasibility(inp["x"], inp["u_qp"], nys.qp_lower(qp), nys.SolverOptions(eps_inf=10.0), 0.8)
+    assert (chk.status.value if chk.status else "none") == str(gold["inf_status"])
+    assert int(chk.near_trigger) == int(gold["inf_near"])
