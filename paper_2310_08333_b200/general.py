@@ -168,8 +168,6 @@ class _GenericPart:
         missing = [nm for nm in ("f", "grad_f", "hess", "g", "prox_g") if getattr(gp, nm) is None]
         if missing:
             raise CapabilityError(f"generic problem without {', '.join(missing)}: nothing to solve")
-        if np.any(gp.c != 0.0):
-            raise CapabilityError("generic problems with a nonzero offset c are outside the B200 path")
         self.f, self.grad_f, self.g, self.prox_g = UserFn(gp.f), UserFn(gp.grad_f), UserFn(gp.g), UserFn(gp.prox_g)
         self.hess = gp.hess
 
@@ -197,6 +195,8 @@ class _GeneralEngine:
         else:
             self.const_hess = self.ml.const
             self.diag_shift = self.ml.l2
+        # the constraint offset of M x - z = c: zero for every lowered ML / QP problem
+        self.c = to_device(gp.c, kx.device) if np.any(gp.c != 0.0) else None
         self.stats = _Stats(kx, 128)
         self._grad_x = None  # (x version, grad, f(x)) cache
         self._xver = 0
@@ -398,7 +398,12 @@ class _GeneralEngine:
             """compute_residuals (admm.py:215-224); launches only."""
             g, fout = self.eval_at_x(x)
             s_rp = self.stats.slot(3)
-            kx.vstats(Mx, z, s_rp)  # rp = Mx - z - c, c = 0
+            if self.c is None:
+                kx.vstats(Mx, z, s_rp)  # rp = Mx - z - c, c = 0
+            else:
+                zc = z.clone()
+                kx.axpby(1.0, self.c, 1.0, zc)
+                kx.vstats(Mx, zc, s_rp)
             s_mx = self.stats.slot(3)
             kx.vstats(Mx, None, s_mx)
             s_z = self.stats.slot(3)
@@ -419,10 +424,14 @@ class _GeneralEngine:
                 rd, ds = float(d[2]), float(d[3])
             else:
                 rd, ds = math.sqrt(max(d[0], 0.0)), math.sqrt(max(d[1], 0.0))
-            return Residuals(None, None, rp, rd, max(nmx, nz, 0.0), ds, m)
+            return Residuals(None, None, rp, rd, max(nmx, nz, c_norm[kind]), ds, m)
 
         def offs(t):
             return int(t.data_ptr() - self.stats.dev.data_ptr()) // 8
+
+        c_norm = {"l2": 0.0, "linf": 0.0}  # ||c|| in the primal scale (admm.py:222)
+        if self.c is not None:
+            c_norm = {"l2": float(np.linalg.norm(self.gp.c)), "linf": float(np.max(np.abs(self.gp.c)))}
 
         sl = residuals(x, z, u, Mx, rho)
         h = self.stats.read()
@@ -486,6 +495,8 @@ class _GeneralEngine:
             kx.axpby(-1.0, g_x, 1.0, rhs)
             target = z.clone()
             kx.axpby(-1.0, u, 1.0, target)  # z + c - u
+            if self.c is not None:
+                kx.axpby(1.0, self.c, 1.0, target)
             kx.axpby(rho, target if self.identity_M else self.M_adj(target), 1.0, rhs)
             shift = rho + sigma_eff
             rho_now = rho
@@ -522,14 +533,21 @@ class _GeneralEngine:
             if self.gen:
                 # w = alpha Mx + (1 - alpha) z; z = prox_g(w + u, rho, tol_k); u += w - z with
                 # tol_k = prox_tol0 / k^(2 gamma) (admm.py:278-300)
+                # (with an offset: w = alpha Mx + (1 - alpha)(z + c); z = prox_g(w - c + u); u += w - z - c)
                 w = Mx.clone()
                 kx.axpby(1.0 - opts.alpha, z, opts.alpha, w)
+                if self.c is not None:
+                    kx.axpby(1.0 - opts.alpha, self.c, 1.0, w)
                 v = w.clone()
                 kx.axpby(1.0, u, 1.0, v)
+                if self.c is not None:
+                    kx.axpby(-1.0, self.c, 1.0, v)
                 prox_tol = opts.prox_tol0 / max(k, 1) ** (2.0 * opts.gamma)
                 z = self.gen.prox_g(v, rho, max(prox_tol, 1e-15)).clone()
                 kx.axpby(1.0, w, 1.0, u)
                 kx.axpby(-1.0, z, 1.0, u)
+                if self.c is not None:
+                    kx.axpby(-1.0, self.c, 1.0, u)
             elif self.ml:
                 kx.admm_zu(Mx, z, u, opts.alpha, _lib.PROX_SOFT, self.ml.l1 / rho, None, None, None, None, False)
             else:

@@ -189,9 +189,46 @@ def _qp_dense_M(n=40, m=60, seed=41):
     return dict(P=P, q=rng.standard_normal(n), M=M, lo=-np.ones(m), hi=np.ones(m))
 
 
+def _generic(kind, seed, offset=False):
+    """Problems handed over as callables (problems.py:125-157): "lasso" = a lasso through
+    f / grad f / Hessian-vector product / soft-threshold prox on NumPy arrays, optionally
+    with a nonzero constraint offset c (x - z = c); "portfolio" = the simplex-prox
+    splitting of the stored portfolio data (bench/datagen.py:184-214)."""
+    if kind == "portfolio":
+        import os
+
+        f = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "input_portfolio.npz"))
+        return dict(generic="portfolio", d=f["d"], F=f["F"], mu=f["mu"], gamma=float(f["gamma"]))
+    g = np.random.default_rng(seed)
+    N, n = 80, 40
+    A = g.standard_normal((N, n)) / np.sqrt(N)
+    xs = np.where(g.random(n) < 0.2, g.standard_normal(n), 0.0)
+    b = A @ xs + 0.01 * g.standard_normal(N)
+    lam = 0.1 * float(np.max(np.abs(A.T @ b)))
+    c = 0.05 * g.standard_normal(n) if offset else np.zeros(n)
+    return dict(generic="lasso", A=A, b=b, lam=lam, c=c)
+
+
+def build_generic(spec, ns):
+    if spec["generic"] == "portfolio":
+        import importlib
+
+        bench = importlib.import_module(ns.__name__ + ".bench")
+        return bench.portfolio_generic_problem(spec["d"], spec["F"], spec["mu"], spec["gamma"])
+    A, b, lam, c = spec["A"], spec["b"], spec["lam"], spec["c"]
+    n = A.shape[1]
+    return ns.GenericProblem(
+        n=n, m=n, f=lambda x: 0.5 * float(np.linalg.norm(A @ x - b) ** 2), grad_f=lambda x: A.T @ (A @ x - b),
+        hess=ns.FunctionHessian(n, lambda x, v: A.T @ (A @ v)), g=lambda z: lam * float(np.abs(z).sum()),
+        prox_g=lambda v, rho, tol: np.sign(v) * np.maximum(np.abs(v) - lam / rho, 0.0),
+        M=ns.IdentityOperator(n), c=c, full_rank=True)
+
+
 def build_problem(spec, ns):
     """Problem of a case spec in the namespace ``ns`` (the reference package or
     this repo's: both export the same constructors)."""
+    if "generic" in spec:
+        return build_generic(spec, ns)
     if "lasso_qp" in spec:
         return ns.lasso_as_qp(*spec["lasso_qp"])
     if "P" not in spec:
@@ -231,6 +268,16 @@ GENERAL_CASES = {
     "qp_check_rank": (lambda: _qp_check_rank(), dict(check_rank=True, max_iter=300, rng_seed=2)),
     "qp_assume_rank": (lambda: _qp_check_rank(), dict(assume_full_rank=True, max_iter=300, rng_seed=2)),
     "qp_dense_M": (lambda: _qp_dense_M(), dict(sketch_rank=8, rng_seed=41, max_iter=3000)),
+}
+
+# problems given as callables (the reference's generic front end); pinned to the
+# reference's outputs directly (the CPU oracle covers the ML / QP forms only)
+GENERIC_CASES = {
+    "generic_lasso": (lambda: _generic("lasso", 61), dict(sketch_rank=8, rng_seed=61, max_iter=3000)),
+    "generic_offset": (lambda: _generic("lasso", 62, offset=True),
+                       dict(sketch_rank=8, rng_seed=62, max_iter=3000, rho0=5.0, penalty_warmup=5,
+                            penalty_update_every=5)),
+    "generic_portfolio": (lambda: _generic("portfolio", 0), dict(rng_seed=5, max_iter=3000)),
 }
 
 
@@ -273,7 +320,7 @@ SOLVE_CASES = {
     "cfg5_shard": (lambda: _cfg5_shard(0), dict(sketch_rank=300, rng_seed=4)),
 }
 
-ALL_CASES = {**SOLVE_CASES, **GENERAL_CASES}
+ALL_CASES = {**SOLVE_CASES, **GENERAL_CASES, **GENERIC_CASES}
 
 # tolerances of the configs: eps_abs = eps_rel = eps_dual_gap = 1e-4 (BASELINE.json)
 BASE_OPTIONS = dict(eps_abs=1e-4, eps_rel=1e-4, eps_dual_gap=1e-4)

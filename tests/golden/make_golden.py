@@ -99,7 +99,7 @@ def run_solve(name):
         ref_precond_s=np.float64(res.timings.precond_s),
         ref_linsys_s=np.float64(res.timings.linsys_total_s),
     )
-    if "A" in spec:
+    if "A" in spec and "generic" not in spec:
         p = ref_problem(spec)
         out["ml_objective_z"] = np.float64(ml_objective(p, res.z))
     np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), **out)
@@ -250,7 +250,7 @@ def main():
     ap.add_argument("--big", action="store_true", help="also run config 4 (~10 min)")
     ap.add_argument("--only", nargs="*", default=None)
     args = ap.parse_args()
-    names = args.only if args.only else (list(cases.DEFAULT_SOLVES) + list(cases.GENERAL_CASES)
+    names = args.only if args.only else (list(cases.DEFAULT_SOLVES) + list(cases.GENERAL_CASES) + list(cases.GENERIC_CASES)
                                          + (["cfg4"] if args.big else []))
     make_inputs()
     if not args.only:

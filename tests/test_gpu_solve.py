@@ -160,6 +160,16 @@ def test_solve_general_cases(name):
     assert res.device_stats.get("engine") == "general"
 
 
+@pytest.mark.parametrize("name", list(cases.GENERIC_CASES))
+def test_solve_generic_cases(name):
+    """Problems handed over as callables (problems.py:125-157) -- a lasso through NumPy
+    f / grad f / Hessian-vector product / prox callables, the same with a nonzero constraint
+    offset c and a changing penalty, and the simplex-prox portfolio splitting -- against the
+    reference's own trajectories (iteration and CG counts, penalty events, iterates)."""
+    res, _ = check_case(name)
+    assert res.device_stats.get("engine") == "general"
+
+
 def test_check_rank_probe_matches_assertion():
     """check_rank certifies the PD composite: the same trajectory as the
     explicit full-rank assertion (test_admm.py:605-615)."""
