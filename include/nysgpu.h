@@ -463,7 +463,11 @@ int nys_ml_tail_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const
                     size_t ws_bytes, void* stream);
 /* The same with g_b = A^T b (n): for the square loss with z the cluster stream
  * then accumulates A^T (A x) and A^T (A z) only (two products instead of three)
- * and AT = [A^T(Ax) - g_b, A^T(Ax), A^T(Az) - g_b]; other losses ignore g_b. */
+ * and AT = [A^T(Ax) - g_b, A^T(Ax), A^T(Az) - g_b]; other losses ignore g_b.
+ * With g_b, rows beyond the whole-slice plan (114688 < n <= ~229000, config 5's
+ * n = 200000) have their own one-pass plan (x and the A^T(Az) accumulator in
+ * tensor memory, z visited through its nonzeros: meant for a sparse prox output;
+ * a dense z stays correct but is slower than two passes). */
 int nys_ml_tail_gb_f64(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, const double* z,
                        const double* b, int loss, const double* gb, double* T, double* w, double* AT,
                        double* rowsums, void* ws, size_t ws_bytes, void* stream);
