@@ -28,12 +28,28 @@ from .prox import box_recession_distance, box_support
 from .sketch import NystromPreconditioner
 
 
+def _kx():
+    from .kernels import get_kernels
+
+    return get_kernels()
+
+
 def _norm_dev(v: torch.Tensor, kind: str) -> float:
+    """l2 or linf norm by the fixed-order reduction kernel of the general engine (nys_vstats_f64)."""
     if v.numel() == 0:
         return 0.0
-    if kind == "linf":
-        return float(v.abs().max())
-    return float(torch.linalg.vector_norm(v))
+    kx = _kx()
+    out = kx.zeros(3)
+    kx.vstats(v.contiguous(), None, out)  # [sum v, sum v^2, max |v|]
+    h = out.cpu().numpy()
+    return float(h[2]) if kind == "linf" else math.sqrt(max(float(h[1]), 0.0))
+
+
+def _lin(a: float, x: torch.Tensor, b: float, y: torch.Tensor) -> torch.Tensor:
+    """a x + b y as a fresh vector (nys_axpby_f64)."""
+    out = y.clone()
+    _kx().axpby(a, x.contiguous(), b, out)
+    return out
 
 
 def _np(t: torch.Tensor) -> np.ndarray:
@@ -45,12 +61,12 @@ def compute_residuals(problem: GenericProblem, state: SolverState, options: Solv
     x, z, u = to_device(state.x), to_device(state.z), to_device(state.u)
     c = to_device(problem.c)
     Mx = to_device(state.Mx) if state.Mx is not None else problem.M._apply_dev(x)
-    rp = Mx - z - c
+    rp = _lin(-1.0, c, 1.0, _lin(-1.0, z, 1.0, Mx))
     Mtu = problem.M._apply_adjoint_dev(u)
-    rd = to_device(problem.grad_f(state.x)) + state.rho * Mtu
+    rd = _lin(state.rho, Mtu, 1.0, to_device(problem.grad_f(state.x)))
     kind = options.norm_kind
     primal_scale = max(_norm_dev(Mx, kind), _norm_dev(z, kind), _norm_dev(c, kind))
-    dual_scale = _norm_dev(state.rho * Mtu, kind)
+    dual_scale = _norm_dev(_lin(state.rho, Mtu, 0.0, Mtu), kind)
     return Residuals(_np(rp), _np(rd), _norm_dev(rp, kind), _norm_dev(rd, kind), primal_scale, dual_scale,
                      size=int(rp.numel()))
 
@@ -78,13 +94,14 @@ def x_update(problem: GenericProblem, state: SolverState, options: SolverOptions
     def matvec(v):
         vt = to_device(v)
         if identity_M:
-            return hess._apply_dev(vt) + shift * vt
-        return hess._apply_dev(vt) + rho * M._apply_adjoint_dev(M._apply_dev(vt)) + sigma_eff * vt
+            return _lin(shift, vt, 1.0, hess._apply_dev(vt))
+        y = _lin(rho, M._apply_adjoint_dev(M._apply_dev(vt)), 1.0, hess._apply_dev(vt))
+        return _lin(sigma_eff, vt, 1.0, y)
 
     x = to_device(state.x)
-    rhs = hess._apply_dev(x) + sigma_eff * x - to_device(problem.grad_f(state.x))
-    target = to_device(state.z) + to_device(problem.c) - to_device(state.u)
-    rhs = rhs + (rho * target if identity_M else rho * M._apply_adjoint_dev(target))
+    rhs = _lin(-1.0, to_device(problem.grad_f(state.x)), 1.0, _lin(sigma_eff, x, 1.0, hess._apply_dev(x)))
+    target = _lin(-1.0, to_device(state.u), 1.0, _lin(1.0, to_device(problem.c), 1.0, to_device(state.z)))
+    rhs = _lin(rho, target if identity_M else M._apply_adjoint_dev(target), 1.0, rhs)
     Minv = preconditioner.apply if preconditioner is not None else None
     x_new, rep = pcg(matvec, rhs, x0=x, Minv=Minv, tol_rel=tol, max_iter=10 * problem.n)
     return _np(to_device(x_new)), rep
@@ -92,33 +109,35 @@ def x_update(problem: GenericProblem, state: SolverState, options: SolverOptions
 
 def relaxed_constraint_point(Mx_new, state: SolverState, problem: GenericProblem, alpha: float) -> np.ndarray:
     """alpha Mx + (1 - alpha)(z + c) (admm.py:278-280)."""
-    w = alpha * to_device(Mx_new) + (1.0 - alpha) * (to_device(state.z) + to_device(problem.c))
-    return _np(w)
+    zc = _lin(1.0, to_device(problem.c), 1.0, to_device(state.z))
+    return _np(_lin(alpha, to_device(Mx_new), 1.0 - alpha, zc))
 
 
 def z_update(problem: GenericProblem, state: SolverState, options: SolverOptions, w) -> np.ndarray:
     """Proximal step at the over-relaxed point, tolerance tol0 / k^(2 gamma) (admm.py:283-296)."""
     prox_tol = options.prox_tol0 / max(state.k, 1) ** (2.0 * options.gamma)
-    v = to_device(w) - to_device(problem.c) + to_device(state.u)
+    v = _lin(1.0, to_device(state.u), 1.0, _lin(-1.0, to_device(problem.c), 1.0, to_device(w)))
     vin = v if isinstance(state.u, torch.Tensor) else _np(v)  # the prox sees the caller's array kind
     return _np(to_device(problem.prox_g(vin, state.rho, max(prox_tol, 1e-15))))
 
 
 def u_update(state: SolverState, w, z_new, problem: GenericProblem) -> np.ndarray:
     """u + w - z_new - c (admm.py:299-300)."""
-    return _np(to_device(state.u) + to_device(w) - to_device(z_new) - to_device(problem.c))
+    uw = _lin(1.0, to_device(w), 1.0, to_device(state.u))
+    return _np(_lin(-1.0, to_device(problem.c), 1.0, _lin(-1.0, to_device(z_new), 1.0, uw)))
 
 
 def _change_penalty(state: SolverState, rho_new: float, preconditioner: Optional[NystromPreconditioner] = None,
                     nu_of_rho: Optional[Callable[[float], float]] = None) -> PenaltyEvent:
     """New penalty with the scaled dual rescaled so that rho u is unchanged (admm.py:303-320)."""
     rho_old = state.rho
-    u = to_device(state.u)
-    y_old = rho_old * u
-    u_new = u * (rho_old / rho_new)
-    y_new = rho_new * u_new
-    denom = max(float(torch.linalg.vector_norm(y_old)), 1e-30)
-    jump = float(torch.linalg.vector_norm(y_new - y_old)) / denom
+    kx = _kx()
+    u_new = to_device(state.u).clone()
+    out = kx.zeros(2)
+    kx.scale_dual(u_new, rho_old, rho_new, out)  # u *= rho_old / rho_new; [||y_old||^2, ||y_new - y_old||^2]
+    o = out.cpu().numpy()
+    denom = max(math.sqrt(max(float(o[0]), 0.0)), 1e-30)
+    jump = math.sqrt(max(float(o[1]), 0.0)) / denom
     if isinstance(state.u, np.ndarray):
         state.u[...] = _np(u_new)  # in place, as the reference's `state.u *= ...`
     else:
@@ -174,20 +193,22 @@ def check_infeasibility(delta_x, delta_u, problem: GenericProblem, options: Solv
     cert_p = cert_d = None
     du, dx = to_device(delta_u), to_device(delta_x)
 
-    du_norm = float(torch.linalg.vector_norm(du))
+    du_norm = _norm_dev(du, "l2")
     if du_norm > 1e-14:
-        t_map = float(torch.linalg.vector_norm(qp.M._apply_adjoint_dev(du)))
+        t_map = _norm_dev(qp.M._apply_adjoint_dev(du), "l2")
         t_support = box_support(du, qp.box)
         primal = t_map < eps * du_norm and t_support < eps * du_norm
         near_primal = t_map < 10 * eps * du_norm and t_support < 10 * eps * du_norm
         if primal:
-            cert_p = _np(rho * du)
+            cert_p = rho * _np(du)
 
-    dx_norm = float(torch.linalg.vector_norm(dx))
+    dx_norm = _norm_dev(dx, "l2")
     if dx_norm > 1e-14:
-        s_obj = float(torch.linalg.vector_norm(qp.P._apply_dev(dx)))
+        s_obj = _norm_dev(qp.P._apply_dev(dx), "l2")
         s_cone = box_recession_distance(qp.M._apply_dev(dx), qp.box)
-        s_lin = float(torch.dot(to_device(qp.q), dx))
+        lin = _kx().zeros(1)
+        _kx().dot(to_device(qp.q).contiguous(), dx.contiguous(), lin)
+        s_lin = float(lin)
         dual = s_obj < eps * dx_norm and s_cone < eps * dx_norm and s_lin < eps * dx_norm
         near_dual = s_obj < 10 * eps * dx_norm and s_cone < 10 * eps * dx_norm and s_lin < 10 * eps * dx_norm
         if dual:

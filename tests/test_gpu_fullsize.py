@@ -95,3 +95,24 @@ def test_one_pass_tail_full_size_matches_two_passes(kx, rows, n):
     np.testing.assert_allclose(rs.cpu().numpy()[:5], rs2.cpu().numpy()[:5], rtol=1e-11, atol=1e-9)
     del A
     torch.cuda.empty_cache()
+
+
+def test_one_pass_logistic_tail_full_size_matches_two_passes(kx):
+    """The logistic epilogue of the cluster stream (config 2's loss at config 4's size)."""
+    rows, n = 20000, 100000
+    A, g = _matrix(kx, rows, n, 11)
+    x = kx.empty(n).normal_(generator=g)
+    z = x * (torch.rand(n, device=x.device, generator=g) < 0.3)
+    b = kx.zeros(rows)
+    T, w, AT, rs = kx.empty(3, rows), kx.empty(rows), kx.empty(3, n), kx.zeros(8)
+    kx.ml_tail("logistic", A, x, z, b, T, w, AT, rs)
+    XZ = torch.stack([x, z]).contiguous()
+    AXZ, T2, w2, AT2, rs2 = kx.empty(2, rows), kx.empty(3, rows), kx.empty(rows), kx.empty(3, n), kx.zeros(8)
+    kx.gemv(A, XZ, AXZ)
+    kx.ml_rowwise("logistic", AXZ[0], AXZ[1], b, T2[0], w2, T2[1], T2[2], rs2)
+    kx.gemvT(A, T2, AT2)
+    for j in range(3):
+        assert _rel(T[j], T2[j]) < 1e-12
+        assert _rel(AT[j], AT2[j]) < 1e-11
+    assert _rel(w, w2) < 1e-12
+    np.testing.assert_allclose(rs.cpu().numpy()[:5], rs2.cpu().numpy()[:5], rtol=1e-11, atol=1e-9)
