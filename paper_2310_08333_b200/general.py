@@ -85,9 +85,11 @@ class _MLPart:
             self.fwd, self.bwd = p.A.device_csr(kx.device)
         self.N, self.n = p.N, p.n
         self.b = to_device(p.b, kx.device)
-        self.loss = p.loss.kind
-        if self.loss not in _lib.LOSS:
-            raise DataError(f"unknown loss kind {self.loss!r}")
+        # a built-in kind (the fused kernels) or the user's Loss object (its callables on the host)
+        self.loss = p.loss.kind if p.loss.kind in _lib.LOSS else p.loss
+        if not isinstance(self.loss, str) and not all(callable(getattr(p.loss, nm, None))
+                                                      for nm in ("value", "deriv", "deriv2")):
+            raise DataError(f"loss {p.loss.kind!r} is neither built in nor given with value / deriv / deriv2")
         self.l1, self.l2 = float(p.lambda1), float(p.lambda2)
         self.const = p.loss.deriv2_constant
         self.w = None  # l''(Ax - b) at the Hessian point; None == 1 (square loss)

@@ -12,6 +12,7 @@ import ctypes as C
 import os
 from typing import Optional
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -253,15 +254,60 @@ class Kernels:
                                         _p(hi), out.data_ptr(), self.red.data_ptr(), self.sp), "admm_norms")
 
     def ml_rowwise(self, loss, Ax, Az, b, tg, w, thx, tnu, out) -> None:
+        """Row-wise loss epilogue; ``loss`` is a built-in kind (the fused kernel) or a
+        user-defined ``Loss`` (its NumPy callables, see ``_custom_rowwise``)."""
+        if not isinstance(loss, str):
+            return self._custom_rowwise(loss, Ax, Az, b, tg, w, thx, tnu, out)
         self.launches += 1
         check(self.L.nys_ml_rowwise_f64(b.numel(), _lib.LOSS[loss], _p(Ax), _p(Az), b.data_ptr(), _p(tg),
                                         _p(w), _p(thx), _p(tnu), out.data_ptr(), self.red.data_ptr(),
                                         self.sp), "ml_rowwise")
 
     def ml_conj_scaled(self, loss, nu, c, b, out) -> None:
+        if not isinstance(loss, str):
+            return self._custom_conj_scaled(loss, nu, c, b, out)
         self.launches += 1
         check(self.L.nys_ml_conj_scaled_f64(b.numel(), _lib.LOSS[loss], nu.data_ptr(), float(c), b.data_ptr(),
                                             out.data_ptr(), self.red.data_ptr(), self.sp), "conj_scaled")
+
+    # user-defined losses (problems.py:35-50, "custom losses" of the reference's ML front
+    # end): value / deriv / deriv2 / conj are the user's NumPy callables, so they -- and
+    # only they -- run on the host, on copies of the N-vectors; same outputs as the kernels
+    def _custom_rowwise(self, loss, Ax, Az, b, tg, w, thx, tnu, out) -> None:
+        f64 = lambda a: np.ascontiguousarray(np.asarray(a, dtype=np.float64))  # noqa: E731
+        put = lambda dst, a: dst.copy_(torch.from_numpy(f64(a)).to(dst.device))  # noqa: E731
+        bh = b.cpu().numpy()
+        s = np.zeros(5)
+        if Ax is not None:
+            ax = Ax.cpu().numpy()
+            r1 = ax - bh
+            s[0] = float(np.sum(loss.value(r1)))
+            if tg is not None:
+                put(tg, loss.deriv(r1))
+            wi = f64(loss.deriv2(r1))
+            if w is not None:
+                put(w, wi)
+            if thx is not None:
+                put(thx, wi * ax)
+        if Az is not None:
+            r2 = Az.cpu().numpy() - bh
+            s[1] = float(np.sum(loss.value(r2)))
+            nu = f64(loss.deriv(r2))
+            if tnu is not None:
+                put(tnu, nu)
+            if loss.conj is not None:
+                cv = f64(loss.conj(nu))
+                inf = np.isinf(cv)
+                s[2], s[3] = float(cv[~inf].sum()), float(inf.sum())
+            s[4] = float(bh @ nu)
+        out[:5].copy_(torch.from_numpy(s).to(out.device))
+
+    def _custom_conj_scaled(self, loss, nu, c, b, out) -> None:
+        y = nu.cpu().numpy() * float(c)
+        cv = np.asarray(loss.conj(y), dtype=np.float64)
+        inf = np.isinf(cv)
+        s = np.array([float(cv[~inf].sum()), float(inf.sum()), float(b.cpu().numpy() @ y)])
+        out[:3].copy_(torch.from_numpy(s).to(out.device))
 
     # ------------------------------------------------------ K13/K14 ----
     def window_norms(self, ring, cur, others, out) -> None:

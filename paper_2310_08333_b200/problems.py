@@ -101,6 +101,11 @@ def huber_loss() -> Loss:
     return Loss("huber")
 
 
+def _loss_arg(loss: Loss):
+    """What the row-wise kernels take: the kind of a built-in loss, else the Loss itself."""
+    return loss.kind if loss.kind in ("square", "logistic", "huber") else loss
+
+
 def builtin_loss(kind: str) -> Loss:
     factories = {"square": square_loss, "logistic": logistic_loss, "huber": huber_loss}
     if kind not in factories:
@@ -342,7 +347,7 @@ class _MLEval:
         AX = _a_rows(self.p, X)
         tg, w, thx, tnu = (kx.empty(self.N) for _ in range(4))
         out = kx.zeros(8)
-        kx.ml_rowwise(self.p.loss.kind, AX[0], AX[1] if z is not None else None, self.b, tg, w, thx,
+        kx.ml_rowwise(_loss_arg(self.p.loss), AX[0], AX[1] if z is not None else None, self.b, tg, w, thx,
                       tnu if z is not None else None, out)
         return AX, tg, w, thx, tnu, out
 
@@ -501,7 +506,7 @@ def ml_dual_value(p: MLProblem, nu) -> float:
     nut = to_device(nu)
     b = to_device(p.b)
     out = kx.zeros(4)
-    kx.ml_conj_scaled(p.loss.kind, nut, 1.0, b, out)
+    kx.ml_conj_scaled(_loss_arg(p.loss), nut, 1.0, b, out)
     o = out.cpu().numpy()
     if o[1] > 0:
         return -np.inf

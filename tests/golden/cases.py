@@ -209,6 +209,19 @@ def _generic(kind, seed, offset=False):
     return dict(generic="lasso", A=A, b=b, lam=lam, c=c)
 
 
+def pseudo_huber(ns):
+    """A user-defined loss (problems.py:35-50): l(w) = sqrt(1 + w^2) - 1 with its derivatives and
+    its conjugate 1 - sqrt(1 - y^2) on |y| <= 1 (+inf outside)."""
+    def conj(y):
+        y = np.asarray(y, dtype=float)
+        inside = np.abs(y) <= 1.0
+        return np.where(inside, 1.0 - np.sqrt(np.clip(1.0 - y * y, 0.0, None)), np.inf)
+
+    return ns.Loss(kind="pseudo_huber", value=lambda w: np.sqrt(1.0 + np.asarray(w, dtype=float) ** 2) - 1.0,
+                   deriv=lambda w: np.asarray(w, dtype=float) / np.sqrt(1.0 + np.asarray(w, dtype=float) ** 2),
+                   deriv2=lambda w: (1.0 + np.asarray(w, dtype=float) ** 2) ** -1.5, conj=conj)
+
+
 def build_generic(spec, ns):
     if spec["generic"] == "portfolio":
         import importlib
@@ -229,6 +242,8 @@ def build_problem(spec, ns):
     this repo's: both export the same constructors)."""
     if "generic" in spec:
         return build_generic(spec, ns)
+    if spec.get("loss") == "pseudo_huber":
+        return ns.MLProblem(pseudo_huber(ns), spec["A"], spec["b"], spec["lambda1"], spec["lambda2"])
     if "lasso_qp" in spec:
         return ns.lasso_as_qp(*spec["lasso_qp"])
     if "P" not in spec:
@@ -278,6 +293,9 @@ GENERIC_CASES = {
                        dict(sketch_rank=8, rng_seed=62, max_iter=3000, rho0=5.0, penalty_warmup=5,
                             penalty_update_every=5)),
     "generic_portfolio": (lambda: _generic("portfolio", 0), dict(rng_seed=5, max_iter=3000)),
+    # a user-defined loss through the ML front end (gap stop via its conjugate; resketches every 20)
+    "custom_loss": (lambda: {**_ml_small("square", 150, 60, 71, lam2=1e-3, lam_frac=0.1), "loss": "pseudo_huber"},
+                    dict(sketch_rank=8, rng_seed=71, max_iter=3000, eps_dual_gap=1e-10)),
 }
 
 

@@ -296,3 +296,25 @@ def test_steps_match_reference_golden(nys):
     chk = check_infeasibility(inp["x"], inp["u_qp"], nys.qp_lower(qp), nys.SolverOptions(eps_inf=10.0), 0.8)
     assert (chk.status.value if chk.status else "none") == str(gold["inf_status"])
     assert int(chk.near_trigger) == int(gold["inf_near"])
+
+
+def test_custom_loss_oracles(nys, rng):
+    """A user-defined Loss (problems.py:35-50) through the ML oracles: objective, gradient,
+    Hessian-vector product and dual value against NumPy."""
+    import cases
+
+    loss = cases.pseudo_huber(nys)
+    A, b = rng.standard_normal((40, 15)), rng.standard_normal(40)
+    p = nys.MLProblem(loss, A, b, 0.2, 0.05)
+    x, v = rng.standard_normal(15), rng.standard_normal(15)
+    r = A @ x - b
+    assert nys.ml_smooth_value(p, x) == pytest.approx(np.sum(np.sqrt(1 + r * r) - 1) + 0.025 * x @ x, rel=1e-12)
+    assert nys.ml_objective(p, x) == pytest.approx(nys.ml_smooth_value(p, x) + 0.2 * np.abs(x).sum(), rel=1e-12)
+    np.testing.assert_allclose(nys.ml_gradient(p, x), A.T @ (r / np.sqrt(1 + r * r)) + 0.05 * x, rtol=1e-12)
+    H = nys.ml_hessian_operator(p, x)
+    np.testing.assert_allclose(H.apply(v), A.T @ ((1 + r * r) ** -1.5 * (A @ v)) + 0.05 * v, rtol=1e-11)
+    nu = nys.ml_dual_point(p, x)
+    at = A.T @ nu
+    want = -np.sum(1 - np.sqrt(1 - nu * nu)) - b @ nu - np.sum(np.maximum(np.abs(at) - 0.2, 0) ** 2) / (2 * 0.05)
+    assert nys.ml_dual_value(p, nu) == pytest.approx(want, rel=1e-11)
+    assert nys.ml_dual_gap(p, x) >= -1e-12
