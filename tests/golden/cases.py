@@ -401,3 +401,48 @@ def steps_inputs(seed=77):
     inp["hi"][:3] = np.inf
     inp["lo"][2:5] = -np.inf
     return inp
+
+
+# ---------------------------------------------------------------------------
+# Randomised small problems (differential test against the reference): shapes
+# from 1 x 1 up, odd sizes, N < n and N > n, every front end and a spread of
+# options; FUZZ_COUNT specs, each a pure function of its index.
+FUZZ_COUNT = 36
+
+
+def fuzz_case(i):
+    g = np.random.default_rng(9000 + i)
+    kind = ["lasso", "enet", "logistic", "boxqp", "qp_M"][i % 5]
+    N, n = int(g.integers(1, 61)), int(g.integers(1, 41))
+    opts = dict(alpha=float(g.choice([1.0, 1.5, 1.8])), rho0=float(g.choice([0.1, 1.0, 10.0])),
+                norm_kind=str(g.choice(["l2", "linf"])), use_preconditioner=bool(g.random() < 0.8),
+                sketch_rank=int(g.choice([1, 3, 8])), penalty_update_every=int(g.choice([0, 5, 25])),
+                penalty_warmup=int(g.choice([5, 50])), rng_seed=int(g.integers(0, 1000)), max_iter=400,
+                eps_abs=1e-5, eps_rel=1e-5, eps_dual_gap=1e-5)
+    if kind in ("lasso", "enet", "logistic"):
+        A = g.standard_normal((N, n)) / np.sqrt(max(N, 1))
+        if kind == "logistic":
+            A = -np.sign(g.standard_normal(N))[:, None] * A
+            b = np.zeros(N)
+            lam1 = 0.1 * float(np.max(np.abs(A.T @ np.ones(N)))) / 2.0
+        else:
+            b = g.standard_normal(N)
+            lam1 = 0.1 * float(np.max(np.abs(A.T @ b)))
+        lam2 = 0.0 if kind == "lasso" else float(g.choice([1e-3, 0.1]))
+        if g.random() < 0.3:
+            opts["use_dual_gap"] = False
+        spec = dict(loss="logistic" if kind == "logistic" else "square", A=A, b=b, lambda1=lam1, lambda2=lam2)
+    else:
+        B = g.standard_normal((n, max(1, n // 2)))
+        P = B @ B.T + float(g.choice([0.0, 0.1])) * np.eye(n)
+        q = g.standard_normal(n)
+        if kind == "boxqp":
+            spec = dict(P=P, q=q, lo=-np.abs(g.standard_normal(n)), hi=np.abs(g.standard_normal(n)))
+        else:
+            m = int(g.integers(1, 31))
+            M = g.standard_normal((m, n))
+            lo, hi = -np.abs(g.standard_normal(m)) - 0.1, np.abs(g.standard_normal(m)) + 0.1
+            lo[g.random(m) < 0.2] = -np.inf
+            hi[g.random(m) < 0.2] = np.inf
+            spec = dict(P=P, q=q, M=M, lo=lo, hi=hi)
+    return spec, opts

@@ -245,6 +245,21 @@ def run_steps():
                      if k.endswith(("iters", "pen", "status"))}, flush=True)
 
 
+def run_fuzz():
+    """The reference on the randomised small problems of cases.fuzz_case."""
+    out = {}
+    for i in range(cases.FUZZ_COUNT):
+        spec, o = cases.fuzz_case(i)
+        res = nysopt.solve(ref_problem(spec), SolverOptions(**o))
+        out[f"c{i}_x"], out[f"c{i}_z"] = res.x, res.z
+        out[f"c{i}_meta"] = np.array([res.iterations, res.objective, res.rp_norm, res.rd_norm,
+                                      sum(h.cg_iters for h in res.history), len(res.penalty_events)])
+        out[f"c{i}_status"] = np.array(res.status.value)
+        print(f"fuzz {i}: {res.status.value} iters={res.iterations} obj={res.objective:.8e} "
+              f"events={len(res.penalty_events)}", flush=True)
+    np.savez_compressed(os.path.join(HERE, "solve_fuzz.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run config 4 (~10 min)")
@@ -257,6 +272,7 @@ def main():
         run_kernels()
         run_bench_goldens()
         run_steps()
+        run_fuzz()
     for name in names:
         run_solve(name)
 
