@@ -407,13 +407,22 @@ def steps_inputs(seed=77):
 # Randomised small problems (differential test against the reference): shapes
 # from 1 x 1 up, odd sizes, N < n and N > n, every front end and a spread of
 # options; FUZZ_COUNT specs, each a pure function of its index.
-FUZZ_COUNT = 36
+FUZZ_COUNT = 48
+
+
+FUZZ_MEDIUM = 12  # the last FUZZ_MEDIUM cases: dense ML / box-QP shapes in the hundreds to thousands
+# (persistent and batched PCG plans, even and odd widths, rows below and above the SM count)
 
 
 def fuzz_case(i):
     g = np.random.default_rng(9000 + i)
     kind = ["lasso", "enet", "logistic", "boxqp", "qp_M"][i % 5]
     N, n = int(g.integers(1, 61)), int(g.integers(1, 41))
+    if i >= FUZZ_COUNT - FUZZ_MEDIUM:
+        kind = ["lasso", "enet", "logistic", "boxqp"][i % 4]
+        N, n = int(g.integers(60, 1500)), int(g.integers(60, 2500))
+        if kind == "boxqp":
+            n = int(g.integers(150, 900))
     opts = dict(alpha=float(g.choice([1.0, 1.5, 1.8])), rho0=float(g.choice([0.1, 1.0, 10.0])),
                 norm_kind=str(g.choice(["l2", "linf"])), use_preconditioner=bool(g.random() < 0.8),
                 sketch_rank=int(g.choice([1, 3, 8])), penalty_update_every=int(g.choice([0, 5, 25])),
