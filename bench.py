@@ -389,6 +389,12 @@ def _cfg5_desc():
 def kernel_name(kx, d, n, rows_loc, world):
     """The kernel that runs the x-update's Hessian application for this shape."""
     persistent = (os.environ.get("NYS_CG_PERSIST", "1") != "0" and n <= 13312 and (d.kind == "boxqp" or world == 1))
+    try:
+        import paper_2310_08333_b200.dist as _dist
+
+        persistent = persistent and not (_dist.FORCE_COLLECTIVES and d.kind != "boxqp")
+    except ImportError:
+        pass
     if persistent:
         return "cg_persist_kernel", "one Hessian application of the persistent PCG, incl. its CG vector phases"
     plan = kx.hvp_plan_name(rows_loc, n) if hasattr(kx, "hvp_plan_name") else "hvp"
@@ -412,6 +418,15 @@ def run_ours(args):
                                              if os.environ.get("NYS_DIST_BACKEND", "nccl") == "nccl" else None)
     else:
         torch.cuda.set_device(0)
+        if args.collectives:
+            # the row-sharded engine and its NCCL exchange steps on one rank (what a one-GPU box
+            # allows): measures the sharded schedule's own cost, no NVLink transfer in it
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29591")
+            torch.distributed.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+            import paper_2310_08333_b200.dist as _dist
+
+            _dist.FORCE_COLLECTIVES = True
     import paper_2310_08333_b200 as nys
     from paper_2310_08333_b200.kernels import get_kernels
 
@@ -592,8 +607,11 @@ def run_ours(args):
             "roofline": roof, "hvp_alone": hvp_alone, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if getattr(args, "collectives", False) and world == 1:
+            line["config"]["parallelism"] = ("row-sharded engine on one rank, exchange steps over NCCL "
+                                             "(world-size-1 group; --collectives)")
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or (torch.distributed.is_available() and torch.distributed.is_initialized()):
         torch.distributed.destroy_process_group()
 
 
@@ -628,6 +646,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--collectives", action="store_true",
+                    help="N = 1 only: run the row-sharded engine with its NCCL exchange steps on a world-size-1 group")
     args = ap.parse_args()
     relaunch(args)
     if args.impl == "reference":

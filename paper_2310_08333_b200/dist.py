@@ -22,14 +22,17 @@ class Shard:
     row_start: int = 0
     row_stop: int = 0
     rows_global: int = 0
+    # run the exchange steps even on one rank (a world-size-1 process group: the
+    # NCCL path of the tests on a one-GPU box)
+    collectives: bool = False
 
     @property
     def sharded(self) -> bool:
-        return self.world > 1
+        return self.world > 1 or self.collectives
 
     def allreduce(self, t: torch.Tensor) -> torch.Tensor:
         """Sum ``t`` in place over all ranks (no-op on one rank)."""
-        if self.world > 1:
+        if self.sharded:
             torch.distributed.all_reduce(t)
         return t
 
@@ -42,6 +45,11 @@ def row_range(N: int, rank: int, world: int) -> tuple[int, int]:
     return start, stop
 
 
+# harness hook (bench.py --collectives, tests): a world-size-1 process group still runs the
+# exchange steps, so the NCCL path can be exercised on a one-GPU box
+FORCE_COLLECTIVES = False
+
+
 def current_shard(N: int) -> Shard:
     """Shard of an N-row matrix for this process (whole matrix without a
     process group)."""
@@ -51,4 +59,5 @@ def current_shard(N: int) -> Shard:
     else:
         rank, world = 0, 1
     a, b = row_range(N, rank, world)
-    return Shard(rank, world, a, b, N)
+    return Shard(rank, world, a, b, N, collectives=bool(FORCE_COLLECTIVES and world == 1
+                                                       and torch.distributed.is_initialized()))

@@ -116,3 +116,46 @@ def test_gpu_row_sharded_solve_matches_single(tmp_path, name, pipelined):
         assert abs(int(r0["it"]) - int(gold["iterations"])) <= 2
         assert abs(float(r0["obj"]) - float(gold["objective"])) <= 1e-6 * abs(float(gold["objective"]))
         assert np.linalg.norm(r0["x"] - gold["x"]) <= 1e-5 * max(np.linalg.norm(gold["x"]), 1e-30)
+
+
+def _nccl_worker(rank, port, name, out_path, pipelined):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ["NYS_SHARD_FAST"] = "1" if pipelined else "0"
+    torch.cuda.set_device(0)
+    torch.distributed.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sys.path.insert(0, ROOT)
+        from paper_2310_08333_b200.dist import Shard
+
+        spec, opts = _problem(name)
+        N = spec["A"].shape[0]
+        shard = Shard(0, 1, 0, N, N, collectives=True)
+        assert shard.sharded
+        res = _solve(spec, opts, shard)
+        np.savez(out_path + ".npz", x=res.x, z=res.z, it=res.iterations, obj=res.objective,
+                 pipelined=bool(res.device_stats["pipelined"]))
+    finally:
+        torch.distributed.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,pipelined", [("lasso_small", True), ("logistic_small", True), ("lasso_wide", True),
+                                           ("logistic_small", False)])
+def test_gpu_sharded_path_over_nccl_one_rank(tmp_path, name, pipelined):
+    """The row-sharded engine with its exchange steps on NCCL (a world-size-1
+    group is all a one-GPU box allows): every collective of the sharded path --
+    the HVP partial sum issued from the C driver's reduce hook inside the CG
+    batches, the packed per-iteration sum, the sketch sum -- runs as a real
+    ``ncclAllReduce`` ordered against the solve stream, and the solve must match
+    the reference golden.  What it cannot show is cross-rank ordering (the
+    2-rank gloo tests above cover the rank logic)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    out = str(tmp_path / "r")
+    mp.spawn(_nccl_worker, args=(_free_port(), name, out, pipelined), nprocs=1, join=True)
+    r = np.load(out + ".npz")
+    assert bool(r["pipelined"]) == pipelined
+    gold = np.load(os.path.join(HERE, "golden", f"solve_{name}.npz"))
+    assert abs(int(r["it"]) - int(gold["iterations"])) <= 2
+    assert abs(float(r["obj"]) - float(gold["objective"])) <= 1e-6 * abs(float(gold["objective"]))
+    assert np.linalg.norm(r["x"] - gold["x"]) <= 1e-5 * max(np.linalg.norm(gold["x"]), 1e-30)
+    assert np.linalg.norm(r["z"] - gold["z"]) <= 1e-5 * max(np.linalg.norm(gold["z"]), 1e-30)
