@@ -438,6 +438,23 @@ def run_ours(args):
         # 160 GB: generated in HBM per rank (each rank holds only its row blocks)
         d, opts, A_dev = build_cfg5(world, rank)
         args.no_e2e = True
+    elif cfg == 4 and args.collectives and args.as_rank_of > 1:
+        # per-rank cost of an N-rank run, measured on one GPU: this process holds the rows of rank 0
+        # of N and solves the statistically equivalent stand-in (sqrt(N) A_loc, sqrt(N) b_loc: the
+        # rows are i.i.d., so A'^T A' ~ A^T A and A'^T b' ~ A^T b, with the global lambda) through
+        # the sharded engine and NCCL.  Same kernels, shapes and exchange calls as that rank would
+        # run; not the global problem, so iterations / CG counts are reported, not asserted.
+        import math
+
+        import numpy as np
+
+        d, opts, A_dev = build_cfg4_device(args.as_rank_of, 0, False)
+        r0, r1 = d.row0, d.row0 + A_dev.shape[0]
+        A_dev.mul_(math.sqrt(args.as_rank_of))
+        d.b = np.ascontiguousarray(d.b[r0:r1]) * math.sqrt(args.as_rank_of)
+        d.N, d.row0 = A_dev.shape[0], 0
+        args.no_e2e = True
+        want_cpu = False
     elif cfg == 4:
         need_host = (not args.no_e2e) or want_cpu
         d, opts, A_dev = build_cfg4_device(world, rank if world > 1 else 0, need_host and world == 1)
@@ -610,6 +627,11 @@ def run_ours(args):
         if getattr(args, "collectives", False) and world == 1:
             line["config"]["parallelism"] = ("row-sharded engine on one rank, exchange steps over NCCL "
                                              "(world-size-1 group; --collectives)")
+            if args.as_rank_of > 1:
+                line["config"]["parallelism"] += (f"; rows of ONE rank of {args.as_rank_of} "
+                                                  "(scaled stand-in problem: a per-rank cost projection, "
+                                                  "not the global solve)")
+                line["result"]["cg_iterations"] = int(sum(h.cg_iters for h in res.history))
         print(json.dumps(line), flush=True)
     if world > 1 or (torch.distributed.is_available() and torch.distributed.is_initialized()):
         torch.distributed.destroy_process_group()
@@ -646,6 +668,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--as-rank-of", type=int, default=1,
+                    help="with --collectives, config 4: hold the rows of one rank of N and solve the "
+                         "statistically equivalent stand-in (per-rank cost projection)")
     ap.add_argument("--collectives", action="store_true",
                     help="N = 1 only: run the row-sharded engine with its NCCL exchange steps on a world-size-1 group")
     args = ap.parse_args()
