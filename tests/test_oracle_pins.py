@@ -160,3 +160,21 @@ def test_oracle_sparse_apply_matches_reference():
     A = cases._sparse_ml("square", 300, 200, 51)["A"]
     np.testing.assert_allclose(A @ gold["v"], gold["Av"], rtol=1e-14, atol=1e-14)
     np.testing.assert_allclose(A.T @ gold["t"], gold["Atv"], rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("i", range(cases.FUZZ_COUNT - cases.FUZZ_MEDIUM))
+def test_oracle_matches_reference_on_randomised_problems(i):
+    """The oracle against the reference's outputs on the 36 small randomised problems of the
+    differential test (cases.fuzz_case; solve_fuzz.npz made by make_golden.py): every front end
+    incl. a general M, random options; same status, iteration count, total CG count and number
+    of penalty events exactly, iterates to 1e-9."""
+    gold = load_golden("solve_fuzz.npz")
+    spec, o = cases.fuzz_case(i)
+    res = port.solve(oracle_problem(spec), port.Options(**o))
+    meta = gold[f"c{i}_meta"]
+    assert res.status == str(gold[f"c{i}_status"])
+    assert res.iterations == int(meta[0])
+    assert int(sum(res.cg_iters)) == int(meta[4])
+    assert len(res.penalty_events) == int(meta[5])
+    np.testing.assert_allclose(res.x, gold[f"c{i}_x"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(res.z, gold[f"c{i}_z"], rtol=1e-9, atol=1e-12)
